@@ -1,0 +1,515 @@
+#!/usr/bin/env python
+"""bench.py -- Stream VByte on B200: the BASELINE.json metric on its configs.
+
+Default workload (N=1): configs[1] = "cfg2", delta encode + delta decode of one
+sorted 64M-uint32 array (geometric gaps, mean 8), prev = 0.  A step is one
+round trip (encode kernel + decode kernel) over the whole array with inputs
+resident in HBM.  Other workloads: --workload cfg3 (2^28 plain, mixed widths),
+cfg4 (1M posting lists, delta, batch kernels), cfg5 (2^31 ints in 64K-int
+prev-seeded chunks, delta, batch kernels).
+
+JSON line keys follow the driver contract; value = integers round-tripped per
+second over all ranks (Gint/s = billions of uint32 encoded AND decoded per s),
+each kernel timed with CUDA events on its launch stream, L2 flushed (256 MiB
+write) before every timed kernel.  `--impl reference` times the CPU reference
+(the oracle port, all host threads) on the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "billions of uint32/sec decoded (plain & delta) and encoded; % of HBM roofline"
+
+
+def _peaks():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+# ---------------------------------------------------------------------------
+# clocks sampling during the timed region
+# ---------------------------------------------------------------------------
+class ClockSampler:
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.gpu = gpu_index
+        self.proc = None
+        self.lines: list[str] = []
+        self._t = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.gpu}", f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self._t = threading.Thread(target=self._read, daemon=True)
+            self._t.start()
+        except FileNotFoundError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+            if self._t:
+                self._t.join(timeout=2)
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                mx = float(f[2])
+            except ValueError:
+                continue
+            for nm, val in zip(names, f[5:9]):
+                if val.lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ---------------------------------------------------------------------------
+# workloads
+# ---------------------------------------------------------------------------
+def _rank_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+class SingleArray:
+    """cfg2 / cfg3: one array, single-array look-back kernels."""
+
+    def __init__(self, cfg: int, delta: bool, n: int | None, rank: int):
+        from paper_1709_08990_b200 import gen
+        self.cfg, self.delta = cfg, delta
+        self.values = gen.config_array(cfg, n)
+        self.n = int(self.values.size)
+        self.name = f"cfg{cfg}"
+
+    def describe(self):
+        if self.cfg == 2:
+            return {"workload": "cfg2: delta encode+decode of one sorted array, geometric gaps mean 8, prev=0",
+                    "n": self.n}
+        return {"workload": "cfg3: plain encode+decode of one array, byte length uniform 1-4", "n": self.n}
+
+    def setup(self, dev, torch):
+        self.dev = dev
+        self.d_v = torch.from_numpy(self.values.view(np.int32)).cuda()
+        cap = (self.n + 3) // 4 + 4 * self.n
+        self.d_c = torch.empty(cap, dtype=torch.uint8, device="cuda")
+        self.d_len = torch.zeros(1, dtype=torch.int64, device="cuda")
+        self.d_o = torch.empty_like(self.d_v)
+        self.d_last = torch.zeros(1, dtype=torch.int32, device="cuda")
+        self.encode()
+        torch.cuda.synchronize()
+        self.cmp = int(self.d_len.item())
+
+    def encode(self):
+        self.dev.encode(self.d_v, self.d_c, self.d_len, delta=self.delta, prev=0)
+
+    def decode(self):
+        self.dev.decode(self.d_c, self.n, self.d_o, in_len=self.cmp, delta=self.delta, base=0, last=self.d_last)
+
+    def verify(self, torch):
+        self.dev.check()
+        assert torch.equal(self.d_o, self.d_v), "round trip mismatch"
+
+    # e2e through the reference-facing host C-ABI (pinned host buffers)
+    def e2e_setup(self, torch):
+        from paper_1709_08990_b200 import codec
+        self.h_v = torch.from_numpy(self.values.view(np.int32)).pin_memory().numpy().view(np.uint32)
+        self.h_c = torch.empty((self.n + 3) // 4 + 4 * self.n, dtype=torch.uint8).pin_memory().numpy()
+        self.h_o = torch.empty(self.n, dtype=torch.int32).pin_memory().numpy().view(np.uint32)
+        self._codec = codec
+
+    def e2e_step(self):
+        import ctypes as C
+        from paper_1709_08990_b200._native import lib
+        ctx = self._codec._ctx()
+        ln = C.c_size_t(0)
+        st = lib.bcgpu_svb_encode_host(ctx, self.h_v.ctypes.data, self.n, int(self.delta), 0, self.h_c.ctypes.data,
+                                       self.h_c.size, C.byref(ln))
+        assert st == 0, st
+        last = C.c_uint32(0)
+        st = lib.bcgpu_svb_decode_host(ctx, self.h_c.ctypes.data, ln.value, self.n, int(self.delta), 0,
+                                       self.h_o.ctypes.data, C.byref(last))
+        assert st == 0, st
+        return 4 * self.n + ln.value, ln.value + 4 * self.n  # h2d, d2h bytes
+
+    def e2e_verify(self):
+        assert np.array_equal(self.h_o, self.values)
+
+    # CPU reference: a bounded sample with all host threads
+    def cpu_sample(self, n_sample: int):
+        return self.values[:n_sample]
+
+
+class Batch:
+    """cfg4 / cfg5: independent segments, batch kernels; sharded across ranks."""
+
+    def __init__(self, cfg: int, rank: int, world: int, scale: float = 1.0):
+        from paper_1709_08990_b200 import gen
+        self.cfg, self.delta = cfg, True
+        if cfg == 4:
+            nl = int((1 << 20) * scale)
+            lb = gen.posting_lists(nl, gen.SEEDS[4], cap_total=int((1 << 30) * scale))
+            lens, offs, vals, prevs = lb.lengths, lb.offsets, lb.values, np.zeros(nl, np.uint32)
+            self.cap = lb.cap
+        else:
+            total = int((1 << 31) * scale) // gen.CFG5_CHUNK * gen.CFG5_CHUNK
+            vals = gen.geometric_sorted(total, 32.0, gen.SEEDS[5])
+            nl = total // gen.CFG5_CHUNK
+            lens = np.full(nl, gen.CFG5_CHUNK, np.uint32)
+            offs = np.arange(nl + 1, dtype=np.uint64) * gen.CFG5_CHUNK
+            prevs = np.zeros(nl, np.uint32)
+            prevs[1:] = vals[gen.CFG5_CHUNK - 1:-1:gen.CFG5_CHUNK]
+            self.cap = None
+        # shard: contiguous segment ranges cut at equal cumulative cost
+        from paper_1709_08990_b200.shard import partition_by_cost
+        lo, hi = partition_by_cost(lens.astype(np.float64) * 6.0, world)[rank]
+        self.lens = lens[lo:hi]
+        self.prevs = prevs[lo:hi]
+        base = int(offs[lo])
+        self.offs = offs[lo:hi + 1] - base
+        self.values = vals[base:int(offs[hi])]
+        self.n = int(self.values.size)
+        self.nseg = hi - lo
+        self.max_n = int(self.lens.max()) if self.nseg else 0
+        self.total_segments = int(nl)
+
+    def describe(self):
+        if self.cfg == 4:
+            return {"workload": "cfg4: 1M posting-list-like arrays, delta encode+decode per list (prev=0), "
+                                "water-fill capped to 2^30 ints", "lists": self.total_segments, "cap": self.cap,
+                    "n": self.n}
+        return {"workload": "cfg5: 2^31 sorted ints (gaps mean 32, wrapping) in 64K-int chunks, prev-seeded "
+                            "delta encode+decode", "chunks": self.total_segments, "n": self.n}
+
+    def setup(self, dev, torch):
+        from paper_1709_08990_b200.device import DECODE_SEG_DTYPE, ENCODE_SEG_DTYPE, segments_to_tensor
+        self.dev = dev
+        n, nseg = self.n, self.nseg
+        caps = (self.lens.astype(np.uint64) + 3) // 4 + 4 * self.lens.astype(np.uint64)
+        eoff = np.zeros(nseg + 1, np.uint64)
+        np.cumsum(caps, out=eoff[1:])
+        es = np.zeros(nseg, ENCODE_SEG_DTYPE)
+        es["src_offset"], es["dst_capacity"], es["dst_offset"] = self.offs[:-1], caps, eoff[:-1]
+        es["n"], es["prev"] = self.lens, self.prevs
+        self.d_esegs = segments_to_tensor(es, "cuda")
+        self.d_v = torch.from_numpy(self.values.view(np.int32)).cuda()
+        self.d_c = torch.empty(int(eoff[-1]) + 16, dtype=torch.uint8, device="cuda")
+        self.d_lens = torch.zeros(nseg, dtype=torch.int64, device="cuda")
+        self.d_o = torch.empty_like(self.d_v)
+        self.encode()
+        torch.cuda.synchronize()
+        lens = self.d_lens.cpu().numpy().astype(np.uint64)
+        self.cmp = int(lens.sum())
+        ds = np.zeros(nseg, DECODE_SEG_DTYPE)
+        ds["src_offset"], ds["src_bytes"], ds["dst_offset"] = eoff[:-1], lens, self.offs[:-1]
+        ds["n"], ds["prev"] = self.lens, self.prevs
+        self.d_dsegs = segments_to_tensor(ds, "cuda")
+
+    def encode(self):
+        self.dev.encode_batch(self.d_esegs, self.nseg, self.d_v, self.d_c, self.d_lens, delta=True,
+                              max_seg_n=self.max_n)
+
+    def decode(self):
+        self.dev.decode_batch(self.d_dsegs, self.nseg, self.d_c, self.d_o, delta=True, max_seg_n=self.max_n)
+
+    def verify(self, torch):
+        self.dev.check()
+        assert torch.equal(self.d_o, self.d_v), "round trip mismatch"
+
+    def e2e_setup(self, torch):
+        self.h_v = torch.from_numpy(self.values.view(np.int32)).pin_memory()
+        self.h_c = torch.empty(self.d_c.numel(), dtype=torch.uint8).pin_memory()
+        self.h_o = torch.empty(self.n, dtype=torch.int32).pin_memory()
+        self._torch = torch
+
+    def e2e_step(self):
+        # batch API: H2D values, encode_batch, D2H streams; H2D streams, decode_batch, D2H values
+        torch = self._torch
+        self.d_v.copy_(self.h_v, non_blocking=True)
+        self.encode()
+        self.h_c.copy_(self.d_c, non_blocking=True)
+        self.d_c.copy_(self.h_c, non_blocking=True)
+        self.decode()
+        self.h_o.copy_(self.d_o, non_blocking=True)
+        torch.cuda.synchronize()
+        slots = self.d_c.numel()
+        return 4 * self.n + slots, slots + 4 * self.n
+
+    def e2e_verify(self):
+        assert np.array_equal(self.h_o.numpy().view(np.uint32), self.values)
+
+    def cpu_sample(self, n_sample: int):
+        return None
+
+
+def make_workload(name: str, rank: int, world: int, n: int | None, scale: float):
+    if name == "cfg2":
+        return SingleArray(2, True, n, rank)
+    if name == "cfg3":
+        return SingleArray(3, False, n, rank)
+    if name in ("cfg4", "cfg5"):
+        return Batch(int(name[-1]), rank, world, scale)
+    raise SystemExit(f"unknown workload {name}")
+
+
+# ---------------------------------------------------------------------------
+# CPU reference (oracle port, all host threads)
+# ---------------------------------------------------------------------------
+def cpu_reference_sample(wl_name: str, n_sample: int, threads: int, min_seconds: float):
+    """Time the CPU reference (oracle mt encode + O2 mt decode) on a bounded sample of the
+    workload; returns (Gint/s round trip, reps, seconds)."""
+    import oracle
+    from paper_1709_08990_b200 import gen
+    delta = wl_name != "cfg3"
+    if wl_name == "cfg2":
+        v = gen.config_array(2, n_sample)
+    elif wl_name == "cfg3":
+        v = gen.config_array(3, n_sample)
+    elif wl_name == "cfg5":
+        v = gen.geometric_sorted(n_sample, 32.0, gen.SEEDS[5])
+    else:
+        lb = gen.posting_lists(max(1, n_sample // 1000), gen.SEEDS[4], cap_total=n_sample)
+        v = lb.values
+    out = np.empty((v.size + 3) // 4 + 4 * v.size + 1, np.uint8)
+    dec = np.empty(v.size, np.uint32)
+    reps, t_total = 0, 0.0
+    while reps < 3 or t_total < min_seconds:
+        t0 = time.perf_counter()
+        m = oracle.mt_encode(v, delta=delta, prev=0, threads=threads, out=out)
+        st, _ = oracle.mt_decode(out[:m], v.size, dec, delta=delta, base=0, threads=threads)
+        t_total += time.perf_counter() - t0
+        reps += 1
+        assert st == 0 and np.array_equal(dec, v)
+    return v.size * reps / t_total / 1e9, reps, t_total, int(v.size)
+
+
+def run_reference(args):
+    rank, world, local = _rank_env()
+    if rank != 0:
+        return 0
+    threads = os.cpu_count() or 1
+    n_sample = args.cpu_sample or (1 << 24)
+    for _ in range(args.warmup):
+        cpu_reference_sample(args.workload, n_sample, threads, 0.0)
+    vals = []
+    t_all = time.perf_counter()
+    for _ in range(args.steps):
+        g, reps, secs, ns = cpu_reference_sample(args.workload, n_sample, threads, 0.0)
+        vals.append(g)
+    elapsed = time.perf_counter() - t_all
+    value = statistics.median(vals)
+    sample = (f"{ns} ints of {args.workload} (seeded synthetic), delta={'no' if args.workload == 'cfg3' else 'yes'}"
+              f", multi-threaded encode+decode round trip per step")
+    line = {
+        "impl": "reference", "metric": METRIC, "value": round(value, 4), "unit": "Gint/s", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(1e3 * elapsed / max(1, args.steps), 3),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u32", "data": "synthetic",
+        "config": {"workload": args.workload, "sample_ints": ns},
+        "cpu_baseline": {"value": round(value, 4), "unit": "Gint/s", "cores": threads, "kind": "port",
+                         "sample": sample},
+        "e2e": {"value": round(value, 4), "unit": "Gint/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "note": "reference is headers-only (no src/*.cpp, SURVEY.md §0); the CPU reference arm is the pinned "
+                "oracle port: O1 encoder + paper Fig. 4 SSSE3 decoder, pthreads over chunks",
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ---------------------------------------------------------------------------
+# GPU arm
+# ---------------------------------------------------------------------------
+def run_gpu(args):
+    import torch
+    rank, world, local = _rank_env()
+    if world > 1:
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    else:
+        torch.cuda.set_device(0)
+    from paper_1709_08990_b200 import _native
+    from paper_1709_08990_b200.device import DeviceCodec
+
+    wl = make_workload(args.workload, rank, world, args.n, args.scale)
+    dev = DeviceCodec(torch.cuda.current_device())
+    wl.setup(dev, torch)
+    stream = torch.cuda.current_stream()
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+
+    def step(evs):
+        flush.fill_(1)
+        evs[0].record(stream)
+        wl.encode()
+        evs[1].record(stream)
+        flush.fill_(2)
+        evs[2].record(stream)
+        wl.decode()
+        evs[3].record(stream)
+
+    for _ in range(max(3, args.warmup)):
+        step([torch.cuda.Event(enable_timing=True) for _ in range(4)])
+    torch.cuda.synchronize()
+    wl.verify(torch)
+
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(args.steps)]
+    if world > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize()
+    launches0 = _native.kernel_launch_count()
+    with ClockSampler(torch.cuda.current_device() if "CUDA_VISIBLE_DEVICES" not in os.environ else local) as clk:
+        for k in range(args.steps):
+            step(evs[k])
+        torch.cuda.synchronize()
+    if world > 1:
+        torch.distributed.barrier()
+    launches = _native.kernel_launch_count() - launches0
+    t_enc = [e[0].elapsed_time(e[1]) for e in evs]
+    t_dec = [e[2].elapsed_time(e[3]) for e in evs]
+    ms_step = statistics.mean(a + b for a, b in zip(t_enc, t_dec))
+    if world > 1:
+        t = torch.tensor([ms_step], dtype=torch.float64, device="cuda")
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        ms_step_max = float(t.item())
+        ntot = torch.tensor([wl.n], dtype=torch.float64, device="cuda")
+        torch.distributed.all_reduce(ntot)
+        n_all = float(ntot.item())
+    else:
+        ms_step_max, n_all = ms_step, float(wl.n)
+    wl.verify(torch)
+
+    peak, peak_src = _peaks()
+    alg = wl.cmp + 4 * wl.n
+    me, md = statistics.mean(t_enc), statistics.mean(t_dec)
+    phases = {
+        "encode": {"ms": round(me, 4), "gint_s": round(wl.n / me / 1e6, 2), "gbs": round(alg / me / 1e6, 1),
+                   "frac": round(alg / me / 1e6 / peak, 4)},
+        "decode": {"ms": round(md, 4), "gint_s": round(wl.n / md / 1e6, 2), "gbs": round(alg / md / 1e6, 1),
+                   "frac": round(alg / md / 1e6 / peak, 4)},
+    }
+    dom = "decode" if md >= me else "encode"
+    traffic = None
+    tf = ROOT / "profiles" / "traffic.json"
+    if tf.exists():
+        traffic = json.loads(tf.read_text()).get(f"{args.workload}:{dom}")
+
+    # e2e through the host C-ABI / batch API with pinned host buffers
+    e2e = None
+    if not args.no_e2e:
+        wl.e2e_setup(torch)
+        wl.e2e_step()
+        reps = max(1, min(args.steps, 5))
+        t0 = time.perf_counter()
+        for _ in range(reps):
+            h2d, d2h = wl.e2e_step()
+        torch.cuda.synchronize()
+        t_e2e = (time.perf_counter() - t0) / reps
+        wl.e2e_verify()
+        e2e_local = torch.tensor([t_e2e], dtype=torch.float64, device="cuda")
+        if world > 1:
+            torch.distributed.all_reduce(e2e_local, op=torch.distributed.ReduceOp.MAX)
+        e2e = {"value": round(n_all / float(e2e_local.item()) / 1e9, 4), "unit": "Gint/s",
+               "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
+               "path": "bcgpu_svb_encode_host + bcgpu_svb_decode_host (pinned host buffers)"
+               if isinstance(wl, SingleArray) else "H2D + encode_batch + D2H, H2D + decode_batch + D2H"}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu and isinstance(wl, SingleArray):
+        threads = os.cpu_count() or 1
+        g, reps, secs, ns = cpu_reference_sample(args.workload, args.cpu_sample or (1 << 24), threads,
+                                                 args.cpu_seconds)
+        cpu = {"value": round(g, 4), "unit": "Gint/s", "cores": threads, "kind": "port",
+               "sample": f"{ns}-int prefix of the {args.workload} input, encode+decode round trip, {reps} reps "
+                         f"in {secs:.1f}s (O1 encoder + SSSE3 Fig.4 decoder, pthreads)"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC,
+            "value": round(n_all / ms_step_max / 1e6, 3),
+            "unit": "Gint/s",
+            "n_gpus": world,
+            "steps": args.steps,
+            "warmup": max(3, args.warmup),
+            "ms_per_step": round(ms_step_max, 4),
+            "higher_is_better": True,
+            "scaling": "weak",
+            "vs_baseline": None,
+            "dtype": "u32",
+            "data": "synthetic (seeded splitmix64 generators standing in for BASELINE.json configs)",
+            "config": dict(wl.describe(), compressed_bytes=wl.cmp, bytes_per_int=round(wl.cmp / wl.n, 4),
+                           step="encode kernel + decode kernel (round trip), each CUDA-event timed",
+                           l2="flushed (256 MiB write) before every timed kernel",
+                           parallelism=f"{'replicas' if isinstance(wl, SingleArray) else 'segment shards'} x{world}"),
+            "phases": phases,
+            "roofline": {"bound": "hbm", "kernel": dom, "achieved": phases[dom]["gbs"], "peak": peak,
+                         "unit": "GB/s", "frac": phases[dom]["frac"], "traffic": traffic,
+                         "algorithmic_bytes_per_launch": alg, "peak_source": peak_src},
+            "e2e": e2e,
+            "gpu_launches": int(launches),
+            "clocks": clk.summary(),
+            "cpu_baseline": cpu,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        torch.distributed.destroy_process_group()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="cfg2", choices=["cfg2", "cfg3", "cfg4", "cfg5"])
+    ap.add_argument("--n", type=int, default=None, help="override array size (single-array workloads)")
+    ap.add_argument("--scale", type=float, default=1.0, help="scale batch workloads (cfg4/cfg5)")
+    ap.add_argument("--cpu-sample", type=int, default=0)
+    ap.add_argument("--cpu-seconds", type=float, default=10.0)
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_gpu(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

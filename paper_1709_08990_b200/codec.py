@@ -1,0 +1,247 @@
+"""Python mirror of the reference's Stream VByte operator API.
+
+Names, argument meaning and error behaviour follow
+``proj/core/include/bytecodec/codec.hpp:17-96`` and ``stream_vbyte.hpp:24-54``
+(namespace ``bytecodec``): the same ``codec_id`` tags, the same ``errc``
+taxonomy raised as :class:`CodecError`, ``encode``/``decode`` over
+:class:`EncodedBuffer`, and the ``svb_*`` functions.  Host arrays (numpy) go
+through the C ABI's synchronous ``*_host`` entry points; CUDA tensors go
+through :class:`DeviceCodec` (stream-ordered ``*_device`` entry points).
+Every call runs on the GPU -- there is no CPU path.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import enum
+import threading
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _native
+from ._native import lib
+
+
+class codec_id(enum.IntEnum):
+    """Wire tags, reference codec.hpp:17-22."""
+    vbyte = 0
+    varint_gb = 1
+    varint_g8iu = 2
+    stream_vbyte = 3
+
+
+class errc(enum.IntEnum):
+    """reference codec.hpp:28-47 (same order)."""
+    truncated = 0
+    trailing_bytes = 1
+    run_too_long = 2
+    value_overflow = 3
+    oversized_integer = 4
+    count_mismatch = 5
+    bad_stream_size = 6
+    bad_magic = 7
+    unknown_codec = 8
+    reserved_flags = 9
+    length_mismatch = 10
+    unsupported = 11
+    out_of_range = 12
+    io_failure = 13
+    bad_config = 14
+
+
+class CodecError(RuntimeError):
+    """codec_error (codec.hpp:49-58): carries an :class:`errc`."""
+
+    def __init__(self, code: errc, what: str):
+        super().__init__(what)
+        self.code = code
+
+
+class GpuError(RuntimeError):
+    """A CUDA / argument failure the reference cannot produce."""
+
+
+def _check(st: int, where: str) -> None:
+    if st == 0:
+        return
+    if 1 <= st <= 15:
+        raise CodecError(errc(st - 1), f"{where}: {_native.status_string(st)}")
+    msg = f"{where}: {_native.status_string(st)}"
+    if st == 101:
+        msg += f" ({_native.last_cuda_error()})"
+    raise GpuError(msg)
+
+
+@dataclass
+class EncodedBuffer:
+    """encoded_buffer, codec.hpp:60-67."""
+    codec: codec_id = codec_id.vbyte
+    count: int = 0
+    delta: bool = False
+    bytes: bytes = field(default=b"")
+
+
+def byte_length(x: int) -> int:
+    """codec.hpp:70-72 (served by the library)."""
+    return int(lib.bcgpu_byte_length(int(x) & 0xFFFFFFFF))
+
+
+def svb_control_bytes(n: int) -> int:
+    """stream_vbyte.hpp:34."""
+    return int(lib.bcgpu_svb_control_bytes(n))
+
+
+def svb_max_compressed_bytes(n: int) -> int:
+    return int(lib.bcgpu_svb_max_compressed_bytes(n))
+
+
+def svb_tables() -> tuple[np.ndarray, np.ndarray]:
+    """decode_tables (stream_vbyte.hpp:24-32): (length[256], shuffle[256,16])."""
+    length = np.zeros(256, np.uint8)
+    shuffle = np.zeros((256, 16), np.uint8)
+    lib.bcgpu_svb_tables(length.ctypes.data, shuffle.ctypes.data)
+    return length, shuffle
+
+
+# ---- per-thread context --------------------------------------------------
+_tls = threading.local()
+
+
+def _ctx(device: int = 0) -> int:
+    ctxs = getattr(_tls, "ctxs", None)
+    if ctxs is None:
+        ctxs = _tls.ctxs = {}
+    if device not in ctxs:
+        p = C.c_void_p()
+        _check(lib.bcgpu_ctx_create(device, C.byref(p)), "bcgpu_ctx_create")
+        ctxs[device] = p.value
+    return ctxs[device]
+
+
+def _u32_array(values) -> np.ndarray:
+    a = np.ascontiguousarray(values, dtype=np.uint32)
+    return a
+
+
+def _byte_array(data) -> np.ndarray:
+    if isinstance(data, (bytes, bytearray, memoryview)):
+        return np.frombuffer(bytes(data), dtype=np.uint8)
+    return np.ascontiguousarray(data, dtype=np.uint8)
+
+
+# ---- host-span API (reference signatures) --------------------------------
+def _encode(values, delta: bool, prev: int) -> bytes:
+    v = _u32_array(values)
+    n = v.size
+    out = np.empty(max(1, svb_max_compressed_bytes(n)), np.uint8)
+    out_len = C.c_size_t(0)
+    _check(lib.bcgpu_svb_encode_host(_ctx(), v.ctypes.data, n, int(delta), prev & 0xFFFFFFFF,
+                                     out.ctypes.data, out.size, C.byref(out_len)), "svb_encode")
+    return out[: out_len.value].tobytes()
+
+
+def svb_encode(values) -> bytes:
+    """stream_vbyte.hpp:36."""
+    return _encode(values, False, 0)
+
+
+def svb_encode_delta(values, prev: int = 0) -> bytes:
+    """Extension E2: prev-seeded delta encode."""
+    return _encode(values, True, prev)
+
+
+def _decode(data, n: int, delta: bool, base: int, out) -> int:
+    b = _byte_array(data)
+    if out is None:
+        raise ValueError("out must hold n integers")
+    if out.dtype != np.uint32 or not out.flags.c_contiguous or out.size < n:
+        raise ValueError("out must be a C-contiguous uint32 array of at least n elements")
+    last = C.c_uint32(0)
+    _check(lib.bcgpu_svb_decode_host(_ctx(), b.ctypes.data if b.size else None, b.size, n, int(delta),
+                                     base & 0xFFFFFFFF, out.ctypes.data, C.byref(last)),
+           "svb_decode_delta" if delta else "svb_decode")
+    return int(last.value)
+
+
+def svb_decode(data, n: int, out: np.ndarray | None = None) -> np.ndarray:
+    """stream_vbyte.hpp:38-39 (both overloads: fills ``out`` or returns a new array)."""
+    o = np.empty(n, np.uint32) if out is None else out
+    _decode(data, n, False, 0, o)
+    return o
+
+
+def svb_decode_delta(data, n: int, base: int, out: np.ndarray) -> int:
+    """stream_vbyte.hpp:41-42: fused decode + prefix sum; returns the last value."""
+    return _decode(data, n, True, base, out)
+
+
+def svb_block_data_offsets(data, n: int) -> np.ndarray:
+    """stream_vbyte.hpp:48-49."""
+    b = _byte_array(data)
+    offs = np.empty(max(1, svb_control_bytes(n)), np.uint64)
+    _check(lib.bcgpu_svb_block_offsets_host(_ctx(), b.ctypes.data if b.size else None, b.size, n,
+                                            offs.ctypes.data), "svb_block_data_offsets")
+    return offs[: svb_control_bytes(n)]
+
+
+def svb_decode_block(data, n: int, block: int, data_offset: int) -> np.ndarray:
+    """stream_vbyte.hpp:51-54: returns the block's integers (4, or fewer for the tail)."""
+    vals, counts = svb_decode_blocks(data, n, np.array([block], np.uint64), np.array([data_offset], np.uint64))
+    return vals[0, : counts[0]]
+
+
+def svb_decode_blocks(data, n: int, blocks, offsets) -> tuple[np.ndarray, np.ndarray]:
+    """Batched random-access block decode: (values[nblocks,4], counts[nblocks])."""
+    b = _byte_array(data)
+    blk = np.ascontiguousarray(blocks, np.uint64)
+    off = np.ascontiguousarray(offsets, np.uint64)
+    out = np.zeros((blk.size, 4), np.uint32)
+    cnt = np.zeros(blk.size, np.uint32)
+    _check(lib.bcgpu_svb_decode_blocks_host(_ctx(), b.ctypes.data if b.size else None, b.size, n,
+                                            blk.ctypes.data, off.ctypes.data, blk.size, out.ctypes.data,
+                                            cnt.ctypes.data), "svb_decode_block")
+    return out, cnt
+
+
+def _require_svb(cid) -> None:
+    if codec_id(cid) != codec_id.stream_vbyte:
+        raise CodecError(errc.unsupported, "only codec_id.stream_vbyte is implemented on the GPU path")
+
+
+def encode_payload(cid, values) -> bytes:
+    """codec.hpp:84."""
+    _require_svb(cid)
+    return svb_encode(values)
+
+
+def decode_payload(cid, data, n: int, out: np.ndarray) -> None:
+    """codec.hpp:85."""
+    _require_svb(cid)
+    svb_decode(data, n, out)
+
+
+def decode_payload_delta(cid, data, n: int, base: int, out: np.ndarray) -> int:
+    """codec.hpp:89-90."""
+    _require_svb(cid)
+    return svb_decode_delta(data, n, base, out)
+
+
+def encode(cid, values, delta: bool = False) -> EncodedBuffer:
+    """codec.hpp:92-93 (delta base 0)."""
+    _require_svb(cid)
+    v = _u32_array(values)
+    if v.size > 0xFFFFFFFF:
+        raise CodecError(errc.out_of_range, "count exceeds uint32")
+    data = svb_encode_delta(v, 0) if delta else svb_encode(v)
+    return EncodedBuffer(codec_id(cid), int(v.size), bool(delta), data)
+
+
+def decode(buf: EncodedBuffer) -> np.ndarray:
+    """codec.hpp:95-96."""
+    _require_svb(buf.codec)
+    out = np.empty(buf.count, np.uint32)
+    if buf.delta:
+        svb_decode_delta(buf.bytes, buf.count, 0, out)
+    else:
+        svb_decode(buf.bytes, buf.count, out)
+    return out

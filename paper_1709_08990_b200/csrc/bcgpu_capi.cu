@@ -1,0 +1,477 @@
+// bcgpu_capi.cu -- the extern "C" boundary (include/bcgpu/bcgpu.h).
+//
+// Owns the per-context device workspace (look-back status words, tile ticket,
+// status word) and the host-pointer entry points that give the reference's
+// synchronous call semantics (H2D, kernel, D2H, codec_error mapping).
+// No CPU fallback: every compute entry point launches a kernel or fails.
+#include <atomic>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <new>
+
+#include <cuda_runtime.h>
+
+#include "bcgpu/bcgpu.h"
+#include "svb_device.cuh"
+#include "svb_kernels.cuh"
+
+using namespace bcgpu;
+
+namespace {
+
+std::atomic<uint64_t> g_launches{0};
+thread_local char g_cuda_err[256] = "";
+
+int cuda_fail(cudaError_t e, const char* where) {
+    std::snprintf(g_cuda_err, sizeof(g_cuda_err), "%s: %s", where, cudaGetErrorString(e));
+    return BCGPU_ERR_CUDA;
+}
+
+#define BC_CUDA(call)                                   \
+    do {                                                \
+        cudaError_t e_ = (call);                        \
+        if (e_ != cudaSuccess) return cuda_fail(e_, #call); \
+    } while (0)
+
+struct DeviceGuard {
+    int prev = -1;
+    explicit DeviceGuard(int dev) {
+        cudaGetDevice(&prev);
+        if (prev != dev) cudaSetDevice(dev);
+    }
+    ~DeviceGuard() {
+        int cur = -1;
+        cudaGetDevice(&cur);
+        if (prev >= 0 && cur != prev) cudaSetDevice(prev);
+    }
+};
+
+}  // namespace
+
+struct bcgpu_ctx {
+    int device = 0;
+    int num_sms = 148;
+    // look-back workspace: [ticket | status word | off_status[cap] | sum_status[cap]]
+    unsigned long long* ws = nullptr;
+    size_t ws_tiles = 0;
+    uint32_t epoch = 0;
+    unsigned long long ticket_base = 0;
+    uint32_t last_epoch = 0;  // epoch of the last *_device call
+    // batch grid sizes
+    int warp_grid = 0, dec_cta_grid = 0, enc_cta_grid = 0;
+    // host-API scratch (device) and stream
+    cudaStream_t stream = nullptr;
+    void* d_scratch = nullptr;
+    size_t d_scratch_cap = 0;
+};
+
+static unsigned long long* ticket_ptr(bcgpu_ctx* c) { return c->ws; }
+static unsigned long long* status_ptr(bcgpu_ctx* c) { return c->ws + 1; }
+static uint64_t* off_status(bcgpu_ctx* c) { return reinterpret_cast<uint64_t*>(c->ws + 2); }
+static uint64_t* sum_status(bcgpu_ctx* c) { return reinterpret_cast<uint64_t*>(c->ws + 2 + c->ws_tiles); }
+
+static int ensure_ws(bcgpu_ctx* c, size_t tiles) {
+    if (tiles < 1024) tiles = 1024;
+    if (c->ws && tiles <= c->ws_tiles) return BCGPU_OK;
+    size_t cap = c->ws_tiles ? c->ws_tiles : 1024;
+    while (cap < tiles) cap *= 2;
+    if (c->ws) {
+        BC_CUDA(cudaDeviceSynchronize());
+        BC_CUDA(cudaFree(c->ws));
+        c->ws = nullptr;
+    }
+    const size_t bytes = (2 + 2 * cap) * sizeof(unsigned long long);
+    BC_CUDA(cudaMalloc(&c->ws, bytes));
+    BC_CUDA(cudaMemset(c->ws, 0, bytes));
+    c->ws_tiles = cap;
+    c->epoch = 0;
+    c->ticket_base = 0;
+    return BCGPU_OK;
+}
+
+// Next launch epoch; status words of older launches never match it.
+static int next_epoch(bcgpu_ctx* c, cudaStream_t s) {
+    if (c->epoch >= kEpochMax) {
+        BC_CUDA(cudaMemsetAsync(c->ws + 1, 0, (1 + 2 * c->ws_tiles) * sizeof(unsigned long long), s));
+        c->epoch = 0;
+    }
+    c->epoch += 1;
+    c->last_epoch = c->epoch;
+    return BCGPU_OK;
+}
+
+static int make_lookback(bcgpu_ctx* c, uint64_t ngroups, cudaStream_t s, LookbackArgs* lb) {
+    const size_t tiles = (ngroups + kTileGroups - 1) / kTileGroups;
+    int st = ensure_ws(c, tiles);
+    if (st) return st;
+    st = next_epoch(c, s);
+    if (st) return st;
+    lb->off_status = off_status(c);
+    lb->sum_status = sum_status(c);
+    lb->ticket = ticket_ptr(c);
+    lb->ticket_base = c->ticket_base;
+    lb->epoch = c->epoch;
+    lb->num_tiles = (uint32_t)tiles;
+    lb->status = status_ptr(c);
+    c->ticket_base += tiles;
+    return BCGPU_OK;
+}
+
+static int make_batch(bcgpu_ctx* c, cudaStream_t s, BatchArgs* ba) {
+    int st = ensure_ws(c, 1024);
+    if (st) return st;
+    st = next_epoch(c, s);
+    if (st) return st;
+    ba->status = status_ptr(c);
+    ba->epoch = c->epoch;
+    ba->warp_grid = c->warp_grid;
+    ba->cta_grid = c->dec_cta_grid;
+    return BCGPU_OK;
+}
+
+// ---------------------------------------------------------------------------
+extern "C" {
+
+int bcgpu_abi_version(void) { return BCGPU_ABI_VERSION; }
+
+const char* bcgpu_last_cuda_error(void) { return g_cuda_err; }
+
+uint64_t bcgpu_kernel_launch_count(void) { return g_launches.load(); }
+
+const char* bcgpu_status_string(int s) {
+    switch (s) {
+        case BCGPU_OK: return "ok";
+        case BCGPU_ERR_TRUNCATED: return "truncated";
+        case BCGPU_ERR_TRAILING_BYTES: return "trailing_bytes";
+        case BCGPU_ERR_RUN_TOO_LONG: return "run_too_long";
+        case BCGPU_ERR_VALUE_OVERFLOW: return "value_overflow";
+        case BCGPU_ERR_OVERSIZED_INTEGER: return "oversized_integer";
+        case BCGPU_ERR_COUNT_MISMATCH: return "count_mismatch";
+        case BCGPU_ERR_BAD_STREAM_SIZE: return "bad_stream_size";
+        case BCGPU_ERR_BAD_MAGIC: return "bad_magic";
+        case BCGPU_ERR_UNKNOWN_CODEC: return "unknown_codec";
+        case BCGPU_ERR_RESERVED_FLAGS: return "reserved_flags";
+        case BCGPU_ERR_LENGTH_MISMATCH: return "length_mismatch";
+        case BCGPU_ERR_UNSUPPORTED: return "unsupported";
+        case BCGPU_ERR_OUT_OF_RANGE: return "out_of_range";
+        case BCGPU_ERR_IO_FAILURE: return "io_failure";
+        case BCGPU_ERR_BAD_CONFIG: return "bad_config";
+        case BCGPU_ERR_INVALID_ARGUMENT: return "invalid_argument";
+        case BCGPU_ERR_CUDA: return "cuda_error";
+        case BCGPU_ERR_NO_DEVICE: return "no_device";
+        default: return "unknown_status";
+    }
+}
+
+uint32_t bcgpu_byte_length(uint32_t x) {
+    return x < (1u << 8) ? 1u : x < (1u << 16) ? 2u : x < (1u << 24) ? 3u : 4u;
+}
+
+size_t bcgpu_svb_control_bytes(size_t n) { return (n + 3) / 4; }
+
+size_t bcgpu_svb_max_compressed_bytes(size_t n) { return (n + 3) / 4 + 4 * n; }
+
+void bcgpu_svb_tables(uint8_t length[256], uint8_t shuffle[256][16]) {
+    for (int c = 0; c < 256; ++c) {
+        int start = 0;
+        for (int i = 0; i < 4; ++i) {
+            const int len = ((c >> (2 * i)) & 3) + 1;
+            for (int b = 0; b < 4; ++b) shuffle[c][4 * i + b] = (uint8_t)(b < len ? start + b : 0xFF);
+            start += len;
+        }
+        length[c] = (uint8_t)start;
+    }
+}
+
+int bcgpu_ctx_create(int device, bcgpu_ctx** out) {
+    if (!out) return BCGPU_ERR_INVALID_ARGUMENT;
+    *out = nullptr;
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) return BCGPU_ERR_NO_DEVICE;
+    if (device < 0 || device >= ndev) return BCGPU_ERR_INVALID_ARGUMENT;
+    DeviceGuard g(device);
+    bcgpu_ctx* c = new (std::nothrow) bcgpu_ctx();
+    if (!c) return BCGPU_ERR_INVALID_ARGUMENT;
+    c->device = device;
+    cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, device);
+    c->warp_grid = c->num_sms * occupancy_decode_batch_warp();
+    c->dec_cta_grid = c->num_sms * occupancy_decode_batch_cta();
+    c->enc_cta_grid = c->num_sms * occupancy_encode_batch_cta();
+    cudaError_t e = cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking);
+    if (e != cudaSuccess) {
+        delete c;
+        return cuda_fail(e, "cudaStreamCreate");
+    }
+    const int st = ensure_ws(c, 1024);
+    if (st) {
+        cudaStreamDestroy(c->stream);
+        delete c;
+        return st;
+    }
+    *out = c;
+    return BCGPU_OK;
+}
+
+int bcgpu_ctx_destroy(bcgpu_ctx* c) {
+    if (!c) return BCGPU_OK;
+    DeviceGuard g(c->device);
+    cudaDeviceSynchronize();
+    if (c->ws) cudaFree(c->ws);
+    if (c->d_scratch) cudaFree(c->d_scratch);
+    if (c->stream) cudaStreamDestroy(c->stream);
+    delete c;
+    return BCGPU_OK;
+}
+
+int bcgpu_ctx_sync_status(bcgpu_ctx* c, void* stream) {
+    if (!c) return BCGPU_ERR_INVALID_ARGUMENT;
+    DeviceGuard g(c->device);
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    unsigned long long word = 0;
+    BC_CUDA(cudaMemcpyAsync(&word, status_ptr(c), sizeof(word), cudaMemcpyDeviceToHost, s));
+    BC_CUDA(cudaStreamSynchronize(s));
+    if ((uint32_t)(word >> 32) != c->last_epoch) return BCGPU_OK;  // no error reported by that launch
+    return (int)(uint32_t)word;
+}
+
+// ---------------------------------------------------------------------------
+// device-pointer entry points
+// ---------------------------------------------------------------------------
+int bcgpu_svb_encode_device(bcgpu_ctx* c, const uint32_t* d_in, size_t n, int delta, uint32_t prev, uint8_t* d_out,
+                            size_t out_cap, uint64_t* d_out_len, void* stream) {
+    if (!c || (n && (!d_in || !d_out))) return BCGPU_ERR_INVALID_ARGUMENT;
+    if (out_cap < bcgpu_svb_max_compressed_bytes(n)) return BCGPU_ERR_INVALID_ARGUMENT;
+    DeviceGuard g(c->device);
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    if (n == 0) {
+        if (d_out_len) BC_CUDA(cudaMemsetAsync(d_out_len, 0, sizeof(uint64_t), s));
+        return BCGPU_OK;
+    }
+    LookbackArgs lb;
+    int st = make_lookback(c, (n + 3) / 4, s, &lb);
+    if (st) return st;
+    BC_CUDA(launch_encode(d_in, n, delta, prev, d_out, d_out_len, lb, s));
+    g_launches.fetch_add(1);
+    return BCGPU_OK;
+}
+
+int bcgpu_svb_decode_device(bcgpu_ctx* c, const uint8_t* d_in, size_t in_len, size_t n, int delta, uint32_t base,
+                            uint32_t* d_out, uint32_t* d_last, void* stream) {
+    if (!c || (n && (!d_in || !d_out))) return BCGPU_ERR_INVALID_ARGUMENT;
+    const size_t nctrl = (n + 3) / 4;
+    if (in_len < nctrl) return BCGPU_ERR_TRUNCATED;
+    DeviceGuard g(c->device);
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    if (n == 0) {
+        if (d_last) BC_CUDA(cudaMemcpyAsync(d_last, &base, sizeof(uint32_t), cudaMemcpyHostToDevice, s));
+        if (in_len != 0) return BCGPU_ERR_TRAILING_BYTES;
+        return BCGPU_OK;
+    }
+    LookbackArgs lb;
+    int st = make_lookback(c, nctrl, s, &lb);
+    if (st) return st;
+    BC_CUDA(launch_decode(d_in, in_len, n, delta, base, d_out, d_last, lb, s));
+    g_launches.fetch_add(1);
+    return BCGPU_OK;
+}
+
+int bcgpu_svb_block_offsets_device(bcgpu_ctx* c, const uint8_t* d_in, size_t in_len, size_t n, uint64_t* d_offsets,
+                                   void* stream) {
+    if (!c || (n && (!d_in || !d_offsets))) return BCGPU_ERR_INVALID_ARGUMENT;
+    const size_t nctrl = (n + 3) / 4;
+    if (in_len < nctrl) return BCGPU_ERR_TRUNCATED;
+    if (n == 0) return BCGPU_OK;
+    DeviceGuard g(c->device);
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    LookbackArgs lb;
+    int st = make_lookback(c, nctrl, s, &lb);
+    if (st) return st;
+    BC_CUDA(launch_block_offsets(d_in, n, d_offsets, lb, s));
+    g_launches.fetch_add(1);
+    return BCGPU_OK;
+}
+
+int bcgpu_svb_decode_blocks_device(bcgpu_ctx* c, const uint8_t* d_in, size_t in_len, size_t n,
+                                   const uint64_t* d_blocks, const uint64_t* d_offsets, size_t nblocks,
+                                   uint32_t* d_out, uint32_t* d_counts, void* stream) {
+    if (!c || (nblocks && (!d_in || !d_blocks || !d_offsets || !d_out || !d_counts))) return BCGPU_ERR_INVALID_ARGUMENT;
+    if (nblocks == 0) return BCGPU_OK;
+    DeviceGuard g(c->device);
+    BC_CUDA(launch_decode_blocks(d_in, in_len, n, d_blocks, d_offsets, nblocks, d_out, d_counts,
+                                 static_cast<cudaStream_t>(stream)));
+    g_launches.fetch_add(1);
+    return BCGPU_OK;
+}
+
+int bcgpu_svb_decode_batch_device(bcgpu_ctx* c, const bcgpu_decode_segment* d_segs, size_t nseg, const uint8_t* d_in,
+                                  uint32_t* d_out, int delta, uint32_t max_seg_n, void* stream) {
+    if (!c || (nseg && (!d_segs || !d_in || !d_out))) return BCGPU_ERR_INVALID_ARGUMENT;
+    if (nseg == 0) return BCGPU_OK;
+    DeviceGuard g(c->device);
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    BatchArgs ba;
+    int st = make_batch(c, s, &ba);
+    if (st) return st;
+    ba.cta_grid = c->dec_cta_grid;
+    int launches = 0;
+    BC_CUDA(launch_decode_batch(d_segs, nseg, d_in, d_out, delta, max_seg_n, ba, s, &launches));
+    g_launches.fetch_add((uint64_t)launches);
+    return BCGPU_OK;
+}
+
+int bcgpu_svb_encode_batch_device(bcgpu_ctx* c, const bcgpu_encode_segment* d_segs, size_t nseg, const uint32_t* d_in,
+                                  uint8_t* d_out, uint64_t* d_out_lens, int delta, uint32_t max_seg_n, void* stream) {
+    if (!c || (nseg && (!d_segs || !d_in || !d_out || !d_out_lens))) return BCGPU_ERR_INVALID_ARGUMENT;
+    if (nseg == 0) return BCGPU_OK;
+    DeviceGuard g(c->device);
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    BatchArgs ba;
+    int st = make_batch(c, s, &ba);
+    if (st) return st;
+    ba.cta_grid = c->enc_cta_grid;
+    int launches = 0;
+    BC_CUDA(launch_encode_batch(d_segs, nseg, d_in, d_out, d_out_lens, delta, max_seg_n, ba, s, &launches));
+    g_launches.fetch_add((uint64_t)launches);
+    return BCGPU_OK;
+}
+
+int bcgpu_svb_encoded_sizes_batch_device(bcgpu_ctx* c, const bcgpu_encode_segment* d_segs, size_t nseg,
+                                         const uint32_t* d_in, uint64_t* d_out_lens, int delta, uint32_t max_seg_n,
+                                         void* stream) {
+    (void)max_seg_n;
+    if (!c || (nseg && (!d_segs || !d_in || !d_out_lens))) return BCGPU_ERR_INVALID_ARGUMENT;
+    if (nseg == 0) return BCGPU_OK;
+    DeviceGuard g(c->device);
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    BatchArgs ba;
+    int st = make_batch(c, s, &ba);
+    if (st) return st;
+    BC_CUDA(launch_sizes_batch(d_segs, nseg, d_in, d_out_lens, delta, ba, s));
+    g_launches.fetch_add(1);
+    return BCGPU_OK;
+}
+
+// ---------------------------------------------------------------------------
+// host-pointer entry points (synchronous; the reference's call semantics)
+// ---------------------------------------------------------------------------
+static int scratch(bcgpu_ctx* c, size_t bytes, void** p) {
+    if (bytes > c->d_scratch_cap) {
+        if (c->d_scratch) {
+            BC_CUDA(cudaStreamSynchronize(c->stream));
+            BC_CUDA(cudaFree(c->d_scratch));
+            c->d_scratch = nullptr;
+            c->d_scratch_cap = 0;
+        }
+        size_t cap = bytes + bytes / 8 + 4096;
+        BC_CUDA(cudaMalloc(&c->d_scratch, cap));
+        c->d_scratch_cap = cap;
+    }
+    *p = c->d_scratch;
+    return BCGPU_OK;
+}
+
+static inline size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+
+int bcgpu_svb_encode_host(bcgpu_ctx* c, const uint32_t* values, size_t n, int delta, uint32_t prev, uint8_t* out,
+                          size_t out_cap, size_t* out_len) {
+    if (!c || !out_len || (n && (!values || !out))) return BCGPU_ERR_INVALID_ARGUMENT;
+    *out_len = 0;
+    if (n == 0) return BCGPU_OK;
+    const size_t max_out = bcgpu_svb_max_compressed_bytes(n);
+    DeviceGuard g(c->device);
+    const size_t in_bytes = 4 * n;
+    const size_t off_out = align_up(in_bytes, 256), off_len = align_up(off_out + max_out, 256);
+    void* base = nullptr;
+    int st = scratch(c, off_len + 256, &base);
+    if (st) return st;
+    uint8_t* d = static_cast<uint8_t*>(base);
+    BC_CUDA(cudaMemcpyAsync(d, values, in_bytes, cudaMemcpyHostToDevice, c->stream));
+    st = bcgpu_svb_encode_device(c, reinterpret_cast<uint32_t*>(d), n, delta, prev, d + off_out, max_out,
+                                 reinterpret_cast<uint64_t*>(d + off_len), c->stream);
+    if (st) return st;
+    uint64_t len = 0;
+    BC_CUDA(cudaMemcpyAsync(&len, d + off_len, sizeof(len), cudaMemcpyDeviceToHost, c->stream));
+    BC_CUDA(cudaStreamSynchronize(c->stream));
+    if (len > out_cap) return BCGPU_ERR_INVALID_ARGUMENT;
+    BC_CUDA(cudaMemcpyAsync(out, d + off_out, len, cudaMemcpyDeviceToHost, c->stream));
+    BC_CUDA(cudaStreamSynchronize(c->stream));
+    *out_len = (size_t)len;
+    return BCGPU_OK;
+}
+
+int bcgpu_svb_decode_host(bcgpu_ctx* c, const uint8_t* bytes, size_t len, size_t n, int delta, uint32_t base,
+                          uint32_t* out, uint32_t* last) {
+    if (!c || (n && (!bytes || !out))) return BCGPU_ERR_INVALID_ARGUMENT;
+    const size_t nctrl = (n + 3) / 4;
+    if (len < nctrl) return BCGPU_ERR_TRUNCATED;
+    if (n == 0) {
+        if (last) *last = base;
+        return len ? BCGPU_ERR_TRAILING_BYTES : BCGPU_OK;
+    }
+    DeviceGuard g(c->device);
+    const size_t off_out = align_up(len, 256), off_last = align_up(off_out + 4 * n, 256);
+    void* sp = nullptr;
+    int st = scratch(c, off_last + 256, &sp);
+    if (st) return st;
+    uint8_t* d = static_cast<uint8_t*>(sp);
+    BC_CUDA(cudaMemcpyAsync(d, bytes, len, cudaMemcpyHostToDevice, c->stream));
+    st = bcgpu_svb_decode_device(c, d, len, n, delta, base, reinterpret_cast<uint32_t*>(d + off_out),
+                                 reinterpret_cast<uint32_t*>(d + off_last), c->stream);
+    if (st) return st;
+    st = bcgpu_ctx_sync_status(c, c->stream);
+    if (st) return st;
+    BC_CUDA(cudaMemcpyAsync(out, d + off_out, 4 * n, cudaMemcpyDeviceToHost, c->stream));
+    uint32_t lv = 0;
+    BC_CUDA(cudaMemcpyAsync(&lv, d + off_last, sizeof(lv), cudaMemcpyDeviceToHost, c->stream));
+    BC_CUDA(cudaStreamSynchronize(c->stream));
+    if (last) *last = delta ? lv : out[n - 1];
+    return BCGPU_OK;
+}
+
+int bcgpu_svb_decode_blocks_host(bcgpu_ctx* c, const uint8_t* bytes, size_t len, size_t n, const size_t* blocks,
+                                 const size_t* offsets, size_t nblocks, uint32_t* out, uint32_t* counts) {
+    if (!c || (nblocks && (!blocks || !offsets || !out || !counts)) || (len && !bytes))
+        return BCGPU_ERR_INVALID_ARGUMENT;
+    if (nblocks == 0) return BCGPU_OK;
+    DeviceGuard g(c->device);
+    const size_t off_q = align_up(len, 256), off_o = off_q + 16 * nblocks, off_c = off_o + 16 * nblocks;
+    void* sp = nullptr;
+    int st = scratch(c, off_c + 4 * nblocks + 256, &sp);
+    if (st) return st;
+    uint8_t* d = static_cast<uint8_t*>(sp);
+    if (len) BC_CUDA(cudaMemcpyAsync(d, bytes, len, cudaMemcpyHostToDevice, c->stream));
+    static_assert(sizeof(size_t) == sizeof(uint64_t), "size_t must be 64-bit");
+    BC_CUDA(cudaMemcpyAsync(d + off_q, blocks, 8 * nblocks, cudaMemcpyHostToDevice, c->stream));
+    BC_CUDA(cudaMemcpyAsync(d + off_q + 8 * nblocks, offsets, 8 * nblocks, cudaMemcpyHostToDevice, c->stream));
+    st = bcgpu_svb_decode_blocks_device(c, d, len, n, reinterpret_cast<uint64_t*>(d + off_q),
+                                        reinterpret_cast<uint64_t*>(d + off_q + 8 * nblocks), nblocks,
+                                        reinterpret_cast<uint32_t*>(d + off_o), reinterpret_cast<uint32_t*>(d + off_c),
+                                        c->stream);
+    if (st) return st;
+    BC_CUDA(cudaMemcpyAsync(out, d + off_o, 16 * nblocks, cudaMemcpyDeviceToHost, c->stream));
+    BC_CUDA(cudaMemcpyAsync(counts, d + off_c, 4 * nblocks, cudaMemcpyDeviceToHost, c->stream));
+    BC_CUDA(cudaStreamSynchronize(c->stream));
+    return BCGPU_OK;
+}
+
+int bcgpu_svb_block_offsets_host(bcgpu_ctx* c, const uint8_t* bytes, size_t len, size_t n, uint64_t* offsets) {
+    if (!c || (n && (!bytes || !offsets))) return BCGPU_ERR_INVALID_ARGUMENT;
+    const size_t nctrl = (n + 3) / 4;
+    if (len < nctrl) return BCGPU_ERR_TRUNCATED;
+    if (n == 0) return BCGPU_OK;
+    DeviceGuard g(c->device);
+    const size_t off_o = align_up(nctrl, 256);
+    void* sp = nullptr;
+    int st = scratch(c, off_o + 8 * nctrl, &sp);
+    if (st) return st;
+    uint8_t* d = static_cast<uint8_t*>(sp);
+    BC_CUDA(cudaMemcpyAsync(d, bytes, nctrl, cudaMemcpyHostToDevice, c->stream));
+    st = bcgpu_svb_block_offsets_device(c, d, nctrl, n, reinterpret_cast<uint64_t*>(d + off_o), c->stream);
+    if (st) return st;
+    BC_CUDA(cudaMemcpyAsync(offsets, d + off_o, 8 * nctrl, cudaMemcpyDeviceToHost, c->stream));
+    BC_CUDA(cudaStreamSynchronize(c->stream));
+    return BCGPU_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,179 @@
+// bytecodec_host.cpp -- the reference's C++ API (namespace bytecodec) on top of
+// the C ABI.  Signatures: reference proj/core/include/bytecodec/codec.hpp:24-96
+// and stream_vbyte.hpp:32-54; semantics: SPEC.md:270-402.
+//
+// Each host thread owns one bcgpu_ctx per device (a ctx is single-stream).
+// Errors from the GPU path surface as codec_error{errc} exactly where the
+// reference would throw.
+#include <map>
+#include <memory>
+#include <mutex>
+#include <string>
+
+#include "bcgpu/bcgpu.h"
+#include "bytecodec/codec.hpp"
+#include "bytecodec/stream_vbyte.hpp"
+
+namespace bytecodec {
+namespace {
+
+thread_local int t_device = 0;
+
+struct CtxHolder {
+    std::map<int, bcgpu_ctx*> by_dev;
+    ~CtxHolder() {
+        for (auto& kv : by_dev) bcgpu_ctx_destroy(kv.second);
+    }
+};
+thread_local CtxHolder t_ctx;
+
+[[noreturn]] void throw_status(int st, const char* where) {
+    std::string msg = std::string(where) + ": " + bcgpu_status_string(st);
+    if (st >= 1 && st <= 15) throw codec_error(static_cast<errc>(st - 1), msg);
+    if (st == BCGPU_ERR_CUDA) msg += std::string(" (") + bcgpu_last_cuda_error() + ")";
+    throw std::runtime_error(msg);
+}
+
+bcgpu_ctx* ctx() {
+    auto it = t_ctx.by_dev.find(t_device);
+    if (it != t_ctx.by_dev.end()) return it->second;
+    bcgpu_ctx* c = nullptr;
+    const int st = bcgpu_ctx_create(t_device, &c);
+    if (st) throw_status(st, "bcgpu_ctx_create");
+    t_ctx.by_dev[t_device] = c;
+    return c;
+}
+
+void require_svb(codec_id id) {
+    if (id != codec_id::stream_vbyte)
+        throw codec_error(errc::unsupported, "only codec_id::stream_vbyte is implemented on the GPU path");
+}
+
+std::vector<uint8_t> encode_impl(std::span<const uint32_t> values, bool delta, uint32_t prev) {
+    std::vector<uint8_t> out(bcgpu_svb_max_compressed_bytes(values.size()));
+    size_t len = 0;
+    const int st = bcgpu_svb_encode_host(ctx(), values.data(), values.size(), delta ? 1 : 0, prev, out.data(),
+                                         out.size(), &len);
+    if (st) throw_status(st, "svb_encode");
+    out.resize(len);
+    out.shrink_to_fit();
+    return out;
+}
+
+}  // namespace
+
+void set_device(int device) { t_device = device; }
+
+std::string_view codec_name(codec_id id) {
+    switch (id) {
+        case codec_id::vbyte: return "vbyte";
+        case codec_id::varint_gb: return "varint-gb";
+        case codec_id::varint_g8iu: return "varint-g8iu";
+        case codec_id::stream_vbyte: return "stream-vbyte";
+    }
+    return "unknown";
+}
+
+std::optional<codec_id> codec_from_name(std::string_view name) {
+    for (uint8_t t = 0; t < 4; ++t)
+        if (codec_name(static_cast<codec_id>(t)) == name) return static_cast<codec_id>(t);
+    return std::nullopt;
+}
+
+std::optional<codec_id> codec_from_tag(uint8_t tag) {
+    if (tag < 4) return static_cast<codec_id>(tag);
+    return std::nullopt;
+}
+
+const decode_tables& svb_tables() {
+    static const decode_tables tables = [] {
+        decode_tables t{};
+        uint8_t len[256];
+        uint8_t shuf[256][16];
+        bcgpu_svb_tables(len, shuf);
+        for (int c = 0; c < 256; ++c) {
+            t.length[c] = len[c];
+            for (int i = 0; i < 16; ++i) t.shuffle[c][i] = shuf[c][i];
+        }
+        return t;
+    }();
+    return tables;
+}
+
+std::vector<uint8_t> svb_encode(std::span<const uint32_t> values) { return encode_impl(values, false, 0); }
+
+std::vector<uint8_t> svb_encode_delta(std::span<const uint32_t> values, uint32_t prev) {
+    return encode_impl(values, true, prev);
+}
+
+void svb_decode(std::span<const uint8_t> bytes, size_t n, uint32_t* out) {
+    const int st = bcgpu_svb_decode_host(ctx(), bytes.data(), bytes.size(), n, 0, 0, out, nullptr);
+    if (st) throw_status(st, "svb_decode");
+}
+
+std::vector<uint32_t> svb_decode(std::span<const uint8_t> bytes, size_t n) {
+    std::vector<uint32_t> out(n);
+    svb_decode(bytes, n, out.data());
+    return out;
+}
+
+uint32_t svb_decode_delta(std::span<const uint8_t> bytes, size_t n, uint32_t base, uint32_t* out) {
+    uint32_t last = base;
+    const int st = bcgpu_svb_decode_host(ctx(), bytes.data(), bytes.size(), n, 1, base, out, &last);
+    if (st) throw_status(st, "svb_decode_delta");
+    return last;
+}
+
+std::vector<size_t> svb_block_data_offsets(std::span<const uint8_t> bytes, size_t n) {
+    std::vector<uint64_t> tmp(svb_control_bytes(n));
+    const int st = bcgpu_svb_block_offsets_host(ctx(), bytes.data(), bytes.size(), n, tmp.data());
+    if (st) throw_status(st, "svb_block_data_offsets");
+    return std::vector<size_t>(tmp.begin(), tmp.end());
+}
+
+size_t svb_decode_block(std::span<const uint8_t> bytes, size_t n, size_t block, size_t data_offset,
+                        uint32_t out[4]) {
+    uint32_t cnt = 0;
+    const int st = bcgpu_svb_decode_blocks_host(ctx(), bytes.data(), bytes.size(), n, &block, &data_offset, 1, out,
+                                                &cnt);
+    if (st) throw_status(st, "svb_decode_block");
+    return cnt;
+}
+
+std::vector<uint8_t> encode_payload(codec_id id, std::span<const uint32_t> values) {
+    require_svb(id);
+    return svb_encode(values);
+}
+
+void decode_payload(codec_id id, std::span<const uint8_t> bytes, size_t n, uint32_t* out) {
+    require_svb(id);
+    svb_decode(bytes, n, out);
+}
+
+uint32_t decode_payload_delta(codec_id id, std::span<const uint8_t> bytes, size_t n, uint32_t base, uint32_t* out) {
+    require_svb(id);
+    return svb_decode_delta(bytes, n, base, out);
+}
+
+encoded_buffer encode(codec_id id, std::span<const uint32_t> values, bool delta) {
+    require_svb(id);
+    if (values.size() > 0xFFFFFFFFull) throw codec_error(errc::out_of_range, "count exceeds uint32");
+    encoded_buffer b;
+    b.codec = id;
+    b.count = static_cast<uint32_t>(values.size());
+    b.delta = delta;
+    b.bytes = encode_impl(values, delta, 0);  // base 0
+    return b;
+}
+
+std::vector<uint32_t> decode(const encoded_buffer& buf) {
+    require_svb(buf.codec);
+    std::vector<uint32_t> out(buf.count);
+    if (buf.delta)
+        svb_decode_delta(buf.bytes, buf.count, 0, out.data());
+    else
+        svb_decode(buf.bytes, buf.count, out.data());
+    return out;
+}
+
+}  // namespace bytecodec

@@ -1,0 +1,289 @@
+"""GPU parity: the sm_100a kernels, called through the C ABI, against the pinned
+CPU oracle on identical seeded inputs.  Bit-exact for compressed bytes and
+decoded integers (integer/byte work: no tolerance)."""
+import json
+
+import numpy as np
+import pytest
+
+import oracle
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def P():
+    import paper_1709_08990_b200 as P
+    return P
+
+
+@pytest.fixture(scope="module")
+def dev():
+    from paper_1709_08990_b200.device import DeviceCodec
+    return DeviceCodec(0)
+
+
+def _mixed(rng, n, classes=(0, 1, 2, 3)):
+    k = rng.choice(np.array(classes), n)
+    lo = np.where(k == 0, 0, 1 << (8 * k)).astype(np.uint64)
+    span = ((1 << (8 * (k + 1))) - lo).astype(np.uint64)
+    return (lo + (rng.integers(0, 2**62, n, dtype=np.uint64) % span)).astype(np.uint32)
+
+
+def _check_roundtrip(P, v, delta=False, prev=0):
+    want = oracle.encode(v, delta=delta, prev=prev)
+    got = P.svb_encode_delta(v, prev) if delta else P.svb_encode(v)
+    assert got == want, f"encode mismatch n={v.size} delta={delta}"
+    out = np.empty(v.size, np.uint32)
+    if delta:
+        last = P.svb_decode_delta(want, v.size, prev, out)
+        assert last == (int(v[-1]) if v.size else prev)
+    else:
+        P.svb_decode(want, v.size, out)
+    assert np.array_equal(out, v), f"decode mismatch n={v.size} delta={delta}"
+
+
+# ---- SPEC golden vectors through the reference-shaped API -------------------
+def test_spec_vectors(P, golden_dir):
+    spec = json.loads((golden_dir / "spec_vectors.json").read_text())
+    for case in spec["encode"]["cases"]:
+        assert list(P.svb_encode(np.array(case["values"], np.uint32))) == case["bytes"]
+    for case in spec["decode"]["cases"]:
+        assert list(P.svb_decode(bytes(case["bytes"]), case["n"])) == case["values"]
+    for src, want in spec["delta_encode"]["cases"]:
+        # delta encode of src with base 0 == plain encode of the deltas
+        assert P.svb_encode_delta(np.array(src, np.uint32), 0) == oracle.encode(np.array(want, np.uint32))
+    for src, base, want in spec["prefix_sum"]["cases"]:
+        out = np.empty(4, np.uint32)
+        last = P.svb_decode_delta(oracle.encode(np.array(src, np.uint32)), 4, base, out)
+        assert list(out) == want and last == want[-1]
+    buf = P.encode(P.codec_id.stream_vbyte, np.array([3, 7, 19, 20], np.uint32), delta=True)
+    assert buf.count == 4 and buf.delta and list(P.decode(buf)) == [3, 7, 19, 20]
+
+
+def test_size_identity_10_bits(P):
+    v = np.random.default_rng(3).integers(128, 256, 1000, dtype=np.uint32)
+    assert len(P.svb_encode(v)) * 8 / 1000 == 10.0
+
+
+# ---- random property round trips (acceptance 1) ----------------
+def test_random_roundtrips(P):
+    rng = np.random.default_rng(42)
+    sizes = list(range(0, 70)) + [127, 128, 129, 1000, 4095, 4096, 4097, 8191, 8192, 8193, 10000, 16383,
+                                  16384, 16385, 24577, 65536, 100003]
+    for i, n in enumerate(sizes):
+        v = _mixed(rng, n)
+        _check_roundtrip(P, v, delta=False)
+        _check_roundtrip(P, v, delta=True, prev=int(rng.integers(0, 2**32)) if i % 2 else 0)
+
+
+@pytest.mark.parametrize("classes", [(0,), (1,), (2,), (3,), (0, 3), (0, 1)])
+def test_adversarial_classes(P, classes):
+    """all-0x00 / all-0xFF / alternating control streams, every length boundary."""
+    rng = np.random.default_rng(sum(classes) + 17)
+    for n in (1, 3, 4, 5, 8191, 8192, 8193, 40000):
+        _check_roundtrip(P, _mixed(rng, n, classes))
+        _check_roundtrip(P, np.sort(_mixed(rng, n, classes)), delta=True)
+
+
+def test_length_boundaries(P):
+    b = []
+    for e in (8, 16, 24):
+        b += [(1 << e) - 2, (1 << e) - 1, 1 << e, (1 << e) + 1]
+    v = np.array(b * 300 + [0, 1, 2**32 - 1], np.uint32)
+    _check_roundtrip(P, v)
+    _check_roundtrip(P, v, delta=True, prev=2**32 - 1)  # prev > x_0: wraps
+
+
+def test_malformed(P):
+    v = np.arange(1, 100000, 7, dtype=np.uint32) * 977
+    enc = P.svb_encode(v)
+    out = np.empty(v.size, np.uint32)
+    with pytest.raises(P.CodecError) as e:
+        P.svb_decode(enc[:-1], v.size, out)
+    assert e.value.code == P.errc.truncated
+    with pytest.raises(P.CodecError) as e:
+        P.svb_decode(enc + b"\x00\x01", v.size, out)
+    assert e.value.code == P.errc.trailing_bytes
+    with pytest.raises(P.CodecError) as e:
+        P.svb_decode(enc[:10], v.size, out)
+    assert e.value.code == P.errc.truncated
+    with pytest.raises(P.CodecError) as e:
+        P.encode(P.codec_id.vbyte, v)
+    assert e.value.code == P.errc.unsupported
+    # a truncated stream cut deep inside: guarded reads, error reported
+    with pytest.raises(P.CodecError):
+        P.svb_decode(enc[: len(enc) // 2], v.size, out)
+
+
+# ---- device API: misaligned buffers, offsets, blocks -------------------------
+def test_device_misaligned_pointers(P, dev):
+    import torch
+    rng = np.random.default_rng(8)
+    for n in (5, 1001, 20011):
+        v = _mixed(rng, n)
+        want = oracle.encode(v, delta=True, prev=99)
+        for shift_in in (0, 1, 4, 7):
+            for shift_out in (0, 1, 3):
+                src = torch.zeros(n + 8, dtype=torch.int32, device="cuda")
+                src[shift_out:shift_out + n] = torch.from_numpy(v.view(np.int32)).cuda()
+                cap = (n + 3) // 4 + 4 * n
+                outb = torch.zeros(cap + 16, dtype=torch.uint8, device="cuda")
+                olen = torch.zeros(1, dtype=torch.int64, device="cuda")
+                dev.encode(src[shift_out:shift_out + n], outb[shift_in:shift_in + cap], olen, delta=True, prev=99)
+                m = int(olen.item())
+                assert m == len(want)
+                assert outb[shift_in:shift_in + m].cpu().numpy().tobytes() == want
+                # decode from a misaligned input into a misaligned output
+                dec = torch.zeros(n + 8, dtype=torch.int32, device="cuda")
+                last = torch.zeros(1, dtype=torch.int32, device="cuda")
+                dev.decode(outb[shift_in:shift_in + m], n, dec[shift_out:shift_out + n], delta=True, base=99,
+                           last=last)
+                dev.check()
+                assert np.array_equal(dec[shift_out:shift_out + n].cpu().numpy().view(np.uint32), v)
+                assert (int(last.item()) & 0xFFFFFFFF) == int(v[-1])
+
+
+def test_block_offsets_and_random_access(P):
+    rng = np.random.default_rng(21)
+    for n in (1, 3, 4, 7, 8192 * 3 + 5, 100001):
+        v = _mixed(rng, n)
+        enc = oracle.encode(v)
+        want = oracle.block_data_offsets(enc, n)
+        got = P.svb_block_data_offsets(enc, n)
+        assert np.array_equal(got, want)
+        ks = rng.integers(0, len(want), min(2000, len(want)))
+        vals, cnts = P.svb_decode_blocks(enc, n, ks, want[ks])
+        for j, k in enumerate(ks):
+            ref = oracle.decode_block(enc, n, int(k), int(want[k]))
+            assert cnts[j] == len(ref) and list(vals[j, :cnts[j]]) == list(ref)
+    assert list(P.svb_decode_block(oracle.encode(np.array([1, 2, 300], np.uint32)), 3, 0, 0)) == [1, 2, 300]
+
+
+# ---- BASELINE.json configs (scaled where the oracle needs it) ---------------
+def test_config1_full(P):
+    from paper_1709_08990_b200 import gen
+    v = gen.config_array(1)  # 2^20, the reference's CPU-runnable config
+    _check_roundtrip(P, v)
+
+
+def test_config2_scaled(P):
+    from paper_1709_08990_b200 import gen
+    v = gen.config_array(2, 1 << 22)
+    _check_roundtrip(P, v, delta=True, prev=0)
+
+
+def test_config3_scaled(P):
+    from paper_1709_08990_b200 import gen
+    v = gen.config_array(3, 1 << 23)
+    _check_roundtrip(P, v)
+
+
+def _batch_decode_check(dev, values_list, prevs, delta, max_hint):
+    import torch
+    from paper_1709_08990_b200.device import DECODE_SEG_DTYPE, ENCODE_SEG_DTYPE, segments_to_tensor
+    encs = [oracle.encode(v, delta=delta, prev=p) for v, p in zip(values_list, prevs)]
+    nseg = len(values_list)
+    segs = np.zeros(nseg, DECODE_SEG_DTYPE)
+    src_off = np.concatenate([[0], np.cumsum([len(e) for e in encs])])
+    dst_off = np.concatenate([[0], np.cumsum([v.size for v in values_list])])
+    segs["src_offset"], segs["src_bytes"] = src_off[:-1], np.diff(src_off)
+    segs["dst_offset"], segs["n"], segs["prev"] = dst_off[:-1], [v.size for v in values_list], prevs
+    blob = np.frombuffer(b"".join(encs), np.uint8)
+    d_in = torch.from_numpy(blob.copy()).cuda()
+    d_out = torch.zeros(int(dst_off[-1]) + 1, dtype=torch.int32, device="cuda")
+    d_segs = segments_to_tensor(segs, "cuda")
+    dev.decode_batch(d_segs, nseg, d_in, d_out, delta=delta, max_seg_n=max_hint)
+    dev.check()
+    got = d_out.cpu().numpy().view(np.uint32)
+    assert np.array_equal(got[: dst_off[-1]], np.concatenate(values_list))
+    # encode batch into worst-case slots, then compare every segment's bytes
+    esegs = np.zeros(nseg, ENCODE_SEG_DTYPE)
+    caps = np.array([(v.size + 3) // 4 + 4 * v.size for v in values_list], np.uint64)
+    eoff = np.concatenate([[0], np.cumsum(caps)])
+    esegs["src_offset"], esegs["dst_capacity"], esegs["dst_offset"] = dst_off[:-1], caps, eoff[:-1]
+    esegs["n"], esegs["prev"] = [v.size for v in values_list], prevs
+    d_vals = torch.from_numpy(np.concatenate(values_list).view(np.int32).copy()).cuda()
+    d_enc = torch.zeros(int(eoff[-1]) + 16, dtype=torch.uint8, device="cuda")
+    d_lens = torch.zeros(nseg, dtype=torch.int64, device="cuda")
+    d_esegs = segments_to_tensor(esegs, "cuda")
+    dev.encode_batch(d_esegs, nseg, d_vals, d_enc, d_lens, delta=delta, max_seg_n=max_hint)
+    d_sizes = torch.zeros(nseg, dtype=torch.int64, device="cuda")
+    dev.encoded_sizes_batch(d_esegs, nseg, d_vals, d_sizes, delta=delta)
+    dev.check()
+    lens = d_lens.cpu().numpy()
+    assert np.array_equal(lens, [len(e) for e in encs])
+    assert np.array_equal(d_sizes.cpu().numpy(), lens)
+    enc_host = d_enc.cpu().numpy()
+    for i, e in enumerate(encs):
+        assert enc_host[int(eoff[i]): int(eoff[i]) + len(e)].tobytes() == e, i
+
+
+def test_batch_config4_scaled(dev):
+    from paper_1709_08990_b200 import gen
+    lb = gen.posting_lists(3000, 4, cap_total=3000 * 1875)
+    lists = [lb.values[int(lb.offsets[i]):int(lb.offsets[i + 1])] for i in range(3000)]
+    _batch_decode_check(dev, lists, [0] * len(lists), True, int(lb.lengths.max()))
+
+
+def test_batch_config5_scaled(dev):
+    from paper_1709_08990_b200 import gen
+    seq = gen.geometric_sorted(24 * 65536, 32.0, 5)
+    chunks = [seq[i * 65536:(i + 1) * 65536] for i in range(24)]
+    prevs = [0] + [int(c[-1]) for c in chunks[:-1]]
+    _batch_decode_check(dev, chunks, prevs, True, 65536)
+
+
+def test_batch_mixed_sizes(dev):
+    rng = np.random.default_rng(77)
+    sizes = [0, 1, 2, 3, 4, 5, 31, 128, 129, 4095, 4096, 4097, 5000, 8192, 8193, 20000, 70001, 17, 3]
+    lists = [_mixed(rng, int(n)) for n in sizes]
+    prevs = [int(rng.integers(0, 2**32)) for _ in sizes]
+    _batch_decode_check(dev, lists, prevs, True, 0)
+    _batch_decode_check(dev, lists, [0] * len(sizes), False, max(sizes))
+
+
+# ---- full BASELINE sizes: size-independent properties -----------------------
+@pytest.mark.slow
+def test_config2_full_roundtrip(dev):
+    """64M delta: GPU encode == O1 encode bytes (digest), GPU decode round trip exact."""
+    import hashlib
+
+    import torch
+    from paper_1709_08990_b200 import gen
+    v = gen.config_array(2)
+    want = oracle.encode(v, delta=True, prev=0)
+    d_v = torch.from_numpy(v.view(np.int32)).cuda()
+    cap = (v.size + 3) // 4 + 4 * v.size
+    d_c = torch.empty(cap, dtype=torch.uint8, device="cuda")
+    d_len = torch.zeros(1, dtype=torch.int64, device="cuda")
+    dev.encode(d_v, d_c, d_len, delta=True, prev=0)
+    m = int(d_len.item())
+    assert m == len(want)
+    assert hashlib.sha256(d_c[:m].cpu().numpy().tobytes()).hexdigest() == hashlib.sha256(want).hexdigest()
+    d_o = torch.empty_like(d_v)
+    dev.decode(d_c, v.size, d_o, in_len=m, delta=True, base=0)
+    dev.check()
+    assert torch.equal(d_o, d_v)
+
+
+@pytest.mark.slow
+def test_config3_full_roundtrip(dev):
+    import hashlib
+
+    import torch
+    from paper_1709_08990_b200 import gen
+    v = gen.config_array(3)
+    want = oracle.encode(v)
+    d_v = torch.from_numpy(v.view(np.int32)).cuda()
+    cap = (v.size + 3) // 4 + 4 * v.size
+    d_c = torch.empty(cap, dtype=torch.uint8, device="cuda")
+    d_len = torch.zeros(1, dtype=torch.int64, device="cuda")
+    dev.encode(d_v, d_c, d_len)
+    m = int(d_len.item())
+    assert m == len(want)
+    assert hashlib.sha256(d_c[:m].cpu().numpy().tobytes()).hexdigest() == hashlib.sha256(want).hexdigest()
+    d_o = torch.empty_like(d_v)
+    dev.decode(d_c, v.size, d_o, in_len=m)
+    dev.check()
+    assert torch.equal(d_o, d_v)
