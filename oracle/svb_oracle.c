@@ -408,8 +408,9 @@ static void mt_enc_fn(void *p, int t, int nt) {
             prev = x;
             uint32_t len = svbo_byte_length(v);
             ctrl[(i - lo) / 4] |= (uint8_t)((len - 1) << (2 * ((i - lo) % 4)));
-            if (i + 1 < hi) {
-                memcpy(data, &v, 4); /* little-endian host; the spill is overwritten by the next int */
+            if (i + 3 < hi) {
+                /* little-endian host; the <=3-byte spill lands on the next 3 ints, which are in this chunk */
+                memcpy(data, &v, 4);
             } else {
                 for (uint32_t b = 0; b < len; ++b) data[b] = (uint8_t)(v >> (8 * b)); /* chunk seam: exact */
             }

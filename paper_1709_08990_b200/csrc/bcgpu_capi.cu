@@ -58,18 +58,25 @@ struct bcgpu_ctx {
     uint32_t epoch = 0;
     unsigned long long ticket_base = 0;
     uint32_t last_epoch = 0;  // epoch of the last *_device call
-    // batch grid sizes
-    int warp_grid = 0, dec_cta_grid = 0, enc_cta_grid = 0;
+    unsigned long long* trace = nullptr;  // debug phase trace (bcgpu_debug_set_trace)
+    uint32_t debug_flags = 0;
+    // batch kernels: CTAs for full residency
+    int batch_grid = 0;
     // host-API scratch (device) and stream
     cudaStream_t stream = nullptr;
+    uint64_t* offs = nullptr;  // decode: per-sub-tile data offsets
+    size_t offs_cap = 0;
     void* d_scratch = nullptr;
     size_t d_scratch_cap = 0;
 };
 
 static unsigned long long* ticket_ptr(bcgpu_ctx* c) { return c->ws; }
 static unsigned long long* status_ptr(bcgpu_ctx* c) { return c->ws + 1; }
-static uint64_t* off_status(bcgpu_ctx* c) { return reinterpret_cast<uint64_t*>(c->ws + 2); }
-static uint64_t* sum_status(bcgpu_ctx* c) { return reinterpret_cast<uint64_t*>(c->ws + 2 + c->ws_tiles); }
+// status arrays hold one word per kStatusStride u64 (64 B) per tile
+static uint64_t* off_status(bcgpu_ctx* c) { return reinterpret_cast<uint64_t*>(c->ws + 16); }
+static uint64_t* sum_status(bcgpu_ctx* c) {
+    return reinterpret_cast<uint64_t*>(c->ws + 16 + kStatusStride * c->ws_tiles);
+}
 
 static int ensure_ws(bcgpu_ctx* c, size_t tiles) {
     if (tiles < 1024) tiles = 1024;
@@ -81,7 +88,7 @@ static int ensure_ws(bcgpu_ctx* c, size_t tiles) {
         BC_CUDA(cudaFree(c->ws));
         c->ws = nullptr;
     }
-    const size_t bytes = (2 + 2 * cap) * sizeof(unsigned long long);
+    const size_t bytes = (16 + 2 * kStatusStride * cap) * sizeof(unsigned long long);
     BC_CUDA(cudaMalloc(&c->ws, bytes));
     BC_CUDA(cudaMemset(c->ws, 0, bytes));
     c->ws_tiles = cap;
@@ -93,7 +100,7 @@ static int ensure_ws(bcgpu_ctx* c, size_t tiles) {
 // Next launch epoch; status words of older launches never match it.
 static int next_epoch(bcgpu_ctx* c, cudaStream_t s) {
     if (c->epoch >= kEpochMax) {
-        BC_CUDA(cudaMemsetAsync(c->ws + 1, 0, (1 + 2 * c->ws_tiles) * sizeof(unsigned long long), s));
+        BC_CUDA(cudaMemsetAsync(c->ws + 1, 0, (15 + 2 * kStatusStride * c->ws_tiles) * sizeof(unsigned long long), s));
         c->epoch = 0;
     }
     c->epoch += 1;
@@ -101,20 +108,19 @@ static int next_epoch(bcgpu_ctx* c, cudaStream_t s) {
     return BCGPU_OK;
 }
 
-static int make_lookback(bcgpu_ctx* c, uint64_t ngroups, cudaStream_t s, LookbackArgs* lb) {
-    const size_t tiles = (ngroups + kTileGroups - 1) / kTileGroups;
+static int make_lookback(bcgpu_ctx* c, uint64_t ngroups, uint32_t tile_groups, cudaStream_t s, LookbackArgs* lb) {
+    const size_t tiles = (ngroups + tile_groups - 1) / tile_groups;
     int st = ensure_ws(c, tiles);
     if (st) return st;
     st = next_epoch(c, s);
     if (st) return st;
+    lb->trace = c->trace;
+    lb->debug_flags = c->debug_flags;
     lb->off_status = off_status(c);
     lb->sum_status = sum_status(c);
-    lb->ticket = ticket_ptr(c);
-    lb->ticket_base = c->ticket_base;
     lb->epoch = c->epoch;
     lb->num_tiles = (uint32_t)tiles;
     lb->status = status_ptr(c);
-    c->ticket_base += tiles;
     return BCGPU_OK;
 }
 
@@ -125,8 +131,7 @@ static int make_batch(bcgpu_ctx* c, cudaStream_t s, BatchArgs* ba) {
     if (st) return st;
     ba->status = status_ptr(c);
     ba->epoch = c->epoch;
-    ba->warp_grid = c->warp_grid;
-    ba->cta_grid = c->dec_cta_grid;
+    ba->grid = c->batch_grid;
     return BCGPU_OK;
 }
 
@@ -134,6 +139,20 @@ static int make_batch(bcgpu_ctx* c, cudaStream_t s, BatchArgs* ba) {
 extern "C" {
 
 int bcgpu_abi_version(void) { return BCGPU_ABI_VERSION; }
+
+// Debug only (not in bcgpu.h): route per-tile phase timestamps (8 x u64 per
+// look-back tile, %globaltimer ns) of the single-array kernels to d_trace.
+int bcgpu_debug_set_trace(bcgpu_ctx* c, void* d_trace) {
+    if (!c) return BCGPU_ERR_INVALID_ARGUMENT;
+    c->trace = static_cast<unsigned long long*>(d_trace);
+    return BCGPU_OK;
+}
+
+int bcgpu_debug_set_flags(bcgpu_ctx* c, uint32_t flags) {
+    if (!c) return BCGPU_ERR_INVALID_ARGUMENT;
+    c->debug_flags = flags;
+    return BCGPU_OK;
+}
 
 const char* bcgpu_last_cuda_error(void) { return g_cuda_err; }
 
@@ -195,9 +214,7 @@ int bcgpu_ctx_create(int device, bcgpu_ctx** out) {
     if (!c) return BCGPU_ERR_INVALID_ARGUMENT;
     c->device = device;
     cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, device);
-    c->warp_grid = c->num_sms * occupancy_decode_batch_warp();
-    c->dec_cta_grid = c->num_sms * occupancy_decode_batch_cta();
-    c->enc_cta_grid = c->num_sms * occupancy_encode_batch_cta();
+    c->batch_grid = c->num_sms * occupancy_batch();
     cudaError_t e = cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking);
     if (e != cudaSuccess) {
         delete c;
@@ -219,6 +236,7 @@ int bcgpu_ctx_destroy(bcgpu_ctx* c) {
     cudaDeviceSynchronize();
     if (c->ws) cudaFree(c->ws);
     if (c->d_scratch) cudaFree(c->d_scratch);
+    if (c->offs) cudaFree(c->offs);
     if (c->stream) cudaStreamDestroy(c->stream);
     delete c;
     return BCGPU_OK;
@@ -249,7 +267,7 @@ int bcgpu_svb_encode_device(bcgpu_ctx* c, const uint32_t* d_in, size_t n, int de
         return BCGPU_OK;
     }
     LookbackArgs lb;
-    int st = make_lookback(c, (n + 3) / 4, s, &lb);
+    int st = make_lookback(c, (n + 3) / 4, kEncodeTileGroups, s, &lb);
     if (st) return st;
     BC_CUDA(launch_encode(d_in, n, delta, prev, d_out, d_out_len, lb, s));
     g_launches.fetch_add(1);
@@ -268,11 +286,34 @@ int bcgpu_svb_decode_device(bcgpu_ctx* c, const uint8_t* d_in, size_t in_len, si
         if (in_len != 0) return BCGPU_ERR_TRAILING_BYTES;
         return BCGPU_OK;
     }
-    LookbackArgs lb;
-    int st = make_lookback(c, nctrl, s, &lb);
+    const size_t words = decode2_offsets_words(n);
+    if (words > c->offs_cap) {
+        if (c->offs) {
+            BC_CUDA(cudaStreamSynchronize(s));
+            BC_CUDA(cudaFree(c->offs));
+            c->offs = nullptr;
+        }
+        size_t cap = words + words / 4 + 64;
+        BC_CUDA(cudaMalloc(&c->offs, cap * sizeof(uint64_t)));
+        c->offs_cap = cap;
+    }
+    const uint32_t chunks = decode2_chunks(n), tiles = decode2_tiles(n);
+    int st = ensure_ws(c, chunks > tiles ? chunks : tiles);
     if (st) return st;
-    BC_CUDA(launch_decode(d_in, in_len, n, delta, base, d_out, d_last, lb, s));
-    g_launches.fetch_add(1);
+    st = next_epoch(c, s);
+    if (st) return st;
+    LookbackArgs lb{};
+    lb.off_status = off_status(c);
+    lb.sum_status = sum_status(c);
+    lb.trace = c->trace;
+    lb.debug_flags = c->debug_flags;
+    lb.epoch = c->epoch;
+    lb.status = status_ptr(c);
+    LookbackArgs lb1 = lb, lb2 = lb;
+    lb1.num_tiles = chunks;
+    lb2.num_tiles = tiles;
+    BC_CUDA(launch_decode2(d_in, in_len, n, delta, base, d_out, d_last, c->offs, lb1, lb2, s));
+    g_launches.fetch_add(2);
     return BCGPU_OK;
 }
 
@@ -285,7 +326,7 @@ int bcgpu_svb_block_offsets_device(bcgpu_ctx* c, const uint8_t* d_in, size_t in_
     DeviceGuard g(c->device);
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     LookbackArgs lb;
-    int st = make_lookback(c, nctrl, s, &lb);
+    int st = make_lookback(c, nctrl, kOffsetsTileGroups, s, &lb);
     if (st) return st;
     BC_CUDA(launch_block_offsets(d_in, n, d_offsets, lb, s));
     g_launches.fetch_add(1);
@@ -313,10 +354,9 @@ int bcgpu_svb_decode_batch_device(bcgpu_ctx* c, const bcgpu_decode_segment* d_se
     BatchArgs ba;
     int st = make_batch(c, s, &ba);
     if (st) return st;
-    ba.cta_grid = c->dec_cta_grid;
-    int launches = 0;
-    BC_CUDA(launch_decode_batch(d_segs, nseg, d_in, d_out, delta, max_seg_n, ba, s, &launches));
-    g_launches.fetch_add((uint64_t)launches);
+    (void)max_seg_n;  // reserved hint: one warp-per-segment kernel serves every size
+    BC_CUDA(launch_decode_batch(d_segs, nseg, d_in, d_out, delta, ba, s));
+    g_launches.fetch_add(1);
     return BCGPU_OK;
 }
 
@@ -329,10 +369,9 @@ int bcgpu_svb_encode_batch_device(bcgpu_ctx* c, const bcgpu_encode_segment* d_se
     BatchArgs ba;
     int st = make_batch(c, s, &ba);
     if (st) return st;
-    ba.cta_grid = c->enc_cta_grid;
-    int launches = 0;
-    BC_CUDA(launch_encode_batch(d_segs, nseg, d_in, d_out, d_out_lens, delta, max_seg_n, ba, s, &launches));
-    g_launches.fetch_add((uint64_t)launches);
+    (void)max_seg_n;
+    BC_CUDA(launch_encode_batch(d_segs, nseg, d_in, d_out, d_out_lens, delta, ba, s));
+    g_launches.fetch_add(1);
     return BCGPU_OK;
 }
 

@@ -97,6 +97,86 @@ __device__ __forceinline__ uint64_t lookback_exclusive(const uint64_t* status, u
     return excl;
 }
 
+// Status words are spread one per 64 B (kStatusStride u64) so the ~256 newest
+// ones -- which every in-flight look-back polls -- land in many L2 slices
+// instead of hammering a few lines.
+constexpr int kStatusStride = 1;
+
+__device__ __forceinline__ uint64_t* status_slot(uint64_t* base, uint64_t tile) { return base + tile * kStatusStride; }
+__device__ __forceinline__ const uint64_t* status_slot(const uint64_t* base, uint64_t tile) {
+    return base + tile * kStatusStride;
+}
+
+// Wide decoupled look-back: each lane inspects 8 consecutive predecessors, so
+// one warp round trip covers 256 tiles.  Only entries not yet published are
+// re-polled, with exponential back-off.  Returns the exclusive prefix of `tile`.
+__device__ __forceinline__ uint64_t lookback_exclusive_wide(const uint64_t* status, uint32_t tile, uint32_t epoch,
+                                                            uint32_t* stats = nullptr) {
+    const int lane = threadIdx.x & 31;
+    uint64_t excl = 0;
+    int64_t top = (int64_t)tile - 1;
+    uint32_t spins = 0, rounds = 0;
+    unsigned long long t_first = 0, t_begin = 0;
+    if (stats) asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t_begin));
+    while (true) {
+        ++rounds;
+        uint64_t v[8];
+        uint32_t f[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) f[i] = 0, v[i] = 0;
+        uint32_t sleep_ns = 32;
+        while (true) {
+            bool ok = true;
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+                if (f[i] == 0) {
+                    const int64_t idx = top - 8 * lane - i;
+                    if (idx >= 0) {
+                        const uint64_t s = ld_relaxed_gpu(status_slot(status, (uint64_t)idx));
+                        f[i] = ((uint32_t)(s >> kEpochShift) == epoch) ? (uint32_t)((s >> kFlagShift) & 3u) : 0u;
+                        v[i] = s & kValueMask;
+                    } else {
+                        f[i] = kFlagInclusive;
+                        v[i] = 0;
+                    }
+                }
+                ok = ok && f[i] != 0;
+            }
+            if (stats && t_first == 0) {
+                uint64_t dep = 0;
+#pragma unroll
+                for (int i = 0; i < 8; ++i) dep += v[i] + f[i];
+                asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t_first) : "l"(dep));
+            }
+            if (__all_sync(kFull, ok)) break;
+            ++spins;
+            __nanosleep(sleep_ns);
+            sleep_ns = sleep_ns < 512 ? 2 * sleep_ns : 512;
+        }
+        int first = 8;
+#pragma unroll
+        for (int i = 7; i >= 0; --i)
+            if (f[i] == kFlagInclusive) first = i;
+        const unsigned m = __ballot_sync(kFull, first < 8);
+        const int fl = m ? __ffs(m) - 1 : 32;
+        uint64_t contrib = 0;
+#pragma unroll
+        for (int i = 0; i < 8; ++i)
+            if (lane < fl || (lane == fl && i <= first)) contrib += v[i];
+#pragma unroll
+        for (int o = 16; o; o >>= 1) contrib += __shfl_xor_sync(kFull, contrib, o);
+        excl += contrib;
+        if (m) break;
+        top -= 256;
+    }
+    if (stats) {
+        stats[0] = spins;
+        stats[1] = rounds;
+        stats[2] = (uint32_t)(t_first - t_begin);
+    }
+    return excl;
+}
+
 // ---- scans -------------------------------------------------------------
 __device__ __forceinline__ uint32_t warp_inclusive_scan(uint32_t v) {
     const int lane = threadIdx.x & 31;

@@ -12,16 +12,22 @@ namespace bcgpu {
 struct LookbackArgs {
     uint64_t* off_status;          // per-tile byte-offset status words
     uint64_t* sum_status;          // per-tile delta-sum status words
-    unsigned long long* ticket;    // monotonically increasing tile ticket
-    unsigned long long ticket_base;
+    unsigned long long* trace;     // debug: per-tile phase timestamps (nullptr = off)
+    uint32_t debug_flags;          // debug: bit0 = skip output stores (timing experiments only)
     uint32_t epoch;
     uint32_t num_tiles;
     unsigned long long* status;    // [epoch:32 | bcgpu_status:32] of the last call
 };
 
 // Launchers (return cudaError_t of the launch).
-cudaError_t launch_decode(const uint8_t* in, uint64_t in_len, uint64_t n, int delta, uint32_t base, uint32_t* out,
-                          uint32_t* d_last, const LookbackArgs& lb, cudaStream_t stream);
+// Single-array decode = sub-tile offsets pre-pass + tile decode (svb_decode.cu);
+// offs must hold decode2_offsets_words(n) u64, 16-B aligned.
+cudaError_t launch_decode2(const uint8_t* in, uint64_t in_len, uint64_t n, int delta, uint32_t base, uint32_t* out,
+                           uint32_t* d_last, uint64_t* offs, const LookbackArgs& lb_offs, const LookbackArgs& lb_dec,
+                           cudaStream_t stream);
+uint64_t decode2_offsets_words(uint64_t n);
+uint32_t decode2_chunks(uint64_t n);  // look-back tiles of the offsets pre-pass
+uint32_t decode2_tiles(uint64_t n);   // look-back tiles (CTAs) of the tile decode
 cudaError_t launch_encode(const uint32_t* in, uint64_t n, int delta, uint32_t prev, uint8_t* out,
                           uint64_t* d_out_len, const LookbackArgs& lb, cudaStream_t stream);
 cudaError_t launch_block_offsets(const uint8_t* in, uint64_t n, uint64_t* d_offsets, const LookbackArgs& lb,
@@ -34,28 +40,22 @@ cudaError_t launch_decode_blocks(const uint8_t* in, uint64_t in_len, uint64_t n,
 struct BatchArgs {
     unsigned long long* status;  // [epoch:32 | bcgpu_status:32]
     uint32_t epoch;
-    int warp_grid;               // CTAs for the warp-per-segment kernel
-    int cta_grid;                // CTAs for the CTA-per-segment kernel
+    int grid;                    // CTAs of the warp-per-segment kernels (full residency)
 };
 
-// Segments with n <= warp_max go to the warp-per-segment kernel, larger ones
-// to the CTA-per-segment kernel; either launch is skipped when the hint says
-// it has no work.
 cudaError_t launch_decode_batch(const bcgpu_decode_segment* segs, uint64_t nseg, const uint8_t* in, uint32_t* out,
-                                int delta, uint32_t max_seg_n, const BatchArgs& ba, cudaStream_t stream,
-                                int* launches);
+                                int delta, const BatchArgs& ba, cudaStream_t stream);
 cudaError_t launch_encode_batch(const bcgpu_encode_segment* segs, uint64_t nseg, const uint32_t* in, uint8_t* out,
-                                uint64_t* out_lens, int delta, uint32_t max_seg_n, const BatchArgs& ba,
-                                cudaStream_t stream, int* launches);
+                                uint64_t* out_lens, int delta, const BatchArgs& ba, cudaStream_t stream);
 cudaError_t launch_sizes_batch(const bcgpu_encode_segment* segs, uint64_t nseg, const uint32_t* in,
                                uint64_t* out_lens, int delta, const BatchArgs& ba, cudaStream_t stream);
 
-// Occupancy (CTAs per SM) of each kernel family, for grid sizing.
-int occupancy_decode_batch_cta();
-int occupancy_decode_batch_warp();
-int occupancy_encode_batch_cta();
-int occupancy_encode_batch_warp();
+// CTAs per SM of the batch kernels, for grid sizing.
+int occupancy_batch();
 
-constexpr uint32_t kWarpSegmentMax = 4096;  // segments up to this many ints: warp-per-segment
+// Control bytes per look-back tile of each single-array kernel.
+constexpr uint32_t kDecodeTileGroups = 2048;  // CTA tile of 8 warp sub-tiles (svb_warp.cuh kCTGroups)
+constexpr uint32_t kEncodeTileGroups = 2048;
+constexpr uint32_t kOffsetsTileGroups = 2048;  // CTA tile (kTileGroups)
 
 }  // namespace bcgpu

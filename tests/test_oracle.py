@@ -185,3 +185,11 @@ def test_mt_reference_matches_o1():
             dec = np.empty(max(n, 1), np.uint32)
             st, last = oracle.mt_decode(ref, n, dec, delta=delta, base=7, threads=5)
             assert st == oracle.OK and np.array_equal(dec[:n], v)
+    # chunk seams with 1-byte ints (the <=3-byte store spill must stay inside its chunk)
+    from paper_1709_08990_b200 import gen
+    v = gen.config_array(2, 1 << 21)
+    ref = oracle.encode(v, delta=True)
+    for th in (2, 7, 16):
+        out = np.empty((v.size + 3) // 4 + 4 * v.size + 1, np.uint8)
+        m = oracle.mt_encode(v, delta=True, threads=th, out=out)
+        assert out[:m].tobytes() == ref
