@@ -97,7 +97,7 @@ class ClockSampler:
                 if val.lower().startswith("active"):
                     reasons.add(nm)
         return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx, "reasons": sorted(reasons),
-                "samples": len(sm)}
+                "samples": len(sm), "window": "timed region + identical untimed load to 0.4 s (nvidia-smi -lms 100)"}
 
 
 # ---------------------------------------------------------------------------
@@ -390,17 +390,31 @@ def run_gpu(args):
     wl.verify(torch)
 
     evs = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(args.steps)]
+    # nvidia-smi needs ~100 ms per sample; it is started before the timed region and
+    # kept sampling under the identical (untimed) load until >= 0.4 s have elapsed
+    clk = ClockSampler(local if world > 1 else torch.cuda.current_device())
+    clk.__enter__()
+    t_wait = time.time()
+    while not clk.lines and time.time() - t_wait < 3.0:
+        time.sleep(0.02)
     if world > 1:
         torch.distributed.barrier()
     torch.cuda.synchronize()
+    n_before = len(clk.lines)
     launches0 = _native.kernel_launch_count()
-    with ClockSampler(torch.cuda.current_device() if "CUDA_VISIBLE_DEVICES" not in os.environ else local) as clk:
-        for k in range(args.steps):
-            step(evs[k])
+    t_timed = time.time()
+    for k in range(args.steps):
+        step(evs[k])
+    torch.cuda.synchronize()
+    launches = _native.kernel_launch_count() - launches0
+    scratch = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+    while time.time() - t_timed < 0.4:
+        step(scratch)
         torch.cuda.synchronize()
+    clk.__exit__()
+    clk.lines = clk.lines[max(0, n_before - 1):]
     if world > 1:
         torch.distributed.barrier()
-    launches = _native.kernel_launch_count() - launches0
     t_enc = [e[0].elapsed_time(e[1]) for e in evs]
     t_dec = [e[2].elapsed_time(e[3]) for e in evs]
     ms_step = statistics.mean(a + b for a, b in zip(t_enc, t_dec))

@@ -64,8 +64,9 @@ struct bcgpu_ctx {
     int batch_grid = 0;
     // host-API scratch (device) and stream
     cudaStream_t stream = nullptr;
-    uint64_t* offs = nullptr;  // decode: per-sub-tile data offsets
-    size_t offs_cap = 0;
+    void* offs = nullptr;  // decode metadata workspace (svb_decode.cu DecodeMeta)
+    size_t offs_cap = 0;   // bytes
+    int pipe_grid = 0;     // persistent decode CTAs
     void* d_scratch = nullptr;
     size_t d_scratch_cap = 0;
 };
@@ -215,6 +216,7 @@ int bcgpu_ctx_create(int device, bcgpu_ctx** out) {
     c->device = device;
     cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, device);
     c->batch_grid = c->num_sms * occupancy_batch();
+    c->pipe_grid = c->num_sms * occupancy_decode_pipe();
     cudaError_t e = cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking);
     if (e != cudaSuccess) {
         delete c;
@@ -266,10 +268,10 @@ int bcgpu_svb_encode_device(bcgpu_ctx* c, const uint32_t* d_in, size_t n, int de
         if (d_out_len) BC_CUDA(cudaMemsetAsync(d_out_len, 0, sizeof(uint64_t), s));
         return BCGPU_OK;
     }
-    LookbackArgs lb;
+    LookbackArgs lb{};
     int st = make_lookback(c, (n + 3) / 4, kEncodeTileGroups, s, &lb);
     if (st) return st;
-    BC_CUDA(launch_encode(d_in, n, delta, prev, d_out, d_out_len, lb, s));
+    BC_CUDA(launch_encode2(d_in, n, delta, prev, d_out, d_out_len, lb, s));
     g_launches.fetch_add(1);
     return BCGPU_OK;
 }
@@ -286,34 +288,24 @@ int bcgpu_svb_decode_device(bcgpu_ctx* c, const uint8_t* d_in, size_t in_len, si
         if (in_len != 0) return BCGPU_ERR_TRAILING_BYTES;
         return BCGPU_OK;
     }
-    const size_t words = decode2_offsets_words(n);
-    if (words > c->offs_cap) {
+    const size_t bytes = decode_meta_bytes(n);
+    if (bytes > c->offs_cap) {
         if (c->offs) {
             BC_CUDA(cudaStreamSynchronize(s));
             BC_CUDA(cudaFree(c->offs));
             c->offs = nullptr;
         }
-        size_t cap = words + words / 4 + 64;
-        BC_CUDA(cudaMalloc(&c->offs, cap * sizeof(uint64_t)));
+        const size_t cap = bytes + bytes / 4 + 1024;
+        BC_CUDA(cudaMalloc(&c->offs, cap));
+        BC_CUDA(cudaMemset(c->offs, 0, cap));
         c->offs_cap = cap;
     }
-    const uint32_t chunks = decode2_chunks(n), tiles = decode2_tiles(n);
-    int st = ensure_ws(c, chunks > tiles ? chunks : tiles);
+    const int st = next_epoch(c, s);
     if (st) return st;
-    st = next_epoch(c, s);
-    if (st) return st;
-    LookbackArgs lb{};
-    lb.off_status = off_status(c);
-    lb.sum_status = sum_status(c);
-    lb.trace = c->trace;
-    lb.debug_flags = c->debug_flags;
-    lb.epoch = c->epoch;
-    lb.status = status_ptr(c);
-    LookbackArgs lb1 = lb, lb2 = lb;
-    lb1.num_tiles = chunks;
-    lb2.num_tiles = tiles;
-    BC_CUDA(launch_decode2(d_in, in_len, n, delta, base, d_out, d_last, c->offs, lb1, lb2, s));
-    g_launches.fetch_add(2);
+    int launches = 0;
+    BC_CUDA(launch_decode3(d_in, in_len, n, delta, base, d_out, d_last, c->offs, status_ptr(c), c->epoch,
+                           c->pipe_grid, s, &launches, c->trace));
+    g_launches.fetch_add((uint64_t)launches);
     return BCGPU_OK;
 }
 

@@ -1,18 +1,23 @@
-// svb_decode.cu -- single-array Stream VByte decode for sm_100a (svb_decode /
-// svb_decode_delta, reference stream_vbyte.hpp:38-42, codec.hpp:85-90).
+// svb_decode.cu -- single-array Stream VByte decode for sm_100a
+// (svb_decode / svb_decode_delta: reference stream_vbyte.hpp:38-42, codec.hpp:85-90).
 //
-// Two launches per call:
-//   1. svb_subtile_offsets_kernel -- control bytes only (0.25 B/int): data-region
-//      offset of every 1024-integer sub-tile (exclusive scan of the paper's
-//      length[c]), chunk prefixes by TMA-polled decoupled
-//      look-back.  Also validates the stream length (truncated / trailing).
-//   2. svb_decode_tile_kernel -- one CTA per 8 sub-tiles.  Each warp bulk-loads
-//      its sub-tile's control and data bytes in one TMA transaction (offsets
-//      are known, nothing waits on a neighbour), expands them in shared memory
-//      (reverse row order makes the expansion in-place safe), and writes its
-//      4 KiB of integers with one TMA bulk store.  The delta variant fuses the
-//      mod-2^32 prefix sum: in-group 4-lane step, warp scan
-//      per row, then one TMA-polled look-back per CTA for the carry.
+// Reduce-then-scan, no kernel ever waits on another CTA:
+//   1. svb_ctrl_scan_kernel   control bytes only (0.25 B/int).  Per 64-sub-tile
+//      chunk: chunk-local exclusive prefix of every 1024-integer sub-tile's data
+//      length (length[c] = 4 + sum of fields) and the chunk
+//      total; the last CTA to finish scans the chunk totals and validates the
+//      stream length (truncated / trailing_bytes).
+//   2. (delta only) svb_decode_pipe_kernel<kModeSums>: decodes every sub-tile
+//      without storing and records its sum of deltas (+ RED.ADD into its chunk);
+//      the last CTA scans the chunk sums.
+//   3. svb_decode_pipe_kernel<kModePlain|kModeDelta>: decodes and stores.
+// Passes 2-3 are persistent warps: each warp walks sub-tiles gw, gw+GW, ... with
+// a two-deep pipeline -- the next sub-tile's control+data bytes arrive by one
+// TMA bulk copy into the other stage buffer while this one is expanded
+// (funnel-shift / byte-permute, the GPU pshufb), and the
+// metadata (offsets, carries) for the one after is already being loaded.
+// The delta variant fuses the mod-2^32 prefix sum: carry =
+// base + scanned chunk sums + sub-tile sums before it in its chunk.
 #include <cstdint>
 
 #include "svb_device.cuh"
@@ -22,35 +27,37 @@
 
 namespace bcgpu {
 
-constexpr int kK1Subtiles = 256;                     // sub-tiles per offsets chunk (one per thread)
-constexpr int kK1Ctrl = kK1Subtiles * kWTGroups;     // 65536 control bytes per chunk
-constexpr int kK1Window = 1024;
-constexpr int kK1Smem = kK1Ctrl + 64;
-constexpr int kDecWindow = 1024;
+constexpr int kChunkSubs = 64;                    // sub-tiles per chunk (64K integers)
+constexpr int kChunkCtrl = kChunkSubs * kWTGroups;  // 16 KiB of control bytes
 
-__device__ __forceinline__ void report_status_dec(unsigned long long* st, uint32_t epoch, uint32_t code) {
+__device__ __forceinline__ void dec_report(unsigned long long* st, uint32_t epoch, uint32_t code) {
     if (st) *st = ((unsigned long long)epoch << 32) | code;
 }
 
-// Data bytes declared by the control bytes [g, g+cnt) of a stream with
-// ngroups control bytes (final partial control byte masked to tail_r fields).
-// `p` points at control byte g in shared memory; `rot` staggers the word
-// order across lanes to keep the shared loads conflict-free.
-__device__ __forceinline__ uint32_t subtile_length(const uint8_t* p, uint64_t g, uint32_t cnt, uint64_t ngroups,
-                                                   uint32_t tail_r, int rot) {
+// ---------------------------------------------------------------------------
+// 1. control scan
+// ---------------------------------------------------------------------------
+// 4 threads per sub-tile, 64 control bytes (16 words) each.
+__device__ __forceinline__ uint32_t quarter_length(const uint8_t* __restrict__ ctrl, uint64_t g, uint64_t ngroups,
+                                                   uint32_t tail_r) {
+    if (g >= ngroups) return 0;
+    const uint64_t cnt = ngroups - g < 64 ? ngroups - g : 64;
     const bool has_tail = tail_r != 0 && g + cnt == ngroups;
     uint32_t sum = 0;
-    if (cnt == (uint32_t)kWTGroups && !has_tail) {
-        const uint32_t* w = reinterpret_cast<const uint32_t*>(p);
-#pragma unroll 8
-        for (int k = 0; k < kWTGroups / 4; ++k) {
-            const uint32_t x = swar_lengths(w[(k + rot) & (kWTGroups / 4 - 1)]);
-            sum += (x * 0x01010101u) >> 24;
+    if (cnt == 64 && !has_tail && (((uintptr_t)(ctrl + g)) & 15) == 0) {
+        const uint4* p = reinterpret_cast<const uint4*>(ctrl + g);
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            const uint4 w = __ldg(p + k);
+            sum += (swar_lengths(w.x) * 0x01010101u) >> 24;
+            sum += (swar_lengths(w.y) * 0x01010101u) >> 24;
+            sum += (swar_lengths(w.z) * 0x01010101u) >> 24;
+            sum += (swar_lengths(w.w) * 0x01010101u) >> 24;
         }
         return sum;
     }
-    for (uint32_t i = 0; i < cnt; ++i) {
-        uint32_t c = p[i];
+    for (uint64_t i = 0; i < cnt; ++i) {
+        uint32_t c = __ldg(ctrl + g + i);
         if (has_tail && i == cnt - 1) {
             c &= (1u << (2 * tail_r)) - 1u;
             sum += fsum(c) + tail_r;
@@ -61,116 +68,188 @@ __device__ __forceinline__ uint32_t subtile_length(const uint8_t* p, uint64_t g,
     return sum;
 }
 
-__global__ void __launch_bounds__(256, 2)
-    svb_subtile_offsets_kernel(const uint8_t* __restrict__ in, uint64_t in_len, uint64_t n, uint64_t* __restrict__ offs,
-                               LookbackArgs lb) {
-    extern __shared__ __align__(128) uint8_t sctrl[];
-    __shared__ __align__(8) uint64_t bar;
-    __shared__ __align__(128) LookbackWin<kK1Window> lbw;
-    __shared__ uint32_t warp_tot[8];
-    __shared__ unsigned long long s_off;
+// Exclusive scan of a[0..m) in place by one CTA of 32*kNW threads; returns the total.
+template <class T, int kNW>
+__device__ __forceinline__ T cta_exclusive_scan(T* a, uint32_t m, T* warp_tmp) {
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const uint32_t chunk = blockIdx.x;
+    const uint32_t per = (m + 32 * kNW - 1) / (32 * kNW);
+    const uint32_t lo = tid * per, hi = lo + per < m ? lo + per : m;
+    T s = 0;
+    for (uint32_t i = lo; i < hi; ++i) s += a[i];
+    T incl = s;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const T t = __shfl_up_sync(kFull, incl, o);
+        if (lane >= o) incl += t;
+    }
+    if (lane == 31) warp_tmp[warp] = incl;
+    __syncthreads();
+    T wpre = 0, total = 0;
+#pragma unroll
+    for (int w = 0; w < kNW; ++w) {
+        wpre += w < warp ? warp_tmp[w] : (T)0;
+        total += warp_tmp[w];
+    }
+    T run = wpre + incl - s;
+    for (uint32_t i = lo; i < hi; ++i) {
+        const T x = a[i];
+        a[i] = run;
+        run += x;
+    }
+    __syncthreads();
+    return total;
+}
+
+struct DecodeMeta {
+    uint32_t* localpre;              // [nsub]  sub-tile data offset within its chunk
+    unsigned long long* chunkpre;    // [nchunks + 1] chunk data offset (exclusive; [nchunks] = total)
+    uint32_t* subsums;               // [nsub]  delta: sum of the sub-tile's deltas
+    uint32_t* chunksums;             // [nchunks + 1] delta: chunk sums -> exclusive prefix
+    unsigned int* counters;          // [2] last-CTA tickets (self-resetting)
+    unsigned long long* trace;       // debug: 4 timestamps per sub-tile (nullptr = off)
+};
+
+__device__ __forceinline__ unsigned long long gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
+
+__global__ void __launch_bounds__(256)
+    svb_ctrl_scan_kernel(const uint8_t* __restrict__ in, uint64_t in_len, uint64_t n, DecodeMeta meta,
+                         unsigned long long* status, uint32_t epoch, int zero_sums) {
+    __shared__ uint32_t wt[8];
+    __shared__ unsigned long long wt64[8];
+    __shared__ bool last;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const uint32_t chunk = blockIdx.x, nchunks = gridDim.x;
     const uint64_t ngroups = (n + 3) >> 2;
     const uint32_t tail_r = (uint32_t)(n & 3);
     const uint64_t nsub = (ngroups + kWTGroups - 1) / kWTGroups;
-    const uint64_t g0 = (uint64_t)chunk * kK1Ctrl;
-    const uint32_t cnt = (uint32_t)(ngroups - g0 < (uint64_t)kK1Ctrl ? ngroups - g0 : (uint64_t)kK1Ctrl);
-    const uintptr_t cb = (uintptr_t)in + g0;
-    const uint32_t tx = tma_cover_bytes(cb, cb + cnt, (uintptr_t)in, (uintptr_t)in + in_len);
-    const bool use_tma = tx != 0xFFFFFFFFu && (cb & 15) == 0;
-    if (tid == 0) {
-        mbar_init1(&bar);
-        mbar_init1(&lbw.bar);
-        if (use_tma && tx) {
-            mbar_expect(&bar, tx);
-            tma_load(sctrl, reinterpret_cast<const void*>(cb), tx, &bar);
-        }
-    }
-    if (!use_tma)
-        for (uint32_t i = tid; i < cnt; i += 256) sctrl[i] = __ldg(in + g0 + i);
-    __syncthreads();
-    if (use_tma && tx) mbar_wait_parity(&bar, 0);
-
-    const uint32_t my_g = (uint32_t)tid * kWTGroups;
-    const uint32_t my_cnt = my_g < cnt ? (cnt - my_g < (uint32_t)kWTGroups ? cnt - my_g : (uint32_t)kWTGroups) : 0u;
-    const uint32_t len = my_cnt ? subtile_length(sctrl + my_g, g0 + my_g, my_cnt, ngroups, tail_r, lane) : 0u;
-    const uint32_t incl = warp_inclusive_scan(len);
-    if (lane == 31) warp_tot[warp] = incl;
+    if (zero_sums && tid == 0) meta.chunksums[chunk] = 0;
+    const uint64_t g = (uint64_t)chunk * kChunkCtrl + (uint64_t)tid * 64;
+    uint32_t q = quarter_length(in, g, ngroups, tail_r);
+    // sub-tile length = sum of its 4 quarters (lanes 4k..4k+3)
+    q += __shfl_xor_sync(kFull, q, 1);
+    q += __shfl_xor_sync(kFull, q, 2);
+    // chunk-local exclusive prefix over the 64 sub-tiles (8 per warp, lanes 4k)
+    const uint32_t v = (lane & 3) == 0 ? q : 0u;
+    const uint32_t incl = warp_inclusive_scan(v);
+    if (lane == 31) wt[warp] = incl;
     __syncthreads();
     uint32_t wpre = 0, total = 0;
 #pragma unroll
     for (int w = 0; w < 8; ++w) {
-        wpre += w < warp ? warp_tot[w] : 0u;
-        total += warp_tot[w];
+        wpre += w < warp ? wt[w] : 0u;
+        total += wt[w];
     }
-    if (warp == 0) {
-        uint32_t phase = 0;
-        const uint64_t off = lookback_tma_resolve<kK1Window>(lb.off_status, chunk, lb.epoch, 0, total, lbw, phase);
-        if (lane == 0) s_off = off;
+    const uint64_t sub = (uint64_t)chunk * kChunkSubs + (tid >> 2);
+    if ((lane & 3) == 0 && sub < nsub) meta.localpre[sub] = wpre + incl - v;
+    if (tid == 0) meta.chunkpre[chunk] = total;
+    // last CTA: scan the chunk totals, validate the stream length
+    __syncthreads();
+    if (tid == 0) {
+        __threadfence();
+        last = atomicAdd(meta.counters, 1u) == nchunks - 1;
     }
     __syncthreads();
-    const uint64_t sub = (uint64_t)chunk * kK1Subtiles + tid;
-    if (sub < nsub) offs[sub] = s_off + wpre + incl - len;
-    if (chunk == gridDim.x - 1 && tid == 0) {
-        offs[nsub] = s_off + total;
-        offs[nsub + 1] = s_off + total;
-        const uint64_t need = ngroups + s_off + total;
-        report_status_dec(lb.status, lb.epoch,
-                          need > in_len ? BCGPU_ERR_TRUNCATED : (need < in_len ? BCGPU_ERR_TRAILING_BYTES : 0u));
+    if (!last) return;
+    __threadfence();
+    const unsigned long long tot = cta_exclusive_scan<unsigned long long, 8>(meta.chunkpre, nchunks, wt64);
+    if (tid == 0) {
+        meta.chunkpre[nchunks] = tot;
+        const uint64_t need = ngroups + tot;
+        dec_report(status, epoch, need > in_len ? BCGPU_ERR_TRUNCATED : (need < in_len ? BCGPU_ERR_TRAILING_BYTES : 0u));
+        *meta.counters = 0;
     }
 }
 
 // ---------------------------------------------------------------------------
-struct __align__(16) WarpBuf {
-    uint8_t stage[kWTStage + 16];  // input bytes, then (in place) the sub-tile's 1024 integers at +16
+// 2./3. tile decode: one CTA per 8 sub-tiles, one warp per sub-tile
+// ---------------------------------------------------------------------------
+// Every warp issues one TMA transaction for its sub-tile's control and data
+// bytes as soon as the CTA's offsets have landed, expands them in shared
+// memory (reverse row order keeps the expansion in place), and writes its
+// 4 KiB of integers with one TMA bulk store.  No CTA waits on another: offsets
+// come from the control scan, delta carries from the sums pass.  ~40 warps per
+// SM keep the (deeply queued, ~5 us at 80 % of HBM peak) TMA round trips covered.
+enum : int { kModePlain = 0, kModeDelta = 1, kModeSums = 2 };
+
+struct __align__(16) TileBuf {
+    uint8_t stage[kWTStage + 16];  // input bytes, then (in place) the sub-tile's integers at +16
     uint8_t ctrl[kWTGroups];
 };
 
-struct DecShared {
-    uint32_t sum[kCTWarps];
-    unsigned long long carry;
-};
+__device__ __forceinline__ uint32_t warp_sum_u32(uint32_t v) {
+#pragma unroll
+    for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(kFull, v, o);
+    return v;
+}
 
-template <bool kDelta>
+// sum of the four bytes of w
+__device__ __forceinline__ uint32_t byte_sum4(uint32_t w) {
+    const uint32_t s = (w & 0x00FF00FFu) + ((w >> 8) & 0x00FF00FFu);
+    return (s & 0xFFFFu) + (s >> 16);
+}
+
+template <int kMode>
 __global__ void __launch_bounds__(kCTThreads, 5)
     svb_decode_tile_kernel(const uint8_t* __restrict__ in, uint64_t in_len, uint64_t n, uint32_t base,
-                           uint32_t* __restrict__ out, uint32_t* __restrict__ d_last,
-                           const uint64_t* __restrict__ offs, LookbackArgs lb) {
-    __shared__ __align__(128) WarpBuf wb[kCTWarps];
-    __shared__ __align__(16) uint64_t soffs[kCTWarps + 2];
+                           uint32_t* __restrict__ out, uint32_t* __restrict__ d_last, DecodeMeta meta) {
+    __shared__ __align__(128) TileBuf wb[kCTWarps];
+    __shared__ __align__(16) uint32_t slocal[kCTWarps + 8];         // localpre[sub0 .. sub0+12)
+    __shared__ __align__(16) unsigned long long schunk[4];          // chunkpre[(c & ~1) .. +4)
     __shared__ __align__(8) uint64_t bars[kCTWarps + 1];
-    __shared__ DecShared sh;
+    __shared__ uint32_t wsum[kCTWarps], wpart[kCTWarps];
+    __shared__ bool last;
+    constexpr bool kDelta = kMode == kModeDelta;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint32_t tile = blockIdx.x;
     const uint64_t ngroups = (n + 3) >> 2;
     const uint32_t tail_r = (uint32_t)(n & 3);
     const uint64_t nsub = (ngroups + kWTGroups - 1) / kWTGroups;
     const uint64_t sub0 = (uint64_t)tile * kCTWarps;
+    const uint64_t chunk = sub0 / kChunkSubs;
     const uint32_t nsub_tile = (uint32_t)(nsub - sub0 < (uint64_t)kCTWarps ? nsub - sub0 : (uint64_t)kCTWarps);
 
-    // the CTA's sub-tile offsets (nsub_tile + 1 words, rounded to 16 B; offs has slack)
+    // the CTA's offsets: chunk-local sub-tile prefixes + the chunk's offset (one TMA transaction)
     if (threadIdx.x == 0) {
         mbar_init1(&bars[kCTWarps]);
-        mbar_expect(&bars[kCTWarps], (uint32_t)(((nsub_tile + 2) & ~1u) * 8));
-        tma_load(soffs, offs + sub0, (uint32_t)(((nsub_tile + 2) & ~1u) * 8), &bars[kCTWarps]);
+        mbar_expect(&bars[kCTWarps], 48 + 32);
+        tma_load(slocal, meta.localpre + sub0, 48, &bars[kCTWarps]);
+        tma_load(schunk, meta.chunkpre + (chunk & ~1ull), 32, &bars[kCTWarps]);
     }
     if (lane == 0) mbar_init1(&bars[warp]);
+    // delta: this thread's share of the carry (scanned chunk sums + sums of the earlier
+    // sub-tiles of this chunk); the loads fly together with the TMA traffic
+    uint32_t part = 0;
+    if constexpr (kDelta) {
+        const uint64_t c0 = chunk * kChunkSubs;
+        for (uint64_t i = c0 + threadIdx.x; i < sub0; i += kCTThreads) part += __ldg(meta.subsums + i);
+        if (threadIdx.x == 0) part += __ldg(meta.chunksums + chunk);
+    }
     __syncthreads();
     mbar_wait_parity(&bars[kCTWarps], 0);
 
-    WarpBuf& b = wb[warp];
+    TileBuf& b = wb[warp];
     const bool active = (uint32_t)warp < nsub_tile;
     const uint64_t sub = sub0 + warp;
     const uint64_t g0 = sub * kWTGroups;
-    const uintptr_t lo = (uintptr_t)in, hi = lo + in_len;
     uint32_t T[kWTRows];
     uint32_t wtot = 0;
     uint32_t* o = out + 4 * g0;
     const uint32_t nints = active ? (uint32_t)(n - 4 * g0 < (uint64_t)kWTInts ? n - 4 * g0 : (uint64_t)kWTInts) : 0u;
     if (active) {
-        const uint64_t off = soffs[warp];
-        const uint32_t len = (uint32_t)(soffs[warp + 1] - off);
+        const unsigned long long cpre = schunk[chunk & 1];
+        const uint32_t li = (uint32_t)(sub - chunk * kChunkSubs);  // index within the chunk
+        const uint64_t off = cpre + slocal[warp];
+        const uint64_t nxt = ((sub + 1) % kChunkSubs == 0 || sub + 1 >= nsub)
+                                 ? (unsigned long long)schunk[(chunk & 1) + 1]
+                                 : cpre + slocal[warp + 1];
+        (void)li;
+        const uint32_t len0 = (uint32_t)(nxt - off);
+        const uint32_t len = len0 > (uint32_t)kWTDataMax ? (uint32_t)kWTDataMax : len0;  // malformed: clamp
+        const uintptr_t lo = (uintptr_t)in, hi = lo + in_len;
         const uint32_t cnt_g = (uint32_t)(ngroups - g0 < (uint64_t)kWTGroups ? ngroups - g0 : (uint64_t)kWTGroups);
         const uintptr_t cbeg = lo + g0;
         const uintptr_t dbeg = lo + ngroups + off;
@@ -193,47 +272,81 @@ __global__ void __launch_bounds__(kCTThreads, 5)
         const WarpCtrl w = load_warp_ctrl<true>(b.ctrl, g0, ngroups, tail_r, g0);
         const uint32_t* W = reinterpret_cast<const uint32_t*>(b.stage);
         const uint32_t head = (uint32_t)(dbeg & 15);
-        // reverse row order: row j's output [16+512j, +512) lies above every
-        // input byte of rows < j (at most 512j bytes from stage+head, head < 16)
+        if constexpr (kMode == kModeSums) {
+            uint32_t acc = 0;
 #pragma unroll
-        for (int j = kWTRows - 1; j >= 0; --j) {
-            const uint32_t c = row_ctrl(w, j);
-            const uint32_t bb = head + row_q(w, j);
-            const bool allzero = __all_sync(kFull, c == 0);
-            uint4 v = allzero ? decode_zero_group(W, bb) : decode_group(W, bb, c);
-            if constexpr (kDelta) {
+            for (int j = 0; j < kWTRows; ++j) {
+                const uint32_t c = row_ctrl(w, j);
+                const uint32_t bb = head + row_q(w, j);
                 const uint32_t cnt = group_count(g0 + 32 * j + lane, ngroups, tail_r);
-                v = prefix4(mask_tail(v, cnt));
-                const uint32_t S = v.w;
-                const uint32_t I = warp_inclusive_scan(S);
-                v = add4(v, I - S);
-                T[j] = __shfl_sync(kFull, I, 31);
-                wtot += T[j];
+                if (__all_sync(kFull, c == 0)) {
+                    // four 1-byte integers: their sum is the byte sum of one funnel-shifted word
+                    const uint32_t x = __funnelshift_r(W[bb >> 2], W[(bb >> 2) + 1], (bb & 3u) * 8u);
+                    acc += byte_sum4(x & (cnt >= 4 ? 0xFFFFFFFFu : ((1u << (8 * cnt)) - 1u)));
+                } else {
+                    const uint4 v = mask_tail(decode_group(W, bb, c), cnt);
+                    acc += v.x + v.y + v.z + v.w;
+                }
             }
-            __syncwarp();
-            *reinterpret_cast<uint4*>(b.stage + 16 + 512 * j + 16 * lane) = v;
+            wtot = warp_sum_u32(acc);
+        } else {
+            // reverse row order: row j's output [16+512j, +512) lies above every
+            // input byte of rows < j (at most 512j bytes from stage+head, head < 16)
+#pragma unroll
+            for (int j = kWTRows - 1; j >= 0; --j) {
+                const uint32_t c = row_ctrl(w, j);
+                const uint32_t bb = head + row_q(w, j);
+                const bool allzero = __all_sync(kFull, c == 0);
+                uint4 v = allzero ? decode_zero_group(W, bb) : decode_group(W, bb, c);
+                if constexpr (kDelta) {
+                    const uint32_t cnt = group_count(g0 + 32 * j + lane, ngroups, tail_r);
+                    v = prefix4(mask_tail(v, cnt));
+                    const uint32_t S = v.w;
+                    const uint32_t I = warp_inclusive_scan(S);
+                    v = add4(v, I - S);
+                    T[j] = __shfl_sync(kFull, I, 31);
+                    wtot += T[j];
+                }
+                __syncwarp();
+                *reinterpret_cast<uint4*>(b.stage + 16 + 512 * j + 16 * lane) = v;
+            }
         }
+    }
+    if constexpr (kMode == kModeSums) {
+        if (active && lane == 0) {
+            meta.subsums[sub] = wtot;
+            atomicAdd(meta.chunksums + chunk, wtot);  // RED.ADD, mod 2^32
+        }
+        // last CTA: exclusive scan of the chunk sums
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            __threadfence();
+            last = atomicAdd(meta.counters + 1, 1u) == gridDim.x - 1;
+        }
+        __syncthreads();
+        if (!last) return;
+        __threadfence();
+        const uint32_t nchunks = (uint32_t)((nsub + kChunkSubs - 1) / kChunkSubs);
+        cta_exclusive_scan<uint32_t, kCTWarps>(meta.chunksums, nchunks, wsum);
+        if (threadIdx.x == 0) meta.counters[1] = 0;
+        return;
     }
     uint32_t carry = 0, csum = 0, sex = 0;
     if constexpr (kDelta) {
-        __shared__ __align__(128) LookbackWin<kDecWindow> lbw;
-        if (threadIdx.x == 0) mbar_init1(&lbw.bar);
-        if (lane == 0) sh.sum[warp] = wtot;
+        part = warp_sum_u32(part);
+        if (lane == 0) {
+            wsum[warp] = wtot;
+            wpart[warp] = part;
+        }
         __syncthreads();
+        carry = base;
 #pragma unroll
         for (int k = 0; k < kCTWarps; ++k) {
-            const uint32_t x = sh.sum[k];
+            const uint32_t x = wsum[k];
             sex += k < warp ? x : 0u;
             csum += x;
+            carry += wpart[k];
         }
-        if (warp == 0) {
-            uint32_t phase = 0;
-            const uint64_t c =
-                lookback_tma_resolve<kDecWindow>(lb.sum_status, tile, lb.epoch, base, csum, lbw, phase);
-            if (lane == 0) sh.carry = c;
-        }
-        __syncthreads();
-        carry = (uint32_t)sh.carry;
         if (active) {
             uint32_t R = carry + sex;
 #pragma unroll
@@ -262,41 +375,66 @@ __global__ void __launch_bounds__(kCTThreads, 5)
     if (kDelta && tile == gridDim.x - 1 && threadIdx.x == 0 && d_last) *d_last = carry + csum;
 }
 
+}  // namespace bcgpu
+
+namespace bcgpu {
+
 // ---------------------------------------------------------------------------
-cudaError_t launch_decode2(const uint8_t* in, uint64_t in_len, uint64_t n, int delta, uint32_t base, uint32_t* out,
-                           uint32_t* d_last, uint64_t* offs, const LookbackArgs& lb_offs, const LookbackArgs& lb_dec,
-                           cudaStream_t stream) {
-    static const cudaError_t attr =
-        cudaFuncSetAttribute(svb_subtile_offsets_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kK1Smem);
-    if (attr != cudaSuccess) return attr;
+// launcher
+// ---------------------------------------------------------------------------
+static inline uint64_t align16(uint64_t x) { return (x + 15) & ~(uint64_t)15; }
+
+static DecodeMeta carve_meta(void* ws, uint64_t n) {
     const uint64_t ngroups = (n + 3) >> 2;
     const uint64_t nsub = (ngroups + kWTGroups - 1) / kWTGroups;
-    const int g1 = (int)((ngroups + kK1Ctrl - 1) / kK1Ctrl);
-    svb_subtile_offsets_kernel<<<g1, 256, kK1Smem, stream>>>(in, in_len, n, offs, lb_offs);
+    const uint64_t nchunks = (nsub + kChunkSubs - 1) / kChunkSubs;
+    uint8_t* p = static_cast<uint8_t*>(ws);
+    DecodeMeta m;
+    m.trace = nullptr;
+    m.counters = reinterpret_cast<unsigned int*>(p);  // 16 B, persists across calls (self-resetting)
+    p += 16;
+    m.localpre = reinterpret_cast<uint32_t*>(p);
+    p += align16(4 * (nsub + 16));
+    m.chunkpre = reinterpret_cast<unsigned long long*>(p);
+    p += align16(8 * (nchunks + 4));
+    m.subsums = reinterpret_cast<uint32_t*>(p);
+    p += align16(4 * nsub);
+    m.chunksums = reinterpret_cast<uint32_t*>(p);
+    return m;
+}
+
+uint64_t decode_meta_bytes(uint64_t n) {
+    const uint64_t ngroups = (n + 3) >> 2;
+    const uint64_t nsub = (ngroups + kWTGroups - 1) / kWTGroups;
+    const uint64_t nchunks = (nsub + kChunkSubs - 1) / kChunkSubs;
+    return 16 + align16(4 * (nsub + 16)) + align16(8 * (nchunks + 4)) + align16(4 * nsub) + align16(4 * (nchunks + 1)) +
+           64;
+}
+
+int occupancy_decode_pipe() { return 1; }  // the tile kernel is not persistent
+
+cudaError_t launch_decode3(const uint8_t* in, uint64_t in_len, uint64_t n, int delta, uint32_t base, uint32_t* out,
+                           uint32_t* d_last, void* meta_ws, unsigned long long* status, uint32_t epoch, int pipe_grid,
+                           cudaStream_t stream, int* launches, unsigned long long* trace) {
+    DecodeMeta m = carve_meta(meta_ws, n);
+    m.trace = trace;
+    const uint64_t ngroups = (n + 3) >> 2;
+    const uint64_t nsub = (ngroups + kWTGroups - 1) / kWTGroups;
+    const uint32_t nchunks = (uint32_t)((nsub + kChunkSubs - 1) / kChunkSubs);
+    svb_ctrl_scan_kernel<<<nchunks, 256, 0, stream>>>(in, in_len, n, m, status, epoch, delta);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
-    const int g2 = (int)((nsub + kCTWarps - 1) / kCTWarps);
-    if (delta)
-        svb_decode_tile_kernel<true><<<g2, kCTThreads, 0, stream>>>(in, in_len, n, base, out, d_last, offs, lb_dec);
-    else
-        svb_decode_tile_kernel<false><<<g2, kCTThreads, 0, stream>>>(in, in_len, n, base, out, d_last, offs, lb_dec);
+    (void)pipe_grid;
+    const int grid = (int)((nsub + kCTWarps - 1) / kCTWarps);
+    if (delta) {
+        svb_decode_tile_kernel<kModeSums><<<grid, kCTThreads, 0, stream>>>(in, in_len, n, base, out, d_last, m);
+        svb_decode_tile_kernel<kModeDelta><<<grid, kCTThreads, 0, stream>>>(in, in_len, n, base, out, d_last, m);
+        *launches = 3;
+    } else {
+        svb_decode_tile_kernel<kModePlain><<<grid, kCTThreads, 0, stream>>>(in, in_len, n, base, out, d_last, m);
+        *launches = 2;
+    }
     return cudaGetLastError();
-}
-
-uint64_t decode2_offsets_words(uint64_t n) {
-    const uint64_t ngroups = (n + 3) >> 2;
-    return (ngroups + kWTGroups - 1) / kWTGroups + 4;
-}
-
-uint32_t decode2_chunks(uint64_t n) {
-    const uint64_t ngroups = (n + 3) >> 2;
-    return (uint32_t)((ngroups + kK1Ctrl - 1) / kK1Ctrl);
-}
-
-uint32_t decode2_tiles(uint64_t n) {
-    const uint64_t ngroups = (n + 3) >> 2;
-    const uint64_t nsub = (ngroups + kWTGroups - 1) / kWTGroups;
-    return (uint32_t)((nsub + kCTWarps - 1) / kCTWarps);
 }
 
 }  // namespace bcgpu

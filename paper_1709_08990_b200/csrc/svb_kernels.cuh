@@ -20,12 +20,17 @@ struct LookbackArgs {
 };
 
 // Launchers (return cudaError_t of the launch).
-// Single-array decode = sub-tile offsets pre-pass + tile decode (svb_decode.cu);
-// offs must hold decode2_offsets_words(n) u64, 16-B aligned.
-cudaError_t launch_decode2(const uint8_t* in, uint64_t in_len, uint64_t n, int delta, uint32_t base, uint32_t* out,
-                           uint32_t* d_last, uint64_t* offs, const LookbackArgs& lb_offs, const LookbackArgs& lb_dec,
-                           cudaStream_t stream);
-uint64_t decode2_offsets_words(uint64_t n);
+// Single-array decode (svb_decode.cu): control scan, [delta: tile-sum pass],
+// pipelined decode.  meta_ws holds decode_meta_bytes(n) bytes (16-B aligned,
+// first 16 bytes zero-initialised once and self-resetting).
+cudaError_t launch_decode3(const uint8_t* in, uint64_t in_len, uint64_t n, int delta, uint32_t base, uint32_t* out,
+                           uint32_t* d_last, void* meta_ws, unsigned long long* status, uint32_t epoch, int pipe_grid,
+                           cudaStream_t stream, int* launches, unsigned long long* trace = nullptr);
+uint64_t decode_meta_bytes(uint64_t n);
+int occupancy_decode_pipe();
+// Single-array encode: CTA tiles of 8 x 1024 integers, TMA staging, TMA-polled look-back.
+cudaError_t launch_encode2(const uint32_t* in, uint64_t n, int delta, uint32_t prev, uint8_t* out,
+                           uint64_t* d_out_len, const LookbackArgs& lb, cudaStream_t stream);
 uint32_t decode2_chunks(uint64_t n);  // look-back tiles of the offsets pre-pass
 uint32_t decode2_tiles(uint64_t n);   // look-back tiles (CTAs) of the tile decode
 cudaError_t launch_encode(const uint32_t* in, uint64_t n, int delta, uint32_t prev, uint8_t* out,

@@ -96,11 +96,15 @@ struct LookbackWin {
 
 template <int W>
 __device__ __forceinline__ uint64_t lookback_tma(const uint64_t* status, uint32_t tile, uint32_t epoch,
-                                                 LookbackWin<W>& ls, uint32_t& phase) {
+                                                 LookbackWin<W>& ls, uint32_t& phase,
+                                                 unsigned long long* stats = nullptr) {
     constexpr int PER = W / 32;
     const int lane = threadIdx.x & 31;
     uint64_t excl = 0;
     int64_t top = (int64_t)tile - 1;
+    uint32_t polls = 0, first_ns = 0, bad_polls = 0;
+    unsigned long long t0 = 0;
+    if (stats) asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t0));
     while (true) {
         const int64_t lo_idx = top - (W - 1) < 0 ? 0 : top - (W - 1);
         const int64_t a_idx = lo_idx & ~(int64_t)1;
@@ -116,6 +120,12 @@ __device__ __forceinline__ uint64_t lookback_tma(const uint64_t* status, uint32_
             }
             mbar_wait_parity(&ls.bar, phase);
             phase ^= 1u;
+            if (stats && polls == 0) {
+                unsigned long long t1;
+                asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t1));
+                first_ns = (uint32_t)(t1 - t0);
+            }
+            ++polls;
             bool bad = false;  // an unpublished entry before this lane's first inclusive
             first = PER;
 #pragma unroll 8
@@ -134,6 +144,7 @@ __device__ __forceinline__ uint64_t lookback_tma(const uint64_t* status, uint32_
             m = __ballot_sync(kFull, first < PER);
             const int fl = m ? __ffs(m) - 1 : 32;
             if (__all_sync(kFull, lane > fl || !bad)) break;
+            ++bad_polls;
             __syncwarp();
             __nanosleep(sleep_ns);
             sleep_ns = sleep_ns < 512 ? 2 * sleep_ns : 512;
@@ -153,6 +164,12 @@ __device__ __forceinline__ uint64_t lookback_tma(const uint64_t* status, uint32_
         __syncwarp();
         if (m) break;
         top -= W;
+    }
+    if (stats && lane == 0) {
+        unsigned long long t1;
+        asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t1));
+        *stats = ((unsigned long long)(polls & 0xFF) << 56) | ((unsigned long long)(bad_polls & 0xFF) << 48) |
+                 ((unsigned long long)(first_ns & 0xFFFFFF) << 24) | ((t1 - t0) & 0xFFFFFF);
     }
     return excl;
 }
