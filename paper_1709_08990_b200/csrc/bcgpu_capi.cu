@@ -136,6 +136,21 @@ static int make_batch(bcgpu_ctx* c, cudaStream_t s, BatchArgs* ba) {
     return BCGPU_OK;
 }
 
+static int ensure_meta(bcgpu_ctx* c, uint64_t n, cudaStream_t s) {
+    const size_t bytes = decode_meta_bytes(n);
+    if (bytes <= c->offs_cap) return BCGPU_OK;
+    if (c->offs) {
+        BC_CUDA(cudaStreamSynchronize(s));
+        BC_CUDA(cudaFree(c->offs));
+        c->offs = nullptr;
+    }
+    const size_t cap = bytes + bytes / 4 + 1024;
+    BC_CUDA(cudaMalloc(&c->offs, cap));
+    BC_CUDA(cudaMemset(c->offs, 0, cap));
+    c->offs_cap = cap;
+    return BCGPU_OK;
+}
+
 // ---------------------------------------------------------------------------
 extern "C" {
 
@@ -268,11 +283,13 @@ int bcgpu_svb_encode_device(bcgpu_ctx* c, const uint32_t* d_in, size_t n, int de
         if (d_out_len) BC_CUDA(cudaMemsetAsync(d_out_len, 0, sizeof(uint64_t), s));
         return BCGPU_OK;
     }
-    LookbackArgs lb{};
-    int st = make_lookback(c, (n + 3) / 4, kEncodeTileGroups, s, &lb);
+    int st = ensure_meta(c, n, s);
     if (st) return st;
-    BC_CUDA(launch_encode2(d_in, n, delta, prev, d_out, d_out_len, lb, s));
-    g_launches.fetch_add(1);
+    st = next_epoch(c, s);
+    if (st) return st;
+    int launches = 0;
+    BC_CUDA(launch_encode3(d_in, n, delta, prev, d_out, d_out_len, c->offs, status_ptr(c), c->epoch, s, &launches));
+    g_launches.fetch_add((uint64_t)launches);
     return BCGPU_OK;
 }
 
@@ -288,18 +305,8 @@ int bcgpu_svb_decode_device(bcgpu_ctx* c, const uint8_t* d_in, size_t in_len, si
         if (in_len != 0) return BCGPU_ERR_TRAILING_BYTES;
         return BCGPU_OK;
     }
-    const size_t bytes = decode_meta_bytes(n);
-    if (bytes > c->offs_cap) {
-        if (c->offs) {
-            BC_CUDA(cudaStreamSynchronize(s));
-            BC_CUDA(cudaFree(c->offs));
-            c->offs = nullptr;
-        }
-        const size_t cap = bytes + bytes / 4 + 1024;
-        BC_CUDA(cudaMalloc(&c->offs, cap));
-        BC_CUDA(cudaMemset(c->offs, 0, cap));
-        c->offs_cap = cap;
-    }
+    int st0 = ensure_meta(c, n, s);
+    if (st0) return st0;
     const int st = next_epoch(c, s);
     if (st) return st;
     int launches = 0;

@@ -23,12 +23,11 @@
 #include "svb_device.cuh"
 #include "svb_kernels.cuh"
 #include "svb_tma.cuh"
+#include "svb_scan.cuh"
 #include "svb_warp.cuh"
 
 namespace bcgpu {
 
-constexpr int kChunkSubs = 64;                    // sub-tiles per chunk (64K integers)
-constexpr int kChunkCtrl = kChunkSubs * kWTGroups;  // 16 KiB of control bytes
 
 __device__ __forceinline__ void dec_report(unsigned long long* st, uint32_t epoch, uint32_t code) {
     if (st) *st = ((unsigned long long)epoch << 32) | code;
@@ -66,53 +65,6 @@ __device__ __forceinline__ uint32_t quarter_length(const uint8_t* __restrict__ c
         }
     }
     return sum;
-}
-
-// Exclusive scan of a[0..m) in place by one CTA of 32*kNW threads; returns the total.
-template <class T, int kNW>
-__device__ __forceinline__ T cta_exclusive_scan(T* a, uint32_t m, T* warp_tmp) {
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const uint32_t per = (m + 32 * kNW - 1) / (32 * kNW);
-    const uint32_t lo = tid * per, hi = lo + per < m ? lo + per : m;
-    T s = 0;
-    for (uint32_t i = lo; i < hi; ++i) s += a[i];
-    T incl = s;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-        const T t = __shfl_up_sync(kFull, incl, o);
-        if (lane >= o) incl += t;
-    }
-    if (lane == 31) warp_tmp[warp] = incl;
-    __syncthreads();
-    T wpre = 0, total = 0;
-#pragma unroll
-    for (int w = 0; w < kNW; ++w) {
-        wpre += w < warp ? warp_tmp[w] : (T)0;
-        total += warp_tmp[w];
-    }
-    T run = wpre + incl - s;
-    for (uint32_t i = lo; i < hi; ++i) {
-        const T x = a[i];
-        a[i] = run;
-        run += x;
-    }
-    __syncthreads();
-    return total;
-}
-
-struct DecodeMeta {
-    uint32_t* localpre;              // [nsub]  sub-tile data offset within its chunk
-    unsigned long long* chunkpre;    // [nchunks + 1] chunk data offset (exclusive; [nchunks] = total)
-    uint32_t* subsums;               // [nsub]  delta: sum of the sub-tile's deltas
-    uint32_t* chunksums;             // [nchunks + 1] delta: chunk sums -> exclusive prefix
-    unsigned int* counters;          // [2] last-CTA tickets (self-resetting)
-    unsigned long long* trace;       // debug: 4 timestamps per sub-tile (nullptr = off)
-};
-
-__device__ __forceinline__ unsigned long long gtimer() {
-    unsigned long long t;
-    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
-    return t;
 }
 
 __global__ void __launch_bounds__(256)
@@ -384,7 +336,7 @@ namespace bcgpu {
 // ---------------------------------------------------------------------------
 static inline uint64_t align16(uint64_t x) { return (x + 15) & ~(uint64_t)15; }
 
-static DecodeMeta carve_meta(void* ws, uint64_t n) {
+DecodeMeta carve_decode_meta(void* ws, uint64_t n) {
     const uint64_t ngroups = (n + 3) >> 2;
     const uint64_t nsub = (ngroups + kWTGroups - 1) / kWTGroups;
     const uint64_t nchunks = (nsub + kChunkSubs - 1) / kChunkSubs;
@@ -416,7 +368,7 @@ int occupancy_decode_pipe() { return 1; }  // the tile kernel is not persistent
 cudaError_t launch_decode3(const uint8_t* in, uint64_t in_len, uint64_t n, int delta, uint32_t base, uint32_t* out,
                            uint32_t* d_last, void* meta_ws, unsigned long long* status, uint32_t epoch, int pipe_grid,
                            cudaStream_t stream, int* launches, unsigned long long* trace) {
-    DecodeMeta m = carve_meta(meta_ws, n);
+    DecodeMeta m = carve_decode_meta(meta_ws, n);
     m.trace = trace;
     const uint64_t ngroups = (n + 3) >> 2;
     const uint64_t nsub = (ngroups + kWTGroups - 1) / kWTGroups;

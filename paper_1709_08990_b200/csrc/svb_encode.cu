@@ -2,84 +2,165 @@
 // reference stream_vbyte.hpp:36; delta encode codec.hpp:92-93 and the
 // prev-seeded extension E2).
 //
-// One launch: svb_encode_tile_kernel, one CTA per 8 sub-tiles of 1024 integers.
-// Each warp TMA-loads its 4 KiB of integers (plus the preceding integer for the
-// delta seed), classifies byte lengths (max(1, 4 - clz/8), codec.hpp:70-72),
-// TMA-stores its 256 control bytes (field i of control byte k = len-1 in bits
-// 2i), and packs the data bytes in place.  The CTA publishes
-// its byte count right after the length scan and resolves its output offset
-// with a TMA-polled decoupled look-back that overlaps the packing.
+// Reduce-then-scan, no CTA ever waits on another:
+//   1. svb_size_scan_kernel  reads the integers once (4 B/int): every
+//      1024-integer sub-tile's data size (sum of byte_length, codec.hpp:70-72,
+//      of the values or of their mod-2^32 deltas), chunk-local prefixes, chunk
+//      totals; the last CTA scans the chunk totals and writes the exact size.
+//   2. svb_encode_tile_kernel one CTA per 8 sub-tiles.  Each warp TMA-loads its
+//      4 KiB of integers (+ the 4 before, for the delta seed) while the CTA's
+//      offsets arrive, classifies lengths (max(1, 4 - clz/8)), TMA-stores its
+//      256 control bytes (field i of control byte k = len-1 in bits 2i,
+//      SPEC.md:275-281), packs the data bytes in place at the destination's
+//      16-B phase and writes them with one TMA bulk store (+ edge bytes).
+// When the input is L2-resident (it was just produced), the second read is an
+// L2 hit; from HBM the encode moves 8 + cmp bytes per 4-byte integer.
 #include <cstdint>
 
 #include "svb_device.cuh"
 #include "svb_kernels.cuh"
+#include "svb_scan.cuh"
 #include "svb_tma.cuh"
 #include "svb_warp.cuh"
 
 namespace bcgpu {
 
-__device__ __forceinline__ void trace_ts(const LookbackArgs& lb, uint32_t tile, int k) {
-    if (lb.trace && threadIdx.x == 0) {
-        unsigned long long t;
-        asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
-        lb.trace[8 * tile + k] = t;
-    }
-}
-
-__device__ __forceinline__ void report_status_enc(unsigned long long* st, uint32_t epoch, uint32_t code) {
+__device__ __forceinline__ void enc_report(unsigned long long* st, uint32_t epoch, uint32_t code) {
     if (st) *st = ((unsigned long long)epoch << 32) | code;
 }
 
-struct __align__(16) WarpBuf {
-    uint8_t stage[kWTStage + 16];  // the sub-tile's integers at +16 (+ the 4 before), packed in place from 0
-    uint8_t ctrl[kWTGroups];
-};
-
-static inline uint32_t encode_tiles(uint64_t n) {
-    const uint64_t ngroups = (n + 3) >> 2;
-    const uint64_t nsub = (ngroups + kWTGroups - 1) / kWTGroups;
-    return (uint32_t)((nsub + kCTWarps - 1) / kCTWarps);
+__device__ __forceinline__ uint32_t lens4(uint4 x, uint32_t cnt) {
+    return (cnt > 0 ? dev_byte_length(x.x) : 0u) + (cnt > 1 ? dev_byte_length(x.y) : 0u) +
+           (cnt > 2 ? dev_byte_length(x.z) : 0u) + (cnt > 3 ? dev_byte_length(x.w) : 0u);
 }
 
 // ---------------------------------------------------------------------------
-// encode
+// 1. size scan: warp w of a chunk CTA sizes sub-tiles 8w .. 8w+7
 // ---------------------------------------------------------------------------
-constexpr int kEncWindow = 512;
+template <bool kDelta>
+__global__ void __launch_bounds__(256)
+    svb_size_scan_kernel(const uint32_t* __restrict__ in, uint64_t n, uint32_t prev, DecodeMeta meta,
+                         uint64_t* __restrict__ d_out_len, unsigned long long* status, uint32_t epoch) {
+    __shared__ uint32_t wt[8];
+    __shared__ unsigned long long wt64[8];
+    __shared__ bool last;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const uint32_t chunk = blockIdx.x, nchunks = gridDim.x;
+    const uint64_t ngroups = (n + 3) >> 2;
+    const uint32_t tail_r = (uint32_t)(n & 3);
+    const uint64_t nsub = (ngroups + kWTGroups - 1) / kWTGroups;
+    const bool in16 = (((uintptr_t)in) & 15) == 0;
+    uint32_t my_size = 0;  // lane k < 8: size of sub-tile 8*warp + k
+#pragma unroll 1
+    for (int k = 0; k < 8; ++k) {
+        const uint64_t s = (uint64_t)chunk * kChunkSubs + 8 * warp + k;
+        if (s >= nsub) break;
+        const uint64_t g0 = s * kWTGroups;
+        uint32_t last_w = prev;
+        if (kDelta && g0) last_w = __ldg(in + 4 * g0 - 1);
+        uint4 x[kWTRows];
+        uint32_t cnt[kWTRows];
+#pragma unroll
+        for (int j = 0; j < kWTRows; ++j) {
+            const uint64_t g = g0 + 32 * j + lane;
+            cnt[j] = group_count(g, ngroups, tail_r);
+            x[j] = make_uint4(0, 0, 0, 0);
+            if (cnt[j] == 4 && in16) {
+                x[j] = ldg_stream_v4(in + 4 * g);
+            } else if (cnt[j]) {
+                x[j].x = __ldg(in + 4 * g);
+                if (cnt[j] > 1) x[j].y = __ldg(in + 4 * g + 1);
+                if (cnt[j] > 2) x[j].z = __ldg(in + 4 * g + 2);
+                if (cnt[j] > 3) x[j].w = __ldg(in + 4 * g + 3);
+            }
+        }
+        uint32_t acc = 0;
+#pragma unroll
+        for (int j = 0; j < kWTRows; ++j) {
+            uint4 v = x[j];
+            if constexpr (kDelta) {
+                uint32_t p = __shfl_up_sync(kFull, v.w, 1);
+                if (lane == 0) p = last_w;
+                last_w = __shfl_sync(kFull, v.w, 31);
+                v = make_uint4(v.x - p, v.y - v.x, v.z - v.y, v.w - v.z);
+            }
+            acc += lens4(v, cnt[j]);
+        }
+#pragma unroll
+        for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(kFull, acc, o);
+        if (lane == k) my_size = acc;
+    }
+    // chunk-local exclusive prefix over the 64 sub-tiles (lanes 0..7 of each warp)
+    const uint32_t v = lane < 8 ? my_size : 0u;
+    const uint32_t incl = warp_inclusive_scan(v);
+    if (lane == 31) wt[warp] = incl;
+    __syncthreads();
+    uint32_t wpre = 0, total = 0;
+#pragma unroll
+    for (int w = 0; w < 8; ++w) {
+        wpre += w < warp ? wt[w] : 0u;
+        total += wt[w];
+    }
+    const uint64_t s = (uint64_t)chunk * kChunkSubs + 8 * warp + lane;
+    if (lane < 8 && s < nsub) meta.localpre[s] = wpre + incl - v;
+    if (tid == 0) meta.chunkpre[chunk] = total;
+    __syncthreads();
+    if (tid == 0) {
+        __threadfence();
+        last = atomicAdd(meta.counters, 1u) == nchunks - 1;
+    }
+    __syncthreads();
+    if (!last) return;
+    __threadfence();
+    const unsigned long long tot = cta_exclusive_scan<unsigned long long, 8>(meta.chunkpre, nchunks, wt64);
+    if (tid == 0) {
+        meta.chunkpre[nchunks] = tot;
+        if (d_out_len) *d_out_len = ngroups + tot;
+        enc_report(status, epoch, 0u);
+        *meta.counters = 0;
+    }
+}
 
-struct EncShared {
-    uint32_t tot[kCTWarps];
-    unsigned long long off;
+// ---------------------------------------------------------------------------
+// 2. encode tiles
+// ---------------------------------------------------------------------------
+struct __align__(16) EncBuf {
+    uint8_t stage[kWTStage + 16];  // [0,16): the 4 integers before the sub-tile, [16, 16+4096): the sub-tile
+    uint8_t ctrl[kWTGroups];
 };
 
 template <bool kDelta>
-__global__ void __launch_bounds__(kCTThreads, 5)
+__global__ void __launch_bounds__(kCTThreads, 4)
     svb_encode_tile_kernel(const uint32_t* __restrict__ in, uint64_t n, uint32_t prev, uint8_t* __restrict__ out,
-                           uint64_t* __restrict__ d_out_len, LookbackArgs lb) {
-    __shared__ __align__(128) WarpBuf wb[kCTWarps];
-    __shared__ __align__(8) uint64_t bars[kCTWarps];
-    __shared__ __align__(128) LookbackWin<kEncWindow> lbw;
-    __shared__ EncShared sh;
+                           DecodeMeta meta) {
+    __shared__ __align__(128) EncBuf wb[kCTWarps];
+    __shared__ __align__(16) uint32_t slocal[kCTWarps + 8];
+    __shared__ __align__(16) unsigned long long schunk[4];
+    __shared__ __align__(8) uint64_t bars[kCTWarps + 1];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint32_t tile = blockIdx.x;
     const uint64_t ngroups = (n + 3) >> 2;
     const uint32_t tail_r = (uint32_t)(n & 3);
-    const uint64_t sub = (uint64_t)tile * kCTWarps + warp;
+    const uint64_t sub0 = (uint64_t)tile * kCTWarps;
+    const uint64_t chunk = sub0 / kChunkSubs;
+    const uint64_t sub = sub0 + warp;
     const uint64_t g0 = sub * kWTGroups;
     const bool active = g0 < ngroups;
-    WarpBuf& b = wb[warp];
-    trace_ts(lb, tile, 0);
+    EncBuf& b = wb[warp];
+    if (threadIdx.x == 0) {
+        mbar_init1(&bars[kCTWarps]);
+        mbar_expect(&bars[kCTWarps], 48 + 32);
+        tma_load(slocal, meta.localpre + sub0, 48, &bars[kCTWarps]);
+        tma_load(schunk, meta.chunkpre + (chunk & ~1ull), 32, &bars[kCTWarps]);
+    }
     if (lane == 0) mbar_init1(&bars[warp]);
-    if (threadIdx.x == 0) mbar_init1(&lbw.bar);
     __syncthreads();
+    if (!active) return;  // no CTA-wide barrier below
 
-    EncodeTile t;
-    t.total = 0;
-    uint32_t cnt_g = 0;
-    if (active) {
-        cnt_g = (uint32_t)(ngroups - g0 < (uint64_t)kWTGroups ? ngroups - g0 : (uint64_t)kWTGroups);
-        const uint64_t i0 = 4 * g0;
-        const uint32_t nints = (uint32_t)(n - i0 < (uint64_t)kWTInts ? n - i0 : (uint64_t)kWTInts);
-        // stage [0,16): the 4 integers before the sub-tile (delta seed), [16, 16+4*nints): the sub-tile
+    // the sub-tile's integers (and the 4 before it) -> stage
+    const uint64_t i0 = 4 * g0;
+    const uint32_t nints = (uint32_t)(n - i0 < (uint64_t)kWTInts ? n - i0 : (uint64_t)kWTInts);
+    {
         const uintptr_t lo = (uintptr_t)in, hi = lo + 4 * n;
         const uintptr_t beg = (uintptr_t)(in + i0) - (g0 ? 16 : 0), end = (uintptr_t)(in + i0 + nints);
         const uint32_t tx = tma_cover_bytes(beg, end, lo, hi);
@@ -91,111 +172,88 @@ __global__ void __launch_bounds__(kCTThreads, 5)
                 tma_load(dst, reinterpret_cast<const void*>(beg), tx, &bars[warp]);
             }
             mbar_wait_parity(&bars[warp], 0);
-            trace_ts(lb, tile, 1);
         } else {
             uint32_t* d32 = reinterpret_cast<uint32_t*>(dst);
             const uint32_t words = (uint32_t)((end - beg) >> 2);
             for (uint32_t i = lane; i < words; i += 32) d32[i] = __ldg(reinterpret_cast<const uint32_t*>(beg) + i);
             __syncwarp();
         }
-        uint32_t P[3] = {0, 0, 0};
-        uint32_t last_w = g0 ? reinterpret_cast<const uint32_t*>(b.stage)[3] : prev;
+    }
+    // lengths, control bytes, tile-local offsets
+    EncodeTile t;
+    uint32_t P[3] = {0, 0, 0};
+    uint32_t last_w = g0 ? reinterpret_cast<const uint32_t*>(b.stage)[3] : prev;
 #pragma unroll
-        for (int j = 0; j < kWTRows; ++j) {
-            const uint32_t cnt = group_count(g0 + 32 * j + lane, ngroups, tail_r);
-            uint4 x = *reinterpret_cast<const uint4*>(b.stage + 16 + 512 * j + 16 * lane);
-            x = mask_tail(x, cnt);
-            if constexpr (kDelta) {
-                uint32_t p = __shfl_up_sync(kFull, x.w, 1);
-                if (lane == 0) p = last_w;
-                last_w = __shfl_sync(kFull, x.w, 31);
-                x = make_uint4(x.x - p, x.y - x.x, x.z - x.y, x.w - x.z);
-            }
-            t.d[j] = x;
-            const uint32_t l0 = cnt > 0 ? dev_byte_length(x.x) : 0u;
-            const uint32_t l1 = cnt > 1 ? dev_byte_length(x.y) : 0u;
-            const uint32_t l2 = cnt > 2 ? dev_byte_length(x.z) : 0u;
-            const uint32_t l3 = cnt > 3 ? dev_byte_length(x.w) : 0u;
-            t.lens[j] = l0 | (l1 << 8) | (l2 << 16) | (l3 << 24);
-            P[j / 3] |= (l0 + l1 + l2 + l3) << (10 * (j % 3));
-            b.ctrl[32 * j + lane] = (uint8_t)((l0 - 1) | (l1 ? ((l1 - 1) << 2) : 0u) | (l2 ? ((l2 - 1) << 4) : 0u) |
-                                              (l3 ? ((l3 - 1) << 6) : 0u));
+    for (int j = 0; j < kWTRows; ++j) {
+        const uint32_t cnt = group_count(g0 + 32 * j + lane, ngroups, tail_r);
+        uint4 x = mask_tail(*reinterpret_cast<const uint4*>(b.stage + 16 + 512 * j + 16 * lane), cnt);
+        if constexpr (kDelta) {
+            uint32_t p = __shfl_up_sync(kFull, x.w, 1);
+            if (lane == 0) p = last_w;
+            last_w = __shfl_sync(kFull, x.w, 31);
+            x = make_uint4(x.x - p, x.y - x.x, x.z - x.y, x.w - x.z);
         }
-        t.total = packed_row_scan(P, t.qw);
-        trace_ts(lb, tile, 2);
+        t.d[j] = x;
+        const uint32_t l0 = cnt > 0 ? dev_byte_length(x.x) : 0u;
+        const uint32_t l1 = cnt > 1 ? dev_byte_length(x.y) : 0u;
+        const uint32_t l2 = cnt > 2 ? dev_byte_length(x.z) : 0u;
+        const uint32_t l3 = cnt > 3 ? dev_byte_length(x.w) : 0u;
+        t.lens[j] = l0 | (l1 << 8) | (l2 << 16) | (l3 << 24);
+        P[j / 3] |= (l0 + l1 + l2 + l3) << (10 * (j % 3));
+        b.ctrl[32 * j + lane] = (uint8_t)((l0 - 1) | (l1 ? ((l1 - 1) << 2) : 0u) | (l2 ? ((l2 - 1) << 4) : 0u) |
+                                          (l3 ? ((l3 - 1) << 6) : 0u));
     }
-    // publish the tile's byte count before packing so successors can look back past it
-    if (lane == 0) sh.tot[warp] = t.total;
-    __syncthreads();
-    uint32_t wex = 0, ctot = 0;
-#pragma unroll
-    for (int k = 0; k < kCTWarps; ++k) {
-        const uint32_t x = sh.tot[k];
-        wex += k < warp ? x : 0u;
-        ctot += x;
+    t.total = packed_row_scan(P, t.qw);
+    const uint32_t cnt_g = (uint32_t)(ngroups - g0 < (uint64_t)kWTGroups ? ngroups - g0 : (uint64_t)kWTGroups);
+    // where the data goes
+    mbar_wait_parity(&bars[kCTWarps], 0);
+    const unsigned long long cpre = schunk[chunk & 1];
+    const uint64_t off = cpre + slocal[warp];
+    const uintptr_t dbeg = (uintptr_t)out + ngroups + off, dend = dbeg + t.total;
+    const uint32_t head = (uint32_t)(dbeg & 15);
+    // pack in place at the destination's 16-B phase: group g's bytes end at or before
+    // head + 16(g+1) <= 16 + 16g + 15 < its successor's input (every input is in registers)
+    __syncwarp();
+    encode_pack_at(t, b.stage, head);
+    fence_async_smem();
+    __syncwarp();
+    uint8_t* cdst = out + g0;
+    const uint32_t cb = (((uintptr_t)cdst & 15) == 0) ? (cnt_g & ~15u) : 0u;
+    const uintptr_t a_lo = (dbeg + 15) & ~(uintptr_t)15, a_hi = dend & ~(uintptr_t)15;
+    const uint32_t db = a_hi > a_lo ? (uint32_t)(a_hi - a_lo) : 0u;
+    if (lane == 0) {
+        if (cb) tma_store(cdst, b.ctrl, cb);
+        if (db) tma_store(reinterpret_cast<void*>(a_lo), b.stage + (a_lo - dbeg) + head, db);
+        if (cb || db) tma_store_commit();
     }
-    if (warp == 0) {
-        // warp 0 resolves the tile offset right away, overlapping the other warps' packing
-        lb_publish(lb.off_status, tile, lb.epoch, 0, ctot);
-        uint32_t phase = 0;
-        uint64_t off = 0;
-        if (tile != 0) {
-            if (lb.debug_flags & 2) {
-                uint32_t st3[3] = {0, 0, 0};
-                unsigned long long ta, tb;
-                asm volatile("mov.u64 %0, %globaltimer;" : "=l"(ta));
-                off = lookback_exclusive_wide(lb.off_status, tile, lb.epoch, st3);
-                asm volatile("mov.u64 %0, %globaltimer;" : "=l"(tb));
-                if (lb.trace && lane == 0)
-                    lb.trace[8 * tile + 7] = ((unsigned long long)(st3[1] & 0xFF) << 56) |
-                                             ((unsigned long long)(st3[0] & 0xFF) << 48) |
-                                             ((unsigned long long)(st3[2] / 1) & 0xFFFFFF) << 24 | ((tb - ta) & 0xFFFFFF);
-            } else {
-                off = lookback_tma<kEncWindow>(lb.off_status, tile, lb.epoch, lbw, phase,
-                                               lb.trace ? lb.trace + 8 * tile + 7 : nullptr);
-            }
-            if (lane == 0) st_relaxed_gpu(lb.off_status + tile, pack_status(lb.epoch, kFlagInclusive, off + ctot));
-        }
-        if (lane == 0) sh.off = off;
+    for (uint32_t i = cb + lane; i < cnt_g; i += 32) cdst[i] = b.ctrl[i];
+    // edge bytes shared with the neighbouring sub-tiles' 16-B granules
+    for (uint32_t i = lane; i < t.total; i += 32) {
+        const uintptr_t x = dbeg + i;
+        if (db == 0 || x < a_lo || x >= a_hi) *reinterpret_cast<uint8_t*>(x) = b.stage[head + i];
     }
-    if (active) {
-        // control bytes: one bulk store of the 16-B multiple, byte stores for the rest
-        uint8_t* cdst = out + g0;
-        const uint32_t cb = (((uintptr_t)cdst & 15) == 0) ? (cnt_g & ~15u) : 0u;
-        fence_async_smem();
-        __syncwarp();
-        if (lane == 0 && cb) {
-            tma_store(cdst, b.ctrl, cb);
-            tma_store_commit();
-        }
-        for (uint32_t i = cb + lane; i < cnt_g; i += 32) cdst[i] = b.ctrl[i];
-        // in place: group g's packed bytes end at or before its own input (stage + 16 + 16 g)
-        encode_pack(t, b.stage);
-        trace_ts(lb, tile, 3);
-    }
-    trace_ts(lb, tile, 4);
-    __syncthreads();
-    trace_ts(lb, tile, 5);
-    const uint64_t cta_off = sh.off;
-    if (active) {
-        __syncwarp();
-        encode_writeout(b.stage, (uintptr_t)out + ngroups + cta_off + wex, t.total);
-        if (lane == 0) tma_store_wait_read();
-    }
-    // (slot 7 carries the look-back statistics)
-    if (tile == gridDim.x - 1 && threadIdx.x == 0) {
-        if (d_out_len) *d_out_len = ngroups + cta_off + ctot;
-        report_status_enc(lb.status, lb.epoch, 0u);
-    }
+    if (lane == 0 && (cb || db)) tma_store_wait_read();
 }
 
-cudaError_t launch_encode2(const uint32_t* in, uint64_t n, int delta, uint32_t prev, uint8_t* out,
-                           uint64_t* d_out_len, const LookbackArgs& lb, cudaStream_t stream) {
-    const int grid = (int)encode_tiles(n);
-    if (delta)
-        svb_encode_tile_kernel<true><<<grid, kCTThreads, 0, stream>>>(in, n, prev, out, d_out_len, lb);
-    else
-        svb_encode_tile_kernel<false><<<grid, kCTThreads, 0, stream>>>(in, n, prev, out, d_out_len, lb);
+// ---------------------------------------------------------------------------
+// launcher (metadata layout shared with the decode: localpre / chunkpre / counters)
+// ---------------------------------------------------------------------------
+cudaError_t launch_encode3(const uint32_t* in, uint64_t n, int delta, uint32_t prev, uint8_t* out,
+                           uint64_t* d_out_len, void* meta_ws, unsigned long long* status, uint32_t epoch,
+                           cudaStream_t stream, int* launches) {
+    const DecodeMeta m = carve_decode_meta(meta_ws, n);
+    const uint64_t ngroups = (n + 3) >> 2;
+    const uint64_t nsub = (ngroups + kWTGroups - 1) / kWTGroups;
+    const uint32_t nchunks = (uint32_t)((nsub + kChunkSubs - 1) / kChunkSubs);
+    const uint32_t tiles = (uint32_t)((nsub + kCTWarps - 1) / kCTWarps);
+    if (delta) {
+        svb_size_scan_kernel<true><<<nchunks, 256, 0, stream>>>(in, n, prev, m, d_out_len, status, epoch);
+        svb_encode_tile_kernel<true><<<tiles, kCTThreads, 0, stream>>>(in, n, prev, out, m);
+    } else {
+        svb_size_scan_kernel<false><<<nchunks, 256, 0, stream>>>(in, n, prev, m, d_out_len, status, epoch);
+        svb_encode_tile_kernel<false><<<tiles, kCTThreads, 0, stream>>>(in, n, prev, out, m);
+    }
+    *launches = 2;
     return cudaGetLastError();
 }
 

@@ -28,9 +28,10 @@ cudaError_t launch_decode3(const uint8_t* in, uint64_t in_len, uint64_t n, int d
                            cudaStream_t stream, int* launches, unsigned long long* trace = nullptr);
 uint64_t decode_meta_bytes(uint64_t n);
 int occupancy_decode_pipe();
-// Single-array encode: CTA tiles of 8 x 1024 integers, TMA staging, TMA-polled look-back.
-cudaError_t launch_encode2(const uint32_t* in, uint64_t n, int delta, uint32_t prev, uint8_t* out,
-                           uint64_t* d_out_len, const LookbackArgs& lb, cudaStream_t stream);
+// Single-array encode (svb_encode.cu): size scan + tile encode; meta_ws as for the decode.
+cudaError_t launch_encode3(const uint32_t* in, uint64_t n, int delta, uint32_t prev, uint8_t* out,
+                           uint64_t* d_out_len, void* meta_ws, unsigned long long* status, uint32_t epoch,
+                           cudaStream_t stream, int* launches);
 uint32_t decode2_chunks(uint64_t n);  // look-back tiles of the offsets pre-pass
 uint32_t decode2_tiles(uint64_t n);   // look-back tiles (CTAs) of the tile decode
 cudaError_t launch_encode(const uint32_t* in, uint64_t n, int delta, uint32_t prev, uint8_t* out,

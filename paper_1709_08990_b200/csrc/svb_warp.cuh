@@ -373,13 +373,13 @@ __device__ __forceinline__ void encode_load(const uint32_t* __restrict__ in, uin
     t.total = packed_row_scan(P, t.qw);
 }
 
-// Write every integer's bytes at its tile-local offset (stage byte 0 = tile data byte 0).
-__device__ __forceinline__ void encode_pack(const EncodeTile& t, uint8_t* stage) {
+// Write every integer's bytes at its tile-local offset + base (stage byte base = tile data byte 0).
+__device__ __forceinline__ void encode_pack_at(const EncodeTile& t, uint8_t* stage, uint32_t base) {
 #pragma unroll
     for (int j = 0; j < kWTRows; ++j) {
         const uint32_t l = t.lens[j];
         if (l) {
-            uint32_t p = (t.qw[j >> 1] >> (16 * (j & 1))) & 0xFFFFu;
+            uint32_t p = base + ((t.qw[j >> 1] >> (16 * (j & 1))) & 0xFFFFu);
             const uint32_t l0 = l & 0xFFu, l1 = (l >> 8) & 0xFFu, l2 = (l >> 16) & 0xFFu, l3 = l >> 24;
             put_int_bytes(stage, p, t.d[j].x, l0);
             p += l0;
@@ -391,6 +391,8 @@ __device__ __forceinline__ void encode_pack(const EncodeTile& t, uint8_t* stage)
         }
     }
 }
+
+__device__ __forceinline__ void encode_pack(const EncodeTile& t, uint8_t* stage) { encode_pack_at(t, stage, 0); }
 
 // Copy stage bytes [0, total) to global [beg, beg + total): aligned 128-bit
 // stores for interior chunks (unaligned shared reads via funnel shifts), byte
