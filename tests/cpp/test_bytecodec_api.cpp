@@ -1,0 +1,105 @@
+// C++ drop-in test: a reference-style caller of namespace bytecodec (reference
+// proj/core/include/bytecodec/{codec,stream_vbyte}.hpp signatures) linked
+// against libbytecodec_b200.so.  Checks SPEC golden vectors (SPEC.md:308-320,
+// 372-383, erratum E1), round trips, malformed input errors and the
+// random-access API.  Exit code 0 = pass.
+#include <cstdint>
+#include <cstdio>
+#include <cstdlib>
+#include <random>
+#include <vector>
+
+#include "bytecodec/codec.hpp"
+#include "bytecodec/stream_vbyte.hpp"
+
+using namespace bytecodec;
+
+static int failures = 0;
+#define CHECK(cond)                                                       \
+    do {                                                                  \
+        if (!(cond)) {                                                    \
+            std::fprintf(stderr, "FAIL %s:%d: %s\n", __FILE__, __LINE__, #cond); \
+            ++failures;                                                   \
+        }                                                                 \
+    } while (0)
+
+int main() {
+    // Fig. 3 values: control [0xC1, 0x40] + 13 data bytes (E1)
+    const std::vector<uint32_t> fig3 = {1024, 12, 10, 1073741824, 1, 2, 3, 1024};
+    const std::vector<uint8_t> fig3_bytes = {0xC1, 0x40, 0, 4, 12, 10, 0, 0, 0, 64, 1, 2, 3, 0, 4};
+    CHECK(svb_encode(fig3) == fig3_bytes);
+    CHECK(svb_decode(fig3_bytes, 8) == fig3);
+    CHECK(svb_encode(std::vector<uint32_t>{0, 0, 0, 0}) == (std::vector<uint8_t>{0, 0, 0, 0, 0}));
+    CHECK(svb_encode(std::vector<uint32_t>{}).empty());
+    CHECK(svb_tables().length[0x00] == 4 && svb_tables().length[0xFF] == 16 && svb_tables().length[0xC1] == 8);
+    CHECK(byte_length(0) == 1 && byte_length(1024) == 2 && byte_length(1073741824) == 4);
+
+    // delta: prefix of (3,4,12,1) -> (3,7,19,20); base chaining
+    {
+        const std::vector<uint32_t> xs = {3, 7, 19, 20};
+        encoded_buffer b = encode(codec_id::stream_vbyte, xs, true);
+        CHECK(b.codec == codec_id::stream_vbyte && b.count == 4 && b.delta);
+        CHECK(b.bytes == svb_encode(std::vector<uint32_t>{3, 4, 12, 1}));
+        CHECK(decode(b) == xs);
+        std::vector<uint32_t> out(4);
+        const uint32_t last = decode_payload_delta(codec_id::stream_vbyte, svb_encode(std::vector<uint32_t>{0, 0, 0, 0}),
+                                                   4, 42, out.data());
+        CHECK(last == 42 && out == (std::vector<uint32_t>{42, 42, 42, 42}));
+    }
+    // random round trips incl. prev-seeded delta encode (extension E2) and wrap-around
+    std::mt19937_64 rng(7);
+    for (int it = 0; it < 40; ++it) {
+        const size_t n = it < 20 ? (size_t)it : (size_t)(rng() % 200000);
+        std::vector<uint32_t> v(n);
+        for (auto& x : v) x = (uint32_t)(rng() >> (rng() % 33));
+        const auto enc = svb_encode(v);
+        CHECK(svb_decode(enc, n) == v);
+        const uint32_t prev = (uint32_t)rng();
+        const auto encd = svb_encode_delta(v, prev);
+        std::vector<uint32_t> out(n);
+        const uint32_t last = svb_decode_delta(encd, n, prev, out.data());
+        CHECK(out == v);
+        CHECK(last == (n ? v.back() : prev));
+        // random access: every block through the offset index
+        if (n) {
+            const auto offs = svb_block_data_offsets(enc, n);
+            CHECK(offs.size() == svb_control_bytes(n));
+            const size_t k = (size_t)(rng() % offs.size());
+            uint32_t blk[4];
+            const size_t cnt = svb_decode_block(enc, n, k, offs[k], blk);
+            CHECK(cnt == (k + 1) * 4 <= n ? 4 : n - 4 * k);
+            for (size_t i = 0; i < cnt; ++i) CHECK(blk[i] == v[4 * k + i]);
+        }
+    }
+    // malformed input -> codec_error with the reference taxonomy (codec.hpp:28-58)
+    {
+        const std::vector<uint32_t> v = {1, 300, 70000, 1u << 31, 5};
+        auto enc = svb_encode(v);
+        std::vector<uint32_t> out(5);
+        auto expect_errc = [&](std::vector<uint8_t> bytes, errc want) {
+            try {
+                svb_decode(bytes, 5, out.data());
+                CHECK(false);
+            } catch (const codec_error& e) {
+                CHECK(e.code() == want);
+            }
+        };
+        expect_errc(std::vector<uint8_t>(enc.begin(), enc.end() - 1), errc::truncated);
+        auto longer = enc;
+        longer.push_back(0);
+        expect_errc(longer, errc::trailing_bytes);
+        expect_errc(std::vector<uint8_t>(enc.begin(), enc.begin() + 1), errc::truncated);
+        try {
+            encode(codec_id::vbyte, v);
+            CHECK(false);
+        } catch (const codec_error& e) {
+            CHECK(e.code() == errc::unsupported);
+        }
+    }
+    if (failures) {
+        std::fprintf(stderr, "%d failures\n", failures);
+        return 1;
+    }
+    std::printf("bytecodec C++ API: all checks passed\n");
+    return 0;
+}
