@@ -311,7 +311,7 @@ int bcgpu_svb_decode_device(bcgpu_ctx* c, const uint8_t* d_in, size_t in_len, si
     if (st) return st;
     int launches = 0;
     BC_CUDA(launch_decode3(d_in, in_len, n, delta, base, d_out, d_last, c->offs, status_ptr(c), c->epoch,
-                           c->pipe_grid, s, &launches, c->trace));
+                           c->pipe_grid, s, &launches, c->trace, c->debug_flags));
     g_launches.fetch_add((uint64_t)launches);
     return BCGPU_OK;
 }

@@ -327,6 +327,215 @@ __global__ void __launch_bounds__(kCTThreads, 5)
     if (kDelta && tile == gridDim.x - 1 && threadIdx.x == 0 && d_last) *d_last = carry + csum;
 }
 
+// ---------------------------------------------------------------------------
+// 2'./3'. pooled decode: one CTA per 8*K sub-tiles, one TMA for all their bytes
+// ---------------------------------------------------------------------------
+// The CTA's sub-tiles are consecutive, so their compressed bytes are one
+// contiguous range: thread 0 issues a single bulk copy of it into a pool sized
+// by the host from the stream's average compression (so compressible streams
+// put 2-4x more sub-tiles in flight per SM than a worst-case 4 KiB per warp),
+// plus one bulk copy of the 256*8K control bytes.  Round r of the CTA is
+// sub-tiles s0 + 8r + warp; if the whole range does not fit the pool the
+// rounds are loaded one at a time (each <= 32 KiB).  Outputs leave as 128-bit
+// stores straight from registers; delta carries are known up front from the
+// sums pass (scanned chunk carry + the earlier sub-tiles' sums).
+struct PoolShared {
+    uint32_t loc[40];                 // localpre[s0 .. s0+36)
+    unsigned long long chk[4];        // chunkpre[(c & ~1) .. +4)
+    uint32_t carry[32];               // delta: carry before each of the CTA's sub-tiles (without base)
+    uint32_t part[8];
+    uint64_t bar_meta, bar_ctrl, bar_data[4];
+};
+
+template <int kMode, int K>
+__global__ void __launch_bounds__(kCTThreads)
+    svb_decode_pool_kernel(const uint8_t* __restrict__ in, uint64_t in_len, uint64_t n, uint32_t base,
+                           uint32_t* __restrict__ out, uint32_t* __restrict__ d_last, DecodeMeta meta,
+                           uint32_t pool_bytes) {
+    constexpr int S = kCTWarps * K;  // sub-tiles per CTA (divides kChunkSubs)
+    static_assert(kChunkSubs % S == 0 && S <= 32, "CTA sub-tiles must stay inside one chunk");
+    extern __shared__ __align__(128) uint8_t dsm[];
+    uint8_t* sctrl = dsm;                           // S * 256 control bytes
+    uint8_t* pool = dsm + S * kWTGroups;            // compressed data
+    __shared__ __align__(16) PoolShared sh;
+    __shared__ bool single;
+    constexpr bool kDelta = kMode == kModeDelta;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint64_t ngroups = (n + 3) >> 2;
+    const uint32_t tail_r = (uint32_t)(n & 3);
+    const uint64_t nsub = (ngroups + kWTGroups - 1) / kWTGroups;
+    const uint64_t s0 = (uint64_t)blockIdx.x * S;
+    const uint64_t chunk = s0 / kChunkSubs;
+    const uint32_t ns = (uint32_t)(nsub - s0 < (uint64_t)S ? nsub - s0 : (uint64_t)S);
+    const uintptr_t lo = (uintptr_t)in, hi = lo + in_len;
+    const uintptr_t data0 = lo + ngroups;
+
+    if (threadIdx.x == 0) {
+        mbar_init1(&sh.bar_meta);
+        mbar_init1(&sh.bar_ctrl);
+#pragma unroll
+        for (int r = 0; r < 4; ++r) mbar_init1(&sh.bar_data[r]);
+        constexpr uint32_t lb = (uint32_t)(((S + 4) * 4 + 15) & ~15);
+        mbar_expect(&sh.bar_meta, lb + 32);
+        tma_load(sh.loc, meta.localpre + s0, lb, &sh.bar_meta);
+        tma_load(sh.chk, meta.chunkpre + (chunk & ~1ull), 32, &sh.bar_meta);
+        // control bytes of the whole CTA in one transaction (no offsets needed)
+        const uintptr_t cb = lo + s0 * kWTGroups;
+        const uint64_t cg = ngroups - s0 * kWTGroups < (uint64_t)S * kWTGroups ? ngroups - s0 * kWTGroups
+                                                                                : (uint64_t)S * kWTGroups;
+        const uint32_t ctx = tma_cover_bytes(cb, cb + cg, lo, hi);
+        if (ctx != 0xFFFFFFFFu && (cb & 15) == 0 && ctx) {
+            mbar_expect(&sh.bar_ctrl, ctx);
+            tma_load(sctrl, reinterpret_cast<const void*>(cb), ctx, &sh.bar_ctrl);
+        } else {
+            for (uint64_t i = 0; i < cg; ++i) sctrl[i] = __ldg(in + s0 * kWTGroups + i);
+            mbar_arrive(&sh.bar_ctrl);
+        }
+    }
+    // delta: carry parts = scanned chunk carry + sums of this chunk's sub-tiles before s0
+    uint32_t part = 0;
+    if constexpr (kDelta) {
+        const uint64_t c0 = chunk * kChunkSubs;
+        for (uint64_t i = c0 + threadIdx.x; i < s0; i += kCTThreads) part += __ldg(meta.subsums + i);
+        if (threadIdx.x == 0) part += __ldg(meta.chunksums + chunk);
+        part = warp_sum_u32(part);
+        if (lane == 0) sh.part[warp] = part;
+        if (threadIdx.x < S) sh.carry[threadIdx.x] = threadIdx.x < ns ? __ldg(meta.subsums + s0 + threadIdx.x) : 0u;
+    }
+    __syncthreads();
+    mbar_wait_parity(&sh.bar_meta, 0);
+    const unsigned long long cpre = sh.chk[chunk & 1];
+    auto sub_off = [&](uint32_t i) -> unsigned long long {  // data offset of sub-tile s0 + i, i <= ns
+        if (i == ns && (s0 + ns == nsub || (s0 + ns) % kChunkSubs == 0)) return sh.chk[(chunk & 1) + 1];
+        return cpre + sh.loc[i];
+    };
+    const unsigned long long A = sub_off(0), B = sub_off(ns);
+    const uintptr_t abeg = data0 + A;
+    if (threadIdx.x == 0) {
+        const uint32_t tx = tma_cover_bytes(abeg, data0 + B, lo, hi);
+        single = tx != 0xFFFFFFFFu && tx + 16 <= pool_bytes;
+        if (single && tx) {
+            mbar_expect(&sh.bar_data[0], tx);
+            tma_load(pool, reinterpret_cast<const void*>(abeg & ~(uintptr_t)15), tx, &sh.bar_data[0]);
+        } else if (single) {
+            mbar_arrive(&sh.bar_data[0]);
+        }
+    }
+    if constexpr (kDelta) {
+        if (threadIdx.x == 0) {  // exclusive prefix of the CTA's sub-tile sums + the CTA carry
+            uint32_t c = base;
+#pragma unroll
+            for (int k = 0; k < kCTWarps; ++k) c += sh.part[k];
+            for (int i = 0; i < S; ++i) {
+                const uint32_t x = sh.carry[i];
+                sh.carry[i] = c;
+                c += x;
+            }
+        }
+    }
+    __syncthreads();
+    mbar_wait_parity(&sh.bar_ctrl, 0);
+    if (single) mbar_wait_parity(&sh.bar_data[0], 0);
+    const bool out16 = (((uintptr_t)out) & 15) == 0;
+    for (int r = 0; r < K; ++r) {
+        // round r = sub-tiles s0 + 8r .. s0 + 8r + 7 (contiguous data)
+        uintptr_t pbase = abeg;  // global address of pool byte (pbase & 15)
+        if (!single) {
+            const uint32_t i0 = (uint32_t)(8 * r), i1 = (uint32_t)(8 * r + 8) < ns ? (uint32_t)(8 * r + 8) : ns;
+            __syncthreads();  // previous round fully consumed
+            if (i0 < ns) {
+                pbase = data0 + sub_off(i0);
+                const uintptr_t pend = data0 + sub_off(i1);
+                if (threadIdx.x == 0) fence_async_smem();
+                const uint32_t tx = tma_cover_bytes(pbase, pend, lo, hi);
+                if (tx != 0xFFFFFFFFu && tx + 16 <= pool_bytes) {
+                    if (threadIdx.x == 0) {
+                        if (tx) {
+                            mbar_expect(&sh.bar_data[r], tx);
+                            tma_load(pool, reinterpret_cast<const void*>(pbase & ~(uintptr_t)15), tx, &sh.bar_data[r]);
+                        } else {
+                            mbar_arrive(&sh.bar_data[r]);
+                        }
+                    }
+                    mbar_wait_parity(&sh.bar_data[r], 0);
+                } else {
+                    // malformed or edge: guarded copy by the whole CTA, clamped to the pool
+                    const uintptr_t a0 = pbase & ~(uintptr_t)15;
+                    uintptr_t a1 = (pend + 15) & ~(uintptr_t)15;
+                    if (a1 - a0 > pool_bytes - 16) a1 = a0 + ((pool_bytes - 16) & ~15u);
+                    for (uint32_t c = threadIdx.x; c < (uint32_t)((a1 - a0) >> 4); c += kCTThreads)
+                        *reinterpret_cast<uint4*>(pool + 16 * c) = load_chunk_guarded(a0 + 16 * (uintptr_t)c, lo, hi);
+                    __syncthreads();
+                }
+            }
+        }
+        const uint32_t i = (uint32_t)(8 * r + warp);
+        if (i >= ns) continue;
+        const uint64_t s = s0 + i;
+        const uint64_t g0 = s * kWTGroups;
+        const WarpCtrl w = load_warp_ctrl<true>(sctrl + (uint32_t)i * kWTGroups, g0, ngroups, tail_r, g0);
+        const uint32_t* W = reinterpret_cast<const uint32_t*>(pool);
+        const unsigned long long so = sub_off(i);
+        const uintptr_t sbeg = data0 + so;
+        uint32_t head = (uint32_t)(sbeg - (pbase & ~(uintptr_t)15));
+        if (head > pool_bytes - 32) head = pool_bytes - 32;  // malformed streams only: keep reads in the pool
+        if constexpr (kMode == kModeSums) {
+            uint32_t acc = 0;
+#pragma unroll
+            for (int j = 0; j < kWTRows; ++j) {
+                const uint32_t c = row_ctrl(w, j);
+                const uint32_t bb = head + row_q(w, j);
+                const uint32_t cnt = group_count(g0 + 32 * j + lane, ngroups, tail_r);
+                if (__all_sync(kFull, c == 0)) {
+                    const uint32_t x = __funnelshift_r(W[bb >> 2], W[(bb >> 2) + 1], (bb & 3u) * 8u);
+                    acc += byte_sum4(x & (cnt >= 4 ? 0xFFFFFFFFu : ((1u << (8 * cnt)) - 1u)));
+                } else {
+                    const uint4 v = mask_tail(decode_group(W, bb, c), cnt);
+                    acc += v.x + v.y + v.z + v.w;
+                }
+            }
+            acc = warp_sum_u32(acc);
+            if (lane == 0) {
+                meta.subsums[s] = acc;
+                atomicAdd(meta.chunksums + chunk, acc);  // RED.ADD, mod 2^32
+            }
+        } else {
+            uint32_t run = kDelta ? sh.carry[i] : 0u;
+#pragma unroll
+            for (int j = 0; j < kWTRows; ++j) {
+                const uint32_t c = row_ctrl(w, j);
+                const uint32_t bb = head + row_q(w, j);
+                const bool allzero = __all_sync(kFull, c == 0);
+                uint4 v = allzero ? decode_zero_group(W, bb) : decode_group(W, bb, c);
+                const uint64_t g = g0 + 32 * j + lane;
+                const uint32_t cnt = group_count(g, ngroups, tail_r);
+                if constexpr (kDelta) {
+                    v = prefix4(mask_tail(v, cnt));
+                    const uint32_t Sx = v.w;
+                    const uint32_t I = warp_inclusive_scan(Sx);
+                    v = add4(v, run + I - Sx);
+                    run += __shfl_sync(kFull, I, 31);
+                }
+                if (cnt) store_group(out + 4 * g, v, cnt, out16);
+            }
+            if (kDelta && s == nsub - 1 && lane == 0 && d_last) *d_last = run;
+        }
+    }
+    if constexpr (kMode == kModeSums) {
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            __threadfence();
+            single = atomicAdd(meta.counters + 1, 1u) == gridDim.x - 1;  // reuse: "last CTA"
+        }
+        __syncthreads();
+        if (!single) return;
+        __threadfence();
+        const uint32_t nchunks = (uint32_t)((nsub + kChunkSubs - 1) / kChunkSubs);
+        cta_exclusive_scan<uint32_t, kCTWarps>(meta.chunksums, nchunks, sh.part);
+        if (threadIdx.x == 0) meta.counters[1] = 0;
+    }
+}
+
 }  // namespace bcgpu
 
 namespace bcgpu {
@@ -346,7 +555,7 @@ DecodeMeta carve_decode_meta(void* ws, uint64_t n) {
     m.counters = reinterpret_cast<unsigned int*>(p);  // 16 B, persists across calls (self-resetting)
     p += 16;
     m.localpre = reinterpret_cast<uint32_t*>(p);
-    p += align16(4 * (nsub + 16));
+    p += align16(4 * (nsub + 64));
     m.chunkpre = reinterpret_cast<unsigned long long*>(p);
     p += align16(8 * (nchunks + 4));
     m.subsums = reinterpret_cast<uint32_t*>(p);
@@ -359,7 +568,7 @@ uint64_t decode_meta_bytes(uint64_t n) {
     const uint64_t ngroups = (n + 3) >> 2;
     const uint64_t nsub = (ngroups + kWTGroups - 1) / kWTGroups;
     const uint64_t nchunks = (nsub + kChunkSubs - 1) / kChunkSubs;
-    return 16 + align16(4 * (nsub + 16)) + align16(8 * (nchunks + 4)) + align16(4 * nsub) + align16(4 * (nchunks + 1)) +
+    return 16 + align16(4 * (nsub + 64)) + align16(8 * (nchunks + 4)) + align16(4 * nsub) + align16(4 * (nchunks + 1)) +
            64;
 }
 
@@ -367,7 +576,7 @@ int occupancy_decode_pipe() { return 1; }  // the tile kernel is not persistent
 
 cudaError_t launch_decode3(const uint8_t* in, uint64_t in_len, uint64_t n, int delta, uint32_t base, uint32_t* out,
                            uint32_t* d_last, void* meta_ws, unsigned long long* status, uint32_t epoch, int pipe_grid,
-                           cudaStream_t stream, int* launches, unsigned long long* trace) {
+                           cudaStream_t stream, int* launches, unsigned long long* trace, uint32_t debug_flags) {
     DecodeMeta m = carve_decode_meta(meta_ws, n);
     m.trace = trace;
     const uint64_t ngroups = (n + 3) >> 2;
@@ -377,6 +586,43 @@ cudaError_t launch_decode3(const uint8_t* in, uint64_t in_len, uint64_t n, int d
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
     (void)pipe_grid;
+    // pooled decode: K sub-tiles per warp and the pool from the stream's average density
+    const double dpb = nsub ? (double)(in_len > ngroups ? in_len - ngroups : 0) / (double)nsub : 0.0;  // B / sub-tile
+    const int K = dpb < 1400.0 ? 4 : 2;
+    const uint32_t S = (uint32_t)(kCTWarps * K);
+    uint64_t pool = (uint64_t)(1.2 * dpb * S) + 64;
+    const uint64_t round_max = 8ull * kWTDataMax + 64;  // one round, worst case
+    if (pool < round_max) pool = round_max;
+    if (pool > 160 * 1024) pool = 160 * 1024;
+    pool = (pool + 15) & ~15ull;
+    const uint32_t smem = (uint32_t)(S * kWTGroups + pool);
+    const int pgrid = (int)((nsub + S - 1) / S);
+    if (!(debug_flags & 4)) {
+#define BC_POOL_LAUNCH(MODE, KK)                                                                                 \
+    do {                                                                                                         \
+        static const cudaError_t a_ = cudaFuncSetAttribute(svb_decode_pool_kernel<MODE, KK>,                    \
+                                                           cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024); \
+        if (a_ != cudaSuccess) return a_;                                                                        \
+        svb_decode_pool_kernel<MODE, KK><<<pgrid, kCTThreads, smem, stream>>>(in, in_len, n, base, out, d_last, m,  \
+                                                                             (uint32_t)pool);                   \
+    } while (0)
+        if (delta) {
+            if (K == 4) {
+                BC_POOL_LAUNCH(kModeSums, 4);
+                BC_POOL_LAUNCH(kModeDelta, 4);
+            } else {
+                BC_POOL_LAUNCH(kModeSums, 2);
+                BC_POOL_LAUNCH(kModeDelta, 2);
+            }
+            *launches = 3;
+        } else {
+            if (K == 4) BC_POOL_LAUNCH(kModePlain, 4);
+            else BC_POOL_LAUNCH(kModePlain, 2);
+            *launches = 2;
+        }
+#undef BC_POOL_LAUNCH
+        return cudaGetLastError();
+    }
     const int grid = (int)((nsub + kCTWarps - 1) / kCTWarps);
     if (delta) {
         svb_decode_tile_kernel<kModeSums><<<grid, kCTThreads, 0, stream>>>(in, in_len, n, base, out, d_last, m);

@@ -227,10 +227,13 @@ __global__ void __launch_bounds__(kCTThreads, 4)
         if (cb || db) tma_store_commit();
     }
     for (uint32_t i = cb + lane; i < cnt_g; i += 32) cdst[i] = b.ctrl[i];
-    // edge bytes shared with the neighbouring sub-tiles' 16-B granules
-    for (uint32_t i = lane; i < t.total; i += 32) {
-        const uintptr_t x = dbeg + i;
-        if (db == 0 || x < a_lo || x >= a_hi) *reinterpret_cast<uint8_t*>(x) = b.stage[head + i];
+    // edge bytes shared with the neighbouring sub-tiles' 16-B granules (< 16 at each end)
+    if (db == 0) {
+        for (uint32_t i = lane; i < t.total; i += 32) *reinterpret_cast<uint8_t*>(dbeg + i) = b.stage[head + i];
+    } else {
+        const uint32_t nh = (uint32_t)(a_lo - dbeg), nt = (uint32_t)(dend - a_hi);
+        if (lane < nh) *reinterpret_cast<uint8_t*>(dbeg + lane) = b.stage[head + lane];
+        if (lane < nt) *reinterpret_cast<uint8_t*>(a_hi + lane) = b.stage[head + (uint32_t)(a_hi - dbeg) + lane];
     }
     if (lane == 0 && (cb || db)) tma_store_wait_read();
 }

@@ -25,7 +25,8 @@ struct LookbackArgs {
 // first 16 bytes zero-initialised once and self-resetting).
 cudaError_t launch_decode3(const uint8_t* in, uint64_t in_len, uint64_t n, int delta, uint32_t base, uint32_t* out,
                            uint32_t* d_last, void* meta_ws, unsigned long long* status, uint32_t epoch, int pipe_grid,
-                           cudaStream_t stream, int* launches, unsigned long long* trace = nullptr);
+                           cudaStream_t stream, int* launches, unsigned long long* trace = nullptr,
+                           uint32_t debug_flags = 0);
 uint64_t decode_meta_bytes(uint64_t n);
 int occupancy_decode_pipe();
 // Single-array encode (svb_encode.cu): size scan + tile encode; meta_ws as for the decode.

@@ -374,10 +374,34 @@ __device__ __forceinline__ void encode_load(const uint32_t* __restrict__ in, uin
 }
 
 // Write every integer's bytes at its tile-local offset + base (stage byte base = tile data byte 0).
+// A row whose 128 integers all take one byte (the usual case for small
+// deltas) packs as 32 consecutive 4-byte words: each lane assembles its 4 low
+// bytes with PRMT and stores the aligned word it starts (merged with its left
+// neighbour's tail through a funnel shift); only the row's first and last
+// partial words go out as bytes.  Every other row stores byte by byte.
 __device__ __forceinline__ void encode_pack_at(const EncodeTile& t, uint8_t* stage, uint32_t base) {
+    const int lane = threadIdx.x & 31;
+    uint32_t* W = reinterpret_cast<uint32_t*>(stage);
 #pragma unroll
     for (int j = 0; j < kWTRows; ++j) {
         const uint32_t l = t.lens[j];
+        if (__all_sync(kFull, l == 0x01010101u)) {
+            const uint4 x = t.d[j];
+            const uint32_t P = __byte_perm(__byte_perm(x.x, x.y, 0x0040), __byte_perm(x.z, x.w, 0x0040), 0x5410);
+            const uint32_t Pp = __shfl_up_sync(kFull, P, 1);
+            const uint32_t p = base + ((t.qw[j >> 1] >> (16 * (j & 1))) & 0xFFFFu);
+            const uint32_t s = p & 3u;
+            if (s == 0) {
+                W[p >> 2] = P;
+            } else {
+                if (lane > 0) W[p >> 2] = __funnelshift_r(Pp, P, 8u * (4u - s));
+                if (lane == 0)
+                    for (uint32_t b = 0; b < 4u - s; ++b) stage[p + b] = (uint8_t)(P >> (8 * b));
+                if (lane == 31)
+                    for (uint32_t b = 4u - s; b < 4u; ++b) stage[p + b] = (uint8_t)(P >> (8 * b));
+            }
+            continue;
+        }
         if (l) {
             uint32_t p = base + ((t.qw[j >> 1] >> (16 * (j & 1))) & 0xFFFFu);
             const uint32_t l0 = l & 0xFFu, l1 = (l >> 8) & 0xFFu, l2 = (l >> 16) & 0xFFu, l3 = l >> 24;
