@@ -21,6 +21,7 @@
 #include <cstdint>
 
 #include "svb_device.cuh"
+#include "svb_fast.cuh"
 #include "svb_kernels.cuh"
 #include "svb_tma.cuh"
 #include "svb_scan.cuh"
@@ -473,6 +474,30 @@ __global__ void __launch_bounds__(kCTThreads)
         if (i >= ns) continue;
         const uint64_t s = s0 + i;
         const uint64_t g0 = s * kWTGroups;
+        uint32_t head0;
+        {
+            const unsigned long long so0 = sub_off(i);
+            head0 = (uint32_t)(data0 + so0 - (pbase & ~(uintptr_t)15));
+        }
+        if ((uint64_t)(s + 1) * kWTInts <= n && head0 <= pool_bytes - 32) {
+            // full sub-tile: lean path (svb_fast.cuh)
+            const WarpCtrl wf = ctrl_full(sh_addr(sctrl) + i * kWTGroups);
+            const uint32_t sd = sh_addr(pool) + head0;
+            uint32_t* o = out + s * kWTInts;
+            if constexpr (kMode == kModeSums) {
+                const uint32_t acc = warp_sum_u32(expand_full<2>(wf, sd, o, out16, 0));
+                if (lane == 0) {
+                    meta.subsums[s] = acc;
+                    atomicAdd(meta.chunksums + chunk, acc);  // RED.ADD, mod 2^32
+                }
+            } else if constexpr (kMode == kModeDelta) {
+                const uint32_t run = expand_full<1>(wf, sd, o, out16, sh.carry[i]);
+                if (s == nsub - 1 && lane == 0 && d_last) *d_last = run;
+            } else {
+                expand_full<0>(wf, sd, o, out16, 0);
+            }
+            continue;
+        }
         const WarpCtrl w = load_warp_ctrl<true>(sctrl + (uint32_t)i * kWTGroups, g0, ngroups, tail_r, g0);
         const uint32_t* W = reinterpret_cast<const uint32_t*>(pool);
         const unsigned long long so = sub_off(i);

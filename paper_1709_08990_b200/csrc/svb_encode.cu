@@ -18,6 +18,7 @@
 #include <cstdint>
 
 #include "svb_device.cuh"
+#include "svb_fast.cuh"
 #include "svb_kernels.cuh"
 #include "svb_scan.cuh"
 #include "svb_tma.cuh"
@@ -179,42 +180,54 @@ __global__ void __launch_bounds__(kCTThreads, 4)
             __syncwarp();
         }
     }
-    // lengths, control bytes, tile-local offsets
-    EncodeTile t;
-    uint32_t P[3] = {0, 0, 0};
-    uint32_t last_w = g0 ? reinterpret_cast<const uint32_t*>(b.stage)[3] : prev;
-#pragma unroll
-    for (int j = 0; j < kWTRows; ++j) {
-        const uint32_t cnt = group_count(g0 + 32 * j + lane, ngroups, tail_r);
-        uint4 x = mask_tail(*reinterpret_cast<const uint4*>(b.stage + 16 + 512 * j + 16 * lane), cnt);
-        if constexpr (kDelta) {
-            uint32_t p = __shfl_up_sync(kFull, x.w, 1);
-            if (lane == 0) p = last_w;
-            last_w = __shfl_sync(kFull, x.w, 31);
-            x = make_uint4(x.x - p, x.y - x.x, x.z - x.y, x.w - x.z);
-        }
-        t.d[j] = x;
-        const uint32_t l0 = cnt > 0 ? dev_byte_length(x.x) : 0u;
-        const uint32_t l1 = cnt > 1 ? dev_byte_length(x.y) : 0u;
-        const uint32_t l2 = cnt > 2 ? dev_byte_length(x.z) : 0u;
-        const uint32_t l3 = cnt > 3 ? dev_byte_length(x.w) : 0u;
-        t.lens[j] = l0 | (l1 << 8) | (l2 << 16) | (l3 << 24);
-        P[j / 3] |= (l0 + l1 + l2 + l3) << (10 * (j % 3));
-        b.ctrl[32 * j + lane] = (uint8_t)((l0 - 1) | (l1 ? ((l1 - 1) << 2) : 0u) | (l2 ? ((l2 - 1) << 4) : 0u) |
-                                          (l3 ? ((l3 - 1) << 6) : 0u));
-    }
-    t.total = packed_row_scan(P, t.qw);
     const uint32_t cnt_g = (uint32_t)(ngroups - g0 < (uint64_t)kWTGroups ? ngroups - g0 : (uint64_t)kWTGroups);
+    const bool full = 4 * (g0 + kWTGroups) <= n;
+    uint32_t total;
+    uint32_t lens[kWTRows], qw[4];
+    EncodeTile t;
+    const uint32_t prev_w = g0 ? reinterpret_cast<const uint32_t*>(b.stage)[3] : prev;
+    if (full) {
+        // lengths, control bytes, tile-local offsets (lean path, svb_fast.cuh)
+        total = enc_full_lengths<kDelta>(sh_addr(b.stage) + 16, prev_w, sh_addr(b.ctrl), lens, qw);
+    } else {
+        uint32_t P[3] = {0, 0, 0};
+        uint32_t last_w = prev_w;
+#pragma unroll
+        for (int j = 0; j < kWTRows; ++j) {
+            const uint32_t cnt = group_count(g0 + 32 * j + lane, ngroups, tail_r);
+            uint4 x = mask_tail(*reinterpret_cast<const uint4*>(b.stage + 16 + 512 * j + 16 * lane), cnt);
+            if constexpr (kDelta) {
+                uint32_t p = __shfl_up_sync(kFull, x.w, 1);
+                if (lane == 0) p = last_w;
+                last_w = __shfl_sync(kFull, x.w, 31);
+                x = make_uint4(x.x - p, x.y - x.x, x.z - x.y, x.w - x.z);
+            }
+            t.d[j] = x;
+            const uint32_t l0 = cnt > 0 ? dev_byte_length(x.x) : 0u;
+            const uint32_t l1 = cnt > 1 ? dev_byte_length(x.y) : 0u;
+            const uint32_t l2 = cnt > 2 ? dev_byte_length(x.z) : 0u;
+            const uint32_t l3 = cnt > 3 ? dev_byte_length(x.w) : 0u;
+            t.lens[j] = l0 | (l1 << 8) | (l2 << 16) | (l3 << 24);
+            P[j / 3] |= (l0 + l1 + l2 + l3) << (10 * (j % 3));
+            b.ctrl[32 * j + lane] = (uint8_t)((l0 - 1) | (l1 ? ((l1 - 1) << 2) : 0u) | (l2 ? ((l2 - 1) << 4) : 0u) |
+                                              (l3 ? ((l3 - 1) << 6) : 0u));
+        }
+        t.total = packed_row_scan(P, t.qw);
+        total = t.total;
+    }
     // where the data goes
     mbar_wait_parity(&bars[kCTWarps], 0);
     const unsigned long long cpre = schunk[chunk & 1];
     const uint64_t off = cpre + slocal[warp];
-    const uintptr_t dbeg = (uintptr_t)out + ngroups + off, dend = dbeg + t.total;
+    const uintptr_t dbeg = (uintptr_t)out + ngroups + off, dend = dbeg + total;
     const uint32_t head = (uint32_t)(dbeg & 15);
     // pack in place at the destination's 16-B phase: group g's bytes end at or before
-    // head + 16(g+1) <= 16 + 16g + 15 < its successor's input (every input is in registers)
+    // head + 16(g+1) <= 16 + 16g + 15 < the input of group g+1 (stage + 16 + 16(g+1))
     __syncwarp();
-    encode_pack_at(t, b.stage, head);
+    if (full)
+        enc_full_pack<kDelta>(sh_addr(b.stage) + 16, prev_w, lens, qw, sh_addr(b.stage) + head);
+    else
+        encode_pack_at(t, b.stage, head);
     fence_async_smem();
     __syncwarp();
     uint8_t* cdst = out + g0;
@@ -229,7 +242,7 @@ __global__ void __launch_bounds__(kCTThreads, 4)
     for (uint32_t i = cb + lane; i < cnt_g; i += 32) cdst[i] = b.ctrl[i];
     // edge bytes shared with the neighbouring sub-tiles' 16-B granules (< 16 at each end)
     if (db == 0) {
-        for (uint32_t i = lane; i < t.total; i += 32) *reinterpret_cast<uint8_t*>(dbeg + i) = b.stage[head + i];
+        for (uint32_t i = lane; i < total; i += 32) *reinterpret_cast<uint8_t*>(dbeg + i) = b.stage[head + i];
     } else {
         const uint32_t nh = (uint32_t)(a_lo - dbeg), nt = (uint32_t)(dend - a_hi);
         if (lane < nh) *reinterpret_cast<uint8_t*>(dbeg + lane) = b.stage[head + lane];

@@ -1,0 +1,222 @@
+// svb_fast.cuh -- lean inner loops for full sub-tiles (every sub-tile but the
+// stream's last): 32-bit shared-memory addressing, no per-lane bounds or tail
+// logic, row-major 128-bit I/O.  The general paths in svb_warp.cuh remain for
+// the final, partial sub-tile.
+#pragma once
+
+#include "svb_device.cuh"
+#include "svb_warp.cuh"
+
+namespace bcgpu {
+
+__device__ __forceinline__ uint32_t sh_addr(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ uint32_t lds8(uint32_t a) {
+    uint32_t v;
+    asm("ld.shared.u8 %0, [%1];" : "=r"(v) : "r"(a));
+    return v;
+}
+__device__ __forceinline__ uint32_t lds32(uint32_t a) {
+    uint32_t v;
+    asm("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(a));
+    return v;
+}
+__device__ __forceinline__ uint4 lds128(uint32_t a) {
+    uint4 v;
+    asm("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(a));
+    return v;
+}
+// ordered against the surrounding shared stores (in-place passes)
+__device__ __forceinline__ uint4 lds128v(uint32_t a) {
+    uint4 v;
+    asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(a) : "memory");
+    return v;
+}
+__device__ __forceinline__ void sts8(uint32_t a, uint32_t v) {
+    asm volatile("st.shared.u8 [%0], %1;" ::"r"(a), "r"(v) : "memory");
+}
+__device__ __forceinline__ void sts32(uint32_t a, uint32_t v) {
+    asm volatile("st.shared.u32 [%0], %1;" ::"r"(a), "r"(v) : "memory");
+}
+
+// Control bytes of a full sub-tile at shared address sc (row j, lane l <-> byte 32j + l).
+__device__ __forceinline__ WarpCtrl ctrl_full(uint32_t sc) {
+    const int lane = threadIdx.x & 31;
+    WarpCtrl w;
+    w.cw[0] = w.cw[1] = 0;
+    uint32_t P[3] = {0, 0, 0};
+#pragma unroll
+    for (int j = 0; j < kWTRows; ++j) {
+        const uint32_t c = lds8(sc + 32 * j + lane);
+        w.cw[j >> 2] |= c << (8 * (j & 3));
+        P[j / 3] |= (fsum(c) + 4u) << (10 * (j % 3));
+    }
+    w.total = packed_row_scan(P, w.qw);
+    return w;
+}
+
+// integer of l bytes at shared byte address a
+__device__ __forceinline__ uint32_t extract_s(uint32_t a, uint32_t l) {
+    const uint32_t w = a & ~3u;
+    const uint32_t x = __funnelshift_r(lds32(w), lds32(w + 4), (a & 3u) << 3);
+    return x & (0xFFFFFFFFu >> ((4u - l) << 3));
+}
+
+// one control byte c whose data starts at shared byte address a
+__device__ __forceinline__ uint4 group_s(uint32_t a, uint32_t c) {
+    const uint32_t l0 = (c & 3u) + 1u, l1 = ((c >> 2) & 3u) + 1u, l2 = ((c >> 4) & 3u) + 1u, l3 = (c >> 6) + 1u;
+    uint4 v;
+    v.x = extract_s(a, l0);
+    a += l0;
+    v.y = extract_s(a, l1);
+    a += l1;
+    v.z = extract_s(a, l2);
+    a += l2;
+    v.w = extract_s(a, l3);
+    return v;
+}
+
+// control byte 0: four 1-byte integers
+__device__ __forceinline__ uint4 zero_group_s(uint32_t a) {
+    const uint32_t w = a & ~3u;
+    const uint32_t x = __funnelshift_r(lds32(w), lds32(w + 4), (a & 3u) << 3);
+    return make_uint4(__byte_perm(x, 0u, 0x4440), __byte_perm(x, 0u, 0x4441), __byte_perm(x, 0u, 0x4442),
+                      __byte_perm(x, 0u, 0x4443));
+}
+
+__device__ __forceinline__ uint32_t byte_sum4_fast(uint32_t w) {
+    const uint32_t s = (w & 0x00FF00FFu) + ((w >> 8) & 0x00FF00FFu);
+    return (s & 0xFFFFu) + (s >> 16);
+}
+
+// kMode: 0 plain store, 1 delta store (run = value before the sub-tile), 2 sum only.
+// sd = shared address of the sub-tile's first data byte; o = the sub-tile's first output integer.
+template <int kMode>
+__device__ __forceinline__ uint32_t expand_full(const WarpCtrl& w, uint32_t sd, uint32_t* __restrict__ o, bool o16,
+                                                uint32_t run) {
+    const int lane = threadIdx.x & 31;
+    uint32_t acc = 0;
+#pragma unroll
+    for (int j = 0; j < kWTRows; ++j) {
+        const uint32_t c = row_ctrl(w, j);
+        const uint32_t a = sd + row_q(w, j);
+        const bool allzero = __all_sync(kFull, c == 0);
+        if constexpr (kMode == 2) {
+            if (allzero) {
+                const uint32_t wa = a & ~3u;
+                acc += byte_sum4_fast(__funnelshift_r(lds32(wa), lds32(wa + 4), (a & 3u) << 3));
+            } else {
+                const uint4 v = group_s(a, c);
+                acc += v.x + v.y + v.z + v.w;
+            }
+        } else {
+            uint4 v = allzero ? zero_group_s(a) : group_s(a, c);
+            if constexpr (kMode == 1) {
+                v.y += v.x;
+                v.z += v.y;
+                v.w += v.z;
+                const uint32_t I = warp_inclusive_scan(v.w);
+                const uint32_t add = run + I - v.w;
+                v.x += add;
+                v.y += add;
+                v.z += add;
+                v.w += add;
+                run += __shfl_sync(kFull, I, 31);
+            }
+            uint32_t* p = o + 128 * j + 4 * lane;
+            if (o16) {
+                stg_stream_v4(p, v);
+            } else {
+                p[0] = v.x;
+                p[1] = v.y;
+                p[2] = v.z;
+                p[3] = v.w;
+            }
+        }
+    }
+    return kMode == 2 ? acc : run;
+}
+
+}  // namespace bcgpu
+
+namespace bcgpu {
+
+// ---- encode, full sub-tiles --------------------------------------------------
+__device__ __forceinline__ uint32_t blen(uint32_t x) { return 4u - (__clz(x | 1u) >> 3); }  // codec.hpp:70-72
+
+// Row j of the sub-tile (integers at shared address sin + 512 j + 16 lane), as
+// values or mod-2^32 deltas; `last` carries x_{-1} in and the row's last raw value out.
+template <bool kDelta>
+__device__ __forceinline__ uint4 enc_row(uint32_t sin, int j, uint32_t& last) {
+    const int lane = threadIdx.x & 31;
+    uint4 x = lds128v(sin + 512 * j + 16 * lane);
+    if constexpr (kDelta) {
+        uint32_t p = __shfl_up_sync(kFull, x.w, 1);
+        if (lane == 0) p = last;
+        last = __shfl_sync(kFull, x.w, 31);
+        x = make_uint4(x.x - p, x.y - x.x, x.z - x.y, x.w - x.z);
+    }
+    return x;
+}
+
+// Pass 1: byte lengths, control bytes (-> shared sctrl), tile-local offsets; returns the data size.
+template <bool kDelta>
+__device__ __forceinline__ uint32_t enc_full_lengths(uint32_t sin, uint32_t prev_w, uint32_t sctrl,
+                                                     uint32_t (&lens)[kWTRows], uint32_t (&qw)[4]) {
+    const int lane = threadIdx.x & 31;
+    uint32_t P[3] = {0, 0, 0};
+    uint32_t last = prev_w;
+#pragma unroll
+    for (int j = 0; j < kWTRows; ++j) {
+        const uint4 x = enc_row<kDelta>(sin, j, last);
+        const uint32_t l0 = blen(x.x), l1 = blen(x.y), l2 = blen(x.z), l3 = blen(x.w);
+        lens[j] = l0 | (l1 << 8) | (l2 << 16) | (l3 << 24);
+        P[j / 3] |= (l0 + l1 + l2 + l3) << (10 * (j % 3));
+        sts8(sctrl + 32 * j + lane, (l0 - 1) | ((l1 - 1) << 2) | ((l2 - 1) << 4) | ((l3 - 1) << 6));
+    }
+    return packed_row_scan(P, qw);
+}
+
+__device__ __forceinline__ void sts_int_bytes(uint32_t a, uint32_t x, uint32_t l) {
+    sts8(a, x);
+    if (l > 1) sts8(a + 1, x >> 8);
+    if (l > 2) sts8(a + 2, x >> 16);
+    if (l > 3) sts8(a + 3, x >> 24);
+}
+
+// Pass 2: pack in place; tile data byte 0 goes to shared address sdst (<= sin - 1 + ...; see caller).
+template <bool kDelta>
+__device__ __forceinline__ void enc_full_pack(uint32_t sin, uint32_t prev_w, const uint32_t (&lens)[kWTRows],
+                                              const uint32_t (&qw)[4], uint32_t sdst) {
+    const int lane = threadIdx.x & 31;
+    uint32_t last = prev_w;
+#pragma unroll
+    for (int j = 0; j < kWTRows; ++j) {
+        const uint4 x = enc_row<kDelta>(sin, j, last);
+        const uint32_t l = lens[j];
+        const uint32_t a = sdst + ((qw[j >> 1] >> (16 * (j & 1))) & 0xFFFFu);
+        __syncwarp();  // every lane has read row j before any lane writes over it
+        if (__all_sync(kFull, l == 0x01010101u)) {
+            const uint32_t P = __byte_perm(__byte_perm(x.x, x.y, 0x0040), __byte_perm(x.z, x.w, 0x0040), 0x5410);
+            const uint32_t Pp = __shfl_up_sync(kFull, P, 1);
+            const uint32_t s = a & 3u;
+            if (s == 0) {
+                sts32(a, P);
+            } else {
+                if (lane > 0) sts32(a & ~3u, __funnelshift_r(Pp, P, 8u * (4u - s)));
+                if (lane == 0)
+                    for (uint32_t b = 0; b < 4u - s; ++b) sts8(a + b, P >> (8 * b));
+                if (lane == 31)
+                    for (uint32_t b = 4u - s; b < 4u; ++b) sts8(a + b, P >> (8 * b));
+            }
+        } else {
+            const uint32_t l0 = l & 0xFFu, l1 = (l >> 8) & 0xFFu, l2 = (l >> 16) & 0xFFu, l3 = l >> 24;
+            sts_int_bytes(a, x.x, l0);
+            sts_int_bytes(a + l0, x.y, l1);
+            sts_int_bytes(a + l0 + l1, x.z, l2);
+            sts_int_bytes(a + l0 + l1 + l2, x.w, l3);
+        }
+    }
+}
+
+}  // namespace bcgpu
