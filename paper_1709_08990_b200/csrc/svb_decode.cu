@@ -479,22 +479,28 @@ __global__ void __launch_bounds__(kCTThreads)
             const unsigned long long so0 = sub_off(i);
             head0 = (uint32_t)(data0 + so0 - (pbase & ~(uintptr_t)15));
         }
-        if ((uint64_t)(s + 1) * kWTInts <= n && head0 <= pool_bytes - 32) {
+        if ((uint64_t)(s + 1) * kWTInts <= n && head0 <= pool_bytes - 32 && (out16 || kMode == kModeSums)) {
             // full sub-tile: lean path (svb_fast.cuh)
-            const WarpCtrl wf = ctrl_full(sh_addr(sctrl) + i * kWTGroups);
+            bool zero;
+            const WarpCtrl wf = ctrl_full(sh_addr(sctrl) + i * kWTGroups, &zero);
             const uint32_t sd = sh_addr(pool) + head0;
             uint32_t* o = out + s * kWTInts;
             if constexpr (kMode == kModeSums) {
-                const uint32_t acc = warp_sum_u32(expand_full<2>(wf, sd, o, out16, 0));
+                const uint32_t acc =
+                    warp_sum_u32(zero ? expand_full<2, true>(wf, sd, o, 0) : expand_full<2, false>(wf, sd, o, 0));
                 if (lane == 0) {
                     meta.subsums[s] = acc;
                     atomicAdd(meta.chunksums + chunk, acc);  // RED.ADD, mod 2^32
                 }
             } else if constexpr (kMode == kModeDelta) {
-                const uint32_t run = expand_full<1>(wf, sd, o, out16, sh.carry[i]);
+                const uint32_t run = zero ? expand_full<1, true>(wf, sd, o, sh.carry[i])
+                                          : expand_full<1, false>(wf, sd, o, sh.carry[i]);
                 if (s == nsub - 1 && lane == 0 && d_last) *d_last = run;
             } else {
-                expand_full<0>(wf, sd, o, out16, 0);
+                if (zero)
+                    expand_full<0, true>(wf, sd, o, 0);
+                else
+                    expand_full<0, false>(wf, sd, o, 0);
             }
             continue;
         }

@@ -40,15 +40,23 @@ __device__ __forceinline__ void sts32(uint32_t a, uint32_t v) {
 }
 
 // Control bytes of a full sub-tile at shared address sc (row j, lane l <-> byte 32j + l).
-__device__ __forceinline__ WarpCtrl ctrl_full(uint32_t sc) {
+// Sets *all_zero (warp-uniform) and skips the offset scan when every control byte is 0:
+// then integer i of the sub-tile is data byte i.
+__device__ __forceinline__ WarpCtrl ctrl_full(uint32_t sc, bool* all_zero) {
     const int lane = threadIdx.x & 31;
     WarpCtrl w;
     w.cw[0] = w.cw[1] = 0;
+#pragma unroll
+    for (int j = 0; j < kWTRows; ++j) w.cw[j >> 2] |= lds8(sc + 32 * j + lane) << (8 * (j & 3));
+    *all_zero = __all_sync(kFull, (w.cw[0] | w.cw[1]) == 0);
+    if (*all_zero) {
+        w.total = kWTInts;
+        return w;
+    }
     uint32_t P[3] = {0, 0, 0};
 #pragma unroll
     for (int j = 0; j < kWTRows; ++j) {
-        const uint32_t c = lds8(sc + 32 * j + lane);
-        w.cw[j >> 2] |= c << (8 * (j & 3));
+        const uint32_t c = (w.cw[j >> 2] >> (8 * (j & 3))) & 0xFFu;
         P[j / 3] |= (fsum(c) + 4u) << (10 * (j % 3));
     }
     w.total = packed_row_scan(P, w.qw);
@@ -90,17 +98,24 @@ __device__ __forceinline__ uint32_t byte_sum4_fast(uint32_t w) {
 }
 
 // kMode: 0 plain store, 1 delta store (run = value before the sub-tile), 2 sum only.
-// sd = shared address of the sub-tile's first data byte; o = the sub-tile's first output integer.
-template <int kMode>
-__device__ __forceinline__ uint32_t expand_full(const WarpCtrl& w, uint32_t sd, uint32_t* __restrict__ o, bool o16,
-                                                uint32_t run) {
+// sd = shared address of the sub-tile's first data byte; o = the sub-tile's first output
+// integer (16-B aligned: callers take the general path otherwise).  kZero: every control
+// byte of the sub-tile is 0, so row j lane l's four 1-byte integers are data bytes 128j+4l..+3.
+template <int kMode, bool kZero>
+__device__ __forceinline__ uint32_t expand_full(const WarpCtrl& w, uint32_t sd, uint32_t* __restrict__ o, uint32_t run) {
     const int lane = threadIdx.x & 31;
     uint32_t acc = 0;
 #pragma unroll
     for (int j = 0; j < kWTRows; ++j) {
-        const uint32_t c = row_ctrl(w, j);
-        const uint32_t a = sd + row_q(w, j);
-        const bool allzero = __all_sync(kFull, c == 0);
+        uint32_t c = 0, a;
+        bool allzero = true;
+        if constexpr (kZero) {
+            a = sd + 128 * j + 4 * lane;
+        } else {
+            c = row_ctrl(w, j);
+            a = sd + row_q(w, j);
+            allzero = __all_sync(kFull, c == 0);
+        }
         if constexpr (kMode == 2) {
             if (allzero) {
                 const uint32_t wa = a & ~3u;
@@ -123,15 +138,7 @@ __device__ __forceinline__ uint32_t expand_full(const WarpCtrl& w, uint32_t sd, 
                 v.w += add;
                 run += __shfl_sync(kFull, I, 31);
             }
-            uint32_t* p = o + 128 * j + 4 * lane;
-            if (o16) {
-                stg_stream_v4(p, v);
-            } else {
-                p[0] = v.x;
-                p[1] = v.y;
-                p[2] = v.z;
-                p[3] = v.w;
-            }
+            stg_stream_v4(o + 128 * j + 4 * lane, v);
         }
     }
     return kMode == 2 ? acc : run;
@@ -173,6 +180,14 @@ __device__ __forceinline__ uint32_t enc_full_lengths(uint32_t sin, uint32_t prev
         lens[j] = l0 | (l1 << 8) | (l2 << 16) | (l3 << 24);
         P[j / 3] |= (l0 + l1 + l2 + l3) << (10 * (j % 3));
         sts8(sctrl + 32 * j + lane, (l0 - 1) | ((l1 - 1) << 2) | ((l2 - 1) << 4) | ((l3 - 1) << 6));
+    }
+    bool ones = true;
+#pragma unroll
+    for (int j = 0; j < kWTRows; ++j) ones = ones && lens[j] == 0x01010101u;
+    if (__all_sync(kFull, ones)) {  // every integer takes one byte: offsets are the identity
+#pragma unroll
+        for (int k = 0; k < 4; ++k) qw[k] = (256u * k + 4u * lane) | ((256u * k + 128u + 4u * lane) << 16);
+        return kWTInts;
     }
     return packed_row_scan(P, qw);
 }
