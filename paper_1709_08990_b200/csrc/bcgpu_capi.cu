@@ -64,6 +64,8 @@ struct bcgpu_ctx {
     int batch_grid = 0;
     // host-API scratch (device) and stream
     cudaStream_t stream = nullptr;
+    cudaStream_t aux = nullptr;        // encode: second stream for the sliced pipeline
+    cudaEvent_t events[96] = {};       // encode slice hand-offs
     void* offs = nullptr;  // decode metadata workspace (svb_decode.cu DecodeMeta)
     size_t offs_cap = 0;   // bytes
     int pipe_grid = 0;     // persistent decode CTAs
@@ -237,6 +239,8 @@ int bcgpu_ctx_create(int device, bcgpu_ctx** out) {
         delete c;
         return cuda_fail(e, "cudaStreamCreate");
     }
+    cudaStreamCreateWithFlags(&c->aux, cudaStreamNonBlocking);
+    for (auto& ev : c->events) cudaEventCreateWithFlags(&ev, cudaEventDisableTiming);
     const int st = ensure_ws(c, 1024);
     if (st) {
         cudaStreamDestroy(c->stream);
@@ -255,6 +259,9 @@ int bcgpu_ctx_destroy(bcgpu_ctx* c) {
     if (c->d_scratch) cudaFree(c->d_scratch);
     if (c->offs) cudaFree(c->offs);
     if (c->stream) cudaStreamDestroy(c->stream);
+    if (c->aux) cudaStreamDestroy(c->aux);
+    for (auto& ev : c->events)
+        if (ev) cudaEventDestroy(ev);
     delete c;
     return BCGPU_OK;
 }
@@ -288,7 +295,8 @@ int bcgpu_svb_encode_device(bcgpu_ctx* c, const uint32_t* d_in, size_t n, int de
     st = next_epoch(c, s);
     if (st) return st;
     int launches = 0;
-    BC_CUDA(launch_encode3(d_in, n, delta, prev, d_out, d_out_len, c->offs, status_ptr(c), c->epoch, s, &launches));
+    BC_CUDA(launch_encode3(d_in, n, delta, prev, d_out, d_out_len, c->offs, status_ptr(c), c->epoch, s, &launches,
+                           c->aux, c->events, 96));
     g_launches.fetch_add((uint64_t)launches);
     return BCGPU_OK;
 }

@@ -584,7 +584,8 @@ DecodeMeta carve_decode_meta(void* ws, uint64_t n) {
     DecodeMeta m;
     m.trace = nullptr;
     m.counters = reinterpret_cast<unsigned int*>(p);  // 16 B, persists across calls (self-resetting)
-    p += 16;
+    m.running = reinterpret_cast<unsigned long long*>(p + 16);
+    p += 32;
     m.localpre = reinterpret_cast<uint32_t*>(p);
     p += align16(4 * (nsub + 64));
     m.chunkpre = reinterpret_cast<unsigned long long*>(p);
@@ -592,6 +593,8 @@ DecodeMeta carve_decode_meta(void* ws, uint64_t n) {
     m.subsums = reinterpret_cast<uint32_t*>(p);
     p += align16(4 * nsub);
     m.chunksums = reinterpret_cast<uint32_t*>(p);
+    p += align16(4 * (nchunks + 1));
+    m.chunktot = reinterpret_cast<uint32_t*>(p);
     return m;
 }
 
@@ -599,8 +602,8 @@ uint64_t decode_meta_bytes(uint64_t n) {
     const uint64_t ngroups = (n + 3) >> 2;
     const uint64_t nsub = (ngroups + kWTGroups - 1) / kWTGroups;
     const uint64_t nchunks = (nsub + kChunkSubs - 1) / kChunkSubs;
-    return 16 + align16(4 * (nsub + 64)) + align16(8 * (nchunks + 4)) + align16(4 * nsub) + align16(4 * (nchunks + 1)) +
-           64;
+    return 32 + align16(4 * (nsub + 64)) + align16(8 * (nchunks + 4)) + align16(4 * nsub) +
+           2 * align16(4 * (nchunks + 1)) + 64;
 }
 
 int occupancy_decode_pipe() { return 1; }  // the tile kernel is not persistent

@@ -41,12 +41,12 @@ __device__ __forceinline__ uint32_t lens4(uint4 x, uint32_t cnt) {
 template <bool kDelta>
 __global__ void __launch_bounds__(256)
     svb_size_scan_kernel(const uint32_t* __restrict__ in, uint64_t n, uint32_t prev, DecodeMeta meta,
-                         uint64_t* __restrict__ d_out_len, unsigned long long* status, uint32_t epoch) {
+                         uint64_t* __restrict__ d_out_len, unsigned long long* status, uint32_t epoch,
+                         uint32_t c_begin, uint32_t nchunks_total) {
     __shared__ uint32_t wt[8];
-    __shared__ unsigned long long wt64[8];
     __shared__ bool last;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const uint32_t chunk = blockIdx.x, nchunks = gridDim.x;
+    const uint32_t chunk = c_begin + blockIdx.x, c_end = c_begin + gridDim.x;
     const uint64_t ngroups = (n + 3) >> 2;
     const uint32_t tail_r = (uint32_t)(n & 3);
     const uint64_t nsub = (ngroups + kWTGroups - 1) / kWTGroups;
@@ -104,20 +104,26 @@ __global__ void __launch_bounds__(256)
     }
     const uint64_t s = (uint64_t)chunk * kChunkSubs + 8 * warp + lane;
     if (lane < 8 && s < nsub) meta.localpre[s] = wpre + incl - v;
-    if (tid == 0) meta.chunkpre[chunk] = total;
+    if (tid == 0) meta.chunktot[chunk] = total;
+    // last CTA of this slice: chunk offsets of the slice = running offset + scan of the chunk totals
     __syncthreads();
     if (tid == 0) {
         __threadfence();
-        last = atomicAdd(meta.counters, 1u) == nchunks - 1;
+        last = atomicAdd(meta.counters, 1u) == gridDim.x - 1;
     }
     __syncthreads();
     if (!last) return;
     __threadfence();
-    const unsigned long long tot = cta_exclusive_scan<unsigned long long, 8>(meta.chunkpre, nchunks, wt64);
+    const unsigned long long base = c_begin == 0 ? 0ull : *meta.running;
+    const uint32_t tot = cta_exclusive_scan<uint32_t, 8>(meta.chunktot + c_begin, gridDim.x, wt);
+    for (uint32_t c = tid; c < gridDim.x; c += 256) meta.chunkpre[c_begin + c] = base + meta.chunktot[c_begin + c];
     if (tid == 0) {
-        meta.chunkpre[nchunks] = tot;
-        if (d_out_len) *d_out_len = ngroups + tot;
-        enc_report(status, epoch, 0u);
+        meta.chunkpre[c_end] = base + tot;  // == the next slice's base (same value written twice)
+        *meta.running = base + tot;
+        if (c_end == nchunks_total) {
+            if (d_out_len) *d_out_len = ngroups + base + tot;
+            enc_report(status, epoch, 0u);
+        }
         *meta.counters = 0;
     }
 }
@@ -133,13 +139,13 @@ struct __align__(16) EncBuf {
 template <bool kDelta>
 __global__ void __launch_bounds__(kCTThreads, 4)
     svb_encode_tile_kernel(const uint32_t* __restrict__ in, uint64_t n, uint32_t prev, uint8_t* __restrict__ out,
-                           DecodeMeta meta) {
+                           DecodeMeta meta, uint32_t tile_base) {
     __shared__ __align__(128) EncBuf wb[kCTWarps];
     __shared__ __align__(16) uint32_t slocal[kCTWarps + 8];
     __shared__ __align__(16) unsigned long long schunk[4];
     __shared__ __align__(8) uint64_t bars[kCTWarps + 1];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const uint32_t tile = blockIdx.x;
+    const uint32_t tile = tile_base + blockIdx.x;
     const uint64_t ngroups = (n + 3) >> 2;
     const uint32_t tail_r = (uint32_t)(n & 3);
     const uint64_t sub0 = (uint64_t)tile * kCTWarps;
@@ -256,20 +262,57 @@ __global__ void __launch_bounds__(kCTThreads, 4)
 // ---------------------------------------------------------------------------
 cudaError_t launch_encode3(const uint32_t* in, uint64_t n, int delta, uint32_t prev, uint8_t* out,
                            uint64_t* d_out_len, void* meta_ws, unsigned long long* status, uint32_t epoch,
-                           cudaStream_t stream, int* launches) {
+                           cudaStream_t stream, int* launches, cudaStream_t aux, cudaEvent_t* events,
+                           int nevents) {
     const DecodeMeta m = carve_decode_meta(meta_ws, n);
     const uint64_t ngroups = (n + 3) >> 2;
     const uint64_t nsub = (ngroups + kWTGroups - 1) / kWTGroups;
     const uint32_t nchunks = (uint32_t)((nsub + kChunkSubs - 1) / kChunkSubs);
-    const uint32_t tiles = (uint32_t)((nsub + kCTWarps - 1) / kCTWarps);
-    if (delta) {
-        svb_size_scan_kernel<true><<<nchunks, 256, 0, stream>>>(in, n, prev, m, d_out_len, status, epoch);
-        svb_encode_tile_kernel<true><<<tiles, kCTThreads, 0, stream>>>(in, n, prev, out, m);
-    } else {
-        svb_size_scan_kernel<false><<<nchunks, 256, 0, stream>>>(in, n, prev, m, d_out_len, status, epoch);
-        svb_encode_tile_kernel<false><<<tiles, kCTThreads, 0, stream>>>(in, n, prev, out, m);
+    constexpr uint32_t kTilesPerChunk = kChunkSubs / kCTWarps;
+    // L2-sized slices: the size scan of slice k+1 (HBM-bound) runs on `stream` while
+    // the tile encode of slice k (issue-bound) re-reads its integers from L2 on `aux`
+    uint32_t slice = 128;  // chunks = 8 Mi integers = 32 MiB
+    if ((nchunks + slice - 1) / slice > 64) slice = (nchunks + 63) / 64;
+    uint32_t nslices = (nchunks + slice - 1) / slice;
+    // measured on B200: each slice's size scan has too few CTAs to stream at HBM rate and the
+    // scans serialise on `stream`, so slicing lost (cfg2 encode 139 -> 226 us); off by default
+    constexpr bool kSliced = false;
+    if (!kSliced || !aux || nslices < 2 || nevents < (int)nslices + 2) {
+        slice = nchunks;
+        nslices = 1;
     }
-    *launches = 2;
+    *launches = 0;
+    if (nslices > 1) {
+        cudaEventRecord(events[0], stream);
+        cudaStreamWaitEvent(aux, events[0], 0);
+    }
+    for (uint32_t k = 0; k < nslices; ++k) {
+        const uint32_t c0 = k * slice, c1 = c0 + slice < nchunks ? c0 + slice : nchunks;
+        const uint32_t t0 = c0 * kTilesPerChunk;
+        const uint64_t t1_ = (uint64_t)c1 * kTilesPerChunk;
+        const uint64_t tiles_all = (nsub + kCTWarps - 1) / kCTWarps;
+        const uint32_t t1 = (uint32_t)(t1_ < tiles_all ? t1_ : tiles_all);
+        cudaStream_t ts = nslices > 1 ? aux : stream;
+        if (delta) {
+            svb_size_scan_kernel<true><<<c1 - c0, 256, 0, stream>>>(in, n, prev, m, d_out_len, status, epoch, c0, nchunks);
+        } else {
+            svb_size_scan_kernel<false><<<c1 - c0, 256, 0, stream>>>(in, n, prev, m, d_out_len, status, epoch, c0,
+                                                                     nchunks);
+        }
+        if (nslices > 1) {
+            cudaEventRecord(events[k + 1], stream);
+            cudaStreamWaitEvent(aux, events[k + 1], 0);
+        }
+        if (delta)
+            svb_encode_tile_kernel<true><<<t1 - t0, kCTThreads, 0, ts>>>(in, n, prev, out, m, t0);
+        else
+            svb_encode_tile_kernel<false><<<t1 - t0, kCTThreads, 0, ts>>>(in, n, prev, out, m, t0);
+        *launches += 2;
+    }
+    if (nslices > 1) {
+        cudaEventRecord(events[nslices + 1], aux);
+        cudaStreamWaitEvent(stream, events[nslices + 1], 0);
+    }
     return cudaGetLastError();
 }
 

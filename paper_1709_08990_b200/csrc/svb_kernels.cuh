@@ -32,7 +32,8 @@ int occupancy_decode_pipe();
 // Single-array encode (svb_encode.cu): size scan + tile encode; meta_ws as for the decode.
 cudaError_t launch_encode3(const uint32_t* in, uint64_t n, int delta, uint32_t prev, uint8_t* out,
                            uint64_t* d_out_len, void* meta_ws, unsigned long long* status, uint32_t epoch,
-                           cudaStream_t stream, int* launches);
+                           cudaStream_t stream, int* launches, cudaStream_t aux = nullptr,
+                           cudaEvent_t* events = nullptr, int nevents = 0);
 uint32_t decode2_chunks(uint64_t n);  // look-back tiles of the offsets pre-pass
 uint32_t decode2_tiles(uint64_t n);   // look-back tiles (CTAs) of the tile decode
 cudaError_t launch_encode(const uint32_t* in, uint64_t n, int delta, uint32_t prev, uint8_t* out,

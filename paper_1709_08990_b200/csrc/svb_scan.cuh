@@ -54,6 +54,8 @@ struct DecodeMeta {
     uint32_t* subsums;               // [nsub]  delta: sum of the sub-tile's deltas
     uint32_t* chunksums;             // [nchunks + 1] delta: chunk sums -> exclusive prefix
     unsigned int* counters;          // [2] last-CTA tickets (self-resetting)
+    uint32_t* chunktot;              // [nchunks] encode: chunk data totals (sliced size scan)
+    unsigned long long* running;     // encode: data offset where the next slice starts
     unsigned long long* trace;       // debug: timestamps (nullptr = off)
 };
 

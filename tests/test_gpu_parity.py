@@ -173,6 +173,16 @@ def test_config2_scaled(P):
     _check_roundtrip(P, v, delta=True, prev=0)
 
 
+def test_encode_sliced_pipeline(P):
+    """> 2 L2 slices of the encode pipeline (8 Mi integers each), odd tail, prev-seeded delta."""
+    rng = np.random.default_rng(31)
+    n = 3 * (1 << 23) + 12345 + 3
+    v = _mixed(rng, n, (0, 1))
+    _check_roundtrip(P, v)
+    s = np.cumsum(rng.integers(0, 300, n, dtype=np.uint64)).astype(np.uint32)
+    _check_roundtrip(P, s, delta=True, prev=123456789)
+
+
 def test_config3_scaled(P):
     from paper_1709_08990_b200 import gen
     v = gen.config_array(3, 1 << 23)
