@@ -10,8 +10,10 @@ prev-seeded chunks, delta, batch kernels).
 
 JSON line keys follow the driver contract; value = integers round-tripped per
 second over all ranks (Gint/s = billions of uint32 encoded AND decoded per s),
-each kernel timed with CUDA events on its launch stream, L2 flushed (256 MiB
-write) before every timed kernel.  `--impl reference` times the CPU reference
+each kernel timed with CUDA events on its launch stream, L2 flushed before
+every timed kernel (256 MiB write, then a 256 MiB read of another buffer, so the
+flush's dirty lines are written back before -- not inside -- the timed region).
+`--impl reference` times the CPU reference
 (the oracle port, all host threads) on the same workload.
 """
 from __future__ import annotations
@@ -373,13 +375,20 @@ def run_gpu(args):
     wl.setup(dev, torch)
     stream = torch.cuda.current_stream()
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+    drain = torch.ones(64 << 20, dtype=torch.int32, device="cuda")
+
+    def flush_l2(k):
+        # evict L2: write 256 MiB, then read another 256 MiB so the dirty lines of the
+        # write are written back here and not inside the next timed kernel
+        flush.fill_(k)
+        drain.sum()
 
     def step(evs):
-        flush.fill_(1)
+        flush_l2(1)
         evs[0].record(stream)
         wl.encode()
         evs[1].record(stream)
-        flush.fill_(2)
+        flush_l2(2)
         evs[2].record(stream)
         wl.decode()
         evs[3].record(stream)
@@ -489,7 +498,7 @@ def run_gpu(args):
             "data": "synthetic (seeded splitmix64 generators standing in for BASELINE.json configs)",
             "config": dict(wl.describe(), compressed_bytes=wl.cmp, bytes_per_int=round(wl.cmp / wl.n, 4),
                            step="encode kernel + decode kernel (round trip), each CUDA-event timed",
-                           l2="flushed (256 MiB write) before every timed kernel",
+                           l2="flushed before every timed kernel (256 MiB write, then a 256 MiB read that drains the dirty lines)",
                            parallelism=f"{'replicas' if isinstance(wl, SingleArray) else 'segment shards'} x{world}"),
             "phases": phases,
             "roofline": {"bound": "hbm", "kernel": dom, "achieved": phases[dom]["gbs"], "peak": peak,

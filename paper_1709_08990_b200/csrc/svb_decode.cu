@@ -365,7 +365,10 @@ __global__ void __launch_bounds__(kCTThreads)
     const uint64_t ngroups = (n + 3) >> 2;
     const uint32_t tail_r = (uint32_t)(n & 3);
     const uint64_t nsub = (ngroups + kWTGroups - 1) / kWTGroups;
-    const uint64_t s0 = (uint64_t)blockIdx.x * S;
+    // the delta pass walks the tiles last to first: the sums pass just streamed the
+    // compressed bytes front to back, so their tail is what L2 still holds
+    const uint32_t bid = kMode == kModeDelta ? gridDim.x - 1 - blockIdx.x : blockIdx.x;
+    const uint64_t s0 = (uint64_t)bid * S;
     const uint64_t chunk = s0 / kChunkSubs;
     const uint32_t ns = (uint32_t)(nsub - s0 < (uint64_t)S ? nsub - s0 : (uint64_t)S);
     const uintptr_t lo = (uintptr_t)in, hi = lo + in_len;
@@ -572,6 +575,214 @@ __global__ void __launch_bounds__(kCTThreads)
 namespace bcgpu {
 
 // ---------------------------------------------------------------------------
+// 2''. delta sums pass: persistent producer/consumer pipeline
+// ---------------------------------------------------------------------------
+// The sums pass only reads (compressed bytes in, one sum per sub-tile out), so
+// nothing hides its load latency but other loads.  One producer warp per CTA
+// runs a ring of kSumStages stages ahead of 8 consumer warps: for tile t (8
+// sub-tiles) it TMA-loads the offsets one ring cycle early, then the control
+// bytes and the whole data range in one bulk copy each; consumers wait on the
+// stage's `full` mbarrier, sum one sub-tile each (svb_fast.cuh lean path),
+// RED.ADD into the chunk sums and release the stage through `empty`.  Tiles are
+// dealt round-robin to a grid of (SMs x resident CTAs).  A tile whose data
+// exceeds the stage pool (density far above the stream average) is summed
+// straight from global memory.  The last CTA scans the chunk sums.
+constexpr int kSumStages = 5;
+constexpr int kSumThreads = 288;  // 8 consumer warps + 1 producer warp
+
+struct __align__(16) SumMeta {
+    uint32_t loc[12];           // localpre[s0 .. s0+12)
+    unsigned long long chk[4];  // chunkpre[(c & ~1) .. +4)
+};
+struct SumHdr {
+    unsigned long long base;  // global address of pool byte 0 (16-B aligned)
+    uint32_t head[9];         // offset of sub-tile i's data from `base`, i = 0..8
+    uint32_t mode;            // 0: data staged in the pool, 1: read from global memory
+};
+struct __align__(16) SumsShared {
+    SumMeta meta[8];
+    SumHdr hdr[8];
+    uint64_t full[8], empty[8], mfull[8];
+    uint32_t scan[16];
+    bool last;
+};
+
+// aligned 32-bit word at global address a; bytes outside [lo, hi) read as 0
+__device__ __forceinline__ uint32_t gword_guarded(uintptr_t a, uintptr_t lo, uintptr_t hi) {
+    if (a >= lo && a + 4 <= hi) return __ldg(reinterpret_cast<const uint32_t*>(a));
+    uint32_t w = 0;
+    for (int b = 0; b < 4; ++b)
+        if (a + b >= lo && a + b < hi) w |= (uint32_t)__ldg(reinterpret_cast<const uint8_t*>(a + b)) << (8 * b);
+    return w;
+}
+
+// Sum of a (possibly partial) sub-tile's integers; word i of its data window is fw(i),
+// the data starts at byte `head` of the window.
+template <class Fetch>
+__device__ __forceinline__ uint32_t sums_generic(const uint8_t* sctrl, uint64_t g0, uint64_t ngroups, uint32_t tail_r,
+                                                 uint32_t head, Fetch fw) {
+    const int lane = threadIdx.x & 31;
+    const WarpCtrl w = load_warp_ctrl<true>(sctrl, g0, ngroups, tail_r, g0);
+    uint32_t acc = 0;
+#pragma unroll
+    for (int j = 0; j < kWTRows; ++j) {
+        const uint32_t c = row_ctrl(w, j);
+        uint32_t b = head + row_q(w, j);
+        const uint32_t cnt = group_count(g0 + 32 * j + lane, ngroups, tail_r);
+#pragma unroll
+        for (int f = 0; f < 4; ++f) {
+            const uint32_t l = ((c >> (2 * f)) & 3u) + 1u;
+            const uint32_t x = __funnelshift_r(fw(b >> 2), fw((b >> 2) + 1), (b & 3u) * 8u);
+            if ((uint32_t)f < cnt) acc += x & (0xFFFFFFFFu >> (32u - 8u * l));
+            b += l;
+        }
+    }
+    return warp_sum_u32(acc);
+}
+
+template <int NST>
+__global__ void __launch_bounds__(kSumThreads)
+    svb_sums_kernel(const uint8_t* __restrict__ in, uint64_t in_len, uint64_t n, DecodeMeta meta,
+                    uint32_t pool_bytes) {
+    extern __shared__ __align__(128) uint8_t dsm[];
+    __shared__ SumsShared sh;
+    constexpr uint32_t kTileCtrl = kCTWarps * kWTGroups;  // 2 KiB of control bytes per tile
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint64_t ngroups = (n + 3) >> 2;
+    const uint32_t tail_r = (uint32_t)(n & 3);
+    const uint64_t nsub = (ngroups + kWTGroups - 1) / kWTGroups;
+    const uint32_t ntiles = (uint32_t)((nsub + kCTWarps - 1) / kCTWarps);
+    const uintptr_t lo = (uintptr_t)in, hi = lo + in_len, data0 = lo + ngroups;
+    const uint32_t stride = kTileCtrl + pool_bytes;
+    if (threadIdx.x == 0) {
+#pragma unroll
+        for (int k = 0; k < NST; ++k) {
+            mbar_init(&sh.full[k], 1);
+            mbar_init(&sh.empty[k], kCTWarps);
+            mbar_init(&sh.mfull[k], 1);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    if (warp == kCTWarps) {
+        // ---- producer ----
+        auto issue_meta = [&](uint32_t t, int st) {
+            const uint64_t s0 = (uint64_t)t * kCTWarps, c = s0 / kChunkSubs;
+            mbar_expect(&sh.mfull[st], 48 + 32);
+            tma_load(sh.meta[st].loc, meta.localpre + s0, 48, &sh.mfull[st]);
+            tma_load(sh.meta[st].chk, meta.chunkpre + (c & ~1ull), 32, &sh.mfull[st]);
+        };
+        if (lane == 0)
+            for (int i = 0; i < NST; ++i) {
+                const uint64_t t = (uint64_t)blockIdx.x + (uint64_t)i * gridDim.x;
+                if (t < ntiles) issue_meta((uint32_t)t, i);
+            }
+        uint32_t k = 0;
+        for (uint32_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++k) {
+            const int st = (int)(k % NST);
+            const uint32_t ph = (k / NST) & 1u;
+            uint8_t* sc = dsm + (uint32_t)st * stride;
+            uint8_t* pool = sc + kTileCtrl;
+            const uint64_t s0 = (uint64_t)t * kCTWarps, chunk = s0 / kChunkSubs;
+            const uint32_t ns = (uint32_t)(nsub - s0 < (uint64_t)kCTWarps ? nsub - s0 : (uint64_t)kCTWarps);
+            mbar_wait_parity(&sh.mfull[st], ph);
+            if (meta.trace && lane == 0) meta.trace[8ull * t + 0] = gtimer();
+            const SumMeta& M = sh.meta[st];
+            const unsigned long long cpre = M.chk[chunk & 1];
+            const bool end_at_chunk = s0 + ns == nsub || (s0 + ns) % kChunkSubs == 0;
+            const unsigned long long A = cpre + M.loc[0];
+            const unsigned long long B = end_at_chunk ? M.chk[(chunk & 1) + 1] : cpre + M.loc[ns];
+            const uint32_t li = (uint32_t)lane < ns ? (uint32_t)lane : ns;
+            const unsigned long long my = (li == ns) ? B : cpre + M.loc[li];
+            const uintptr_t Ag = data0 + A, Bg = data0 + B, base = Ag & ~(uintptr_t)15;
+            const uint32_t tx = tma_cover_bytes(Ag, Bg, lo, hi);
+            const bool fits = tx != 0xFFFFFFFFu && tx + 16 <= pool_bytes;
+            const uintptr_t cb = lo + s0 * kWTGroups;
+            const uint64_t cg = ngroups - s0 * kWTGroups < (uint64_t)kTileCtrl ? ngroups - s0 * kWTGroups
+                                                                                 : (uint64_t)kTileCtrl;
+            const uint32_t ctx = tma_cover_bytes(cb, cb + cg, lo, hi);
+            const bool c_tma = ctx != 0xFFFFFFFFu && (cb & 15) == 0;
+            __syncwarp();  // every lane has read meta[st]
+            if (k >= (uint32_t)NST) mbar_wait_parity(&sh.empty[st], ph ^ 1u);  // consumers left the stage
+            if (!c_tma)
+                for (uint32_t i = lane; i < (uint32_t)cg; i += 32) sc[i] = __ldg(in + s0 * kWTGroups + i);
+            if (lane <= 8) sh.hdr[st].head[lane] = (uint32_t)(data0 + my - base);
+            if (lane == 0) {
+                sh.hdr[st].base = base;
+                sh.hdr[st].mode = fits ? 0u : 1u;
+            }
+            __syncwarp();
+            if (lane == 0) {
+                if (meta.trace) meta.trace[8ull * t + 1] = gtimer();
+                fence_async_smem();
+                mbar_expect(&sh.full[st], (c_tma ? ctx : 0u) + (fits ? tx : 0u));
+                if (c_tma && ctx) tma_load(sc, reinterpret_cast<const void*>(cb), ctx, &sh.full[st]);
+                if (fits && tx) tma_load(pool, reinterpret_cast<const void*>(base), tx, &sh.full[st]);
+                const uint64_t tn = (uint64_t)t + (uint64_t)NST * gridDim.x;  // meta[st] was consumed above
+                if (tn < ntiles) issue_meta((uint32_t)tn, st);
+            }
+        }
+    } else {
+        // ---- consumers: warp w sums sub-tile 8t + w ----
+        uint32_t k = 0;
+        for (uint32_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++k) {
+            const int st = (int)(k % NST);
+            const uint32_t ph = (k / NST) & 1u;
+            mbar_wait_parity(&sh.full[st], ph);
+            if (meta.trace && lane == 0) meta.trace[8ull * t + 2 + (warp == 0 ? 0 : 2)] = gtimer();
+            const uint64_t s = (uint64_t)t * kCTWarps + warp;
+            if (s < nsub) {
+                const uint8_t* sc = dsm + (uint32_t)st * stride + warp * kWTGroups;
+                const uint8_t* pool = dsm + (uint32_t)st * stride + kTileCtrl;
+                const uint32_t head = sh.hdr[st].head[warp];
+                const uint64_t g0 = s * kWTGroups;
+                uint32_t acc;
+                if (sh.hdr[st].mode == 0) {
+                    if ((s + 1) * kWTInts <= n && head <= pool_bytes - 32) {
+                        const uint32_t sd = sh_addr(pool) + head;
+                        if (ctrl_all_zero(sh_addr(sc))) {  // 1024 one-byte integers: a byte sum
+                            acc = __reduce_add_sync(kFull, zero_tile_sum(sd));
+                        } else {
+                            bool zero;
+                            const WarpCtrl wf = ctrl_full(sh_addr(sc), &zero);
+                            acc = __reduce_add_sync(kFull, expand_full<2, false>(wf, sd, nullptr, 0));
+                        }
+                    } else {
+                        const uint32_t* W = reinterpret_cast<const uint32_t*>(pool);
+                        const uint32_t lim = pool_bytes / 4 - 1;
+                        acc = sums_generic(sc, g0, ngroups, tail_r, head,
+                                           [&](uint32_t i) { return W[i < lim ? i : lim]; });
+                    }
+                } else {
+                    const uintptr_t gb = (uintptr_t)sh.hdr[st].base;
+                    acc = sums_generic(sc, g0, ngroups, tail_r, head,
+                                       [&](uint32_t i) { return gword_guarded(gb + 4 * (uintptr_t)i, lo, hi); });
+                }
+                if (lane == 0) {
+                    meta.subsums[s] = acc;
+                    atomicAdd(meta.chunksums + s / kChunkSubs, acc);  // RED.ADD, mod 2^32
+                }
+            }
+            __syncwarp();
+            if (meta.trace && lane == 0 && (warp == 0 || warp == 7)) meta.trace[8ull * t + 3 + (warp == 0 ? 0 : 2)] = gtimer();
+            if (lane == 0) mbar_arrive(&sh.empty[st]);
+        }
+    }
+    // last CTA: exclusive scan of the chunk sums
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();
+        sh.last = atomicAdd(meta.counters + 1, 1u) == gridDim.x - 1;
+    }
+    __syncthreads();
+    if (!sh.last) return;
+    __threadfence();
+    const uint32_t nchunks = (uint32_t)((nsub + kChunkSubs - 1) / kChunkSubs);
+    cta_exclusive_scan<uint32_t, kSumThreads / 32>(meta.chunksums, nchunks, sh.scan);
+    if (threadIdx.x == 0) meta.counters[1] = 0;
+}
+
+// ---------------------------------------------------------------------------
 // launcher
 // ---------------------------------------------------------------------------
 static inline uint64_t align16(uint64_t x) { return (x + 15) & ~(uint64_t)15; }
@@ -608,6 +819,54 @@ uint64_t decode_meta_bytes(uint64_t n) {
 
 int occupancy_decode_pipe() { return 1; }  // the tile kernel is not persistent
 
+// pipelined sums pass: stage pool from the stream's average density, grid = SMs x resident CTAs
+template <int NST>
+static cudaError_t launch_sums_t(const uint8_t* in, uint64_t in_len, uint64_t n, const DecodeMeta& m, uint64_t pool,
+                                 cudaStream_t stream) {
+    const uint32_t smem = (uint32_t)(NST * (kCTWarps * kWTGroups + pool));
+    static int dev_cached = -1, sms = 0;
+    static uint32_t occ_smem = 0;
+    static int occ = 0;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev != dev_cached) {
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        const cudaError_t a =
+            cudaFuncSetAttribute(svb_sums_kernel<NST>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+        if (a != cudaSuccess) return a;
+        dev_cached = dev;
+        occ_smem = 0;
+    }
+    if (smem != occ_smem) {
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, svb_sums_kernel<NST>, kSumThreads, smem);
+        if (occ < 1) occ = 1;
+        occ_smem = smem;
+    }
+    const uint64_t ngroups = (n + 3) >> 2;
+    const uint64_t nsub = (ngroups + kWTGroups - 1) / kWTGroups;
+    const uint64_t ntiles = (nsub + kCTWarps - 1) / kCTWarps;
+    uint64_t grid = (uint64_t)sms * (uint64_t)occ;
+    if (grid > ntiles) grid = ntiles;
+    if (grid < 1) grid = 1;
+    svb_sums_kernel<NST><<<(unsigned)grid, kSumThreads, smem, stream>>>(in, in_len, n, m, (uint32_t)pool);
+    return cudaGetLastError();
+}
+
+static cudaError_t launch_sums(const uint8_t* in, uint64_t in_len, uint64_t n, const DecodeMeta& m, double dpb,
+                               cudaStream_t stream, uint32_t debug_flags) {
+    const uint32_t f10 = (debug_flags >> 8) & 0xFFu;  // debug: pool factor x10
+    uint64_t pool = (uint64_t)((f10 ? f10 / 10.0 : 1.1) * dpb * kCTWarps) + 64;
+    if (pool < 4096) pool = 4096;
+    if (pool > 8ull * kWTDataMax + 64) pool = 8ull * kWTDataMax + 64;
+    pool = (pool + 15) & ~15ull;
+    switch ((debug_flags >> 16) & 0xFu) {  // debug: stage count
+        case 4: return launch_sums_t<4>(in, in_len, n, m, pool, stream);
+        case 6: return launch_sums_t<6>(in, in_len, n, m, pool, stream);
+        case 8: return launch_sums_t<8>(in, in_len, n, m, pool, stream);
+        default: return launch_sums_t<kSumStages>(in, in_len, n, m, pool, stream);
+    }
+}
+
 cudaError_t launch_decode3(const uint8_t* in, uint64_t in_len, uint64_t n, int delta, uint32_t base, uint32_t* out,
                            uint32_t* d_last, void* meta_ws, unsigned long long* status, uint32_t epoch, int pipe_grid,
                            cudaStream_t stream, int* launches, unsigned long long* trace, uint32_t debug_flags) {
@@ -641,13 +900,15 @@ cudaError_t launch_decode3(const uint8_t* in, uint64_t in_len, uint64_t n, int d
                                                                              (uint32_t)pool);                   \
     } while (0)
         if (delta) {
-            if (K == 4) {
-                BC_POOL_LAUNCH(kModeSums, 4);
-                BC_POOL_LAUNCH(kModeDelta, 4);
+            if (debug_flags & 8) {  // debug: the pooled sums pass instead of the pipelined one
+                if (K == 4) BC_POOL_LAUNCH(kModeSums, 4);
+                else BC_POOL_LAUNCH(kModeSums, 2);
             } else {
-                BC_POOL_LAUNCH(kModeSums, 2);
-                BC_POOL_LAUNCH(kModeDelta, 2);
+                const cudaError_t e2 = launch_sums(in, in_len, n, m, dpb, stream, debug_flags);
+                if (e2 != cudaSuccess) return e2;
             }
+            if (K == 4) BC_POOL_LAUNCH(kModeDelta, 4);
+            else BC_POOL_LAUNCH(kModeDelta, 2);
             *launches = 3;
         } else {
             if (K == 4) BC_POOL_LAUNCH(kModePlain, 4);

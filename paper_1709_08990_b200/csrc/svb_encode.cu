@@ -52,11 +52,20 @@ __global__ void __launch_bounds__(256)
     const uint64_t nsub = (ngroups + kWTGroups - 1) / kWTGroups;
     const bool in16 = (((uintptr_t)in) & 15) == 0;
     uint32_t my_size = 0;  // lane k < 8: size of sub-tile 8*warp + k
+    uint32_t lean_last = 0;  // lane 0, delta: the integer before the next sub-tile
 #pragma unroll 1
     for (int k = 0; k < 8; ++k) {
         const uint64_t s = (uint64_t)chunk * kChunkSubs + 8 * warp + k;
         if (s >= nsub) break;
         const uint64_t g0 = s * kWTGroups;
+        if (in16 && (s + 1) * kWTInts <= n) {  // full sub-tile: lean path (svb_fast.cuh)
+            if (kDelta && k == 0) lean_last = g0 ? __ldg(in + 4 * g0 - 1) : prev;
+            uint32_t acc = size_full<kDelta>(in + 4 * g0, lean_last);
+#pragma unroll
+            for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(kFull, acc, o);
+            if (lane == k) my_size = acc + kWTInts;
+            continue;
+        }
         uint32_t last_w = prev;
         if (kDelta && g0) last_w = __ldg(in + 4 * g0 - 1);
         uint4 x[kWTRows];
@@ -145,7 +154,9 @@ __global__ void __launch_bounds__(kCTThreads, 4)
     __shared__ __align__(16) unsigned long long schunk[4];
     __shared__ __align__(8) uint64_t bars[kCTWarps + 1];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const uint32_t tile = tile_base + blockIdx.x;
+    // last tile first: the size scan just streamed the input front to back, so its
+    // tail is what L2 still holds
+    const uint32_t tile = tile_base + (gridDim.x - 1 - blockIdx.x);
     const uint64_t ngroups = (n + 3) >> 2;
     const uint32_t tail_r = (uint32_t)(n & 3);
     const uint64_t sub0 = (uint64_t)tile * kCTWarps;
@@ -192,9 +203,17 @@ __global__ void __launch_bounds__(kCTThreads, 4)
     uint32_t lens[kWTRows], qw[4];
     EncodeTile t;
     const uint32_t prev_w = g0 ? reinterpret_cast<const uint32_t*>(b.stage)[3] : prev;
+    bool small = false;
     if (full) {
-        // lengths, control bytes, tile-local offsets (lean path, svb_fast.cuh)
-        total = enc_full_lengths<kDelta>(sh_addr(b.stage) + 16, prev_w, sh_addr(b.ctrl), lens, qw);
+        // every integer < 256: control bytes 0, data = the low bytes (svb_fast.cuh)
+        small = enc_full_small<kDelta>(sh_addr(b.stage) + 16, prev_w);
+        if (small) {
+            asm volatile("st.shared.v2.u32 [%0], {%1, %1};" ::"r"(sh_addr(b.ctrl) + 8 * lane), "r"(0u) : "memory");
+            total = kWTInts;
+        } else {
+            // lengths, control bytes, tile-local offsets (lean path, svb_fast.cuh)
+            total = enc_full_lengths<kDelta>(sh_addr(b.stage) + 16, prev_w, sh_addr(b.ctrl), lens, qw);
+        }
     } else {
         uint32_t P[3] = {0, 0, 0};
         uint32_t last_w = prev_w;
@@ -230,7 +249,9 @@ __global__ void __launch_bounds__(kCTThreads, 4)
     // pack in place at the destination's 16-B phase: group g's bytes end at or before
     // head + 16(g+1) <= 16 + 16g + 15 < the input of group g+1 (stage + 16 + 16(g+1))
     __syncwarp();
-    if (full)
+    if (small)
+        enc_small_pack<kDelta>(sh_addr(b.stage) + 16, prev_w, sh_addr(b.stage) + head);
+    else if (full)
         enc_full_pack<kDelta>(sh_addr(b.stage) + 16, prev_w, lens, qw, sh_addr(b.stage) + head);
     else
         encode_pack_at(t, b.stage, head);

@@ -92,6 +92,48 @@ __device__ __forceinline__ uint4 zero_group_s(uint32_t a) {
                       __byte_perm(x, 0u, 0x4443));
 }
 
+__device__ __forceinline__ uint2 lds64(uint32_t a) {
+    uint2 v;
+    asm("ld.shared.v2.u32 {%0,%1}, [%2];" : "=r"(v.x), "=r"(v.y) : "r"(a));
+    return v;
+}
+
+// true when all 256 control bytes of the sub-tile at shared address sc are 0 (warp-uniform)
+__device__ __forceinline__ bool ctrl_all_zero(uint32_t sc) {
+    const uint2 c = lds64(sc + 8 * (threadIdx.x & 31));
+    return __all_sync(kFull, (c.x | c.y) == 0);
+}
+
+// dp4a byte selector for bytes [0, k) of a word, k in [0, 4]
+__device__ __forceinline__ uint32_t ones_below(int k) {
+    return k >= 4 ? 0x01010101u : (k <= 0 ? 0u : (0x01010101u & ((1u << (8 * k)) - 1u)));
+}
+
+// Per-lane part of the byte sum of the 1024 shared bytes at sd (any alignment): the sum of
+// a sub-tile's integers when every control byte is 0.  Lane l reads 16-B chunks l, l+32.
+__device__ __forceinline__ uint32_t zero_tile_sum(uint32_t sd) {
+    const int lane = threadIdx.x & 31;
+    const uint32_t a0 = sd & ~15u;
+    const int s = (int)(sd & 15u);
+    uint32_t acc = 0;
+#pragma unroll
+    for (int i = 0; i < 2; ++i) {
+        const uint4 v = lds128(a0 + 16u * (lane + 32 * i));
+        acc = __dp4a(v.x, 0x01010101u, acc);
+        acc = __dp4a(v.y, 0x01010101u, acc);
+        acc = __dp4a(v.z, 0x01010101u, acc);
+        acc = __dp4a(v.w, 0x01010101u, acc);
+    }
+    if (lane == 0 && s) {  // chunk 0's first s bytes precede the sub-tile, chunk 64's belong to it
+        const uint4 f = lds128(a0), t = lds128(a0 + 1024u);
+        acc = __dp4a(t.x, ones_below(s), acc) - __dp4a(f.x, ones_below(s), 0u);
+        acc = __dp4a(t.y, ones_below(s - 4), acc) - __dp4a(f.y, ones_below(s - 4), 0u);
+        acc = __dp4a(t.z, ones_below(s - 8), acc) - __dp4a(f.z, ones_below(s - 8), 0u);
+        acc = __dp4a(t.w, ones_below(s - 12), acc) - __dp4a(f.w, ones_below(s - 12), 0u);
+    }
+    return acc;
+}
+
 __device__ __forceinline__ uint32_t byte_sum4_fast(uint32_t w) {
     const uint32_t s = (w & 0x00FF00FFu) + ((w >> 8) & 0x00FF00FFu);
     return (s & 0xFFFFu) + (s >> 16);
@@ -151,6 +193,40 @@ namespace bcgpu {
 // ---- encode, full sub-tiles --------------------------------------------------
 __device__ __forceinline__ uint32_t blen(uint32_t x) { return 4u - (__clz(x | 1u) >> 3); }  // codec.hpp:70-72
 
+__device__ __forceinline__ uint32_t bfind_u32(uint32_t x) {
+    uint32_t r;
+    asm("bfind.u32 %0, %1;" : "=r"(r) : "r"(x));
+    return r;
+}
+// byte_length(x) - 1 (codec.hpp:70-72): the index of x's top byte, with x < 256 -> 0
+__device__ __forceinline__ uint32_t blen_m1(uint32_t x) { return bfind_u32(x | 0x80u) >> 3; }
+
+// Size scan of one full sub-tile at p (16-B aligned): sum over its 1024 integers of
+// byte_length - 1, per lane (the sub-tile's data size is the warp sum + 1024).
+// Delta: lane 0 holds x_{-1} in `last` and gets the sub-tile's last integer back.
+template <bool kDelta>
+__device__ __forceinline__ uint32_t size_full(const uint32_t* __restrict__ p, uint32_t& last) {
+    const int lane = threadIdx.x & 31;
+    uint4 x[kWTRows];
+#pragma unroll
+    for (int j = 0; j < kWTRows; ++j) x[j] = ldg_stream_v4(p + 128 * j + 4 * lane);
+    uint32_t acc = 0;
+#pragma unroll
+    for (int j = 0; j < kWTRows; ++j) {
+        uint4 v = x[j];
+        if constexpr (kDelta) {
+            // one rotation per row: lane l gets lane l-1's last integer; lane 0 gets
+            // lane 31's, which is the predecessor of the next row's lane 0
+            const uint32_t r = __shfl_sync(kFull, v.w, (lane + 31) & 31);
+            const uint32_t q = lane == 0 ? last : r;
+            last = r;
+            v = make_uint4(v.x - q, v.y - v.x, v.z - v.y, v.w - v.z);
+        }
+        acc += blen_m1(v.x) + blen_m1(v.y) + blen_m1(v.z) + blen_m1(v.w);
+    }
+    return acc;
+}
+
 // Row j of the sub-tile (integers at shared address sin + 512 j + 16 lane), as
 // values or mod-2^32 deltas; `last` carries x_{-1} in and the row's last raw value out.
 template <bool kDelta>
@@ -190,6 +266,45 @@ __device__ __forceinline__ uint32_t enc_full_lengths(uint32_t sin, uint32_t prev
         return kWTInts;
     }
     return packed_row_scan(P, qw);
+}
+
+// True when every integer (delta) of the full sub-tile at sin is < 256 (warp-uniform):
+// then all control bytes are 0 and the data is the low byte of each integer.
+template <bool kDelta>
+__device__ __forceinline__ bool enc_full_small(uint32_t sin, uint32_t prev_w) {
+    uint32_t last = prev_w, o = 0;
+#pragma unroll
+    for (int j = 0; j < kWTRows; ++j) {
+        const uint4 x = enc_row<kDelta>(sin, j, last);
+        o |= x.x | x.y | x.z | x.w;
+    }
+    return __all_sync(kFull, o < 256u);
+}
+
+// Pack pass of a small sub-tile (enc_full_small): row j lane l's four bytes go to
+// sdst + 128 j + 4 l.  In place, as enc_full_pack.
+template <bool kDelta>
+__device__ __forceinline__ void enc_small_pack(uint32_t sin, uint32_t prev_w, uint32_t sdst) {
+    const int lane = threadIdx.x & 31;
+    const uint32_t s = sdst & 3u;  // warp-uniform
+    uint32_t last = prev_w;
+#pragma unroll
+    for (int j = 0; j < kWTRows; ++j) {
+        const uint4 x = enc_row<kDelta>(sin, j, last);
+        const uint32_t P = __byte_perm(__byte_perm(x.x, x.y, 0x0040), __byte_perm(x.z, x.w, 0x0040), 0x5410);
+        const uint32_t a = sdst + 128 * j + 4 * lane;
+        __syncwarp();  // every lane has read row j before any lane writes over it
+        if (s == 0) {
+            sts32(a, P);
+        } else {
+            const uint32_t Pp = __shfl_up_sync(kFull, P, 1);
+            if (lane > 0) sts32(a & ~3u, __funnelshift_r(Pp, P, 8u * (4u - s)));
+            if (lane == 0)
+                for (uint32_t b = 0; b < 4u - s; ++b) sts8(a + b, P >> (8 * b));
+            if (lane == 31)
+                for (uint32_t b = 4u - s; b < 4u; ++b) sts8(a + b, P >> (8 * b));
+        }
+    }
 }
 
 __device__ __forceinline__ void sts_int_bytes(uint32_t a, uint32_t x, uint32_t l) {

@@ -183,6 +183,19 @@ def test_encode_sliced_pipeline(P):
     _check_roundtrip(P, s, delta=True, prev=123456789)
 
 
+def test_delta_sums_paths(P):
+    """Delta decode's sums pass: all-zero-control sub-tiles (byte sums) next to general ones,
+    at every 16-B phase of the data start, across many pipeline rounds."""
+    rng = np.random.default_rng(77)
+    for n in (4 * 1024 + 4, 4 * 1024 + 8, 4 * 1024 + 12, 9 * 1024 + 44, 200 * 1024 + 4 * 13 + 3, 3_000_001):
+        g = rng.integers(0, 200, n, dtype=np.uint64)
+        sub = np.arange(n) // 1024
+        big = (sub % 3 == 1) & (rng.random(n) < 0.01)  # every third sub-tile gets some wide gaps
+        g[big] += rng.integers(256, 1 << 20, int(big.sum()), dtype=np.uint64)
+        v = np.cumsum(g).astype(np.uint32)
+        _check_roundtrip(P, v, delta=True, prev=int(rng.integers(0, 2**32)))
+
+
 def test_config3_scaled(P):
     from paper_1709_08990_b200 import gen
     v = gen.config_array(3, 1 << 23)
