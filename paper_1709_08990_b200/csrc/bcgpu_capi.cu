@@ -71,6 +71,8 @@ struct bcgpu_ctx {
     int pipe_grid = 0;     // persistent decode CTAs
     void* d_scratch = nullptr;
     size_t d_scratch_cap = 0;
+    uint8_t* slots = nullptr;  // encode: per-tile packing slots (svb_encode.cu)
+    size_t slots_cap = 0;
 };
 
 static unsigned long long* ticket_ptr(bcgpu_ctx* c) { return c->ws; }
@@ -150,6 +152,33 @@ static int ensure_meta(bcgpu_ctx* c, uint64_t n, cudaStream_t s) {
     BC_CUDA(cudaMalloc(&c->offs, cap));
     BC_CUDA(cudaMemset(c->offs, 0, cap));
     c->offs_cap = cap;
+    return BCGPU_OK;
+}
+
+// Encode packing slots (svb_encode.cu).  The slot encode reads the integers once but
+// moves the compressed bytes twice more (slot, then final place); measured on B200 it
+// wins when they compress well (cfg2, 1.25 B/int: 99 vs 108 us) and loses on wide
+// data (cfg3, ~2.5 B/int: 785 vs 648 us).  The compressed size is unknown up front,
+// so: delta streams (sorted ids, small gaps) use slots, plain streams read twice.
+// Debug flag 16 forces the two-read path, 32 the slot path.
+static int ensure_slots(bcgpu_ctx* c, uint64_t n, int delta, cudaStream_t s, uint8_t** p) {
+    *p = nullptr;
+    if (c->debug_flags & 16) return BCGPU_OK;
+    if (!delta && !(c->debug_flags & 32)) return BCGPU_OK;
+    if (n > (1ull << 30)) return BCGPU_OK;  // slots take ~4 B/int of scratch
+    const size_t bytes = encode_slot_bytes(n);
+    if (bytes > c->slots_cap) {
+        if (c->slots) {
+            BC_CUDA(cudaStreamSynchronize(s));
+            BC_CUDA(cudaFree(c->slots));
+            c->slots = nullptr;
+            c->slots_cap = 0;
+        }
+        const size_t cap = bytes + bytes / 8 + 4096;
+        BC_CUDA(cudaMalloc(&c->slots, cap));
+        c->slots_cap = cap;
+    }
+    *p = c->slots;
     return BCGPU_OK;
 }
 
@@ -258,6 +287,7 @@ int bcgpu_ctx_destroy(bcgpu_ctx* c) {
     if (c->ws) cudaFree(c->ws);
     if (c->d_scratch) cudaFree(c->d_scratch);
     if (c->offs) cudaFree(c->offs);
+    if (c->slots) cudaFree(c->slots);
     if (c->stream) cudaStreamDestroy(c->stream);
     if (c->aux) cudaStreamDestroy(c->aux);
     for (auto& ev : c->events)
@@ -294,9 +324,12 @@ int bcgpu_svb_encode_device(bcgpu_ctx* c, const uint32_t* d_in, size_t n, int de
     if (st) return st;
     st = next_epoch(c, s);
     if (st) return st;
+    uint8_t* slots = nullptr;
+    st = ensure_slots(c, n, delta, s, &slots);
+    if (st) return st;
     int launches = 0;
     BC_CUDA(launch_encode3(d_in, n, delta, prev, d_out, d_out_len, c->offs, status_ptr(c), c->epoch, s, &launches,
-                           c->aux, c->events, 96));
+                           c->aux, c->events, 96, slots, (c->debug_flags & 32) ? ((c->debug_flags >> 6) & 3u) : 3u));
     g_launches.fetch_add((uint64_t)launches);
     return BCGPU_OK;
 }

@@ -806,6 +806,8 @@ DecodeMeta carve_decode_meta(void* ws, uint64_t n) {
     m.chunksums = reinterpret_cast<uint32_t*>(p);
     p += align16(4 * (nchunks + 1));
     m.chunktot = reinterpret_cast<uint32_t*>(p);
+    p += align16(4 * (nchunks + 1));
+    m.tilesize = reinterpret_cast<uint32_t*>(p);
     return m;
 }
 
@@ -813,8 +815,9 @@ uint64_t decode_meta_bytes(uint64_t n) {
     const uint64_t ngroups = (n + 3) >> 2;
     const uint64_t nsub = (ngroups + kWTGroups - 1) / kWTGroups;
     const uint64_t nchunks = (nsub + kChunkSubs - 1) / kChunkSubs;
+    const uint64_t ntiles = (nsub + kCTWarps - 1) / kCTWarps;
     return 32 + align16(4 * (nsub + 64)) + align16(8 * (nchunks + 4)) + align16(4 * nsub) +
-           2 * align16(4 * (nchunks + 1)) + 64;
+           2 * align16(4 * (nchunks + 1)) + align16(4 * (ntiles + 8)) + 64;
 }
 
 int occupancy_decode_pipe() { return 1; }  // the tile kernel is not persistent

@@ -125,7 +125,10 @@ __global__ void __launch_bounds__(256)
     __threadfence();
     const unsigned long long base = c_begin == 0 ? 0ull : *meta.running;
     const uint32_t tot = cta_exclusive_scan<uint32_t, 8>(meta.chunktot + c_begin, gridDim.x, wt);
-    for (uint32_t c = tid; c < gridDim.x; c += 256) meta.chunkpre[c_begin + c] = base + meta.chunktot[c_begin + c];
+    for (uint32_t c = tid; c < gridDim.x; c += 256) {
+        meta.chunkpre[c_begin + c] = base + meta.chunktot[c_begin + c];
+        meta.chunktot[c_begin + c] = 0;  // the slot encode accumulates into zeroed totals
+    }
     if (tid == 0) {
         meta.chunkpre[c_end] = base + tot;  // == the next slice's base (same value written twice)
         *meta.running = base + tot;
@@ -279,12 +282,283 @@ __global__ void __launch_bounds__(kCTThreads, 4)
 }
 
 // ---------------------------------------------------------------------------
+// 3. single-read encode: pack into per-tile slots, then compact
+// ---------------------------------------------------------------------------
+// svb_encode_slot_kernel reads every integer once.  CTA t (8 sub-tiles) sizes and
+// packs its sub-tiles exactly like the tile kernel, but with no offsets to wait
+// for: the control bytes go straight to their final place (byte g of the
+// stream), the data bytes to a private, 128-B aligned, worst-case-sized slot in
+// scratch (kept in L2: evict_last; the integers stream through with
+// evict_first), the tile's data size to tilesize[t] and (RED.ADD) to its
+// chunk's total; the last CTA scans the chunk totals.  svb_encode_compact_kernel
+// then moves each slot to its final offset -- one warp per tile, 16-B
+// granules realigned with funnel shifts, 128-bit stores -- and discards each
+// slot line from L2 once read, so the slots never cost a DRAM write-back.
+// From HBM: 4 B/int in, cmp bytes out (+ whatever of the slots L2 cannot hold).
+constexpr uint32_t kSlotStride = kCTWarps * kWTDataMax + 128;  // worst-case tile data + slack, 128-B multiple
+
+template <bool kDelta>
+__global__ void __launch_bounds__(kCTThreads, 4)
+    svb_encode_slot_kernel(const uint32_t* __restrict__ in, uint64_t n, uint32_t prev, uint8_t* __restrict__ out,
+                           DecodeMeta meta, uint8_t* __restrict__ slots, uint64_t* __restrict__ d_out_len,
+                           unsigned long long* status, uint32_t epoch, uint32_t hints) {
+    __shared__ __align__(128) EncBuf wb[kCTWarps];
+    __shared__ __align__(8) uint64_t bars[kCTWarps];
+    __shared__ uint32_t wtot[kCTWarps];
+    __shared__ unsigned long long wscan[kCTWarps];
+    __shared__ bool last;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t tile = blockIdx.x;
+    const uint64_t ngroups = (n + 3) >> 2;
+    const uint32_t tail_r = (uint32_t)(n & 3);
+    const uint64_t sub = (uint64_t)tile * kCTWarps + warp;
+    const uint64_t g0 = sub * kWTGroups;
+    const bool active = g0 < ngroups;
+    EncBuf& b = wb[warp];
+    if (lane == 0) mbar_init1(&bars[warp]);
+    __syncwarp();
+
+    uint32_t total = 0;
+    bool small = false, full = false;
+    uint32_t lens[kWTRows], qw[4];
+    EncodeTile t;
+    uint32_t prev_w = prev;
+    const uint64_t i0 = 4 * g0;
+    const uint32_t nints = active ? (uint32_t)(n - i0 < (uint64_t)kWTInts ? n - i0 : (uint64_t)kWTInts) : 0u;
+    if (active) {
+        // the sub-tile's integers (and the 4 before it) -> stage
+        const uintptr_t lo = (uintptr_t)in, hi = lo + 4 * n;
+        const uintptr_t beg = (uintptr_t)(in + i0) - (g0 ? 16 : 0), end = (uintptr_t)(in + i0 + nints);
+        const uint32_t tx = tma_cover_bytes(beg, end, lo, hi);
+        const bool use_tma = tx != 0xFFFFFFFFu && (beg & 15) == 0;
+        uint8_t* dst = b.stage + (g0 ? 0 : 16);
+        if (use_tma) {
+            if (lane == 0) {
+                mbar_expect(&bars[warp], tx);
+                if (hints & 1)
+                    tma_load_hint(dst, reinterpret_cast<const void*>(beg), tx, &bars[warp], l2_policy_drop());
+                else
+                    tma_load(dst, reinterpret_cast<const void*>(beg), tx, &bars[warp]);
+            }
+            mbar_wait_parity(&bars[warp], 0);
+        } else {
+            uint32_t* d32 = reinterpret_cast<uint32_t*>(dst);
+            const uint32_t words = (uint32_t)((end - beg) >> 2);
+            for (uint32_t i = lane; i < words; i += 32) d32[i] = __ldg(reinterpret_cast<const uint32_t*>(beg) + i);
+            __syncwarp();
+        }
+        full = 4 * (g0 + kWTGroups) <= n;
+        if (g0) prev_w = reinterpret_cast<const uint32_t*>(b.stage)[3];
+        if (full) {
+            small = enc_full_small<kDelta>(sh_addr(b.stage) + 16, prev_w);
+            if (small) {
+                asm volatile("st.shared.v2.u32 [%0], {%1, %1};" ::"r"(sh_addr(b.ctrl) + 8 * lane), "r"(0u) : "memory");
+                total = kWTInts;
+            } else {
+                total = enc_full_lengths<kDelta>(sh_addr(b.stage) + 16, prev_w, sh_addr(b.ctrl), lens, qw);
+            }
+        } else {
+            uint32_t P[3] = {0, 0, 0};
+            uint32_t last_w = prev_w;
+#pragma unroll
+            for (int j = 0; j < kWTRows; ++j) {
+                const uint32_t cnt = group_count(g0 + 32 * j + lane, ngroups, tail_r);
+                uint4 x = mask_tail(*reinterpret_cast<const uint4*>(b.stage + 16 + 512 * j + 16 * lane), cnt);
+                if constexpr (kDelta) {
+                    uint32_t p = __shfl_up_sync(kFull, x.w, 1);
+                    if (lane == 0) p = last_w;
+                    last_w = __shfl_sync(kFull, x.w, 31);
+                    x = make_uint4(x.x - p, x.y - x.x, x.z - x.y, x.w - x.z);
+                }
+                t.d[j] = x;
+                const uint32_t l0 = cnt > 0 ? dev_byte_length(x.x) : 0u;
+                const uint32_t l1 = cnt > 1 ? dev_byte_length(x.y) : 0u;
+                const uint32_t l2 = cnt > 2 ? dev_byte_length(x.z) : 0u;
+                const uint32_t l3 = cnt > 3 ? dev_byte_length(x.w) : 0u;
+                t.lens[j] = l0 | (l1 << 8) | (l2 << 16) | (l3 << 24);
+                P[j / 3] |= (l0 + l1 + l2 + l3) << (10 * (j % 3));
+                b.ctrl[32 * j + lane] = (uint8_t)((l0 - 1) | (l1 ? ((l1 - 1) << 2) : 0u) | (l2 ? ((l2 - 1) << 4) : 0u) |
+                                                  (l3 ? ((l3 - 1) << 6) : 0u));
+            }
+            t.total = packed_row_scan(P, t.qw);
+            total = t.total;
+        }
+    }
+    // tile-local offsets of the 8 sub-tiles' data within the slot
+    if (lane == 0) wtot[warp] = total;
+    __syncthreads();
+    uint32_t pre = 0, ttot = 0;
+#pragma unroll
+    for (int w = 0; w < kCTWarps; ++w) {
+        const uint32_t x = wtot[w];
+        pre += w < warp ? x : 0u;
+        ttot += x;
+    }
+    if (active) {
+        uint8_t* slot = slots + (size_t)tile * kSlotStride;
+        const uintptr_t dbeg = (uintptr_t)slot + pre, dend = dbeg + total;
+        const uint32_t head = (uint32_t)(dbeg & 15);
+        __syncwarp();
+        if (small)
+            enc_small_pack<kDelta>(sh_addr(b.stage) + 16, prev_w, sh_addr(b.stage) + head);
+        else if (full)
+            enc_full_pack<kDelta>(sh_addr(b.stage) + 16, prev_w, lens, qw, sh_addr(b.stage) + head);
+        else
+            encode_pack_at(t, b.stage, head);
+        fence_async_smem();
+        __syncwarp();
+        const uint32_t cnt_g = (uint32_t)(ngroups - g0 < (uint64_t)kWTGroups ? ngroups - g0 : (uint64_t)kWTGroups);
+        uint8_t* cdst = out + g0;
+        const uint32_t cb = (((uintptr_t)cdst & 15) == 0) ? (cnt_g & ~15u) : 0u;
+        const uintptr_t a_lo = (dbeg + 15) & ~(uintptr_t)15, a_hi = dend & ~(uintptr_t)15;
+        const uint32_t db = a_hi > a_lo ? (uint32_t)(a_hi - a_lo) : 0u;
+        if (lane == 0) {
+            if (cb) tma_store(cdst, b.ctrl, cb);
+            if (db) {
+                if (hints & 2)
+                    tma_store_hint(reinterpret_cast<void*>(a_lo), b.stage + (a_lo - dbeg) + head, db, l2_policy_keep());
+                else
+                    tma_store(reinterpret_cast<void*>(a_lo), b.stage + (a_lo - dbeg) + head, db);
+            }
+            if (cb || db) tma_store_commit();
+        }
+        for (uint32_t i = cb + lane; i < cnt_g; i += 32) cdst[i] = b.ctrl[i];
+        // edge bytes shared with the neighbouring sub-tiles' 16-B granules (< 16 at each end)
+        if (db == 0) {
+            for (uint32_t i = lane; i < total; i += 32) *reinterpret_cast<uint8_t*>(dbeg + i) = b.stage[head + i];
+        } else {
+            const uint32_t nh = (uint32_t)(a_lo - dbeg), nt = (uint32_t)(dend - a_hi);
+            if (lane < nh) *reinterpret_cast<uint8_t*>(dbeg + lane) = b.stage[head + lane];
+            if (lane < nt) *reinterpret_cast<uint8_t*>(a_hi + lane) = b.stage[head + (uint32_t)(a_hi - dbeg) + lane];
+        }
+        if (lane == 0 && (cb || db)) tma_store_wait_read();
+    }
+    if (threadIdx.x == 0) meta.tilesize[tile] = ttot;
+    // last CTA: chunk offsets = exclusive scan of the chunk totals (8 tile sizes each)
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();
+        last = atomicAdd(meta.counters, 1u) == gridDim.x - 1;
+    }
+    __syncthreads();
+    if (!last) return;
+    __threadfence();
+    const uint64_t nsub = (ngroups + kWTGroups - 1) / kWTGroups;
+    const uint32_t nchunks = (uint32_t)((nsub + kChunkSubs - 1) / kChunkSubs);
+    const uint32_t ntiles = gridDim.x;
+    static_assert(kChunkSubs / kCTWarps == 8, "8 tiles per chunk");
+    for (uint32_t c = threadIdx.x; c < nchunks; c += kCTThreads) {
+        uint32_t sum = 0;
+        if (8 * c + 8 <= ntiles) {  // tilesize is 16-B aligned (DecodeMeta carve)
+            const uint4 a = __ldcg(reinterpret_cast<const uint4*>(meta.tilesize) + 2 * c);
+            const uint4 b = __ldcg(reinterpret_cast<const uint4*>(meta.tilesize) + 2 * c + 1);
+            sum = a.x + a.y + a.z + a.w + b.x + b.y + b.z + b.w;
+        } else {
+            for (uint32_t i = 8 * c; i < ntiles; ++i) sum += __ldcg(meta.tilesize + i);
+        }
+        meta.chunkpre[c] = sum;
+    }
+    __syncthreads();
+    const unsigned long long tot = cta_exclusive_scan<unsigned long long, kCTWarps>(meta.chunkpre, nchunks, wscan);
+    if (threadIdx.x == 0) {
+        meta.chunkpre[nchunks] = tot;
+        if (d_out_len) *d_out_len = ngroups + tot;
+        enc_report(status, epoch, 0u);
+        *meta.counters = 0;
+    }
+}
+
+// bytes S .. S+15 of the 32-byte window a ++ b (S in [0, 16])
+__device__ __forceinline__ uint4 window16(const uint4& a, const uint4& b, uint32_t S) {
+    const uint32_t r = (S & 3u) * 8u;
+    uint32_t w0, w1, w2, w3, w4;
+    switch (S >> 2) {
+        case 0: w0 = a.x; w1 = a.y; w2 = a.z; w3 = a.w; w4 = b.x; break;
+        case 1: w0 = a.y; w1 = a.z; w2 = a.w; w3 = b.x; w4 = b.y; break;
+        case 2: w0 = a.z; w1 = a.w; w2 = b.x; w3 = b.y; w4 = b.z; break;
+        case 3: w0 = a.w; w1 = b.x; w2 = b.y; w3 = b.z; w4 = b.w; break;
+        default: w0 = b.x; w1 = b.y; w2 = b.z; w3 = b.w; w4 = 0; break;
+    }
+    return make_uint4(__funnelshift_r(w0, w1, r), __funnelshift_r(w1, w2, r), __funnelshift_r(w2, w3, r),
+                      __funnelshift_r(w3, w4, r));
+}
+
+__device__ __forceinline__ uint4 shfl_up4(const uint4& v, int d) {
+    return make_uint4(__shfl_up_sync(kFull, v.x, d), __shfl_up_sync(kFull, v.y, d), __shfl_up_sync(kFull, v.z, d),
+                      __shfl_up_sync(kFull, v.w, d));
+}
+__device__ __forceinline__ uint4 shfl4(const uint4& v, int l) {
+    return make_uint4(__shfl_sync(kFull, v.x, l), __shfl_sync(kFull, v.y, l), __shfl_sync(kFull, v.z, l),
+                      __shfl_sync(kFull, v.w, l));
+}
+
+__global__ void __launch_bounds__(kCTThreads)
+    svb_encode_compact_kernel(uint8_t* __restrict__ out, uint64_t n, DecodeMeta meta, uint8_t* __restrict__ slots) {
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint64_t ngroups = (n + 3) >> 2;
+    const uint64_t nsub = (ngroups + kWTGroups - 1) / kWTGroups;
+    const uint32_t ntiles = (uint32_t)((nsub + kCTWarps - 1) / kCTWarps);
+    const uint32_t t = blockIdx.x * kCTWarps + warp;
+    if (t >= ntiles) return;
+    constexpr uint32_t kTilesPerChunk = kChunkSubs / kCTWarps;
+    const uint32_t c = t / kTilesPerChunk, t0 = c * kTilesPerChunk;
+    const uint32_t x = (t0 + lane < ntiles && lane < (int)kTilesPerChunk) ? __ldcg(meta.tilesize + t0 + lane) : 0u;
+    const uint32_t pre = __reduce_add_sync(kFull, (uint32_t)lane < t - t0 ? x : 0u);
+    const uint32_t size = __shfl_sync(kFull, x, (int)(t - t0));
+    if (size == 0) return;
+    const uintptr_t D = (uintptr_t)out + ngroups + __ldcg(meta.chunkpre + c) + pre;
+    const uint32_t p = (uint32_t)(D & 15);
+    const uintptr_t Dal = D - p, Dend = D + size;
+    const uint32_t nout = (p + size + 15) >> 4;  // destination granules touched
+    const uint8_t* src = slots + (size_t)t * kSlotStride;
+    uint4 carry = make_uint4(0, 0, 0, 0);
+    for (uint32_t k0 = 0; k0 < nout; k0 += 128) {
+        uint4 cur[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const uint32_t k = k0 + 32 * u + lane;
+            cur[u] = k < nout ? __ldcg(reinterpret_cast<const uint4*>(src) + k) : make_uint4(0, 0, 0, 0);
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const uint32_t k = k0 + 32 * u + lane;
+            uint4 prv = shfl_up4(cur[u], 1);
+            if (lane == 0) prv = carry;
+            carry = shfl4(cur[u], 31);
+            if (k < nout) {
+                // destination granule k = slot bytes [16k - p, 16k - p + 16)
+                const uint4 v = window16(prv, cur[u], 16u - p);
+                const uintptr_t a = Dal + 16 * (uintptr_t)k;
+                if (a >= D && a + 16 <= Dend) {
+                    *reinterpret_cast<uint4*>(a) = v;
+                } else {
+                    const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+                    for (int bi = 0; bi < 16; ++bi)
+                        if (a + bi >= D && a + bi < Dend)
+                            *reinterpret_cast<uint8_t*>(a + bi) = (uint8_t)(w[bi >> 2] >> (8 * (bi & 3)));
+                }
+            }
+        }
+        // the slot lines just read are dead: drop them from L2 without a write-back
+        if (lane < 16 && 16 * (k0 + 8 * lane) < 16 * nout)
+            asm volatile("discard.global.L2 [%0], 128;" ::"l"(src + 16 * (size_t)k0 + 128 * lane) : "memory");
+    }
+}
+
+// ---------------------------------------------------------------------------
 // launcher (metadata layout shared with the decode: localpre / chunkpre / counters)
 // ---------------------------------------------------------------------------
+uint64_t encode_slot_bytes(uint64_t n) {
+    const uint64_t ngroups = (n + 3) >> 2;
+    const uint64_t nsub = (ngroups + kWTGroups - 1) / kWTGroups;
+    return ((nsub + kCTWarps - 1) / kCTWarps) * (uint64_t)kSlotStride;
+}
+
 cudaError_t launch_encode3(const uint32_t* in, uint64_t n, int delta, uint32_t prev, uint8_t* out,
                            uint64_t* d_out_len, void* meta_ws, unsigned long long* status, uint32_t epoch,
                            cudaStream_t stream, int* launches, cudaStream_t aux, cudaEvent_t* events,
-                           int nevents) {
+                           int nevents, uint8_t* slots, uint32_t hints) {
     const DecodeMeta m = carve_decode_meta(meta_ws, n);
     const uint64_t ngroups = (n + 3) >> 2;
     const uint64_t nsub = (ngroups + kWTGroups - 1) / kWTGroups;
@@ -303,6 +577,19 @@ cudaError_t launch_encode3(const uint32_t* in, uint64_t n, int delta, uint32_t p
         nslices = 1;
     }
     *launches = 0;
+    if (slots) {
+        const uint64_t tiles_all = (nsub + kCTWarps - 1) / kCTWarps;
+        if (delta)
+            svb_encode_slot_kernel<true><<<(unsigned)tiles_all, kCTThreads, 0, stream>>>(in, n, prev, out, m, slots,
+                                                                                        d_out_len, status, epoch, hints);
+        else
+            svb_encode_slot_kernel<false><<<(unsigned)tiles_all, kCTThreads, 0, stream>>>(in, n, prev, out, m, slots,
+                                                                                         d_out_len, status, epoch, hints);
+        svb_encode_compact_kernel<<<(unsigned)((tiles_all + kCTWarps - 1) / kCTWarps), kCTThreads, 0, stream>>>(
+            out, n, m, slots);
+        *launches = 2;
+        return cudaGetLastError();
+    }
     if (nslices > 1) {
         cudaEventRecord(events[0], stream);
         cudaStreamWaitEvent(aux, events[0], 0);

@@ -29,11 +29,15 @@ cudaError_t launch_decode3(const uint8_t* in, uint64_t in_len, uint64_t n, int d
                            uint32_t debug_flags = 0);
 uint64_t decode_meta_bytes(uint64_t n);
 int occupancy_decode_pipe();
-// Single-array encode (svb_encode.cu): size scan + tile encode; meta_ws as for the decode.
+// Single-array encode (svb_encode.cu); meta_ws as for the decode.  With `slots`
+// (encode_slot_bytes(n) of device scratch, 128-B aligned): slot encode + compaction,
+// one read of the integers; without: size scan + tile encode (two reads).
 cudaError_t launch_encode3(const uint32_t* in, uint64_t n, int delta, uint32_t prev, uint8_t* out,
                            uint64_t* d_out_len, void* meta_ws, unsigned long long* status, uint32_t epoch,
                            cudaStream_t stream, int* launches, cudaStream_t aux = nullptr,
-                           cudaEvent_t* events = nullptr, int nevents = 0);
+                           cudaEvent_t* events = nullptr, int nevents = 0, uint8_t* slots = nullptr,
+                           uint32_t hints = 3);
+uint64_t encode_slot_bytes(uint64_t n);
 uint32_t decode2_chunks(uint64_t n);  // look-back tiles of the offsets pre-pass
 uint32_t decode2_tiles(uint64_t n);   // look-back tiles (CTAs) of the tile decode
 cudaError_t launch_encode(const uint32_t* in, uint64_t n, int delta, uint32_t prev, uint8_t* out,

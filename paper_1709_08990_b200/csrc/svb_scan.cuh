@@ -57,6 +57,7 @@ struct DecodeMeta {
     uint32_t* chunktot;              // [nchunks] encode: chunk data totals (sliced size scan)
     unsigned long long* running;     // encode: data offset where the next slice starts
     unsigned long long* trace;       // debug: timestamps (nullptr = off)
+    uint32_t* tilesize;              // [ntiles] encode: packed data bytes of each 8-sub-tile tile
 };
 
 

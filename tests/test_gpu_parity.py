@@ -144,6 +144,32 @@ def test_device_misaligned_pointers(P, dev):
                 assert (int(last.item()) & 0xFFFFFFFF) == int(v[-1])
 
 
+@pytest.mark.parametrize("flags", [16, 32])
+def test_encode_both_paths(dev, flags):
+    """Both single-array encode paths, whichever the dispatch picks for the stream kind:
+    16 = size scan + tile encode (two reads), 32 = slot encode + compaction (one read)."""
+    import ctypes as C
+    import torch
+    from paper_1709_08990_b200._native import lib
+    lib.bcgpu_debug_set_flags.argtypes = [C.c_void_p, C.c_uint32]
+    rng = np.random.default_rng(5 + flags)
+    lib.bcgpu_debug_set_flags(dev._ctx, flags)
+    try:
+        for n in (1, 5, 1023, 1024, 8193, 65536 + 7, 600_001):
+            for delta, v in ((False, _mixed(rng, n)), (True, np.sort(_mixed(rng, n, (0, 1, 2))))):
+                prev = int(rng.integers(0, 2**32)) if delta else 0
+                want = oracle.encode(v, delta=delta, prev=prev)
+                src = torch.from_numpy(v.view(np.int32)).cuda()
+                outb = torch.zeros((n + 3) // 4 + 4 * n, dtype=torch.uint8, device="cuda")
+                olen = torch.zeros(1, dtype=torch.int64, device="cuda")
+                dev.encode(src, outb, olen, delta=delta, prev=prev)
+                dev.check()
+                m = int(olen.item())
+                assert m == len(want) and outb[:m].cpu().numpy().tobytes() == want, (n, delta, flags)
+    finally:
+        lib.bcgpu_debug_set_flags(dev._ctx, 0)
+
+
 def test_block_offsets_and_random_access(P):
     rng = np.random.default_rng(21)
     for n in (1, 3, 4, 7, 8192 * 3 + 5, 100001):
