@@ -137,6 +137,7 @@ static int make_batch(bcgpu_ctx* c, cudaStream_t s, BatchArgs* ba) {
     ba->status = status_ptr(c);
     ba->epoch = c->epoch;
     ba->grid = c->batch_grid;
+    ba->flags = c->debug_flags;
     return BCGPU_OK;
 }
 

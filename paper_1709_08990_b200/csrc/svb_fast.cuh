@@ -229,10 +229,22 @@ __device__ __forceinline__ uint32_t size_full(const uint32_t* __restrict__ p, ui
 
 // Row j of the sub-tile (integers at shared address sin + 512 j + 16 lane), as
 // values or mod-2^32 deltas; `last` carries x_{-1} in and the row's last raw value out.
-template <bool kDelta>
+__device__ __forceinline__ uint32_t lds32v(uint32_t a) {
+    uint32_t v;
+    asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(a) : "memory");
+    return v;
+}
+
+// kAny: sin is only 4-B aligned (segments of a batch start at any element)
+template <bool kDelta, bool kAny = false>
 __device__ __forceinline__ uint4 enc_row(uint32_t sin, int j, uint32_t& last) {
     const int lane = threadIdx.x & 31;
-    uint4 x = lds128v(sin + 512 * j + 16 * lane);
+    const uint32_t a = sin + 512 * j + 16 * lane;
+    uint4 x;
+    if (kAny && (sin & 15u))
+        x = make_uint4(lds32v(a), lds32v(a + 4), lds32v(a + 8), lds32v(a + 12));
+    else
+        x = lds128v(a);
     if constexpr (kDelta) {
         uint32_t p = __shfl_up_sync(kFull, x.w, 1);
         if (lane == 0) p = last;
@@ -243,7 +255,7 @@ __device__ __forceinline__ uint4 enc_row(uint32_t sin, int j, uint32_t& last) {
 }
 
 // Pass 1: byte lengths, control bytes (-> shared sctrl), tile-local offsets; returns the data size.
-template <bool kDelta>
+template <bool kDelta, bool kAny = false>
 __device__ __forceinline__ uint32_t enc_full_lengths(uint32_t sin, uint32_t prev_w, uint32_t sctrl,
                                                      uint32_t (&lens)[kWTRows], uint32_t (&qw)[4]) {
     const int lane = threadIdx.x & 31;
@@ -251,7 +263,7 @@ __device__ __forceinline__ uint32_t enc_full_lengths(uint32_t sin, uint32_t prev
     uint32_t last = prev_w;
 #pragma unroll
     for (int j = 0; j < kWTRows; ++j) {
-        const uint4 x = enc_row<kDelta>(sin, j, last);
+        const uint4 x = enc_row<kDelta, kAny>(sin, j, last);
         const uint32_t l0 = blen(x.x), l1 = blen(x.y), l2 = blen(x.z), l3 = blen(x.w);
         lens[j] = l0 | (l1 << 8) | (l2 << 16) | (l3 << 24);
         P[j / 3] |= (l0 + l1 + l2 + l3) << (10 * (j % 3));
@@ -270,12 +282,12 @@ __device__ __forceinline__ uint32_t enc_full_lengths(uint32_t sin, uint32_t prev
 
 // True when every integer (delta) of the full sub-tile at sin is < 256 (warp-uniform):
 // then all control bytes are 0 and the data is the low byte of each integer.
-template <bool kDelta>
+template <bool kDelta, bool kAny = false>
 __device__ __forceinline__ bool enc_full_small(uint32_t sin, uint32_t prev_w) {
     uint32_t last = prev_w, o = 0;
 #pragma unroll
     for (int j = 0; j < kWTRows; ++j) {
-        const uint4 x = enc_row<kDelta>(sin, j, last);
+        const uint4 x = enc_row<kDelta, kAny>(sin, j, last);
         o |= x.x | x.y | x.z | x.w;
     }
     return __all_sync(kFull, o < 256u);
@@ -283,14 +295,14 @@ __device__ __forceinline__ bool enc_full_small(uint32_t sin, uint32_t prev_w) {
 
 // Pack pass of a small sub-tile (enc_full_small): row j lane l's four bytes go to
 // sdst + 128 j + 4 l.  In place, as enc_full_pack.
-template <bool kDelta>
+template <bool kDelta, bool kAny = false>
 __device__ __forceinline__ void enc_small_pack(uint32_t sin, uint32_t prev_w, uint32_t sdst) {
     const int lane = threadIdx.x & 31;
     const uint32_t s = sdst & 3u;  // warp-uniform
     uint32_t last = prev_w;
 #pragma unroll
     for (int j = 0; j < kWTRows; ++j) {
-        const uint4 x = enc_row<kDelta>(sin, j, last);
+        const uint4 x = enc_row<kDelta, kAny>(sin, j, last);
         const uint32_t P = __byte_perm(__byte_perm(x.x, x.y, 0x0040), __byte_perm(x.z, x.w, 0x0040), 0x5410);
         const uint32_t a = sdst + 128 * j + 4 * lane;
         __syncwarp();  // every lane has read row j before any lane writes over it
@@ -315,14 +327,14 @@ __device__ __forceinline__ void sts_int_bytes(uint32_t a, uint32_t x, uint32_t l
 }
 
 // Pass 2: pack in place; tile data byte 0 goes to shared address sdst (<= sin - 1 + ...; see caller).
-template <bool kDelta>
+template <bool kDelta, bool kAny = false>
 __device__ __forceinline__ void enc_full_pack(uint32_t sin, uint32_t prev_w, const uint32_t (&lens)[kWTRows],
                                               const uint32_t (&qw)[4], uint32_t sdst) {
     const int lane = threadIdx.x & 31;
     uint32_t last = prev_w;
 #pragma unroll
     for (int j = 0; j < kWTRows; ++j) {
-        const uint4 x = enc_row<kDelta>(sin, j, last);
+        const uint4 x = enc_row<kDelta, kAny>(sin, j, last);
         const uint32_t l = lens[j];
         const uint32_t a = sdst + ((qw[j >> 1] >> (16 * (j & 1))) & 0xFFFFu);
         __syncwarp();  // every lane has read row j before any lane writes over it
@@ -340,6 +352,74 @@ __device__ __forceinline__ void enc_full_pack(uint32_t sin, uint32_t prev_w, con
                     for (uint32_t b = 4u - s; b < 4u; ++b) sts8(a + b, P >> (8 * b));
             }
         } else {
+            const uint32_t l0 = l & 0xFFu, l1 = (l >> 8) & 0xFFu, l2 = (l >> 16) & 0xFFu, l3 = l >> 24;
+            sts_int_bytes(a, x.x, l0);
+            sts_int_bytes(a + l0, x.y, l1);
+            sts_int_bytes(a + l0 + l1, x.z, l2);
+            sts_int_bytes(a + l0 + l1 + l2, x.w, l3);
+        }
+    }
+}
+
+// ---- rolled variants (one row body in the binary) -----------------------------
+// For kernels whose hot loop must stay small (the batch encode: several tile paths
+// are live at once and the fully unrolled bodies overflow the instruction cache).
+// Row j's packed lengths are rebuilt from its control byte, row offsets are picked
+// from qw with selects: no per-row arrays, so nothing spills to local memory.
+__device__ __forceinline__ uint32_t lens_of_ctrl(uint32_t c) {  // l_i = field_i + 1, one per byte
+    const uint32_t t = c | (c << 6);  // OR, not a multiply: the shifted copies overlap
+    return ((t | (t << 12)) & 0x03030303u) + 0x01010101u;
+}
+__device__ __forceinline__ uint32_t row_q_sel(const uint32_t (&qw)[4], int j) {
+    const uint32_t w = (j >> 1) == 0 ? qw[0] : (j >> 1) == 1 ? qw[1] : (j >> 1) == 2 ? qw[2] : qw[3];
+    return (w >> (16 * (j & 1))) & 0xFFFFu;
+}
+
+template <bool kDelta, bool kAny>
+__device__ __forceinline__ uint32_t enc_full_lengths_r(uint32_t sin, uint32_t prev_w, uint32_t sctrl, uint32_t (&qw)[4]) {
+    const int lane = threadIdx.x & 31;
+    uint32_t P0 = 0, P1 = 0, P2 = 0;
+    uint32_t last = prev_w;
+#pragma unroll 1
+    for (int j = 0; j < kWTRows; ++j) {
+        const uint4 x = enc_row<kDelta, kAny>(sin, j, last);
+        const uint32_t m0 = blen_m1(x.x), m1 = blen_m1(x.y), m2 = blen_m1(x.z), m3 = blen_m1(x.w);
+        const uint32_t v = (m0 + m1 + m2 + m3 + 4u) << (10 * (j % 3));
+        P0 |= j < 3 ? v : 0u;
+        P1 |= (j >= 3 && j < 6) ? v : 0u;
+        P2 |= j >= 6 ? v : 0u;
+        sts8(sctrl + 32 * j + lane, m0 | (m1 << 2) | (m2 << 4) | (m3 << 6));
+    }
+    const uint32_t P[3] = {P0, P1, P2};
+    return packed_row_scan(P, qw);
+}
+
+template <bool kDelta, bool kAny>
+__device__ __forceinline__ void enc_full_pack_r(uint32_t sin, uint32_t prev_w, uint32_t sctrl, const uint32_t (&qw)[4],
+                                                uint32_t sdst) {
+    const int lane = threadIdx.x & 31;
+    uint32_t last = prev_w;
+#pragma unroll 1
+    for (int j = 0; j < kWTRows; ++j) {
+        const uint4 x = enc_row<kDelta, kAny>(sin, j, last);
+        const uint32_t c = lds8(sctrl + 32 * j + lane);
+        const uint32_t a = sdst + row_q_sel(qw, j);
+        __syncwarp();  // every lane has read row j before any lane writes over it
+        if (__all_sync(kFull, c == 0)) {
+            const uint32_t P = __byte_perm(__byte_perm(x.x, x.y, 0x0040), __byte_perm(x.z, x.w, 0x0040), 0x5410);
+            const uint32_t Pp = __shfl_up_sync(kFull, P, 1);
+            const uint32_t s = a & 3u;
+            if (s == 0) {
+                sts32(a, P);
+            } else {
+                if (lane > 0) sts32(a & ~3u, __funnelshift_r(Pp, P, 8u * (4u - s)));
+                if (lane == 0)
+                    for (uint32_t b = 0; b < 4u - s; ++b) sts8(a + b, P >> (8 * b));
+                if (lane == 31)
+                    for (uint32_t b = 4u - s; b < 4u; ++b) sts8(a + b, P >> (8 * b));
+            }
+        } else {
+            const uint32_t l = lens_of_ctrl(c);
             const uint32_t l0 = l & 0xFFu, l1 = (l >> 8) & 0xFFu, l2 = (l >> 16) & 0xFFu, l3 = l >> 24;
             sts_int_bytes(a, x.x, l0);
             sts_int_bytes(a + l0, x.y, l1);

@@ -357,6 +357,7 @@ static int batch_grid(uint64_t nseg, int grid_cap) {
 
 cudaError_t launch_decode_batch(const bcgpu_decode_segment* segs, uint64_t nseg, const uint8_t* in, uint32_t* out,
                                 int delta, const BatchArgs& ba, cudaStream_t stream) {
+    if (!(ba.flags & (64 | 256))) return launch_decode_batch2(segs, nseg, in, out, delta, ba, stream);
     const int grid = batch_grid(nseg, ba.grid);
     if (grid <= 0) return cudaSuccess;
     if (delta)
@@ -368,6 +369,7 @@ cudaError_t launch_decode_batch(const bcgpu_decode_segment* segs, uint64_t nseg,
 
 cudaError_t launch_encode_batch(const bcgpu_encode_segment* segs, uint64_t nseg, const uint32_t* in, uint8_t* out,
                                 uint64_t* out_lens, int delta, const BatchArgs& ba, cudaStream_t stream) {
+    if (!(ba.flags & 64)) return launch_encode_batch2(segs, nseg, in, out, out_lens, delta, ba, stream);
     const int grid = batch_grid(nseg, ba.grid);
     if (grid <= 0) return cudaSuccess;
     if (delta)

@@ -53,6 +53,7 @@ struct BatchArgs {
     unsigned long long* status;  // [epoch:32 | bcgpu_status:32]
     uint32_t epoch;
     int grid;                    // CTAs of the warp-per-segment kernels (full residency)
+    uint32_t flags = 0;          // debug flags of the ctx (64: the unpipelined batch kernels, 256: old decode)
 };
 
 cudaError_t launch_decode_batch(const bcgpu_decode_segment* segs, uint64_t nseg, const uint8_t* in, uint32_t* out,
@@ -61,6 +62,13 @@ cudaError_t launch_encode_batch(const bcgpu_encode_segment* segs, uint64_t nseg,
                                 uint64_t* out_lens, int delta, const BatchArgs& ba, cudaStream_t stream);
 cudaError_t launch_sizes_batch(const bcgpu_encode_segment* segs, uint64_t nseg, const uint32_t* in,
                                uint64_t* out_lens, int delta, const BatchArgs& ba, cudaStream_t stream);
+
+// warp-pipelined batch decode (svb_batch2.cu)
+cudaError_t launch_decode_batch2(const bcgpu_decode_segment* segs, uint64_t nseg, const uint8_t* in, uint32_t* out,
+                                 int delta, const BatchArgs& ba, cudaStream_t stream);
+
+cudaError_t launch_encode_batch2(const bcgpu_encode_segment* segs, uint64_t nseg, const uint32_t* in, uint8_t* out,
+                                 uint64_t* out_lens, int delta, const BatchArgs& ba, cudaStream_t stream);
 
 // CTAs per SM of the batch kernels, for grid sizing.
 int occupancy_batch();

@@ -71,6 +71,11 @@ __device__ __forceinline__ void tma_store_hint(void* dst, const void* src, uint3
 
 __device__ __forceinline__ void tma_store_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
 
+// wait until all but the newest committed bulk-store group have finished reading shared memory
+__device__ __forceinline__ void tma_store_wait_read_but1() {
+    asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+}
+
 // wait until every committed bulk store has finished reading shared memory
 __device__ __forceinline__ void tma_store_wait_read() {
     asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");

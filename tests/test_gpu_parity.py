@@ -283,6 +283,15 @@ def test_batch_config5_scaled(dev):
     _batch_decode_check(dev, chunks, prevs, True, 65536)
 
 
+def test_batch_many_segments(dev):
+    """Thousands of posting lists per warp pipeline (tile and segment hand-offs, every
+    control-byte pattern of multi-byte gaps) through both batch kernels, bytes vs the oracle."""
+    from paper_1709_08990_b200 import gen
+    lb = gen.posting_lists(12000, 9, cap_total=12000 * 1500)
+    lists = [lb.values[int(lb.offsets[i]):int(lb.offsets[i + 1])] for i in range(12000)]
+    _batch_decode_check(dev, lists, [0] * len(lists), True, int(lb.lengths.max()))
+
+
 def test_batch_mixed_sizes(dev):
     rng = np.random.default_rng(77)
     sizes = [0, 1, 2, 3, 4, 5, 31, 128, 129, 4095, 4096, 4097, 5000, 8192, 8193, 20000, 70001, 17, 3]
