@@ -73,6 +73,9 @@ struct bcgpu_ctx {
     size_t d_scratch_cap = 0;
     uint8_t* slots = nullptr;  // encode: per-tile packing slots (svb_encode.cu)
     size_t slots_cap = 0;
+    cudaStream_t aux2 = nullptr;             // host pipeline: device -> host copies
+    unsigned long long* pin = nullptr;       // host pipeline: pinned offsets / status
+    size_t pin_cap = 0;                      // entries
 };
 
 static unsigned long long* ticket_ptr(bcgpu_ctx* c) { return c->ws; }
@@ -270,6 +273,10 @@ int bcgpu_ctx_create(int device, bcgpu_ctx** out) {
         return cuda_fail(e, "cudaStreamCreate");
     }
     cudaStreamCreateWithFlags(&c->aux, cudaStreamNonBlocking);
+    cudaStreamCreateWithFlags(&c->aux2, cudaStreamNonBlocking);
+    if (cudaHostAlloc(reinterpret_cast<void**>(&c->pin), 4096 * sizeof(unsigned long long), cudaHostAllocDefault) ==
+        cudaSuccess)
+        c->pin_cap = 4096;
     for (auto& ev : c->events) cudaEventCreateWithFlags(&ev, cudaEventDisableTiming);
     const int st = ensure_ws(c, 1024);
     if (st) {
@@ -291,6 +298,8 @@ int bcgpu_ctx_destroy(bcgpu_ctx* c) {
     if (c->slots) cudaFree(c->slots);
     if (c->stream) cudaStreamDestroy(c->stream);
     if (c->aux) cudaStreamDestroy(c->aux);
+    if (c->aux2) cudaStreamDestroy(c->aux2);
+    if (c->pin) cudaFreeHost(c->pin);
     for (auto& ev : c->events)
         if (ev) cudaEventDestroy(ev);
     delete c;
@@ -330,7 +339,7 @@ int bcgpu_svb_encode_device(bcgpu_ctx* c, const uint32_t* d_in, size_t n, int de
     if (st) return st;
     int launches = 0;
     BC_CUDA(launch_encode3(d_in, n, delta, prev, d_out, d_out_len, c->offs, status_ptr(c), c->epoch, s, &launches,
-                           c->aux, c->events, 96, slots, (c->debug_flags & 32) ? ((c->debug_flags >> 6) & 3u) : 3u));
+                           slots, (c->debug_flags & 32) ? ((c->debug_flags >> 6) & 3u) : 3u));
     g_launches.fetch_add((uint64_t)launches);
     return BCGPU_OK;
 }
@@ -453,6 +462,62 @@ static int scratch(bcgpu_ctx* c, size_t bytes, void** p) {
 
 static inline size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 
+// ---- host pipeline: the array moves in pieces so that the host->device copies,
+// the kernels and the device->host copies of different pieces overlap (PCIe is full
+// duplex).  A piece is a whole number of 64 Ki-integer chunks; at most 30 pieces.
+static constexpr uint64_t kChunkInts = 65536;
+static uint64_t pipe_piece_ints(uint64_t n) {
+    uint64_t p = 4ull << 20;  // 16 MiB of integers
+    const uint64_t minp = (n + 29) / 30;
+    if (p < minp) p = minp;
+    return (p + kChunkInts - 1) / kChunkInts * kChunkInts;
+}
+
+// Encode: pieces stream in on `aux`; piece k's size scan continues from piece k-1's
+// running offset and its tile encode follows on `stream`; once its offset is known on the
+// host (pinned copy) its control and data bytes stream out on `aux2`.
+static int encode_host_pipelined(bcgpu_ctx* c, const uint32_t* values, size_t n, int delta, uint32_t prev,
+                                 uint8_t* out, uint8_t* d, size_t off_out, size_t* out_len) {
+    const uint64_t P = pipe_piece_ints(n), K = (n + P - 1) / P;
+    const uint64_t ngroups = (n + 3) / 4;
+    cudaStream_t sc = c->stream, si = c->aux, so = c->aux2;
+    int st = ensure_meta(c, n, sc);
+    if (st) return st;
+    st = next_epoch(c, sc);
+    if (st) return st;
+    const uint32_t* d_in = reinterpret_cast<const uint32_t*>(d);
+    uint8_t* d_out = d + off_out;
+    unsigned long long* running = encode_running_ptr(c->offs, n);
+    cudaEvent_t* ev_in = c->events;
+    cudaEvent_t* ev_done = c->events + 32;
+    for (uint64_t k = 0; k < K; ++k) {
+        const uint64_t o = k * P, cnt = n - o < P ? n - o : P;
+        BC_CUDA(cudaMemcpyAsync(d + 4 * o, values + o, 4 * cnt, cudaMemcpyHostToDevice, si));
+        BC_CUDA(cudaEventRecord(ev_in[k], si));
+    }
+    const uint32_t cpp = (uint32_t)(P / kChunkInts);
+    for (uint64_t k = 0; k < K; ++k) {
+        BC_CUDA(cudaStreamWaitEvent(sc, ev_in[k], 0));
+        BC_CUDA(launch_encode_piece(d_in, n, delta, prev, d_out, nullptr, c->offs, status_ptr(c), c->epoch,
+                                    (uint32_t)k * cpp, (uint32_t)(k + 1) * cpp, sc));
+        BC_CUDA(cudaMemcpyAsync(c->pin + k, running, sizeof(unsigned long long), cudaMemcpyDeviceToHost, sc));
+        BC_CUDA(cudaEventRecord(ev_done[k], sc));
+    }
+    g_launches.fetch_add(2 * K);
+    for (uint64_t k = 0; k < K; ++k) {
+        BC_CUDA(cudaEventSynchronize(ev_done[k]));
+        const uint64_t lo = k ? c->pin[k - 1] : 0ull, hi = c->pin[k];
+        const uint64_t g0 = k * P / 4, g1 = (k + 1) * P / 4 < ngroups ? (k + 1) * P / 4 : ngroups;
+        BC_CUDA(cudaStreamWaitEvent(so, ev_done[k], 0));
+        BC_CUDA(cudaMemcpyAsync(out + g0, d_out + g0, g1 - g0, cudaMemcpyDeviceToHost, so));
+        if (hi > lo)
+            BC_CUDA(cudaMemcpyAsync(out + ngroups + lo, d_out + ngroups + lo, hi - lo, cudaMemcpyDeviceToHost, so));
+    }
+    BC_CUDA(cudaStreamSynchronize(so));
+    *out_len = (size_t)(ngroups + c->pin[K - 1]);
+    return BCGPU_OK;
+}
+
 int bcgpu_svb_encode_host(bcgpu_ctx* c, const uint32_t* values, size_t n, int delta, uint32_t prev, uint8_t* out,
                           size_t out_cap, size_t* out_len) {
     if (!c || !out_len || (n && (!values || !out))) return BCGPU_ERR_INVALID_ARGUMENT;
@@ -466,6 +531,8 @@ int bcgpu_svb_encode_host(bcgpu_ctx* c, const uint32_t* values, size_t n, int de
     int st = scratch(c, off_len + 256, &base);
     if (st) return st;
     uint8_t* d = static_cast<uint8_t*>(base);
+    if (out_cap >= max_out && n >= 2 * pipe_piece_ints(n) && !(c->debug_flags & 512))
+        return encode_host_pipelined(c, values, n, delta, prev, out, d, off_out, out_len);
     BC_CUDA(cudaMemcpyAsync(d, values, in_bytes, cudaMemcpyHostToDevice, c->stream));
     st = bcgpu_svb_encode_device(c, reinterpret_cast<uint32_t*>(d), n, delta, prev, d + off_out, max_out,
                                  reinterpret_cast<uint64_t*>(d + off_len), c->stream);
@@ -477,6 +544,75 @@ int bcgpu_svb_encode_host(bcgpu_ctx* c, const uint32_t* values, size_t n, int de
     BC_CUDA(cudaMemcpyAsync(out, d + off_out, len, cudaMemcpyDeviceToHost, c->stream));
     BC_CUDA(cudaStreamSynchronize(c->stream));
     *out_len = (size_t)len;
+    return BCGPU_OK;
+}
+
+static int ensure_pin(bcgpu_ctx* c, size_t entries) {
+    if (entries <= c->pin_cap) return BCGPU_OK;
+    BC_CUDA(cudaStreamSynchronize(c->stream));
+    BC_CUDA(cudaStreamSynchronize(c->aux2));
+    if (c->pin) cudaFreeHost(c->pin);
+    c->pin = nullptr;
+    c->pin_cap = 0;
+    BC_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&c->pin), entries * sizeof(unsigned long long), cudaHostAllocDefault));
+    c->pin_cap = entries;
+    return BCGPU_OK;
+}
+
+// Decode: the control bytes go first and are scanned on the device; the chunk offsets
+// come back (pinned) so each piece's data range can stream in on `aux` while earlier
+// pieces decode on `stream` and their integers stream out on `aux2`.
+static int decode_host_pipelined(bcgpu_ctx* c, const uint8_t* bytes, size_t len, size_t n, int delta, uint32_t base,
+                                 uint32_t* out, uint32_t* last, uint8_t* d, size_t off_out, size_t off_last) {
+    const uint64_t P = pipe_piece_ints(n), K = (n + P - 1) / P;
+    const uint64_t ngroups = (n + 3) / 4, nsub = (ngroups + 255) / 256, nchunks = (nsub + 63) / 64;
+    cudaStream_t sc = c->stream, si = c->aux, so = c->aux2;
+    int st = ensure_meta(c, n, sc);
+    if (st) return st;
+    st = ensure_pin(c, nchunks + 8);
+    if (st) return st;
+    st = next_epoch(c, sc);
+    if (st) return st;
+    uint32_t* d_out = reinterpret_cast<uint32_t*>(d + off_out);
+    uint32_t* d_last = reinterpret_cast<uint32_t*>(d + off_last);
+    cudaEvent_t* ev_in = c->events;
+    cudaEvent_t* ev_done = c->events + 32;
+    cudaEvent_t ev_ctrl = c->events[64];
+    // 1. control bytes -> control scan -> chunk offsets + status to the host
+    BC_CUDA(cudaMemcpyAsync(d, bytes, ngroups, cudaMemcpyHostToDevice, si));
+    BC_CUDA(cudaEventRecord(ev_ctrl, si));
+    BC_CUDA(cudaStreamWaitEvent(sc, ev_ctrl, 0));
+    BC_CUDA(launch_decode_ctrl(d, len, n, delta, c->offs, status_ptr(c), c->epoch, sc));
+    BC_CUDA(cudaMemcpyAsync(c->pin, decode_chunkpre_ptr(c->offs, n), 8 * (nchunks + 1), cudaMemcpyDeviceToHost, sc));
+    BC_CUDA(cudaMemcpyAsync(c->pin + nchunks + 1, status_ptr(c), 8, cudaMemcpyDeviceToHost, sc));
+    BC_CUDA(cudaStreamSynchronize(sc));
+    g_launches.fetch_add(1);
+    const unsigned long long word = c->pin[nchunks + 1];
+    if ((uint32_t)(word >> 32) == c->epoch && (uint32_t)word) return (int)(uint32_t)word;
+    const unsigned long long* cpre = c->pin;
+    const uint64_t cpp = P / kChunkInts;
+    // 2. pieces: data in, decode, integers out
+    for (uint64_t k = 0; k < K; ++k) {
+        const uint64_t c0 = k * cpp, c1 = (k + 1) * cpp < nchunks ? (k + 1) * cpp : nchunks;
+        const uint64_t lo = ngroups + cpre[c0], hi = ngroups + cpre[c1];
+        if (hi > lo) BC_CUDA(cudaMemcpyAsync(d + lo, bytes + lo, hi - lo, cudaMemcpyHostToDevice, si));
+        BC_CUDA(cudaEventRecord(ev_in[k], si));
+    }
+    for (uint64_t k = 0; k < K; ++k) {
+        BC_CUDA(cudaStreamWaitEvent(sc, ev_in[k], 0));
+        int l = 0;
+        BC_CUDA(launch_decode_range(d, len, n, delta, base, d_out, d_last, c->offs, k * cpp * 64, (k + 1) * cpp * 64, sc,
+                                    &l, c->trace));
+        g_launches.fetch_add((uint64_t)l);
+        BC_CUDA(cudaEventRecord(ev_done[k], sc));
+        BC_CUDA(cudaStreamWaitEvent(so, ev_done[k], 0));
+        const uint64_t i0 = k * P, cnt = n - i0 < P ? n - i0 : P;
+        BC_CUDA(cudaMemcpyAsync(out + i0, d_out + i0, 4 * cnt, cudaMemcpyDeviceToHost, so));
+    }
+    uint32_t lv = 0;
+    if (delta) BC_CUDA(cudaMemcpyAsync(&lv, d_last, sizeof(lv), cudaMemcpyDeviceToHost, so));
+    BC_CUDA(cudaStreamSynchronize(so));
+    if (last) *last = delta ? lv : out[n - 1];
     return BCGPU_OK;
 }
 
@@ -495,6 +631,8 @@ int bcgpu_svb_decode_host(bcgpu_ctx* c, const uint8_t* bytes, size_t len, size_t
     int st = scratch(c, off_last + 256, &sp);
     if (st) return st;
     uint8_t* d = static_cast<uint8_t*>(sp);
+    if (n >= 2 * pipe_piece_ints(n) && !(c->debug_flags & 512))
+        return decode_host_pipelined(c, bytes, len, n, delta, base, out, last, d, off_out, off_last);
     BC_CUDA(cudaMemcpyAsync(d, bytes, len, cudaMemcpyHostToDevice, c->stream));
     st = bcgpu_svb_decode_device(c, d, len, n, delta, base, reinterpret_cast<uint32_t*>(d + off_out),
                                  reinterpret_cast<uint32_t*>(d + off_last), c->stream);

@@ -352,7 +352,7 @@ template <int kMode, int K>
 __global__ void __launch_bounds__(kCTThreads)
     svb_decode_pool_kernel(const uint8_t* __restrict__ in, uint64_t in_len, uint64_t n, uint32_t base,
                            uint32_t* __restrict__ out, uint32_t* __restrict__ d_last, DecodeMeta meta,
-                           uint32_t pool_bytes) {
+                           uint32_t pool_bytes, uint64_t sub_begin) {
     constexpr int S = kCTWarps * K;  // sub-tiles per CTA (divides kChunkSubs)
     static_assert(kChunkSubs % S == 0 && S <= 32, "CTA sub-tiles must stay inside one chunk");
     extern __shared__ __align__(128) uint8_t dsm[];
@@ -368,7 +368,7 @@ __global__ void __launch_bounds__(kCTThreads)
     // the delta pass walks the tiles last to first: the sums pass just streamed the
     // compressed bytes front to back, so their tail is what L2 still holds
     const uint32_t bid = kMode == kModeDelta ? gridDim.x - 1 - blockIdx.x : blockIdx.x;
-    const uint64_t s0 = (uint64_t)bid * S;
+    const uint64_t s0 = sub_begin + (uint64_t)bid * S;
     const uint64_t chunk = s0 / kChunkSubs;
     const uint32_t ns = (uint32_t)(nsub - s0 < (uint64_t)S ? nsub - s0 : (uint64_t)S);
     const uintptr_t lo = (uintptr_t)in, hi = lo + in_len;
@@ -643,7 +643,7 @@ __device__ __forceinline__ uint32_t sums_generic(const uint8_t* sctrl, uint64_t 
 template <int NST>
 __global__ void __launch_bounds__(kSumThreads)
     svb_sums_kernel(const uint8_t* __restrict__ in, uint64_t in_len, uint64_t n, DecodeMeta meta,
-                    uint32_t pool_bytes) {
+                    uint32_t pool_bytes, uint32_t t_begin, uint32_t t_end) {
     extern __shared__ __align__(128) uint8_t dsm[];
     __shared__ SumsShared sh;
     constexpr uint32_t kTileCtrl = kCTWarps * kWTGroups;  // 2 KiB of control bytes per tile
@@ -651,7 +651,7 @@ __global__ void __launch_bounds__(kSumThreads)
     const uint64_t ngroups = (n + 3) >> 2;
     const uint32_t tail_r = (uint32_t)(n & 3);
     const uint64_t nsub = (ngroups + kWTGroups - 1) / kWTGroups;
-    const uint32_t ntiles = (uint32_t)((nsub + kCTWarps - 1) / kCTWarps);
+    const uint32_t ntiles = t_end;  // tiles [t_begin, t_end) of this launch
     const uintptr_t lo = (uintptr_t)in, hi = lo + in_len, data0 = lo + ngroups;
     const uint32_t stride = kTileCtrl + pool_bytes;
     if (threadIdx.x == 0) {
@@ -674,11 +674,11 @@ __global__ void __launch_bounds__(kSumThreads)
         };
         if (lane == 0)
             for (int i = 0; i < NST; ++i) {
-                const uint64_t t = (uint64_t)blockIdx.x + (uint64_t)i * gridDim.x;
+                const uint64_t t = (uint64_t)t_begin + blockIdx.x + (uint64_t)i * gridDim.x;
                 if (t < ntiles) issue_meta((uint32_t)t, i);
             }
         uint32_t k = 0;
-        for (uint32_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++k) {
+        for (uint32_t t = t_begin + blockIdx.x; t < ntiles; t += gridDim.x, ++k) {
             const int st = (int)(k % NST);
             const uint32_t ph = (k / NST) & 1u;
             uint8_t* sc = dsm + (uint32_t)st * stride;
@@ -725,7 +725,7 @@ __global__ void __launch_bounds__(kSumThreads)
     } else {
         // ---- consumers: warp w sums sub-tile 8t + w ----
         uint32_t k = 0;
-        for (uint32_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++k) {
+        for (uint32_t t = t_begin + blockIdx.x; t < ntiles; t += gridDim.x, ++k) {
             const int st = (int)(k % NST);
             const uint32_t ph = (k / NST) & 1u;
             mbar_wait_parity(&sh.full[st], ph);
@@ -777,9 +777,20 @@ __global__ void __launch_bounds__(kSumThreads)
     __syncthreads();
     if (!sh.last) return;
     __threadfence();
+    // chunks of this launch: exclusive scan continuing from the carry of the chunks before
+    // (meta.running, left by the previous piece's launch)
     const uint32_t nchunks = (uint32_t)((nsub + kChunkSubs - 1) / kChunkSubs);
-    cta_exclusive_scan<uint32_t, kSumThreads / 32>(meta.chunksums, nchunks, sh.scan);
-    if (threadIdx.x == 0) meta.counters[1] = 0;
+    constexpr uint32_t kTilesPerChunk = kChunkSubs / kCTWarps;
+    const uint32_t c0 = t_begin / kTilesPerChunk;
+    const uint32_t c1e = (t_end + kTilesPerChunk - 1) / kTilesPerChunk, c1 = c1e < nchunks ? c1e : nchunks;
+    const uint32_t base = c0 == 0 ? 0u : (uint32_t)__ldcg(meta.running);
+    const uint32_t tot = cta_exclusive_scan<uint32_t, kSumThreads / 32>(meta.chunksums + c0, c1 - c0, sh.scan);
+    if (base)
+        for (uint32_t c = threadIdx.x; c < c1 - c0; c += kSumThreads) meta.chunksums[c0 + c] += base;
+    if (threadIdx.x == 0) {
+        *meta.running = base + tot;
+        meta.counters[1] = 0;
+    }
 }
 
 // ---------------------------------------------------------------------------
@@ -823,10 +834,13 @@ uint64_t decode_meta_bytes(uint64_t n) {
 int occupancy_decode_pipe() { return 1; }  // the tile kernel is not persistent
 
 // pipelined sums pass: stage pool from the stream's average density, grid = SMs x resident CTAs
-template <int NST>
-static cudaError_t launch_sums_t(const uint8_t* in, uint64_t in_len, uint64_t n, const DecodeMeta& m, uint64_t pool,
-                                 cudaStream_t stream) {
-    const uint32_t smem = (uint32_t)(NST * (kCTWarps * kWTGroups + pool));
+static cudaError_t launch_sums(const uint8_t* in, uint64_t in_len, uint64_t n, const DecodeMeta& m, double dpb,
+                               uint32_t t_begin, uint32_t t_end, cudaStream_t stream) {
+    uint64_t pool = (uint64_t)(1.1 * dpb * kCTWarps) + 64;
+    if (pool < 4096) pool = 4096;
+    if (pool > 8ull * kWTDataMax + 64) pool = 8ull * kWTDataMax + 64;
+    pool = (pool + 15) & ~15ull;
+    const uint32_t smem = (uint32_t)(kSumStages * (kCTWarps * kWTGroups + pool));
     static int dev_cached = -1, sms = 0;
     static uint32_t occ_smem = 0;
     static int occ = 0;
@@ -834,54 +848,49 @@ static cudaError_t launch_sums_t(const uint8_t* in, uint64_t in_len, uint64_t n,
     cudaGetDevice(&dev);
     if (dev != dev_cached) {
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        const cudaError_t a =
-            cudaFuncSetAttribute(svb_sums_kernel<NST>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+        const cudaError_t a = cudaFuncSetAttribute(svb_sums_kernel<kSumStages>,
+                                                   cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
         if (a != cudaSuccess) return a;
         dev_cached = dev;
         occ_smem = 0;
     }
     if (smem != occ_smem) {
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, svb_sums_kernel<NST>, kSumThreads, smem);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, svb_sums_kernel<kSumStages>, kSumThreads, smem);
         if (occ < 1) occ = 1;
         occ_smem = smem;
     }
-    const uint64_t ngroups = (n + 3) >> 2;
-    const uint64_t nsub = (ngroups + kWTGroups - 1) / kWTGroups;
-    const uint64_t ntiles = (nsub + kCTWarps - 1) / kCTWarps;
+    if (t_end <= t_begin) return cudaSuccess;
     uint64_t grid = (uint64_t)sms * (uint64_t)occ;
-    if (grid > ntiles) grid = ntiles;
-    if (grid < 1) grid = 1;
-    svb_sums_kernel<NST><<<(unsigned)grid, kSumThreads, smem, stream>>>(in, in_len, n, m, (uint32_t)pool);
+    if (grid > t_end - t_begin) grid = t_end - t_begin;
+    svb_sums_kernel<kSumStages><<<(unsigned)grid, kSumThreads, smem, stream>>>(in, in_len, n, m, (uint32_t)pool,
+                                                                               t_begin, t_end);
     return cudaGetLastError();
 }
 
-static cudaError_t launch_sums(const uint8_t* in, uint64_t in_len, uint64_t n, const DecodeMeta& m, double dpb,
-                               cudaStream_t stream, uint32_t debug_flags) {
-    const uint32_t f10 = (debug_flags >> 8) & 0xFFu;  // debug: pool factor x10
-    uint64_t pool = (uint64_t)((f10 ? f10 / 10.0 : 1.1) * dpb * kCTWarps) + 64;
-    if (pool < 4096) pool = 4096;
-    if (pool > 8ull * kWTDataMax + 64) pool = 8ull * kWTDataMax + 64;
-    pool = (pool + 15) & ~15ull;
-    switch ((debug_flags >> 16) & 0xFu) {  // debug: stage count
-        case 4: return launch_sums_t<4>(in, in_len, n, m, pool, stream);
-        case 6: return launch_sums_t<6>(in, in_len, n, m, pool, stream);
-        case 8: return launch_sums_t<8>(in, in_len, n, m, pool, stream);
-        default: return launch_sums_t<kSumStages>(in, in_len, n, m, pool, stream);
-    }
-}
-
-cudaError_t launch_decode3(const uint8_t* in, uint64_t in_len, uint64_t n, int delta, uint32_t base, uint32_t* out,
-                           uint32_t* d_last, void* meta_ws, unsigned long long* status, uint32_t epoch, int pipe_grid,
-                           cudaStream_t stream, int* launches, unsigned long long* trace, uint32_t debug_flags) {
-    DecodeMeta m = carve_decode_meta(meta_ws, n);
-    m.trace = trace;
+// decode pass 1 over the whole stream (control bytes only); zeroes the chunk sums for delta
+cudaError_t launch_decode_ctrl(const uint8_t* in, uint64_t in_len, uint64_t n, int delta, void* meta_ws,
+                               unsigned long long* status, uint32_t epoch, cudaStream_t stream) {
+    const DecodeMeta m = carve_decode_meta(meta_ws, n);
     const uint64_t ngroups = (n + 3) >> 2;
     const uint64_t nsub = (ngroups + kWTGroups - 1) / kWTGroups;
     const uint32_t nchunks = (uint32_t)((nsub + kChunkSubs - 1) / kChunkSubs);
     svb_ctrl_scan_kernel<<<nchunks, 256, 0, stream>>>(in, in_len, n, m, status, epoch, delta);
-    cudaError_t e = cudaGetLastError();
-    if (e != cudaSuccess) return e;
-    (void)pipe_grid;
+    return cudaGetLastError();
+}
+
+// Decode passes 2-3 for sub-tiles [sub_begin, sub_end) (multiples of a 64-sub-tile chunk,
+// except at the stream's end), after launch_decode_ctrl.  Delta ranges must be issued in
+// order on one stream (each continues the previous range's carry).
+cudaError_t launch_decode_range(const uint8_t* in, uint64_t in_len, uint64_t n, int delta, uint32_t base,
+                                uint32_t* out, uint32_t* d_last, void* meta_ws, uint64_t sub_begin, uint64_t sub_end,
+                                cudaStream_t stream, int* launches, unsigned long long* trace) {
+    DecodeMeta m = carve_decode_meta(meta_ws, n);
+    m.trace = trace;
+    const uint64_t ngroups = (n + 3) >> 2;
+    const uint64_t nsub = (ngroups + kWTGroups - 1) / kWTGroups;
+    if (sub_end > nsub) sub_end = nsub;
+    *launches = 0;
+    if (sub_begin >= sub_end) return cudaSuccess;
     // pooled decode: K sub-tiles per warp and the pool from the stream's average density
     const double dpb = nsub ? (double)(in_len > ngroups ? in_len - ngroups : 0) / (double)nsub : 0.0;  // B / sub-tile
     const int K = dpb < 1400.0 ? 4 : 2;
@@ -892,45 +901,47 @@ cudaError_t launch_decode3(const uint8_t* in, uint64_t in_len, uint64_t n, int d
     if (pool > 160 * 1024) pool = 160 * 1024;
     pool = (pool + 15) & ~15ull;
     const uint32_t smem = (uint32_t)(S * kWTGroups + pool);
-    const int pgrid = (int)((nsub + S - 1) / S);
-    if (!(debug_flags & 4)) {
+    const int pgrid = (int)((sub_end - sub_begin + S - 1) / S);
 #define BC_POOL_LAUNCH(MODE, KK)                                                                                 \
     do {                                                                                                         \
         static const cudaError_t a_ = cudaFuncSetAttribute(svb_decode_pool_kernel<MODE, KK>,                    \
                                                            cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024); \
         if (a_ != cudaSuccess) return a_;                                                                        \
         svb_decode_pool_kernel<MODE, KK><<<pgrid, kCTThreads, smem, stream>>>(in, in_len, n, base, out, d_last, m,  \
-                                                                             (uint32_t)pool);                   \
+                                                                             (uint32_t)pool, sub_begin);        \
     } while (0)
-        if (delta) {
-            if (debug_flags & 8) {  // debug: the pooled sums pass instead of the pipelined one
-                if (K == 4) BC_POOL_LAUNCH(kModeSums, 4);
-                else BC_POOL_LAUNCH(kModeSums, 2);
-            } else {
-                const cudaError_t e2 = launch_sums(in, in_len, n, m, dpb, stream, debug_flags);
-                if (e2 != cudaSuccess) return e2;
-            }
-            if (K == 4) BC_POOL_LAUNCH(kModeDelta, 4);
-            else BC_POOL_LAUNCH(kModeDelta, 2);
-            *launches = 3;
-        } else {
-            if (K == 4) BC_POOL_LAUNCH(kModePlain, 4);
-            else BC_POOL_LAUNCH(kModePlain, 2);
-            *launches = 2;
-        }
-#undef BC_POOL_LAUNCH
-        return cudaGetLastError();
-    }
-    const int grid = (int)((nsub + kCTWarps - 1) / kCTWarps);
     if (delta) {
-        svb_decode_tile_kernel<kModeSums><<<grid, kCTThreads, 0, stream>>>(in, in_len, n, base, out, d_last, m);
-        svb_decode_tile_kernel<kModeDelta><<<grid, kCTThreads, 0, stream>>>(in, in_len, n, base, out, d_last, m);
-        *launches = 3;
-    } else {
-        svb_decode_tile_kernel<kModePlain><<<grid, kCTThreads, 0, stream>>>(in, in_len, n, base, out, d_last, m);
+        const uint32_t t0 = (uint32_t)(sub_begin / kCTWarps), t1 = (uint32_t)((sub_end + kCTWarps - 1) / kCTWarps);
+        const cudaError_t e2 = launch_sums(in, in_len, n, m, dpb, t0, t1, stream);
+        if (e2 != cudaSuccess) return e2;
+        if (K == 4) BC_POOL_LAUNCH(kModeDelta, 4);
+        else BC_POOL_LAUNCH(kModeDelta, 2);
         *launches = 2;
+    } else {
+        if (K == 4) BC_POOL_LAUNCH(kModePlain, 4);
+        else BC_POOL_LAUNCH(kModePlain, 2);
+        *launches = 1;
     }
+#undef BC_POOL_LAUNCH
     return cudaGetLastError();
 }
+
+cudaError_t launch_decode3(const uint8_t* in, uint64_t in_len, uint64_t n, int delta, uint32_t base, uint32_t* out,
+                           uint32_t* d_last, void* meta_ws, unsigned long long* status, uint32_t epoch, int pipe_grid,
+                           cudaStream_t stream, int* launches, unsigned long long* trace, uint32_t debug_flags) {
+    (void)pipe_grid;
+    (void)debug_flags;
+    cudaError_t e = launch_decode_ctrl(in, in_len, n, delta, meta_ws, status, epoch, stream);
+    if (e != cudaSuccess) return e;
+    const uint64_t ngroups = (n + 3) >> 2;
+    const uint64_t nsub = (ngroups + kWTGroups - 1) / kWTGroups;
+    int l = 0;
+    e = launch_decode_range(in, in_len, n, delta, base, out, d_last, meta_ws, 0, nsub, stream, &l, trace);
+    *launches = 1 + l;
+    return e;
+}
+
+// device address of the chunk offsets (nchunks + 1 entries, after launch_decode_ctrl)
+unsigned long long* decode_chunkpre_ptr(void* meta_ws, uint64_t n) { return carve_decode_meta(meta_ws, n).chunkpre; }
 
 }  // namespace bcgpu

@@ -557,26 +557,11 @@ uint64_t encode_slot_bytes(uint64_t n) {
 
 cudaError_t launch_encode3(const uint32_t* in, uint64_t n, int delta, uint32_t prev, uint8_t* out,
                            uint64_t* d_out_len, void* meta_ws, unsigned long long* status, uint32_t epoch,
-                           cudaStream_t stream, int* launches, cudaStream_t aux, cudaEvent_t* events,
-                           int nevents, uint8_t* slots, uint32_t hints) {
+                           cudaStream_t stream, int* launches, uint8_t* slots, uint32_t hints) {
     const DecodeMeta m = carve_decode_meta(meta_ws, n);
     const uint64_t ngroups = (n + 3) >> 2;
     const uint64_t nsub = (ngroups + kWTGroups - 1) / kWTGroups;
     const uint32_t nchunks = (uint32_t)((nsub + kChunkSubs - 1) / kChunkSubs);
-    constexpr uint32_t kTilesPerChunk = kChunkSubs / kCTWarps;
-    // L2-sized slices: the size scan of slice k+1 (HBM-bound) runs on `stream` while
-    // the tile encode of slice k (issue-bound) re-reads its integers from L2 on `aux`
-    uint32_t slice = 128;  // chunks = 8 Mi integers = 32 MiB
-    if ((nchunks + slice - 1) / slice > 64) slice = (nchunks + 63) / 64;
-    uint32_t nslices = (nchunks + slice - 1) / slice;
-    // measured on B200: each slice's size scan has too few CTAs to stream at HBM rate and the
-    // scans serialise on `stream`, so slicing lost (cfg2 encode 139 -> 226 us); off by default
-    constexpr bool kSliced = false;
-    if (!kSliced || !aux || nslices < 2 || nevents < (int)nslices + 2) {
-        slice = nchunks;
-        nslices = 1;
-    }
-    *launches = 0;
     if (slots) {
         const uint64_t tiles_all = (nsub + kCTWarps - 1) / kCTWarps;
         if (delta)
@@ -590,38 +575,38 @@ cudaError_t launch_encode3(const uint32_t* in, uint64_t n, int delta, uint32_t p
         *launches = 2;
         return cudaGetLastError();
     }
-    if (nslices > 1) {
-        cudaEventRecord(events[0], stream);
-        cudaStreamWaitEvent(aux, events[0], 0);
-    }
-    for (uint32_t k = 0; k < nslices; ++k) {
-        const uint32_t c0 = k * slice, c1 = c0 + slice < nchunks ? c0 + slice : nchunks;
-        const uint32_t t0 = c0 * kTilesPerChunk;
-        const uint64_t t1_ = (uint64_t)c1 * kTilesPerChunk;
-        const uint64_t tiles_all = (nsub + kCTWarps - 1) / kCTWarps;
-        const uint32_t t1 = (uint32_t)(t1_ < tiles_all ? t1_ : tiles_all);
-        cudaStream_t ts = nslices > 1 ? aux : stream;
-        if (delta) {
-            svb_size_scan_kernel<true><<<c1 - c0, 256, 0, stream>>>(in, n, prev, m, d_out_len, status, epoch, c0, nchunks);
-        } else {
-            svb_size_scan_kernel<false><<<c1 - c0, 256, 0, stream>>>(in, n, prev, m, d_out_len, status, epoch, c0,
-                                                                     nchunks);
-        }
-        if (nslices > 1) {
-            cudaEventRecord(events[k + 1], stream);
-            cudaStreamWaitEvent(aux, events[k + 1], 0);
-        }
-        if (delta)
-            svb_encode_tile_kernel<true><<<t1 - t0, kCTThreads, 0, ts>>>(in, n, prev, out, m, t0);
-        else
-            svb_encode_tile_kernel<false><<<t1 - t0, kCTThreads, 0, ts>>>(in, n, prev, out, m, t0);
-        *launches += 2;
-    }
-    if (nslices > 1) {
-        cudaEventRecord(events[nslices + 1], aux);
-        cudaStreamWaitEvent(stream, events[nslices + 1], 0);
+    *launches = 2;
+    return launch_encode_piece(in, n, delta, prev, out, d_out_len, meta_ws, status, epoch, 0, nchunks, stream);
+}
+
+// Chunks [c0, c1) of a two-read encode: size scan continuing from the running offset of
+// the chunks before c0 (meta.running, left by the previous piece's scan), then the tile
+// encode of those chunks.  Pieces must be issued in order on one stream.
+cudaError_t launch_encode_piece(const uint32_t* in, uint64_t n, int delta, uint32_t prev, uint8_t* out,
+                                uint64_t* d_out_len, void* meta_ws, unsigned long long* status, uint32_t epoch,
+                                uint32_t c0, uint32_t c1, cudaStream_t stream) {
+    const DecodeMeta m = carve_decode_meta(meta_ws, n);
+    const uint64_t ngroups = (n + 3) >> 2;
+    const uint64_t nsub = (ngroups + kWTGroups - 1) / kWTGroups;
+    const uint32_t nchunks = (uint32_t)((nsub + kChunkSubs - 1) / kChunkSubs);
+    constexpr uint32_t kTilesPerChunk = kChunkSubs / kCTWarps;
+    if (c1 > nchunks) c1 = nchunks;
+    if (c0 >= c1) return cudaSuccess;
+    const uint64_t tiles_all = (nsub + kCTWarps - 1) / kCTWarps;
+    const uint32_t t0 = c0 * kTilesPerChunk;
+    const uint64_t t1_ = (uint64_t)c1 * kTilesPerChunk;
+    const uint32_t t1 = (uint32_t)(t1_ < tiles_all ? t1_ : tiles_all);
+    if (delta) {
+        svb_size_scan_kernel<true><<<c1 - c0, 256, 0, stream>>>(in, n, prev, m, d_out_len, status, epoch, c0, nchunks);
+        svb_encode_tile_kernel<true><<<t1 - t0, kCTThreads, 0, stream>>>(in, n, prev, out, m, t0);
+    } else {
+        svb_size_scan_kernel<false><<<c1 - c0, 256, 0, stream>>>(in, n, prev, m, d_out_len, status, epoch, c0, nchunks);
+        svb_encode_tile_kernel<false><<<t1 - t0, kCTThreads, 0, stream>>>(in, n, prev, out, m, t0);
     }
     return cudaGetLastError();
 }
+
+// device address of the running data offset (bytes after the last encoded piece)
+unsigned long long* encode_running_ptr(void* meta_ws, uint64_t n) { return carve_decode_meta(meta_ws, n).running; }
 
 }  // namespace bcgpu

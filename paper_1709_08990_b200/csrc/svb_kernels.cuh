@@ -28,15 +28,27 @@ cudaError_t launch_decode3(const uint8_t* in, uint64_t in_len, uint64_t n, int d
                            cudaStream_t stream, int* launches, unsigned long long* trace = nullptr,
                            uint32_t debug_flags = 0);
 uint64_t decode_meta_bytes(uint64_t n);
+// The same split for the pipelined host API: the control scan over the whole stream,
+// then passes 2-3 per range of sub-tiles (chunk multiples, in order for delta).
+cudaError_t launch_decode_ctrl(const uint8_t* in, uint64_t in_len, uint64_t n, int delta, void* meta_ws,
+                               unsigned long long* status, uint32_t epoch, cudaStream_t stream);
+cudaError_t launch_decode_range(const uint8_t* in, uint64_t in_len, uint64_t n, int delta, uint32_t base,
+                                uint32_t* out, uint32_t* d_last, void* meta_ws, uint64_t sub_begin, uint64_t sub_end,
+                                cudaStream_t stream, int* launches, unsigned long long* trace = nullptr);
+unsigned long long* decode_chunkpre_ptr(void* meta_ws, uint64_t n);
 int occupancy_decode_pipe();
 // Single-array encode (svb_encode.cu); meta_ws as for the decode.  With `slots`
 // (encode_slot_bytes(n) of device scratch, 128-B aligned): slot encode + compaction,
 // one read of the integers; without: size scan + tile encode (two reads).
 cudaError_t launch_encode3(const uint32_t* in, uint64_t n, int delta, uint32_t prev, uint8_t* out,
                            uint64_t* d_out_len, void* meta_ws, unsigned long long* status, uint32_t epoch,
-                           cudaStream_t stream, int* launches, cudaStream_t aux = nullptr,
-                           cudaEvent_t* events = nullptr, int nevents = 0, uint8_t* slots = nullptr,
-                           uint32_t hints = 3);
+                           cudaStream_t stream, int* launches, uint8_t* slots = nullptr, uint32_t hints = 3);
+// Chunks [c0, c1) (64 Ki integers each) of the two-read encode, continuing from the
+// previous piece's running offset; 2 launches.  For the pipelined host API.
+cudaError_t launch_encode_piece(const uint32_t* in, uint64_t n, int delta, uint32_t prev, uint8_t* out,
+                                uint64_t* d_out_len, void* meta_ws, unsigned long long* status, uint32_t epoch,
+                                uint32_t c0, uint32_t c1, cudaStream_t stream);
+unsigned long long* encode_running_ptr(void* meta_ws, uint64_t n);
 uint64_t encode_slot_bytes(uint64_t n);
 uint32_t decode2_chunks(uint64_t n);  // look-back tiles of the offsets pre-pass
 uint32_t decode2_tiles(uint64_t n);   // look-back tiles (CTAs) of the tile decode

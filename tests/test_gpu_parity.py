@@ -116,6 +116,25 @@ def test_malformed(P):
         P.svb_decode(enc[: len(enc) // 2], v.size, out)
 
 
+def test_host_pipeline_pieces(P):
+    """Arrays large enough for the pipelined host API (pieces of 4 Mi integers streamed
+    over PCIe): round trips, odd tail, and malformed streams still reported."""
+    rng = np.random.default_rng(13)
+    n = 9 * (1 << 20) + 4 * 65536 + 777
+    v = np.cumsum(rng.integers(0, 3000, n, dtype=np.uint64)).astype(np.uint32)
+    _check_roundtrip(P, v, delta=True, prev=7)
+    w = _mixed(rng, n, (0, 1, 3))
+    _check_roundtrip(P, w)
+    enc = oracle.encode(v, delta=True, prev=7)
+    out = np.empty(n, np.uint32)
+    with pytest.raises(P.CodecError) as e:
+        P.svb_decode_delta(enc[:-3], n, 7, out)
+    assert e.value.code == P.errc.truncated
+    with pytest.raises(P.CodecError) as e:
+        P.svb_decode_delta(enc + b"\x05", n, 7, out)
+    assert e.value.code == P.errc.trailing_bytes
+
+
 # ---- device API: misaligned buffers, offsets, blocks -------------------------
 def test_device_misaligned_pointers(P, dev):
     import torch
