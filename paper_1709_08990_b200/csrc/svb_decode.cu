@@ -80,6 +80,11 @@ __global__ void __launch_bounds__(256)
     const uint32_t tail_r = (uint32_t)(n & 3);
     const uint64_t nsub = (ngroups + kWTGroups - 1) / kWTGroups;
     if (zero_sums && tid == 0) meta.chunksums[chunk] = 0;
+    // delta: clear this chunk's one-pass aggregates, so nothing stale can carry the call's epoch
+    if (zero_sums && tid < kChunkSubs / kCTWarps) {
+        const uint64_t tile = (uint64_t)chunk * (kChunkSubs / kCTWarps) + tid;
+        if (tile * kCTWarps < nsub) meta.agg[tile] = 0;
+    }
     const uint64_t g = (uint64_t)chunk * kChunkCtrl + (uint64_t)tid * 64;
     uint32_t q = quarter_length(in, g, ngroups, tail_r);
     // sub-tile length = sum of its 4 quarters (lanes 4k..4k+3)
@@ -390,7 +395,7 @@ __global__ void __launch_bounds__(kCTThreads)
         const uint32_t ctx = tma_cover_bytes(cb, cb + cg, lo, hi);
         if (ctx != 0xFFFFFFFFu && (cb & 15) == 0 && ctx) {
             mbar_expect(&sh.bar_ctrl, ctx);
-            tma_load(sctrl, reinterpret_cast<const void*>(cb), ctx, &sh.bar_ctrl);
+            tma_load_hint(sctrl, reinterpret_cast<const void*>(cb), ctx, &sh.bar_ctrl, l2_policy_drop());
         } else {
             for (uint64_t i = 0; i < cg; ++i) sctrl[i] = __ldg(in + s0 * kWTGroups + i);
             mbar_arrive(&sh.bar_ctrl);
@@ -420,7 +425,7 @@ __global__ void __launch_bounds__(kCTThreads)
         single = tx != 0xFFFFFFFFu && tx + 16 <= pool_bytes;
         if (single && tx) {
             mbar_expect(&sh.bar_data[0], tx);
-            tma_load(pool, reinterpret_cast<const void*>(abeg & ~(uintptr_t)15), tx, &sh.bar_data[0]);
+            tma_load_hint(pool, reinterpret_cast<const void*>(abeg & ~(uintptr_t)15), tx, &sh.bar_data[0], l2_policy_drop());
         } else if (single) {
             mbar_arrive(&sh.bar_data[0]);
         }
@@ -716,8 +721,10 @@ __global__ void __launch_bounds__(kSumThreads)
                 if (meta.trace) meta.trace[8ull * t + 1] = gtimer();
                 fence_async_smem();
                 mbar_expect(&sh.full[st], (c_tma ? ctx : 0u) + (fits ? tx : 0u));
-                if (c_tma && ctx) tma_load(sc, reinterpret_cast<const void*>(cb), ctx, &sh.full[st]);
-                if (fits && tx) tma_load(pool, reinterpret_cast<const void*>(base), tx, &sh.full[st]);
+                // the delta pass re-reads these bytes right after: keep them in L2
+                const uint64_t keep = l2_policy_keep();
+                if (c_tma && ctx) tma_load_hint(sc, reinterpret_cast<const void*>(cb), ctx, &sh.full[st], keep);
+                if (fits && tx) tma_load_hint(pool, reinterpret_cast<const void*>(base), tx, &sh.full[st], keep);
                 const uint64_t tn = (uint64_t)t + (uint64_t)NST * gridDim.x;  // meta[st] was consumed above
                 if (tn < ntiles) issue_meta((uint32_t)tn, st);
             }
@@ -794,6 +801,337 @@ __global__ void __launch_bounds__(kSumThreads)
 }
 
 // ---------------------------------------------------------------------------
+// 2b. one-pass delta decode: deferred look-back
+// ---------------------------------------------------------------------------
+// Replaces the sums pass + delta pass (two reads of the compressed bytes) with one
+// read, and no CTA ever waits on a CTA of its own round.  Persistent CTAs
+// (cooperative launch: all co-resident) take tiles t = b, b + G, ...  The producer
+// warp streams control + data bytes through a TMA ring exactly as in the sums
+// pass.  For tile t (round r) the 8 consumer warps:
+//   1. sum their sub-tiles straight from the staged bytes (dp4a for all-zero
+//      control bytes, as the sums pass) and publish the tile sum A(t) as an
+//      epoch-tagged aggregate (relaxed 64-bit store);
+//   2. resolve the carry of the CTA's previous tile tp = t - G, deferred by one
+//      round: carry(tp) = incl(tp - G) + sum of A(j), tp - G < j < tp -- its own
+//      inclusive prefix from two rounds back plus the aggregates of the G - 1
+//      tiles in between, all published a round or more earlier (their loads were
+//      issued at the top of the iteration, so their latency hides behind step 1);
+//   3. decode tile tp from its stage -- held one extra round -- with that carry,
+//      store it from registers, and release the stage.
+// The compressed bytes are read from HBM once (the stage is re-read from smem).
+// A round-r aggregate only depends on waits for rounds <= r - 1, so with every
+// CTA resident the chain cannot deadlock.  Only aggregates are shared; every CTA
+// keeps its own inclusive chain.
+constexpr int kD1Stages = 5;  // tiles t and t - G held, the rest in flight
+
+struct __align__(16) D1Shared {
+    SumMeta meta[kD1Stages];
+    SumHdr hdr[kD1Stages];
+    uint64_t full[kD1Stages], empty[kD1Stages], mfull[kD1Stages];
+    uint32_t wsum[3][kCTWarps];  // sub-tile sums, by round % 3
+    uint32_t red[kCTWarps];
+    uint32_t carry, incl;
+};
+
+__device__ __forceinline__ unsigned long long ld_relaxed_u64(const unsigned long long* p) {
+    unsigned long long v;
+    asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_relaxed_u64(unsigned long long* p, unsigned long long v) {
+    asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ void consumers_sync() { asm volatile("bar.sync 1, 256;" ::: "memory"); }
+__device__ __forceinline__ void sts128(uint32_t a, const uint4& v) {
+    asm volatile("st.shared.v4.u32 [%0], {%1,%2,%3,%4};" ::"r"(a), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w) : "memory");
+}
+
+// any sub-tile (partial, or data read from global memory) with carry `run`: word i of its
+// data window is fw(i), data at byte `head`; stores its integers, returns the last value
+template <class Fetch>
+__device__ __forceinline__ uint32_t decode_generic_store(const uint8_t* sctrl, uint64_t g0, uint64_t ngroups,
+                                                         uint32_t tail_r, uint32_t head, Fetch fw, uint32_t run,
+                                                         uint32_t* __restrict__ out) {
+    const int lane = threadIdx.x & 31;
+    const WarpCtrl w = load_warp_ctrl<true>(sctrl, g0, ngroups, tail_r, g0);
+    const bool out16 = (((uintptr_t)(out + 4 * g0)) & 15) == 0;
+#pragma unroll 1
+    for (int j = 0; j < kWTRows; ++j) {
+        const uint32_t c = row_ctrl(w, j);
+        uint32_t b = head + row_q(w, j);
+        const uint64_t g = g0 + 32 * j + lane;
+        const uint32_t cnt = group_count(g, ngroups, tail_r);
+        uint32_t x[4];
+#pragma unroll
+        for (int f = 0; f < 4; ++f) {
+            const uint32_t l = ((c >> (2 * f)) & 3u) + 1u;
+            const uint32_t y = __funnelshift_r(fw(b >> 2), fw((b >> 2) + 1), (b & 3u) * 8u);
+            x[f] = (uint32_t)f < cnt ? (y & (0xFFFFFFFFu >> (32u - 8u * l))) : 0u;
+            b += l;
+        }
+        uint4 v = make_uint4(x[0], x[0] + x[1], x[0] + x[1] + x[2], x[0] + x[1] + x[2] + x[3]);
+        const uint32_t I = warp_inclusive_scan(v.w);
+        v = add4(v, run + I - v.w);
+        if (cnt) store_group(out + 4 * g, v, cnt, out16);
+        run += __shfl_sync(kFull, I, 31);
+    }
+    return run;
+}
+
+__global__ void __launch_bounds__(kSumThreads, 3)
+    svb_decode1_kernel(const uint8_t* __restrict__ in, uint64_t in_len, uint64_t n, uint32_t base,
+                       uint32_t* __restrict__ out, uint32_t* __restrict__ d_last, DecodeMeta meta, uint32_t pool_bytes,
+                       uint32_t epoch) {
+    extern __shared__ __align__(128) uint8_t dsm[];
+    __shared__ D1Shared sh;
+    constexpr uint32_t kTileCtrl = kCTWarps * kWTGroups;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint64_t ngroups = (n + 3) >> 2;
+    const uint32_t tail_r = (uint32_t)(n & 3);
+    const uint64_t nsub = (ngroups + kWTGroups - 1) / kWTGroups;
+    const uint32_t ntiles = (uint32_t)((nsub + kCTWarps - 1) / kCTWarps);
+    const uint32_t G = gridDim.x;
+    const uintptr_t lo = (uintptr_t)in, hi = lo + in_len, data0 = lo + ngroups;
+    const uint32_t stride = kTileCtrl + pool_bytes;
+    if (threadIdx.x == 0) {
+#pragma unroll
+        for (int k = 0; k < kD1Stages; ++k) {
+            mbar_init(&sh.full[k], 1);
+            mbar_init(&sh.empty[k], kCTWarps);
+            mbar_init(&sh.mfull[k], 1);
+        }
+        sh.incl = base;
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    if (warp == kCTWarps) {
+        // ---- producer (as in svb_sums_kernel) ----
+        auto issue_meta = [&](uint32_t t, int st) {
+            const uint64_t s0 = (uint64_t)t * kCTWarps, c = s0 / kChunkSubs;
+            mbar_expect(&sh.mfull[st], 48 + 32);
+            tma_load(sh.meta[st].loc, meta.localpre + s0, 48, &sh.mfull[st]);
+            tma_load(sh.meta[st].chk, meta.chunkpre + (c & ~1ull), 32, &sh.mfull[st]);
+        };
+        if (lane == 0)
+            for (int i = 0; i < kD1Stages; ++i) {
+                const uint64_t t = (uint64_t)blockIdx.x + (uint64_t)i * G;
+                if (t < ntiles) issue_meta((uint32_t)t, i);
+            }
+        uint32_t k = 0;
+        for (uint32_t t = blockIdx.x; t < ntiles; t += G, ++k) {
+            const int st = (int)(k % kD1Stages);
+            const uint32_t ph = (k / kD1Stages) & 1u;
+            uint8_t* sc = dsm + (uint32_t)st * stride;
+            uint8_t* pool = sc + kTileCtrl;
+            const uint64_t s0 = (uint64_t)t * kCTWarps, chunk = s0 / kChunkSubs;
+            const uint32_t ns = (uint32_t)(nsub - s0 < (uint64_t)kCTWarps ? nsub - s0 : (uint64_t)kCTWarps);
+            mbar_wait_parity(&sh.mfull[st], ph);
+            const SumMeta& M = sh.meta[st];
+            const unsigned long long cpre = M.chk[chunk & 1];
+            const bool end_at_chunk = s0 + ns == nsub || (s0 + ns) % kChunkSubs == 0;
+            const unsigned long long A = cpre + M.loc[0];
+            const unsigned long long B = end_at_chunk ? M.chk[(chunk & 1) + 1] : cpre + M.loc[ns];
+            const uint32_t li = (uint32_t)lane < ns ? (uint32_t)lane : ns;
+            const unsigned long long my = (li == ns) ? B : cpre + M.loc[li];
+            const uintptr_t Ag = data0 + A, Bg = data0 + B, bse = Ag & ~(uintptr_t)15;
+            const uint32_t tx = tma_cover_bytes(Ag, Bg, lo, hi);
+            const bool fits = tx != 0xFFFFFFFFu && tx + 16 <= pool_bytes;
+            const uintptr_t cb = lo + s0 * kWTGroups;
+            const uint64_t cg = ngroups - s0 * kWTGroups < (uint64_t)kTileCtrl ? ngroups - s0 * kWTGroups
+                                                                                 : (uint64_t)kTileCtrl;
+            const uint32_t ctx = tma_cover_bytes(cb, cb + cg, lo, hi);
+            const bool c_tma = ctx != 0xFFFFFFFFu && (cb & 15) == 0;
+            __syncwarp();
+            if (k >= (uint32_t)kD1Stages) mbar_wait_parity(&sh.empty[st], ph ^ 1u);
+            if (!c_tma)
+                for (uint32_t i = lane; i < (uint32_t)cg; i += 32) sc[i] = __ldg(in + s0 * kWTGroups + i);
+            if (lane <= 8) sh.hdr[st].head[lane] = (uint32_t)(data0 + my - bse);
+            if (lane == 0) {
+                sh.hdr[st].base = bse;
+                sh.hdr[st].mode = fits ? 0u : 1u;
+            }
+            __syncwarp();
+            if (lane == 0) {
+                fence_async_smem();
+                mbar_expect(&sh.full[st], (c_tma ? ctx : 0u) + (fits ? tx : 0u));
+                const uint64_t pol = l2_policy_drop();
+                if (c_tma && ctx) tma_load_hint(sc, reinterpret_cast<const void*>(cb), ctx, &sh.full[st], pol);
+                if (fits && tx) tma_load_hint(pool, reinterpret_cast<const void*>(bse), tx, &sh.full[st], pol);
+                const uint64_t tn = (uint64_t)t + (uint64_t)kD1Stages * G;
+                if (tn < ntiles) issue_meta((uint32_t)tn, st);
+            }
+        }
+        return;
+    }
+    // ---- consumers ----
+    const int ct = threadIdx.x;  // 0..255
+    // look-back window of tile tp: tiles max(0, tp - G + 1) .. tp - 1; two entries per
+    // thread prefetched, any more read at resolve time
+    auto window_lo = [&](uint32_t tp) -> uint32_t { return tp + 1 > G ? tp + 1 - G : 0u; };
+    unsigned long long pf0 = 0, pf1 = 0;
+    auto prefetch = [&](uint32_t tp) {
+        const uint32_t wl = window_lo(tp);
+        pf0 = wl + ct < tp ? ld_relaxed_u64(meta.agg + wl + ct) : 0ull;
+        pf1 = wl + ct + 256 < tp ? ld_relaxed_u64(meta.agg + wl + ct + 256) : 0ull;
+    };
+    auto entry = [&](uint32_t j, unsigned long long v) -> uint32_t {  // tile j's aggregate of this call
+        while ((uint32_t)(v >> 32) != epoch) v = ld_relaxed_u64(meta.agg + j);
+        return (uint32_t)v;
+    };
+    // resolve tile tp (its sub-tile sums in wsum[q]), decode it from stage st with the carry,
+    // store it and release the stage
+    auto resolve = [&](uint32_t tp, int st, int q) {
+        const uint32_t wl = window_lo(tp);
+        uint32_t part = 0;
+        if (wl + ct < tp) part += entry(wl + ct, pf0);
+        if (wl + ct + 256 < tp) part += entry(wl + ct + 256, pf1);
+        for (uint32_t j = wl + ct + 512; j < tp; j += 256) part += entry(j, ld_relaxed_u64(meta.agg + j));
+        part = __reduce_add_sync(kFull, part);
+        if (lane == 0) sh.red[warp] = part;
+        consumers_sync();
+        if (ct == 0) {
+            uint32_t x = 0, a = 0;
+#pragma unroll
+            for (int w = 0; w < kCTWarps; ++w) {
+                x += sh.red[w];
+                a += sh.wsum[q][w];
+            }
+            const uint32_t c = (tp >= G ? sh.incl : base) + x;  // carry before tile tp
+            sh.carry = c;
+            sh.incl = c + a;
+        }
+        consumers_sync();
+        const uint64_t s = (uint64_t)tp * kCTWarps + warp;
+        if (s < nsub) {
+            uint32_t E = sh.carry;
+#pragma unroll
+            for (int w = 0; w < kCTWarps; ++w) E += w < warp ? sh.wsum[q][w] : 0u;
+            const uint64_t g0 = s * kWTGroups;
+            const uint8_t* sc = dsm + (uint32_t)st * stride + warp * kWTGroups;
+            const uint8_t* pool = dsm + (uint32_t)st * stride + kTileCtrl;
+            const uint32_t head = sh.hdr[st].head[warp];
+            uint32_t* o = out + 4 * g0;
+            uint32_t run;
+            if (sh.hdr[st].mode == 0 && (s + 1) * kWTInts <= n && head <= pool_bytes - 32 &&
+                (((uintptr_t)o) & 15) == 0) {
+                bool zero;
+                const WarpCtrl wf = ctrl_full(sh_addr(sc), &zero);
+                const uint32_t sd = sh_addr(pool) + head;
+                run = zero ? expand_full<1, true>(wf, sd, o, E) : expand_full<1, false>(wf, sd, o, E);
+            } else if (sh.hdr[st].mode == 0) {
+                const uint32_t* W = reinterpret_cast<const uint32_t*>(pool);
+                const uint32_t lim = pool_bytes / 4 - 1;
+                run = decode_generic_store(sc, g0, ngroups, tail_r, head, [&](uint32_t i) { return W[i < lim ? i : lim]; },
+                                           E, out);
+            } else {
+                const uintptr_t gb = (uintptr_t)sh.hdr[st].base;
+                run = decode_generic_store(sc, g0, ngroups, tail_r, head,
+                                           [&](uint32_t i) { return gword_guarded(gb + 4 * (uintptr_t)i, lo, hi); }, E,
+                                           out);
+            }
+            if (s == nsub - 1 && lane == 0 && d_last) *d_last = run;
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&sh.empty[st]);  // tile tp is decoded: its stage is free
+    };
+
+    uint32_t k = 0;
+    uint32_t tprev = 0;
+    for (uint32_t t = blockIdx.x; t < ntiles; t += G, ++k) {
+        const int st = (int)(k % kD1Stages);
+        const uint32_t ph = (k / kD1Stages) & 1u;
+        if (k) prefetch(tprev);
+        mbar_wait_parity(&sh.full[st], ph);
+        const uint64_t s = (uint64_t)t * kCTWarps + warp;
+        uint32_t sum = 0;
+        if (s < nsub) {
+            const uint8_t* sc = dsm + (uint32_t)st * stride + warp * kWTGroups;
+            const uint8_t* pool = dsm + (uint32_t)st * stride + kTileCtrl;
+            const uint32_t head = sh.hdr[st].head[warp];
+            const uint64_t g0 = s * kWTGroups;
+            if (sh.hdr[st].mode == 0) {
+                if ((s + 1) * kWTInts <= n && head <= pool_bytes - 32) {
+                    const uint32_t sd = sh_addr(pool) + head;
+                    if (ctrl_all_zero(sh_addr(sc))) {
+                        sum = __reduce_add_sync(kFull, zero_tile_sum(sd));
+                    } else {
+                        bool zero;
+                        const WarpCtrl wf = ctrl_full(sh_addr(sc), &zero);
+                        sum = __reduce_add_sync(kFull, expand_full<2, false>(wf, sd, nullptr, 0));
+                    }
+                } else {
+                    const uint32_t* W = reinterpret_cast<const uint32_t*>(pool);
+                    const uint32_t lim = pool_bytes / 4 - 1;
+                    sum = sums_generic(sc, g0, ngroups, tail_r, head, [&](uint32_t i) { return W[i < lim ? i : lim]; });
+                }
+            } else {
+                const uintptr_t gb = (uintptr_t)sh.hdr[st].base;
+                sum = sums_generic(sc, g0, ngroups, tail_r, head,
+                                   [&](uint32_t i) { return gword_guarded(gb + 4 * (uintptr_t)i, lo, hi); });
+            }
+        }
+        if (lane == 0) sh.wsum[k % 3][warp] = sum;
+        consumers_sync();
+        if (ct == 0) {
+            uint32_t a = 0;
+#pragma unroll
+            for (int w = 0; w < kCTWarps; ++w) a += sh.wsum[k % 3][w];
+            st_relaxed_u64(meta.agg + t, ((unsigned long long)epoch << 32) | a);
+        }
+        if (k) resolve(tprev, (int)((k - 1) % kD1Stages), (int)((k - 1) % 3));
+        tprev = t;
+    }
+    if (k) {
+        prefetch(tprev);
+        resolve(tprev, (int)((k - 1) % kD1Stages), (int)((k - 1) % 3));
+    }
+}
+
+static cudaError_t launch_decode1(const uint8_t* in, uint64_t in_len, uint64_t n, uint32_t base, uint32_t* out,
+                                  uint32_t* d_last, const DecodeMeta& m, double dpb, uint32_t epoch, cudaStream_t stream,
+                                  bool* used) {
+    *used = false;
+    uint64_t pool = (uint64_t)(1.1 * dpb * kCTWarps) + 64;
+    if (pool < 4096) pool = 4096;
+    if (pool > 8ull * kWTDataMax + 64) pool = 8ull * kWTDataMax + 64;
+    pool = (pool + 15) & ~15ull;
+    const uint32_t smem = (uint32_t)(kD1Stages * (kCTWarps * kWTGroups + pool));
+    static int dev_cached = -1, sms = 0, coop = 0;
+    static uint32_t occ_smem = 0;
+    static int occ = 0;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev != dev_cached) {
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, dev);
+        const cudaError_t a =
+            cudaFuncSetAttribute(svb_decode1_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
+        if (a != cudaSuccess) return a;
+        dev_cached = dev;
+        occ_smem = 0;
+    }
+    if (!coop) return cudaSuccess;
+    if (smem != occ_smem) {
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, svb_decode1_kernel, kSumThreads, smem);
+        occ_smem = smem;
+    }
+    if (occ < 1) return cudaSuccess;  // caller falls back to the sums + delta passes
+    const uint64_t ngroups = (n + 3) >> 2;
+    const uint64_t nsub = (ngroups + kWTGroups - 1) / kWTGroups;
+    const uint64_t ntiles = (nsub + kCTWarps - 1) / kCTWarps;
+    uint64_t grid = (uint64_t)sms * (uint64_t)occ;
+    if (grid > ntiles) grid = ntiles;
+    DecodeMeta mm = m;
+    uint32_t pb = (uint32_t)pool;
+    void* args[] = {(void*)&in, (void*)&in_len, (void*)&n,  (void*)&base, (void*)&out,
+                    (void*)&d_last, (void*)&mm, (void*)&pb, (void*)&epoch};
+    const cudaError_t e = cudaLaunchCooperativeKernel((const void*)svb_decode1_kernel, dim3((unsigned)grid),
+                                                      dim3(kSumThreads), args, smem, stream);
+    if (e == cudaSuccess) *used = true;
+    return e;
+}
+
+// ---------------------------------------------------------------------------
 // launcher
 // ---------------------------------------------------------------------------
 static inline uint64_t align16(uint64_t x) { return (x + 15) & ~(uint64_t)15; }
@@ -819,6 +1157,9 @@ DecodeMeta carve_decode_meta(void* ws, uint64_t n) {
     m.chunktot = reinterpret_cast<uint32_t*>(p);
     p += align16(4 * (nchunks + 1));
     m.tilesize = reinterpret_cast<uint32_t*>(p);
+    const uint64_t ntiles = (nsub + kCTWarps - 1) / kCTWarps;
+    p += align16(4 * (ntiles + 8));
+    m.agg = reinterpret_cast<unsigned long long*>(p);
     return m;
 }
 
@@ -828,7 +1169,7 @@ uint64_t decode_meta_bytes(uint64_t n) {
     const uint64_t nchunks = (nsub + kChunkSubs - 1) / kChunkSubs;
     const uint64_t ntiles = (nsub + kCTWarps - 1) / kCTWarps;
     return 32 + align16(4 * (nsub + 64)) + align16(8 * (nchunks + 4)) + align16(4 * nsub) +
-           2 * align16(4 * (nchunks + 1)) + align16(4 * (ntiles + 8)) + 64;
+           2 * align16(4 * (nchunks + 1)) + align16(4 * (ntiles + 8)) + align16(8 * (ntiles + 8)) + 64;
 }
 
 int occupancy_decode_pipe() { return 1; }  // the tile kernel is not persistent
@@ -883,7 +1224,7 @@ cudaError_t launch_decode_ctrl(const uint8_t* in, uint64_t in_len, uint64_t n, i
 // order on one stream (each continues the previous range's carry).
 cudaError_t launch_decode_range(const uint8_t* in, uint64_t in_len, uint64_t n, int delta, uint32_t base,
                                 uint32_t* out, uint32_t* d_last, void* meta_ws, uint64_t sub_begin, uint64_t sub_end,
-                                cudaStream_t stream, int* launches, unsigned long long* trace) {
+                                cudaStream_t stream, int* launches, unsigned long long* trace, uint32_t epoch) {
     DecodeMeta m = carve_decode_meta(meta_ws, n);
     m.trace = trace;
     const uint64_t ngroups = (n + 3) >> 2;
@@ -910,6 +1251,15 @@ cudaError_t launch_decode_range(const uint8_t* in, uint64_t in_len, uint64_t n, 
         svb_decode_pool_kernel<MODE, KK><<<pgrid, kCTThreads, smem, stream>>>(in, in_len, n, base, out, d_last, m,  \
                                                                              (uint32_t)pool, sub_begin);        \
     } while (0)
+    if (delta && sub_begin == 0 && sub_end == nsub && epoch) {
+        bool used = false;
+        const cudaError_t e1 = launch_decode1(in, in_len, n, base, out, d_last, m, dpb, epoch, stream, &used);
+        if (e1 != cudaSuccess) return e1;
+        if (used) {
+            *launches = 1;
+            return cudaSuccess;
+        }
+    }
     if (delta) {
         const uint32_t t0 = (uint32_t)(sub_begin / kCTWarps), t1 = (uint32_t)((sub_end + kCTWarps - 1) / kCTWarps);
         const cudaError_t e2 = launch_sums(in, in_len, n, m, dpb, t0, t1, stream);
@@ -930,13 +1280,13 @@ cudaError_t launch_decode3(const uint8_t* in, uint64_t in_len, uint64_t n, int d
                            uint32_t* d_last, void* meta_ws, unsigned long long* status, uint32_t epoch, int pipe_grid,
                            cudaStream_t stream, int* launches, unsigned long long* trace, uint32_t debug_flags) {
     (void)pipe_grid;
-    (void)debug_flags;
     cudaError_t e = launch_decode_ctrl(in, in_len, n, delta, meta_ws, status, epoch, stream);
     if (e != cudaSuccess) return e;
     const uint64_t ngroups = (n + 3) >> 2;
     const uint64_t nsub = (ngroups + kWTGroups - 1) / kWTGroups;
     int l = 0;
-    e = launch_decode_range(in, in_len, n, delta, base, out, d_last, meta_ws, 0, nsub, stream, &l, trace);
+    e = launch_decode_range(in, in_len, n, delta, base, out, d_last, meta_ws, 0, nsub, stream, &l, trace,
+                            (debug_flags & 1024) ? 0u : epoch);
     *launches = 1 + l;
     return e;
 }

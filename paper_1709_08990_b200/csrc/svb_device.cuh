@@ -322,6 +322,12 @@ __device__ __forceinline__ uint4 ldg_hint_v4(const void* p, uint64_t pol) {
     return v;
 }
 
+__device__ __forceinline__ void stg_hint_v4(void* p, const uint4& v, uint64_t pol) {
+    asm volatile("st.global.L1::no_allocate.L2::cache_hint.v4.u32 [%0], {%1,%2,%3,%4}, %5;" ::"l"(p), "r"(v.x), "r"(v.y),
+                 "r"(v.z), "r"(v.w), "l"(pol)
+                 : "memory");
+}
+
 __device__ __forceinline__ void stg_stream_v4(void* p, const uint4& v) {
     asm volatile("st.global.cs.v4.u32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w)
                  : "memory");

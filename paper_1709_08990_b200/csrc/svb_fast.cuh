@@ -180,7 +180,10 @@ __device__ __forceinline__ uint32_t expand_full(const WarpCtrl& w, uint32_t sd, 
                 v.w += add;
                 run += __shfl_sync(kFull, I, 31);
             }
-            stg_stream_v4(o + 128 * j + 4 * lane, v);
+            if constexpr (kMode == 1)
+                stg_hint_v4(o + 128 * j + 4 * lane, v, l2_policy_drop());  // keep L2 for the compressed input
+            else
+                stg_stream_v4(o + 128 * j + 4 * lane, v);
         }
     }
     return kMode == 2 ? acc : run;

@@ -34,7 +34,8 @@ cudaError_t launch_decode_ctrl(const uint8_t* in, uint64_t in_len, uint64_t n, i
                                unsigned long long* status, uint32_t epoch, cudaStream_t stream);
 cudaError_t launch_decode_range(const uint8_t* in, uint64_t in_len, uint64_t n, int delta, uint32_t base,
                                 uint32_t* out, uint32_t* d_last, void* meta_ws, uint64_t sub_begin, uint64_t sub_end,
-                                cudaStream_t stream, int* launches, unsigned long long* trace = nullptr);
+                                cudaStream_t stream, int* launches, unsigned long long* trace = nullptr,
+                                uint32_t epoch = 0);  // epoch != 0: a whole-stream delta decode may run one-pass
 unsigned long long* decode_chunkpre_ptr(void* meta_ws, uint64_t n);
 int occupancy_decode_pipe();
 // Single-array encode (svb_encode.cu); meta_ws as for the decode.  With `slots`

@@ -58,6 +58,7 @@ struct DecodeMeta {
     unsigned long long* running;     // encode: data offset where the next slice starts
     unsigned long long* trace;       // debug: timestamps (nullptr = off)
     uint32_t* tilesize;              // [ntiles] encode: packed data bytes of each 8-sub-tile tile
+    unsigned long long* agg;         // [ntiles] one-pass delta decode: (epoch << 32) | tile sum
 };
 
 
