@@ -76,6 +76,7 @@ struct bcgpu_ctx {
     cudaStream_t aux2 = nullptr;             // host pipeline: device -> host copies
     unsigned long long* pin = nullptr;       // host pipeline: pinned offsets / status
     size_t pin_cap = 0;                      // entries
+    uint64_t agg_n = 0;                      // n whose tile aggregates hold no current-epoch tag
 };
 
 static unsigned long long* ticket_ptr(bcgpu_ctx* c) { return c->ws; }
@@ -110,6 +111,7 @@ static int next_epoch(bcgpu_ctx* c, cudaStream_t s) {
     if (c->epoch >= kEpochMax) {
         BC_CUDA(cudaMemsetAsync(c->ws + 1, 0, (15 + 2 * kStatusStride * c->ws_tiles) * sizeof(unsigned long long), s));
         c->epoch = 0;
+        c->agg_n = 0;  // old tags may repeat
     }
     c->epoch += 1;
     c->last_epoch = c->epoch;
@@ -146,7 +148,9 @@ static int make_batch(bcgpu_ctx* c, cudaStream_t s, BatchArgs* ba) {
 
 static int ensure_meta(bcgpu_ctx* c, uint64_t n, cudaStream_t s) {
     const size_t bytes = decode_meta_bytes(n);
+    if (c->agg_n != n) c->agg_n = 0;  // another layout may overwrite the aggregates of agg_n's
     if (bytes <= c->offs_cap) return BCGPU_OK;
+    c->agg_n = 0;
     if (c->offs) {
         BC_CUDA(cudaStreamSynchronize(s));
         BC_CUDA(cudaFree(c->offs));
@@ -335,11 +339,29 @@ int bcgpu_svb_encode_device(bcgpu_ctx* c, const uint32_t* d_in, size_t n, int de
     st = next_epoch(c, s);
     if (st) return st;
     uint8_t* slots = nullptr;
-    st = ensure_slots(c, n, delta, s, &slots);
-    if (st) return st;
+    uint32_t hints = (c->debug_flags & 32) ? ((c->debug_flags >> 6) & 3u) : 3u;
+    // one-pass for delta streams (cfg2: 76 us vs 99 slot / 108 two-read); wide plain data is
+    // compute-bound and runs faster through the 4-CTA/SM two-read kernels (cfg3: 646 vs 819 us).
+    // Debug flags: 16 two-read, 32 slots, 2048 no one-pass, 4096 one-pass for plain too.
+    const bool one_pass = !(c->debug_flags & (16 | 32 | 2048)) && (((uintptr_t)d_in) & 15) == 0 &&
+                          (delta || (c->debug_flags & 4096));
+    if (one_pass) {
+        // the one-pass encode's tile aggregates must not hold this epoch's tag: true when the
+        // workspace was last laid out for this n (older epochs only), else clear them
+        if (c->agg_n != n) {
+            uint64_t cnt = 0;
+            unsigned long long* agg = meta_agg_ptr(c->offs, n, &cnt);
+            BC_CUDA(cudaMemsetAsync(agg, 0, cnt * sizeof(unsigned long long), s));
+        }
+        hints |= 0x100;
+    } else {
+        st = ensure_slots(c, n, delta, s, &slots);
+        if (st) return st;
+    }
+    c->agg_n = n;
     int launches = 0;
     BC_CUDA(launch_encode3(d_in, n, delta, prev, d_out, d_out_len, c->offs, status_ptr(c), c->epoch, s, &launches,
-                           slots, (c->debug_flags & 32) ? ((c->debug_flags >> 6) & 3u) : 3u));
+                           slots, hints));
     g_launches.fetch_add((uint64_t)launches);
     return BCGPU_OK;
 }
@@ -363,6 +385,7 @@ int bcgpu_svb_decode_device(bcgpu_ctx* c, const uint8_t* d_in, size_t in_len, si
     int launches = 0;
     BC_CUDA(launch_decode3(d_in, in_len, n, delta, base, d_out, d_last, c->offs, status_ptr(c), c->epoch,
                            c->pipe_grid, s, &launches, c->trace, c->debug_flags));
+    if (delta) c->agg_n = n;  // its control scan cleared the aggregates of this layout
     g_launches.fetch_add((uint64_t)launches);
     return BCGPU_OK;
 }

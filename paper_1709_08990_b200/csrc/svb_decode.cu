@@ -833,15 +833,6 @@ struct __align__(16) D1Shared {
     uint32_t carry, incl;
 };
 
-__device__ __forceinline__ unsigned long long ld_relaxed_u64(const unsigned long long* p) {
-    unsigned long long v;
-    asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
-    return v;
-}
-__device__ __forceinline__ void st_relaxed_u64(unsigned long long* p, unsigned long long v) {
-    asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
-}
-__device__ __forceinline__ void consumers_sync() { asm volatile("bar.sync 1, 256;" ::: "memory"); }
 __device__ __forceinline__ void sts128(uint32_t a, const uint4& v) {
     asm volatile("st.shared.v4.u32 [%0], {%1,%2,%3,%4};" ::"r"(a), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w) : "memory");
 }
@@ -1289,6 +1280,14 @@ cudaError_t launch_decode3(const uint8_t* in, uint64_t in_len, uint64_t n, int d
                             (debug_flags & 1024) ? 0u : epoch);
     *launches = 1 + l;
     return e;
+}
+
+// device address and size of the one-pass tile aggregates for an n-integer stream
+unsigned long long* meta_agg_ptr(void* meta_ws, uint64_t n, uint64_t* count) {
+    const uint64_t ngroups = (n + 3) >> 2;
+    const uint64_t nsub = (ngroups + kWTGroups - 1) / kWTGroups;
+    *count = (nsub + kCTWarps - 1) / kCTWarps;
+    return carve_decode_meta(meta_ws, n).agg;
 }
 
 // device address of the chunk offsets (nchunks + 1 entries, after launch_decode_ctrl)

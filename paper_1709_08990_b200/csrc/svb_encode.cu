@@ -547,6 +547,289 @@ __global__ void __launch_bounds__(kCTThreads)
 }
 
 // ---------------------------------------------------------------------------
+// 4. one-pass encode with deferred look-back
+// ---------------------------------------------------------------------------
+// Replaces slot encode + compaction (or size scan + tile encode): the integers are
+// read once and the compressed bytes written once, straight to their final place.
+// Persistent CTAs (cooperative launch: all co-resident) take tiles t = b, b + G, ...
+// A producer warp TMA-loads each tile's 8192 integers (+ the 4 before them) into a
+// 3-stage ring.  For tile t (round r) the 8 consumer warps
+//   1. size their sub-tiles (all-small shortcut as above), write the control bytes
+//      to their final place (their position does not depend on any data size),
+//      pack the data bytes in place at phase 0, and publish the tile's data size
+//      A(t) as an epoch-tagged aggregate;
+//   2. resolve the data offset of the CTA's previous tile tp = t - G one round
+//      later -- own inclusive offset from two rounds back + the aggregates of the
+//      G - 1 tiles in between (loads issued early) -- and store its packed bytes
+//      from smem, realigned to the destination's 16-B phase (funnel shifts,
+//      128-bit stores), then release its stage.
+// No CTA waits on a tile of its own round (see svb_decode1_kernel).
+constexpr int kE1Stages = 3;
+constexpr uint32_t kE1Ints = kCTWarps * kWTInts;                          // 8192 per tile
+constexpr uint32_t kE1Stride = 16 + kE1Ints * 4 + 16 + kCTWarps * kWTGroups;  // prefix, tile, slack, ctrl
+
+struct __align__(16) E1Shared {
+    uint64_t full[kE1Stages], empty[kE1Stages];
+    uint32_t wsum[3][kCTWarps];
+    uint32_t red[kCTWarps];
+    unsigned long long carry, incl;
+};
+
+// packed bytes [src, src + len) of shared memory (16-B aligned) -> global dst (any alignment)
+__device__ __forceinline__ void store_realigned(uint32_t src, uint32_t len, uint8_t* dst) {
+    const int lane = threadIdx.x & 31;
+    const uintptr_t D = (uintptr_t)dst;
+    const uint32_t p = (uint32_t)(D & 15);
+    const uintptr_t Dal = D - p, Dend = D + len;
+    const uint32_t nout = (p + len + 15) >> 4;
+    uint4 carry = make_uint4(0, 0, 0, 0);
+    for (uint32_t k0 = 0; k0 < nout; k0 += 32) {
+        const uint32_t k = k0 + lane;
+        const uint4 cur = k < nout ? lds128v(src + 16 * k) : make_uint4(0, 0, 0, 0);
+        uint4 prv = shfl_up4(cur, 1);
+        if (lane == 0) prv = carry;
+        carry = shfl4(cur, 31);
+        if (k < nout) {
+            const uint4 v = window16(prv, cur, 16u - p);  // destination granule k = source bytes [16k - p, +16)
+            const uintptr_t a = Dal + 16 * (uintptr_t)k;
+            if (a >= D && a + 16 <= Dend) {
+                *reinterpret_cast<uint4*>(a) = v;
+            } else {
+                const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+                for (int bi = 0; bi < 16; ++bi)
+                    if (a + bi >= D && a + bi < Dend) *reinterpret_cast<uint8_t*>(a + bi) = (uint8_t)(w[bi >> 2] >> (8 * (bi & 3)));
+            }
+        }
+    }
+}
+
+template <bool kDelta>
+__global__ void __launch_bounds__(kCTThreads + 32, 2)
+    svb_encode1_kernel(const uint32_t* __restrict__ in, uint64_t n, uint32_t prev, uint8_t* __restrict__ out,
+                       DecodeMeta meta, uint64_t* __restrict__ d_out_len, unsigned long long* status, uint32_t epoch) {
+    extern __shared__ __align__(128) uint8_t dsm[];
+    __shared__ E1Shared sh;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint64_t ngroups = (n + 3) >> 2;
+    const uint32_t tail_r = (uint32_t)(n & 3);
+    const uint64_t nsub = (ngroups + kWTGroups - 1) / kWTGroups;
+    const uint32_t ntiles = (uint32_t)((nsub + kCTWarps - 1) / kCTWarps);
+    const uint32_t G = gridDim.x;
+    if (threadIdx.x == 0) {
+#pragma unroll
+        for (int k = 0; k < kE1Stages; ++k) {
+            mbar_init(&sh.full[k], 1);
+            mbar_init(&sh.empty[k], kCTWarps);
+        }
+        sh.incl = 0;
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    if (warp == kCTWarps) {
+        // ---- producer: the tile's integers (and the 4 before them) -> stage ----
+        const uintptr_t lo = (uintptr_t)in, hi = lo + 4 * n;
+        uint32_t k = 0;
+        for (uint32_t t = blockIdx.x; t < ntiles; t += G, ++k) {
+            const int st = (int)(k % kE1Stages);
+            uint8_t* stage = dsm + (uint32_t)st * kE1Stride;
+            if (k >= (uint32_t)kE1Stages) mbar_wait_parity(&sh.empty[st], ((k / kE1Stages) & 1u) ^ 1u);
+            const uint64_t i0 = (uint64_t)t * kE1Ints;
+            const uint64_t cnt = n - i0 < (uint64_t)kE1Ints ? n - i0 : (uint64_t)kE1Ints;
+            const uintptr_t beg = (uintptr_t)(in + i0) - (t ? 16 : 0), end = (uintptr_t)(in + i0 + cnt);
+            uint8_t* dst = stage + (t ? 0 : 16);
+            const uint32_t tx = tma_cover_bytes(beg, end, lo, hi);
+            if (tx != 0xFFFFFFFFu && tx) {
+                if (lane == 0) {
+                    fence_async_smem();
+                    mbar_expect(&sh.full[st], tx);
+                    tma_load_hint(dst, reinterpret_cast<const void*>(beg), tx, &sh.full[st], l2_policy_drop());
+                }
+            } else {
+                uint32_t* d32 = reinterpret_cast<uint32_t*>(dst);
+                const uint32_t words = (uint32_t)((end - beg) >> 2);
+                for (uint32_t i = lane; i < words; i += 32) d32[i] = __ldg(reinterpret_cast<const uint32_t*>(beg) + i);
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&sh.full[st]);
+            }
+        }
+        return;
+    }
+    // ---- consumers ----
+    const int ct = threadIdx.x;
+    auto window_lo = [&](uint32_t tp) -> uint32_t { return tp + 1 > G ? tp + 1 - G : 0u; };
+    unsigned long long pf0 = 0, pf1 = 0;
+    auto prefetch = [&](uint32_t tp) {
+        const uint32_t wl = window_lo(tp);
+        pf0 = wl + ct < tp ? ld_relaxed_u64(meta.agg + wl + ct) : 0ull;
+        pf1 = wl + ct + 256 < tp ? ld_relaxed_u64(meta.agg + wl + ct + 256) : 0ull;
+    };
+    auto entry = [&](uint32_t j, unsigned long long v) -> uint32_t {
+        while ((uint32_t)(v >> 32) != epoch) v = ld_relaxed_u64(meta.agg + j);
+        return (uint32_t)v;
+    };
+    auto resolve = [&](uint32_t tp, int st, int q) {
+        const uint32_t wl = window_lo(tp);
+        uint32_t part = 0;
+        if (wl + ct < tp) part += entry(wl + ct, pf0);
+        if (wl + ct + 256 < tp) part += entry(wl + ct + 256, pf1);
+        for (uint32_t j = wl + ct + 512; j < tp; j += 256) part += entry(j, ld_relaxed_u64(meta.agg + j));
+        part = __reduce_add_sync(kFull, part);
+        if (lane == 0) sh.red[warp] = part;
+        consumers_sync();
+        if (ct == 0) {
+            unsigned long long x = 0;
+            uint32_t a = 0;
+#pragma unroll
+            for (int w = 0; w < kCTWarps; ++w) {
+                x += sh.red[w];
+                a += sh.wsum[q][w];
+            }
+            const unsigned long long c = (tp >= G ? sh.incl : 0ull) + x;  // data offset of tile tp
+            sh.carry = c;
+            sh.incl = c + a;
+            if (tp == ntiles - 1) {
+                if (d_out_len) *d_out_len = ngroups + c + a;
+                if (status) *status = ((unsigned long long)epoch << 32);
+            }
+        }
+        consumers_sync();
+        const uint64_t s = (uint64_t)tp * kCTWarps + warp;
+        if (s < nsub) {
+            uint32_t pre = 0;
+#pragma unroll
+            for (int w = 0; w < kCTWarps; ++w) pre += w < warp ? sh.wsum[q][w] : 0u;
+            const uint32_t src = sh_addr(dsm) + (uint32_t)st * kE1Stride + 16 + (uint32_t)warp * (kWTInts * 4);
+            store_realigned(src, sh.wsum[q][warp], out + ngroups + sh.carry + pre);
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&sh.empty[st]);
+    };
+
+    uint32_t k = 0, tprev = 0;
+    for (uint32_t t = blockIdx.x; t < ntiles; t += G, ++k) {
+        const int st = (int)(k % kE1Stages);
+        if (k) prefetch(tprev);
+        mbar_wait_parity(&sh.full[st], (k / kE1Stages) & 1u);
+        uint8_t* stage = dsm + (uint32_t)st * kE1Stride;
+        const uint64_t s = (uint64_t)t * kCTWarps + warp;
+        const uint64_t g0 = s * kWTGroups;
+        uint32_t total = 0;
+        if (g0 < ngroups) {
+            const uint32_t sin = sh_addr(stage) + 16 + (uint32_t)warp * (kWTInts * 4);
+            uint8_t* sctrl = stage + 16 + kE1Ints * 4 + 16 + warp * kWTGroups;
+            const uint32_t prev_w = warp ? lds32(sin - 4) : (t ? lds32(sh_addr(stage) + 12) : prev);
+            const uint32_t cnt_g = (uint32_t)(ngroups - g0 < (uint64_t)kWTGroups ? ngroups - g0 : (uint64_t)kWTGroups);
+            uint8_t* cdst = out + g0;
+            if ((s + 1) * kWTInts <= n) {
+                const bool small = enc_full_small<kDelta>(sin, prev_w);
+                if (small) {
+                    total = kWTInts;
+                    __syncwarp();
+                    enc_small_pack<kDelta>(sin, prev_w, sin);
+                    for (uint32_t i = lane; i < kWTGroups / 4; i += 32) {  // 256 zero control bytes
+                        uint8_t* c4 = cdst + 4 * i;
+                        if ((((uintptr_t)c4) & 3) == 0)
+                            *reinterpret_cast<uint32_t*>(c4) = 0u;
+                        else
+                            c4[0] = c4[1] = c4[2] = c4[3] = 0;
+                    }
+                } else {
+                    uint32_t lens[kWTRows], qw[4];
+                    total = enc_full_lengths<kDelta>(sin, prev_w, sh_addr(sctrl), lens, qw);
+                    __syncwarp();
+                    enc_full_pack<kDelta>(sin, prev_w, lens, qw, sin);
+                    for (uint32_t i = lane; i < cnt_g; i += 32) cdst[i] = sctrl[i];
+                }
+            } else {
+                // the stream's last, partial sub-tile
+                EncodeTile tt;
+                uint32_t P[3] = {0, 0, 0};
+                uint32_t last_w = prev_w;
+                const uint8_t* sbytes = stage + 16 + warp * (kWTInts * 4);
+#pragma unroll
+                for (int j = 0; j < kWTRows; ++j) {
+                    const uint32_t cnt = group_count(g0 + 32 * j + lane, ngroups, tail_r);
+                    uint4 x = mask_tail(*reinterpret_cast<const uint4*>(sbytes + 512 * j + 16 * lane), cnt);
+                    if constexpr (kDelta) {
+                        uint32_t p = __shfl_up_sync(kFull, x.w, 1);
+                        if (lane == 0) p = last_w;
+                        last_w = __shfl_sync(kFull, x.w, 31);
+                        x = make_uint4(x.x - p, x.y - x.x, x.z - x.y, x.w - x.z);
+                    }
+                    tt.d[j] = x;
+                    const uint32_t l0 = cnt > 0 ? dev_byte_length(x.x) : 0u;
+                    const uint32_t l1 = cnt > 1 ? dev_byte_length(x.y) : 0u;
+                    const uint32_t l2 = cnt > 2 ? dev_byte_length(x.z) : 0u;
+                    const uint32_t l3 = cnt > 3 ? dev_byte_length(x.w) : 0u;
+                    tt.lens[j] = l0 | (l1 << 8) | (l2 << 16) | (l3 << 24);
+                    P[j / 3] |= (l0 + l1 + l2 + l3) << (10 * (j % 3));
+                    if (cnt)
+                        cdst[32 * j + lane] = (uint8_t)((l0 - 1) | (l1 ? ((l1 - 1) << 2) : 0u) |
+                                                        (l2 ? ((l2 - 1) << 4) : 0u) | (l3 ? ((l3 - 1) << 6) : 0u));
+                }
+                tt.total = packed_row_scan(P, tt.qw);
+                total = tt.total;
+                __syncwarp();
+                encode_pack_at(tt, stage + 16 + warp * (kWTInts * 4), 0);
+            }
+        }
+        __syncwarp();
+        if (lane == 0) sh.wsum[k % 3][warp] = total;
+        consumers_sync();
+        if (ct == 0) {
+            uint32_t a = 0;
+#pragma unroll
+            for (int w = 0; w < kCTWarps; ++w) a += sh.wsum[k % 3][w];
+            st_relaxed_u64(meta.agg + t, ((unsigned long long)epoch << 32) | a);
+        }
+        if (k) resolve(tprev, (int)((k - 1) % kE1Stages), (int)((k - 1) % 3));
+        tprev = t;
+    }
+    if (k) {
+        prefetch(tprev);
+        resolve(tprev, (int)((k - 1) % kE1Stages), (int)((k - 1) % 3));
+    }
+}
+
+// one-pass encode if the device can run it (cooperative launch, 16-B aligned input);
+// *used = false leaves the call to the other paths
+static cudaError_t launch_encode1(const uint32_t* in, uint64_t n, int delta, uint32_t prev, uint8_t* out,
+                                  uint64_t* d_out_len, const DecodeMeta& m, unsigned long long* status, uint32_t epoch,
+                                  cudaStream_t stream, bool* used) {
+    *used = false;
+    if (((uintptr_t)in) & 15) return cudaSuccess;
+    const uint32_t smem = (uint32_t)(kE1Stages * kE1Stride);
+    static int dev_cached = -1, sms = 0, coop = 0, occ = 0;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev != dev_cached) {
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, dev);
+        cudaFuncSetAttribute(svb_encode1_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        cudaFuncSetAttribute(svb_encode1_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        int o1 = 0, o2 = 0;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o1, svb_encode1_kernel<true>, kCTThreads + 32, smem);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o2, svb_encode1_kernel<false>, kCTThreads + 32, smem);
+        occ = o1 < o2 ? o1 : o2;
+        dev_cached = dev;
+    }
+    if (!coop || occ < 1) return cudaSuccess;
+    const uint64_t ngroups = (n + 3) >> 2;
+    const uint64_t nsub = (ngroups + kWTGroups - 1) / kWTGroups;
+    const uint64_t ntiles = (nsub + kCTWarps - 1) / kCTWarps;
+    uint64_t grid = (uint64_t)sms * (uint64_t)occ;
+    if (grid > ntiles) grid = ntiles;
+    DecodeMeta mm = m;
+    void* args[] = {(void*)&in, (void*)&n, (void*)&prev, (void*)&out, (void*)&mm, (void*)&d_out_len, (void*)&status,
+                    (void*)&epoch};
+    const void* fn = delta ? (const void*)svb_encode1_kernel<true> : (const void*)svb_encode1_kernel<false>;
+    const cudaError_t e = cudaLaunchCooperativeKernel(fn, dim3((unsigned)grid), dim3(kCTThreads + 32), args, smem, stream);
+    if (e == cudaSuccess) *used = true;
+    return e;
+}
+
+// ---------------------------------------------------------------------------
 // launcher (metadata layout shared with the decode: localpre / chunkpre / counters)
 // ---------------------------------------------------------------------------
 uint64_t encode_slot_bytes(uint64_t n) {
@@ -562,6 +845,15 @@ cudaError_t launch_encode3(const uint32_t* in, uint64_t n, int delta, uint32_t p
     const uint64_t ngroups = (n + 3) >> 2;
     const uint64_t nsub = (ngroups + kWTGroups - 1) / kWTGroups;
     const uint32_t nchunks = (uint32_t)((nsub + kChunkSubs - 1) / kChunkSubs);
+    if (hints & 0x100) {  // one-pass (the ctrl scan of a decode is not run here: clear the aggregates)
+        bool used = false;
+        const cudaError_t e = launch_encode1(in, n, delta, prev, out, d_out_len, m, status, epoch, stream, &used);
+        if (e != cudaSuccess) return e;
+        if (used) {
+            *launches = 1;
+            return cudaSuccess;
+        }
+    }
     if (slots) {
         const uint64_t tiles_all = (nsub + kCTWarps - 1) / kCTWarps;
         if (delta)

@@ -37,6 +37,7 @@ cudaError_t launch_decode_range(const uint8_t* in, uint64_t in_len, uint64_t n, 
                                 cudaStream_t stream, int* launches, unsigned long long* trace = nullptr,
                                 uint32_t epoch = 0);  // epoch != 0: a whole-stream delta decode may run one-pass
 unsigned long long* decode_chunkpre_ptr(void* meta_ws, uint64_t n);
+unsigned long long* meta_agg_ptr(void* meta_ws, uint64_t n, uint64_t* count);
 int occupancy_decode_pipe();
 // Single-array encode (svb_encode.cu); meta_ws as for the decode.  With `slots`
 // (encode_slot_bytes(n) of device scratch, 128-B aligned): slot encode + compaction,
@@ -44,6 +45,8 @@ int occupancy_decode_pipe();
 cudaError_t launch_encode3(const uint32_t* in, uint64_t n, int delta, uint32_t prev, uint8_t* out,
                            uint64_t* d_out_len, void* meta_ws, unsigned long long* status, uint32_t epoch,
                            cudaStream_t stream, int* launches, uint8_t* slots = nullptr, uint32_t hints = 3);
+// hints: bit 0/1 L2 policies of the slot encode; 0x100 try the one-pass encode first (needs the
+// workspace's tile aggregates free of this epoch's tag: see bcgpu_capi.cu)
 // Chunks [c0, c1) (64 Ki integers each) of the two-read encode, continuing from the
 // previous piece's running offset; 2 launches.  For the pipelined host API.
 cudaError_t launch_encode_piece(const uint32_t* in, uint64_t n, int delta, uint32_t prev, uint8_t* out,

@@ -48,6 +48,18 @@ __device__ __forceinline__ T cta_exclusive_scan(T* a, uint32_t m, T* warp_tmp) {
     return total;
 }
 
+// one-pass kernels (deferred look-back): epoch-tagged tile aggregates, relaxed at gpu scope
+__device__ __forceinline__ unsigned long long ld_relaxed_u64(const unsigned long long* p) {
+    unsigned long long v;
+    asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_relaxed_u64(unsigned long long* p, unsigned long long v) {
+    asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+// named barrier of the 8 consumer warps of a producer/consumer CTA (the producer warp skips it)
+__device__ __forceinline__ void consumers_sync() { asm volatile("bar.sync 1, 256;" ::: "memory"); }
+
 struct DecodeMeta {
     uint32_t* localpre;              // [nsub]  sub-tile data offset within its chunk
     unsigned long long* chunkpre;    // [nchunks + 1] chunk data offset (exclusive; [nchunks] = total)

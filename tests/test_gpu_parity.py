@@ -163,10 +163,11 @@ def test_device_misaligned_pointers(P, dev):
                 assert (int(last.item()) & 0xFFFFFFFF) == int(v[-1])
 
 
-@pytest.mark.parametrize("flags", [16, 32])
+@pytest.mark.parametrize("flags", [16, 32, 4096])
 def test_encode_both_paths(dev, flags):
-    """Both single-array encode paths, whichever the dispatch picks for the stream kind:
-    16 = size scan + tile encode (two reads), 32 = slot encode + compaction (one read)."""
+    """Every single-array encode path, whichever the dispatch picks for the stream kind:
+    16 = size scan + tile encode (two reads), 32 = slot encode + compaction (one read),
+    4096 = one-pass encode with deferred look-back (for plain streams too)."""
     import ctypes as C
     import torch
     from paper_1709_08990_b200._native import lib
@@ -174,7 +175,7 @@ def test_encode_both_paths(dev, flags):
     rng = np.random.default_rng(5 + flags)
     lib.bcgpu_debug_set_flags(dev._ctx, flags)
     try:
-        for n in (1, 5, 1023, 1024, 8193, 65536 + 7, 600_001):
+        for n in (1, 5, 1023, 1024, 8193, 65536 + 7, 600_001, 5_000_003):
             for delta, v in ((False, _mixed(rng, n)), (True, np.sort(_mixed(rng, n, (0, 1, 2))))):
                 prev = int(rng.integers(0, 2**32)) if delta else 0
                 want = oracle.encode(v, delta=delta, prev=prev)
