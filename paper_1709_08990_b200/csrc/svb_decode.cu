@@ -829,6 +829,7 @@ struct __align__(16) D1Shared {
     SumHdr hdr[kD1Stages];
     uint64_t full[kD1Stages], empty[kD1Stages], mfull[kD1Stages];
     uint32_t wsum[3][kCTWarps];  // sub-tile sums, by round % 3
+    uint32_t wcarry[kCTWarps];   // carry before each sub-tile of the tile being resolved
     uint32_t red[kCTWarps];
     uint32_t carry, incl;
 };
@@ -990,13 +991,17 @@ __global__ void __launch_bounds__(kSumThreads, 3)
             const uint32_t c = (tp >= G ? sh.incl : base) + x;  // carry before tile tp
             sh.carry = c;
             sh.incl = c + a;
+            uint32_t e = c;
+#pragma unroll
+            for (int w = 0; w < kCTWarps; ++w) {
+                sh.wcarry[w] = e;
+                e += sh.wsum[q][w];
+            }
         }
         consumers_sync();
         const uint64_t s = (uint64_t)tp * kCTWarps + warp;
         if (s < nsub) {
-            uint32_t E = sh.carry;
-#pragma unroll
-            for (int w = 0; w < kCTWarps; ++w) E += w < warp ? sh.wsum[q][w] : 0u;
+            const uint32_t E = sh.wcarry[warp];
             const uint64_t g0 = s * kWTGroups;
             const uint8_t* sc = dsm + (uint32_t)st * stride + warp * kWTGroups;
             const uint8_t* pool = dsm + (uint32_t)st * stride + kTileCtrl;

@@ -571,26 +571,28 @@ constexpr uint32_t kE1Stride = 16 + kE1Ints * 4 + 16 + kCTWarps * kWTGroups;  //
 struct __align__(16) E1Shared {
     uint64_t full[kE1Stages], empty[kE1Stages];
     uint32_t wsum[3][kCTWarps];
+    uint32_t wpre[kCTWarps];  // exclusive prefix of the resolved tile's sub-tile sizes
     uint32_t red[kCTWarps];
     unsigned long long carry, incl;
 };
 
-// packed bytes [src, src + len) of shared memory (16-B aligned) -> global dst (any alignment)
+// packed bytes [src, src + len) of shared memory (16-B aligned, with >= 16 readable bytes
+// before and after) -> global dst (any alignment): destination granule k is the 16 source
+// bytes at src + 16k - p, read as 5 words and funnel-shifted (p = dst's 16-B phase)
 __device__ __forceinline__ void store_realigned(uint32_t src, uint32_t len, uint8_t* dst) {
     const int lane = threadIdx.x & 31;
     const uintptr_t D = (uintptr_t)dst;
     const uint32_t p = (uint32_t)(D & 15);
     const uintptr_t Dal = D - p, Dend = D + len;
     const uint32_t nout = (p + len + 15) >> 4;
-    uint4 carry = make_uint4(0, 0, 0, 0);
-    for (uint32_t k0 = 0; k0 < nout; k0 += 32) {
-        const uint32_t k = k0 + lane;
-        const uint4 cur = k < nout ? lds128v(src + 16 * k) : make_uint4(0, 0, 0, 0);
-        uint4 prv = shfl_up4(cur, 1);
-        if (lane == 0) prv = carry;
-        carry = shfl4(cur, 31);
-        if (k < nout) {
-            const uint4 v = window16(prv, cur, 16u - p);  // destination granule k = source bytes [16k - p, +16)
+    const uint32_t r = ((0u - p) & 3u) * 8u;
+    for (uint32_t k = lane; k < nout; k += 32) {
+        const uint32_t wa = (src + 16 * k - p) & ~3u;
+        const uint32_t w0 = lds32v(wa), w1 = lds32v(wa + 4), w2 = lds32v(wa + 8), w3 = lds32v(wa + 12),
+                       w4 = lds32v(wa + 16);
+        {
+            const uint4 v = make_uint4(__funnelshift_r(w0, w1, r), __funnelshift_r(w1, w2, r),
+                                       __funnelshift_r(w2, w3, r), __funnelshift_r(w3, w4, r));
             const uintptr_t a = Dal + 16 * (uintptr_t)k;
             if (a >= D && a + 16 <= Dend) {
                 *reinterpret_cast<uint4*>(a) = v;
@@ -688,6 +690,12 @@ __global__ void __launch_bounds__(kCTThreads + 32, 2)
             const unsigned long long c = (tp >= G ? sh.incl : 0ull) + x;  // data offset of tile tp
             sh.carry = c;
             sh.incl = c + a;
+            uint32_t pr = 0;
+#pragma unroll
+            for (int w = 0; w < kCTWarps; ++w) {
+                sh.wpre[w] = pr;
+                pr += sh.wsum[q][w];
+            }
             if (tp == ntiles - 1) {
                 if (d_out_len) *d_out_len = ngroups + c + a;
                 if (status) *status = ((unsigned long long)epoch << 32);
@@ -696,11 +704,8 @@ __global__ void __launch_bounds__(kCTThreads + 32, 2)
         consumers_sync();
         const uint64_t s = (uint64_t)tp * kCTWarps + warp;
         if (s < nsub) {
-            uint32_t pre = 0;
-#pragma unroll
-            for (int w = 0; w < kCTWarps; ++w) pre += w < warp ? sh.wsum[q][w] : 0u;
             const uint32_t src = sh_addr(dsm) + (uint32_t)st * kE1Stride + 16 + (uint32_t)warp * (kWTInts * 4);
-            store_realigned(src, sh.wsum[q][warp], out + ngroups + sh.carry + pre);
+            store_realigned(src, sh.wsum[q][warp], out + ngroups + sh.carry + sh.wpre[warp]);
         }
         __syncwarp();
         if (lane == 0) mbar_arrive(&sh.empty[st]);
@@ -722,11 +727,9 @@ __global__ void __launch_bounds__(kCTThreads + 32, 2)
             const uint32_t cnt_g = (uint32_t)(ngroups - g0 < (uint64_t)kWTGroups ? ngroups - g0 : (uint64_t)kWTGroups);
             uint8_t* cdst = out + g0;
             if ((s + 1) * kWTInts <= n) {
-                const bool small = enc_full_small<kDelta>(sin, prev_w);
+                const bool small = enc_full_small_pack0<kDelta>(sin, prev_w);
                 if (small) {
                     total = kWTInts;
-                    __syncwarp();
-                    enc_small_pack<kDelta>(sin, prev_w, sin);
                     for (uint32_t i = lane; i < kWTGroups / 4; i += 32) {  // 256 zero control bytes
                         uint8_t* c4 = cdst + 4 * i;
                         if ((((uintptr_t)c4) & 3) == 0)

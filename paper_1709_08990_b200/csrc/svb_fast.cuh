@@ -147,6 +147,31 @@ template <int kMode, bool kZero>
 __device__ __forceinline__ uint32_t expand_full(const WarpCtrl& w, uint32_t sd, uint32_t* __restrict__ o, uint32_t run) {
     const int lane = threadIdx.x & 31;
     uint32_t acc = 0;
+    if constexpr (kMode == 1 && kZero) {
+        // every integer is one byte: a row's group sums (<= 1020) and totals (<= 32640) fit
+        // 16 bits, so two rows share one warp scan
+        const uint64_t pol = l2_policy_drop();
+#pragma unroll
+        for (int j = 0; j < kWTRows; j += 2) {
+            uint4 v0 = zero_group_s(sd + 128 * j + 4 * lane), v1 = zero_group_s(sd + 128 * (j + 1) + 4 * lane);
+            v0.y += v0.x;
+            v0.z += v0.y;
+            v0.w += v0.z;
+            v1.y += v1.x;
+            v1.z += v1.y;
+            v1.w += v1.z;
+            const uint32_t Pk = v0.w | (v1.w << 16);
+            const uint32_t I = warp_inclusive_scan(Pk);
+            const uint32_t T = __shfl_sync(kFull, I, 31);
+            const uint32_t a0 = run + (I & 0xFFFFu) - v0.w;
+            const uint32_t a1 = run + (T & 0xFFFFu) + (I >> 16) - v1.w;
+            stg_hint_v4(o + 128 * j + 4 * lane, add4(v0, a0), pol);
+            stg_hint_v4(o + 128 * (j + 1) + 4 * lane, add4(v1, a1), pol);
+            run += (T & 0xFFFFu) + (T >> 16);
+        }
+        return run;
+    }
+    const uint64_t pol1 = l2_policy_drop();
 #pragma unroll
     for (int j = 0; j < kWTRows; ++j) {
         uint32_t c = 0, a;
@@ -181,7 +206,7 @@ __device__ __forceinline__ uint32_t expand_full(const WarpCtrl& w, uint32_t sd, 
                 run += __shfl_sync(kFull, I, 31);
             }
             if constexpr (kMode == 1)
-                stg_hint_v4(o + 128 * j + 4 * lane, v, l2_policy_drop());  // keep L2 for the compressed input
+                stg_hint_v4(o + 128 * j + 4 * lane, v, pol1);  // evict-first: keep L2 for the compressed input
             else
                 stg_stream_v4(o + 128 * j + 4 * lane, v);
         }
@@ -294,6 +319,28 @@ __device__ __forceinline__ bool enc_full_small(uint32_t sin, uint32_t prev_w) {
         o |= x.x | x.y | x.z | x.w;
     }
     return __all_sync(kFull, o < 256u);
+}
+
+// Fused check + pack at phase 0 (the one-pass encode, whose destination phase is not
+// known yet): every row is read once; if every integer (delta) is < 256 the low bytes
+// are written as 32 aligned words per row over the consumed input (sdst = sin) and the
+// function returns true; otherwise nothing is written.
+template <bool kDelta>
+__device__ __forceinline__ bool enc_full_small_pack0(uint32_t sin, uint32_t prev_w) {
+    const int lane = threadIdx.x & 31;
+    uint32_t last = prev_w, o = 0;
+    uint32_t P[kWTRows];
+#pragma unroll
+    for (int j = 0; j < kWTRows; ++j) {
+        const uint4 x = enc_row<kDelta>(sin, j, last);
+        o |= x.x | x.y | x.z | x.w;
+        P[j] = __byte_perm(__byte_perm(x.x, x.y, 0x0040), __byte_perm(x.z, x.w, 0x0040), 0x5410);
+    }
+    if (!__all_sync(kFull, o < 256u)) return false;
+    __syncwarp();  // every lane has read every row
+#pragma unroll
+    for (int j = 0; j < kWTRows; ++j) sts32(sin + 128 * j + 4 * lane, P[j]);
+    return true;
 }
 
 // Pack pass of a small sub-tile (enc_full_small): row j lane l's four bytes go to
