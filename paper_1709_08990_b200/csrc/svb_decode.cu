@@ -947,6 +947,7 @@ __global__ void __launch_bounds__(kSumThreads, 3)
                 fence_async_smem();
                 mbar_expect(&sh.full[st], (c_tma ? ctx : 0u) + (fits ? tx : 0u));
                 const uint64_t pol = l2_policy_drop();
+                if (meta.trace) meta.trace[8ull * t + 0] = gtimer();
                 if (c_tma && ctx) tma_load_hint(sc, reinterpret_cast<const void*>(cb), ctx, &sh.full[st], pol);
                 if (fits && tx) tma_load_hint(pool, reinterpret_cast<const void*>(bse), tx, &sh.full[st], pol);
                 const uint64_t tn = (uint64_t)t + (uint64_t)kD1Stages * G;
@@ -981,6 +982,7 @@ __global__ void __launch_bounds__(kSumThreads, 3)
         part = __reduce_add_sync(kFull, part);
         if (lane == 0) sh.red[warp] = part;
         consumers_sync();
+        if (meta.trace && ct == 0) meta.trace[8ull * tp + 4] = gtimer();
         if (ct == 0) {
             uint32_t x = 0, a = 0;
 #pragma unroll
@@ -1028,6 +1030,7 @@ __global__ void __launch_bounds__(kSumThreads, 3)
             if (s == nsub - 1 && lane == 0 && d_last) *d_last = run;
         }
         __syncwarp();
+        if (meta.trace && ct == 0) meta.trace[8ull * tp + 5] = gtimer();
         if (lane == 0) mbar_arrive(&sh.empty[st]);  // tile tp is decoded: its stage is free
     };
 
@@ -1037,7 +1040,9 @@ __global__ void __launch_bounds__(kSumThreads, 3)
         const int st = (int)(k % kD1Stages);
         const uint32_t ph = (k / kD1Stages) & 1u;
         if (k) prefetch(tprev);
+        if (meta.trace && ct == 0) meta.trace[8ull * t + 1] = gtimer();
         mbar_wait_parity(&sh.full[st], ph);
+        if (meta.trace && ct == 0) meta.trace[8ull * t + 2] = gtimer();
         const uint64_t s = (uint64_t)t * kCTWarps + warp;
         uint32_t sum = 0;
         if (s < nsub) {
@@ -1073,6 +1078,7 @@ __global__ void __launch_bounds__(kSumThreads, 3)
 #pragma unroll
             for (int w = 0; w < kCTWarps; ++w) a += sh.wsum[k % 3][w];
             st_relaxed_u64(meta.agg + t, ((unsigned long long)epoch << 32) | a);
+            if (meta.trace) meta.trace[8ull * t + 3] = gtimer();
         }
         if (k) resolve(tprev, (int)((k - 1) % kD1Stages), (int)((k - 1) % 3));
         tprev = t;
