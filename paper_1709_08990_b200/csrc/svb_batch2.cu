@@ -239,13 +239,10 @@ __global__ void __launch_bounds__(kBThreads)
                         expand_full<0, false>(wA, sd, ot, 0);
                 }
             } else {
-                uint4 vv[kWTRows];
-                const uint32_t tsum =
-                    expand_tile<kDelta>(wA, B.data[ds], head, g0, ngroups, A.n & 3u, o, out16, vv);
-                if constexpr (kDelta) {
-                    store_tile<kDelta>(vv, carry, g0, ngroups, A.n & 3u, o, out16);
-                    after = carry + tsum;
-                }
+                // partial tile and/or unaligned output: lean masked expansion, realigned stores
+                const uint32_t ng = (uint32_t)(ngroups - g0 < (uint64_t)kWTGroups ? ngroups - g0 : (uint64_t)kWTGroups);
+                const uint32_t tail = (g0 + ng == ngroups && (A.n & 3u)) ? (A.n & 3u) : 4u;
+                after = expand_any<kDelta>(wA, sh_addr(B.data[ds]) + head, ng, tail, o + 4 * g0, carry);
             }
             // end of the segment: the stream must end exactly here
             if ((uint64_t)(A.k + 1) * kWTInts >= A.n && lane == 0) {
@@ -568,7 +565,9 @@ cudaError_t launch_decode_batch2(const bcgpu_decode_segment* segs, uint64_t nseg
         occ = o1 < o2 ? o1 : o2;
         if (occ < 1) occ = 1;
     }
-    const uint64_t want = (nseg + kBWarps - 1) / kBWarps, cap = (uint64_t)sms * occ;
+    const uint32_t occ_cap = (ba.flags >> 12) & 7u;  // debug: CTAs per SM
+    const uint64_t want = (nseg + kBWarps - 1) / kBWarps,
+                   cap = (uint64_t)sms * (occ_cap && (int)occ_cap < occ ? (int)occ_cap : occ);
     const int grid = (int)(want < cap ? want : cap);
     if (grid <= 0) return cudaSuccess;
     if (delta)

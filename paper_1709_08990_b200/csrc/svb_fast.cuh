@@ -214,6 +214,70 @@ __device__ __forceinline__ uint32_t expand_full(const WarpCtrl& w, uint32_t sd, 
     return kMode == 2 ? acc : run;
 }
 
+
+// ---- any tile (batches): partial tiles, any output alignment ------------------
+// ng groups (1..256) with `tail` integers (1..4) in the last one, control in w (the tail's
+// unused fields already masked), data at shared address sd, output o at any 4-B alignment.
+// Group g of row j goes to elements 4(32j + lane) ..; a lane stores the 16-B aligned
+// granule holding elements [4g - r, 4g - r + 4) (r = o's 4-B phase inside 16 B): the
+// previous lane's last r integers (shuffled up; lane 0 keeps the previous row's lane 31)
+// and its own first 4 - r.  Whole granules leave as 128-bit stores, the tile's first and
+// last partial granules as scalars.  Returns the running value (delta) after the tile.
+template <bool kDelta>
+__device__ __forceinline__ uint32_t expand_any(const WarpCtrl& w, uint32_t sd, uint32_t ng, uint32_t tail,
+                                               uint32_t* __restrict__ o, uint32_t run) {
+    const int lane = threadIdx.x & 31;
+    const int nints = (int)(4 * (ng - 1) + tail);
+    const uint32_t r = (uint32_t)(((uintptr_t)o >> 2) & 3u);
+    uint32_t* A = o - r;
+    uint4 carry = make_uint4(0, 0, 0, 0);
+    const uint32_t rows = (ng + 31) >> 5;
+#pragma unroll 1
+    for (uint32_t j = 0; j < rows; ++j) {
+        const uint32_t gl = 32 * j + lane;
+        const uint32_t cnt = gl + 1 < ng ? 4u : (gl + 1 == ng ? tail : 0u);
+        const uint32_t c = row_ctrl(w, (int)j);
+        const uint32_t a = sd + row_q(w, (int)j);
+        uint4 v = __all_sync(kFull, c == 0) ? zero_group_s(a) : group_s(a, c);
+        v = mask_tail(v, cnt);
+        if constexpr (kDelta) {
+            v.y += v.x;
+            v.z += v.y;
+            v.w += v.z;
+            const uint32_t I = warp_inclusive_scan(v.w);
+            v = add4(v, run + I - v.w);
+            run += __shfl_sync(kFull, I, 31);
+        }
+        if (r == 0) {
+            if (cnt == 4)
+                stg_stream_v4(o + 4 * gl, v);
+            else if (cnt)
+                store_group(o + 4 * gl, v, cnt, false);
+        } else {
+            uint4 prv = make_uint4(__shfl_up_sync(kFull, v.x, 1), __shfl_up_sync(kFull, v.y, 1),
+                                   __shfl_up_sync(kFull, v.z, 1), __shfl_up_sync(kFull, v.w, 1));
+            if (lane == 0) prv = carry;
+            carry = make_uint4(__shfl_sync(kFull, v.x, 31), __shfl_sync(kFull, v.y, 31), __shfl_sync(kFull, v.z, 31),
+                               __shfl_sync(kFull, v.w, 31));
+            const uint4 g = r == 1 ? make_uint4(prv.w, v.x, v.y, v.z)
+                          : r == 2 ? make_uint4(prv.z, prv.w, v.x, v.y)
+                                   : make_uint4(prv.y, prv.z, prv.w, v.x);
+            const int e0 = 4 * (int)gl - (int)r;
+            if (e0 >= 0 && e0 + 4 <= nints) {
+                stg_stream_v4(A + 4 * gl, g);
+            } else {
+#pragma unroll
+                for (int i = 0; i < 4; ++i)
+                    if (e0 + i >= 0 && e0 + i < nints) A[4 * gl + i] = comp(g, i);
+            }
+        }
+    }
+    if (r && lane < (int)r) {  // the last row's final r integers (lane 31's, in `carry`)
+        const int e = 128 * (int)rows - (int)r + lane;
+        if (e >= 0 && e < nints) o[e] = comp(carry, 4 - (int)r + lane);
+    }
+    return run;
+}
 }  // namespace bcgpu
 
 namespace bcgpu {
