@@ -168,6 +168,32 @@ int bcgpu_svb_decode_blocks_host(bcgpu_ctx *ctx, const uint8_t *bytes, size_t le
 int bcgpu_svb_block_offsets_host(bcgpu_ctx *ctx, const uint8_t *bytes, size_t len, size_t n,
                                  uint64_t *offsets);
 
+/* ---- format plumbing on the host (no device, no ctx) -------------------- */
+
+/* Data + control length the control stream of an n-integer Stream VByte payload
+ * declares: ceil(n/4) + sum of byte lengths.  TRUNCATED when
+ * len < ceil(n/4). */
+int bcgpu_svb_payload_length(const uint8_t *bytes, size_t len, size_t n, size_t *expect);
+
+/* svb_append (reference stream_vbyte.hpp:44-46): appends `value`
+ * as integer n of the payload buf[0..len), in place; the result is byte-identical to
+ * a one-shot encode of the n+1 integers (a new control byte shifts the data region
+ * up by one byte).  cap = capacity of buf (needs len + 5 in the worst case).  The
+ * payload is validated first (truncated / trailing_bytes). */
+int bcgpu_svb_append(uint8_t *buf, size_t len, size_t cap, size_t n, uint32_t value, size_t *new_len);
+
+/* The 14-byte container: "SVB1", codec tag, flags (bit 0 = delta),
+ * LE32 count, LE32 payload_length, then the payload. */
+#define BCGPU_CONTAINER_HEADER 14
+int bcgpu_container_write(uint8_t codec, int delta, size_t count, const uint8_t *payload, size_t payload_len,
+                          uint8_t *out, size_t cap, size_t *out_len);
+/* Validates magic (BAD_MAGIC), codec tag (UNKNOWN_CODEC), reserved flags
+ * (RESERVED_FLAGS), source length (TRUNCATED / TRAILING_BYTES) and, for Stream
+ * VByte, the payload length against the size identity (LENGTH_MISMATCH).  Other
+ * known codecs are parsed but return UNSUPPORTED (outside this library). */
+int bcgpu_container_read(const uint8_t *src, size_t len, uint8_t *codec, int *delta, uint32_t *count,
+                         size_t *payload_offset, size_t *payload_len);
+
 #ifdef __cplusplus
 }
 #endif

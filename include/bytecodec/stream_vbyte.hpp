@@ -45,6 +45,11 @@ uint32_t svb_decode_delta(std::span<const uint8_t> bytes, size_t n, uint32_t bas
 // svb_encode_delta(v, 0) == encode(codec_id::stream_vbyte, v, true).bytes.
 std::vector<uint8_t> svb_encode_delta(std::span<const uint32_t> values, uint32_t prev);
 
+// reference stream_vbyte.hpp:44-46: append one integer to the payload, keeping the
+// buffer byte-identical to a one-shot svb_encode of the extended sequence.
+// On a delta buffer `value` is the next payload integer (the next delta).
+void svb_append(encoded_buffer& buf, uint32_t value);
+
 // reference stream_vbyte.hpp:48-49
 std::vector<size_t> svb_block_data_offsets(std::span<const uint8_t> bytes, size_t n);
 

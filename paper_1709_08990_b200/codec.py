@@ -245,3 +245,49 @@ def decode(buf: EncodedBuffer) -> np.ndarray:
     else:
         svb_decode(buf.bytes, buf.count, out)
     return out
+
+
+# ---- format plumbing on the host (svb_format.cpp): no device, no context -------------
+def svb_payload_length(data, n: int) -> int:
+    """ceil(n/4) + the data bytes the control stream declares."""
+    b = _byte_array(data)
+    out = C.c_size_t(0)
+    _check(lib.bcgpu_svb_payload_length(b.ctypes.data if b.size else None, b.size, n, C.byref(out)),
+           "svb_payload_length")
+    return int(out.value)
+
+
+def svb_append(buf: EncodedBuffer, value: int) -> None:
+    """svb_append, reference stream_vbyte.hpp:44-46: appends `value` as
+    the next payload integer in place; the bytes stay identical to a one-shot encode."""
+    _require_svb(buf.codec)
+    b = np.frombuffer(bytes(buf.bytes) + b"\0" * 5, np.uint8).copy()
+    n_old = len(buf.bytes)
+    out = C.c_size_t(0)
+    _check(lib.bcgpu_svb_append(b.ctypes.data, n_old, b.size, buf.count, int(value) & 0xFFFFFFFF, C.byref(out)),
+           "svb_append")
+    buf.bytes = b[: out.value].tobytes()
+    buf.count += 1
+
+
+def write_container(buf: EncodedBuffer) -> bytes:
+    """The 14-byte "SVB1" container: header then payload."""
+    p = _byte_array(buf.bytes)
+    out = np.empty(14 + p.size, np.uint8)
+    n = C.c_size_t(0)
+    _check(lib.bcgpu_container_write(int(buf.codec), int(bool(buf.delta)), int(buf.count),
+                                     p.ctypes.data if p.size else None, p.size, out.ctypes.data, out.size,
+                                     C.byref(n)), "write_container")
+    return out[: n.value].tobytes()
+
+
+def read_container(data) -> EncodedBuffer:
+    """Inverse of write_container; bad_magic / unknown_codec / reserved_flags / truncated /
+    trailing_bytes / length_mismatch are distinct errors."""
+    b = _byte_array(data)
+    tag, delta, count = C.c_uint8(0), C.c_int(0), C.c_uint32(0)
+    off, plen = C.c_size_t(0), C.c_size_t(0)
+    _check(lib.bcgpu_container_read(b.ctypes.data if b.size else None, b.size, C.byref(tag), C.byref(delta),
+                                    C.byref(count), C.byref(off), C.byref(plen)), "read_container")
+    return EncodedBuffer(codec_id(tag.value), int(count.value), bool(delta.value),
+                         b[off.value: off.value + plen.value].tobytes())

@@ -13,6 +13,7 @@
 #include "bcgpu/bcgpu.h"
 #include "bytecodec/codec.hpp"
 #include "bytecodec/stream_vbyte.hpp"
+#include "bytecodec/container.hpp"
 
 namespace bytecodec {
 namespace {
@@ -138,6 +139,45 @@ size_t svb_decode_block(std::span<const uint8_t> bytes, size_t n, size_t block, 
                                                 &cnt);
     if (st) throw_status(st, "svb_decode_block");
     return cnt;
+}
+
+void svb_append(encoded_buffer& buf, uint32_t value) {
+    require_svb(buf.codec);
+    const size_t len = buf.bytes.size();
+    buf.bytes.resize(len + 5);  // worst case: a new control byte + 4 data bytes
+    size_t new_len = 0;
+    const int st = bcgpu_svb_append(buf.bytes.data(), len, buf.bytes.size(), buf.count, value, &new_len);
+    if (st) {
+        buf.bytes.resize(len);
+        throw_status(st, "svb_append");
+    }
+    buf.bytes.resize(new_len);
+    buf.count += 1;
+}
+
+std::vector<uint8_t> write_container(const encoded_buffer& buf) {
+    std::vector<uint8_t> out(BCGPU_CONTAINER_HEADER + buf.bytes.size());
+    size_t n = 0;
+    const int st = bcgpu_container_write(static_cast<uint8_t>(buf.codec), buf.delta ? 1 : 0, buf.count,
+                                         buf.bytes.data(), buf.bytes.size(), out.data(), out.size(), &n);
+    if (st) throw_status(st, "write_container");
+    out.resize(n);
+    return out;
+}
+
+encoded_buffer read_container(std::span<const uint8_t> src) {
+    uint8_t tag = 0;
+    int delta = 0;
+    uint32_t count = 0;
+    size_t off = 0, plen = 0;
+    const int st = bcgpu_container_read(src.data(), src.size(), &tag, &delta, &count, &off, &plen);
+    if (st) throw_status(st, "read_container");
+    encoded_buffer b;
+    b.codec = static_cast<codec_id>(tag);
+    b.count = count;
+    b.delta = delta != 0;
+    b.bytes.assign(src.begin() + (std::ptrdiff_t)off, src.begin() + (std::ptrdiff_t)(off + plen));
+    return b;
 }
 
 std::vector<uint8_t> encode_payload(codec_id id, std::span<const uint32_t> values) {

@@ -11,6 +11,7 @@
 
 #include "bytecodec/codec.hpp"
 #include "bytecodec/stream_vbyte.hpp"
+#include "bytecodec/container.hpp"
 
 using namespace bytecodec;
 
@@ -67,7 +68,7 @@ int main() {
             const size_t k = (size_t)(rng() % offs.size());
             uint32_t blk[4];
             const size_t cnt = svb_decode_block(enc, n, k, offs[k], blk);
-            CHECK(cnt == (k + 1) * 4 <= n ? 4 : n - 4 * k);
+            CHECK(cnt == ((k + 1) * 4 <= n ? 4 : n - 4 * k));
             for (size_t i = 0; i < cnt; ++i) CHECK(blk[i] == v[4 * k + i]);
         }
     }
@@ -94,6 +95,30 @@ int main() {
             CHECK(false);
         } catch (const codec_error& e) {
             CHECK(e.code() == errc::unsupported);
+        }
+    }
+    // svb_append keeps the one-shot encoding; the SVB1 container round trip
+    {
+        std::mt19937 rng(11);
+        encoded_buffer b = encode(codec_id::stream_vbyte, std::vector<uint32_t>{});
+        std::vector<uint32_t> seq;
+        for (int i = 0; i < 300; ++i) {
+            const uint32_t x = rng() >> (rng() % 32);
+            svb_append(b, x);
+            seq.push_back(x);
+        }
+        CHECK(b.count == 300 && b.bytes == svb_encode(seq));
+        const std::vector<uint8_t> f = write_container(b);
+        CHECK(f.size() == 14 + b.bytes.size() && f[0] == 'S' && f[3] == '1');
+        const encoded_buffer r = read_container(f);
+        CHECK(r.count == b.count && r.delta == b.delta && r.bytes == b.bytes && r.codec == codec_id::stream_vbyte);
+        auto bad = f;
+        bad[0] = 'X';
+        try {
+            read_container(bad);
+            CHECK(false);
+        } catch (const codec_error& e) {
+            CHECK(e.code() == errc::bad_magic);
         }
     }
     if (failures) {
