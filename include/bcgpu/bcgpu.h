@@ -168,6 +168,25 @@ int bcgpu_svb_decode_blocks_host(bcgpu_ctx *ctx, const uint8_t *bytes, size_t le
 int bcgpu_svb_block_offsets_host(bcgpu_ctx *ctx, const uint8_t *bytes, size_t len, size_t n,
                                  uint64_t *offsets);
 
+/* ---- batched seek / select over one delta-coded stream ------------------- */
+/* (module stream_query; the reference's query.cpp has no header.)
+ * The logical sequence is base + the prefix sums of the n payload integers; seek
+ * requires it non-decreasing (sorted ids).  seek: for every target, the first index
+ * with value >= target (ties: lowest index) and that value; index = n means not
+ * found.  select: the value at every index (indices must be < n; the _host variant
+ * returns OUT_OF_RANGE otherwise).  The stream is never decoded in full: a metadata
+ * pass (control scan + sums: 8 B per 1024 integers), then one warp per query decodes
+ * one 1024-integer sub-tile.  Malformed streams are reported as for decode. */
+int bcgpu_svb_seek_batch_device(bcgpu_ctx *ctx, const uint8_t *d_in, size_t in_len, size_t n, uint32_t base,
+                                const uint32_t *d_targets, size_t q, uint64_t *d_index, uint32_t *d_values,
+                                void *stream);
+int bcgpu_svb_select_batch_device(bcgpu_ctx *ctx, const uint8_t *d_in, size_t in_len, size_t n, uint32_t base,
+                                  const uint64_t *d_idx, size_t q, uint32_t *d_values, void *stream);
+int bcgpu_svb_seek_host(bcgpu_ctx *ctx, const uint8_t *bytes, size_t len, size_t n, uint32_t base,
+                        const uint32_t *targets, size_t q, uint64_t *index, uint32_t *values);
+int bcgpu_svb_select_host(bcgpu_ctx *ctx, const uint8_t *bytes, size_t len, size_t n, uint32_t base,
+                          const uint64_t *idx, size_t q, uint32_t *values);
+
 /* ---- format plumbing on the host (no device, no ctx) -------------------- */
 
 /* Data + control length the control stream of an n-integer Stream VByte payload

@@ -291,3 +291,49 @@ def read_container(data) -> EncodedBuffer:
                                     C.byref(count), C.byref(off), C.byref(plen)), "read_container")
     return EncodedBuffer(codec_id(tag.value), int(count.value), bool(delta.value),
                          b[off.value: off.value + plen.value].tobytes())
+
+
+# ---- batched seek / select on the GPU (svb_query.cu) ---------------
+def _require_delta(buf: EncodedBuffer) -> None:
+    _require_svb(buf.codec)
+    if not buf.delta:
+        raise CodecError(errc.unsupported, "seek / select need a delta-coded buffer (SPEC.md:414)")
+
+
+def seek_batch(buf: EncodedBuffer, targets) -> tuple[np.ndarray, np.ndarray]:
+    """For every target the first (index, value) with value >= target over the buffer's
+    non-decreasing logical sequence; index == buf.count means not found."""
+    _require_delta(buf)
+    b = _byte_array(buf.bytes)
+    t = _u32_array(targets)
+    idx = np.empty(t.size, np.uint64)
+    val = np.empty(t.size, np.uint32)
+    _check(lib.bcgpu_svb_seek_host(_ctx(), b.ctypes.data if b.size else None, b.size, buf.count, 0,
+                                   t.ctypes.data if t.size else None, t.size, idx.ctypes.data if t.size else None,
+                                   val.ctypes.data if t.size else None), "seek")
+    return idx, val
+
+
+def select_batch(buf: EncodedBuffer, indices) -> np.ndarray:
+    """The logical value at every index (out_of_range if any index >= buf.count)."""
+    _require_delta(buf)
+    b = _byte_array(buf.bytes)
+    i = np.ascontiguousarray(np.asarray(indices, dtype=np.uint64))
+    val = np.empty(i.size, np.uint32)
+    _check(lib.bcgpu_svb_select_host(_ctx(), b.ctypes.data if b.size else None, b.size, buf.count, 0,
+                                     i.ctypes.data if i.size else None, i.size, val.ctypes.data if i.size else None),
+           "select")
+    return val
+
+
+def seek(buf: EncodedBuffer, target: int):
+    """(index, value) of the first value >= target, or None (not found)."""
+    idx, val = seek_batch(buf, [target])
+    return None if int(idx[0]) >= buf.count else (int(idx[0]), int(val[0]))
+
+
+def select(buf: EncodedBuffer, i: int) -> int:
+    """the i-th logical value."""
+    if i < 0 or i >= buf.count:
+        raise CodecError(errc.out_of_range, f"select: index {i} not below count {buf.count}")
+    return int(select_batch(buf, [i])[0])

@@ -77,6 +77,8 @@ struct bcgpu_ctx {
     unsigned long long* pin = nullptr;       // host pipeline: pinned offsets / status
     size_t pin_cap = 0;                      // entries
     uint64_t agg_n = 0;                      // n whose tile aggregates hold no current-epoch tag
+    uint32_t* endval = nullptr;              // seek / select: last value of every sub-tile
+    size_t endval_cap = 0;                   // entries
 };
 
 static unsigned long long* ticket_ptr(bcgpu_ctx* c) { return c->ws; }
@@ -300,6 +302,7 @@ int bcgpu_ctx_destroy(bcgpu_ctx* c) {
     if (c->d_scratch) cudaFree(c->d_scratch);
     if (c->offs) cudaFree(c->offs);
     if (c->slots) cudaFree(c->slots);
+    if (c->endval) cudaFree(c->endval);
     if (c->stream) cudaStreamDestroy(c->stream);
     if (c->aux) cudaStreamDestroy(c->aux);
     if (c->aux2) cudaStreamDestroy(c->aux2);
@@ -331,6 +334,8 @@ int bcgpu_svb_encode_device(bcgpu_ctx* c, const uint32_t* d_in, size_t n, int de
     DeviceGuard g(c->device);
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     if (n == 0) {
+        const int se = next_epoch(c, s);  // a fresh status epoch: no earlier call's error is reported
+        if (se) return se;
         if (d_out_len) BC_CUDA(cudaMemsetAsync(d_out_len, 0, sizeof(uint64_t), s));
         return BCGPU_OK;
     }
@@ -374,6 +379,8 @@ int bcgpu_svb_decode_device(bcgpu_ctx* c, const uint8_t* d_in, size_t in_len, si
     DeviceGuard g(c->device);
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     if (n == 0) {
+        const int se = next_epoch(c, s);
+        if (se) return se;
         if (d_last) BC_CUDA(cudaMemcpyAsync(d_last, &base, sizeof(uint32_t), cudaMemcpyHostToDevice, s));
         if (in_len != 0) return BCGPU_ERR_TRAILING_BYTES;
         return BCGPU_OK;
@@ -395,9 +402,9 @@ int bcgpu_svb_block_offsets_device(bcgpu_ctx* c, const uint8_t* d_in, size_t in_
     if (!c || (n && (!d_in || !d_offsets))) return BCGPU_ERR_INVALID_ARGUMENT;
     const size_t nctrl = (n + 3) / 4;
     if (in_len < nctrl) return BCGPU_ERR_TRUNCATED;
-    if (n == 0) return BCGPU_OK;
     DeviceGuard g(c->device);
     cudaStream_t s = static_cast<cudaStream_t>(stream);
+    if (n == 0) return next_epoch(c, s);
     LookbackArgs lb;
     int st = make_lookback(c, nctrl, kOffsetsTileGroups, s, &lb);
     if (st) return st;
@@ -461,6 +468,79 @@ int bcgpu_svb_encoded_sizes_batch_device(bcgpu_ctx* c, const bcgpu_encode_segmen
     if (st) return st;
     BC_CUDA(launch_sizes_batch(d_segs, nseg, d_in, d_out_lens, delta, ba, s));
     g_launches.fetch_add(1);
+    return BCGPU_OK;
+}
+
+// ---------------------------------------------------------------------------
+// batched seek / select over one delta stream (svb_query.cu)
+// ---------------------------------------------------------------------------
+static int query_prepare(bcgpu_ctx* c, const uint8_t* d_in, size_t in_len, size_t n, uint32_t base, cudaStream_t s) {
+    const size_t nsub = ((n + 3) / 4 + 255) / 256;
+    int st = ensure_meta(c, n, s);
+    if (st) return st;
+    if (nsub + 1 > c->endval_cap) {
+        if (c->endval) {
+            BC_CUDA(cudaStreamSynchronize(s));
+            BC_CUDA(cudaFree(c->endval));
+            c->endval = nullptr;
+            c->endval_cap = 0;
+        }
+        const size_t cap = nsub + nsub / 4 + 64;
+        BC_CUDA(cudaMalloc(&c->endval, cap * sizeof(uint32_t)));
+        c->endval_cap = cap;
+    }
+    st = next_epoch(c, s);
+    if (st) return st;
+    int launches = 0;
+    BC_CUDA(launch_query_meta(d_in, in_len, n, base, c->offs, c->endval, status_ptr(c), c->epoch, s, &launches));
+    g_launches.fetch_add((uint64_t)launches);
+    c->agg_n = n;  // the control scan cleared this layout's aggregates
+    return BCGPU_OK;
+}
+
+int bcgpu_svb_seek_batch_device(bcgpu_ctx* c, const uint8_t* d_in, size_t in_len, size_t n, uint32_t base,
+                                const uint32_t* d_targets, size_t q, uint64_t* d_index, uint32_t* d_values,
+                                void* stream) {
+    if (!c || (q && (!d_targets || !d_index || !d_values)) || (n && !d_in)) return BCGPU_ERR_INVALID_ARGUMENT;
+    if (in_len < (n + 3) / 4) return BCGPU_ERR_TRUNCATED;
+    DeviceGuard g(c->device);
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    if (n == 0) {  // nothing to find: every index = n = 0 (not found)
+        const int se = next_epoch(c, s);
+        if (se) return se;
+        if (in_len) return BCGPU_ERR_TRAILING_BYTES;
+        if (q) {
+            BC_CUDA(cudaMemsetAsync(d_index, 0, 8 * q, s));
+            BC_CUDA(cudaMemsetAsync(d_values, 0, 4 * q, s));
+        }
+        return BCGPU_OK;
+    }
+    int st = query_prepare(c, d_in, in_len, n, base, s);
+    if (st) return st;
+    BC_CUDA(launch_query(d_in, in_len, n, base, c->offs, c->endval, 1, d_targets, q, d_index, d_values,
+                         c->num_sms * 8, s));
+    if (q) g_launches.fetch_add(1);
+    return BCGPU_OK;
+}
+
+int bcgpu_svb_select_batch_device(bcgpu_ctx* c, const uint8_t* d_in, size_t in_len, size_t n, uint32_t base,
+                                  const uint64_t* d_idx, size_t q, uint32_t* d_values, void* stream) {
+    if (!c || (q && (!d_idx || !d_values)) || (n && !d_in)) return BCGPU_ERR_INVALID_ARGUMENT;
+    if (in_len < (n + 3) / 4) return BCGPU_ERR_TRUNCATED;
+    DeviceGuard g(c->device);
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    if (n == 0) {  // no valid index
+        const int se = next_epoch(c, s);
+        if (se) return se;
+        if (in_len) return BCGPU_ERR_TRAILING_BYTES;
+        if (q) BC_CUDA(cudaMemsetAsync(d_values, 0, 4 * q, s));
+        return BCGPU_OK;
+    }
+    int st = query_prepare(c, d_in, in_len, n, base, s);
+    if (st) return st;
+    BC_CUDA(launch_query(d_in, in_len, n, base, c->offs, c->endval, 0, d_idx, q, nullptr, d_values,
+                         c->num_sms * 8, s));
+    if (q) g_launches.fetch_add(1);
     return BCGPU_OK;
 }
 
@@ -711,6 +791,57 @@ int bcgpu_svb_block_offsets_host(bcgpu_ctx* c, const uint8_t* bytes, size_t len,
     st = bcgpu_svb_block_offsets_device(c, d, nctrl, n, reinterpret_cast<uint64_t*>(d + off_o), c->stream);
     if (st) return st;
     BC_CUDA(cudaMemcpyAsync(offsets, d + off_o, 8 * nctrl, cudaMemcpyDeviceToHost, c->stream));
+    BC_CUDA(cudaStreamSynchronize(c->stream));
+    return BCGPU_OK;
+}
+
+
+int bcgpu_svb_seek_host(bcgpu_ctx* c, const uint8_t* bytes, size_t len, size_t n, uint32_t base, const uint32_t* targets,
+                        size_t q, uint64_t* index, uint32_t* values) {
+    if (!c || (q && (!targets || !index || !values)) || (len && !bytes)) return BCGPU_ERR_INVALID_ARGUMENT;
+    if (len < (n + 3) / 4) return BCGPU_ERR_TRUNCATED;
+    DeviceGuard g(c->device);
+    const size_t off_t = align_up(len, 256), off_i = align_up(off_t + 4 * q, 256), off_v = align_up(off_i + 8 * q, 256);
+    void* sp = nullptr;
+    int st = scratch(c, off_v + 4 * q + 256, &sp);
+    if (st) return st;
+    uint8_t* d = static_cast<uint8_t*>(sp);
+    if (len) BC_CUDA(cudaMemcpyAsync(d, bytes, len, cudaMemcpyHostToDevice, c->stream));
+    if (q) BC_CUDA(cudaMemcpyAsync(d + off_t, targets, 4 * q, cudaMemcpyHostToDevice, c->stream));
+    st = bcgpu_svb_seek_batch_device(c, d, len, n, base, reinterpret_cast<uint32_t*>(d + off_t), q,
+                                     reinterpret_cast<uint64_t*>(d + off_i), reinterpret_cast<uint32_t*>(d + off_v),
+                                     c->stream);
+    if (st) return st;
+    st = bcgpu_ctx_sync_status(c, c->stream);
+    if (st) return st;
+    if (q) {
+        BC_CUDA(cudaMemcpyAsync(index, d + off_i, 8 * q, cudaMemcpyDeviceToHost, c->stream));
+        BC_CUDA(cudaMemcpyAsync(values, d + off_v, 4 * q, cudaMemcpyDeviceToHost, c->stream));
+    }
+    BC_CUDA(cudaStreamSynchronize(c->stream));
+    return BCGPU_OK;
+}
+
+int bcgpu_svb_select_host(bcgpu_ctx* c, const uint8_t* bytes, size_t len, size_t n, uint32_t base, const uint64_t* idx,
+                          size_t q, uint32_t* values) {
+    if (!c || (q && (!idx || !values)) || (len && !bytes)) return BCGPU_ERR_INVALID_ARGUMENT;
+    for (size_t i = 0; i < q; ++i)
+        if (idx[i] >= n) return BCGPU_ERR_OUT_OF_RANGE;
+    if (len < (n + 3) / 4) return BCGPU_ERR_TRUNCATED;
+    DeviceGuard g(c->device);
+    const size_t off_i = align_up(len, 256), off_v = align_up(off_i + 8 * q, 256);
+    void* sp = nullptr;
+    int st = scratch(c, off_v + 4 * q + 256, &sp);
+    if (st) return st;
+    uint8_t* d = static_cast<uint8_t*>(sp);
+    if (len) BC_CUDA(cudaMemcpyAsync(d, bytes, len, cudaMemcpyHostToDevice, c->stream));
+    if (q) BC_CUDA(cudaMemcpyAsync(d + off_i, idx, 8 * q, cudaMemcpyHostToDevice, c->stream));
+    st = bcgpu_svb_select_batch_device(c, d, len, n, base, reinterpret_cast<uint64_t*>(d + off_i), q,
+                                       reinterpret_cast<uint32_t*>(d + off_v), c->stream);
+    if (st) return st;
+    st = bcgpu_ctx_sync_status(c, c->stream);
+    if (st) return st;
+    if (q) BC_CUDA(cudaMemcpyAsync(values, d + off_v, 4 * q, cudaMemcpyDeviceToHost, c->stream));
     BC_CUDA(cudaStreamSynchronize(c->stream));
     return BCGPU_OK;
 }

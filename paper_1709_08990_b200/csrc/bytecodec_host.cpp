@@ -14,6 +14,7 @@
 #include "bytecodec/codec.hpp"
 #include "bytecodec/stream_vbyte.hpp"
 #include "bytecodec/container.hpp"
+#include "bytecodec/query.hpp"
 
 namespace bytecodec {
 namespace {
@@ -179,6 +180,40 @@ encoded_buffer read_container(std::span<const uint8_t> src) {
     b.bytes.assign(src.begin() + (std::ptrdiff_t)off, src.begin() + (std::ptrdiff_t)(off + plen));
     return b;
 }
+
+static void require_delta(const encoded_buffer& buf) {
+    require_svb(buf.codec);
+    if (!buf.delta) throw codec_error(errc::unsupported, "seek / select need a delta-coded buffer");
+}
+
+std::vector<std::optional<seek_result>> seek(const encoded_buffer& buf, std::span<const uint32_t> targets) {
+    require_delta(buf);
+    std::vector<uint64_t> idx(targets.size());
+    std::vector<uint32_t> val(targets.size());
+    const int st = bcgpu_svb_seek_host(ctx(), buf.bytes.data(), buf.bytes.size(), buf.count, 0, targets.data(),
+                                       targets.size(), idx.data(), val.data());
+    if (st) throw_status(st, "seek");
+    std::vector<std::optional<seek_result>> out(targets.size());
+    for (size_t i = 0; i < targets.size(); ++i)
+        if (idx[i] < buf.count) out[i] = seek_result{(size_t)idx[i], val[i]};
+    return out;
+}
+
+std::optional<seek_result> seek(const encoded_buffer& buf, uint32_t target) {
+    return seek(buf, std::span<const uint32_t>(&target, 1))[0];
+}
+
+std::vector<uint32_t> select(const encoded_buffer& buf, std::span<const size_t> indices) {
+    require_delta(buf);
+    std::vector<uint64_t> idx(indices.begin(), indices.end());
+    std::vector<uint32_t> val(indices.size());
+    const int st = bcgpu_svb_select_host(ctx(), buf.bytes.data(), buf.bytes.size(), buf.count, 0, idx.data(),
+                                         idx.size(), val.data());
+    if (st) throw_status(st, "select");
+    return val;
+}
+
+uint32_t select(const encoded_buffer& buf, size_t i) { return select(buf, std::span<const size_t>(&i, 1))[0]; }
 
 std::vector<uint8_t> encode_payload(codec_id id, std::span<const uint32_t> values) {
     require_svb(id);

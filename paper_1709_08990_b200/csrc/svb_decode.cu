@@ -1301,6 +1301,16 @@ unsigned long long* meta_agg_ptr(void* meta_ws, uint64_t n, uint64_t* count) {
     return carve_decode_meta(meta_ws, n).agg;
 }
 
+// the sums pass over the whole stream (after launch_decode_ctrl): per-sub-tile sums and
+// scanned per-chunk carries in the workspace (batched seek / select, svb_query.cu)
+cudaError_t launch_decode_sums(const uint8_t* in, uint64_t in_len, uint64_t n, void* meta_ws, cudaStream_t stream) {
+    const DecodeMeta m = carve_decode_meta(meta_ws, n);
+    const uint64_t ngroups = (n + 3) >> 2;
+    const uint64_t nsub = (ngroups + kWTGroups - 1) / kWTGroups;
+    const double dpb = nsub ? (double)(in_len > ngroups ? in_len - ngroups : 0) / (double)nsub : 0.0;
+    return launch_sums(in, in_len, n, m, dpb, 0, (uint32_t)((nsub + kCTWarps - 1) / kCTWarps), stream);
+}
+
 // device address of the chunk offsets (nchunks + 1 entries, after launch_decode_ctrl)
 unsigned long long* decode_chunkpre_ptr(void* meta_ws, uint64_t n) { return carve_decode_meta(meta_ws, n).chunkpre; }
 

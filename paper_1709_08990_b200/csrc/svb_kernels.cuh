@@ -38,6 +38,15 @@ cudaError_t launch_decode_range(const uint8_t* in, uint64_t in_len, uint64_t n, 
                                 uint32_t epoch = 0);  // epoch != 0: a whole-stream delta decode may run one-pass
 unsigned long long* decode_chunkpre_ptr(void* meta_ws, uint64_t n);
 unsigned long long* meta_agg_ptr(void* meta_ws, uint64_t n, uint64_t* count);
+cudaError_t launch_decode_sums(const uint8_t* in, uint64_t in_len, uint64_t n, void* meta_ws, cudaStream_t stream);
+// Batched seek / select over one delta stream (svb_query.cu): metadata pass (3 launches,
+// endval = last logical value of each 1024-integer sub-tile), then one warp per query.
+cudaError_t launch_query_meta(const uint8_t* in, uint64_t in_len, uint64_t n, uint32_t base, void* meta_ws,
+                              uint32_t* endval, unsigned long long* status, uint32_t epoch, cudaStream_t stream,
+                              int* launches);
+cudaError_t launch_query(const uint8_t* in, uint64_t in_len, uint64_t n, uint32_t base, void* meta_ws,
+                         const uint32_t* endval, int seek, const void* queries, uint64_t q, uint64_t* out_index,
+                         uint32_t* out_value, int grid_cap, cudaStream_t stream);
 int occupancy_decode_pipe();
 // Single-array encode (svb_encode.cu); meta_ws as for the decode.  With `slots`
 // (encode_slot_bytes(n) of device scratch, 128-B aligned): slot encode + compaction,

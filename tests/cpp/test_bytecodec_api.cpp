@@ -12,6 +12,7 @@
 #include "bytecodec/codec.hpp"
 #include "bytecodec/stream_vbyte.hpp"
 #include "bytecodec/container.hpp"
+#include "bytecodec/query.hpp"
 
 using namespace bytecodec;
 
@@ -120,6 +121,15 @@ int main() {
         } catch (const codec_error& e) {
             CHECK(e.code() == errc::bad_magic);
         }
+    }
+    // seek / select on a compressed delta buffer
+    {
+        const encoded_buffer b = encode(codec_id::stream_vbyte, std::vector<uint32_t>{3, 7, 19, 20}, true);
+        const auto r = seek(b, 8u);
+        CHECK(r && r->index == 2 && r->value == 19);
+        CHECK(seek(b, 3u) && seek(b, 3u)->index == 0);
+        CHECK(!seek(b, 21u));
+        CHECK(select(b, (size_t)1) == 7 && select(b, (size_t)3) == 20);
     }
     if (failures) {
         std::fprintf(stderr, "%d failures\n", failures);
