@@ -1,0 +1,78 @@
+"""Randomised parity: hypothesis draws sizes, value shapes, delta/prev and buffer offsets, and
+every encode / decode path the library dispatches between (one-pass, slot, two-read, sums +
+pooled decode) must reproduce the pinned oracle byte for byte."""
+import ctypes as C
+import os
+
+import numpy as np
+import pytest
+from hypothesis import HealthCheck, given, settings
+from hypothesis import strategies as st
+
+import oracle
+
+pytestmark = pytest.mark.gpu
+
+# debug flags of the ctx (bcgpu_capi.cu): which path runs
+ENCODE_PATHS = {"default": 0, "two_read": 16, "slots": 32, "one_pass_plain": 4096}
+DECODE_PATHS = {"default": 0, "sums_pooled": 0x400}
+
+
+@pytest.fixture(scope="module")
+def env():
+    import torch
+    from paper_1709_08990_b200._native import lib
+    from paper_1709_08990_b200.device import DeviceCodec
+    lib.bcgpu_debug_set_flags.argtypes = [C.c_void_p, C.c_uint32]
+    return torch, lib, DeviceCodec(0)
+
+
+def _values(kind, n, seed):
+    rng = np.random.default_rng(seed)
+    if kind == "classes":
+        k = rng.integers(0, 4, n)
+        return (rng.integers(0, 2**32, n, dtype=np.uint64) >> (8 * (3 - k)).astype(np.uint64)).astype(np.uint32)
+    if kind == "sorted_small":
+        return np.cumsum(rng.integers(0, 200, n, dtype=np.uint64)).astype(np.uint32)
+    if kind == "sorted_wide":
+        return np.cumsum(rng.integers(0, 1 << 22, n, dtype=np.uint64)).astype(np.uint32)  # wraps mod 2^32
+    if kind == "constant":
+        return np.full(n, rng.integers(0, 2**32), np.uint32)
+    return rng.integers(0, 256, n, dtype=np.uint64).astype(np.uint32)
+
+
+@settings(max_examples=int(os.environ.get("FUZZ_EXAMPLES", "200")), deadline=None, suppress_health_check=list(HealthCheck))
+@given(n=st.one_of(st.integers(0, 3000), st.integers(3000, 400_000), st.sampled_from([8192, 65536, 1 << 20])),
+       kind=st.sampled_from(["classes", "sorted_small", "sorted_wide", "constant", "bytes"]),
+       delta=st.booleans(), prev=st.integers(0, 2**32 - 1), seed=st.integers(0, 2**31),
+       in_off=st.sampled_from([0, 1, 2, 3, 4]), out_off=st.integers(0, 17),
+       enc=st.sampled_from(sorted(ENCODE_PATHS)), dec=st.sampled_from(sorted(DECODE_PATHS)))
+def test_fuzz_roundtrip(env, n, kind, delta, prev, seed, in_off, out_off, enc, dec):
+    torch, lib, dev = env
+    v = _values(kind, n, seed)
+    if not delta:
+        prev = 0
+    want = oracle.encode(v, delta=delta, prev=prev)
+    src = torch.zeros(n + 8, dtype=torch.int32, device="cuda")
+    if n:
+        src[in_off:in_off + n] = torch.from_numpy(v.view(np.int32)).cuda()
+    cap = (n + 3) // 4 + 4 * n
+    outb = torch.zeros(cap + 32, dtype=torch.uint8, device="cuda")
+    olen = torch.zeros(1, dtype=torch.int64, device="cuda")
+    try:
+        lib.bcgpu_debug_set_flags(dev._ctx, ENCODE_PATHS[enc])
+        dev.encode(src[in_off:in_off + n], outb[out_off:out_off + cap], olen, delta=delta, prev=prev)
+        dev.check()
+        m = int(olen.item())
+        assert m == len(want)
+        assert outb[out_off:out_off + m].cpu().numpy().tobytes() == want
+        lib.bcgpu_debug_set_flags(dev._ctx, DECODE_PATHS[dec])
+        dst = torch.zeros(n + 8, dtype=torch.int32, device="cuda")
+        last = torch.zeros(1, dtype=torch.int32, device="cuda")
+        dev.decode(outb[out_off:out_off + m], n, dst[in_off:in_off + n], delta=delta, base=prev, last=last)
+        dev.check()
+        assert np.array_equal(dst[in_off:in_off + n].cpu().numpy().view(np.uint32), v)
+        if delta:
+            assert (int(last.item()) & 0xFFFFFFFF) == (int(v[-1]) if n else prev)
+    finally:
+        lib.bcgpu_debug_set_flags(dev._ctx, 0)
