@@ -576,36 +576,6 @@ struct __align__(16) E1Shared {
     unsigned long long carry, incl;
 };
 
-// packed bytes [src, src + len) of shared memory (16-B aligned, with >= 16 readable bytes
-// before and after) -> global dst (any alignment): destination granule k is the 16 source
-// bytes at src + 16k - p, read as 5 words and funnel-shifted (p = dst's 16-B phase)
-__device__ __forceinline__ void store_realigned(uint32_t src, uint32_t len, uint8_t* dst) {
-    const int lane = threadIdx.x & 31;
-    const uintptr_t D = (uintptr_t)dst;
-    const uint32_t p = (uint32_t)(D & 15);
-    const uintptr_t Dal = D - p, Dend = D + len;
-    const uint32_t nout = (p + len + 15) >> 4;
-    const uint32_t r = ((0u - p) & 3u) * 8u;
-    for (uint32_t k = lane; k < nout; k += 32) {
-        const uint32_t wa = (src + 16 * k - p) & ~3u;
-        const uint32_t w0 = lds32v(wa), w1 = lds32v(wa + 4), w2 = lds32v(wa + 8), w3 = lds32v(wa + 12),
-                       w4 = lds32v(wa + 16);
-        {
-            const uint4 v = make_uint4(__funnelshift_r(w0, w1, r), __funnelshift_r(w1, w2, r),
-                                       __funnelshift_r(w2, w3, r), __funnelshift_r(w3, w4, r));
-            const uintptr_t a = Dal + 16 * (uintptr_t)k;
-            if (a >= D && a + 16 <= Dend) {
-                *reinterpret_cast<uint4*>(a) = v;
-            } else {
-                const uint32_t w[4] = {v.x, v.y, v.z, v.w};
-#pragma unroll
-                for (int bi = 0; bi < 16; ++bi)
-                    if (a + bi >= D && a + bi < Dend) *reinterpret_cast<uint8_t*>(a + bi) = (uint8_t)(w[bi >> 2] >> (8 * (bi & 3)));
-            }
-        }
-    }
-}
-
 template <bool kDelta>
 __global__ void __launch_bounds__(kCTThreads + 32, 2)
     svb_encode1_kernel(const uint32_t* __restrict__ in, uint64_t n, uint32_t prev, uint8_t* __restrict__ out,
@@ -727,7 +697,7 @@ __global__ void __launch_bounds__(kCTThreads + 32, 2)
             const uint32_t cnt_g = (uint32_t)(ngroups - g0 < (uint64_t)kWTGroups ? ngroups - g0 : (uint64_t)kWTGroups);
             uint8_t* cdst = out + g0;
             if ((s + 1) * kWTInts <= n) {
-                const bool small = enc_full_small_pack0<kDelta>(sin, prev_w);
+                const bool small = enc_full_small_pack0<kDelta>(sin, prev_w, sin);
                 if (small) {
                     total = kWTInts;
                     for (uint32_t i = lane; i < kWTGroups / 4; i += 32) {  // 256 zero control bytes

@@ -389,21 +389,22 @@ __device__ __forceinline__ bool enc_full_small(uint32_t sin, uint32_t prev_w) {
 // known yet): every row is read once; if every integer (delta) is < 256 the low bytes
 // are written as 32 aligned words per row over the consumed input (sdst = sin) and the
 // function returns true; otherwise nothing is written.
-template <bool kDelta>
-__device__ __forceinline__ bool enc_full_small_pack0(uint32_t sin, uint32_t prev_w) {
+// sdst: where the packed bytes go (16-B aligned, <= sin; sin itself when 16-B aligned).
+template <bool kDelta, bool kAny = false>
+__device__ __forceinline__ bool enc_full_small_pack0(uint32_t sin, uint32_t prev_w, uint32_t sdst) {
     const int lane = threadIdx.x & 31;
     uint32_t last = prev_w, o = 0;
     uint32_t P[kWTRows];
 #pragma unroll
     for (int j = 0; j < kWTRows; ++j) {
-        const uint4 x = enc_row<kDelta>(sin, j, last);
+        const uint4 x = enc_row<kDelta, kAny>(sin, j, last);
         o |= x.x | x.y | x.z | x.w;
         P[j] = __byte_perm(__byte_perm(x.x, x.y, 0x0040), __byte_perm(x.z, x.w, 0x0040), 0x5410);
     }
     if (!__all_sync(kFull, o < 256u)) return false;
     __syncwarp();  // every lane has read every row
 #pragma unroll
-    for (int j = 0; j < kWTRows; ++j) sts32(sin + 128 * j + 4 * lane, P[j]);
+    for (int j = 0; j < kWTRows; ++j) sts32(sdst + 128 * j + 4 * lane, P[j]);
     return true;
 }
 
@@ -471,6 +472,36 @@ __device__ __forceinline__ void enc_full_pack(uint32_t sin, uint32_t prev_w, con
             sts_int_bytes(a + l0, x.y, l1);
             sts_int_bytes(a + l0 + l1, x.z, l2);
             sts_int_bytes(a + l0 + l1 + l2, x.w, l3);
+        }
+    }
+}
+
+// packed bytes [src, src + len) of shared memory (16-B aligned, with >= 16 readable bytes
+// before and after) -> global dst (any alignment): destination granule k is the 16 source
+// bytes at src + 16k - p, read as 5 words and funnel-shifted (p = dst's 16-B phase)
+__device__ __forceinline__ void store_realigned(uint32_t src, uint32_t len, uint8_t* dst) {
+    const int lane = threadIdx.x & 31;
+    const uintptr_t D = (uintptr_t)dst;
+    const uint32_t p = (uint32_t)(D & 15);
+    const uintptr_t Dal = D - p, Dend = D + len;
+    const uint32_t nout = (p + len + 15) >> 4;
+    const uint32_t r = ((0u - p) & 3u) * 8u;
+    for (uint32_t k = lane; k < nout; k += 32) {
+        const uint32_t wa = (src + 16 * k - p) & ~3u;
+        const uint32_t w0 = lds32v(wa), w1 = lds32v(wa + 4), w2 = lds32v(wa + 8), w3 = lds32v(wa + 12),
+                       w4 = lds32v(wa + 16);
+        {
+            const uint4 v = make_uint4(__funnelshift_r(w0, w1, r), __funnelshift_r(w1, w2, r),
+                                       __funnelshift_r(w2, w3, r), __funnelshift_r(w3, w4, r));
+            const uintptr_t a = Dal + 16 * (uintptr_t)k;
+            if (a >= D && a + 16 <= Dend) {
+                *reinterpret_cast<uint4*>(a) = v;
+            } else {
+                const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+                for (int bi = 0; bi < 16; ++bi)
+                    if (a + bi >= D && a + bi < Dend) *reinterpret_cast<uint8_t*>(a + bi) = (uint8_t)(w[bi >> 2] >> (8 * (bi & 3)));
+            }
         }
     }
 }
