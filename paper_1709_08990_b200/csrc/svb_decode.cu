@@ -1,23 +1,18 @@
 // svb_decode.cu -- single-array Stream VByte decode for sm_100a
 // (svb_decode / svb_decode_delta: reference stream_vbyte.hpp:38-42, codec.hpp:85-90).
 //
-// Reduce-then-scan, no kernel ever waits on another CTA:
-//   1. svb_ctrl_scan_kernel   control bytes only (0.25 B/int).  Per 64-sub-tile
-//      chunk: chunk-local exclusive prefix of every 1024-integer sub-tile's data
-//      length (length[c] = 4 + sum of fields) and the chunk
-//      total; the last CTA to finish scans the chunk totals and validates the
-//      stream length (truncated / trailing_bytes).
-//   2. (delta only) svb_decode_pipe_kernel<kModeSums>: decodes every sub-tile
-//      without storing and records its sum of deltas (+ RED.ADD into its chunk);
-//      the last CTA scans the chunk sums.
-//   3. svb_decode_pipe_kernel<kModePlain|kModeDelta>: decodes and stores.
-// Passes 2-3 are persistent warps: each warp walks sub-tiles gw, gw+GW, ... with
-// a two-deep pipeline -- the next sub-tile's control+data bytes arrive by one
-// TMA bulk copy into the other stage buffer while this one is expanded
-// (funnel-shift / byte-permute, the GPU pshufb), and the
-// metadata (offsets, carries) for the one after is already being loaded.
-// The delta variant fuses the mod-2^32 prefix sum: carry =
-// base + scanned chunk sums + sub-tile sums before it in its chunk.
+//   1. svb_ctrl_scan_kernel   control bytes only (0.25 B/int): per 64-sub-tile chunk
+//      the chunk-local exclusive prefix of every 1024-integer sub-tile's data length
+//      (length[c] = 4 + sum of fields) and the chunk total; the last
+//      CTA to finish scans the chunk totals and validates the stream length
+//      (truncated / trailing_bytes).
+//   2. plain:  svb_decode_pool_kernel<kModePlain> -- one TMA for a CTA's control bytes,
+//      one for its whole data range, expansion straight to 128-bit stores.
+//      delta:  svb_decode1_kernel -- one pass with deferred look-back over tile sums
+//      (cooperative launch), or, for a piece of a stream (host pipeline), the pipelined
+//      sums pass svb_sums_kernel + svb_decode_pool_kernel<kModeDelta> with the carries.
+// The delta variants fuse the mod-2^32 prefix sum.  No kernel waits on
+// a CTA of its own round.
 #include <cstdint>
 
 #include "svb_device.cuh"
@@ -123,214 +118,16 @@ __global__ void __launch_bounds__(256)
 }
 
 // ---------------------------------------------------------------------------
-// 2./3. tile decode: one CTA per 8 sub-tiles, one warp per sub-tile
+// 2./3. decode passes
 // ---------------------------------------------------------------------------
-// Every warp issues one TMA transaction for its sub-tile's control and data
-// bytes as soon as the CTA's offsets have landed, expands them in shared
-// memory (reverse row order keeps the expansion in place), and writes its
-// 4 KiB of integers with one TMA bulk store.  No CTA waits on another: offsets
-// come from the control scan, delta carries from the sums pass.  ~40 warps per
-// SM keep the (deeply queued, ~5 us at 80 % of HBM peak) TMA round trips covered.
+// kModePlain / kModeDelta: what svb_decode_pool_kernel stores; kModeSums: expand_full's
+// sum-only mode (svb_fast.cuh), used by the sums pass and the one-pass decode.
 enum : int { kModePlain = 0, kModeDelta = 1, kModeSums = 2 };
-
-struct __align__(16) TileBuf {
-    uint8_t stage[kWTStage + 16];  // input bytes, then (in place) the sub-tile's integers at +16
-    uint8_t ctrl[kWTGroups];
-};
 
 __device__ __forceinline__ uint32_t warp_sum_u32(uint32_t v) {
 #pragma unroll
     for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(kFull, v, o);
     return v;
-}
-
-// sum of the four bytes of w
-__device__ __forceinline__ uint32_t byte_sum4(uint32_t w) {
-    const uint32_t s = (w & 0x00FF00FFu) + ((w >> 8) & 0x00FF00FFu);
-    return (s & 0xFFFFu) + (s >> 16);
-}
-
-template <int kMode>
-__global__ void __launch_bounds__(kCTThreads, 5)
-    svb_decode_tile_kernel(const uint8_t* __restrict__ in, uint64_t in_len, uint64_t n, uint32_t base,
-                           uint32_t* __restrict__ out, uint32_t* __restrict__ d_last, DecodeMeta meta) {
-    __shared__ __align__(128) TileBuf wb[kCTWarps];
-    __shared__ __align__(16) uint32_t slocal[kCTWarps + 8];         // localpre[sub0 .. sub0+12)
-    __shared__ __align__(16) unsigned long long schunk[4];          // chunkpre[(c & ~1) .. +4)
-    __shared__ __align__(8) uint64_t bars[kCTWarps + 1];
-    __shared__ uint32_t wsum[kCTWarps], wpart[kCTWarps];
-    __shared__ bool last;
-    constexpr bool kDelta = kMode == kModeDelta;
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const uint32_t tile = blockIdx.x;
-    const uint64_t ngroups = (n + 3) >> 2;
-    const uint32_t tail_r = (uint32_t)(n & 3);
-    const uint64_t nsub = (ngroups + kWTGroups - 1) / kWTGroups;
-    const uint64_t sub0 = (uint64_t)tile * kCTWarps;
-    const uint64_t chunk = sub0 / kChunkSubs;
-    const uint32_t nsub_tile = (uint32_t)(nsub - sub0 < (uint64_t)kCTWarps ? nsub - sub0 : (uint64_t)kCTWarps);
-
-    // the CTA's offsets: chunk-local sub-tile prefixes + the chunk's offset (one TMA transaction)
-    if (threadIdx.x == 0) {
-        mbar_init1(&bars[kCTWarps]);
-        mbar_expect(&bars[kCTWarps], 48 + 32);
-        tma_load(slocal, meta.localpre + sub0, 48, &bars[kCTWarps]);
-        tma_load(schunk, meta.chunkpre + (chunk & ~1ull), 32, &bars[kCTWarps]);
-    }
-    if (lane == 0) mbar_init1(&bars[warp]);
-    // delta: this thread's share of the carry (scanned chunk sums + sums of the earlier
-    // sub-tiles of this chunk); the loads fly together with the TMA traffic
-    uint32_t part = 0;
-    if constexpr (kDelta) {
-        const uint64_t c0 = chunk * kChunkSubs;
-        for (uint64_t i = c0 + threadIdx.x; i < sub0; i += kCTThreads) part += __ldg(meta.subsums + i);
-        if (threadIdx.x == 0) part += __ldg(meta.chunksums + chunk);
-    }
-    __syncthreads();
-    mbar_wait_parity(&bars[kCTWarps], 0);
-
-    TileBuf& b = wb[warp];
-    const bool active = (uint32_t)warp < nsub_tile;
-    const uint64_t sub = sub0 + warp;
-    const uint64_t g0 = sub * kWTGroups;
-    uint32_t T[kWTRows];
-    uint32_t wtot = 0;
-    uint32_t* o = out + 4 * g0;
-    const uint32_t nints = active ? (uint32_t)(n - 4 * g0 < (uint64_t)kWTInts ? n - 4 * g0 : (uint64_t)kWTInts) : 0u;
-    if (active) {
-        const unsigned long long cpre = schunk[chunk & 1];
-        const uint32_t li = (uint32_t)(sub - chunk * kChunkSubs);  // index within the chunk
-        const uint64_t off = cpre + slocal[warp];
-        const uint64_t nxt = ((sub + 1) % kChunkSubs == 0 || sub + 1 >= nsub)
-                                 ? (unsigned long long)schunk[(chunk & 1) + 1]
-                                 : cpre + slocal[warp + 1];
-        (void)li;
-        const uint32_t len0 = (uint32_t)(nxt - off);
-        const uint32_t len = len0 > (uint32_t)kWTDataMax ? (uint32_t)kWTDataMax : len0;  // malformed: clamp
-        const uintptr_t lo = (uintptr_t)in, hi = lo + in_len;
-        const uint32_t cnt_g = (uint32_t)(ngroups - g0 < (uint64_t)kWTGroups ? ngroups - g0 : (uint64_t)kWTGroups);
-        const uintptr_t cbeg = lo + g0;
-        const uintptr_t dbeg = lo + ngroups + off;
-        const uint32_t ctx = tma_cover_bytes(cbeg, cbeg + cnt_g, lo, hi);
-        const uint32_t dtx = tma_cover_bytes(dbeg, dbeg + len, lo, hi);
-        const bool c_tma = ctx != 0xFFFFFFFFu && (cbeg & 15) == 0;
-        const bool d_tma = dtx != 0xFFFFFFFFu;
-        const uint32_t expect = (c_tma ? ctx : 0u) + (d_tma ? dtx : 0u);
-        if (lane == 0 && expect) {
-            mbar_expect(&bars[warp], expect);
-            if (c_tma && ctx) tma_load(b.ctrl, reinterpret_cast<const void*>(cbeg), ctx, &bars[warp]);
-            if (d_tma && dtx) tma_load(b.stage, reinterpret_cast<const void*>(dbeg & ~(uintptr_t)15), dtx, &bars[warp]);
-        }
-        if (!c_tma)
-            for (uint32_t i = lane; i < cnt_g; i += 32) b.ctrl[i] = __ldg(in + g0 + i);
-        if (!d_tma) copy_guarded_warp(b.stage, dbeg, dbeg + len, lo, hi);
-        __syncwarp();
-        if (expect) mbar_wait_parity(&bars[warp], 0);
-
-        const WarpCtrl w = load_warp_ctrl<true>(b.ctrl, g0, ngroups, tail_r, g0);
-        const uint32_t* W = reinterpret_cast<const uint32_t*>(b.stage);
-        const uint32_t head = (uint32_t)(dbeg & 15);
-        if constexpr (kMode == kModeSums) {
-            uint32_t acc = 0;
-#pragma unroll
-            for (int j = 0; j < kWTRows; ++j) {
-                const uint32_t c = row_ctrl(w, j);
-                const uint32_t bb = head + row_q(w, j);
-                const uint32_t cnt = group_count(g0 + 32 * j + lane, ngroups, tail_r);
-                if (__all_sync(kFull, c == 0)) {
-                    // four 1-byte integers: their sum is the byte sum of one funnel-shifted word
-                    const uint32_t x = __funnelshift_r(W[bb >> 2], W[(bb >> 2) + 1], (bb & 3u) * 8u);
-                    acc += byte_sum4(x & (cnt >= 4 ? 0xFFFFFFFFu : ((1u << (8 * cnt)) - 1u)));
-                } else {
-                    const uint4 v = mask_tail(decode_group(W, bb, c), cnt);
-                    acc += v.x + v.y + v.z + v.w;
-                }
-            }
-            wtot = warp_sum_u32(acc);
-        } else {
-            // reverse row order: row j's output [16+512j, +512) lies above every
-            // input byte of rows < j (at most 512j bytes from stage+head, head < 16)
-#pragma unroll
-            for (int j = kWTRows - 1; j >= 0; --j) {
-                const uint32_t c = row_ctrl(w, j);
-                const uint32_t bb = head + row_q(w, j);
-                const bool allzero = __all_sync(kFull, c == 0);
-                uint4 v = allzero ? decode_zero_group(W, bb) : decode_group(W, bb, c);
-                if constexpr (kDelta) {
-                    const uint32_t cnt = group_count(g0 + 32 * j + lane, ngroups, tail_r);
-                    v = prefix4(mask_tail(v, cnt));
-                    const uint32_t S = v.w;
-                    const uint32_t I = warp_inclusive_scan(S);
-                    v = add4(v, I - S);
-                    T[j] = __shfl_sync(kFull, I, 31);
-                    wtot += T[j];
-                }
-                __syncwarp();
-                *reinterpret_cast<uint4*>(b.stage + 16 + 512 * j + 16 * lane) = v;
-            }
-        }
-    }
-    if constexpr (kMode == kModeSums) {
-        if (active && lane == 0) {
-            meta.subsums[sub] = wtot;
-            atomicAdd(meta.chunksums + chunk, wtot);  // RED.ADD, mod 2^32
-        }
-        // last CTA: exclusive scan of the chunk sums
-        __syncthreads();
-        if (threadIdx.x == 0) {
-            __threadfence();
-            last = atomicAdd(meta.counters + 1, 1u) == gridDim.x - 1;
-        }
-        __syncthreads();
-        if (!last) return;
-        __threadfence();
-        const uint32_t nchunks = (uint32_t)((nsub + kChunkSubs - 1) / kChunkSubs);
-        cta_exclusive_scan<uint32_t, kCTWarps>(meta.chunksums, nchunks, wsum);
-        if (threadIdx.x == 0) meta.counters[1] = 0;
-        return;
-    }
-    uint32_t carry = 0, csum = 0, sex = 0;
-    if constexpr (kDelta) {
-        part = warp_sum_u32(part);
-        if (lane == 0) {
-            wsum[warp] = wtot;
-            wpart[warp] = part;
-        }
-        __syncthreads();
-        carry = base;
-#pragma unroll
-        for (int k = 0; k < kCTWarps; ++k) {
-            const uint32_t x = wsum[k];
-            sex += k < warp ? x : 0u;
-            csum += x;
-            carry += wpart[k];
-        }
-        if (active) {
-            uint32_t R = carry + sex;
-#pragma unroll
-            for (int j = 0; j < kWTRows; ++j) {
-                uint4* p = reinterpret_cast<uint4*>(b.stage + 16 + 512 * j + 16 * lane);
-                *p = add4(*p, R);
-                R += T[j];
-            }
-        }
-    }
-    if (active) {
-        // one bulk store of the sub-tile's integers (16-B aligned part), lanes store the rest
-        const uint32_t bytes = 4 * nints;
-        const bool o16 = (((uintptr_t)o) & 15) == 0;
-        const uint32_t tbytes = o16 ? (bytes & ~15u) : 0u;
-        fence_async_smem();
-        __syncwarp();
-        if (lane == 0 && tbytes) {
-            tma_store(o, b.stage + 16, tbytes);
-            tma_store_commit();
-        }
-        const uint32_t* src = reinterpret_cast<const uint32_t*>(b.stage + 16);
-        for (uint32_t i = tbytes / 4 + lane; i < nints; i += 32) o[i] = src[i];
-        if (lane == 0 && tbytes) tma_store_wait_read();
-    }
-    if (kDelta && tile == gridDim.x - 1 && threadIdx.x == 0 && d_last) *d_last = carry + csum;
 }
 
 // ---------------------------------------------------------------------------
@@ -487,20 +284,13 @@ __global__ void __launch_bounds__(kCTThreads)
             const unsigned long long so0 = sub_off(i);
             head0 = (uint32_t)(data0 + so0 - (pbase & ~(uintptr_t)15));
         }
-        if ((uint64_t)(s + 1) * kWTInts <= n && head0 <= pool_bytes - 32 && (out16 || kMode == kModeSums)) {
+        if ((uint64_t)(s + 1) * kWTInts <= n && head0 <= pool_bytes - 32 && out16) {
             // full sub-tile: lean path (svb_fast.cuh)
             bool zero;
             const WarpCtrl wf = ctrl_full(sh_addr(sctrl) + i * kWTGroups, &zero);
             const uint32_t sd = sh_addr(pool) + head0;
             uint32_t* o = out + s * kWTInts;
-            if constexpr (kMode == kModeSums) {
-                const uint32_t acc =
-                    warp_sum_u32(zero ? expand_full<2, true>(wf, sd, o, 0) : expand_full<2, false>(wf, sd, o, 0));
-                if (lane == 0) {
-                    meta.subsums[s] = acc;
-                    atomicAdd(meta.chunksums + chunk, acc);  // RED.ADD, mod 2^32
-                }
-            } else if constexpr (kMode == kModeDelta) {
+            if constexpr (kMode == kModeDelta) {
                 const uint32_t run = zero ? expand_full<1, true>(wf, sd, o, sh.carry[i])
                                           : expand_full<1, false>(wf, sd, o, sh.carry[i]);
                 if (s == nsub - 1 && lane == 0 && d_last) *d_last = run;
@@ -518,27 +308,7 @@ __global__ void __launch_bounds__(kCTThreads)
         const uintptr_t sbeg = data0 + so;
         uint32_t head = (uint32_t)(sbeg - (pbase & ~(uintptr_t)15));
         if (head > pool_bytes - 32) head = pool_bytes - 32;  // malformed streams only: keep reads in the pool
-        if constexpr (kMode == kModeSums) {
-            uint32_t acc = 0;
-#pragma unroll
-            for (int j = 0; j < kWTRows; ++j) {
-                const uint32_t c = row_ctrl(w, j);
-                const uint32_t bb = head + row_q(w, j);
-                const uint32_t cnt = group_count(g0 + 32 * j + lane, ngroups, tail_r);
-                if (__all_sync(kFull, c == 0)) {
-                    const uint32_t x = __funnelshift_r(W[bb >> 2], W[(bb >> 2) + 1], (bb & 3u) * 8u);
-                    acc += byte_sum4(x & (cnt >= 4 ? 0xFFFFFFFFu : ((1u << (8 * cnt)) - 1u)));
-                } else {
-                    const uint4 v = mask_tail(decode_group(W, bb, c), cnt);
-                    acc += v.x + v.y + v.z + v.w;
-                }
-            }
-            acc = warp_sum_u32(acc);
-            if (lane == 0) {
-                meta.subsums[s] = acc;
-                atomicAdd(meta.chunksums + chunk, acc);  // RED.ADD, mod 2^32
-            }
-        } else {
+        {
             uint32_t run = kDelta ? sh.carry[i] : 0u;
 #pragma unroll
             for (int j = 0; j < kWTRows; ++j) {
@@ -559,19 +329,6 @@ __global__ void __launch_bounds__(kCTThreads)
             }
             if (kDelta && s == nsub - 1 && lane == 0 && d_last) *d_last = run;
         }
-    }
-    if constexpr (kMode == kModeSums) {
-        __syncthreads();
-        if (threadIdx.x == 0) {
-            __threadfence();
-            single = atomicAdd(meta.counters + 1, 1u) == gridDim.x - 1;  // reuse: "last CTA"
-        }
-        __syncthreads();
-        if (!single) return;
-        __threadfence();
-        const uint32_t nchunks = (uint32_t)((nsub + kChunkSubs - 1) / kChunkSubs);
-        cta_exclusive_scan<uint32_t, kCTWarps>(meta.chunksums, nchunks, sh.part);
-        if (threadIdx.x == 0) meta.counters[1] = 0;
     }
 }
 

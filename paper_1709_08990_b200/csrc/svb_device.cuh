@@ -57,45 +57,6 @@ __device__ __forceinline__ void st_relaxed_gpu(uint64_t* p, uint64_t v) {
     asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
 
-// Decoupled look-back (Merrill & Garland single-pass scan), executed by one
-// full warp: lane l inspects tile (pred - l); waits until all 32 have at least
-// an aggregate, sums back to the nearest inclusive prefix.  Status words of
-// older launches carry a different epoch and read as "not yet published".
-__device__ __forceinline__ uint64_t lookback_exclusive(const uint64_t* status, uint32_t tile, uint32_t epoch) {
-    const int lane = threadIdx.x & 31;
-    uint64_t excl = 0;
-    int64_t pred = (int64_t)tile - 1;
-    while (true) {
-        const int64_t idx = pred - lane;
-        uint32_t flag;
-        uint64_t val;
-        while (true) {
-            if (idx >= 0) {
-                const uint64_t s = ld_relaxed_gpu(status + idx);
-                const bool cur = (uint32_t)(s >> kEpochShift) == epoch;
-                flag = cur ? (uint32_t)((s >> kFlagShift) & 3u) : 0u;
-                val = s & kValueMask;
-            } else {
-                flag = kFlagInclusive;
-                val = 0;
-            }
-            if (__all_sync(kFull, flag != 0)) break;
-            __nanosleep(20);
-        }
-        const unsigned incl = __ballot_sync(kFull, flag == kFlagInclusive);
-        uint64_t contrib = val;
-        if (incl) {
-            const int first = __ffs(incl) - 1;
-            if (lane > first) contrib = 0;
-        }
-#pragma unroll
-        for (int o = 16; o; o >>= 1) contrib += __shfl_xor_sync(kFull, contrib, o);
-        excl += contrib;
-        if (incl) break;
-        pred -= 32;
-    }
-    return excl;
-}
 
 // Status words are spread one per 64 B (kStatusStride u64) so the ~256 newest
 // ones -- which every in-flight look-back polls -- land in many L2 slices
@@ -313,13 +274,6 @@ __device__ __forceinline__ uint64_t l2_policy_drop() {
     uint64_t pol;
     asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
     return pol;
-}
-__device__ __forceinline__ uint4 ldg_hint_v4(const void* p, uint64_t pol) {
-    uint4 v;
-    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.u32 {%0,%1,%2,%3}, [%4], %5;"
-                 : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
-                 : "l"(p), "l"(pol));
-    return v;
 }
 
 __device__ __forceinline__ void stg_hint_v4(void* p, const uint4& v, uint64_t pol) {

@@ -9,11 +9,10 @@
 //   decode block      stream_vbyte.hpp:51-54
 //   chained chunks    codec.hpp:87-90, SPEC.md:555 (segmented batches)
 //
-// Kernel families:
-//   * single array  -- one warp per 1024-integer tile (svb_warp.cuh), tiles in
-//     blockIdx order, byte offsets and delta carries by decoupled look-back.
-//   * batch         -- one warp per segment, tiles walked in order with the
-//     offset and carry in registers (no look-back, no collective).
+// This file: block offsets (decoupled look-back over control-byte lengths),
+// batched random-access block decode, the size-only batch pass, and the batch
+// launchers (the kernels live in svb_batch2.cu; single arrays in svb_decode.cu /
+// svb_encode.cu).
 #include <cstdint>
 
 #include "svb_device.cuh"
@@ -22,80 +21,8 @@
 
 namespace bcgpu {
 
-__device__ __forceinline__ unsigned long long global_ns() {
-    unsigned long long t;
-    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
-    return t;
-}
-// debug trace: 8 timestamps per tile, written by thread 0
-#define BC_TRACE(lb, tile, k)                                                  \
-    do {                                                                       \
-        if ((lb).trace && threadIdx.x == 0) (lb).trace[8 * (tile) + (k)] = global_ns(); \
-    } while (0)
-
 __device__ __forceinline__ void report_status(unsigned long long* st, uint32_t epoch, uint32_t code) {
     if (st) *st = ((unsigned long long)epoch << 32) | code;
-}
-
-// ===========================================================================
-// single-array kernels: CTA look-back tile = 8 warp sub-tiles of 1024 integers
-// ===========================================================================
-// Each warp decodes its own 1024-integer sub-tile (svb_warp.cuh); the CTA's
-// 8192 integers share one look-back status word per quantity, so the chip has
-// ~600 look-back tiles in flight instead of ~4700, which the 256-wide
-// look-back resolves in one or two round trips.
-struct CtaShared {
-    uint32_t tot[kCTWarps];  // per-warp data bytes
-    uint32_t sum[kCTWarps];  // per-warp delta sums
-    unsigned long long off, carry;
-};
-
-// exclusive prefix of this warp within the CTA + CTA total, from a per-warp smem array
-__device__ __forceinline__ uint32_t cta_warp_prefix(const uint32_t* a, int warp, uint32_t* total) {
-    uint32_t ex = 0, t = 0;
-#pragma unroll
-    for (int k = 0; k < kCTWarps; ++k) {
-        const uint32_t x = a[k];
-        ex += k < warp ? x : 0u;
-        t += x;
-    }
-    *total = t;
-    return ex;
-}
-
-template <bool kDelta>
-__global__ void __launch_bounds__(kCTThreads, 4)
-    svb_encode_ct_kernel(const uint32_t* __restrict__ in, uint64_t n, uint32_t prev, uint8_t* __restrict__ out,
-                         uint64_t* __restrict__ d_out_len, LookbackArgs lb) {
-    __shared__ __align__(128) uint8_t stage_all[kCTWarps][kWTStage];
-    __shared__ CtaShared sh;
-    const int warp = threadIdx.x >> 5;
-    const uint32_t tile = blockIdx.x;
-    uint8_t* stage = stage_all[warp];
-    const uint64_t ngroups = (n + 3) >> 2;
-    const uint32_t tail_r = (uint32_t)(n & 3);
-    const uint64_t g0 = (uint64_t)tile * kCTGroups + (uint64_t)warp * kWTGroups;
-    uint32_t prev_in = prev;
-    if (kDelta && g0 != 0 && g0 < ngroups) prev_in = __ldg(in + 4 * g0 - 1);
-    EncodeTile t;
-    encode_load<kDelta>(in, g0, ngroups, tail_r, prev_in, out, t);
-    if ((threadIdx.x & 31) == 0) sh.tot[warp] = t.total;
-    encode_pack(t, stage);
-    __syncthreads();
-    uint32_t ctot;
-    const uint32_t wex = cta_warp_prefix(sh.tot, warp, &ctot);
-    if (warp == 0) {
-        lb_publish(lb.off_status, tile, lb.epoch, 0, ctot);
-        const uint64_t off = lb_resolve(lb.off_status, tile, lb.epoch, 0, ctot);
-        if ((threadIdx.x & 31) == 0) sh.off = off;
-    }
-    __syncthreads();
-    const uint64_t cta_off = sh.off;
-    encode_writeout(stage, (uintptr_t)out + ngroups + cta_off + wex, t.total);
-    if (tile == lb.num_tiles - 1 && threadIdx.x == 0) {
-        if (d_out_len) *d_out_len = ngroups + cta_off + ctot;
-        report_status(lb.status, lb.epoch, 0u);
-    }
 }
 
 // ===========================================================================
@@ -205,90 +132,6 @@ __device__ __forceinline__ SegDesc load_desc_warp(const void* segs, uint64_t s) 
     return d;
 }
 
-// ===========================================================================
-// batch kernels: one warp per segment, tiles in order, state in registers
-// ===========================================================================
-template <bool kDelta>
-__global__ void __launch_bounds__(kWTThreads, 8)
-    svb_decode_batch_kernel(const bcgpu_decode_segment* __restrict__ segs, uint64_t nseg,
-                            const uint8_t* __restrict__ in, uint32_t* __restrict__ out, unsigned long long* status,
-                            uint32_t epoch) {
-    __shared__ __align__(128) uint8_t stage_all[kWTWarps][kWTStage];
-    __shared__ __align__(8) uint64_t bars[kWTWarps];
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    uint8_t* stage = stage_all[warp];
-    uint64_t* bar = &bars[warp];
-    if (lane == 0) mbar_init(bar, 1);
-    __syncwarp();
-    uint32_t phase = 0;
-    bool used = false;
-    const uint64_t gw = (uint64_t)blockIdx.x * kWTWarps + warp, nw = (uint64_t)gridDim.x * kWTWarps;
-    for (uint64_t s = gw; s < nseg; s += nw) {
-        const SegDesc d = load_desc_warp(segs, s);
-        const uint64_t ngroups = ((uint64_t)d.n + 3) >> 2;
-        const uint32_t tail_r = d.n & 3u;
-        if (d.b < ngroups) {
-            if (lane == 0) report_status(status, epoch, BCGPU_ERR_TRUNCATED);
-            continue;
-        }
-        const uint8_t* seg = in + d.a;
-        uint32_t* o = out + d.c;
-        const bool out16 = (((uintptr_t)o) & 15) == 0;
-        const uintptr_t lo = (uintptr_t)seg, hi = lo + d.b;
-        uint64_t off = 0;
-        uint32_t carry = d.prev;
-        for (uint64_t g0 = 0; g0 < ngroups; g0 += kWTGroups) {
-            const WarpCtrl w = load_warp_ctrl(seg, g0, ngroups, tail_r);
-            const uintptr_t beg = lo + ngroups + off;
-            __syncwarp();  // every lane is done reading the previous tile from stage
-            stage_tile(stage, bar, phase, beg, beg + w.total, lo, hi, used);
-            used = true;
-            uint4 vv[kWTRows];
-            const uint32_t tsum = expand_tile<kDelta>(w, stage, (uint32_t)(beg & 15), g0, ngroups, tail_r, o, out16, vv);
-            if constexpr (kDelta) {
-                store_tile<kDelta>(vv, carry, g0, ngroups, tail_r, o, out16);
-                carry += tsum;
-            }
-            off += w.total;
-        }
-        if (lane == 0 && ngroups + off != d.b)
-            report_status(status, epoch, ngroups + off > d.b ? BCGPU_ERR_TRUNCATED : BCGPU_ERR_TRAILING_BYTES);
-    }
-}
-
-template <bool kDelta>
-__global__ void __launch_bounds__(kWTThreads, 8)
-    svb_encode_batch_kernel(const bcgpu_encode_segment* __restrict__ segs, uint64_t nseg,
-                            const uint32_t* __restrict__ in, uint8_t* __restrict__ out,
-                            uint64_t* __restrict__ out_lens, unsigned long long* status, uint32_t epoch) {
-    __shared__ __align__(128) uint8_t stage_all[kWTWarps][kWTStage];
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    uint8_t* stage = stage_all[warp];
-    const uint64_t gw = (uint64_t)blockIdx.x * kWTWarps + warp, nw = (uint64_t)gridDim.x * kWTWarps;
-    for (uint64_t s = gw; s < nseg; s += nw) {
-        const SegDesc e = load_desc_warp(segs, s);
-        const uint64_t ngroups = ((uint64_t)e.n + 3) >> 2;
-        if (e.b < ngroups + 4ull * e.n) {
-            if (lane == 0) report_status(status, epoch, BCGPU_ERR_INVALID_ARGUMENT);
-            continue;
-        }
-        const uint32_t* src = in + e.a;
-        uint8_t* dst = out + e.c;
-        uint64_t off = 0;
-        for (uint64_t g0 = 0; g0 < ngroups; g0 += kWTGroups) {
-            const uint32_t prev_in = (kDelta && g0 != 0) ? __ldg(src + 4 * g0 - 1) : e.prev;
-            EncodeTile t;
-            encode_load<kDelta>(src, g0, ngroups, e.n & 3u, prev_in, dst, t);
-            __syncwarp();  // previous tile's write-out finished reading stage
-            encode_pack(t, stage);
-            __syncwarp();
-            encode_writeout(stage, (uintptr_t)dst + ngroups + off, t.total);
-            off += t.total;
-        }
-        if (lane == 0) out_lens[s] = ngroups + off;
-    }
-}
-
 // -------- size-only pass, warp per segment
 template <bool kDelta>
 __global__ void __launch_bounds__(kThreads) svb_sizes_batch_kernel(const bcgpu_encode_segment* __restrict__ segs,
@@ -315,15 +158,6 @@ __global__ void __launch_bounds__(kThreads) svb_sizes_batch_kernel(const bcgpu_e
 // ===========================================================================
 // launchers
 // ===========================================================================
-cudaError_t launch_encode(const uint32_t* in, uint64_t n, int delta, uint32_t prev, uint8_t* out,
-                          uint64_t* d_out_len, const LookbackArgs& lb, cudaStream_t stream) {
-    if (delta)
-        svb_encode_ct_kernel<true><<<lb.num_tiles, kCTThreads, 0, stream>>>(in, n, prev, out, d_out_len, lb);
-    else
-        svb_encode_ct_kernel<false><<<lb.num_tiles, kCTThreads, 0, stream>>>(in, n, prev, out, d_out_len, lb);
-    return cudaGetLastError();
-}
-
 cudaError_t launch_block_offsets(const uint8_t* in, uint64_t n, uint64_t* d_offsets, const LookbackArgs& lb,
                                  cudaStream_t stream) {
     svb_block_offsets_kernel<<<(int)lb.num_tiles, kThreads, 0, stream>>>(in, n, d_offsets, lb);
@@ -344,41 +178,17 @@ static int occ_of(const void* k, int threads) {
     return occ;
 }
 
-int occupancy_batch() {
-    const int a = occ_of((const void*)svb_decode_batch_kernel<true>, kWTThreads);
-    const int b = occ_of((const void*)svb_encode_batch_kernel<true>, kWTThreads);
-    return a < b ? a : b;
-}
+int occupancy_batch() { return occ_of((const void*)svb_sizes_batch_kernel<true>, kThreads) * kWarps / kWTWarps; }
 
-static int batch_grid(uint64_t nseg, int grid_cap) {
-    const uint64_t want = (nseg + kWTWarps - 1) / kWTWarps;
-    return (int)(want < (uint64_t)grid_cap ? want : (uint64_t)grid_cap);
-}
-
+// decode / encode batches: the warp-pipelined kernels of svb_batch2.cu
 cudaError_t launch_decode_batch(const bcgpu_decode_segment* segs, uint64_t nseg, const uint8_t* in, uint32_t* out,
                                 int delta, const BatchArgs& ba, cudaStream_t stream) {
-    if (!(ba.flags & (64 | 256))) return launch_decode_batch2(segs, nseg, in, out, delta, ba, stream);
-    const int grid = batch_grid(nseg, ba.grid);
-    if (grid <= 0) return cudaSuccess;
-    if (delta)
-        svb_decode_batch_kernel<true><<<grid, kWTThreads, 0, stream>>>(segs, nseg, in, out, ba.status, ba.epoch);
-    else
-        svb_decode_batch_kernel<false><<<grid, kWTThreads, 0, stream>>>(segs, nseg, in, out, ba.status, ba.epoch);
-    return cudaGetLastError();
+    return launch_decode_batch2(segs, nseg, in, out, delta, ba, stream);
 }
 
 cudaError_t launch_encode_batch(const bcgpu_encode_segment* segs, uint64_t nseg, const uint32_t* in, uint8_t* out,
                                 uint64_t* out_lens, int delta, const BatchArgs& ba, cudaStream_t stream) {
-    if (!(ba.flags & 64)) return launch_encode_batch2(segs, nseg, in, out, out_lens, delta, ba, stream);
-    const int grid = batch_grid(nseg, ba.grid);
-    if (grid <= 0) return cudaSuccess;
-    if (delta)
-        svb_encode_batch_kernel<true><<<grid, kWTThreads, 0, stream>>>(segs, nseg, in, out, out_lens, ba.status,
-                                                                        ba.epoch);
-    else
-        svb_encode_batch_kernel<false><<<grid, kWTThreads, 0, stream>>>(segs, nseg, in, out, out_lens, ba.status,
-                                                                         ba.epoch);
-    return cudaGetLastError();
+    return launch_encode_batch2(segs, nseg, in, out, out_lens, delta, ba, stream);
 }
 
 cudaError_t launch_sizes_batch(const bcgpu_encode_segment* segs, uint64_t nseg, const uint32_t* in,

@@ -63,10 +63,6 @@ cudaError_t launch_encode_piece(const uint32_t* in, uint64_t n, int delta, uint3
                                 uint32_t c0, uint32_t c1, cudaStream_t stream);
 unsigned long long* encode_running_ptr(void* meta_ws, uint64_t n);
 uint64_t encode_slot_bytes(uint64_t n);
-uint32_t decode2_chunks(uint64_t n);  // look-back tiles of the offsets pre-pass
-uint32_t decode2_tiles(uint64_t n);   // look-back tiles (CTAs) of the tile decode
-cudaError_t launch_encode(const uint32_t* in, uint64_t n, int delta, uint32_t prev, uint8_t* out,
-                          uint64_t* d_out_len, const LookbackArgs& lb, cudaStream_t stream);
 cudaError_t launch_block_offsets(const uint8_t* in, uint64_t n, uint64_t* d_offsets, const LookbackArgs& lb,
                                  cudaStream_t stream);
 
@@ -78,7 +74,7 @@ struct BatchArgs {
     unsigned long long* status;  // [epoch:32 | bcgpu_status:32]
     uint32_t epoch;
     int grid;                    // CTAs of the warp-per-segment kernels (full residency)
-    uint32_t flags = 0;          // debug flags of the ctx (64: the unpipelined batch kernels, 256: old decode)
+    uint32_t flags = 0;          // debug flags of the ctx (bits 12..14: batch-decode CTAs per SM)
 };
 
 cudaError_t launch_decode_batch(const bcgpu_decode_segment* segs, uint64_t nseg, const uint8_t* in, uint32_t* out,
@@ -98,9 +94,7 @@ cudaError_t launch_encode_batch2(const bcgpu_encode_segment* segs, uint64_t nseg
 // CTAs per SM of the batch kernels, for grid sizing.
 int occupancy_batch();
 
-// Control bytes per look-back tile of each single-array kernel.
-constexpr uint32_t kDecodeTileGroups = 2048;  // CTA tile of 8 warp sub-tiles (svb_warp.cuh kCTGroups)
-constexpr uint32_t kEncodeTileGroups = 2048;
-constexpr uint32_t kOffsetsTileGroups = 2048;  // CTA tile (kTileGroups)
+// Control bytes per look-back tile of the block-offsets kernel.
+constexpr uint32_t kOffsetsTileGroups = 2048;
 
 }  // namespace bcgpu
