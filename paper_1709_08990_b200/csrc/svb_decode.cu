@@ -74,6 +74,9 @@ __global__ void __launch_bounds__(256)
     const uint64_t ngroups = (n + 3) >> 2;
     const uint32_t tail_r = (uint32_t)(n & 3);
     const uint64_t nsub = (ngroups + kWTGroups - 1) / kWTGroups;
+    // the next kernel (programmatic dependent launch) may start its prologue now; it waits
+    // for this grid's completion before reading anything written here
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     if (zero_sums && tid == 0) meta.chunksums[chunk] = 0;
     // delta: clear this chunk's one-pass aggregates, so nothing stale can carry the call's epoch
     if (zero_sums && tid < kChunkSubs / kCTWarps) {
@@ -568,18 +571,22 @@ __global__ void __launch_bounds__(kSumThreads)
 //   1. sum their sub-tiles straight from the staged bytes (dp4a for all-zero
 //      control bytes, as the sums pass) and publish the tile sum A(t) as an
 //      epoch-tagged aggregate (relaxed 64-bit store);
-//   2. resolve the carry of the CTA's previous tile tp = t - G, deferred by one
-//      round: carry(tp) = incl(tp - G) + sum of A(j), tp - G < j < tp -- its own
-//      inclusive prefix from two rounds back plus the aggregates of the G - 1
-//      tiles in between, all published a round or more earlier (their loads were
-//      issued at the top of the iteration, so their latency hides behind step 1);
-//   3. decode tile tp from its stage -- held one extra round -- with that carry,
-//      store it from registers, and release the stage.
+//   2. resolve the carry of the CTA's tile tp = t - kD1Lag*G, deferred by kD1Lag
+//      rounds: carry(tp) = incl(tp - G) + sum of A(j), tp - G < j < tp -- its own
+//      inclusive prefix from the round before plus the aggregates of the G - 1
+//      tiles in between, all published kD1Lag - 1 rounds or more earlier (their
+//      loads were issued at the top of the iteration, so their latency hides behind
+//      step 1).  Two rounds of lag let a CTA run a full round ahead of a slow one
+//      before it has to wait on it (with one, the resolve spun on the previous
+//      round's aggregates and the CTA stalled at the next named barrier);
+//   3. decode tile tp from its stage -- held kD1Lag extra rounds -- with that
+//      carry, store it from registers, and release the stage.
 // The compressed bytes are read from HBM once (the stage is re-read from smem).
 // A round-r aggregate only depends on waits for rounds <= r - 1, so with every
 // CTA resident the chain cannot deadlock.  Only aggregates are shared; every CTA
 // keeps its own inclusive chain.
-constexpr int kD1Stages = 5;  // tiles t and t - G held, the rest in flight
+constexpr int kD1Lag = 2;     // tile t is resolved kD1Lag rounds after it is summed
+constexpr int kD1Stages = 6;  // tiles t, t - G, ..., t - kD1Lag*G held, the rest in flight
 
 struct __align__(16) D1Shared {
     SumMeta meta[kD1Stages];
@@ -652,6 +659,9 @@ __global__ void __launch_bounds__(kSumThreads, 3)
         sh.incl = base;
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
+    // launched as a programmatic dependent of the control scan: its offsets (and the
+    // cleared aggregates) are visible after this
+    asm volatile("griddepcontrol.wait;" ::: "memory");
     __syncthreads();
     if (warp == kCTWarps) {
         // ---- producer (as in svb_sums_kernel) ----
@@ -715,27 +725,32 @@ __global__ void __launch_bounds__(kSumThreads, 3)
     }
     // ---- consumers ----
     const int ct = threadIdx.x;  // 0..255
-    // look-back window of tile tp: tiles max(0, tp - G + 1) .. tp - 1; two entries per
-    // thread prefetched, any more read at resolve time
+    // look-back window of tile tp: tiles max(0, tp - G + 1) .. tp - 1, read as 16-B aligned
+    // pairs (2e, 2e + 1); each thread prefetches one pair, any more are read at resolve time
     auto window_lo = [&](uint32_t tp) -> uint32_t { return tp + 1 > G ? tp + 1 - G : 0u; };
-    unsigned long long pf0 = 0, pf1 = 0;
+    ulonglong2 pf = make_ulonglong2(0ull, 0ull);
     auto prefetch = [&](uint32_t tp) {
-        const uint32_t wl = window_lo(tp);
-        pf0 = wl + ct < tp ? ld_relaxed_u64(meta.agg + wl + ct) : 0ull;
-        pf1 = wl + ct + 256 < tp ? ld_relaxed_u64(meta.agg + wl + ct + 256) : 0ull;
+        const uint32_t e = (window_lo(tp) & ~1u) + 2u * (uint32_t)ct;
+        if (e < tp) pf = ld_relaxed_u64x2(meta.agg + e);
     };
     auto entry = [&](uint32_t j, unsigned long long v) -> uint32_t {  // tile j's aggregate of this call
         while ((uint32_t)(v >> 32) != epoch) v = ld_relaxed_u64(meta.agg + j);
         return (uint32_t)v;
     };
+    auto pair_sum = [&](uint32_t e, ulonglong2 v, uint32_t wl, uint32_t tp) -> uint32_t {
+        uint32_t r = 0;
+        if (e >= wl) r += entry(e, v.x);
+        if (e + 1 < tp) r += entry(e + 1, v.y);
+        return r;
+    };
     // resolve tile tp (its sub-tile sums in wsum[q]), decode it from stage st with the carry,
-    // store it and release the stage
-    auto resolve = [&](uint32_t tp, int st, int q) {
+    // store it and release the stage; zero: the sum pass found this warp's control bytes all 0
+    auto resolve = [&](uint32_t tp, int st, int q, bool zero) {
         const uint32_t wl = window_lo(tp);
         uint32_t part = 0;
-        if (wl + ct < tp) part += entry(wl + ct, pf0);
-        if (wl + ct + 256 < tp) part += entry(wl + ct + 256, pf1);
-        for (uint32_t j = wl + ct + 512; j < tp; j += 256) part += entry(j, ld_relaxed_u64(meta.agg + j));
+        const uint32_t e0 = (wl & ~1u) + 2u * (uint32_t)ct;
+        if (e0 < tp) part += pair_sum(e0, pf, wl, tp);
+        for (uint32_t e = e0 + 512; e < tp; e += 512) part += pair_sum(e, ld_relaxed_u64x2(meta.agg + e), wl, tp);
         part = __reduce_add_sync(kFull, part);
         if (lane == 0) sh.red[warp] = part;
         consumers_sync();
@@ -769,10 +784,15 @@ __global__ void __launch_bounds__(kSumThreads, 3)
             uint32_t run;
             if (sh.hdr[st].mode == 0 && (s + 1) * kWTInts <= n && head <= pool_bytes - 32 &&
                 (((uintptr_t)o) & 15) == 0) {
-                bool zero;
-                const WarpCtrl wf = ctrl_full(sh_addr(sc), &zero);
                 const uint32_t sd = sh_addr(pool) + head;
-                run = zero ? expand_full<1, true>(wf, sd, o, E) : expand_full<1, false>(wf, sd, o, E);
+                if (zero) {
+                    WarpCtrl wz;
+                    run = expand_full<1, true>(wz, sd, o, E);
+                } else {
+                    bool z;
+                    const WarpCtrl wf = ctrl_full(sh_addr(sc), &z);
+                    run = expand_full<1, false>(wf, sd, o, E);
+                }
             } else if (sh.hdr[st].mode == 0) {
                 const uint32_t* W = reinterpret_cast<const uint32_t*>(pool);
                 const uint32_t lim = pool_bytes / 4 - 1;
@@ -791,12 +811,15 @@ __global__ void __launch_bounds__(kSumThreads, 3)
         if (lane == 0) mbar_arrive(&sh.empty[st]);  // tile tp is decoded: its stage is free
     };
 
+    // the tile of iteration i is blockIdx.x + i * G; iteration k resolves iteration k - kD1Lag's
     uint32_t k = 0;
-    uint32_t tprev = 0;
-    for (uint32_t t = blockIdx.x; t < ntiles; t += G, ++k) {
+    const uint32_t b0 = blockIdx.x;
+    uint32_t zbits = 0;  // bit i: the warp's sub-tile of iteration k - i had all-zero control bytes
+    for (uint32_t t = b0; t < ntiles; t += G, ++k) {
         const int st = (int)(k % kD1Stages);
         const uint32_t ph = (k / kD1Stages) & 1u;
-        if (k) prefetch(tprev);
+        zbits <<= 1;
+        if (k >= (uint32_t)kD1Lag) prefetch(t - kD1Lag * G);
         if (meta.trace && ct == 0) meta.trace[8ull * t + 1] = gtimer();
         mbar_wait_parity(&sh.full[st], ph);
         if (meta.trace && ct == 0) meta.trace[8ull * t + 2] = gtimer();
@@ -811,6 +834,7 @@ __global__ void __launch_bounds__(kSumThreads, 3)
                 if ((s + 1) * kWTInts <= n && head <= pool_bytes - 32) {
                     const uint32_t sd = sh_addr(pool) + head;
                     if (ctrl_all_zero(sh_addr(sc))) {
+                        zbits |= 1u;
                         sum = __reduce_add_sync(kFull, zero_tile_sum(sd));
                     } else {
                         bool zero;
@@ -837,12 +861,14 @@ __global__ void __launch_bounds__(kSumThreads, 3)
             st_relaxed_u64(meta.agg + t, ((unsigned long long)epoch << 32) | a);
             if (meta.trace) meta.trace[8ull * t + 3] = gtimer();
         }
-        if (k) resolve(tprev, (int)((k - 1) % kD1Stages), (int)((k - 1) % 3));
-        tprev = t;
+        if (k >= (uint32_t)kD1Lag) {
+            const uint32_t i = k - kD1Lag;
+            resolve(t - kD1Lag * G, (int)(i % kD1Stages), (int)(i % 3), (zbits >> kD1Lag) & 1u);
+        }
     }
-    if (k) {
-        prefetch(tprev);
-        resolve(tprev, (int)((k - 1) % kD1Stages), (int)((k - 1) % 3));
+    for (uint32_t i = k > (uint32_t)kD1Lag ? k - kD1Lag : 0u; i < k; ++i) {
+        prefetch(b0 + i * G);
+        resolve(b0 + i * G, (int)(i % kD1Stages), (int)(i % 3), (zbits >> (k - 1 - i)) & 1u);
     }
 }
 
@@ -884,8 +910,19 @@ static cudaError_t launch_decode1(const uint8_t* in, uint64_t in_len, uint64_t n
     uint32_t pb = (uint32_t)pool;
     void* args[] = {(void*)&in, (void*)&in_len, (void*)&n,  (void*)&base, (void*)&out,
                     (void*)&d_last, (void*)&mm, (void*)&pb, (void*)&epoch};
-    const cudaError_t e = cudaLaunchCooperativeKernel((const void*)svb_decode1_kernel, dim3((unsigned)grid),
-                                                      dim3(kSumThreads), args, smem, stream);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)grid);
+    cfg.blockDim = dim3(kSumThreads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = stream;
+    cudaLaunchAttribute attr[2];
+    attr[0].id = cudaLaunchAttributeCooperative;
+    attr[0].val.cooperative = 1;
+    attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;  // overlap the control scan's tail
+    attr[1].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 2;
+    const cudaError_t e = cudaLaunchKernelExC(&cfg, (const void*)svb_decode1_kernel, args);
     if (e == cudaSuccess) *used = true;
     return e;
 }
@@ -1041,6 +1078,10 @@ cudaError_t launch_decode3(const uint8_t* in, uint64_t in_len, uint64_t n, int d
     (void)pipe_grid;
     cudaError_t e = launch_decode_ctrl(in, in_len, n, delta, meta_ws, status, epoch, stream);
     if (e != cudaSuccess) return e;
+    if (debug_flags & 0x8000) {  // dev timing: the control scan alone
+        *launches = 1;
+        return cudaSuccess;
+    }
     const uint64_t ngroups = (n + 3) >> 2;
     const uint64_t nsub = (ngroups + kWTGroups - 1) / kWTGroups;
     int l = 0;

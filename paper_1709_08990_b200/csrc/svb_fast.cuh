@@ -110,7 +110,8 @@ __device__ __forceinline__ uint32_t ones_below(int k) {
 }
 
 // Per-lane part of the byte sum of the 1024 shared bytes at sd (any alignment): the sum of
-// a sub-tile's integers when every control byte is 0.  Lane l reads 16-B chunks l, l+32.
+// a sub-tile's integers when every control byte is 0 (callers reduce over the warp).  Lane l
+// reads 16-B chunks l, l+32; reads up to 16 bytes past the sub-tile when sd is unaligned.
 __device__ __forceinline__ uint32_t zero_tile_sum(uint32_t sd) {
     const int lane = threadIdx.x & 31;
     const uint32_t a0 = sd & ~15u;
@@ -124,12 +125,10 @@ __device__ __forceinline__ uint32_t zero_tile_sum(uint32_t sd) {
         acc = __dp4a(v.z, 0x01010101u, acc);
         acc = __dp4a(v.w, 0x01010101u, acc);
     }
-    if (lane == 0 && s) {  // chunk 0's first s bytes precede the sub-tile, chunk 64's belong to it
-        const uint4 f = lds128(a0), t = lds128(a0 + 1024u);
-        acc = __dp4a(t.x, ones_below(s), acc) - __dp4a(f.x, ones_below(s), 0u);
-        acc = __dp4a(t.y, ones_below(s - 4), acc) - __dp4a(f.y, ones_below(s - 4), 0u);
-        acc = __dp4a(t.z, ones_below(s - 8), acc) - __dp4a(f.z, ones_below(s - 8), 0u);
-        acc = __dp4a(t.w, ones_below(s - 12), acc) - __dp4a(f.w, ones_below(s - 12), 0u);
+    if (s) {  // chunk 0's first s bytes precede the sub-tile, chunk 64's belong to it: lanes 0-3 fix word `lane`
+        const uint32_t sel = lane < 4 ? ones_below(s - 4 * lane) : 0u;
+        const uint32_t wa = a0 + 4u * (uint32_t)(lane & 3);
+        acc = __dp4a(lds32(wa + 1024u), sel, acc) - __dp4a(lds32(wa), sel, 0u);
     }
     return acc;
 }

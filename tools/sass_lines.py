@@ -1,13 +1,14 @@
 """Dev tool: dynamic instruction counts per source line for one kernel.
 Joins an ncu source-page SASS csv (Instructions Executed per address) with nvdisasm -g
-line info.  Usage: python tools/sass_lines.py NCU_SASS_CSV NVDISASM_OUT KERNEL_SUBSTR MANGLED_PREFIX UNITS"""
+line info.  Usage: python tools/sass_lines.py NCU_SASS_CSV NVDISASM_OUT KERNEL_SUBSTR MANGLED_PREFIX UNITS [COLUMN]
+(COLUMN defaults to "Instructions Executed"; e.g. "Warp Stall Sampling (All Samples)", "stall_long_sb")."""
 import collections
 import csv
 import re
 import sys
 
 
-def main(csv_path, sass_path, kname, mangled, units):
+def main(csv_path, sass_path, kname, mangled, units, col="Instructions Executed"):
     rows = list(csv.reader(open(csv_path)))
     secs, cur = [], None
     for r in rows:
@@ -19,7 +20,7 @@ def main(csv_path, sass_path, kname, mangled, units):
             cur["rows"].append(r)
     sec = [s for s in secs if kname in s["name"]][0]
     h, data = sec["rows"][0], sec["rows"][1:]
-    ia, iex = h.index("Address"), h.index("Instructions Executed")
+    ia, iex = h.index("Address"), h.index(col)
     base = min(int(r[ia], 16) for r in data)
     ex = {int(r[ia], 16) - base: float(r[iex] or 0) for r in data}
     lines, curl, inside = {}, None, False
@@ -53,4 +54,4 @@ def main(csv_path, sass_path, kname, mangled, units):
 
 
 if __name__ == "__main__":
-    main(sys.argv[1], sys.argv[2], sys.argv[3], sys.argv[4], float(sys.argv[5]))
+    main(sys.argv[1], sys.argv[2], sys.argv[3], sys.argv[4], float(sys.argv[5]), *sys.argv[6:7])
