@@ -634,6 +634,7 @@ __device__ __forceinline__ uint32_t decode_generic_store(const uint8_t* sctrl, u
     return run;
 }
 
+template <bool kTrace>
 __global__ void __launch_bounds__(kSumThreads, 3)
     svb_decode1_kernel(const uint8_t* __restrict__ in, uint64_t in_len, uint64_t n, uint32_t base,
                        uint32_t* __restrict__ out, uint32_t* __restrict__ d_last, DecodeMeta meta, uint32_t pool_bytes,
@@ -677,9 +678,9 @@ __global__ void __launch_bounds__(kSumThreads, 3)
                 if (t < ntiles) issue_meta((uint32_t)t, i);
             }
         uint32_t k = 0;
-        for (uint32_t t = blockIdx.x; t < ntiles; t += G, ++k) {
-            const int st = (int)(k % kD1Stages);
-            const uint32_t ph = (k / kD1Stages) & 1u;
+        int st = 0;
+        uint32_t ph = 0;
+        for (uint32_t t = blockIdx.x; t < ntiles; t += G, ++k, st = st + 1 == kD1Stages ? 0 : st + 1, ph ^= st == 0) {
             uint8_t* sc = dsm + (uint32_t)st * stride;
             uint8_t* pool = sc + kTileCtrl;
             const uint64_t s0 = (uint64_t)t * kCTWarps, chunk = s0 / kChunkSubs;
@@ -701,7 +702,7 @@ __global__ void __launch_bounds__(kSumThreads, 3)
             const uint32_t ctx = tma_cover_bytes(cb, cb + cg, lo, hi);
             const bool c_tma = ctx != 0xFFFFFFFFu && (cb & 15) == 0;
             __syncwarp();
-            if (k >= (uint32_t)kD1Stages) mbar_wait_parity(&sh.empty[st], ph ^ 1u);
+            if (k >= (uint32_t)kD1Stages) mbar_wait_parity_sleep(&sh.empty[st], ph ^ 1u);
             if (!c_tma)
                 for (uint32_t i = lane; i < (uint32_t)cg; i += 32) sc[i] = __ldg(in + s0 * kWTGroups + i);
             if (lane <= 8) sh.hdr[st].head[lane] = (uint32_t)(data0 + my - bse);
@@ -714,7 +715,7 @@ __global__ void __launch_bounds__(kSumThreads, 3)
                 fence_async_smem();
                 mbar_expect(&sh.full[st], (c_tma ? ctx : 0u) + (fits ? tx : 0u));
                 const uint64_t pol = l2_policy_drop();
-                if (meta.trace) meta.trace[8ull * t + 0] = gtimer();
+                if (kTrace) meta.trace[8ull * t + 0] = gtimer();
                 if (c_tma && ctx) tma_load_hint(sc, reinterpret_cast<const void*>(cb), ctx, &sh.full[st], pol);
                 if (fits && tx) tma_load_hint(pool, reinterpret_cast<const void*>(bse), tx, &sh.full[st], pol);
                 const uint64_t tn = (uint64_t)t + (uint64_t)kD1Stages * G;
@@ -754,7 +755,7 @@ __global__ void __launch_bounds__(kSumThreads, 3)
         part = __reduce_add_sync(kFull, part);
         if (lane == 0) sh.red[warp] = part;
         consumers_sync();
-        if (meta.trace && ct == 0) meta.trace[8ull * tp + 4] = gtimer();
+        if (kTrace && ct == 0) meta.trace[8ull * tp + 4] = gtimer();
         if (ct == 0) {
             uint32_t x = 0, a = 0;
 #pragma unroll
@@ -773,16 +774,16 @@ __global__ void __launch_bounds__(kSumThreads, 3)
             }
         }
         consumers_sync();
-        const uint64_t s = (uint64_t)tp * kCTWarps + warp;
+        const uint32_t s = tp * kCTWarps + warp;  // < 2^32: ntiles is 32-bit
         if (s < nsub) {
             const uint32_t E = sh.wcarry[warp];
-            const uint64_t g0 = s * kWTGroups;
+            const uint64_t g0 = (uint64_t)s * kWTGroups;
             const uint8_t* sc = dsm + (uint32_t)st * stride + warp * kWTGroups;
             const uint8_t* pool = dsm + (uint32_t)st * stride + kTileCtrl;
             const uint32_t head = sh.hdr[st].head[warp];
             uint32_t* o = out + 4 * g0;
             uint32_t run;
-            if (sh.hdr[st].mode == 0 && (s + 1) * kWTInts <= n && head <= pool_bytes - 32 &&
+            if (sh.hdr[st].mode == 0 && (uint64_t)(s + 1) * kWTInts <= n && head <= pool_bytes - 32 &&
                 (((uintptr_t)o) & 15) == 0) {
                 const uint32_t sd = sh_addr(pool) + head;
                 if (zero) {
@@ -804,10 +805,10 @@ __global__ void __launch_bounds__(kSumThreads, 3)
                                            [&](uint32_t i) { return gword_guarded(gb + 4 * (uintptr_t)i, lo, hi); }, E,
                                            out);
             }
-            if (s == nsub - 1 && lane == 0 && d_last) *d_last = run;
+            if (d_last && s + 1 == nsub && lane == 0) *d_last = run;
         }
         __syncwarp();
-        if (meta.trace && ct == 0) meta.trace[8ull * tp + 5] = gtimer();
+        if (kTrace && ct == 0) meta.trace[8ull * tp + 5] = gtimer();
         if (lane == 0) mbar_arrive(&sh.empty[st]);  // tile tp is decoded: its stage is free
     };
 
@@ -815,14 +816,15 @@ __global__ void __launch_bounds__(kSumThreads, 3)
     uint32_t k = 0;
     const uint32_t b0 = blockIdx.x;
     uint32_t zbits = 0;  // bit i: the warp's sub-tile of iteration k - i had all-zero control bytes
-    for (uint32_t t = b0; t < ntiles; t += G, ++k) {
-        const int st = (int)(k % kD1Stages);
-        const uint32_t ph = (k / kD1Stages) & 1u;
+    int st = 0, q = 0;  // stage and wsum slot of iteration k
+    uint32_t ph = 0;
+    for (uint32_t t = b0; t < ntiles;
+         t += G, ++k, q = q == 2 ? 0 : q + 1, st = st + 1 == kD1Stages ? 0 : st + 1, ph ^= st == 0) {
         zbits <<= 1;
         if (k >= (uint32_t)kD1Lag) prefetch(t - kD1Lag * G);
-        if (meta.trace && ct == 0) meta.trace[8ull * t + 1] = gtimer();
+        if (kTrace && ct == 0) meta.trace[8ull * t + 1] = gtimer();
         mbar_wait_parity(&sh.full[st], ph);
-        if (meta.trace && ct == 0) meta.trace[8ull * t + 2] = gtimer();
+        if (kTrace && ct == 0) meta.trace[8ull * t + 2] = gtimer();
         const uint64_t s = (uint64_t)t * kCTWarps + warp;
         uint32_t sum = 0;
         if (s < nsub) {
@@ -852,19 +854,19 @@ __global__ void __launch_bounds__(kSumThreads, 3)
                                    [&](uint32_t i) { return gword_guarded(gb + 4 * (uintptr_t)i, lo, hi); });
             }
         }
-        if (lane == 0) sh.wsum[k % 3][warp] = sum;
+        if (lane == 0) sh.wsum[q][warp] = sum;
         consumers_sync();
         if (ct == 0) {
             uint32_t a = 0;
 #pragma unroll
-            for (int w = 0; w < kCTWarps; ++w) a += sh.wsum[k % 3][w];
+            for (int w = 0; w < kCTWarps; ++w) a += sh.wsum[q][w];
             st_relaxed_u64(meta.agg + t, ((unsigned long long)epoch << 32) | a);
-            if (meta.trace) meta.trace[8ull * t + 3] = gtimer();
+            if (kTrace) meta.trace[8ull * t + 3] = gtimer();
         }
-        if (k >= (uint32_t)kD1Lag) {
-            const uint32_t i = k - kD1Lag;
-            resolve(t - kD1Lag * G, (int)(i % kD1Stages), (int)(i % 3), (zbits >> kD1Lag) & 1u);
-        }
+        static_assert(kD1Lag == 2, "wsum ring of 3: iteration k - 2 uses slot q + 1 (mod 3)");
+        if (k >= (uint32_t)kD1Lag)
+            resolve(t - kD1Lag * G, st >= kD1Lag ? st - kD1Lag : st + kD1Stages - kD1Lag, q == 2 ? 0 : q + 1,
+                    (zbits >> kD1Lag) & 1u);
     }
     for (uint32_t i = k > (uint32_t)kD1Lag ? k - kD1Lag : 0u; i < k; ++i) {
         prefetch(b0 + i * G);
@@ -890,14 +892,17 @@ static cudaError_t launch_decode1(const uint8_t* in, uint64_t in_len, uint64_t n
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
         cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, dev);
         const cudaError_t a =
-            cudaFuncSetAttribute(svb_decode1_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
+            cudaFuncSetAttribute(svb_decode1_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
         if (a != cudaSuccess) return a;
+        const cudaError_t a2 =
+            cudaFuncSetAttribute(svb_decode1_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
+        if (a2 != cudaSuccess) return a2;
         dev_cached = dev;
         occ_smem = 0;
     }
     if (!coop) return cudaSuccess;
     if (smem != occ_smem) {
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, svb_decode1_kernel, kSumThreads, smem);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, svb_decode1_kernel<false>, kSumThreads, smem);
         occ_smem = smem;
     }
     if (occ < 1) return cudaSuccess;  // caller falls back to the sums + delta passes
@@ -922,7 +927,8 @@ static cudaError_t launch_decode1(const uint8_t* in, uint64_t in_len, uint64_t n
     attr[1].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 2;
-    const cudaError_t e = cudaLaunchKernelExC(&cfg, (const void*)svb_decode1_kernel, args);
+    const void* fn = m.trace ? (const void*)svb_decode1_kernel<true> : (const void*)svb_decode1_kernel<false>;
+    const cudaError_t e = cudaLaunchKernelExC(&cfg, fn, args);
     if (e == cudaSuccess) *used = true;
     return e;
 }

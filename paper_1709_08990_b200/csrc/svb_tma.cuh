@@ -37,6 +37,19 @@ __device__ __forceinline__ void mbar_wait_parity(uint64_t* bar, uint32_t parity)
         : "memory");
 }
 
+// the same for a warp that has nothing else to do meanwhile (a producer waiting for a free
+// stage): the suspend-time hint lets the thread sleep until the phase completes instead of
+// spinning on issue slots the consumer warps of its SM sub-partition need
+__device__ __forceinline__ void mbar_wait_parity_sleep(uint64_t* bar, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n\t"
+        "@!p bra WAIT_%=;\n}" ::"r"(smem_addr(bar)),
+        "r"(parity), "r"(0x989680)
+        : "memory");
+}
+
 __device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 
 // global -> shared, completion on `bar` (dst, src 16-B aligned; bytes % 16 == 0)
