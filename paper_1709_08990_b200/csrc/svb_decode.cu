@@ -468,7 +468,7 @@ __global__ void __launch_bounds__(kSumThreads)
             const uint32_t ctx = tma_cover_bytes(cb, cb + cg, lo, hi);
             const bool c_tma = ctx != 0xFFFFFFFFu && (cb & 15) == 0;
             __syncwarp();  // every lane has read meta[st]
-            if (k >= (uint32_t)NST) mbar_wait_parity(&sh.empty[st], ph ^ 1u);  // consumers left the stage
+            if (k >= (uint32_t)NST) mbar_wait_parity_sleep(&sh.empty[st], ph ^ 1u);  // consumers left the stage
             if (!c_tma)
                 for (uint32_t i = lane; i < (uint32_t)cg; i += 32) sc[i] = __ldg(in + s0 * kWTGroups + i);
             if (lane <= 8) sh.hdr[st].head[lane] = (uint32_t)(data0 + my - base);

@@ -605,7 +605,7 @@ __global__ void __launch_bounds__(kCTThreads + 32, 2)
         for (uint32_t t = blockIdx.x; t < ntiles; t += G, ++k) {
             const int st = (int)(k % kE1Stages);
             uint8_t* stage = dsm + (uint32_t)st * kE1Stride;
-            if (k >= (uint32_t)kE1Stages) mbar_wait_parity(&sh.empty[st], ((k / kE1Stages) & 1u) ^ 1u);
+            if (k >= (uint32_t)kE1Stages) mbar_wait_parity_sleep(&sh.empty[st], ((k / kE1Stages) & 1u) ^ 1u);
             const uint64_t i0 = (uint64_t)t * kE1Ints;
             const uint64_t cnt = n - i0 < (uint64_t)kE1Ints ? n - i0 : (uint64_t)kE1Ints;
             const uintptr_t beg = (uintptr_t)(in + i0) - (t ? 16 : 0), end = (uintptr_t)(in + i0 + cnt);

@@ -8,7 +8,7 @@ import re
 import sys
 
 
-def main(csv_path, sass_path, kname, mangled, units, col="Instructions Executed"):
+def main(csv_path, sass_path, kname, mangled, units, col="Instructions Executed", top=40):
     rows = list(csv.reader(open(csv_path)))
     secs, cur = [], None
     for r in rows:
@@ -44,7 +44,7 @@ def main(csv_path, sass_path, kname, mangled, units, col="Instructions Executed"
         cnt[lines.get(off, ("?", 0))] += e
     tot = sum(cnt.values())
     print(f"total {tot:.0f} = {tot / units:.1f} per unit")
-    for (f, l), c in sorted(cnt.items(), key=lambda x: -x[1])[:40]:
+    for (f, l), c in sorted(cnt.items(), key=lambda x: -x[1])[:top]:
         src = ""
         try:
             src = open("paper_1709_08990_b200/csrc/" + f).read().split("\n")[l - 1].strip()[:90]
