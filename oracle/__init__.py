@@ -52,6 +52,10 @@ def _load() -> C.CDLL:
         "svbo_mt_decode": (i, [vp, sz, sz, i, u32, vp, vp, i]),
         "svbo_decode_batch": (i, [vp, sz, vp, vp, i, i]),
         "svbo_encode_batch": (i, [vp, sz, vp, vp, vp, i, i]),
+        "gbo_compressed_size": (sz, [vp, sz]),
+        "gbo_encode": (sz, [vp, sz, vp]),
+        "gbo_decode": (i, [vp, sz, sz, i, u32, vp, vp, i]),
+        "gbo_decode_group_general": (vp, [C.c_uint8, vp, vp, sz, vp]),
     }
     for name, (res, args) in sig.items():
         f = getattr(lib, name)
@@ -183,3 +187,34 @@ def encode_batch(segs: np.ndarray, values, out: np.ndarray, out_lens: np.ndarray
     s = np.ascontiguousarray(segs)
     return int(lib.svbo_encode_batch(s.ctypes.data, s.size, _ptr(v), out.ctypes.data, out_lens.ctypes.data,
                                      int(delta), threads or os.cpu_count() or 1))
+
+
+# ---- varint-GB (gb_oracle.h) ----
+def gb_compressed_size(values) -> int:
+    v = _u32(values)
+    return int(lib.gbo_compressed_size(_ptr(v), v.size))
+
+
+def gb_encode(values) -> bytes:
+    v = _u32(values)
+    out = np.empty((v.size + 3) // 4 + 4 * v.size + 1, dtype=np.uint8)
+    m = lib.gbo_encode(_ptr(v), v.size, _ptr(out))
+    return out[:m].tobytes()
+
+
+def gb_decode(data, n: int, delta: bool = False, base: int = 0, fast: bool = True) -> tuple[int, np.ndarray, int]:
+    """(status, values, last) -- varint_gb.hpp:21-25."""
+    b = _u8(data)
+    out = np.zeros(max(n, 1), dtype=np.uint32)
+    last = C.c_uint32(0)
+    st = lib.gbo_decode(_ptr(b), b.size, n, int(delta), base & 0xFFFFFFFF, _ptr(out), C.byref(last), int(fast))
+    return st, out[:n], last.value
+
+
+def gb_decode_group_general(control: int, data, k: int) -> np.ndarray | None:
+    """varint_gb.hpp:30-31: one group decoded field by field; None when it runs past the data."""
+    b = _u8(data)
+    out = np.zeros(4, dtype=np.uint32)
+    base = b.ctypes.data
+    r = lib.gbo_decode_group_general(control, base, base + b.size, k, _ptr(out))
+    return None if not r else out[:k]
