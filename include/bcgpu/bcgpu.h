@@ -187,6 +187,28 @@ int bcgpu_svb_seek_host(bcgpu_ctx *ctx, const uint8_t *bytes, size_t len, size_t
 int bcgpu_svb_select_host(bcgpu_ctx *ctx, const uint8_t *bytes, size_t len, size_t n, uint32_t base,
                           const uint64_t *idx, size_t q, uint32_t *values);
 
+/* ---- varint-GB (reference varint_gb.hpp:14-31) --------- */
+/* Groups of four integers, each a control byte (field i = byte_length(x_i) - 1, integer
+ * 0 in the low two bits) followed by its data bytes; the final group may be incomplete
+ * (zero unused fields, no data bytes for absent integers).  Same size as the Stream
+ * VByte encoding of the same integers, so bcgpu_svb_max_compressed_bytes bounds it. */
+/* gb_encode (varint_gb.hpp:19); delta != 0 first applies the mod-2^32 delta transform
+ * seeded with prev (as codec.hpp:92-93's encode(varint_gb, values, true) does with
+ * prev = 0).  d_out holds >= bcgpu_svb_max_compressed_bytes(n) bytes; the exact length
+ * goes to *d_out_len (device, may be NULL). */
+int bcgpu_gb_encode_device(bcgpu_ctx *ctx, const uint32_t *d_in, size_t n, int delta, uint32_t prev,
+                           uint8_t *d_out, size_t out_cap, uint64_t *d_out_len, void *stream);
+/* gb_decode / gb_decode_delta (varint_gb.hpp:21-25): validates (truncated /
+ * trailing_bytes, reported as for bcgpu_svb_decode_device), decodes n integers; delta
+ * adds the prefix sum seeded with base and writes the last value to *d_last (device,
+ * may be NULL). */
+int bcgpu_gb_decode_device(bcgpu_ctx *ctx, const uint8_t *d_in, size_t in_len, size_t n, int delta, uint32_t base,
+                           uint32_t *d_out, uint32_t *d_last, void *stream);
+int bcgpu_gb_encode_host(bcgpu_ctx *ctx, const uint32_t *values, size_t n, int delta, uint32_t prev,
+                         uint8_t *out, size_t out_cap, size_t *out_len);
+int bcgpu_gb_decode_host(bcgpu_ctx *ctx, const uint8_t *bytes, size_t len, size_t n, int delta, uint32_t base,
+                         uint32_t *out, uint32_t *last);
+
 /* ---- format plumbing on the host (no device, no ctx) -------------------- */
 
 /* Data + control length the control stream of an n-integer Stream VByte payload

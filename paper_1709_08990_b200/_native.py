@@ -70,6 +70,10 @@ SIGNATURES = {
     "bcgpu_svb_select_batch_device": (_int, [_vp, _vp, _sz, _sz, _u32, _vp, _sz, _vp, _vp]),
     "bcgpu_svb_seek_host": (_int, [_vp, _vp, _sz, _sz, _u32, _vp, _sz, _vp, _vp]),
     "bcgpu_svb_select_host": (_int, [_vp, _vp, _sz, _sz, _u32, _vp, _sz, _vp]),
+    "bcgpu_gb_encode_device": (_int, [_vp, _vp, _sz, _int, _u32, _vp, _sz, _vp, _vp]),
+    "bcgpu_gb_decode_device": (_int, [_vp, _vp, _sz, _sz, _int, _u32, _vp, _vp, _vp]),
+    "bcgpu_gb_encode_host": (_int, [_vp, _vp, _sz, _int, _u32, _vp, _sz, C.POINTER(_sz)]),
+    "bcgpu_gb_decode_host": (_int, [_vp, _vp, _sz, _sz, _int, _u32, _vp, C.POINTER(_u32)]),
     "bcgpu_svb_payload_length": (_int, [_vp, _sz, _sz, C.POINTER(_sz)]),
     "bcgpu_svb_append": (_int, [_vp, _sz, _sz, _sz, _u32, C.POINTER(_sz)]),
     "bcgpu_container_write": (_int, [C.c_uint8, _int, _sz, _vp, _sz, _vp, _sz, C.POINTER(_sz)]),

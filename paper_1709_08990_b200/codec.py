@@ -203,48 +203,107 @@ def svb_decode_blocks(data, n: int, blocks, offsets) -> tuple[np.ndarray, np.nda
     return out, cnt
 
 
-def _require_svb(cid) -> None:
-    if codec_id(cid) != codec_id.stream_vbyte:
-        raise CodecError(errc.unsupported, "only codec_id.stream_vbyte is implemented on the GPU path")
+# ---- varint-GB (varint_gb.hpp:14-31) -----------------------
+def _gb_encode(values, delta: bool, prev: int) -> bytes:
+    v = _u32_array(values)
+    n = v.size
+    out = np.empty(max(1, svb_max_compressed_bytes(n)), np.uint8)
+    out_len = C.c_size_t(0)
+    _check(lib.bcgpu_gb_encode_host(_ctx(), v.ctypes.data, n, int(delta), prev & 0xFFFFFFFF, out.ctypes.data,
+                                    out.size, C.byref(out_len)), "gb_encode")
+    return out[: out_len.value].tobytes()
+
+
+def gb_encode(values) -> bytes:
+    """varint_gb.hpp:19."""
+    return _gb_encode(values, False, 0)
+
+
+def gb_encode_delta(values, prev: int = 0) -> bytes:
+    """The delta transform (seeded with prev) then gb_encode -- encode(varint_gb, v, True)."""
+    return _gb_encode(values, True, prev)
+
+
+def _gb_decode(data, n: int, delta: bool, base: int, out) -> int:
+    b = _byte_array(data)
+    if out.dtype != np.uint32 or not out.flags.c_contiguous or out.size < n:
+        raise ValueError("out must be a C-contiguous uint32 array of at least n elements")
+    last = C.c_uint32(0)
+    _check(lib.bcgpu_gb_decode_host(_ctx(), b.ctypes.data if b.size else None, b.size, n, int(delta),
+                                    base & 0xFFFFFFFF, out.ctypes.data, C.byref(last)),
+           "gb_decode_delta" if delta else "gb_decode")
+    return int(last.value)
+
+
+def gb_decode(data, n: int, out: np.ndarray | None = None) -> np.ndarray:
+    """varint_gb.hpp:21-22 (both overloads: fills ``out`` or returns a new array)."""
+    o = np.empty(n, np.uint32) if out is None else out
+    _gb_decode(data, n, False, 0, o)
+    return o
+
+
+def gb_decode_delta(data, n: int, base: int, out: np.ndarray) -> int:
+    """varint_gb.hpp:24-25: fused decode + prefix sum; returns the last value."""
+    return _gb_decode(data, n, True, base, out)
+
+
+_GPU_CODECS = (codec_id.stream_vbyte, codec_id.varint_gb)
+
+
+def _require_gpu_codec(cid) -> codec_id:
+    c = codec_id(cid)
+    if c not in _GPU_CODECS:
+        raise CodecError(errc.unsupported, "only stream_vbyte and varint_gb are implemented on the GPU path")
+    return c
 
 
 def encode_payload(cid, values) -> bytes:
     """codec.hpp:84."""
-    _require_svb(cid)
-    return svb_encode(values)
+    return gb_encode(values) if _require_gpu_codec(cid) == codec_id.varint_gb else svb_encode(values)
 
 
 def decode_payload(cid, data, n: int, out: np.ndarray) -> None:
     """codec.hpp:85."""
-    _require_svb(cid)
-    svb_decode(data, n, out)
+    if _require_gpu_codec(cid) == codec_id.varint_gb:
+        gb_decode(data, n, out)
+    else:
+        svb_decode(data, n, out)
 
 
 def decode_payload_delta(cid, data, n: int, base: int, out: np.ndarray) -> int:
     """codec.hpp:89-90."""
-    _require_svb(cid)
+    if _require_gpu_codec(cid) == codec_id.varint_gb:
+        return gb_decode_delta(data, n, base, out)
     return svb_decode_delta(data, n, base, out)
 
 
 def encode(cid, values, delta: bool = False) -> EncodedBuffer:
     """codec.hpp:92-93 (delta base 0)."""
-    _require_svb(cid)
+    c = _require_gpu_codec(cid)
     v = _u32_array(values)
     if v.size > 0xFFFFFFFF:
         raise CodecError(errc.out_of_range, "count exceeds uint32")
-    data = svb_encode_delta(v, 0) if delta else svb_encode(v)
-    return EncodedBuffer(codec_id(cid), int(v.size), bool(delta), data)
+    if c == codec_id.varint_gb:
+        data = gb_encode_delta(v, 0) if delta else gb_encode(v)
+    else:
+        data = svb_encode_delta(v, 0) if delta else svb_encode(v)
+    return EncodedBuffer(c, int(v.size), bool(delta), data)
 
 
 def decode(buf: EncodedBuffer) -> np.ndarray:
     """codec.hpp:95-96."""
-    _require_svb(buf.codec)
+    _require_gpu_codec(buf.codec)
     out = np.empty(buf.count, np.uint32)
     if buf.delta:
-        svb_decode_delta(buf.bytes, buf.count, 0, out)
+        decode_payload_delta(buf.codec, buf.bytes, buf.count, 0, out)
     else:
-        svb_decode(buf.bytes, buf.count, out)
+        decode_payload(buf.codec, buf.bytes, buf.count, out)
     return out
+
+
+def _require_svb(cid) -> None:
+    if codec_id(cid) != codec_id.stream_vbyte:
+        raise CodecError(errc.unsupported, "this operation is defined for codec_id.stream_vbyte only")
 
 
 # ---- format plumbing on the host (svb_format.cpp): no device, no context -------------

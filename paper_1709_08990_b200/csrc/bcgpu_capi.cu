@@ -79,6 +79,8 @@ struct bcgpu_ctx {
     uint64_t agg_n = 0;                      // n whose tile aggregates hold no current-epoch tag
     uint32_t* endval = nullptr;              // seek / select: last value of every sub-tile
     size_t endval_cap = 0;                   // entries
+    void* gbws = nullptr;                    // varint-GB decode: chunk transfer tables (svb_gb.cu)
+    size_t gbws_cap = 0;                     // bytes
 };
 
 static unsigned long long* ticket_ptr(bcgpu_ctx* c) { return c->ws; }
@@ -303,6 +305,7 @@ int bcgpu_ctx_destroy(bcgpu_ctx* c) {
     if (c->offs) cudaFree(c->offs);
     if (c->slots) cudaFree(c->slots);
     if (c->endval) cudaFree(c->endval);
+    if (c->gbws) cudaFree(c->gbws);
     if (c->stream) cudaStreamDestroy(c->stream);
     if (c->aux) cudaStreamDestroy(c->aux);
     if (c->aux2) cudaStreamDestroy(c->aux2);
@@ -843,6 +846,128 @@ int bcgpu_svb_select_host(bcgpu_ctx* c, const uint8_t* bytes, size_t len, size_t
     if (st) return st;
     if (q) BC_CUDA(cudaMemcpyAsync(values, d + off_v, 4 * q, cudaMemcpyDeviceToHost, c->stream));
     BC_CUDA(cudaStreamSynchronize(c->stream));
+    return BCGPU_OK;
+}
+
+// ---------------------------------------------------------------------------
+// varint-GB (svb_gb.cu)
+// ---------------------------------------------------------------------------
+static int ensure_gbws(bcgpu_ctx* c, uint64_t len, cudaStream_t s, void** p) {
+    const size_t bytes = gb_decode_ws_bytes(len);
+    if (bytes > c->gbws_cap) {
+        if (c->gbws) {
+            BC_CUDA(cudaStreamSynchronize(s));
+            BC_CUDA(cudaFree(c->gbws));
+            c->gbws = nullptr;
+            c->gbws_cap = 0;
+        }
+        const size_t cap = bytes + bytes / 4 + 4096;
+        BC_CUDA(cudaMalloc(&c->gbws, cap));
+        c->gbws_cap = cap;
+    }
+    *p = c->gbws;
+    return BCGPU_OK;
+}
+
+int bcgpu_gb_encode_device(bcgpu_ctx* c, const uint32_t* d_in, size_t n, int delta, uint32_t prev, uint8_t* d_out,
+                           size_t out_cap, uint64_t* d_out_len, void* stream) {
+    if (!c || (n && (!d_in || !d_out))) return BCGPU_ERR_INVALID_ARGUMENT;
+    if (out_cap < bcgpu_svb_max_compressed_bytes(n)) return BCGPU_ERR_INVALID_ARGUMENT;
+    DeviceGuard g(c->device);
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    if (n == 0) {
+        const int se = next_epoch(c, s);
+        if (se) return se;
+        if (d_out_len) BC_CUDA(cudaMemsetAsync(d_out_len, 0, sizeof(uint64_t), s));
+        return BCGPU_OK;
+    }
+    int st = ensure_meta(c, n, s);
+    if (st) return st;
+    st = next_epoch(c, s);
+    if (st) return st;
+    int launches = 0;
+    BC_CUDA(launch_gb_encode(d_in, n, delta, prev, d_out, d_out_len, c->offs, status_ptr(c), c->epoch, s,
+                             &launches));
+    g_launches.fetch_add((uint64_t)launches);
+    return BCGPU_OK;
+}
+
+int bcgpu_gb_decode_device(bcgpu_ctx* c, const uint8_t* d_in, size_t in_len, size_t n, int delta, uint32_t base,
+                           uint32_t* d_out, uint32_t* d_last, void* stream) {
+    if (!c || (n && (!d_in || !d_out))) return BCGPU_ERR_INVALID_ARGUMENT;
+    DeviceGuard g(c->device);
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    if (n == 0) {
+        const int se = next_epoch(c, s);
+        if (se) return se;
+        if (d_last) BC_CUDA(cudaMemcpyAsync(d_last, &base, sizeof(uint32_t), cudaMemcpyHostToDevice, s));
+        return in_len ? BCGPU_ERR_TRAILING_BYTES : BCGPU_OK;
+    }
+    // every group holds a control byte and every integer at least one data byte
+    if (in_len < (n + 3) / 4 + n) return BCGPU_ERR_TRUNCATED;
+    void* ws = nullptr;
+    int st = ensure_gbws(c, in_len, s, &ws);
+    if (st) return st;
+    st = next_epoch(c, s);
+    if (st) return st;
+    int launches = 0;
+    BC_CUDA(launch_gb_decode(d_in, in_len, n, delta, base, d_out, d_last, ws, status_ptr(c), c->epoch, s,
+                             &launches));
+    g_launches.fetch_add((uint64_t)launches);
+    return BCGPU_OK;
+}
+
+int bcgpu_gb_encode_host(bcgpu_ctx* c, const uint32_t* values, size_t n, int delta, uint32_t prev, uint8_t* out,
+                         size_t out_cap, size_t* out_len) {
+    if (!c || !out_len || (n && (!values || !out))) return BCGPU_ERR_INVALID_ARGUMENT;
+    *out_len = 0;
+    if (n == 0) return BCGPU_OK;
+    const size_t max_out = bcgpu_svb_max_compressed_bytes(n);
+    DeviceGuard g(c->device);
+    const size_t off_out = align_up(4 * n, 256), off_len = align_up(off_out + max_out, 256);
+    void* sp = nullptr;
+    int st = scratch(c, off_len + 256, &sp);
+    if (st) return st;
+    uint8_t* d = static_cast<uint8_t*>(sp);
+    BC_CUDA(cudaMemcpyAsync(d, values, 4 * n, cudaMemcpyHostToDevice, c->stream));
+    st = bcgpu_gb_encode_device(c, reinterpret_cast<uint32_t*>(d), n, delta, prev, d + off_out, max_out,
+                                reinterpret_cast<uint64_t*>(d + off_len), c->stream);
+    if (st) return st;
+    uint64_t len = 0;
+    BC_CUDA(cudaMemcpyAsync(&len, d + off_len, sizeof(len), cudaMemcpyDeviceToHost, c->stream));
+    BC_CUDA(cudaStreamSynchronize(c->stream));
+    if (len > out_cap) return BCGPU_ERR_INVALID_ARGUMENT;
+    BC_CUDA(cudaMemcpyAsync(out, d + off_out, len, cudaMemcpyDeviceToHost, c->stream));
+    BC_CUDA(cudaStreamSynchronize(c->stream));
+    *out_len = (size_t)len;
+    return BCGPU_OK;
+}
+
+int bcgpu_gb_decode_host(bcgpu_ctx* c, const uint8_t* bytes, size_t len, size_t n, int delta, uint32_t base,
+                         uint32_t* out, uint32_t* last) {
+    if (!c || (n && (!bytes || !out))) return BCGPU_ERR_INVALID_ARGUMENT;
+    if (n == 0) {
+        if (last) *last = base;
+        return len ? BCGPU_ERR_TRAILING_BYTES : BCGPU_OK;
+    }
+    if (len < (n + 3) / 4 + n) return BCGPU_ERR_TRUNCATED;
+    DeviceGuard g(c->device);
+    const size_t off_out = align_up(len, 256), off_last = align_up(off_out + 4 * n, 256);
+    void* sp = nullptr;
+    int st = scratch(c, off_last + 256, &sp);
+    if (st) return st;
+    uint8_t* d = static_cast<uint8_t*>(sp);
+    BC_CUDA(cudaMemcpyAsync(d, bytes, len, cudaMemcpyHostToDevice, c->stream));
+    st = bcgpu_gb_decode_device(c, d, len, n, delta, base, reinterpret_cast<uint32_t*>(d + off_out),
+                                reinterpret_cast<uint32_t*>(d + off_last), c->stream);
+    if (st) return st;
+    st = bcgpu_ctx_sync_status(c, c->stream);
+    if (st) return st;
+    BC_CUDA(cudaMemcpyAsync(out, d + off_out, 4 * n, cudaMemcpyDeviceToHost, c->stream));
+    uint32_t lv = 0;
+    BC_CUDA(cudaMemcpyAsync(&lv, d + off_last, sizeof(lv), cudaMemcpyDeviceToHost, c->stream));
+    BC_CUDA(cudaStreamSynchronize(c->stream));
+    if (last) *last = delta ? lv : out[n - 1];
     return BCGPU_OK;
 }
 

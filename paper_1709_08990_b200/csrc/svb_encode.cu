@@ -871,6 +871,19 @@ cudaError_t launch_encode_piece(const uint32_t* in, uint64_t n, int delta, uint3
     return cudaGetLastError();
 }
 
+cudaError_t launch_size_scan(const uint32_t* in, uint64_t n, int delta, uint32_t prev, void* meta_ws,
+                             uint64_t* d_out_len, unsigned long long* status, uint32_t epoch, cudaStream_t stream) {
+    const DecodeMeta m = carve_decode_meta(meta_ws, n);
+    const uint64_t ngroups = (n + 3) >> 2;
+    const uint64_t nsub = (ngroups + kWTGroups - 1) / kWTGroups;
+    const uint32_t nchunks = (uint32_t)((nsub + kChunkSubs - 1) / kChunkSubs);
+    if (delta)
+        svb_size_scan_kernel<true><<<nchunks, 256, 0, stream>>>(in, n, prev, m, d_out_len, status, epoch, 0, nchunks);
+    else
+        svb_size_scan_kernel<false><<<nchunks, 256, 0, stream>>>(in, n, prev, m, d_out_len, status, epoch, 0, nchunks);
+    return cudaGetLastError();
+}
+
 // device address of the running data offset (bytes after the last encoded piece)
 unsigned long long* encode_running_ptr(void* meta_ws, uint64_t n) { return carve_decode_meta(meta_ws, n).running; }
 

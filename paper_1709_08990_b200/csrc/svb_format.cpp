@@ -1,6 +1,6 @@
-// svb_format.cpp -- host-side Stream VByte format plumbing around the GPU codec:
+// svb_format.cpp -- host-side format plumbing around the GPU codecs:
 // svb_append (reference proj/core/include/bytecodec/stream_vbyte.hpp:44-46)
-// and the 14-byte "SVB1" container.  Both are byte manipulation of a
+// and the 14-byte "SVB1" container for Stream VByte and varint-GB payloads.  Both are byte manipulation of a
 // single stream on the host -- the reference does them on the host too -- so they never
 // touch the device and need no context.
 #include <cstdint>
@@ -26,6 +26,19 @@ uint64_t svb_declared_data(const uint8_t* ctrl, uint64_t n) {
         for (uint32_t i = 0; i < r; ++i) d += ((c >> (2 * i)) & 3u) + 1u;
     }
     return d;
+}
+
+// varint-GB (varint_gb.hpp:14-17): the group chain's length for n integers, or
+// UINT64_MAX when a control byte lies at or past len (the payload cannot hold them)
+uint64_t gb_declared_length(const uint8_t* p, uint64_t len, uint64_t n) {
+    uint64_t pos = 0;
+    for (uint64_t g = 0; g < n; g += 4) {
+        if (pos >= len) return UINT64_MAX;
+        const uint32_t c = p[pos], k = n - g < 4 ? (uint32_t)(n - g) : 4u;
+        pos += 1;
+        for (uint32_t i = 0; i < k; ++i) pos += ((c >> (2 * i)) & 3u) + 1u;
+    }
+    return pos;
 }
 
 constexpr uint8_t kMagic[4] = {'S', 'V', 'B', '1'};
@@ -112,14 +125,16 @@ int bcgpu_container_read(const uint8_t* src, size_t len, uint8_t* codec, int* de
     *payload_offset = BCGPU_CONTAINER_HEADER;
     *payload_len = plen;
     // payload length against the codec's size formula: the Stream VByte size
-    // identity ceil(N/4) + sum(byte_length) from the control bytes; the other codecs are out
+    // identity ceil(N/4) + sum(byte_length) from the control bytes; for varint-GB the same
+    // total, found by walking the interleaved group chain.  VByte and varint-G8IU are out
     // of this library's scope and their payloads are not verified
+    const uint8_t* pl = src + BCGPU_CONTAINER_HEADER;
     if (src[4] == 3) {
         const uint64_t nctrl = ((uint64_t)nv + 3) / 4;
-        if (plen < nctrl || nctrl + svb_declared_data(src + BCGPU_CONTAINER_HEADER, nv) != plen)
-            return BCGPU_ERR_LENGTH_MISMATCH;
+        if (plen < nctrl || nctrl + svb_declared_data(pl, nv) != plen) return BCGPU_ERR_LENGTH_MISMATCH;
         return BCGPU_OK;
     }
+    if (src[4] == 1) return gb_declared_length(pl, plen, nv) == plen ? BCGPU_OK : BCGPU_ERR_LENGTH_MISMATCH;
     return BCGPU_ERR_UNSUPPORTED;
 }
 

@@ -1,0 +1,434 @@
+// svb_gb.cu -- varint-GB encode / decode on the GPU.
+//
+// Format (reference proj/core/include/bytecodec/varint_gb.hpp:14-17):
+// ceil(n/4) groups, each a control byte (field i = byte_length(x_i) - 1, integer 0 in
+// the low two bits) followed by the little-endian bytes of its integers; a final
+// incomplete group has zero unused fields and no bytes for absent integers.
+//
+// Encode.  The stream is the same size as Stream VByte's (ceil(n/4) + sum of byte
+// lengths), and group k sits at k + (data bytes of groups < k): sub-tile s starts at
+// its Stream VByte data offset + 256 s.  So the Stream VByte size scan
+// (svb_encode.cu; with the same prev-seeded delta transform) provides every sub-tile's
+// offset, and gb_encode_kernel assembles each
+// sub-tile's interleaved groups in shared memory (at the destination's 16-B phase) and
+// writes them with 128-bit stores, byte stores only at the two edges.
+//
+// Decode.  Control positions are data-dependent: group k's control byte follows group
+// k-1's data, so no group can be located without the ones before
+// it.  The chain is resolved with transfer functions:
+//   1. gb_table_kernel: the stream is cut into 4 KiB chunks; a group starting in one
+//      chunk ends at most 16 bytes into the next, so a chunk is entered at one of 17
+//      offsets.  Per chunk, lanes 0..16 of a warp walk the chunk from each entry offset
+//      and record (exit offset into the next chunk, groups started, sum of their
+//      values for delta).
+//   2. gb_compose_kernel / gb_expand_kernel: the tables compose associatively (follow
+//      the exit of one into the next, add counts and sums).  A 32-ary tree of
+//      compositions is built bottom-up, then walked top-down from entry 0 at the
+//      stream's start, which resolves every chunk's true entry offset, index of its
+//      first group, and value carry.  The root's count also settles truncation.
+//   3. gb_decode_kernel: per chunk, lane 0 lists the group starts from the true entry,
+//      then the warp decodes 32 groups per round (all-small fast path for control 0,
+//      field by field otherwise), fuses the delta prefix sum (warp scan + carry), and
+//      stores 128-bit rows.  The warp holding group ceil(n/4)-1 checks the stream end
+//      (truncated / trailing bytes).
+#include <cstdint>
+
+#include "svb_device.cuh"
+#include "svb_fast.cuh"
+#include "svb_kernels.cuh"
+#include "svb_scan.cuh"
+#include "svb_warp.cuh"
+
+namespace bcgpu {
+
+namespace {
+
+constexpr uint32_t kGbChunk = 4096;                 // compressed bytes per decode chunk (one warp)
+constexpr uint32_t kGbStage = kGbChunk + 64;        // staged: <16 phase + chunk + the last group's overhang
+constexpr int kGbE = 17;                            // entry offsets 0..16 (a group spans <= 17 bytes)
+constexpr uint32_t kGbFan = 32;                     // tables composed per tree node
+constexpr int kGbWarps = 8;                         // chunks per CTA (table / decode kernels)
+constexpr int kGbTreeWarps = 4;                     // tree nodes per CTA (compose / expand kernels)
+constexpr uint32_t kGbMaxGroups = kGbChunk / 5 + 2;  // groups starting in one chunk (>= 5 B each but the last)
+constexpr uint32_t kGbEncBuf = kWTGroups + 4 * kWTInts + 32;  // one sub-tile's groups + phase
+
+__device__ __forceinline__ void gb_report(unsigned long long* st, uint32_t epoch, uint32_t code) {
+    if (st) *st = ((unsigned long long)epoch << 32) | code;
+}
+
+// bytes [off, off + cnt) of the stream into buf (16-B aligned) at buf index phase + i,
+// phase = (in + off) & 15; bytes outside the stream read as 0.  Returns the phase.
+__device__ __forceinline__ uint32_t gb_stage(const uint8_t* in, uint64_t len, uint64_t off, uint32_t cnt, uint8_t* buf) {
+    const int lane = threadIdx.x & 31;
+    const uintptr_t lo = (uintptr_t)in, hi = lo + len, a = lo + off, g0 = a & ~(uintptr_t)15;
+    const uint32_t ph = (uint32_t)(a - g0);
+    const uint32_t ng = (ph + cnt + 15) / 16;
+    for (uint32_t i = lane; i < ng; i += 32)
+        *reinterpret_cast<uint4*>(buf + 16 * i) = load_chunk_guarded(g0 + 16 * i, lo, hi);
+    return ph;
+}
+
+// bytes of a full group with control byte c (1 control + 4..16 data)
+__device__ __forceinline__ uint32_t gb_group_bytes(uint32_t c) { return 5u + fsum(c); }
+
+// the k (1..4) integers of the group whose control byte c is at shared address a
+__device__ __forceinline__ uint4 gb_group_values(uint32_t a, uint32_t c, uint32_t k) {
+    uint4 v = make_uint4(0, 0, 0, 0);
+    if (c == 0 && k == 4) {  // all-small fast path: four one-byte integers
+        const uint32_t x = __funnelshift_r(lds32((a + 1) & ~3u), lds32(((a + 1) & ~3u) + 4), ((a + 1) & 3u) * 8u);
+        return make_uint4(x & 0xFFu, (x >> 8) & 0xFFu, (x >> 16) & 0xFFu, x >> 24);
+    }
+    uint32_t p = a + 1;
+    uint32_t x[4] = {0, 0, 0, 0};
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        const uint32_t l = ((c >> (2 * i)) & 3u) + 1u;
+        if ((uint32_t)i < k) {
+            x[i] = extract_s(p, l);
+            p += l;
+        }
+    }
+    v = make_uint4(x[0], x[1], x[2], x[3]);
+    return v;
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------------------
+// encode: one warp per 1024-integer sub-tile, offsets from the Stream VByte size scan
+// ---------------------------------------------------------------------------
+template <bool kDelta>
+__global__ void __launch_bounds__(256)
+    gb_encode_kernel(const uint32_t* __restrict__ in, uint64_t n, uint32_t prev, uint8_t* __restrict__ out,
+                     DecodeMeta meta) {
+    __shared__ __align__(16) uint8_t sbuf[kGbWarps][kGbEncBuf];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint64_t ngroups = (n + 3) >> 2;
+    const uint32_t tail_r = (uint32_t)(n & 3);
+    const uint64_t nsub = (ngroups + kWTGroups - 1) / kWTGroups;
+    const uint64_t s = (uint64_t)blockIdx.x * kGbWarps + warp;
+    if (s >= nsub) return;
+    const uint64_t g0 = s * kWTGroups;
+    const uint64_t o0 = meta.chunkpre[s / kChunkSubs] + meta.localpre[s] + g0;  // data before + control bytes before
+    uint8_t* dst = out + o0;
+    const uint32_t ph = (uint32_t)((uintptr_t)dst & 15);
+    const uint32_t sb = sh_addr(sbuf[warp]);
+    const bool in16 = (((uintptr_t)in) & 15) == 0;
+    uint32_t off = ph;
+#pragma unroll 1
+    for (int j = 0; j < kWTRows; ++j) {
+        const uint64_t g = g0 + 32 * j + lane;
+        const uint32_t cnt = group_count(g, ngroups, tail_r);
+        uint4 x = make_uint4(0, 0, 0, 0);
+        if (cnt == 4 && in16) {
+            x = ldg_stream_v4(in + 4 * g);
+        } else if (cnt) {
+            x.x = __ldg(in + 4 * g);
+            if (cnt > 1) x.y = __ldg(in + 4 * g + 1);
+            if (cnt > 2) x.z = __ldg(in + 4 * g + 2);
+            if (cnt > 3) x.w = __ldg(in + 4 * g + 3);
+        }
+        if constexpr (kDelta) {  // mod-2^32 differences, seeded with prev
+            const uint32_t p = g ? (cnt ? __ldg(in + 4 * g - 1) : 0u) : prev;
+            x = make_uint4(x.x - p, x.y - x.x, x.z - x.y, x.w - x.z);
+        }
+        uint32_t l[4], c = 0, gs = cnt ? 1u : 0u;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            l[i] = (uint32_t)i < cnt ? dev_byte_length(comp(x, i)) : 0u;
+            if ((uint32_t)i < cnt) c |= (l[i] - 1u) << (2 * i);
+            gs += l[i];
+        }
+        const uint32_t incl = warp_inclusive_scan(gs);
+        if (cnt) {
+            uint32_t p = sb + off + incl - gs;
+            sts8(p++, c);
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+                for (uint32_t b = 0; b < l[i]; ++b) sts8(p++, (comp(x, i) >> (8 * b)) & 0xFFu);
+        }
+        off += __shfl_sync(kFull, incl, 31);
+    }
+    __syncwarp();
+    // bytes [ph, off) of the buffer -> dst - ph + [ph, off): whole 16-B granules as 128-bit
+    // stores, the partial first / last granules byte by byte (neighbouring warps own the rest)
+    uint8_t* gdst = dst - ph;
+    const uint32_t ng = (off + 15) / 16;
+    for (uint32_t i = lane; i < ng; i += 32) {
+        const uint32_t b0 = 16 * i, b1 = b0 + 16;
+        if (b0 >= ph && b1 <= off) {
+            *reinterpret_cast<uint4*>(gdst + b0) = lds128(sb + b0);
+        } else {
+            for (uint32_t b = b0 < ph ? ph : b0; b < (b1 < off ? b1 : off); ++b) gdst[b] = (uint8_t)lds8(sb + b);
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// decode 1: per-chunk transfer tables
+// ---------------------------------------------------------------------------
+template <bool kDelta>
+__global__ void __launch_bounds__(256)
+    gb_table_kernel(const uint8_t* __restrict__ in, uint64_t len, uint64_t nchunks, uint32_t* __restrict__ tcnt,
+                    uint32_t* __restrict__ texit, uint32_t* __restrict__ tsum) {
+    __shared__ __align__(16) uint8_t sbuf[kGbWarps][kGbStage];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint64_t chunk = (uint64_t)blockIdx.x * kGbWarps + warp;
+    if (chunk >= nchunks) return;
+    const uint64_t cs = chunk * kGbChunk;
+    const uint32_t clen = (uint32_t)(len - cs < kGbChunk ? len - cs : kGbChunk);
+    const uint32_t ph = gb_stage(in, len, cs, clen + 32, sbuf[warp]);
+    __syncwarp();
+    if (lane < kGbE) {
+        const uint32_t sa = sh_addr(sbuf[warp]) + ph;
+        uint32_t pos = (uint32_t)lane, cnt = 0, sum = 0;
+        while (pos < clen) {
+            const uint32_t c = lds8(sa + pos);
+            if constexpr (kDelta) {
+                const uint4 v = gb_group_values(sa + pos, c, 4);
+                sum += v.x + v.y + v.z + v.w;
+            }
+            pos += gb_group_bytes(c);
+            ++cnt;
+        }
+        const uint64_t i = chunk * kGbE + lane;
+        tcnt[i] = cnt;
+        texit[i] = pos - clen;
+        if constexpr (kDelta) tsum[i] = sum;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// decode 2: compose 32 child tables per node (bottom-up), resolve entries (top-down)
+// ---------------------------------------------------------------------------
+struct GbTreeSmem {
+    uint32_t cnt[kGbFan * kGbE], exit[kGbFan * kGbE], sum[kGbFan * kGbE];
+};
+
+__device__ __forceinline__ uint32_t gb_load_children(GbTreeSmem& sm, const uint32_t* ccnt, const uint32_t* cexit,
+                                                     const uint32_t* csum, uint64_t nchild, uint64_t parent) {
+    const int lane = threadIdx.x & 31;
+    const uint64_t k0 = parent * kGbFan;
+    const uint32_t nk = (uint32_t)(nchild - k0 < kGbFan ? nchild - k0 : kGbFan);
+    for (uint32_t i = lane; i < nk * kGbE; i += 32) {
+        sm.cnt[i] = ccnt[k0 * kGbE + i];
+        sm.exit[i] = cexit[k0 * kGbE + i];
+        sm.sum[i] = csum ? csum[k0 * kGbE + i] : 0u;
+    }
+    __syncwarp();
+    return nk;
+}
+
+__global__ void __launch_bounds__(32 * kGbTreeWarps)
+    gb_compose_kernel(const uint32_t* __restrict__ ccnt, const uint32_t* __restrict__ cexit,
+                      const uint32_t* __restrict__ csum, uint64_t nchild, uint32_t* __restrict__ pcnt,
+                      uint32_t* __restrict__ pexit, uint32_t* __restrict__ psum, uint64_t nparent) {
+    __shared__ GbTreeSmem sm[kGbTreeWarps];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint64_t p = (uint64_t)blockIdx.x * kGbTreeWarps + warp;
+    if (p >= nparent) return;
+    const uint32_t nk = gb_load_children(sm[warp], ccnt, cexit, csum, nchild, p);
+    if (lane < kGbE) {
+        uint32_t x = (uint32_t)lane, cnt = 0, sum = 0;
+        for (uint32_t k = 0; k < nk; ++k) {
+            const uint32_t i = k * kGbE + x;
+            cnt += sm[warp].cnt[i];
+            sum += sm[warp].sum[i];
+            x = sm[warp].exit[i];
+        }
+        pcnt[p * kGbE + lane] = cnt;
+        pexit[p * kGbE + lane] = x;
+        if (psum) psum[p * kGbE + lane] = sum;
+    }
+}
+
+// root != 0: the single top node, entered at offset 0 with carry base; its group count
+// (groups chained from the stream's start) below ceil(n/4) means the stream is truncated
+__global__ void __launch_bounds__(32 * kGbTreeWarps)
+    gb_expand_kernel(const uint32_t* __restrict__ ccnt, const uint32_t* __restrict__ cexit,
+                     const uint32_t* __restrict__ csum, uint64_t nchild, const uint32_t* __restrict__ pentry,
+                     const uint32_t* __restrict__ pcntpre, const uint32_t* __restrict__ psumpre, uint64_t nparent,
+                     uint32_t* __restrict__ centry, uint32_t* __restrict__ ccntpre, uint32_t* __restrict__ csumpre,
+                     int root, uint32_t base, uint64_t ngroups, unsigned long long* status, uint32_t epoch) {
+    __shared__ GbTreeSmem sm[kGbTreeWarps];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint64_t p = (uint64_t)blockIdx.x * kGbTreeWarps + warp;
+    if (p >= nparent) return;
+    const uint32_t nk = gb_load_children(sm[warp], ccnt, cexit, csum, nchild, p);
+    if (lane == 0) {
+        uint32_t x = root ? 0u : pentry[p], cp = root ? 0u : pcntpre[p], sp = root ? base : psumpre[p];
+        for (uint32_t k = 0; k < nk; ++k) {
+            const uint64_t c = p * kGbFan + k;
+            centry[c] = x;
+            ccntpre[c] = cp;
+            csumpre[c] = sp;
+            const uint32_t i = k * kGbE + x;
+            cp += sm[warp].cnt[i];
+            sp += sm[warp].sum[i];
+            x = sm[warp].exit[i];
+        }
+        if (root && (uint64_t)cp < ngroups) gb_report(status, epoch, BCGPU_ERR_TRUNCATED);
+    }
+}
+
+// ---------------------------------------------------------------------------
+// decode 3: groups of each chunk from its resolved entry
+// ---------------------------------------------------------------------------
+template <bool kDelta>
+__global__ void __launch_bounds__(256)
+    gb_decode_kernel(const uint8_t* __restrict__ in, uint64_t len, uint64_t n, uint64_t nchunks,
+                     const uint32_t* __restrict__ rentry, const uint32_t* __restrict__ rcnt,
+                     const uint32_t* __restrict__ rsum, uint32_t* __restrict__ out, uint32_t* __restrict__ d_last,
+                     unsigned long long* status, uint32_t epoch) {
+    __shared__ __align__(16) uint8_t sbuf[kGbWarps][kGbStage];
+    __shared__ uint16_t spos[kGbWarps][kGbMaxGroups];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint64_t chunk = (uint64_t)blockIdx.x * kGbWarps + warp;
+    if (chunk >= nchunks) return;
+    const uint64_t ngroups = (n + 3) >> 2;
+    const uint32_t tail_r = (uint32_t)(n & 3);
+    const uint64_t kb = rcnt[chunk];  // index of the chunk's first group
+    if (kb >= ngroups) return;
+    const uint64_t cs = chunk * kGbChunk;
+    const uint32_t clen = (uint32_t)(len - cs < kGbChunk ? len - cs : kGbChunk);
+    const uint32_t ph = gb_stage(in, len, cs, clen + 32, sbuf[warp]);
+    __syncwarp();
+    const uint32_t sa = sh_addr(sbuf[warp]) + ph;
+    uint32_t m = 0;
+    if (lane == 0) {
+        const uint64_t left = ngroups - kb;
+        const uint32_t lim = (uint32_t)(left < kGbMaxGroups ? left : kGbMaxGroups);
+        uint32_t pos = rentry[chunk];
+        while (pos < clen && m < lim) {
+            spos[warp][m++] = (uint16_t)pos;
+            pos += gb_group_bytes(lds8(sa + pos));
+        }
+    }
+    m = __shfl_sync(kFull, m, 0);
+    __syncwarp();
+    uint32_t run = kDelta ? rsum[chunk] : 0u;
+    const bool out16 = (((uintptr_t)out) & 15) == 0;
+    for (uint32_t r = 0; r < m; r += 32) {
+        const uint32_t i = r + lane;
+        const uint64_t gi = kb + i;
+        const uint32_t k = i < m ? group_count(gi, ngroups, tail_r) : 0u;
+        uint4 v = make_uint4(0, 0, 0, 0);
+        uint32_t c = 0, p = 0;
+        if (k) {
+            p = spos[warp][i];
+            c = lds8(sa + p);
+            v = gb_group_values(sa + p, c, k);
+        }
+        if constexpr (kDelta) {
+            v.y += v.x;
+            v.z += v.y;
+            v.w += v.z;
+            const uint32_t I = warp_inclusive_scan(v.w);
+            v = add4(v, run + I - v.w);
+            run += __shfl_sync(kFull, I, 31);
+        }
+        if (k) store_group(out + 4 * gi, v, k, out16);
+        if (k && gi == ngroups - 1) {
+            // the stream's last group: it must end exactly at the stream's end
+            uint64_t end = cs + p + 1;
+            for (uint32_t f = 0; f < k; ++f) end += ((c >> (2 * f)) & 3u) + 1u;
+            gb_report(status, epoch,
+                      end > len ? BCGPU_ERR_TRUNCATED : (end < len ? BCGPU_ERR_TRAILING_BYTES : (uint32_t)BCGPU_OK));
+            if (d_last) *d_last = comp(v, (int)k - 1);
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// launchers
+// ---------------------------------------------------------------------------
+// device workspace of a decode of len compressed bytes: per tree level, 3 tables of 17
+// words per node and 3 resolved words per node
+static uint64_t gb_levels(uint64_t len, uint64_t* nodes) {
+    uint64_t m = (len + kGbChunk - 1) / kGbChunk, L = 0;
+    if (m == 0) m = 1;
+    for (;;) {
+        nodes[L++] = m;
+        if (m == 1) break;
+        m = (m + kGbFan - 1) / kGbFan;
+    }
+    return L;
+}
+
+size_t gb_decode_ws_bytes(uint64_t len) {
+    uint64_t nodes[16], L = gb_levels(len, nodes), words = 0;
+    for (uint64_t l = 0; l < L; ++l) words += nodes[l] * (3 * kGbE + 3) + 4;
+    return (size_t)(4 * words + 256);
+}
+
+cudaError_t launch_gb_decode(const uint8_t* in, uint64_t len, uint64_t n, int delta, uint32_t base, uint32_t* out,
+                             uint32_t* d_last, void* ws, unsigned long long* status, uint32_t epoch,
+                             cudaStream_t stream, int* launches) {
+    uint64_t nodes[16];
+    const uint64_t L = gb_levels(len, nodes);
+    uint32_t* tc[16];
+    uint32_t* tx[16];
+    uint32_t* ts[16];
+    uint32_t* re[16];
+    uint32_t* rc[16];
+    uint32_t* rs[16];
+    uint32_t* w = static_cast<uint32_t*>(ws);
+    for (uint64_t l = 0; l < L; ++l) {
+        const uint64_t m = nodes[l];
+        tc[l] = w, w += m * kGbE;
+        tx[l] = w, w += m * kGbE;
+        ts[l] = w, w += m * kGbE;
+        re[l] = w, w += m + 1;
+        rc[l] = w, w += m + 1;
+        rs[l] = w, w += m + 2;
+    }
+    const uint64_t nchunks = nodes[0];
+    const unsigned tgrid = (unsigned)((nchunks + kGbWarps - 1) / kGbWarps);
+    if (delta)
+        gb_table_kernel<true><<<tgrid, 256, 0, stream>>>(in, len, nchunks, tc[0], tx[0], ts[0]);
+    else
+        gb_table_kernel<false><<<tgrid, 256, 0, stream>>>(in, len, nchunks, tc[0], tx[0], nullptr);
+    int nl = 1;
+    for (uint64_t l = 0; l + 1 < L; ++l, ++nl)
+        gb_compose_kernel<<<(unsigned)((nodes[l + 1] + kGbTreeWarps - 1) / kGbTreeWarps), 32 * kGbTreeWarps, 0,
+                            stream>>>(tc[l], tx[l], delta ? ts[l] : nullptr, nodes[l], tc[l + 1], tx[l + 1],
+                                      delta ? ts[l + 1] : nullptr, nodes[l + 1]);
+    const uint64_t ngroups = (n + 3) >> 2;
+    // root: the top level's single node, entered at 0
+    gb_expand_kernel<<<1, 32 * kGbTreeWarps, 0, stream>>>(tc[L - 1], tx[L - 1], delta ? ts[L - 1] : nullptr, 1,
+                                                          nullptr, nullptr, nullptr, 1, re[L - 1], rc[L - 1],
+                                                          rs[L - 1], 1, base, ngroups, status, epoch);
+    ++nl;
+    for (uint64_t l = L - 1; l > 0; --l, ++nl)
+        gb_expand_kernel<<<(unsigned)((nodes[l] + kGbTreeWarps - 1) / kGbTreeWarps), 32 * kGbTreeWarps, 0,
+                           stream>>>(tc[l - 1], tx[l - 1], delta ? ts[l - 1] : nullptr, nodes[l - 1], re[l], rc[l],
+                                     rs[l], nodes[l], re[l - 1], rc[l - 1], rs[l - 1], 0, base, ngroups, status,
+                                     epoch);
+    if (delta)
+        gb_decode_kernel<true><<<tgrid, 256, 0, stream>>>(in, len, n, nchunks, re[0], rc[0], rs[0], out, d_last,
+                                                          status, epoch);
+    else
+        gb_decode_kernel<false><<<tgrid, 256, 0, stream>>>(in, len, n, nchunks, re[0], rc[0], rs[0], out, d_last,
+                                                           status, epoch);
+    *launches = nl + 1;
+    return cudaGetLastError();
+}
+
+cudaError_t launch_gb_encode(const uint32_t* in, uint64_t n, int delta, uint32_t prev, uint8_t* out,
+                             uint64_t* d_out_len, void* meta_ws, unsigned long long* status, uint32_t epoch,
+                             cudaStream_t stream, int* launches) {
+    cudaError_t e = launch_size_scan(in, n, delta, prev, meta_ws, d_out_len, status, epoch, stream);
+    if (e != cudaSuccess) return e;
+    const DecodeMeta m = carve_decode_meta(meta_ws, n);
+    const uint64_t ngroups = (n + 3) >> 2;
+    const uint64_t nsub = (ngroups + kWTGroups - 1) / kWTGroups;
+    const unsigned grid = (unsigned)((nsub + kGbWarps - 1) / kGbWarps);
+    if (delta)
+        gb_encode_kernel<true><<<grid, 256, 0, stream>>>(in, n, prev, out, m);
+    else
+        gb_encode_kernel<false><<<grid, 256, 0, stream>>>(in, n, prev, out, m);
+    *launches = 2;
+    return cudaGetLastError();
+}
+
+}  // namespace bcgpu

@@ -62,6 +62,18 @@ cudaError_t launch_encode_piece(const uint32_t* in, uint64_t n, int delta, uint3
                                 uint64_t* d_out_len, void* meta_ws, unsigned long long* status, uint32_t epoch,
                                 uint32_t c0, uint32_t c1, cudaStream_t stream);
 unsigned long long* encode_running_ptr(void* meta_ws, uint64_t n);
+// size scan alone (per-sub-tile data offsets in meta_ws, total size to d_out_len); 1 launch
+cudaError_t launch_size_scan(const uint32_t* in, uint64_t n, int delta, uint32_t prev, void* meta_ws,
+                             uint64_t* d_out_len, unsigned long long* status, uint32_t epoch, cudaStream_t stream);
+// varint-GB (svb_gb.cu): encode = size scan + group writer; decode = chunk tables, tree
+// compose / expand, group decode.  The decode workspace is gb_decode_ws_bytes(len) bytes.
+cudaError_t launch_gb_encode(const uint32_t* in, uint64_t n, int delta, uint32_t prev, uint8_t* out,
+                             uint64_t* d_out_len, void* meta_ws, unsigned long long* status, uint32_t epoch,
+                             cudaStream_t stream, int* launches);
+size_t gb_decode_ws_bytes(uint64_t len);
+cudaError_t launch_gb_decode(const uint8_t* in, uint64_t len, uint64_t n, int delta, uint32_t base, uint32_t* out,
+                             uint32_t* d_last, void* ws, unsigned long long* status, uint32_t epoch,
+                             cudaStream_t stream, int* launches);
 uint64_t encode_slot_bytes(uint64_t n);
 cudaError_t launch_block_offsets(const uint8_t* in, uint64_t n, uint64_t* d_offsets, const LookbackArgs& lb,
                                  cudaStream_t stream);

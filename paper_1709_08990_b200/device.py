@@ -81,6 +81,22 @@ class DeviceCodec:
         _check(lib.bcgpu_svb_decode_device(self._ctx, _ptr(data), in_len, n, int(delta), base & 0xFFFFFFFF,
                                            _ptr(out), _ptr(last), _stream(stream)), "svb_decode")
 
+    def gb_encode(self, values: torch.Tensor, out: torch.Tensor, out_len: torch.Tensor, *, n: int | None = None,
+                  delta: bool = False, prev: int = 0, stream=None) -> None:
+        """varint-GB encode (varint_gb.hpp:19; delta: transform seeded with prev first) into ``out``
+        (capacity >= ceil(n/4)+4n); the exact length lands in ``out_len``."""
+        n = values.numel() if n is None else n
+        _check(lib.bcgpu_gb_encode_device(self._ctx, _ptr(values), n, int(delta), prev & 0xFFFFFFFF, _ptr(out),
+                                          out.numel() * out.element_size(), _ptr(out_len), _stream(stream)),
+               "gb_encode")
+
+    def gb_decode(self, data: torch.Tensor, n: int, out: torch.Tensor, *, in_len: int | None = None,
+                  delta: bool = False, base: int = 0, last: torch.Tensor | None = None, stream=None) -> None:
+        """gb_decode / gb_decode_delta (varint_gb.hpp:21-25) of ``data[:in_len]`` into ``out``."""
+        in_len = data.numel() if in_len is None else in_len
+        _check(lib.bcgpu_gb_decode_device(self._ctx, _ptr(data), in_len, n, int(delta), base & 0xFFFFFFFF,
+                                          _ptr(out), _ptr(last), _stream(stream)), "gb_decode")
+
     def block_offsets(self, data: torch.Tensor, n: int, out: torch.Tensor, *, in_len: int | None = None,
                       stream=None) -> None:
         in_len = data.numel() if in_len is None else in_len

@@ -90,3 +90,25 @@ def test_payload_length_identity():
         v = rng.integers(0, 2**32, n, dtype=np.uint64).astype(np.uint32)
         e = oracle.encode(v)
         assert P.svb_payload_length(e, n) == len(e)
+
+
+def test_container_varint_gb():
+    # varint-GB payloads are verified by walking the group chain
+    rng = np.random.default_rng(4)
+    for n in (0, 1, 3, 4, 5, 999, 4096):
+        v = (rng.integers(0, 2**32, n, dtype=np.uint64) >> rng.integers(0, 32, n).astype(np.uint64)).astype(np.uint32)
+        b = P.EncodedBuffer(P.codec_id.varint_gb, n, False, oracle.gb_encode(v))
+        f = P.write_container(b)
+        assert f[4] == 1 and len(f) == 14 + len(b.bytes) and P.read_container(f) == b
+        if n:
+            for bad_count in (n + 1, n - 1 if n > 1 else n + 4):
+                with pytest.raises(P.CodecError) as e:
+                    P.read_container(f[:6] + bad_count.to_bytes(4, "little") + f[10:])
+                assert e.value.code == P.errc.length_mismatch
+    # a payload shorter than its chain (declared length cut with the count kept)
+    v = np.arange(100, dtype=np.uint32) * 1000
+    p = oracle.gb_encode(v)
+    f = P.write_container(P.EncodedBuffer(P.codec_id.varint_gb, 100, False, p[:-3]))
+    with pytest.raises(P.CodecError) as e:
+        P.read_container(f)
+    assert e.value.code == P.errc.length_mismatch
