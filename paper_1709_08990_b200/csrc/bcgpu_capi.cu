@@ -908,11 +908,13 @@ int bcgpu_gb_decode_device(bcgpu_ctx* c, const uint8_t* d_in, size_t in_len, siz
     void* ws = nullptr;
     int st = ensure_gbws(c, in_len, s, &ws);
     if (st) return st;
-    st = next_epoch(c, s);
+    // delta: the chunk carries come from a decoupled look-back (one status word per chunk)
+    LookbackArgs lb;
+    st = make_lookback(c, gb_decode_chunks(in_len), 1, s, &lb);
     if (st) return st;
     int launches = 0;
-    BC_CUDA(launch_gb_decode(d_in, in_len, n, delta, base, d_out, d_last, ws, status_ptr(c), c->epoch, s,
-                             &launches));
+    BC_CUDA(launch_gb_decode(d_in, in_len, n, delta, base, d_out, d_last, ws, lb.sum_status, status_ptr(c), c->epoch,
+                             s, &launches));
     g_launches.fetch_add((uint64_t)launches);
     return BCGPU_OK;
 }

@@ -47,7 +47,9 @@ constexpr uint32_t kGbChunk = 4096;                 // compressed bytes per deco
 constexpr uint32_t kGbStage = kGbChunk + 64;        // staged: <16 phase + chunk + the last group's overhang
 constexpr int kGbE = 17;                            // entry offsets 0..16 (a group spans <= 17 bytes)
 constexpr uint32_t kGbFan = 32;                     // tables composed per tree node
-constexpr int kGbWarps = 8;                         // chunks per CTA (table / decode kernels)
+constexpr int kGbWarps = 4;                         // chunks per CTA (table / decode kernels)
+constexpr uint32_t kGbSeg = 132;                    // bytes per lane segment of a chunk (31 * 132 + 4 = 4096)
+constexpr int kGbEncWarps = 8;                      // sub-tiles per CTA (encode)
 constexpr int kGbTreeWarps = 4;                     // tree nodes per CTA (compose / expand kernels)
 constexpr uint32_t kGbMaxGroups = kGbChunk / 5 + 2;  // groups starting in one chunk (>= 5 B each but the last)
 constexpr uint32_t kGbEncBuf = kWTGroups + 4 * kWTInts + 32;  // one sub-tile's groups + phase
@@ -101,12 +103,12 @@ template <bool kDelta>
 __global__ void __launch_bounds__(256)
     gb_encode_kernel(const uint32_t* __restrict__ in, uint64_t n, uint32_t prev, uint8_t* __restrict__ out,
                      DecodeMeta meta) {
-    __shared__ __align__(16) uint8_t sbuf[kGbWarps][kGbEncBuf];
+    __shared__ __align__(16) uint8_t sbuf[kGbEncWarps][kGbEncBuf];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint64_t ngroups = (n + 3) >> 2;
     const uint32_t tail_r = (uint32_t)(n & 3);
     const uint64_t nsub = (ngroups + kWTGroups - 1) / kWTGroups;
-    const uint64_t s = (uint64_t)blockIdx.x * kGbWarps + warp;
+    const uint64_t s = (uint64_t)blockIdx.x * kGbEncWarps + warp;
     if (s >= nsub) return;
     const uint64_t g0 = s * kWTGroups;
     const uint64_t o0 = meta.chunkpre[s / kChunkSubs] + meta.localpre[s] + g0;  // data before + control bytes before
@@ -167,11 +169,77 @@ __global__ void __launch_bounds__(256)
 // ---------------------------------------------------------------------------
 // decode 1: per-chunk transfer tables
 // ---------------------------------------------------------------------------
+// Lane l owns segment [132 l, 132 (l + 1)) of the chunk (lane 31: [4092, 4096)); the
+// 132-byte stride puts the 32 lanes' byte reads in 32 different banks.  Walking its
+// segment from the end down, a lane computes for every byte position p the chain
+// started there: F(p) = the first position >= the segment end it reaches, the groups it
+// starts and (delta) the sum of their values -- from the entry of next(p) = p + group
+// bytes, at most 17 ahead, so a 32-entry ring per lane holds all it needs.  The ring
+// ends up holding the segment's lowest 32 positions: its transfer table for entries
+// a .. a + 16.  A chunk table is 32 segment lookups per entry.
+struct GbRing {
+    uint16_t ec[32][32];  // [position & 31][lane]: exit (5 bits) | count << 5
+};
+struct GbRingSum {
+    uint32_t v[32][32];  // [position & 31][lane]: value sum (delta)
+};
+
+__device__ __forceinline__ void gb_seg_bounds(uint32_t l, uint32_t clen, uint32_t& a, uint32_t& b) {
+    a = kGbSeg * l < clen ? kGbSeg * l : clen;
+    const uint32_t e = l == 31 ? kGbChunk : kGbSeg * (l + 1);
+    b = e < clen ? e : clen;
+}
+
 template <bool kDelta>
-__global__ void __launch_bounds__(256)
+__device__ __forceinline__ void gb_segment_dp(uint32_t sa, uint32_t clen, GbRing& R, GbRingSum* S) {
+    const int lane = threadIdx.x & 31;
+    uint32_t a, b;
+    gb_seg_bounds((uint32_t)lane, clen, a, b);
+    for (uint32_t p = b; p > a;) {
+        --p;
+        const uint32_t c = lds8(sa + p);
+        const uint32_t q = p + gb_group_bytes(c);
+        uint32_t ec, sm = 0;
+        if constexpr (kDelta) {
+            const uint4 v = gb_group_values(sa + p, c, 4);
+            sm = v.x + v.y + v.z + v.w;
+        }
+        if (q >= b) {
+            ec = (q - b) | (1u << 5);
+        } else {
+            ec = (uint32_t)R.ec[q & 31][lane] + (1u << 5);
+            if constexpr (kDelta) sm += S->v[q & 31][lane];
+        }
+        R.ec[p & 31][lane] = (uint16_t)ec;
+        if constexpr (kDelta) S->v[p & 31][lane] = sm;
+    }
+}
+
+// follow the chain from chunk position pos through segments [s0, s1): groups and sums added
+template <bool kDelta>
+__device__ __forceinline__ uint32_t gb_chase(const GbRing& R, const GbRingSum* S, uint32_t clen, uint32_t pos,
+                                             uint32_t s0, uint32_t s1, uint32_t& cnt, uint32_t& sum) {
+    for (uint32_t s = s0; s < s1; ++s) {
+        uint32_t a, b;
+        gb_seg_bounds(s, clen, a, b);
+        if (pos >= b) continue;
+        const uint32_t t = R.ec[pos & 31][s];
+        cnt += t >> 5;
+        if constexpr (kDelta) sum += S->v[pos & 31][s];
+        pos = b + (t & 31u);
+    }
+    return pos;
+}
+
+// Tables carry exits and group counts only: the delta decode's value carries come from
+// a look-back over chunk sums in gb_decode_kernel, so no value is summed here (at most
+// byte positions the "control byte" is really data, and summing its would-be group cost
+// more than the whole table).
+__global__ void __launch_bounds__(32 * kGbWarps)
     gb_table_kernel(const uint8_t* __restrict__ in, uint64_t len, uint64_t nchunks, uint32_t* __restrict__ tcnt,
-                    uint32_t* __restrict__ texit, uint32_t* __restrict__ tsum) {
+                    uint32_t* __restrict__ texit, uint16_t* __restrict__ segtab) {
     __shared__ __align__(16) uint8_t sbuf[kGbWarps][kGbStage];
+    __shared__ GbRing ring[kGbWarps];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint64_t chunk = (uint64_t)blockIdx.x * kGbWarps + warp;
     if (chunk >= nchunks) return;
@@ -179,22 +247,23 @@ __global__ void __launch_bounds__(256)
     const uint32_t clen = (uint32_t)(len - cs < kGbChunk ? len - cs : kGbChunk);
     const uint32_t ph = gb_stage(in, len, cs, clen + 32, sbuf[warp]);
     __syncwarp();
+    const uint32_t sa = sh_addr(sbuf[warp]) + ph;
+    gb_segment_dp<false>(sa, clen, ring[warp], nullptr);
+    // the segment tables for the decode pass: entry e of lane l's segment, [e][l]
+    {
+        uint32_t a, b;
+        gb_seg_bounds((uint32_t)lane, clen, a, b);
+        uint16_t* st = segtab + chunk * (kGbE * 32);
+#pragma unroll
+        for (int e = 0; e < kGbE; ++e) st[e * 32 + lane] = ring[warp].ec[(a + e) & 31][lane];
+    }
+    __syncwarp();
     if (lane < kGbE) {
-        const uint32_t sa = sh_addr(sbuf[warp]) + ph;
-        uint32_t pos = (uint32_t)lane, cnt = 0, sum = 0;
-        while (pos < clen) {
-            const uint32_t c = lds8(sa + pos);
-            if constexpr (kDelta) {
-                const uint4 v = gb_group_values(sa + pos, c, 4);
-                sum += v.x + v.y + v.z + v.w;
-            }
-            pos += gb_group_bytes(c);
-            ++cnt;
-        }
+        uint32_t cnt = 0, sum = 0;
+        const uint32_t pos = gb_chase<false>(ring[warp], nullptr, clen, (uint32_t)lane, 0, 32, cnt, sum);
         const uint64_t i = chunk * kGbE + lane;
         tcnt[i] = cnt;
         texit[i] = pos - clen;
-        if constexpr (kDelta) tsum[i] = sum;
     }
 }
 
@@ -275,12 +344,14 @@ __global__ void __launch_bounds__(32 * kGbTreeWarps)
 // decode 3: groups of each chunk from its resolved entry
 // ---------------------------------------------------------------------------
 template <bool kDelta>
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(32 * kGbWarps)
     gb_decode_kernel(const uint8_t* __restrict__ in, uint64_t len, uint64_t n, uint64_t nchunks,
                      const uint32_t* __restrict__ rentry, const uint32_t* __restrict__ rcnt,
-                     const uint32_t* __restrict__ rsum, uint32_t* __restrict__ out, uint32_t* __restrict__ d_last,
-                     unsigned long long* status, uint32_t epoch) {
+                     const uint16_t* __restrict__ segtab, uint32_t base, uint64_t* __restrict__ lstatus,
+                     uint32_t* __restrict__ out, uint32_t* __restrict__ d_last, unsigned long long* status,
+                     uint32_t epoch) {
     __shared__ __align__(16) uint8_t sbuf[kGbWarps][kGbStage];
+    __shared__ __align__(16) uint16_t stab[kGbWarps][kGbE * 32];
     __shared__ uint16_t spos[kGbWarps][kGbMaxGroups];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint64_t chunk = (uint64_t)blockIdx.x * kGbWarps + warp;
@@ -294,19 +365,62 @@ __global__ void __launch_bounds__(256)
     const uint32_t ph = gb_stage(in, len, cs, clen + 32, sbuf[warp]);
     __syncwarp();
     const uint32_t sa = sh_addr(sbuf[warp]) + ph;
-    uint32_t m = 0;
-    if (lane == 0) {
-        const uint64_t left = ngroups - kb;
-        const uint32_t lim = (uint32_t)(left < kGbMaxGroups ? left : kGbMaxGroups);
-        uint32_t pos = rentry[chunk];
-        while (pos < clen && m < lim) {
-            spos[warp][m++] = (uint16_t)pos;
+    // the chunk's segment tables (gb_table_kernel), then every lane finds where the true
+    // chain enters its segment and lists the group starts in it
+    {
+        const uint4* src = reinterpret_cast<const uint4*>(segtab + chunk * (kGbE * 32));
+        uint4* dst = reinterpret_cast<uint4*>(stab[warp]);
+        for (uint32_t g = lane; g < kGbE * 32 * 2 / 16; g += 32) dst[g] = __ldg(src + g);
+    }
+    __syncwarp();
+    uint32_t i = 0, pos = rentry[chunk];
+    for (uint32_t s = 0; s < (uint32_t)lane; ++s) {
+        uint32_t a, b;
+        gb_seg_bounds(s, clen, a, b);
+        if (pos >= b) continue;
+        const uint32_t t = stab[warp][(pos - a) * 32 + s];
+        i += t >> 5;
+        pos = b + (t & 31u);
+    }
+    const uint64_t left = ngroups - kb;
+    const uint32_t lim = (uint32_t)(left < kGbMaxGroups ? left : kGbMaxGroups);  // groups of this call
+    {
+        uint32_t a, b;
+        gb_seg_bounds((uint32_t)lane, clen, a, b);
+        while (pos < b && i < lim) {
+            spos[warp][i++] = (uint16_t)pos;
             pos += gb_group_bytes(lds8(sa + pos));
         }
     }
-    m = __shfl_sync(kFull, m, 0);
+    uint32_t m = __reduce_max_sync(kFull, i);
+    m = m < lim ? m : lim;
     __syncwarp();
-    uint32_t run = kDelta ? rsum[chunk] : 0u;
+    uint32_t run = 0;
+    if constexpr (kDelta) {
+        // the chunk's value sum, then its carry by decoupled look-back over the chunks before
+        // it (lower chunks are dispatched first, so they are resident or done)
+        uint32_t tot = 0;
+        for (uint32_t r = 0; r < m; r += 32) {
+            const uint32_t i = r + lane;
+            const uint32_t k = i < m ? group_count(kb + i, ngroups, tail_r) : 0u;
+            if (k) {
+                const uint32_t p = spos[warp][i];
+                const uint4 v = gb_group_values(sa + p, lds8(sa + p), k);
+                tot += v.x + v.y + v.z + v.w;
+            }
+        }
+        tot = __reduce_add_sync(kFull, tot);
+        if (chunk == 0) {
+            if (lane == 0) st_relaxed_gpu(lstatus, pack_status(epoch, kFlagInclusive, (uint64_t)base + tot));
+            run = base;
+        } else {
+            if (lane == 0) st_relaxed_gpu(status_slot(lstatus, chunk), pack_status(epoch, kFlagAggregate, tot));
+            const uint64_t ex = lookback_exclusive_wide(lstatus, (uint32_t)chunk, epoch);
+            if (lane == 0)
+                st_relaxed_gpu(status_slot(lstatus, chunk), pack_status(epoch, kFlagInclusive, ex + tot));
+            run = (uint32_t)ex;
+        }
+    }
     const bool out16 = (((uintptr_t)out) & 15) == 0;
     for (uint32_t r = 0; r < m; r += 32) {
         const uint32_t i = r + lane;
@@ -355,15 +469,17 @@ static uint64_t gb_levels(uint64_t len, uint64_t* nodes) {
     return L;
 }
 
+uint64_t gb_decode_chunks(uint64_t len) { return len ? (len + kGbChunk - 1) / kGbChunk : 1; }
+
 size_t gb_decode_ws_bytes(uint64_t len) {
     uint64_t nodes[16], L = gb_levels(len, nodes), words = 0;
     for (uint64_t l = 0; l < L; ++l) words += nodes[l] * (3 * kGbE + 3) + 4;
-    return (size_t)(4 * words + 256);
+    return (size_t)(4 * words + 256 + nodes[0] * (2 * kGbE * 32) + 16);
 }
 
 cudaError_t launch_gb_decode(const uint8_t* in, uint64_t len, uint64_t n, int delta, uint32_t base, uint32_t* out,
-                             uint32_t* d_last, void* ws, unsigned long long* status, uint32_t epoch,
-                             cudaStream_t stream, int* launches) {
+                             uint32_t* d_last, void* ws, uint64_t* lstatus, unsigned long long* status,
+                             uint32_t epoch, cudaStream_t stream, int* launches) {
     uint64_t nodes[16];
     const uint64_t L = gb_levels(len, nodes);
     uint32_t* tc[16];
@@ -383,33 +499,30 @@ cudaError_t launch_gb_decode(const uint8_t* in, uint64_t len, uint64_t n, int de
         rs[l] = w, w += m + 2;
     }
     const uint64_t nchunks = nodes[0];
+    uint16_t* segtab = reinterpret_cast<uint16_t*>((reinterpret_cast<uintptr_t>(w) + 15) & ~(uintptr_t)15);
     const unsigned tgrid = (unsigned)((nchunks + kGbWarps - 1) / kGbWarps);
-    if (delta)
-        gb_table_kernel<true><<<tgrid, 256, 0, stream>>>(in, len, nchunks, tc[0], tx[0], ts[0]);
-    else
-        gb_table_kernel<false><<<tgrid, 256, 0, stream>>>(in, len, nchunks, tc[0], tx[0], nullptr);
+    gb_table_kernel<<<tgrid, 32 * kGbWarps, 0, stream>>>(in, len, nchunks, tc[0], tx[0], segtab);
     int nl = 1;
     for (uint64_t l = 0; l + 1 < L; ++l, ++nl)
         gb_compose_kernel<<<(unsigned)((nodes[l + 1] + kGbTreeWarps - 1) / kGbTreeWarps), 32 * kGbTreeWarps, 0,
-                            stream>>>(tc[l], tx[l], delta ? ts[l] : nullptr, nodes[l], tc[l + 1], tx[l + 1],
-                                      delta ? ts[l + 1] : nullptr, nodes[l + 1]);
+                            stream>>>(tc[l], tx[l], nullptr, nodes[l], tc[l + 1], tx[l + 1], nullptr, nodes[l + 1]);
     const uint64_t ngroups = (n + 3) >> 2;
     // root: the top level's single node, entered at 0
-    gb_expand_kernel<<<1, 32 * kGbTreeWarps, 0, stream>>>(tc[L - 1], tx[L - 1], delta ? ts[L - 1] : nullptr, 1,
+    gb_expand_kernel<<<1, 32 * kGbTreeWarps, 0, stream>>>(tc[L - 1], tx[L - 1], nullptr, 1,
                                                           nullptr, nullptr, nullptr, 1, re[L - 1], rc[L - 1],
                                                           rs[L - 1], 1, base, ngroups, status, epoch);
     ++nl;
     for (uint64_t l = L - 1; l > 0; --l, ++nl)
         gb_expand_kernel<<<(unsigned)((nodes[l] + kGbTreeWarps - 1) / kGbTreeWarps), 32 * kGbTreeWarps, 0,
-                           stream>>>(tc[l - 1], tx[l - 1], delta ? ts[l - 1] : nullptr, nodes[l - 1], re[l], rc[l],
+                           stream>>>(tc[l - 1], tx[l - 1], nullptr, nodes[l - 1], re[l], rc[l],
                                      rs[l], nodes[l], re[l - 1], rc[l - 1], rs[l - 1], 0, base, ngroups, status,
                                      epoch);
     if (delta)
-        gb_decode_kernel<true><<<tgrid, 256, 0, stream>>>(in, len, n, nchunks, re[0], rc[0], rs[0], out, d_last,
-                                                          status, epoch);
+        gb_decode_kernel<true><<<tgrid, 32 * kGbWarps, 0, stream>>>(in, len, n, nchunks, re[0], rc[0], segtab, base, lstatus,
+                                                                    out, d_last, status, epoch);
     else
-        gb_decode_kernel<false><<<tgrid, 256, 0, stream>>>(in, len, n, nchunks, re[0], rc[0], rs[0], out, d_last,
-                                                           status, epoch);
+        gb_decode_kernel<false><<<tgrid, 32 * kGbWarps, 0, stream>>>(in, len, n, nchunks, re[0], rc[0], segtab, base,
+                                                                     nullptr, out, d_last, status, epoch);
     *launches = nl + 1;
     return cudaGetLastError();
 }
@@ -422,7 +535,7 @@ cudaError_t launch_gb_encode(const uint32_t* in, uint64_t n, int delta, uint32_t
     const DecodeMeta m = carve_decode_meta(meta_ws, n);
     const uint64_t ngroups = (n + 3) >> 2;
     const uint64_t nsub = (ngroups + kWTGroups - 1) / kWTGroups;
-    const unsigned grid = (unsigned)((nsub + kGbWarps - 1) / kGbWarps);
+    const unsigned grid = (unsigned)((nsub + kGbEncWarps - 1) / kGbEncWarps);
     if (delta)
         gb_encode_kernel<true><<<grid, 256, 0, stream>>>(in, n, prev, out, m);
     else

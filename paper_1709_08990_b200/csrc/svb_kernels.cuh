@@ -71,9 +71,11 @@ cudaError_t launch_gb_encode(const uint32_t* in, uint64_t n, int delta, uint32_t
                              uint64_t* d_out_len, void* meta_ws, unsigned long long* status, uint32_t epoch,
                              cudaStream_t stream, int* launches);
 size_t gb_decode_ws_bytes(uint64_t len);
+// delta: lstatus = look-back status words of >= ceil(len / 4096) chunks tagged with epoch
 cudaError_t launch_gb_decode(const uint8_t* in, uint64_t len, uint64_t n, int delta, uint32_t base, uint32_t* out,
-                             uint32_t* d_last, void* ws, unsigned long long* status, uint32_t epoch,
-                             cudaStream_t stream, int* launches);
+                             uint32_t* d_last, void* ws, uint64_t* lstatus, unsigned long long* status,
+                             uint32_t epoch, cudaStream_t stream, int* launches);
+uint64_t gb_decode_chunks(uint64_t len);
 uint64_t encode_slot_bytes(uint64_t n);
 cudaError_t launch_block_offsets(const uint8_t* in, uint64_t n, uint64_t* d_offsets, const LookbackArgs& lb,
                                  cudaStream_t stream);
