@@ -1,6 +1,6 @@
 // bytecodec_host.cpp -- the reference's C++ API (namespace bytecodec) on top of
 // the C ABI.  Signatures: reference proj/core/include/bytecodec/codec.hpp:24-96
-// and stream_vbyte.hpp:32-54; semantics: SPEC.md:270-402.
+// stream_vbyte.hpp:32-54 and varint_gb.hpp:19-31; semantics: SPEC.md:164-214, 270-402.
 //
 // Each host thread owns one bcgpu_ctx per device (a ctx is single-stream).
 // Errors from the GPU path surface as codec_error{errc} exactly where the
@@ -8,6 +8,7 @@
 #include <map>
 #include <memory>
 #include <mutex>
+#include <cstddef>
 #include <string>
 
 #include "bcgpu/bcgpu.h"
@@ -15,6 +16,7 @@
 #include "bytecodec/stream_vbyte.hpp"
 #include "bytecodec/container.hpp"
 #include "bytecodec/query.hpp"
+#include "bytecodec/varint_gb.hpp"
 
 namespace bytecodec {
 namespace {
@@ -48,7 +50,24 @@ bcgpu_ctx* ctx() {
 
 void require_svb(codec_id id) {
     if (id != codec_id::stream_vbyte)
-        throw codec_error(errc::unsupported, "only codec_id::stream_vbyte is implemented on the GPU path");
+        throw codec_error(errc::unsupported, "this operation is defined for codec_id::stream_vbyte only");
+}
+
+// the codecs with a GPU path: Stream VByte and varint-GB
+void require_gpu_codec(codec_id id) {
+    if (id != codec_id::stream_vbyte && id != codec_id::varint_gb)
+        throw codec_error(errc::unsupported, "only stream_vbyte and varint_gb are implemented on the GPU path");
+}
+
+std::vector<uint8_t> gb_encode_impl(std::span<const uint32_t> values, bool delta, uint32_t prev) {
+    std::vector<uint8_t> out(bcgpu_svb_max_compressed_bytes(values.size()));
+    size_t len = 0;
+    const int st = bcgpu_gb_encode_host(ctx(), values.data(), values.size(), delta ? 1 : 0, prev, out.data(),
+                                        out.size(), &len);
+    if (st) throw_status(st, "gb_encode");
+    out.resize(len);
+    out.shrink_to_fit();
+    return out;
 }
 
 std::vector<uint8_t> encode_impl(std::span<const uint32_t> values, bool delta, uint32_t prev) {
@@ -215,39 +234,84 @@ std::vector<uint32_t> select(const encoded_buffer& buf, std::span<const size_t> 
 
 uint32_t select(const encoded_buffer& buf, size_t i) { return select(buf, std::span<const size_t>(&i, 1))[0]; }
 
+// ---- varint-GB (varint_gb.hpp) ----
+std::vector<uint8_t> gb_encode(std::span<const uint32_t> values) { return gb_encode_impl(values, false, 0); }
+
+std::vector<uint8_t> gb_encode_delta(std::span<const uint32_t> values, uint32_t prev) {
+    return gb_encode_impl(values, true, prev);
+}
+
+void gb_decode(std::span<const uint8_t> bytes, size_t n, uint32_t* out) {
+    const int st = bcgpu_gb_decode_host(ctx(), bytes.data(), bytes.size(), n, 0, 0, out, nullptr);
+    if (st) throw_status(st, "gb_decode");
+}
+
+std::vector<uint32_t> gb_decode(std::span<const uint8_t> bytes, size_t n) {
+    std::vector<uint32_t> out(n);
+    gb_decode(bytes, n, out.data());
+    return out;
+}
+
+uint32_t gb_decode_delta(std::span<const uint8_t> bytes, size_t n, uint32_t base, uint32_t* out) {
+    uint32_t last = base;
+    const int st = bcgpu_gb_decode_host(ctx(), bytes.data(), bytes.size(), n, 1, base, out, &last);
+    if (st) throw_status(st, "gb_decode_delta");
+    return last;
+}
+
+namespace detail {
+const uint8_t* gb_decode_group_general(uint8_t control, const uint8_t* data, const uint8_t* end, size_t k,
+                                       uint32_t* out) {
+    for (size_t i = 0; i < k && i < 4; ++i) {
+        const uint32_t l = ((control >> (2 * i)) & 3u) + 1u;
+        if (end - data < static_cast<std::ptrdiff_t>(l)) return nullptr;
+        uint32_t x = 0;
+        for (uint32_t b = 0; b < l; ++b) x |= static_cast<uint32_t>(data[b]) << (8 * b);
+        out[i] = x;
+        data += l;
+    }
+    return data;
+}
+}  // namespace detail
+
+// ---- codec-generic (codec.hpp:84-96): Stream VByte and varint-GB ----
 std::vector<uint8_t> encode_payload(codec_id id, std::span<const uint32_t> values) {
-    require_svb(id);
-    return svb_encode(values);
+    require_gpu_codec(id);
+    return id == codec_id::varint_gb ? gb_encode(values) : svb_encode(values);
 }
 
 void decode_payload(codec_id id, std::span<const uint8_t> bytes, size_t n, uint32_t* out) {
-    require_svb(id);
-    svb_decode(bytes, n, out);
+    require_gpu_codec(id);
+    if (id == codec_id::varint_gb)
+        gb_decode(bytes, n, out);
+    else
+        svb_decode(bytes, n, out);
 }
 
 uint32_t decode_payload_delta(codec_id id, std::span<const uint8_t> bytes, size_t n, uint32_t base, uint32_t* out) {
-    require_svb(id);
-    return svb_decode_delta(bytes, n, base, out);
+    require_gpu_codec(id);
+    return id == codec_id::varint_gb ? gb_decode_delta(bytes, n, base, out) : svb_decode_delta(bytes, n, base, out);
 }
 
 encoded_buffer encode(codec_id id, std::span<const uint32_t> values, bool delta) {
-    require_svb(id);
+    require_gpu_codec(id);
     if (values.size() > 0xFFFFFFFFull) throw codec_error(errc::out_of_range, "count exceeds uint32");
     encoded_buffer b;
     b.codec = id;
     b.count = static_cast<uint32_t>(values.size());
     b.delta = delta;
-    b.bytes = encode_impl(values, delta, 0);  // base 0
+    // base 0
+    b.bytes = id == codec_id::varint_gb ? gb_encode_impl(values, delta, 0) : encode_impl(values, delta, 0);
     return b;
 }
 
 std::vector<uint32_t> decode(const encoded_buffer& buf) {
-    require_svb(buf.codec);
+    require_gpu_codec(buf.codec);
     std::vector<uint32_t> out(buf.count);
     if (buf.delta)
-        svb_decode_delta(buf.bytes, buf.count, 0, out.data());
+        decode_payload_delta(buf.codec, buf.bytes, buf.count, 0, out.data());
     else
-        svb_decode(buf.bytes, buf.count, out.data());
+        decode_payload(buf.codec, buf.bytes, buf.count, out.data());
     return out;
 }
 

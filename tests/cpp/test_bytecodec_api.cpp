@@ -1,8 +1,8 @@
 // C++ drop-in test: a reference-style caller of namespace bytecodec (reference
 // proj/core/include/bytecodec/{codec,stream_vbyte}.hpp signatures) linked
 // against libbytecodec_b200.so.  Checks SPEC golden vectors (SPEC.md:308-320,
-// 372-383, erratum E1), round trips, malformed input errors and the
-// random-access API.  Exit code 0 = pass.
+// 372-383, erratum E1), round trips, malformed input errors, the random-access
+// API and varint-GB (varint_gb.hpp).  Exit code 0 = pass.
 #include <cstdint>
 #include <cstdio>
 #include <cstdlib>
@@ -13,6 +13,7 @@
 #include "bytecodec/stream_vbyte.hpp"
 #include "bytecodec/container.hpp"
 #include "bytecodec/query.hpp"
+#include "bytecodec/varint_gb.hpp"
 
 using namespace bytecodec;
 
@@ -130,6 +131,38 @@ int main() {
         CHECK(seek(b, 3u) && seek(b, 3u)->index == 0);
         CHECK(!seek(b, 21u));
         CHECK(select(b, (size_t)1) == 7 && select(b, (size_t)3) == 20);
+    }
+    // varint-GB: Fig. 1a -> 0xC1 00 04 | 0C | 0A | 00 00 00 40; [5] -> 00 05
+    {
+        const std::vector<uint32_t> f1a = {1024, 12, 10, 1073741824};
+        const std::vector<uint8_t> f1a_bytes = {0xC1, 0x00, 0x04, 0x0C, 0x0A, 0x00, 0x00, 0x00, 0x40};
+        CHECK(gb_encode(f1a) == f1a_bytes);
+        CHECK(gb_encode(std::vector<uint32_t>{1, 2, 3, 1024}).size() == 6);
+        CHECK(gb_encode(std::vector<uint32_t>{5}) == (std::vector<uint8_t>{0x00, 0x05}));
+        CHECK(gb_decode(f1a_bytes, 4) == f1a);
+        CHECK(gb_decode(std::vector<uint8_t>{0, 1, 2, 3, 4}, 4) == (std::vector<uint32_t>{1, 2, 3, 4}));
+        uint32_t g[4] = {};
+        const uint8_t grp[] = {1, 2, 3, 4};
+        CHECK(detail::gb_decode_group_general(0, grp, grp + 4, 4, g) == grp + 4 && g[3] == 4);
+        CHECK(detail::gb_decode_group_general(0xFF, grp, grp + 4, 4, g) == nullptr);
+        std::mt19937 rng(5);
+        std::vector<uint32_t> v(10001);
+        uint32_t acc = 0;
+        for (auto& x : v) x = acc += rng() % 5000;
+        const encoded_buffer b = encode(codec_id::varint_gb, v, true);
+        CHECK(b.codec == codec_id::varint_gb && decode(b) == v);
+        std::vector<uint32_t> out(v.size());
+        CHECK(gb_decode_delta(gb_encode_delta(v, 0), v.size(), 0, out.data()) == v.back() && out == v);
+        const encoded_buffer r = read_container(write_container(b));
+        CHECK(r.codec == codec_id::varint_gb && r.bytes == b.bytes);
+        auto cut = f1a_bytes;
+        cut.pop_back();
+        try {
+            gb_decode(cut, 4);
+            CHECK(false);
+        } catch (const codec_error& e) {
+            CHECK(e.code() == errc::truncated);
+        }
     }
     if (failures) {
         std::fprintf(stderr, "%d failures\n", failures);
