@@ -39,9 +39,16 @@ t = trace.cpu().numpy().reshape(tiles, 8).astype(np.int64)
 t0 = t[:, 0].min()
 print(f"tiles={tiles} span={(t[:, 5].max() - t0) / 1e3:.1f} us")
 for name, a, b in [("issue->landed", 0, 2), ("wait for data", 1, 2), ("sum+publish", 2, 3), ("publish->resolved*", 3, 4),
-                   ("resolve->stored", 4, 5)]:
+                   ("resolve->stored", 4, 5), ("prod: lookahead+window", 6, 7), ("prod: window->issued", 7, 0)]:
     d = (t[:, b] - t[:, a]) / 1e3
     print(f"  {name:20s} p10={np.percentile(d, 10):6.2f} p50={np.median(d):6.2f} p90={np.percentile(d, 90):6.2f} max={d.max():6.2f} us")
 print("  (* resolved one round later, so this includes a whole round of work)")
 G = int(np.sum(t[:, 0] - t0 < 2000))  # rough
 print("  stored times (us) at 10/50/90%:", np.percentile((t[:, 5] - t0) / 1e3, [10, 50, 90]).round(2))
+
+# fused producer: time between its iterations (tile t -> t + G of the same CTA)
+starts = t[:, 6]
+if starts.max() > 0:
+    G = int(np.argmax(np.diff(starts[: 2048]) < 0)) if False else None
+    order = np.argsort(starts)
+    print("  producer iteration start spread (us):", np.percentile((starts - t0) / 1e3, [10, 50, 90]).round(2))
