@@ -601,11 +601,11 @@ __global__ void __launch_bounds__(kCTThreads + 32, 2)
     if (warp == kCTWarps) {
         // ---- producer: the tile's integers (and the 4 before them) -> stage ----
         const uintptr_t lo = (uintptr_t)in, hi = lo + 4 * n;
-        uint32_t k = 0;
-        for (uint32_t t = blockIdx.x; t < ntiles; t += G, ++k) {
-            const int st = (int)(k % kE1Stages);
+        uint32_t k = 0, ph = 0;
+        int st = 0;
+        for (uint32_t t = blockIdx.x; t < ntiles; t += G, ++k, st = st + 1 == kE1Stages ? 0 : st + 1, ph ^= st == 0) {
             uint8_t* stage = dsm + (uint32_t)st * kE1Stride;
-            if (k >= (uint32_t)kE1Stages) mbar_wait_parity_sleep(&sh.empty[st], ((k / kE1Stages) & 1u) ^ 1u);
+            if (k >= (uint32_t)kE1Stages) mbar_wait_parity_sleep(&sh.empty[st], ph ^ 1u);
             const uint64_t i0 = (uint64_t)t * kE1Ints;
             const uint64_t cnt = n - i0 < (uint64_t)kE1Ints ? n - i0 : (uint64_t)kE1Ints;
             const uintptr_t beg = (uintptr_t)(in + i0) - (t ? 16 : 0), end = (uintptr_t)(in + i0 + cnt);
@@ -629,23 +629,30 @@ __global__ void __launch_bounds__(kCTThreads + 32, 2)
     }
     // ---- consumers ----
     const int ct = threadIdx.x;
+    // look-back window of tile tp: tiles max(0, tp - G + 1) .. tp - 1, read as 16-B aligned
+    // pairs (as svb_decode1_kernel); each thread prefetches one pair
     auto window_lo = [&](uint32_t tp) -> uint32_t { return tp + 1 > G ? tp + 1 - G : 0u; };
-    unsigned long long pf0 = 0, pf1 = 0;
+    ulonglong2 pf = make_ulonglong2(0ull, 0ull);
     auto prefetch = [&](uint32_t tp) {
-        const uint32_t wl = window_lo(tp);
-        pf0 = wl + ct < tp ? ld_relaxed_u64(meta.agg + wl + ct) : 0ull;
-        pf1 = wl + ct + 256 < tp ? ld_relaxed_u64(meta.agg + wl + ct + 256) : 0ull;
+        const uint32_t e = (window_lo(tp) & ~1u) + 2u * (uint32_t)ct;
+        if (e < tp) pf = ld_relaxed_u64x2(meta.agg + e);
     };
     auto entry = [&](uint32_t j, unsigned long long v) -> uint32_t {
         while ((uint32_t)(v >> 32) != epoch) v = ld_relaxed_u64(meta.agg + j);
         return (uint32_t)v;
     };
+    auto pair_sum = [&](uint32_t e, ulonglong2 v, uint32_t wl, uint32_t tp) -> uint32_t {
+        uint32_t r = 0;
+        if (e >= wl) r += entry(e, v.x);
+        if (e + 1 < tp) r += entry(e + 1, v.y);
+        return r;
+    };
     auto resolve = [&](uint32_t tp, int st, int q) {
         const uint32_t wl = window_lo(tp);
         uint32_t part = 0;
-        if (wl + ct < tp) part += entry(wl + ct, pf0);
-        if (wl + ct + 256 < tp) part += entry(wl + ct + 256, pf1);
-        for (uint32_t j = wl + ct + 512; j < tp; j += 256) part += entry(j, ld_relaxed_u64(meta.agg + j));
+        const uint32_t e0 = (wl & ~1u) + 2u * (uint32_t)ct;
+        if (e0 < tp) part += pair_sum(e0, pf, wl, tp);
+        for (uint32_t e = e0 + 512; e < tp; e += 512) part += pair_sum(e, ld_relaxed_u64x2(meta.agg + e), wl, tp);
         part = __reduce_add_sync(kFull, part);
         if (lane == 0) sh.red[warp] = part;
         consumers_sync();
@@ -681,11 +688,12 @@ __global__ void __launch_bounds__(kCTThreads + 32, 2)
         if (lane == 0) mbar_arrive(&sh.empty[st]);
     };
 
-    uint32_t k = 0, tprev = 0;
-    for (uint32_t t = blockIdx.x; t < ntiles; t += G, ++k) {
-        const int st = (int)(k % kE1Stages);
+    uint32_t k = 0, tprev = 0, ph = 0;
+    int st = 0, q = 0, stp = 0, qp = 0;  // stage / wsum slot of this iteration and of the previous one
+    for (uint32_t t = blockIdx.x; t < ntiles;
+         t += G, ++k, stp = st, qp = q, st = st + 1 == kE1Stages ? 0 : st + 1, q = q == 2 ? 0 : q + 1, ph ^= st == 0) {
         if (k) prefetch(tprev);
-        mbar_wait_parity(&sh.full[st], (k / kE1Stages) & 1u);
+        mbar_wait_parity(&sh.full[st], ph);
         uint8_t* stage = dsm + (uint32_t)st * kE1Stride;
         const uint64_t s = (uint64_t)t * kCTWarps + warp;
         const uint64_t g0 = s * kWTGroups;
@@ -700,12 +708,10 @@ __global__ void __launch_bounds__(kCTThreads + 32, 2)
                 const bool small = enc_full_small_pack0<kDelta>(sin, prev_w, sin);
                 if (small) {
                     total = kWTInts;
-                    for (uint32_t i = lane; i < kWTGroups / 4; i += 32) {  // 256 zero control bytes
-                        uint8_t* c4 = cdst + 4 * i;
-                        if ((((uintptr_t)c4) & 3) == 0)
-                            *reinterpret_cast<uint32_t*>(c4) = 0u;
-                        else
-                            c4[0] = c4[1] = c4[2] = c4[3] = 0;
+                    if ((((uintptr_t)cdst) & 15) == 0) {  // 256 zero control bytes
+                        if (lane < (int)(kWTGroups / 16)) reinterpret_cast<uint4*>(cdst)[lane] = make_uint4(0, 0, 0, 0);
+                    } else {
+                        for (uint32_t i = lane; i < kWTGroups; i += 32) cdst[i] = 0;
                     }
                 } else {
                     uint32_t lens[kWTRows], qw[4];
@@ -748,15 +754,15 @@ __global__ void __launch_bounds__(kCTThreads + 32, 2)
             }
         }
         __syncwarp();
-        if (lane == 0) sh.wsum[k % 3][warp] = total;
+        if (lane == 0) sh.wsum[q][warp] = total;
         consumers_sync();
         if (ct == 0) {
             uint32_t a = 0;
 #pragma unroll
-            for (int w = 0; w < kCTWarps; ++w) a += sh.wsum[k % 3][w];
+            for (int w = 0; w < kCTWarps; ++w) a += sh.wsum[q][w];
             st_relaxed_u64(meta.agg + t, ((unsigned long long)epoch << 32) | a);
         }
-        if (k) resolve(tprev, (int)((k - 1) % kE1Stages), (int)((k - 1) % 3));
+        if (k) resolve(tprev, stp, qp);
         tprev = t;
     }
     if (k) {

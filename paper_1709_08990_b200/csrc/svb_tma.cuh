@@ -37,17 +37,28 @@ __device__ __forceinline__ void mbar_wait_parity(uint64_t* bar, uint32_t parity)
         : "memory");
 }
 
-// the same for a warp that has nothing else to do meanwhile (a producer waiting for a free
-// stage): the suspend-time hint lets the thread sleep until the phase completes instead of
-// spinning on issue slots the consumer warps of its SM sub-partition need
-__device__ __forceinline__ void mbar_wait_parity_sleep(uint64_t* bar, uint32_t parity) {
+__device__ __forceinline__ bool mbar_test_parity(uint64_t* bar, uint32_t parity) {
+    uint32_t ok;
     asm volatile(
-        "{\n\t.reg .pred p;\n"
-        "WAIT_%=:\n\t"
-        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n\t"
-        "@!p bra WAIT_%=;\n}" ::"r"(smem_addr(bar)),
-        "r"(parity), "r"(0x989680)
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n}"
+        : "=r"(ok)
+        : "r"(smem_addr(bar)), "r"(parity)
         : "memory");
+    return ok != 0;
+}
+
+// the same for a warp that has nothing else to do meanwhile (a producer waiting for a free
+// stage): back off with nanosleep between polls instead of spinning on issue slots the
+// consumer warps of its SM sub-partition need (a try_wait suspend-time hint still returned
+// ~30 times per sub-tile: ncu)
+__device__ __forceinline__ void mbar_wait_parity_sleep(uint64_t* bar, uint32_t parity) {
+    uint32_t ns = 32;
+    while (!mbar_test_parity(bar, parity)) {
+        __nanosleep(ns);
+        ns = ns < 256 ? 2 * ns : 256;
+    }
 }
 
 __device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
