@@ -36,7 +36,7 @@ for it in range(4):
 f(dev._ctx, None)
 assert torch.equal(d_o, d_v)
 t = trace.cpu().numpy().reshape(tiles, 8).astype(np.int64)
-t0 = t[:, 0].min()
+t0 = t[:, 0][t[:, 0] > 0].min()
 print(f"tiles={tiles} span={(t[:, 5].max() - t0) / 1e3:.1f} us")
 for name, a, b in [("issue->landed", 0, 2), ("wait for data", 1, 2), ("sum+publish", 2, 3), ("publish->resolved*", 3, 4),
                    ("resolve->stored", 4, 5), ("prod: lookahead+window", 6, 7), ("prod: window->issued", 7, 0)]:
@@ -46,9 +46,13 @@ print("  (* resolved one round later, so this includes a whole round of work)")
 G = int(np.sum(t[:, 0] - t0 < 2000))  # rough
 print("  stored times (us) at 10/50/90%:", np.percentile((t[:, 5] - t0) / 1e3, [10, 50, 90]).round(2))
 
-# fused producer: time between its iterations (tile t -> t + G of the same CTA)
-starts = t[:, 6]
-if starts.max() > 0:
-    G = int(np.argmax(np.diff(starts[: 2048]) < 0)) if False else None
-    order = np.argsort(starts)
-    print("  producer iteration start spread (us):", np.percentile((starts - t0) / 1e3, [10, 50, 90]).round(2))
+# fused decode: phase 1 (control scan) and the grid barrier, per CTA (slots 6 / 7 of tile b,
+# slot 7 of tile b + 4096)
+nb = int(np.sum(t[:4096, 6] > 0))
+if nb:
+    p0, p1, p2 = t[:nb, 6], t[:nb, 7], t[4096:4096 + nb, 7]
+    print(f"  fused: {nb} CTAs; phase-1 start {(p0.min() - t0) / 1e3:.2f}..{(p0.max() - t0) / 1e3:.2f} us, "
+          f"phase-1 end p50 {(np.median(p1) - t0) / 1e3:.2f} max {(p1.max() - t0) / 1e3:.2f}, "
+          f"barrier release {(p2.min() - t0) / 1e3:.2f}..{(p2.max() - t0) / 1e3:.2f} us (t0 = first data copy)")
+    print(f"  phase 1 per CTA p50 {np.median(p1 - p0) / 1e3:.2f} us; first copy after release "
+          f"{(t[:, 0].min() - p2.min()) / 1e3:.2f} us")
