@@ -11,19 +11,23 @@ namespace bcgpu {
 
 __device__ __forceinline__ uint32_t sh_addr(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
 
+// Shared loads by address are volatile asm: the compiler must not move them above the
+// mbarrier waits (or the volatile shared stores) they follow -- as plain asm with no memory
+// operand they count as pure functions of the address and may be hoisted (it happened, in
+// an unrolled loop over TMA-staged chunks).  ptxas still schedules the SASS freely.
 __device__ __forceinline__ uint32_t lds8(uint32_t a) {
     uint32_t v;
-    asm("ld.shared.u8 %0, [%1];" : "=r"(v) : "r"(a));
+    asm volatile("ld.shared.u8 %0, [%1];" : "=r"(v) : "r"(a));
     return v;
 }
 __device__ __forceinline__ uint32_t lds32(uint32_t a) {
     uint32_t v;
-    asm("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(a));
+    asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(a));
     return v;
 }
 __device__ __forceinline__ uint4 lds128(uint32_t a) {
     uint4 v;
-    asm("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(a));
+    asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(a));
     return v;
 }
 // ordered against the surrounding shared stores (in-place passes)
@@ -94,7 +98,7 @@ __device__ __forceinline__ uint4 zero_group_s(uint32_t a) {
 
 __device__ __forceinline__ uint2 lds64(uint32_t a) {
     uint2 v;
-    asm("ld.shared.v2.u32 {%0,%1}, [%2];" : "=r"(v.x), "=r"(v.y) : "r"(a));
+    asm volatile("ld.shared.v2.u32 {%0,%1}, [%2];" : "=r"(v.x), "=r"(v.y) : "r"(a));
     return v;
 }
 
