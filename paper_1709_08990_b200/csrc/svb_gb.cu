@@ -238,6 +238,10 @@ __device__ __forceinline__ uint32_t gb_chase(const GbRing& R, const GbRingSum* S
 __global__ void __launch_bounds__(32 * kGbWarps)
     gb_table_kernel(const uint8_t* __restrict__ in, uint64_t len, uint64_t nchunks, uint32_t* __restrict__ tcnt,
                     uint32_t* __restrict__ texit, uint16_t* __restrict__ segtab) {
+    // programmatic dependent launch: the next kernel of the chain may be scheduled now; this
+    // one reads its predecessor's output only after the wait
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    asm volatile("griddepcontrol.wait;" ::: "memory");
     __shared__ __align__(16) uint8_t sbuf[kGbWarps][kGbStage];
     __shared__ GbRing ring[kGbWarps];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -292,6 +296,10 @@ __global__ void __launch_bounds__(32 * kGbTreeWarps)
     gb_compose_kernel(const uint32_t* __restrict__ ccnt, const uint32_t* __restrict__ cexit,
                       const uint32_t* __restrict__ csum, uint64_t nchild, uint32_t* __restrict__ pcnt,
                       uint32_t* __restrict__ pexit, uint32_t* __restrict__ psum, uint64_t nparent) {
+    // programmatic dependent launch: the next kernel of the chain may be scheduled now; this
+    // one reads its predecessor's output only after the wait
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    asm volatile("griddepcontrol.wait;" ::: "memory");
     __shared__ GbTreeSmem sm[kGbTreeWarps];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint64_t p = (uint64_t)blockIdx.x * kGbTreeWarps + warp;
@@ -319,6 +327,10 @@ __global__ void __launch_bounds__(32 * kGbTreeWarps)
                      const uint32_t* __restrict__ pcntpre, const uint32_t* __restrict__ psumpre, uint64_t nparent,
                      uint32_t* __restrict__ centry, uint32_t* __restrict__ ccntpre, uint32_t* __restrict__ csumpre,
                      int root, uint32_t base, uint64_t ngroups, unsigned long long* status, uint32_t epoch) {
+    // programmatic dependent launch: the next kernel of the chain may be scheduled now; this
+    // one reads its predecessor's output only after the wait
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    asm volatile("griddepcontrol.wait;" ::: "memory");
     __shared__ GbTreeSmem sm[kGbTreeWarps];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint64_t p = (uint64_t)blockIdx.x * kGbTreeWarps + warp;
@@ -350,6 +362,10 @@ __global__ void __launch_bounds__(32 * kGbWarps)
                      const uint16_t* __restrict__ segtab, uint32_t base, uint64_t* __restrict__ lstatus,
                      uint32_t* __restrict__ out, uint32_t* __restrict__ d_last, unsigned long long* status,
                      uint32_t epoch) {
+    // programmatic dependent launch: the next kernel of the chain may be scheduled now; this
+    // one reads its predecessor's output only after the wait
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    asm volatile("griddepcontrol.wait;" ::: "memory");
     __shared__ __align__(16) uint8_t sbuf[kGbWarps][kGbStage];
     __shared__ __align__(16) uint16_t stab[kGbWarps][kGbE * 32];
     __shared__ uint16_t spos[kGbWarps][kGbMaxGroups];
@@ -456,6 +472,22 @@ __global__ void __launch_bounds__(32 * kGbWarps)
 // ---------------------------------------------------------------------------
 // launchers
 // ---------------------------------------------------------------------------
+// The decode is a chain of small kernels (table, 2 per tree level, decode): each is launched
+// as a programmatic dependent of the one before, so its launch and ramp-up overlap the
+// predecessor's tail (every kernel of the chain waits before reading its inputs).
+template <typename... KArgs, typename... Args>
+static cudaError_t gb_launch(void (*k)(KArgs...), unsigned grid, unsigned block, cudaStream_t stream, Args... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(block);
+    cfg.stream = stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, k, static_cast<KArgs>(args)...);
+}
 // device workspace of a decode of len compressed bytes: per tree level, 3 tables of 17
 // words per node and 3 resolved words per node
 static uint64_t gb_levels(uint64_t len, uint64_t* nodes) {
@@ -501,28 +533,39 @@ cudaError_t launch_gb_decode(const uint8_t* in, uint64_t len, uint64_t n, int de
     const uint64_t nchunks = nodes[0];
     uint16_t* segtab = reinterpret_cast<uint16_t*>((reinterpret_cast<uintptr_t>(w) + 15) & ~(uintptr_t)15);
     const unsigned tgrid = (unsigned)((nchunks + kGbWarps - 1) / kGbWarps);
-    gb_table_kernel<<<tgrid, 32 * kGbWarps, 0, stream>>>(in, len, nchunks, tc[0], tx[0], segtab);
+    cudaError_t e = gb_launch(gb_table_kernel, tgrid, 32 * kGbWarps, stream, in, len, nchunks, tc[0], tx[0], segtab);
+    if (e != cudaSuccess) return e;
     int nl = 1;
-    for (uint64_t l = 0; l + 1 < L; ++l, ++nl)
-        gb_compose_kernel<<<(unsigned)((nodes[l + 1] + kGbTreeWarps - 1) / kGbTreeWarps), 32 * kGbTreeWarps, 0,
-                            stream>>>(tc[l], tx[l], nullptr, nodes[l], tc[l + 1], tx[l + 1], nullptr, nodes[l + 1]);
+    const uint32_t* nul = nullptr;
+    for (uint64_t l = 0; l + 1 < L; ++l, ++nl) {
+        e = gb_launch(gb_compose_kernel, (unsigned)((nodes[l + 1] + kGbTreeWarps - 1) / kGbTreeWarps),
+                      32 * kGbTreeWarps, stream, (const uint32_t*)tc[l], (const uint32_t*)tx[l], nul, nodes[l],
+                      tc[l + 1], tx[l + 1], (uint32_t*)nullptr, nodes[l + 1]);
+        if (e != cudaSuccess) return e;
+    }
     const uint64_t ngroups = (n + 3) >> 2;
     // root: the top level's single node, entered at 0
-    gb_expand_kernel<<<1, 32 * kGbTreeWarps, 0, stream>>>(tc[L - 1], tx[L - 1], nullptr, 1,
-                                                          nullptr, nullptr, nullptr, 1, re[L - 1], rc[L - 1],
-                                                          rs[L - 1], 1, base, ngroups, status, epoch);
+    e = gb_launch(gb_expand_kernel, 1u, 32 * kGbTreeWarps, stream, (const uint32_t*)tc[L - 1],
+                  (const uint32_t*)tx[L - 1], nul, (uint64_t)1, nul, nul, nul, (uint64_t)1, re[L - 1], rc[L - 1],
+                  rs[L - 1], 1, base, ngroups, status, epoch);
+    if (e != cudaSuccess) return e;
     ++nl;
-    for (uint64_t l = L - 1; l > 0; --l, ++nl)
-        gb_expand_kernel<<<(unsigned)((nodes[l] + kGbTreeWarps - 1) / kGbTreeWarps), 32 * kGbTreeWarps, 0,
-                           stream>>>(tc[l - 1], tx[l - 1], nullptr, nodes[l - 1], re[l], rc[l],
-                                     rs[l], nodes[l], re[l - 1], rc[l - 1], rs[l - 1], 0, base, ngroups, status,
-                                     epoch);
+    for (uint64_t l = L - 1; l > 0; --l, ++nl) {
+        e = gb_launch(gb_expand_kernel, (unsigned)((nodes[l] + kGbTreeWarps - 1) / kGbTreeWarps), 32 * kGbTreeWarps,
+                      stream, (const uint32_t*)tc[l - 1], (const uint32_t*)tx[l - 1], nul, nodes[l - 1],
+                      (const uint32_t*)re[l], (const uint32_t*)rc[l], (const uint32_t*)rs[l], nodes[l], re[l - 1],
+                      rc[l - 1], rs[l - 1], 0, base, ngroups, status, epoch);
+        if (e != cudaSuccess) return e;
+    }
     if (delta)
-        gb_decode_kernel<true><<<tgrid, 32 * kGbWarps, 0, stream>>>(in, len, n, nchunks, re[0], rc[0], segtab, base, lstatus,
-                                                                    out, d_last, status, epoch);
+        e = gb_launch(gb_decode_kernel<true>, tgrid, 32 * kGbWarps, stream, in, len, n, nchunks,
+                      (const uint32_t*)re[0], (const uint32_t*)rc[0], (const uint16_t*)segtab, base, lstatus, out,
+                      d_last, status, epoch);
     else
-        gb_decode_kernel<false><<<tgrid, 32 * kGbWarps, 0, stream>>>(in, len, n, nchunks, re[0], rc[0], segtab, base,
-                                                                     nullptr, out, d_last, status, epoch);
+        e = gb_launch(gb_decode_kernel<false>, tgrid, 32 * kGbWarps, stream, in, len, n, nchunks,
+                      (const uint32_t*)re[0], (const uint32_t*)rc[0], (const uint16_t*)segtab, base,
+                      (uint64_t*)nullptr, out, d_last, status, epoch);
+    if (e != cudaSuccess) return e;
     *launches = nl + 1;
     return cudaGetLastError();
 }
