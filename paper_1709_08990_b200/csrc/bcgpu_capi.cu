@@ -376,7 +376,7 @@ int bcgpu_svb_encode_device(bcgpu_ctx* c, const uint32_t* d_in, size_t n, int de
 
 int bcgpu_svb_decode_device(bcgpu_ctx* c, const uint8_t* d_in, size_t in_len, size_t n, int delta, uint32_t base,
                             uint32_t* d_out, uint32_t* d_last, void* stream) {
-    if (!c || (n && (!d_in || !d_out))) return BCGPU_ERR_INVALID_ARGUMENT;
+    if (!c || ((n && !d_out) || (in_len && !d_in))) return BCGPU_ERR_INVALID_ARGUMENT;
     const size_t nctrl = (n + 3) / 4;
     if (in_len < nctrl) return BCGPU_ERR_TRUNCATED;
     DeviceGuard g(c->device);
@@ -402,7 +402,7 @@ int bcgpu_svb_decode_device(bcgpu_ctx* c, const uint8_t* d_in, size_t in_len, si
 
 int bcgpu_svb_block_offsets_device(bcgpu_ctx* c, const uint8_t* d_in, size_t in_len, size_t n, uint64_t* d_offsets,
                                    void* stream) {
-    if (!c || (n && (!d_in || !d_offsets))) return BCGPU_ERR_INVALID_ARGUMENT;
+    if (!c || ((n && !d_offsets) || (in_len && !d_in))) return BCGPU_ERR_INVALID_ARGUMENT;
     const size_t nctrl = (n + 3) / 4;
     if (in_len < nctrl) return BCGPU_ERR_TRUNCATED;
     DeviceGuard g(c->device);
@@ -724,7 +724,7 @@ static int decode_host_pipelined(bcgpu_ctx* c, const uint8_t* bytes, size_t len,
 
 int bcgpu_svb_decode_host(bcgpu_ctx* c, const uint8_t* bytes, size_t len, size_t n, int delta, uint32_t base,
                           uint32_t* out, uint32_t* last) {
-    if (!c || (n && (!bytes || !out))) return BCGPU_ERR_INVALID_ARGUMENT;
+    if (!c || ((n && !out) || (len && !bytes))) return BCGPU_ERR_INVALID_ARGUMENT;
     const size_t nctrl = (n + 3) / 4;
     if (len < nctrl) return BCGPU_ERR_TRUNCATED;
     if (n == 0) {
@@ -780,7 +780,7 @@ int bcgpu_svb_decode_blocks_host(bcgpu_ctx* c, const uint8_t* bytes, size_t len,
 }
 
 int bcgpu_svb_block_offsets_host(bcgpu_ctx* c, const uint8_t* bytes, size_t len, size_t n, uint64_t* offsets) {
-    if (!c || (n && (!bytes || !offsets))) return BCGPU_ERR_INVALID_ARGUMENT;
+    if (!c || ((n && !offsets) || (len && !bytes))) return BCGPU_ERR_INVALID_ARGUMENT;
     const size_t nctrl = (n + 3) / 4;
     if (len < nctrl) return BCGPU_ERR_TRUNCATED;
     if (n == 0) return BCGPU_OK;
@@ -894,7 +894,7 @@ int bcgpu_gb_encode_device(bcgpu_ctx* c, const uint32_t* d_in, size_t n, int del
 
 int bcgpu_gb_decode_device(bcgpu_ctx* c, const uint8_t* d_in, size_t in_len, size_t n, int delta, uint32_t base,
                            uint32_t* d_out, uint32_t* d_last, void* stream) {
-    if (!c || (n && (!d_in || !d_out))) return BCGPU_ERR_INVALID_ARGUMENT;
+    if (!c || ((n && !d_out) || (in_len && !d_in))) return BCGPU_ERR_INVALID_ARGUMENT;
     DeviceGuard g(c->device);
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     if (n == 0) {
@@ -947,7 +947,7 @@ int bcgpu_gb_encode_host(bcgpu_ctx* c, const uint32_t* values, size_t n, int del
 
 int bcgpu_gb_decode_host(bcgpu_ctx* c, const uint8_t* bytes, size_t len, size_t n, int delta, uint32_t base,
                          uint32_t* out, uint32_t* last) {
-    if (!c || (n && (!bytes || !out))) return BCGPU_ERR_INVALID_ARGUMENT;
+    if (!c || ((n && !out) || (len && !bytes))) return BCGPU_ERR_INVALID_ARGUMENT;
     if (n == 0) {
         if (last) *last = base;
         return len ? BCGPU_ERR_TRAILING_BYTES : BCGPU_OK;

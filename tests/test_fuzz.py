@@ -76,3 +76,79 @@ def test_fuzz_roundtrip(env, n, kind, delta, prev, seed, in_off, out_off, enc, d
             assert (int(last.item()) & 0xFFFFFFFF) == (int(v[-1]) if n else prev)
     finally:
         lib.bcgpu_debug_set_flags(dev._ctx, 0)
+
+
+def _status(P, fn):
+    """0 when fn() succeeds, else the bcgpu status of the CodecError (errc + 1)."""
+    try:
+        fn()
+        return 0
+    except P.CodecError as e:
+        return int(e.code) + 1
+
+
+@settings(max_examples=int(os.environ.get("FUZZ_EXAMPLES", "200")), deadline=None, suppress_health_check=list(HealthCheck))
+@given(n=st.one_of(st.integers(0, 3000), st.integers(3000, 300_000)),
+       kind=st.sampled_from(["classes", "sorted_small", "sorted_wide", "constant", "bytes"]),
+       delta=st.booleans(), seed=st.integers(0, 2**31), in_off=st.sampled_from([0, 1, 3]),
+       out_off=st.integers(0, 17))
+def test_fuzz_varint_gb(env, n, kind, delta, seed, in_off, out_off):
+    """varint-GB (svb_gb.cu) through the device API at any buffer offsets, against the oracle."""
+    torch, lib, dev = env
+    v = _values(kind, n, seed)
+    payload = oracle.delta_encode(v, 0) if delta else v
+    want = oracle.gb_encode(payload)
+    src = torch.zeros(n + 8, dtype=torch.int32, device="cuda")
+    if n:
+        src[in_off:in_off + n] = torch.from_numpy(v.view(np.int32)).cuda()
+    cap = (n + 3) // 4 + 4 * n
+    outb = torch.zeros(cap + 32, dtype=torch.uint8, device="cuda")
+    olen = torch.zeros(1, dtype=torch.int64, device="cuda")
+    dev.gb_encode(src[in_off:in_off + n], outb[out_off:out_off + cap], olen, delta=delta)
+    dev.check()
+    m = int(olen.item())
+    assert m == len(want) and outb[out_off:out_off + m].cpu().numpy().tobytes() == want
+    dst = torch.zeros(n + 8, dtype=torch.int32, device="cuda")
+    dev.gb_decode(outb[out_off:out_off + m], n, dst[in_off:in_off + n], delta=delta)
+    dev.check()
+    assert np.array_equal(dst[in_off:in_off + n].cpu().numpy().view(np.uint32), v)
+
+
+@settings(max_examples=int(os.environ.get("FUZZ_EXAMPLES", "200")), deadline=None, suppress_health_check=list(HealthCheck))
+@given(n=st.integers(1, 60_000), kind=st.sampled_from(["classes", "sorted_small", "bytes"]),
+       codec=st.sampled_from(["svb", "gb"]), delta=st.booleans(), seed=st.integers(0, 2**31),
+       edit=st.sampled_from(["flip", "cut", "extend", "count_up", "count_down"]), where=st.floats(0, 1))
+def test_fuzz_malformed(env, n, kind, codec, delta, seed, edit, where):
+    """Corrupted streams: the GPU's status equals the oracle's (ok / truncated / trailing_bytes),
+    and when both accept the stream they decode the same integers -- no read past the buffer
+    changes either (the buffer is copied to an exact-size host array first)."""
+    import paper_1709_08990_b200 as P
+    v = _values(kind, n, seed)
+    rng = np.random.default_rng(seed ^ 0x5A5A)
+    enc = oracle.encode(v) if codec == "svb" else oracle.gb_encode(v)
+    b = bytearray(enc)
+    n2 = n
+    if edit == "flip":
+        i = min(int(where * len(b)), len(b) - 1)
+        b[i] ^= 1 << int(rng.integers(0, 8))
+    elif edit == "cut":
+        b = b[: int(where * len(b))]
+    elif edit == "extend":
+        b += bytes(rng.integers(0, 256, 1 + int(where * 20)).astype(np.uint8))
+    elif edit == "count_up":
+        n2 = n + 1 + int(where * 7)
+    else:
+        n2 = max(0, n - 1 - int(where * 7))
+    data = bytes(b)
+    if codec == "svb":
+        ost, ovals, _ = oracle.decode(data, n2, delta=delta)
+    else:
+        ost, ovals, _ = oracle.gb_decode(data, n2, delta=delta)
+    out = np.zeros(max(n2, 1), np.uint32)
+    if codec == "svb":
+        gst = _status(P, (lambda: P.svb_decode_delta(data, n2, 0, out)) if delta else (lambda: P.svb_decode(data, n2, out)))
+    else:
+        gst = _status(P, (lambda: P.gb_decode_delta(data, n2, 0, out)) if delta else (lambda: P.gb_decode(data, n2, out)))
+    assert gst == ost, (codec, edit, gst, ost)
+    if ost == oracle.OK:
+        assert np.array_equal(out[:n2], ovals[:n2])
