@@ -115,7 +115,8 @@ def test_fuzz_varint_gb(env, n, kind, delta, seed, in_off, out_off):
 
 
 @settings(max_examples=int(os.environ.get("FUZZ_EXAMPLES", "200")), deadline=None, suppress_health_check=list(HealthCheck))
-@given(n=st.integers(1, 60_000), kind=st.sampled_from(["classes", "sorted_small", "bytes"]),
+@given(n=st.one_of(st.integers(1, 60_000), st.integers(60_000, 300_000)),
+       kind=st.sampled_from(["classes", "sorted_small", "bytes"]),
        codec=st.sampled_from(["svb", "gb"]), delta=st.booleans(), seed=st.integers(0, 2**31),
        edit=st.sampled_from(["flip", "cut", "extend", "count_up", "count_down"]), where=st.floats(0, 1))
 def test_fuzz_malformed(env, n, kind, codec, delta, seed, edit, where):
