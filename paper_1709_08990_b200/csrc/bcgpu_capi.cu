@@ -369,7 +369,7 @@ int bcgpu_svb_encode_device(bcgpu_ctx* c, const uint32_t* d_in, size_t n, int de
     c->agg_n = n;
     int launches = 0;
     BC_CUDA(launch_encode3(d_in, n, delta, prev, d_out, d_out_len, c->offs, status_ptr(c), c->epoch, s, &launches,
-                           slots, hints));
+                           slots, hints, c->trace));
     g_launches.fetch_add((uint64_t)launches);
     return BCGPU_OK;
 }

@@ -576,7 +576,7 @@ struct __align__(16) E1Shared {
     unsigned long long carry, incl;
 };
 
-template <bool kDelta>
+template <bool kDelta, bool kTrace>
 __global__ void __launch_bounds__(kCTThreads + 32, 2)
     svb_encode1_kernel(const uint32_t* __restrict__ in, uint64_t n, uint32_t prev, uint8_t* __restrict__ out,
                        DecodeMeta meta, uint64_t* __restrict__ d_out_len, unsigned long long* status, uint32_t epoch) {
@@ -615,6 +615,7 @@ __global__ void __launch_bounds__(kCTThreads + 32, 2)
                 if (lane == 0) {
                     fence_async_smem();
                     mbar_expect(&sh.full[st], tx);
+                    if (kTrace) meta.trace[8ull * t + 0] = gtimer();
                     tma_load_hint(dst, reinterpret_cast<const void*>(beg), tx, &sh.full[st], l2_policy_drop());
                 }
             } else {
@@ -679,12 +680,14 @@ __global__ void __launch_bounds__(kCTThreads + 32, 2)
             }
         }
         consumers_sync();
+        if (kTrace && ct == 0) meta.trace[8ull * tp + 4] = gtimer();
         const uint64_t s = (uint64_t)tp * kCTWarps + warp;
         if (s < nsub) {
             const uint32_t src = sh_addr(dsm) + (uint32_t)st * kE1Stride + 16 + (uint32_t)warp * (kWTInts * 4);
             store_realigned(src, sh.wsum[q][warp], out + ngroups + sh.carry + sh.wpre[warp]);
         }
         __syncwarp();
+        if (kTrace && ct == 0) meta.trace[8ull * tp + 5] = gtimer();
         if (lane == 0) mbar_arrive(&sh.empty[st]);
     };
 
@@ -693,7 +696,9 @@ __global__ void __launch_bounds__(kCTThreads + 32, 2)
     for (uint32_t t = blockIdx.x; t < ntiles;
          t += G, ++k, stp = st, qp = q, st = st + 1 == kE1Stages ? 0 : st + 1, q = q == 2 ? 0 : q + 1, ph ^= st == 0) {
         if (k) prefetch(tprev);
+        if (kTrace && ct == 0) meta.trace[8ull * t + 1] = gtimer();
         mbar_wait_parity(&sh.full[st], ph);
+        if (kTrace && ct == 0) meta.trace[8ull * t + 2] = gtimer();
         uint8_t* stage = dsm + (uint32_t)st * kE1Stride;
         const uint64_t s = (uint64_t)t * kCTWarps + warp;
         const uint64_t g0 = s * kWTGroups;
@@ -761,6 +766,7 @@ __global__ void __launch_bounds__(kCTThreads + 32, 2)
 #pragma unroll
             for (int w = 0; w < kCTWarps; ++w) a += sh.wsum[q][w];
             st_relaxed_u64(meta.agg + t, ((unsigned long long)epoch << 32) | a);
+            if (kTrace) meta.trace[8ull * t + 3] = gtimer();
         }
         if (k) resolve(tprev, stp, qp);
         tprev = t;
@@ -785,11 +791,12 @@ static cudaError_t launch_encode1(const uint32_t* in, uint64_t n, int delta, uin
     if (dev != dev_cached) {
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
         cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, dev);
-        cudaFuncSetAttribute(svb_encode1_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        cudaFuncSetAttribute(svb_encode1_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        const void* fns[4] = {(const void*)svb_encode1_kernel<true, false>, (const void*)svb_encode1_kernel<false, false>,
+                              (const void*)svb_encode1_kernel<true, true>, (const void*)svb_encode1_kernel<false, true>};
+        for (const void* f : fns) cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         int o1 = 0, o2 = 0;
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o1, svb_encode1_kernel<true>, kCTThreads + 32, smem);
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o2, svb_encode1_kernel<false>, kCTThreads + 32, smem);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o1, svb_encode1_kernel<true, false>, kCTThreads + 32, smem);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o2, svb_encode1_kernel<false, false>, kCTThreads + 32, smem);
         occ = o1 < o2 ? o1 : o2;
         dev_cached = dev;
     }
@@ -802,7 +809,8 @@ static cudaError_t launch_encode1(const uint32_t* in, uint64_t n, int delta, uin
     DecodeMeta mm = m;
     void* args[] = {(void*)&in, (void*)&n, (void*)&prev, (void*)&out, (void*)&mm, (void*)&d_out_len, (void*)&status,
                     (void*)&epoch};
-    const void* fn = delta ? (const void*)svb_encode1_kernel<true> : (const void*)svb_encode1_kernel<false>;
+    const void* fn = m.trace ? (delta ? (const void*)svb_encode1_kernel<true, true> : (const void*)svb_encode1_kernel<false, true>)
+                             : (delta ? (const void*)svb_encode1_kernel<true, false> : (const void*)svb_encode1_kernel<false, false>);
     const cudaError_t e = cudaLaunchCooperativeKernel(fn, dim3((unsigned)grid), dim3(kCTThreads + 32), args, smem, stream);
     if (e == cudaSuccess) *used = true;
     return e;
@@ -819,8 +827,10 @@ uint64_t encode_slot_bytes(uint64_t n) {
 
 cudaError_t launch_encode3(const uint32_t* in, uint64_t n, int delta, uint32_t prev, uint8_t* out,
                            uint64_t* d_out_len, void* meta_ws, unsigned long long* status, uint32_t epoch,
-                           cudaStream_t stream, int* launches, uint8_t* slots, uint32_t hints) {
-    const DecodeMeta m = carve_decode_meta(meta_ws, n);
+                           cudaStream_t stream, int* launches, uint8_t* slots, uint32_t hints,
+                           unsigned long long* trace) {
+    DecodeMeta m = carve_decode_meta(meta_ws, n);
+    m.trace = trace;
     const uint64_t ngroups = (n + 3) >> 2;
     const uint64_t nsub = (ngroups + kWTGroups - 1) / kWTGroups;
     const uint32_t nchunks = (uint32_t)((nsub + kChunkSubs - 1) / kChunkSubs);

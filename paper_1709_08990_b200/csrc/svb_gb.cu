@@ -18,19 +18,20 @@
 // it.  The chain is resolved with transfer functions:
 //   1. gb_table_kernel: the stream is cut into 4 KiB chunks; a group starting in one
 //      chunk ends at most 16 bytes into the next, so a chunk is entered at one of 17
-//      offsets.  Per chunk, lanes 0..16 of a warp walk the chunk from each entry offset
-//      and record (exit offset into the next chunk, groups started, sum of their
-//      values for delta).
+//      offsets.  Per chunk it records, for each entry offset, the exit offset into the
+//      next chunk and the groups started (lane-parallel segment tables, below).
 //   2. gb_compose_kernel / gb_expand_kernel: the tables compose associatively (follow
-//      the exit of one into the next, add counts and sums).  A 32-ary tree of
-//      compositions is built bottom-up, then walked top-down from entry 0 at the
-//      stream's start, which resolves every chunk's true entry offset, index of its
-//      first group, and value carry.  The root's count also settles truncation.
-//   3. gb_decode_kernel: per chunk, lane 0 lists the group starts from the true entry,
-//      then the warp decodes 32 groups per round (all-small fast path for control 0,
-//      field by field otherwise), fuses the delta prefix sum (warp scan + carry), and
-//      stores 128-bit rows.  The warp holding group ceil(n/4)-1 checks the stream end
-//      (truncated / trailing bytes).
+//      the exit of one into the next, add the counts).  A 32-ary tree of compositions
+//      is built bottom-up, then walked top-down from entry 0 at the stream's start,
+//      which resolves every chunk's true entry offset and the index of its first group.
+//      The root's count also settles truncation.
+//   3. gb_decode_kernel: per chunk, every lane lists the group starts in its segment
+//      from the true entry, then the warp decodes 32 groups per round (all-small fast
+//      path for control 0, field by field otherwise) and stores 128-bit rows.  Delta:
+//      the chunk's value carry comes from a decoupled look-back over chunk sums, and the
+//      prefix sum is fused (warp scan + carry).  The warp holding group ceil(n/4)-1
+//      checks the stream end (truncated / trailing bytes).
+// All decode kernels form one chain under programmatic dependent launch.
 #include <cstdint>
 
 #include "svb_device.cuh"
@@ -275,27 +276,25 @@ __global__ void __launch_bounds__(32 * kGbWarps)
 // decode 2: compose 32 child tables per node (bottom-up), resolve entries (top-down)
 // ---------------------------------------------------------------------------
 struct GbTreeSmem {
-    uint32_t cnt[kGbFan * kGbE], exit[kGbFan * kGbE], sum[kGbFan * kGbE];
+    uint32_t cnt[kGbFan * kGbE], exit[kGbFan * kGbE];
 };
 
 __device__ __forceinline__ uint32_t gb_load_children(GbTreeSmem& sm, const uint32_t* ccnt, const uint32_t* cexit,
-                                                     const uint32_t* csum, uint64_t nchild, uint64_t parent) {
+                                                     uint64_t nchild, uint64_t parent) {
     const int lane = threadIdx.x & 31;
     const uint64_t k0 = parent * kGbFan;
     const uint32_t nk = (uint32_t)(nchild - k0 < kGbFan ? nchild - k0 : kGbFan);
     for (uint32_t i = lane; i < nk * kGbE; i += 32) {
         sm.cnt[i] = ccnt[k0 * kGbE + i];
         sm.exit[i] = cexit[k0 * kGbE + i];
-        sm.sum[i] = csum ? csum[k0 * kGbE + i] : 0u;
     }
     __syncwarp();
     return nk;
 }
 
 __global__ void __launch_bounds__(32 * kGbTreeWarps)
-    gb_compose_kernel(const uint32_t* __restrict__ ccnt, const uint32_t* __restrict__ cexit,
-                      const uint32_t* __restrict__ csum, uint64_t nchild, uint32_t* __restrict__ pcnt,
-                      uint32_t* __restrict__ pexit, uint32_t* __restrict__ psum, uint64_t nparent) {
+    gb_compose_kernel(const uint32_t* __restrict__ ccnt, const uint32_t* __restrict__ cexit, uint64_t nchild,
+                      uint32_t* __restrict__ pcnt, uint32_t* __restrict__ pexit, uint64_t nparent) {
     // programmatic dependent launch: the next kernel of the chain may be scheduled now; this
     // one reads its predecessor's output only after the wait
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
@@ -304,29 +303,26 @@ __global__ void __launch_bounds__(32 * kGbTreeWarps)
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint64_t p = (uint64_t)blockIdx.x * kGbTreeWarps + warp;
     if (p >= nparent) return;
-    const uint32_t nk = gb_load_children(sm[warp], ccnt, cexit, csum, nchild, p);
+    const uint32_t nk = gb_load_children(sm[warp], ccnt, cexit, nchild, p);
     if (lane < kGbE) {
-        uint32_t x = (uint32_t)lane, cnt = 0, sum = 0;
+        uint32_t x = (uint32_t)lane, cnt = 0;
         for (uint32_t k = 0; k < nk; ++k) {
             const uint32_t i = k * kGbE + x;
             cnt += sm[warp].cnt[i];
-            sum += sm[warp].sum[i];
             x = sm[warp].exit[i];
         }
         pcnt[p * kGbE + lane] = cnt;
         pexit[p * kGbE + lane] = x;
-        if (psum) psum[p * kGbE + lane] = sum;
     }
 }
 
-// root != 0: the single top node, entered at offset 0 with carry base; its group count
-// (groups chained from the stream's start) below ceil(n/4) means the stream is truncated
+// root != 0: the single top node, entered at offset 0; its group count (groups chained
+// from the stream's start) below ceil(n/4) means the stream is truncated
 __global__ void __launch_bounds__(32 * kGbTreeWarps)
-    gb_expand_kernel(const uint32_t* __restrict__ ccnt, const uint32_t* __restrict__ cexit,
-                     const uint32_t* __restrict__ csum, uint64_t nchild, const uint32_t* __restrict__ pentry,
-                     const uint32_t* __restrict__ pcntpre, const uint32_t* __restrict__ psumpre, uint64_t nparent,
-                     uint32_t* __restrict__ centry, uint32_t* __restrict__ ccntpre, uint32_t* __restrict__ csumpre,
-                     int root, uint32_t base, uint64_t ngroups, unsigned long long* status, uint32_t epoch) {
+    gb_expand_kernel(const uint32_t* __restrict__ ccnt, const uint32_t* __restrict__ cexit, uint64_t nchild,
+                     const uint32_t* __restrict__ pentry, const uint32_t* __restrict__ pcntpre, uint64_t nparent,
+                     uint32_t* __restrict__ centry, uint32_t* __restrict__ ccntpre, int root, uint64_t ngroups,
+                     unsigned long long* status, uint32_t epoch) {
     // programmatic dependent launch: the next kernel of the chain may be scheduled now; this
     // one reads its predecessor's output only after the wait
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
@@ -335,17 +331,15 @@ __global__ void __launch_bounds__(32 * kGbTreeWarps)
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint64_t p = (uint64_t)blockIdx.x * kGbTreeWarps + warp;
     if (p >= nparent) return;
-    const uint32_t nk = gb_load_children(sm[warp], ccnt, cexit, csum, nchild, p);
+    const uint32_t nk = gb_load_children(sm[warp], ccnt, cexit, nchild, p);
     if (lane == 0) {
-        uint32_t x = root ? 0u : pentry[p], cp = root ? 0u : pcntpre[p], sp = root ? base : psumpre[p];
+        uint32_t x = root ? 0u : pentry[p], cp = root ? 0u : pcntpre[p];
         for (uint32_t k = 0; k < nk; ++k) {
             const uint64_t c = p * kGbFan + k;
             centry[c] = x;
             ccntpre[c] = cp;
-            csumpre[c] = sp;
             const uint32_t i = k * kGbE + x;
             cp += sm[warp].cnt[i];
-            sp += sm[warp].sum[i];
             x = sm[warp].exit[i];
         }
         if (root && (uint64_t)cp < ngroups) gb_report(status, epoch, BCGPU_ERR_TRUNCATED);
@@ -505,7 +499,7 @@ uint64_t gb_decode_chunks(uint64_t len) { return len ? (len + kGbChunk - 1) / kG
 
 size_t gb_decode_ws_bytes(uint64_t len) {
     uint64_t nodes[16], L = gb_levels(len, nodes), words = 0;
-    for (uint64_t l = 0; l < L; ++l) words += nodes[l] * (3 * kGbE + 3) + 4;
+    for (uint64_t l = 0; l < L; ++l) words += nodes[l] * (2 * kGbE + 2) + 2;
     return (size_t)(4 * words + 256 + nodes[0] * (2 * kGbE * 32) + 16);
 }
 
@@ -514,21 +508,17 @@ cudaError_t launch_gb_decode(const uint8_t* in, uint64_t len, uint64_t n, int de
                              uint32_t epoch, cudaStream_t stream, int* launches) {
     uint64_t nodes[16];
     const uint64_t L = gb_levels(len, nodes);
-    uint32_t* tc[16];
-    uint32_t* tx[16];
-    uint32_t* ts[16];
-    uint32_t* re[16];
-    uint32_t* rc[16];
-    uint32_t* rs[16];
+    uint32_t* tc[16];  // per level: group counts of the 17 entries of every node
+    uint32_t* tx[16];  // exits
+    uint32_t* re[16];  // resolved entry offset of every node
+    uint32_t* rc[16];  // resolved index of its first group
     uint32_t* w = static_cast<uint32_t*>(ws);
     for (uint64_t l = 0; l < L; ++l) {
         const uint64_t m = nodes[l];
         tc[l] = w, w += m * kGbE;
         tx[l] = w, w += m * kGbE;
-        ts[l] = w, w += m * kGbE;
         re[l] = w, w += m + 1;
         rc[l] = w, w += m + 1;
-        rs[l] = w, w += m + 2;
     }
     const uint64_t nchunks = nodes[0];
     uint16_t* segtab = reinterpret_cast<uint16_t*>((reinterpret_cast<uintptr_t>(w) + 15) & ~(uintptr_t)15);
@@ -539,22 +529,22 @@ cudaError_t launch_gb_decode(const uint8_t* in, uint64_t len, uint64_t n, int de
     const uint32_t* nul = nullptr;
     for (uint64_t l = 0; l + 1 < L; ++l, ++nl) {
         e = gb_launch(gb_compose_kernel, (unsigned)((nodes[l + 1] + kGbTreeWarps - 1) / kGbTreeWarps),
-                      32 * kGbTreeWarps, stream, (const uint32_t*)tc[l], (const uint32_t*)tx[l], nul, nodes[l],
-                      tc[l + 1], tx[l + 1], (uint32_t*)nullptr, nodes[l + 1]);
+                      32 * kGbTreeWarps, stream, (const uint32_t*)tc[l], (const uint32_t*)tx[l], nodes[l], tc[l + 1],
+                      tx[l + 1], nodes[l + 1]);
         if (e != cudaSuccess) return e;
     }
     const uint64_t ngroups = (n + 3) >> 2;
     // root: the top level's single node, entered at 0
     e = gb_launch(gb_expand_kernel, 1u, 32 * kGbTreeWarps, stream, (const uint32_t*)tc[L - 1],
-                  (const uint32_t*)tx[L - 1], nul, (uint64_t)1, nul, nul, nul, (uint64_t)1, re[L - 1], rc[L - 1],
-                  rs[L - 1], 1, base, ngroups, status, epoch);
+                  (const uint32_t*)tx[L - 1], (uint64_t)1, nul, nul, (uint64_t)1, re[L - 1], rc[L - 1], 1, ngroups,
+                  status, epoch);
     if (e != cudaSuccess) return e;
     ++nl;
     for (uint64_t l = L - 1; l > 0; --l, ++nl) {
         e = gb_launch(gb_expand_kernel, (unsigned)((nodes[l] + kGbTreeWarps - 1) / kGbTreeWarps), 32 * kGbTreeWarps,
-                      stream, (const uint32_t*)tc[l - 1], (const uint32_t*)tx[l - 1], nul, nodes[l - 1],
-                      (const uint32_t*)re[l], (const uint32_t*)rc[l], (const uint32_t*)rs[l], nodes[l], re[l - 1],
-                      rc[l - 1], rs[l - 1], 0, base, ngroups, status, epoch);
+                      stream, (const uint32_t*)tc[l - 1], (const uint32_t*)tx[l - 1], nodes[l - 1],
+                      (const uint32_t*)re[l], (const uint32_t*)rc[l], nodes[l], re[l - 1], rc[l - 1], 0, ngroups,
+                      status, epoch);
         if (e != cudaSuccess) return e;
     }
     if (delta)

@@ -53,7 +53,8 @@ int occupancy_decode_pipe();
 // one read of the integers; without: size scan + tile encode (two reads).
 cudaError_t launch_encode3(const uint32_t* in, uint64_t n, int delta, uint32_t prev, uint8_t* out,
                            uint64_t* d_out_len, void* meta_ws, unsigned long long* status, uint32_t epoch,
-                           cudaStream_t stream, int* launches, uint8_t* slots = nullptr, uint32_t hints = 3);
+                           cudaStream_t stream, int* launches, uint8_t* slots = nullptr, uint32_t hints = 3,
+                           unsigned long long* trace = nullptr);
 // hints: bit 0/1 L2 policies of the slot encode; 0x100 try the one-pass encode first (needs the
 // workspace's tile aggregates free of this epoch's tag: see bcgpu_capi.cu)
 // Chunks [c0, c1) (64 Ki integers each) of the two-read encode, continuing from the
