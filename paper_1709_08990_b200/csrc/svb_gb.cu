@@ -363,27 +363,30 @@ __global__ void __launch_bounds__(32 * kGbWarps)
     __shared__ __align__(16) uint8_t sbuf[kGbWarps][kGbStage];
     __shared__ __align__(16) uint16_t stab[kGbWarps][kGbE * 32];
     __shared__ uint16_t spos[kGbWarps][kGbMaxGroups];
+    __shared__ uint32_t wtot[kGbWarps];  // delta: the warps' chunk sums
+    __shared__ uint32_t cta_ex;          // delta: carry before the CTA's first chunk
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint64_t chunk = (uint64_t)blockIdx.x * kGbWarps + warp;
-    if (chunk >= nchunks) return;
     const uint64_t ngroups = (n + 3) >> 2;
     const uint32_t tail_r = (uint32_t)(n & 3);
-    const uint64_t kb = rcnt[chunk];  // index of the chunk's first group
-    if (kb >= ngroups) return;
+    // warps without groups of this call stay for the CTA barriers of the delta carry
+    const uint64_t kb = chunk < nchunks ? rcnt[chunk] : ngroups;  // index of the chunk's first group
+    const bool active = kb < ngroups;
+    if (!kDelta && !active) return;
     const uint64_t cs = chunk * kGbChunk;
-    const uint32_t clen = (uint32_t)(len - cs < kGbChunk ? len - cs : kGbChunk);
-    const uint32_t ph = gb_stage(in, len, cs, clen + 32, sbuf[warp]);
+    const uint32_t clen = active ? (uint32_t)(len - cs < kGbChunk ? len - cs : kGbChunk) : 0u;
+    const uint32_t ph = active ? gb_stage(in, len, cs, clen + 32, sbuf[warp]) : 0u;
     __syncwarp();
     const uint32_t sa = sh_addr(sbuf[warp]) + ph;
     // the chunk's segment tables (gb_table_kernel), then every lane finds where the true
     // chain enters its segment and lists the group starts in it
-    {
+    if (active) {
         const uint4* src = reinterpret_cast<const uint4*>(segtab + chunk * (kGbE * 32));
         uint4* dst = reinterpret_cast<uint4*>(stab[warp]);
         for (uint32_t g = lane; g < kGbE * 32 * 2 / 16; g += 32) dst[g] = __ldg(src + g);
     }
     __syncwarp();
-    uint32_t i = 0, pos = rentry[chunk];
+    uint32_t i = 0, pos = active ? rentry[chunk] : 0u;
     for (uint32_t s = 0; s < (uint32_t)lane; ++s) {
         uint32_t a, b;
         gb_seg_bounds(s, clen, a, b);
@@ -392,7 +395,7 @@ __global__ void __launch_bounds__(32 * kGbWarps)
         i += t >> 5;
         pos = b + (t & 31u);
     }
-    const uint64_t left = ngroups - kb;
+    const uint64_t left = ngroups - kb;  // 0 when inactive
     const uint32_t lim = (uint32_t)(left < kGbMaxGroups ? left : kGbMaxGroups);  // groups of this call
     {
         uint32_t a, b;
@@ -407,8 +410,8 @@ __global__ void __launch_bounds__(32 * kGbWarps)
     __syncwarp();
     uint32_t run = 0;
     if constexpr (kDelta) {
-        // the chunk's value sum, then its carry by decoupled look-back over the chunks before
-        // it (lower chunks are dispatched first, so they are resident or done)
+        // the chunk's value sum, then its carry by decoupled look-back over the CTAs before
+        // it (lower CTAs are dispatched first, so they are resident or done)
         uint32_t tot = 0;
         for (uint32_t r = 0; r < m; r += 32) {
             const uint32_t i = r + lane;
@@ -420,16 +423,29 @@ __global__ void __launch_bounds__(32 * kGbWarps)
             }
         }
         tot = __reduce_add_sync(kFull, tot);
-        if (chunk == 0) {
-            if (lane == 0) st_relaxed_gpu(lstatus, pack_status(epoch, kFlagInclusive, (uint64_t)base + tot));
-            run = base;
-        } else {
-            if (lane == 0) st_relaxed_gpu(status_slot(lstatus, chunk), pack_status(epoch, kFlagAggregate, tot));
-            const uint64_t ex = lookback_exclusive_wide(lstatus, (uint32_t)chunk, epoch);
-            if (lane == 0)
-                st_relaxed_gpu(status_slot(lstatus, chunk), pack_status(epoch, kFlagInclusive, ex + tot));
-            run = (uint32_t)ex;
+        // one look-back per CTA (over CTAs, 4x shallower than per chunk): warp 0 combines the
+        // CTA's chunk sums, every warp adds those of the warps before it
+        if (lane == 0) wtot[warp] = tot;
+        __syncthreads();
+        if (warp == 0) {
+            uint32_t ctot = lane < kGbWarps ? wtot[lane] : 0u;
+            ctot = __reduce_add_sync(kFull, ctot);
+            uint64_t ex = base;
+            if (blockIdx.x == 0) {
+                if (lane == 0) st_relaxed_gpu(lstatus, pack_status(epoch, kFlagInclusive, (uint64_t)base + ctot));
+            } else {
+                if (lane == 0)
+                    st_relaxed_gpu(status_slot(lstatus, blockIdx.x), pack_status(epoch, kFlagAggregate, ctot));
+                ex = lookback_exclusive_wide(lstatus, blockIdx.x, epoch);
+                if (lane == 0)
+                    st_relaxed_gpu(status_slot(lstatus, blockIdx.x), pack_status(epoch, kFlagInclusive, ex + ctot));
+            }
+            if (lane == 0) cta_ex = (uint32_t)ex;
         }
+        __syncthreads();
+        run = cta_ex;
+        for (int w = 0; w < warp; ++w) run += wtot[w];
+        if (!active) return;
     }
     const bool out16 = (((uintptr_t)out) & 15) == 0;
     for (uint32_t r = 0; r < m; r += 32) {
