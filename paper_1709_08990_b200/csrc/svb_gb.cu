@@ -135,6 +135,17 @@ __global__ void __launch_bounds__(256)
             const uint32_t p = g ? (cnt ? __ldg(in + 4 * g - 1) : 0u) : prev;
             x = make_uint4(x.x - p, x.y - x.x, x.z - x.y, x.w - x.z);
         }
+        // all-small row (the encoder side): every group is 00 b0 b1 b2 b3, 160 bytes
+        if (__all_sync(kFull, cnt == 4 && (x.x | x.y | x.z | x.w) < 256u)) {
+            const uint32_t p = sb + off + 5u * (uint32_t)lane;
+            sts8(p, 0u);
+            sts8(p + 1, x.x);
+            sts8(p + 2, x.y);
+            sts8(p + 3, x.z);
+            sts8(p + 4, x.w);
+            off += 160u;
+            continue;
+        }
         uint32_t l[4], c = 0, gs = cnt ? 1u : 0u;
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
