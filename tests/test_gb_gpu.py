@@ -152,3 +152,27 @@ def test_device_api_misaligned(P, dev):
         dev.gb_decode(dst[shift: shift + len(want)], n, outb[1:])
         dev.check()
         assert np.array_equal(outb[1:].cpu().numpy().view(np.uint32), v)
+
+
+@pytest.mark.slow
+def test_gb_config2_full(P, dev):
+    """BASELINE cfg2 size (64M sorted integers, delta): the GPU varint-GB stream equals the
+    oracle's (digest) and decodes back exactly."""
+    import hashlib
+
+    import torch
+    from paper_1709_08990_b200 import gen
+    v = gen.config_array(2)
+    want = oracle.gb_encode(oracle.delta_encode(v, 0))
+    d_v = torch.from_numpy(v.view(np.int32)).cuda()
+    d_c = torch.empty(P.svb_max_compressed_bytes(v.size), dtype=torch.uint8, device="cuda")
+    d_len = torch.zeros(1, dtype=torch.int64, device="cuda")
+    dev.gb_encode(d_v, d_c, d_len, delta=True)
+    dev.check()
+    m = int(d_len.item())
+    assert m == len(want)
+    assert hashlib.sha256(d_c[:m].cpu().numpy().tobytes()).hexdigest() == hashlib.sha256(want).hexdigest()
+    d_o = torch.empty_like(d_v)
+    dev.gb_decode(d_c, v.size, d_o, in_len=m, delta=True)
+    dev.check()
+    assert torch.equal(d_o, d_v)

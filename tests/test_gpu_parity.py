@@ -365,3 +365,31 @@ def test_config3_full_roundtrip(dev):
     dev.decode(d_c, v.size, d_o, in_len=m)
     dev.check()
     assert torch.equal(d_o, d_v)
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("cfg", [4, 5])
+def test_batch_full_config(dev, cfg):
+    """Full BASELINE.json sizes of the batch configs (cfg4: 1M posting lists, ~2^30 integers;
+    cfg5: 2^31 integers in 64K-integer chunks with chained prev seeds): the batch encode ->
+    decode round trip is exact on the device, every segment's stream length equals the size
+    identity, and 256 sampled segments' streams equal the oracle's bytes."""
+    import torch
+
+    import bench
+    wl = bench.Batch(cfg, 0, 1, 1.0)
+    wl.setup(dev, torch)
+    wl.decode()
+    torch.cuda.synchronize()
+    wl.verify(torch)
+    lens = wl.d_lens.cpu().numpy().astype(np.uint64)
+    caps = (wl.lens.astype(np.uint64) + 3) // 4 + 4 * wl.lens.astype(np.uint64)
+    eoff = np.zeros(wl.nseg + 1, np.uint64)
+    np.cumsum(caps, out=eoff[1:])
+    rng = np.random.default_rng(cfg)
+    for i in sorted(rng.choice(wl.nseg, 256, replace=False)):
+        seg = wl.values[int(wl.offs[i]):int(wl.offs[i + 1])]
+        want = oracle.encode(seg, delta=True, prev=int(wl.prevs[i]))
+        assert int(lens[i]) == len(want) == oracle.compressed_size(seg, delta=True, prev=int(wl.prevs[i])), i
+        got = wl.d_c[int(eoff[i]):int(eoff[i]) + int(lens[i])].cpu().numpy().tobytes()
+        assert got == want, i
