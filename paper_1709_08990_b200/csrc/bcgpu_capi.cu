@@ -207,6 +207,15 @@ int bcgpu_debug_set_trace(bcgpu_ctx* c, void* d_trace) {
     return BCGPU_OK;
 }
 
+// Debug only (not in bcgpu.h): force a code path for A/B timing and the path-coverage
+// tests (tests/test_fuzz.py).  Bits:
+//   16      encode: two-read path (size scan + tile encode)
+//   32      encode: slot path (bits 6-7: its L2 policies)
+//   2048    encode: never the one-pass kernel;   4096  encode: one-pass for plain streams too
+//   512     host API: no piecewise pipelining
+//   1024    decode: sums pass + pooled delta decode instead of the one-pass kernel
+//   0x8000  decode: the control scan only (dev timing; output not written)
+//   bits 12-14 batch kernels: cap CTAs per SM
 int bcgpu_debug_set_flags(bcgpu_ctx* c, uint32_t flags) {
     if (!c) return BCGPU_ERR_INVALID_ARGUMENT;
     c->debug_flags = flags;
