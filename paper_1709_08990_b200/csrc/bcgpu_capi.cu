@@ -446,9 +446,9 @@ int bcgpu_svb_decode_batch_device(bcgpu_ctx* c, const bcgpu_decode_segment* d_se
     BatchArgs ba;
     int st = make_batch(c, s, &ba);
     if (st) return st;
-    (void)max_seg_n;  // reserved hint: one warp-per-segment kernel serves every size
+    ba.max_seg_n = max_seg_n;  // bounds every segment's n when non-zero: skips the long-segment kernel
     BC_CUDA(launch_decode_batch(d_segs, nseg, d_in, d_out, delta, ba, s));
-    g_launches.fetch_add(1);
+    g_launches.fetch_add(max_seg_n != 0 && max_seg_n <= kBatchSmallN ? 1 : 2);
     return BCGPU_OK;
 }
 

@@ -91,9 +91,12 @@ struct BCursor {
             const unsigned long long c = __shfl_sync(kFull, raw1, 2), np = __shfl_sync(kFull, raw1, 3);
             const uint32_t n = (uint32_t)np;
             const uint64_t ngroups = ((uint64_t)n + 3) >> 2;
-            if (n == 0 || (k == 0 && b < ngroups)) {
-                if (n != 0 && (threadIdx.x & 31) == 0) report(status, epoch, BCGPU_ERR_TRUNCATED);
-                if (n == 0 && b != 0 && (threadIdx.x & 31) == 0) report(status, epoch, BCGPU_ERR_TRAILING_BYTES);
+            if (n <= kBatchSmallN) {  // decoded segment-resident by svb_batch3.cu
+                next_segment();
+                continue;
+            }
+            if (k == 0 && b < ngroups) {
+                if ((threadIdx.x & 31) == 0) report(status, epoch, BCGPU_ERR_TRUNCATED);
                 next_segment();
                 continue;
             }

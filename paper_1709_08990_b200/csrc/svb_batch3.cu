@@ -1,0 +1,351 @@
+// svb_batch3.cu -- segment-resident batch decode for short segments (sm_100a).
+//
+// Reference behaviour: every segment is an independent Stream VByte stream
+// (svb_decode / svb_decode_delta, stream_vbyte.hpp:38-42, codec.hpp:85-90).
+//
+// Posting-list batches (cfg4) are dominated by short streams: half the lists
+// hold < 1024 integers and each list ends in a partial tile.  The tile
+// pipeline of svb_batch2.cu pays, per tile, a control-byte copy, a scan of
+// 256 control bytes, a data copy sized by that scan and a masked 8-row
+// expansion -- ~1600 warp instructions per tile on cfg4 (ncu), so the kernel
+// was issue-bound at a third of the HBM roofline.
+//
+// Here a segment whose worst-case stream fits kItemMax bytes is ONE item: the
+// descriptor alone locates the whole stream (src_offset, src_bytes), so one
+// TMA bulk copy brings control and data bytes together -- no dependent round
+// trip, no pre-scan.  Each warp owns a byte ring in shared memory and keeps as
+// many segments in flight as fit (up to kRSlots), then decodes the oldest one
+// straight from the ring, 512 integers per warp pass with each lane owning
+// four consecutive groups (one length scan and one delta scan per pass);
+// outputs at any 4-B phase leave as 128-bit stores of 16-B granules.
+// Longer segments stay on svb_batch2.cu (they are skipped here).
+#include <cstdint>
+
+#include "svb_device.cuh"
+#include "svb_fast.cuh"
+#include "svb_kernels.cuh"
+#include "svb_tma.cuh"
+#include "svb_warp.cuh"
+
+namespace bcgpu {
+
+namespace {
+
+constexpr int kRWarps = 4;
+constexpr int kRThreads = 32 * kRWarps;
+constexpr uint32_t kRingDefault = 8192;   // ring bytes per warp (launch-time; >= kItemMax)
+constexpr uint32_t kRingSlack = 192;      // over-reads past an item land here (control bytes of idle lanes: < 140 B)
+constexpr uint32_t kRSlots = 8;           // items in flight per warp
+constexpr uint32_t kItemMax = 8192;       // largest 16-B cover of an item
+static_assert(kBatchSmallN / 4 + 1 + 4ull * kBatchSmallN + 30 <= kItemMax, "short-segment stream must fit an item");
+
+struct RItem {
+    unsigned long long dst;  // element offset of integer 0
+    uint32_t n, prev, bytes;
+    uint32_t spos;           // ring byte of the segment's byte 0
+    uint32_t end;            // ring counter after the item (frees its bytes)
+    uint32_t pad;
+};
+
+struct __align__(16) RWarpHdr {  // per warp, ahead of the rings in dynamic shared memory
+    uint64_t bar[kRSlots];
+    RItem item[kRSlots];
+};
+
+__device__ __forceinline__ void report3(unsigned long long* st, uint32_t epoch, uint32_t code) {
+    if (st) *st = ((unsigned long long)epoch << 32) | code;
+}
+
+// Decode one resident segment.  S = shared address of its byte 0; returns the data bytes the
+// control stream declares (the caller checks it against the stream length).
+//
+// Lane-contiguous layout: a pass covers 128 control bytes (512 integers); lane l owns groups
+// 4l..4l+3 of it, so one 32-bit read gives its four control bytes, SWAR gives their lengths,
+// and ONE warp scan of the lane totals places every group.  The delta prefix is a lane-serial
+// sum over the lane's 16 integers plus one warp scan.  R = the output's 4-B phase inside
+// 16 B (template: the granule assembly below is static register moves): lane l stores the
+// granules [4q - R, 4q - R + 4) for its groups q; the first takes the previous group's last R
+// integers from lane l - 1 (lane 0: the previous pass's lane 31).
+template <uint32_t R>
+__device__ __forceinline__ void store_pass(const uint4 (&v)[4], uint32_t* __restrict__ o, uint32_t g0, int nints,
+                                           uint4& carry) {
+    const int lane = threadIdx.x & 31;
+    if constexpr (R == 0) {
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            const int e0 = 4 * (int)(g0 + k);
+            if (e0 + 4 <= nints)
+                stg_stream_v4(o + e0, v[k]);
+            else if (e0 < nints)
+                store_group(o + e0, v[k], (uint32_t)(nints - e0), false);
+        }
+    } else {
+        uint32_t* A = o - R;  // 16-B aligned
+        const int src = (lane + 31) & 31;
+        uint4 rot = make_uint4(0, 0, 0, 0);
+        rot.w = __shfl_sync(kFull, v[3].w, src);
+        if (R >= 2) rot.z = __shfl_sync(kFull, v[3].z, src);
+        if (R >= 3) rot.y = __shfl_sync(kFull, v[3].y, src);
+        const uint4 prv0 = lane == 0 ? carry : rot;
+        carry = rot;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            const uint4 pv = k == 0 ? prv0 : v[k - 1], cv = v[k];
+            const uint4 g = R == 1 ? make_uint4(pv.w, cv.x, cv.y, cv.z)
+                          : R == 2 ? make_uint4(pv.z, pv.w, cv.x, cv.y)
+                                   : make_uint4(pv.y, pv.z, pv.w, cv.x);
+            const int e0 = 4 * (int)(g0 + k) - (int)R;
+            if (e0 >= 0 && e0 + 4 <= nints) {
+                stg_stream_v4(A + 4 * (g0 + k), g);
+            } else {
+#pragma unroll
+                for (int i = 0; i < 4; ++i)
+                    if (e0 + i >= 0 && e0 + i < nints) A[4 * (g0 + k) + i] = comp(g, i);
+            }
+        }
+    }
+}
+
+template <bool kDelta>
+__device__ __forceinline__ uint32_t decode_resident(uint32_t S, uint32_t bytes, uint32_t n, uint32_t run,
+                                                    uint32_t* __restrict__ o) {
+    const int lane = threadIdx.x & 31;
+    const uint32_t R = (uint32_t)(((uintptr_t)o >> 2) & 3u);  // output phase inside 16 B
+    const uint32_t ng = (n + 3) >> 2;
+    const uint32_t tail = (n & 3u) ? (n & 3u) : 4u;                          // integers in the last group
+    const uint32_t tmask = (n & 3u) ? ((1u << (2 * (n & 3u))) - 1u) : 0xFFu;  // its used fields
+    const uint32_t D = S + ng, Dend = S + bytes;                            // data region [D, Dend)
+    const uint32_t passes = (ng + 127) >> 7;
+    uint32_t off = 0;
+    uint4 carry = make_uint4(0, 0, 0, 0);
+#pragma unroll 1
+    for (uint32_t ps = 0; ps < passes; ++ps) {
+        const uint32_t g0 = 128 * ps + 4 * lane;  // the lane's first group
+        const uint32_t ca = S + g0;
+        uint32_t cw = __funnelshift_r(lds32(ca & ~3u), lds32((ca & ~3u) + 4), (ca & 3u) << 3);
+        uint32_t lens;
+        const bool lastp = ps + 1 == passes;
+        uint32_t nv = 4;  // valid groups of the lane
+        if (!lastp) {
+            lens = swar_lengths(cw);
+        } else {
+            nv = ng > g0 ? (ng - g0 < 4 ? ng - g0 : 4u) : 0u;
+            const uint32_t bm = nv >= 4 ? 0xFFFFFFFFu : ((1u << (8 * nv)) - 1u);
+            if (nv && g0 + nv == ng) cw &= ~(0xFFu << (8 * (nv - 1))) | (tmask << (8 * (nv - 1)));
+            cw &= bm;
+            lens = swar_lengths(cw) & bm;
+            if (nv && g0 + nv == ng) lens -= (4u - tail) << (8 * (nv - 1));
+        }
+        const uint32_t lt = __dp4a(lens, 0x01010101u, 0u);  // <= 64
+        const uint32_t I = warp_inclusive_scan(lt);
+        uint32_t p = D + off + I - lt;
+        off += __shfl_sync(kFull, I, 31);
+        uint4 v[4];
+        if (__all_sync(kFull, cw == 0)) {
+#pragma unroll
+            for (int k = 0; k < 4; ++k) v[k] = zero_group_s(min(p + 4 * k, Dend));
+        } else {
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                v[k] = group_s(min(p, Dend), (cw >> (8 * k)) & 0xFFu);
+                p += (lens >> (8 * k)) & 0xFFu;
+            }
+        }
+        if (lastp) {
+#pragma unroll
+            for (int k = 0; k < 4; ++k)
+                v[k] = mask_tail(v[k], (uint32_t)k + 1 < nv ? 4u : ((uint32_t)k + 1 == nv ? (g0 + nv == ng ? tail : 4u) : 0u));
+        }
+        if constexpr (kDelta) {
+            uint32_t s = 0;
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                v[k].x += s;
+                v[k].y += v[k].x;
+                v[k].z += v[k].y;
+                v[k].w += v[k].z;
+                s = v[k].w;
+            }
+            const uint32_t Iv = warp_inclusive_scan(s);
+            const uint32_t add = run + Iv - s;
+#pragma unroll
+            for (int k = 0; k < 4; ++k) v[k] = add4(v[k], add);
+            run += __shfl_sync(kFull, Iv, 31);
+        }
+        switch (R) {  // warp-uniform; only these small store blocks are per phase
+            case 0: store_pass<0>(v, o, g0, (int)n, carry); break;
+            case 1: store_pass<1>(v, o, g0, (int)n, carry); break;
+            case 2: store_pass<2>(v, o, g0, (int)n, carry); break;
+            default: store_pass<3>(v, o, g0, (int)n, carry); break;
+        }
+    }
+    if (R != 0 && lane == 0) {  // the granule after the last pass: lane 31's last R integers (in carry)
+        const int e0 = 512 * (int)passes - (int)R;
+#pragma unroll
+        for (int i = 0; i < 3; ++i)
+            if (i < (int)R && e0 + i < (int)n) o[e0 + i] = comp(carry, 4 - (int)R + i);
+    }
+    return off;
+}
+
+}  // namespace
+
+template <bool kDelta>
+__global__ void __launch_bounds__(kRThreads)
+    svb_decode_batch3_kernel(const bcgpu_decode_segment* __restrict__ segs, uint64_t nseg,
+                             const uint8_t* __restrict__ in, uint32_t* __restrict__ out, unsigned long long* status,
+                             uint32_t epoch, uint32_t long_hint, uint32_t ring_bytes) {
+    extern __shared__ __align__(128) uint8_t rdsm[];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    RWarpHdr& B = reinterpret_cast<RWarpHdr*>(rdsm)[warp];
+    uint8_t* ring_p = rdsm + kRWarps * sizeof(RWarpHdr) + warp * (ring_bytes + kRingSlack);
+    if (lane == 0)
+        for (uint32_t q = 0; q < kRSlots; ++q) mbar_init1(&B.bar[q]);
+    __syncwarp();
+    const uint64_t gw = (uint64_t)blockIdx.x * kRWarps + warp, GW = (uint64_t)gridDim.x * kRWarps;
+    const uint64_t cnt = nseg > gw ? (nseg - gw + GW - 1) / GW : 0;  // segments gw, gw + GW, ...
+    const uint32_t ring = sh_addr(ring_p);
+    const uint64_t pol = l2_policy_drop();
+    const unsigned long long* sw = reinterpret_cast<const unsigned long long*>(segs);
+
+    // lane l holds the descriptor of the warp's segment dbase + l
+    uint64_t dbase = 0;
+    unsigned long long d0 = 0, d1 = 0, d2 = 0, d3 = 0;
+    auto refill = [&]() {
+        const uint64_t k = dbase + lane;
+        if (k < cnt) {
+            const unsigned long long* p = sw + 4 * (gw + k * GW);
+            d0 = __ldg(p);
+            d1 = __ldg(p + 1);
+            d2 = __ldg(p + 2);
+            d3 = __ldg(p + 3);
+        }
+    };
+    refill();
+    uint32_t di = 0;                // next descriptor of the batch (lane index)
+    uint32_t head = 0, tail = 0;    // ring byte counters (allocated incl. wrap waste, freed)
+    uint32_t hpos = 0;              // ring offset of the next allocation
+    uint32_t qh = 0, qt = 0;        // items issued, consumed
+    for (;;) {
+        // issue every segment that fits
+        while (qh - qt < kRSlots && dbase + di < cnt) {
+            const unsigned long long src = __shfl_sync(kFull, d0, di), bytes = __shfl_sync(kFull, d1, di);
+            const unsigned long long dst = __shfl_sync(kFull, d2, di), np = __shfl_sync(kFull, d3, di);
+            const uint32_t n = (uint32_t)np;
+            bool take = false;
+            uint32_t at = 0, cover = 0, waste = 0;
+            uintptr_t a0 = 0;
+            if (n > kBatchSmallN) {
+                // svb_batch2.cu decodes it -- unless the caller's max_seg_n said no segment is long
+                if (long_hint && n > long_hint && lane == 0) report3(status, epoch, BCGPU_ERR_INVALID_ARGUMENT);
+            } else {
+                const uint64_t ngroups = ((uint64_t)n + 3) >> 2;
+                if (n == 0) {
+                    if (bytes != 0 && lane == 0) report3(status, epoch, BCGPU_ERR_TRAILING_BYTES);
+                } else if (bytes < ngroups) {
+                    if (lane == 0) report3(status, epoch, BCGPU_ERR_TRUNCATED);
+                } else if (bytes > ngroups + 4ull * n) {
+                    if (lane == 0) report3(status, epoch, BCGPU_ERR_TRAILING_BYTES);
+                } else {
+                    const uintptr_t beg = (uintptr_t)in + src;
+                    a0 = beg & ~(uintptr_t)15;
+                    cover = (uint32_t)(((beg + bytes + 15) & ~(uintptr_t)15) - a0);
+                    if (qh == qt) head = tail = hpos = 0;  // empty ring: restart at 0 (any item fits)
+                    const bool wrap = hpos + cover > ring_bytes;  // skip the ring's end (possibly 0 bytes)
+                    waste = wrap ? ring_bytes - hpos : 0u;
+                    at = wrap ? 0u : hpos;
+                    if (head + waste + cover - tail > ring_bytes) break;  // wait for space
+                    take = true;
+                }
+            }
+            if (take) {
+                const uint32_t slot = qh % kRSlots;
+                if (lane == 0) {
+                    RItem& it = B.item[slot];
+                    it.dst = dst;
+                    it.n = n;
+                    it.prev = (uint32_t)(np >> 32);
+                    it.bytes = (uint32_t)bytes;
+                    it.spos = at + (uint32_t)(((uintptr_t)in + src) & 15);
+                    it.end = head + waste + cover;
+                    fence_async_smem();  // the ring bytes were last read through the generic proxy
+                    mbar_expect(&B.bar[slot], cover);
+                    tma_load_hint(ring_p + at, reinterpret_cast<const void*>(a0), cover, &B.bar[slot], pol);
+                }
+                head += waste + cover;
+                hpos = at + cover;
+                ++qh;
+            }
+            if (++di == 32) {
+                dbase += 32;
+                di = 0;
+                refill();
+            }
+        }
+        __syncwarp();  // lane 0's item records before every lane reads them
+        if (qh == qt) break;
+        // decode the oldest item
+        const uint32_t slot = qt % kRSlots;
+        mbar_wait_parity(&B.bar[slot], (qt / kRSlots) & 1u);
+        const RItem it = B.item[slot];
+        uint32_t* o = out + it.dst;
+        const uint32_t data = decode_resident<kDelta>(ring + it.spos, it.bytes, it.n, kDelta ? it.prev : 0u, o);
+        if (lane == 0) {
+            const uint64_t need = (uint64_t)((it.n + 3) >> 2) + data;
+            if (need != it.bytes) report3(status, epoch, need > it.bytes ? BCGPU_ERR_TRUNCATED : BCGPU_ERR_TRAILING_BYTES);
+        }
+        tail = it.end;
+        ++qt;
+        __syncwarp();
+    }
+}
+
+cudaError_t launch_decode_batch3(const bcgpu_decode_segment* segs, uint64_t nseg, const uint8_t* in, uint32_t* out,
+                                 int delta, const BatchArgs& ba, cudaStream_t stream) {
+    static int sms = 0, occ_default = 0;
+    static size_t attr_smem = 0;  // dynamic shared memory the kernels are currently allowed
+    const uint32_t ring_kb = (ba.flags >> 16) & 0xFFu;  // debug: ring KiB per warp
+    const uint32_t ring = ring_kb ? (ring_kb << 10 < kItemMax ? kItemMax : ring_kb << 10) : kRingDefault;
+    const size_t smem = kRWarps * (sizeof(RWarpHdr) + ring + kRingSlack);
+    if (smem > attr_smem) {
+        cudaFuncSetAttribute(svb_decode_batch3_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        cudaFuncSetAttribute(svb_decode_batch3_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        attr_smem = smem;
+    }
+    auto occupancy = [&]() {
+        int o1 = 0, o2 = 0;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o1, svb_decode_batch3_kernel<true>, kRThreads, smem);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o2, svb_decode_batch3_kernel<false>, kRThreads, smem);
+        const int o = o1 < o2 ? o1 : o2;
+        return o < 1 ? 1 : o;
+    };
+    if (!sms) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    }
+    int occ;
+    if (ring == kRingDefault) {
+        if (!occ_default) occ_default = occupancy();
+        occ = occ_default;
+    } else {
+        occ = occupancy();
+    }
+    const uint32_t occ_cap = (ba.flags >> 12) & 7u;  // debug: CTAs per SM
+    if (occ_cap && (int)occ_cap < occ) occ = (int)occ_cap;
+    const uint64_t want = (nseg + kRWarps - 1) / kRWarps, cap = (uint64_t)sms * occ;
+    const int grid = (int)(want < cap ? want : cap);
+    if (grid <= 0) return cudaSuccess;
+    // a non-zero max_seg_n <= kBatchSmallN means no long-segment launch follows: a longer
+    // segment contradicts the hint and is reported instead of silently skipped
+    const uint32_t hint = ba.max_seg_n != 0 && ba.max_seg_n <= kBatchSmallN ? ba.max_seg_n : 0u;
+    if (delta)
+        svb_decode_batch3_kernel<true><<<grid, kRThreads, smem, stream>>>(segs, nseg, in, out, ba.status, ba.epoch, hint,
+                                                                          ring);
+    else
+        svb_decode_batch3_kernel<false><<<grid, kRThreads, smem, stream>>>(segs, nseg, in, out, ba.status, ba.epoch, hint,
+                                                                           ring);
+    return cudaGetLastError();
+}
+
+}  // namespace bcgpu

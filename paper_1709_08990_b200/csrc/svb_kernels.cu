@@ -183,6 +183,9 @@ int occupancy_batch() { return occ_of((const void*)svb_sizes_batch_kernel<true>,
 // decode / encode batches: the warp-pipelined kernels of svb_batch2.cu
 cudaError_t launch_decode_batch(const bcgpu_decode_segment* segs, uint64_t nseg, const uint8_t* in, uint32_t* out,
                                 int delta, const BatchArgs& ba, cudaStream_t stream) {
+    // short segments: one copy per segment (svb_batch3.cu); the rest: tile pipeline (svb_batch2.cu)
+    cudaError_t e = launch_decode_batch3(segs, nseg, in, out, delta, ba, stream);
+    if (e != cudaSuccess || (ba.max_seg_n != 0 && ba.max_seg_n <= kBatchSmallN)) return e;
     return launch_decode_batch2(segs, nseg, in, out, delta, ba, stream);
 }
 

@@ -90,7 +90,12 @@ struct BatchArgs {
     uint32_t epoch;
     int grid;                    // CTAs of the warp-per-segment kernels (full residency)
     uint32_t flags = 0;          // debug flags of the ctx (bits 12..14: batch-decode CTAs per SM)
+    uint32_t max_seg_n = 0;      // caller's bound on every segment's n (0 = unknown)
 };
+
+// Segments with n <= kBatchSmallN decode segment-resident (svb_batch3.cu): their worst-case
+// stream (ceil(n/4) + 4n bytes) fits one ring item; longer ones take the tile pipeline.
+constexpr uint32_t kBatchSmallN = 1920;
 
 cudaError_t launch_decode_batch(const bcgpu_decode_segment* segs, uint64_t nseg, const uint8_t* in, uint32_t* out,
                                 int delta, const BatchArgs& ba, cudaStream_t stream);
@@ -101,6 +106,10 @@ cudaError_t launch_sizes_batch(const bcgpu_encode_segment* segs, uint64_t nseg, 
 
 // warp-pipelined batch decode (svb_batch2.cu)
 cudaError_t launch_decode_batch2(const bcgpu_decode_segment* segs, uint64_t nseg, const uint8_t* in, uint32_t* out,
+                                 int delta, const BatchArgs& ba, cudaStream_t stream);
+
+// segment-resident batch decode of the short segments (svb_batch3.cu)
+cudaError_t launch_decode_batch3(const bcgpu_decode_segment* segs, uint64_t nseg, const uint8_t* in, uint32_t* out,
                                  int delta, const BatchArgs& ba, cudaStream_t stream);
 
 cudaError_t launch_encode_batch2(const bcgpu_encode_segment* segs, uint64_t nseg, const uint32_t* in, uint8_t* out,
