@@ -52,6 +52,35 @@ struct __align__(16) RWarpHdr {  // per warp, ahead of the rings in dynamic shar
     RItem item[kRSlots];
 };
 
+// One control byte c whose data starts at shared byte address a -> 4 integers, from ONE read
+// of the 20-byte window (five 32-bit loads instead of two per integer: the scattered lane
+// addresses make every load ~3.5-way bank-conflicted, and shared-memory wavefronts bound
+// this kernel).  X = the 16 data bytes from a; integer i starts at byte s_i of X.
+__device__ __forceinline__ uint32_t low_bytes(uint32_t x, uint32_t l) {  // l in 1..4
+    return x & (0xFFFFFFFFu >> (32u - 8u * l));
+}
+__device__ __forceinline__ uint4 group_w5(uint32_t a, uint32_t c) {
+    const uint32_t wa = a & ~3u, sh = (a & 3u) << 3;
+    const uint32_t w0 = lds32(wa), w1 = lds32(wa + 4), w2 = lds32(wa + 8), w3 = lds32(wa + 12), w4 = lds32(wa + 16);
+    const uint32_t X0 = __funnelshift_r(w0, w1, sh), X1 = __funnelshift_r(w1, w2, sh),
+                   X2 = __funnelshift_r(w2, w3, sh), X3 = __funnelshift_r(w3, w4, sh);
+    const uint32_t l0 = (c & 3u) + 1u, l1 = ((c >> 2) & 3u) + 1u, l2 = ((c >> 4) & 3u) + 1u, l3 = (c >> 6) + 1u;
+    const uint32_t s1 = l0, s2 = s1 + l1, s3 = s2 + l2;  // s1 in 1..4, s2 in 2..8, s3 in 3..12
+    uint4 v;
+    v.x = low_bytes(X0, l0);
+    v.y = low_bytes(__funnelshift_rc(X0, X1, 8 * s1), l1);
+    {
+        const bool q = s2 > 4;
+        v.z = low_bytes(__funnelshift_rc(q ? X1 : X0, q ? X2 : X1, 8 * (q ? s2 - 4 : s2)), l2);
+    }
+    {
+        const bool q2 = s3 > 8, q1 = s3 > 4;
+        const uint32_t lo = q2 ? X2 : (q1 ? X1 : X0), hi = q2 ? X3 : (q1 ? X2 : X1);
+        v.w = low_bytes(__funnelshift_rc(lo, hi, 8 * (s3 - (q2 ? 8u : (q1 ? 4u : 0u)))), l3);
+    }
+    return v;
+}
+
 __device__ __forceinline__ void report3(unsigned long long* st, uint32_t epoch, uint32_t code) {
     if (st) *st = ((unsigned long long)epoch << 32) | code;
 }
@@ -147,7 +176,7 @@ __device__ __forceinline__ uint32_t decode_resident(uint32_t S, uint32_t bytes, 
         } else {
 #pragma unroll
             for (int k = 0; k < 4; ++k) {
-                v[k] = group_s(min(p, Dend), (cw >> (8 * k)) & 0xFFu);
+                v[k] = group_w5(min(p, Dend), (cw >> (8 * k)) & 0xFFu);
                 p += (lens >> (8 * k)) & 0xFFu;
             }
         }
