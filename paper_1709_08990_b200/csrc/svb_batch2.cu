@@ -317,7 +317,11 @@ struct BECursor {
             const unsigned long long c = __shfl_sync(kFull, raw1, 2), np = __shfl_sync(kFull, raw1, 3);
             const uint32_t n = (uint32_t)np;
             const uint64_t ngroups = ((uint64_t)n + 3) >> 2;
-            if (n == 0 || (k == 0 && b < ngroups + 4ull * n)) {
+            if (n <= kBatchSmallN) {  // encoded segment-resident by svb_batch3.cu
+                next_segment();
+                continue;
+            }
+            if (k == 0 && b < ngroups + 4ull * n) {
                 if ((threadIdx.x & 31) == 0) {
                     if (n == 0)
                         out_lens[s] = 0;

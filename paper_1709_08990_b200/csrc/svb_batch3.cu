@@ -377,4 +377,302 @@ cudaError_t launch_decode_batch3(const bcgpu_decode_segment* segs, uint64_t nseg
     return cudaGetLastError();
 }
 
+// ---------------------------------------------------------------------------
+// segment-resident batch encode (svb_encode / prev-seeded delta encode per segment,
+// stream_vbyte.hpp:36, codec.hpp:92-93, extension E2)
+// ---------------------------------------------------------------------------
+// A segment with n <= kBatchSmallN is one item: one TMA copy of its integers into the
+// warp's ring.  Groups are row-major (row j, lane l <-> control byte 32 j + l).  Per block of
+// three rows every lane first reads its three groups, forms deltas and lengths and writes
+// its control bytes; one packed scan places the rows' data.  Each lane then packs its
+// group's <= 16 bytes into four registers, shifts them onto the 4-B word grid of the data
+// buffer and writes the words it completes; the word it shares with the next group (its
+// "pending" word) travels to the next lane by one shuffle and is merged into that lane's
+// first word, so every shared-memory word is written once, by one lane.  The data is
+// packed in place, 16 bytes below the integers it replaces (a block's output never
+// reaches the next block's input); control bytes go to a small double buffer.  Both
+// leave as bulk stores of their 16-B aligned interiors plus edge bytes.
+namespace {
+
+constexpr uint32_t kEHead = 16;            // ring bytes reserved below an item's integers
+constexpr uint32_t kERingDefault = 9216;   // ring bytes per warp (sweep: 8-9 KiB best, 5 CTAs per SM)
+constexpr uint32_t kECtrlBuf = 512;        // >= 16 + ceil(kBatchSmallN / 4)
+static_assert(16 + (kBatchSmallN + 3) / 4 <= kECtrlBuf, "control buffer");
+
+struct EItem3 {
+    unsigned long long dst;  // byte offset of the segment's stream
+    unsigned long long seg;  // segment index (out_lens)
+    uint32_t n, prev;
+    uint32_t spos;           // ring byte of integer 0
+    uint32_t end;            // ring counter after the item
+};
+
+struct __align__(16) EWarpHdr {
+    uint64_t bar[kRSlots];
+    EItem3 item[kRSlots];
+    uint8_t ctrl[2][kECtrlBuf];
+};
+
+__device__ __forceinline__ uint32_t shl_c(uint32_t x, uint32_t s) { return __funnelshift_lc(0u, x, s); }  // s <= 32
+__device__ __forceinline__ uint32_t shr_c(uint32_t x, uint32_t s) { return __funnelshift_rc(x, 0u, s); }  // s <= 32
+
+// global [g, g + len) <- shared bytes at sp (sp has g's 16-B phase): bulk store of the aligned
+// interior (committed by the caller), lanes store the edge bytes
+__device__ __forceinline__ void put_bytes(uint8_t* g, const uint8_t* sp, uint32_t len) {
+    const int lane = threadIdx.x & 31;
+    const uintptr_t gb = (uintptr_t)g, ge = gb + len;
+    const uintptr_t a_lo = (gb + 15) & ~(uintptr_t)15, a_hi = ge & ~(uintptr_t)15;
+    if (a_hi > a_lo) {
+        if (lane == 0) tma_store(reinterpret_cast<void*>(a_lo), sp + (a_lo - gb), (uint32_t)(a_hi - a_lo));
+        const uint32_t nh = (uint32_t)(a_lo - gb), nt = (uint32_t)(ge - a_hi);
+        if ((uint32_t)lane < nh) g[lane] = sp[lane];
+        if ((uint32_t)lane < nt) g[(a_hi - gb) + lane] = sp[(a_hi - gb) + lane];
+    } else {
+        for (uint32_t i = lane; i < len; i += 32) g[i] = sp[i];
+    }
+}
+
+// Encode one resident segment: integers at shared Sin (4-B aligned), control bytes -> shared
+// byte cb + g, data -> shared byte db + q (db has the data destination's 16-B phase and lies
+// 1..16 bytes below Sin).  Returns the data bytes.
+template <bool kDelta>
+__device__ __forceinline__ uint32_t encode_resident(uint32_t Sin, uint32_t n, uint32_t prev, uint32_t cb, uint32_t db) {
+    const int lane = threadIdx.x & 31;
+    const uint32_t ng = (n + 3) >> 2;
+    const uint32_t tail = (n & 3u) ? (n & 3u) : 4u;
+    const uint32_t rows = (ng + 31) >> 5;
+    const bool al16 = (Sin & 15u) == 0;
+    uint32_t run = prev;   // x_{-1} of the next row (delta)
+    uint32_t carry = 0;    // pending word of the previous row's lane 31
+    uint32_t off = 0;
+#pragma unroll 1
+    for (uint32_t blk = 0; blk < rows; blk += 3) {
+        uint4 d[3];
+        uint32_t L4[3], P = 0;
+#pragma unroll
+        for (int j = 0; j < 3; ++j) {
+            const uint32_t g = 32 * (blk + j) + lane;
+            const uint32_t cnt = g + 1 < ng ? 4u : (g + 1 == ng ? tail : 0u);
+            const uint32_t a = cnt ? Sin + 16 * g : Sin;
+            uint4 x = al16 ? lds128(a) : make_uint4(lds32(a), lds32(a + 4), lds32(a + 8), lds32(a + 12));
+            if (cnt < 4) x = mask_tail(x, cnt);
+            if constexpr (kDelta) {
+                uint32_t pw = __shfl_up_sync(kFull, x.w, 1);
+                if (lane == 0) pw = run;
+                run = __shfl_sync(kFull, x.w, 31);
+                x = make_uint4(x.x - pw, x.y - x.x, x.z - x.y, x.w - x.z);
+                if (cnt < 4) x = mask_tail(x, cnt);
+            }
+            const uint32_t m0 = blen_m1(x.x), m1 = blen_m1(x.y), m2 = blen_m1(x.z), m3 = blen_m1(x.w);
+            // lengths (0 past the stream) packed one per byte; unused fields of a final partial
+            // control byte stay 0 (their integers are 0: length 1, field 0)
+            uint32_t L = (m0 + 1u) | ((m1 + 1u) << 8) | ((m2 + 1u) << 16) | ((m3 + 1u) << 24);
+            L &= cnt >= 4 ? 0xFFFFFFFFu : ((1u << (8 * cnt)) - 1u);
+            if (cnt) sts8(cb + g, m0 | (m1 << 2) | (m2 << 4) | (m3 << 6));
+            d[j] = x;
+            L4[j] = L;
+            P |= __dp4a(L, 0x01010101u, 0u) << (10 * j);
+        }
+        const uint32_t I = warp_inclusive_scan(P);
+        const uint32_t T = __shfl_sync(kFull, I, 31), E = I - P;
+        __syncwarp();  // every lane has read the block's integers before any lane packs over them
+#pragma unroll
+        for (int j = 0; j < 3; ++j) {
+            const uint32_t row = blk + j;
+            if (row >= rows) break;
+            const uint32_t g = 32 * row + lane;
+            const uint32_t L = L4[j];
+            const uint32_t l0 = L & 0xFFu, l1 = (L >> 8) & 0xFFu, l2 = (L >> 16) & 0xFFu;
+            const uint32_t len = ((E >> (10 * j)) & 0x3FFu), tot = __dp4a(L, 0x01010101u, 0u);
+            const uint32_t o = db + off + len;  // shared byte of the group's data
+            off += (T >> (10 * j)) & 0x3FFu;
+            // pack the group: A = d0 ++ d1, B = d2 ++ d3 (64-bit), P = A ++ B (128-bit)
+            const uint4 x = d[j];
+            const uint32_t Alo = x.x | shl_c(x.y, 8 * l0), Ahi = shr_c(x.y, 32 - 8 * l0);
+            const uint32_t Blo = x.z | shl_c(x.w, 8 * l2), Bhi = shr_c(x.w, 32 - 8 * l2);
+            const uint32_t t = 8 * (l0 + l1);  // 0..64
+            const bool hi = t >= 32;
+            const uint32_t tt = hi ? t - 32 : t;
+            const uint32_t q0 = shl_c(Blo, tt), q1 = __funnelshift_lc(Blo, Bhi, tt), q2 = shr_c(Bhi, 32 - tt);
+            const uint32_t P0 = Alo | (hi ? 0u : q0), P1 = Ahi | (hi ? q0 : q1), P2 = hi ? q1 : q2, P3 = hi ? q2 : 0u;
+            // onto the word grid: word k of the group = bytes [4k - u, 4k - u + 4) of P
+            const uint32_t u8 = (o & 3u) << 3;
+            const uint32_t W0 = shl_c(P0, u8), W1 = __funnelshift_lc(P0, P1, u8), W2 = __funnelshift_lc(P1, P2, u8),
+                           W3 = __funnelshift_lc(P2, P3, u8), W4 = __funnelshift_lc(P3, 0u, u8);
+            const uint32_t nw = ((o & 3u) + tot) >> 2;  // words this group completes (0 past the stream)
+            const uint32_t pend = nw == 0 ? W0 : nw == 1 ? W1 : nw == 2 ? W2 : nw == 3 ? W3 : W4;
+            uint32_t pin = __shfl_up_sync(kFull, pend, 1);
+            if (lane == 0) pin = carry;
+            carry = __shfl_sync(kFull, pend, 31);
+            const uint32_t wa = o & ~3u;
+            if (nw > 0) sts32(wa, W0 | pin);
+            if (nw > 1) sts32(wa + 4, W1);
+            if (nw > 2) sts32(wa + 8, W2);
+            if (nw > 3) sts32(wa + 12, W3);
+            if (g + 1 == ng && ((o + tot) & 3u)) sts32((o + tot) & ~3u, nw ? pend : (pend | pin));
+        }
+    }
+    return off;
+}
+
+}  // namespace
+
+template <bool kDelta>
+__global__ void __launch_bounds__(kRThreads)
+    svb_encode_batch3_kernel(const bcgpu_encode_segment* __restrict__ segs, uint64_t nseg,
+                             const uint32_t* __restrict__ in, uint8_t* __restrict__ out,
+                             uint64_t* __restrict__ out_lens, unsigned long long* status, uint32_t epoch,
+                             uint32_t long_hint, uint32_t ring_bytes) {
+    extern __shared__ __align__(128) uint8_t edsm[];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    EWarpHdr& B = reinterpret_cast<EWarpHdr*>(edsm)[warp];
+    uint8_t* ring_p = edsm + kRWarps * sizeof(EWarpHdr) + warp * (ring_bytes + kRingSlack);
+    if (lane == 0)
+        for (uint32_t q = 0; q < kRSlots; ++q) mbar_init1(&B.bar[q]);
+    __syncwarp();
+    const uint64_t gw = (uint64_t)blockIdx.x * kRWarps + warp, GW = (uint64_t)gridDim.x * kRWarps;
+    const uint64_t cnt = nseg > gw ? (nseg - gw + GW - 1) / GW : 0;
+    const uint32_t ring = sh_addr(ring_p);
+    const uint64_t pol = l2_policy_drop();
+    const unsigned long long* sw = reinterpret_cast<const unsigned long long*>(segs);
+    uint64_t dbase = 0;
+    unsigned long long d0 = 0, d1 = 0, d2 = 0, d3 = 0;
+    auto refill = [&]() {
+        const uint64_t k = dbase + lane;
+        if (k < cnt) {
+            const unsigned long long* p = sw + 4 * (gw + k * GW);
+            d0 = __ldg(p);
+            d1 = __ldg(p + 1);
+            d2 = __ldg(p + 2);
+            d3 = __ldg(p + 3);
+        }
+    };
+    refill();
+    uint32_t di = 0;
+    uint32_t head = 0, tail = 0, hpos = 0;
+    uint32_t tail_next = 0;  // freed once the newest item's bulk stores have read the ring
+    uint32_t qh = 0, qt = 0;
+    for (;;) {
+        while (qh - qt < kRSlots && dbase + di < cnt) {
+            const unsigned long long src = __shfl_sync(kFull, d0, di), cap = __shfl_sync(kFull, d1, di);
+            const unsigned long long dst = __shfl_sync(kFull, d2, di), np = __shfl_sync(kFull, d3, di);
+            const uint32_t n = (uint32_t)np;
+            const uint64_t s_idx = gw + (dbase + di) * GW;
+            bool take = false;
+            uint32_t at = 0, cover = 0, waste = 0;
+            uintptr_t a0 = 0;
+            if (n > kBatchSmallN) {
+                if (long_hint && n > long_hint && lane == 0) report3(status, epoch, BCGPU_ERR_INVALID_ARGUMENT);
+            } else if (n == 0) {
+                if (lane == 0) out_lens[s_idx] = 0;
+            } else if (cap < ((uint64_t)n + 3) / 4 + 4ull * n) {
+                if (lane == 0) report3(status, epoch, BCGPU_ERR_INVALID_ARGUMENT);
+            } else {
+                const uintptr_t beg = (uintptr_t)(in + src);
+                a0 = beg & ~(uintptr_t)15;
+                cover = (uint32_t)(((beg + 4ull * n + 15) & ~(uintptr_t)15) - a0) + kEHead;
+                if (qh == qt) {  // nothing unconsumed: once the last item's stores have read it, restart at 0
+                    if (tail_next != tail) {
+                        if (lane == 0) tma_store_wait_read();
+                        __syncwarp();
+                    }
+                    head = tail = tail_next = hpos = 0;
+                }
+                const bool wrap = hpos + cover > ring_bytes;
+                waste = wrap ? ring_bytes - hpos : 0u;
+                at = wrap ? 0u : hpos;
+                if (head + waste + cover - tail > ring_bytes) break;  // wait for space
+                take = true;
+            }
+            if (take) {
+                const uint32_t slot = qh % kRSlots;
+                if (lane == 0) {
+                    EItem3& it = B.item[slot];
+                    it.dst = dst;
+                    it.seg = s_idx;
+                    it.n = n;
+                    it.prev = (uint32_t)(np >> 32);
+                    it.spos = at + kEHead + (uint32_t)(((uintptr_t)(in + src)) & 15);
+                    it.end = head + waste + cover;
+                    fence_async_smem();
+                    mbar_expect(&B.bar[slot], cover - kEHead);
+                    tma_load_hint(ring_p + at + kEHead, reinterpret_cast<const void*>(a0), cover - kEHead, &B.bar[slot],
+                                  pol);
+                }
+                head += waste + cover;
+                hpos = at + cover;
+                ++qh;
+            }
+            if (++di == 32) {
+                dbase += 32;
+                di = 0;
+                refill();
+            }
+        }
+        __syncwarp();
+        if (qh == qt) break;
+        const uint32_t slot = qt % kRSlots;
+        mbar_wait_parity(&B.bar[slot], (qt / kRSlots) & 1u);
+        const EItem3 it = B.item[slot];
+        const uint32_t ng = (it.n + 3) >> 2;
+        uint8_t* gdst = out + it.dst;
+        const uint32_t hc = (uint32_t)((uintptr_t)gdst & 15), hd = (uint32_t)((uintptr_t)(gdst + ng) & 15);
+        const uint32_t Sin = ring + it.spos;
+        const uint32_t db = ((Sin - 16u) & ~15u) + hd;  // the item's reserved head: 1..31 bytes below Sin
+        uint8_t* cbuf = B.ctrl[qt & 1];
+        const uint32_t data = encode_resident<kDelta>(Sin, it.n, kDelta ? it.prev : 0u, sh_addr(cbuf) + hc, db);
+        fence_async_smem();
+        __syncwarp();
+        put_bytes(gdst, cbuf + hc, ng);
+        put_bytes(gdst + ng, ring_p + (db - ring), data);
+        if (lane == 0) {
+            tma_store_commit();
+            out_lens[it.seg] = (uint64_t)ng + data;
+            tma_store_wait_read_but1();  // the previous item's stores have read its ring bytes and ctrl buffer
+        }
+        __syncwarp();
+        tail = tail_next;
+        tail_next = it.end;
+        ++qt;
+    }
+    if (lane == 0) tma_store_wait_read();
+}
+
+cudaError_t launch_encode_batch3(const bcgpu_encode_segment* segs, uint64_t nseg, const uint32_t* in, uint8_t* out,
+                                 uint64_t* out_lens, int delta, const BatchArgs& ba, cudaStream_t stream) {
+    static int sms = 0;
+    static size_t attr_smem = 0;
+    const uint32_t ring_kb = (ba.flags >> 24) & 0xFFu;  // debug: ring KiB per warp
+    const uint32_t ring = ring_kb ? (ring_kb << 10 < kItemMax ? kItemMax : ring_kb << 10) : kERingDefault;
+    const size_t smem = kRWarps * (sizeof(EWarpHdr) + ring + kRingSlack);
+    if (smem > attr_smem) {
+        cudaFuncSetAttribute(svb_encode_batch3_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        cudaFuncSetAttribute(svb_encode_batch3_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        attr_smem = smem;
+    }
+    if (!sms) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    }
+    int o1 = 0, o2 = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o1, svb_encode_batch3_kernel<true>, kRThreads, smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o2, svb_encode_batch3_kernel<false>, kRThreads, smem);
+    int occ = o1 < o2 ? o1 : o2;
+    if (occ < 1) occ = 1;
+    const uint32_t occ_cap = (ba.flags >> 12) & 7u;  // debug: CTAs per SM
+    if (occ_cap && (int)occ_cap < occ) occ = (int)occ_cap;
+    const uint64_t want = (nseg + kRWarps - 1) / kRWarps, capg = (uint64_t)sms * occ;
+    const int grid = (int)(want < capg ? want : capg);
+    if (grid <= 0) return cudaSuccess;
+    const uint32_t hint = ba.max_seg_n != 0 && ba.max_seg_n <= kBatchSmallN ? ba.max_seg_n : 0u;
+    if (delta)
+        svb_encode_batch3_kernel<true><<<grid, kRThreads, smem, stream>>>(segs, nseg, in, out, out_lens, ba.status,
+                                                                          ba.epoch, hint, ring);
+    else
+        svb_encode_batch3_kernel<false><<<grid, kRThreads, smem, stream>>>(segs, nseg, in, out, out_lens, ba.status,
+                                                                           ba.epoch, hint, ring);
+    return cudaGetLastError();
+}
+
 }  // namespace bcgpu

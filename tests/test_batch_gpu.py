@@ -155,3 +155,110 @@ def test_ring_wraps_many_segments_per_warp(dev, ring_kb):
         _check(dev, vals, dst, d_out, s)
     finally:
         lib.bcgpu_debug_set_flags(dev._ctx, 0)
+
+
+def _run_encode(dev, sizes, delta, rng, *, gap_in=True, gap_out=True, hint=None, cap_short=None):
+    import torch
+    from paper_1709_08990_b200.device import ENCODE_SEG_DTYPE, segments_to_tensor
+    vals = [_values(rng, n, delta) for n in sizes]
+    prevs = rng.integers(0, 2**32, len(sizes), dtype=np.uint64).astype(np.uint32)
+    want = [oracle.encode(v, delta=delta, prev=int(p)) for v, p in zip(vals, prevs)]
+    caps = [(n + 3) // 4 + 4 * n for n in sizes]
+    src, dst, p, q = [], [], 0, 0
+    for n, c in zip(sizes, caps):
+        p += int(rng.integers(0, 7)) if gap_in else 0
+        q += int(rng.integers(0, 33)) if gap_out else 0
+        src.append(p)
+        dst.append(q)
+        p += n
+        q += c
+    segs = np.zeros(len(sizes), ENCODE_SEG_DTYPE)
+    segs["src_offset"], segs["dst_capacity"], segs["dst_offset"] = src, caps, dst
+    segs["n"], segs["prev"] = sizes, prevs
+    if cap_short is not None:
+        segs["dst_capacity"][cap_short] -= 1
+    flat = np.zeros(p + 4, np.uint32)
+    for s_, v in zip(src, vals):
+        flat[s_:s_ + v.size] = v
+    d_in = torch.from_numpy(flat.view(np.int32)).cuda()
+    d_out = torch.full((q + 64,), 0x5A, dtype=torch.uint8, device="cuda")
+    d_lens = torch.full((len(sizes),), -1, dtype=torch.int64, device="cuda")
+    dev.encode_batch(segments_to_tensor(segs, "cuda"), len(sizes), d_in, d_out, d_lens, delta=delta,
+                     max_seg_n=max(sizes) if hint is None else hint)
+    return want, dst, d_out, d_lens
+
+
+def _check_encode(dev, want, dst, d_out, d_lens):
+    dev.check()
+    got = d_out.cpu().numpy()
+    lens = d_lens.cpu().numpy()
+    assert np.array_equal(lens, [len(w) for w in want])
+    covered = np.zeros(got.size, bool)
+    for i, (w, d) in enumerate(zip(want, dst)):
+        assert got[d:d + len(w)].tobytes() == w, f"segment {i} n-bytes={len(w)} dst={d}"
+        covered[d:d + len(w)] = True
+    assert np.all(got[~covered] == 0x5A), "write outside the segments' streams"
+
+
+@pytest.mark.parametrize("delta", [True, False])
+def test_encode_short_segments_every_phase(dev, delta):
+    rng = np.random.default_rng(31 + delta)
+    sizes = list(range(1, 140)) + list(rng.integers(1, SMALL_N + 1, 600))
+    _check_encode(dev, *_run_encode(dev, sizes, delta, rng))
+
+
+@pytest.mark.parametrize("delta", [True, False])
+def test_encode_boundary_between_kernels(dev, delta):
+    rng = np.random.default_rng(41 + delta)
+    sizes = [SMALL_N - 1, SMALL_N, SMALL_N + 1, 1024, 1025, 4096 + 3, 96 * 4, 97 * 4, 128 * 3, 128 * 3 + 1,
+             70_000, 1, 2, 3, 4, 0] * 6
+    rng.shuffle(sizes)
+    for hint in (None, 0):
+        _check_encode(dev, *_run_encode(dev, sizes, delta, rng, hint=hint))
+
+
+def test_encode_small_values_and_wide_values(dev):
+    """All-one-byte deltas, all-four-byte values, and alternating widths (every pack shape)."""
+    import torch
+    from paper_1709_08990_b200.device import ENCODE_SEG_DTYPE, segments_to_tensor
+    rng = np.random.default_rng(7)
+    vals = [np.arange(1000, dtype=np.uint32) * 3, np.full(777, 0xF1F2F3F4, np.uint32),
+            np.tile(np.array([1, 300, 70000, 1 << 30], np.uint32), 300), rng.integers(0, 2**32, 1920, dtype=np.uint64).astype(np.uint32)]
+    for delta in (False, True):
+        want = [oracle.encode(v, delta=delta, prev=0) for v in vals]
+        caps = [(v.size + 3) // 4 + 4 * v.size for v in vals]
+        segs = np.zeros(len(vals), ENCODE_SEG_DTYPE)
+        segs["src_offset"] = np.concatenate([[0], np.cumsum([v.size for v in vals])[:-1]])
+        segs["dst_capacity"] = caps
+        segs["dst_offset"] = np.concatenate([[0], np.cumsum(caps)[:-1]]) + 3
+        segs["n"] = [v.size for v in vals]
+        d_in = torch.from_numpy(np.concatenate(vals).view(np.int32)).cuda()
+        d_out = torch.zeros(sum(caps) + 64, dtype=torch.uint8, device="cuda")
+        d_lens = torch.zeros(len(vals), dtype=torch.int64, device="cuda")
+        dev.encode_batch(segments_to_tensor(segs, "cuda"), len(vals), d_in, d_out, d_lens, delta=delta, max_seg_n=1920)
+        dev.check()
+        got = d_out.cpu().numpy()
+        for w, d in zip(want, segs["dst_offset"]):
+            assert got[int(d):int(d) + len(w)].tobytes() == w
+
+
+def test_encode_capacity_too_small(dev):
+    from paper_1709_08990_b200.codec import GpuError
+    rng = np.random.default_rng(9)
+    _run_encode(dev, [10, 500, 20], True, rng, cap_short=1, hint=0)
+    with pytest.raises(GpuError, match="(?i)invalid"):
+        dev.check()
+
+
+@pytest.mark.parametrize("ring_kb", [0, 8, 9, 13, 23])
+def test_encode_ring_wraps_many_segments_per_warp(dev, ring_kb):
+    import ctypes as C
+    from paper_1709_08990_b200._native import lib
+    lib.bcgpu_debug_set_flags.argtypes = [C.c_void_p, C.c_uint32]
+    rng = np.random.default_rng(200 + ring_kb)
+    sizes = list(rng.choice(np.array([1, 5, 64, 700, 1500, 1920]), 40_000, p=[.1, .2, .2, .2, .2, .1]))
+    lib.bcgpu_debug_set_flags(dev._ctx, (ring_kb << 24) | (1 << 12))
+    try:
+        _check_encode(dev, *_run_encode(dev, sizes, True, rng, gap_out=False))
+    finally:
+        lib.bcgpu_debug_set_flags(dev._ctx, 0)
