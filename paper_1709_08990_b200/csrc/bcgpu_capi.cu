@@ -461,9 +461,9 @@ int bcgpu_svb_encode_batch_device(bcgpu_ctx* c, const bcgpu_encode_segment* d_se
     BatchArgs ba;
     int st = make_batch(c, s, &ba);
     if (st) return st;
-    ba.max_seg_n = max_seg_n;
+    (void)max_seg_n;  // one kernel serves every segment length
     BC_CUDA(launch_encode_batch(d_segs, nseg, d_in, d_out, d_out_lens, delta, ba, s));
-    g_launches.fetch_add(max_seg_n != 0 && max_seg_n <= kBatchSmallN ? 1 : 2);
+    g_launches.fetch_add(1);
     return BCGPU_OK;
 }
 

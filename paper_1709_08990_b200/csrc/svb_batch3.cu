@@ -397,13 +397,15 @@ namespace {
 constexpr uint32_t kEHead = 16;            // ring bytes reserved below an item's integers
 constexpr uint32_t kERingDefault = 9216;   // ring bytes per warp (sweep: 8-9 KiB best, 5 CTAs per SM)
 constexpr uint32_t kECtrlBuf = 512;        // >= 16 + ceil(kBatchSmallN / 4)
+constexpr uint32_t kEPieceN = 1024;        // piece of a long segment (multiple of 128)
 static_assert(16 + (kBatchSmallN + 3) / 4 <= kECtrlBuf, "control buffer");
 
-struct EItem3 {
+struct EItem3 {               // one piece of a segment
     unsigned long long dst;  // byte offset of the segment's stream
     unsigned long long seg;  // segment index (out_lens)
-    uint32_t n, prev;
-    uint32_t spos;           // ring byte of integer 0
+    uint32_t n, prev;        // the segment's
+    uint32_t m, piece;       // integers of this piece, its index in the segment
+    uint32_t spos;           // ring byte of the piece's integer 0
     uint32_t end;            // ring counter after the item
 };
 
@@ -432,97 +434,144 @@ __device__ __forceinline__ void put_bytes(uint8_t* g, const uint8_t* sp, uint32_
     }
 }
 
-// Encode one resident segment: integers at shared Sin (4-B aligned), control bytes -> shared
-// byte cb + g, data -> shared byte db + q (db has the data destination's 16-B phase and lies
-// 1..16 bytes below Sin).  Returns the data bytes.
-template <bool kDelta>
-__device__ __forceinline__ uint32_t encode_resident(uint32_t Sin, uint32_t n, uint32_t prev, uint32_t cb, uint32_t db) {
+// One block of three rows of an encode piece (see encode_resident).  kFull: the three rows
+// hold 384 integers (no partial or absent groups, no masking).
+template <bool kDelta, bool kFB>
+__device__ __forceinline__ void encode_block(uint32_t Sin, uint32_t blk, uint32_t ng, uint32_t tail, uint32_t rows,
+                                             bool al16, uint32_t cb, uint32_t db, uint32_t& run, uint32_t& carry,
+                                             uint32_t& off) {
     const int lane = threadIdx.x & 31;
-    const uint32_t ng = (n + 3) >> 2;
-    const uint32_t tail = (n & 3u) ? (n & 3u) : 4u;
+    uint4 d[3];
+    uint32_t cnts[3];
+    uint32_t any = 0;
+#pragma unroll
+    for (int j = 0; j < 3; ++j) {
+        const uint32_t g = 32 * (blk + j) + lane;
+        const uint32_t cnt = kFB ? 4u : (g + 1 < ng ? 4u : (g + 1 == ng ? tail : 0u));
+        const uint32_t a = (kFB || cnt) ? Sin + 16 * g : Sin;
+        uint4 x = al16 ? lds128(a) : make_uint4(lds32(a), lds32(a + 4), lds32(a + 8), lds32(a + 12));
+        if (!kFB && cnt < 4) x = mask_tail(x, cnt);
+        if constexpr (kDelta) {
+            uint32_t pw = __shfl_up_sync(0xffffffffu, x.w, 1);
+            if (lane == 0) pw = run;
+            run = __shfl_sync(0xffffffffu, x.w, 31);
+            x = make_uint4(x.x - pw, x.y - x.x, x.z - x.y, x.w - x.z);
+            if (!kFB && cnt < 4) x = mask_tail(x, cnt);
+        }
+        d[j] = x;
+        cnts[j] = cnt;
+        any |= x.x | x.y | x.z | x.w;
+    }
+    if (kFB && __all_sync(0xffffffffu, any < 256u)) {
+        // every integer takes one byte: control bytes 0, group g's four bytes at data offset 4 g,
+        // one word per lane and row; every lane of a row shares the word phase u
+        const uint32_t u8 = ((db + off) & 3u) << 3;
+#pragma unroll
+        for (int j = 0; j < 3; ++j) {
+            const uint4 x = d[j];
+            sts8(cb + 32 * (blk + j) + lane, 0u);
+            const uint32_t P = __byte_perm(__byte_perm(x.x, x.y, 0x0040), __byte_perm(x.z, x.w, 0x0040), 0x5410);
+            const uint32_t o = db + off + 128 * j + 4 * lane;
+            __syncwarp();  // (in place) every lane has read the block before any lane writes
+            if (u8 == 0) {
+                sts32(o, P);
+            } else {
+                const uint32_t W0 = P << u8, W1 = P >> (32 - u8);
+                uint32_t pin = __shfl_up_sync(0xffffffffu, W1, 1);
+                if (lane == 0) pin = carry;
+                carry = __shfl_sync(0xffffffffu, W1, 31);
+                sts32(o & ~3u, W0 | pin);
+            }
+        }
+        if (u8 == 0) carry = 0;
+        off += 384;
+        // the piece's last group: its bytes in the word after it (lane 31's W1, now in carry)
+        if (blk + 3 == rows && u8 != 0 && lane == 0) sts32((db + off) & ~3u, carry);
+        return;
+    }
+    uint32_t L4[3], P = 0;
+#pragma unroll
+    for (int j = 0; j < 3; ++j) {
+        const uint4 x = d[j];
+        const uint32_t g = 32 * (blk + j) + lane, cnt = cnts[j];
+        const uint32_t m0 = blen_m1(x.x), m1 = blen_m1(x.y), m2 = blen_m1(x.z), m3 = blen_m1(x.w);
+        // lengths (0 past the stream) one per byte; unused fields of a final partial control
+        // byte stay 0 (their integers are 0: length 1, field 0)
+        uint32_t L = (m0 + 1u) | ((m1 + 1u) << 8) | ((m2 + 1u) << 16) | ((m3 + 1u) << 24);
+        if (!kFB) L &= cnt >= 4 ? 0xFFFFFFFFu : ((1u << (8 * cnt)) - 1u);
+        if (kFB || cnt) sts8(cb + g, m0 | (m1 << 2) | (m2 << 4) | (m3 << 6));
+        L4[j] = L;
+        P |= __dp4a(L, 0x01010101u, 0u) << (10 * j);
+    }
+    const uint32_t I = warp_inclusive_scan(P);
+    const uint32_t T = __shfl_sync(0xffffffffu, I, 31), E = I - P;
+    __syncwarp();  // every lane has read the block's integers before any lane packs over them
+#pragma unroll
+    for (int j = 0; j < 3; ++j) {
+        const uint32_t row = blk + j;
+        if (!kFB && row >= rows) break;
+        const uint32_t g = 32 * row + lane;
+        const uint32_t L = L4[j];
+        const uint32_t tot = __dp4a(L, 0x01010101u, 0u);
+        const uint32_t o = db + off + ((E >> (10 * j)) & 0x3FFu);  // shared byte of the group's data
+        off += (T >> (10 * j)) & 0x3FFu;
+        const uint4 x = d[j];
+        // pack the group: A = d0 ++ d1, B = d2 ++ d3 (64-bit), P = A ++ B (128-bit)
+        const uint32_t l0 = L & 0xFFu, l1 = (L >> 8) & 0xFFu, l2 = (L >> 16) & 0xFFu;
+        const uint32_t Alo = x.x | shl_c(x.y, 8 * l0), Ahi = shr_c(x.y, 32 - 8 * l0);
+        const uint32_t Blo = x.z | shl_c(x.w, 8 * l2), Bhi = shr_c(x.w, 32 - 8 * l2);
+        const uint32_t t = 8 * (l0 + l1);  // 0..64
+        const bool hi = t >= 32;
+        const uint32_t tt = hi ? t - 32 : t;
+        const uint32_t q0 = shl_c(Blo, tt), q1 = __funnelshift_lc(Blo, Bhi, tt), q2 = shr_c(Bhi, 32 - tt);
+        const uint32_t P0 = Alo | (hi ? 0u : q0), P1 = Ahi | (hi ? q0 : q1), P2 = hi ? q1 : q2, P3 = hi ? q2 : 0u;
+        // onto the word grid: word k of the group = bytes [4k - u, 4k - u + 4) of P
+        const uint32_t u8 = (o & 3u) << 3;
+        const uint32_t W0 = shl_c(P0, u8), W1 = __funnelshift_lc(P0, P1, u8), W2 = __funnelshift_lc(P1, P2, u8),
+                       W3 = __funnelshift_lc(P2, P3, u8), W4 = __funnelshift_lc(P3, 0u, u8);
+        const uint32_t nw = ((o & 3u) + tot) >> 2;  // words this group completes (0 past the stream)
+        const uint32_t pend = nw == 0 ? W0 : nw == 1 ? W1 : nw == 2 ? W2 : nw == 3 ? W3 : W4;
+        uint32_t pin = __shfl_up_sync(0xffffffffu, pend, 1);
+        if (lane == 0) pin = carry;
+        carry = __shfl_sync(0xffffffffu, pend, 31);
+        const uint32_t wa = o & ~3u;
+        if (nw > 0) sts32(wa, W0 | pin);
+        if (nw > 1) sts32(wa + 4, W1);
+        if (nw > 2) sts32(wa + 8, W2);
+        if (nw > 3) sts32(wa + 12, W3);
+        if (g + 1 == ng && ((o + tot) & 3u)) sts32((o + tot) & ~3u, nw ? pend : (pend | pin));
+    }
+}
+
+// Encode one resident piece of m integers at shared Sin (4-B aligned): control bytes -> shared
+// byte cb + g, data -> shared byte db + q (db has the data destination's 16-B phase and lies
+// 1..31 bytes below Sin).  run: x_{-1} (delta).  Returns the data bytes.
+template <bool kDelta>
+__device__ __forceinline__ uint32_t encode_resident(uint32_t Sin, uint32_t m, uint32_t run, uint32_t cb, uint32_t db) {
+    const uint32_t ng = (m + 3) >> 2;
+    const uint32_t tail = (m & 3u) ? (m & 3u) : 4u;
     const uint32_t rows = (ng + 31) >> 5;
     const bool al16 = (Sin & 15u) == 0;
-    uint32_t run = prev;   // x_{-1} of the next row (delta)
-    uint32_t carry = 0;    // pending word of the previous row's lane 31
+    uint32_t carry = 0;  // pending word of the previous row's lane 31
     uint32_t off = 0;
+    uint32_t blk = 0;
 #pragma unroll 1
-    for (uint32_t blk = 0; blk < rows; blk += 3) {
-        uint4 d[3];
-        uint32_t L4[3], P = 0;
-#pragma unroll
-        for (int j = 0; j < 3; ++j) {
-            const uint32_t g = 32 * (blk + j) + lane;
-            const uint32_t cnt = g + 1 < ng ? 4u : (g + 1 == ng ? tail : 0u);
-            const uint32_t a = cnt ? Sin + 16 * g : Sin;
-            uint4 x = al16 ? lds128(a) : make_uint4(lds32(a), lds32(a + 4), lds32(a + 8), lds32(a + 12));
-            if (cnt < 4) x = mask_tail(x, cnt);
-            if constexpr (kDelta) {
-                uint32_t pw = __shfl_up_sync(kFull, x.w, 1);
-                if (lane == 0) pw = run;
-                run = __shfl_sync(kFull, x.w, 31);
-                x = make_uint4(x.x - pw, x.y - x.x, x.z - x.y, x.w - x.z);
-                if (cnt < 4) x = mask_tail(x, cnt);
-            }
-            const uint32_t m0 = blen_m1(x.x), m1 = blen_m1(x.y), m2 = blen_m1(x.z), m3 = blen_m1(x.w);
-            // lengths (0 past the stream) packed one per byte; unused fields of a final partial
-            // control byte stay 0 (their integers are 0: length 1, field 0)
-            uint32_t L = (m0 + 1u) | ((m1 + 1u) << 8) | ((m2 + 1u) << 16) | ((m3 + 1u) << 24);
-            L &= cnt >= 4 ? 0xFFFFFFFFu : ((1u << (8 * cnt)) - 1u);
-            if (cnt) sts8(cb + g, m0 | (m1 << 2) | (m2 << 4) | (m3 << 6));
-            d[j] = x;
-            L4[j] = L;
-            P |= __dp4a(L, 0x01010101u, 0u) << (10 * j);
-        }
-        const uint32_t I = warp_inclusive_scan(P);
-        const uint32_t T = __shfl_sync(kFull, I, 31), E = I - P;
-        __syncwarp();  // every lane has read the block's integers before any lane packs over them
-#pragma unroll
-        for (int j = 0; j < 3; ++j) {
-            const uint32_t row = blk + j;
-            if (row >= rows) break;
-            const uint32_t g = 32 * row + lane;
-            const uint32_t L = L4[j];
-            const uint32_t l0 = L & 0xFFu, l1 = (L >> 8) & 0xFFu, l2 = (L >> 16) & 0xFFu;
-            const uint32_t len = ((E >> (10 * j)) & 0x3FFu), tot = __dp4a(L, 0x01010101u, 0u);
-            const uint32_t o = db + off + len;  // shared byte of the group's data
-            off += (T >> (10 * j)) & 0x3FFu;
-            // pack the group: A = d0 ++ d1, B = d2 ++ d3 (64-bit), P = A ++ B (128-bit)
-            const uint4 x = d[j];
-            const uint32_t Alo = x.x | shl_c(x.y, 8 * l0), Ahi = shr_c(x.y, 32 - 8 * l0);
-            const uint32_t Blo = x.z | shl_c(x.w, 8 * l2), Bhi = shr_c(x.w, 32 - 8 * l2);
-            const uint32_t t = 8 * (l0 + l1);  // 0..64
-            const bool hi = t >= 32;
-            const uint32_t tt = hi ? t - 32 : t;
-            const uint32_t q0 = shl_c(Blo, tt), q1 = __funnelshift_lc(Blo, Bhi, tt), q2 = shr_c(Bhi, 32 - tt);
-            const uint32_t P0 = Alo | (hi ? 0u : q0), P1 = Ahi | (hi ? q0 : q1), P2 = hi ? q1 : q2, P3 = hi ? q2 : 0u;
-            // onto the word grid: word k of the group = bytes [4k - u, 4k - u + 4) of P
-            const uint32_t u8 = (o & 3u) << 3;
-            const uint32_t W0 = shl_c(P0, u8), W1 = __funnelshift_lc(P0, P1, u8), W2 = __funnelshift_lc(P1, P2, u8),
-                           W3 = __funnelshift_lc(P2, P3, u8), W4 = __funnelshift_lc(P3, 0u, u8);
-            const uint32_t nw = ((o & 3u) + tot) >> 2;  // words this group completes (0 past the stream)
-            const uint32_t pend = nw == 0 ? W0 : nw == 1 ? W1 : nw == 2 ? W2 : nw == 3 ? W3 : W4;
-            uint32_t pin = __shfl_up_sync(kFull, pend, 1);
-            if (lane == 0) pin = carry;
-            carry = __shfl_sync(kFull, pend, 31);
-            const uint32_t wa = o & ~3u;
-            if (nw > 0) sts32(wa, W0 | pin);
-            if (nw > 1) sts32(wa + 4, W1);
-            if (nw > 2) sts32(wa + 8, W2);
-            if (nw > 3) sts32(wa + 12, W3);
-            if (g + 1 == ng && ((o + tot) & 3u)) sts32((o + tot) & ~3u, nw ? pend : (pend | pin));
-        }
-    }
+    for (; (blk + 3) * 128 <= m; blk += 3) encode_block<kDelta, true>(Sin, blk, ng, tail, rows, al16, cb, db, run, carry, off);
+    if (blk < rows) encode_block<kDelta, false>(Sin, blk, ng, tail, rows, al16, cb, db, run, carry, off);
     return off;
 }
 
 }  // namespace
 
+// Items are pieces: a segment of n <= kBatchSmallN integers is one piece; a longer one is cut
+// into kEPieceN-integer pieces that the same warp encodes in order, carrying the data offset
+// and the delta base in registers (control bytes of piece k at k * kEPieceN / 4).
 template <bool kDelta>
 __global__ void __launch_bounds__(kRThreads)
     svb_encode_batch3_kernel(const bcgpu_encode_segment* __restrict__ segs, uint64_t nseg,
                              const uint32_t* __restrict__ in, uint8_t* __restrict__ out,
                              uint64_t* __restrict__ out_lens, unsigned long long* status, uint32_t epoch,
-                             uint32_t long_hint, uint32_t ring_bytes) {
+                             uint32_t ring_bytes) {
     extern __shared__ __align__(128) uint8_t edsm[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     EWarpHdr& B = reinterpret_cast<EWarpHdr*>(edsm)[warp];
@@ -549,28 +598,32 @@ __global__ void __launch_bounds__(kRThreads)
     };
     refill();
     uint32_t di = 0;
+    uint32_t piece = 0;      // next piece of descriptor di
     uint32_t head = 0, tail = 0, hpos = 0;
     uint32_t tail_next = 0;  // freed once the newest item's bulk stores have read the ring
     uint32_t qh = 0, qt = 0;
+    uint32_t run = 0;        // delta base of the next piece of the segment being encoded
+    unsigned long long off = 0;  // data bytes of the segment's earlier pieces
     for (;;) {
         while (qh - qt < kRSlots && dbase + di < cnt) {
             const unsigned long long src = __shfl_sync(kFull, d0, di), cap = __shfl_sync(kFull, d1, di);
             const unsigned long long dst = __shfl_sync(kFull, d2, di), np = __shfl_sync(kFull, d3, di);
             const uint32_t n = (uint32_t)np;
             const uint64_t s_idx = gw + (dbase + di) * GW;
-            bool take = false;
-            uint32_t at = 0, cover = 0, waste = 0;
+            const uint32_t pn = n <= kBatchSmallN ? n : kEPieceN;  // integers per piece
+            const uint32_t npieces = n <= kBatchSmallN ? (n ? 1u : 0u) : (uint32_t)(((uint64_t)n + kEPieceN - 1) / kEPieceN);
+            bool take = false, done = true;
+            uint32_t at = 0, cover = 0, waste = 0, m = 0;
             uintptr_t a0 = 0;
-            if (n > kBatchSmallN) {
-                if (long_hint && n > long_hint && lane == 0) report3(status, epoch, BCGPU_ERR_INVALID_ARGUMENT);
-            } else if (n == 0) {
+            if (n == 0) {
                 if (lane == 0) out_lens[s_idx] = 0;
-            } else if (cap < ((uint64_t)n + 3) / 4 + 4ull * n) {
+            } else if (piece == 0 && cap < ((uint64_t)n + 3) / 4 + 4ull * n) {
                 if (lane == 0) report3(status, epoch, BCGPU_ERR_INVALID_ARGUMENT);
             } else {
-                const uintptr_t beg = (uintptr_t)(in + src);
+                m = piece + 1 < npieces ? pn : n - piece * pn;
+                const uintptr_t beg = (uintptr_t)(in + src + (uint64_t)piece * pn);
                 a0 = beg & ~(uintptr_t)15;
-                cover = (uint32_t)(((beg + 4ull * n + 15) & ~(uintptr_t)15) - a0) + kEHead;
+                cover = (uint32_t)(((beg + 4ull * m + 15) & ~(uintptr_t)15) - a0) + kEHead;
                 if (qh == qt) {  // nothing unconsumed: once the last item's stores have read it, restart at 0
                     if (tail_next != tail) {
                         if (lane == 0) tma_store_wait_read();
@@ -583,6 +636,7 @@ __global__ void __launch_bounds__(kRThreads)
                 at = wrap ? 0u : hpos;
                 if (head + waste + cover - tail > ring_bytes) break;  // wait for space
                 take = true;
+                done = piece + 1 == npieces;
             }
             if (take) {
                 const uint32_t slot = qh % kRSlots;
@@ -592,7 +646,9 @@ __global__ void __launch_bounds__(kRThreads)
                     it.seg = s_idx;
                     it.n = n;
                     it.prev = (uint32_t)(np >> 32);
-                    it.spos = at + kEHead + (uint32_t)(((uintptr_t)(in + src)) & 15);
+                    it.m = m;
+                    it.piece = piece;
+                    it.spos = at + kEHead + (uint32_t)((uintptr_t)(in + src + (uint64_t)piece * pn) & 15);
                     it.end = head + waste + cover;
                     fence_async_smem();
                     mbar_expect(&B.bar[slot], cover - kEHead);
@@ -603,10 +659,15 @@ __global__ void __launch_bounds__(kRThreads)
                 hpos = at + cover;
                 ++qh;
             }
-            if (++di == 32) {
-                dbase += 32;
-                di = 0;
-                refill();
+            if (done) {
+                piece = 0;
+                if (++di == 32) {
+                    dbase += 32;
+                    di = 0;
+                    refill();
+                }
+            } else {
+                ++piece;
             }
         }
         __syncwarp();
@@ -614,20 +675,28 @@ __global__ void __launch_bounds__(kRThreads)
         const uint32_t slot = qt % kRSlots;
         mbar_wait_parity(&B.bar[slot], (qt / kRSlots) & 1u);
         const EItem3 it = B.item[slot];
-        const uint32_t ng = (it.n + 3) >> 2;
-        uint8_t* gdst = out + it.dst;
-        const uint32_t hc = (uint32_t)((uintptr_t)gdst & 15), hd = (uint32_t)((uintptr_t)(gdst + ng) & 15);
+        const uint32_t ngT = (it.n + 3) >> 2, pn = it.n <= kBatchSmallN ? it.n : kEPieceN;
+        const uint32_t ng = (it.m + 3) >> 2;
+        if (it.piece == 0) {
+            run = kDelta ? it.prev : 0u;
+            off = 0;
+        }
+        uint8_t* gctrl = out + it.dst + (uint64_t)it.piece * (pn >> 2);
+        uint8_t* gdata = out + it.dst + ngT + off;
+        const uint32_t hc = (uint32_t)((uintptr_t)gctrl & 15), hd = (uint32_t)((uintptr_t)gdata & 15);
         const uint32_t Sin = ring + it.spos;
         const uint32_t db = ((Sin - 16u) & ~15u) + hd;  // the item's reserved head: 1..31 bytes below Sin
         uint8_t* cbuf = B.ctrl[qt & 1];
-        const uint32_t data = encode_resident<kDelta>(Sin, it.n, kDelta ? it.prev : 0u, sh_addr(cbuf) + hc, db);
+        const uint32_t data = encode_resident<kDelta>(Sin, it.m, run, sh_addr(cbuf) + hc, db);
+        if constexpr (kDelta) run = lds32(Sin + 4 * (it.m - 1));  // x_{-1} of the next piece
+        off += data;
         fence_async_smem();
         __syncwarp();
-        put_bytes(gdst, cbuf + hc, ng);
-        put_bytes(gdst + ng, ring_p + (db - ring), data);
+        put_bytes(gctrl, cbuf + hc, ng);
+        put_bytes(gdata, ring_p + (db - ring), data);
         if (lane == 0) {
             tma_store_commit();
-            out_lens[it.seg] = (uint64_t)ng + data;
+            if ((uint64_t)(it.piece + 1) * pn >= it.n) out_lens[it.seg] = (uint64_t)ngT + off;
             tma_store_wait_read_but1();  // the previous item's stores have read its ring bytes and ctrl buffer
         }
         __syncwarp();
@@ -665,13 +734,12 @@ cudaError_t launch_encode_batch3(const bcgpu_encode_segment* segs, uint64_t nseg
     const uint64_t want = (nseg + kRWarps - 1) / kRWarps, capg = (uint64_t)sms * occ;
     const int grid = (int)(want < capg ? want : capg);
     if (grid <= 0) return cudaSuccess;
-    const uint32_t hint = ba.max_seg_n != 0 && ba.max_seg_n <= kBatchSmallN ? ba.max_seg_n : 0u;
     if (delta)
         svb_encode_batch3_kernel<true><<<grid, kRThreads, smem, stream>>>(segs, nseg, in, out, out_lens, ba.status,
-                                                                          ba.epoch, hint, ring);
+                                                                          ba.epoch, ring);
     else
         svb_encode_batch3_kernel<false><<<grid, kRThreads, smem, stream>>>(segs, nseg, in, out, out_lens, ba.status,
-                                                                           ba.epoch, hint, ring);
+                                                                           ba.epoch, ring);
     return cudaGetLastError();
 }
 

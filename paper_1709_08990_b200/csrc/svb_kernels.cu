@@ -191,10 +191,8 @@ cudaError_t launch_decode_batch(const bcgpu_decode_segment* segs, uint64_t nseg,
 
 cudaError_t launch_encode_batch(const bcgpu_encode_segment* segs, uint64_t nseg, const uint32_t* in, uint8_t* out,
                                 uint64_t* out_lens, int delta, const BatchArgs& ba, cudaStream_t stream) {
-    // short segments: segment-resident (svb_batch3.cu); the rest: tile pipeline (svb_batch2.cu)
-    cudaError_t e = launch_encode_batch3(segs, nseg, in, out, out_lens, delta, ba, stream);
-    if (e != cudaSuccess || (ba.max_seg_n != 0 && ba.max_seg_n <= kBatchSmallN)) return e;
-    return launch_encode_batch2(segs, nseg, in, out, out_lens, delta, ba, stream);
+    // every segment: resident pieces (svb_batch3.cu)
+    return launch_encode_batch3(segs, nseg, in, out, out_lens, delta, ba, stream);
 }
 
 cudaError_t launch_sizes_batch(const bcgpu_encode_segment* segs, uint64_t nseg, const uint32_t* in,

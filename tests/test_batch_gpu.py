@@ -20,7 +20,10 @@ def dev():
     return DeviceCodec(0)
 
 
-def _values(rng, n, delta):
+def _values(rng, n, delta, small=False):
+    if small:  # every delta (or value) < 256: the all-one-byte encode path
+        g = rng.integers(0, 256, n, dtype=np.uint64)
+        return (np.cumsum(g) if delta else g).astype(np.uint32)
     if delta:
         gaps = rng.choice(np.array([1, 200, 70_000, 1 << 24], np.uint64), n, p=[0.4, 0.3, 0.2, 0.1])
         return np.cumsum(gaps * rng.integers(1, 3, n, dtype=np.uint64)).astype(np.uint32)
@@ -157,10 +160,10 @@ def test_ring_wraps_many_segments_per_warp(dev, ring_kb):
         lib.bcgpu_debug_set_flags(dev._ctx, 0)
 
 
-def _run_encode(dev, sizes, delta, rng, *, gap_in=True, gap_out=True, hint=None, cap_short=None):
+def _run_encode(dev, sizes, delta, rng, *, gap_in=True, gap_out=True, hint=None, cap_short=None, small=None):
     import torch
     from paper_1709_08990_b200.device import ENCODE_SEG_DTYPE, segments_to_tensor
-    vals = [_values(rng, n, delta) for n in sizes]
+    vals = [_values(rng, n, delta, small=small is not None and rng.random() < small) for n in sizes]
     prevs = rng.integers(0, 2**32, len(sizes), dtype=np.uint64).astype(np.uint32)
     want = [oracle.encode(v, delta=delta, prev=int(p)) for v, p in zip(vals, prevs)]
     caps = [(n + 3) // 4 + 4 * n for n in sizes]
@@ -262,3 +265,13 @@ def test_encode_ring_wraps_many_segments_per_warp(dev, ring_kb):
         _check_encode(dev, *_run_encode(dev, sizes, True, rng, gap_out=False))
     finally:
         lib.bcgpu_debug_set_flags(dev._ctx, 0)
+
+
+@pytest.mark.parametrize("delta", [True, False])
+def test_encode_one_byte_blocks(dev, delta):
+    """Segments (and long-segment pieces) whose 384-integer blocks are all one-byte, at every
+    data phase, including pieces that end exactly on a block (n = 384 k)."""
+    rng = np.random.default_rng(51 + delta)
+    sizes = [384, 768, 1152, 1536, 1920, 383, 385, 1024, 3 * 1024, 5000, 65536, 130_000, 7] * 4
+    rng.shuffle(sizes)
+    _check_encode(dev, *_run_encode(dev, sizes, delta, rng, small=0.8))
