@@ -255,7 +255,7 @@ __global__ void __launch_bounds__(kCTThreads, 4)
     if (small)
         enc_small_pack<kDelta>(sh_addr(b.stage) + 16, prev_w, sh_addr(b.stage) + head);
     else if (full)
-        enc_full_pack<kDelta>(sh_addr(b.stage) + 16, prev_w, lens, qw, sh_addr(b.stage) + head);
+        enc_full_pack_w<kDelta>(sh_addr(b.stage) + 16, prev_w, lens, qw, sh_addr(b.stage) + head, total);
     else
         encode_pack_at(t, b.stage, head);
     fence_async_smem();

@@ -479,6 +479,61 @@ __device__ __forceinline__ void enc_full_pack(uint32_t sin, uint32_t prev_w, con
     }
 }
 
+// Word-store pack of a full sub-tile (replaces the byte stores of enc_full_pack): each lane
+// packs its group's <= 16 bytes into four registers (two 64-bit concatenations and one
+// 128-bit one), shifts them onto the 4-B word grid and stores the words it completes; the
+// word it shares with the next group travels to the next lane by one shuffle and is OR-ed
+// into that lane's first word, so each shared word is written once, by one lane.  In place
+// like enc_full_pack: a row's completed words end before the next row's integers, and the
+// last lane's shared word is written while packing the next row.  The sub-tile's final
+// shared word is written at the end.
+__device__ __forceinline__ uint32_t shl_clamp(uint32_t x, uint32_t s) { return __funnelshift_lc(0u, x, s); }
+__device__ __forceinline__ uint32_t shr_clamp(uint32_t x, uint32_t s) { return __funnelshift_rc(x, 0u, s); }
+
+// group x (byte lengths packed one per byte in L, tot = their sum) at shared byte o; returns
+// the group's shared trailing word (pend) after storing the completed ones (pin = the
+// previous group's pend)
+__device__ __forceinline__ uint32_t pack_group_words(const uint4& x, uint32_t L, uint32_t o, uint32_t& carry) {
+    const int lane = threadIdx.x & 31;
+    const uint32_t l0 = L & 0xFFu, l1 = (L >> 8) & 0xFFu, l2 = (L >> 16) & 0xFFu;
+    const uint32_t tot = __dp4a(L, 0x01010101u, 0u);
+    const uint32_t Alo = x.x | shl_clamp(x.y, 8 * l0), Ahi = shr_clamp(x.y, 32 - 8 * l0);
+    const uint32_t Blo = x.z | shl_clamp(x.w, 8 * l2), Bhi = shr_clamp(x.w, 32 - 8 * l2);
+    const uint32_t t = 8 * (l0 + l1);
+    const bool hi = t >= 32;
+    const uint32_t tt = hi ? t - 32 : t;
+    const uint32_t q0 = shl_clamp(Blo, tt), q1 = __funnelshift_lc(Blo, Bhi, tt), q2 = shr_clamp(Bhi, 32 - tt);
+    const uint32_t P0 = Alo | (hi ? 0u : q0), P1 = Ahi | (hi ? q0 : q1), P2 = hi ? q1 : q2, P3 = hi ? q2 : 0u;
+    const uint32_t u8 = (o & 3u) << 3;
+    const uint32_t W0 = shl_clamp(P0, u8), W1 = __funnelshift_lc(P0, P1, u8), W2 = __funnelshift_lc(P1, P2, u8),
+                   W3 = __funnelshift_lc(P2, P3, u8), W4 = __funnelshift_lc(P3, 0u, u8);
+    const uint32_t nw = ((o & 3u) + tot) >> 2;  // >= 1: a full group has >= 4 bytes
+    const uint32_t pend = nw == 1 ? W1 : nw == 2 ? W2 : nw == 3 ? W3 : W4;
+    uint32_t pin = __shfl_up_sync(kFull, pend, 1);
+    if (lane == 0) pin = carry;
+    carry = __shfl_sync(kFull, pend, 31);
+    const uint32_t wa = o & ~3u;
+    sts32(wa, W0 | pin);
+    if (nw > 1) sts32(wa + 4, W1);
+    if (nw > 2) sts32(wa + 8, W2);
+    if (nw > 3) sts32(wa + 12, W3);
+    return pend;
+}
+
+template <bool kDelta, bool kAny = false>
+__device__ __forceinline__ void enc_full_pack_w(uint32_t sin, uint32_t prev_w, const uint32_t (&lens)[kWTRows],
+                                                const uint32_t (&qw)[4], uint32_t sdst, uint32_t total) {
+    uint32_t last = prev_w, carry = 0;
+#pragma unroll
+    for (int j = 0; j < kWTRows; ++j) {
+        const uint4 x = enc_row<kDelta, kAny>(sin, j, last);
+        const uint32_t o = sdst + ((qw[j >> 1] >> (16 * (j & 1))) & 0xFFFFu);
+        __syncwarp();  // every lane has read row j before any lane writes over it
+        pack_group_words(x, lens[j], o, carry);
+    }
+    if (((sdst + total) & 3u) && (threadIdx.x & 31) == 0) sts32((sdst + total) & ~3u, carry);
+}
+
 // packed bytes [src, src + len) of shared memory (16-B aligned, with >= 16 readable bytes
 // before and after) -> global dst (any alignment): destination granule k is the 16 source
 // bytes at src + 16k - p, read as 5 words and funnel-shifted (p = dst's 16-B phase)
