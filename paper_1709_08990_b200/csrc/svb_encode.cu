@@ -722,7 +722,7 @@ __global__ void __launch_bounds__(kCTThreads + 32, 2)
                     uint32_t lens[kWTRows], qw[4];
                     total = enc_full_lengths<kDelta>(sin, prev_w, sh_addr(sctrl), lens, qw);
                     __syncwarp();
-                    enc_full_pack<kDelta>(sin, prev_w, lens, qw, sin);
+                    enc_full_pack_w<kDelta>(sin, prev_w, lens, qw, sin, total);
                     for (uint32_t i = lane; i < cnt_g; i += 32) cdst[i] = sctrl[i];
                 }
             } else {
