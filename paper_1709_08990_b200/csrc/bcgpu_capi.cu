@@ -216,6 +216,8 @@ int bcgpu_debug_set_trace(bcgpu_ctx* c, void* d_trace) {
 //   1024    decode: sums pass + pooled delta decode instead of the one-pass kernel
 //   0x8000  decode: the control scan only (dev timing; output not written)
 //   bits 12-14 batch kernels: cap CTAs per SM
+//   bits 16-23 segment-resident batch decode: ring KiB per warp (default 8)
+//   bits 24-31 segment-resident batch encode: ring KiB per warp (default 9)
 int bcgpu_debug_set_flags(bcgpu_ctx* c, uint32_t flags) {
     if (!c) return BCGPU_ERR_INVALID_ARGUMENT;
     c->debug_flags = flags;

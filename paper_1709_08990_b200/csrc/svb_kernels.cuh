@@ -115,9 +115,6 @@ cudaError_t launch_decode_batch3(const bcgpu_decode_segment* segs, uint64_t nseg
 cudaError_t launch_encode_batch3(const bcgpu_encode_segment* segs, uint64_t nseg, const uint32_t* in, uint8_t* out,
                                  uint64_t* out_lens, int delta, const BatchArgs& ba, cudaStream_t stream);
 
-cudaError_t launch_encode_batch2(const bcgpu_encode_segment* segs, uint64_t nseg, const uint32_t* in, uint8_t* out,
-                                 uint64_t* out_lens, int delta, const BatchArgs& ba, cudaStream_t stream);
-
 // CTAs per SM of the batch kernels, for grid sizing.
 int occupancy_batch();
 
