@@ -397,7 +397,7 @@ namespace {
 constexpr uint32_t kEHead = 16;            // ring bytes reserved below an item's integers
 constexpr uint32_t kERingDefault = 9216;   // ring bytes per warp (sweep: 8-9 KiB best, 5 CTAs per SM)
 constexpr uint32_t kECtrlBuf = 512;        // >= 16 + ceil(kBatchSmallN / 4)
-constexpr uint32_t kEPieceN = 1024;        // piece of a long segment (multiple of 128)
+constexpr uint32_t kEPieceN = kBatchSmallN;  // piece of a long segment: five full 384-integer blocks (cfg5: 1024 -> 1152 -> 1536 -> 1920 ints = 2.97 -> 2.25 -> 2.03 -> 1.91 ms)
 static_assert(16 + (kBatchSmallN + 3) / 4 <= kECtrlBuf, "control buffer");
 
 struct EItem3 {               // one piece of a segment
