@@ -349,6 +349,11 @@ __device__ __forceinline__ uint4 enc_row(uint32_t sin, int j, uint32_t& last) {
     return x;
 }
 
+__device__ __forceinline__ uint32_t lens_of_ctrl(uint32_t c) {  // l_i = field_i + 1, one per byte
+    const uint32_t t = c | (c << 6);  // OR, not a multiply: the shifted copies overlap
+    return ((t | (t << 12)) & 0x03030303u) + 0x01010101u;
+}
+
 // Pass 1: byte lengths, control bytes (-> shared sctrl), tile-local offsets; returns the data size.
 template <bool kDelta, bool kAny = false>
 __device__ __forceinline__ uint32_t enc_full_lengths(uint32_t sin, uint32_t prev_w, uint32_t sctrl,
@@ -359,10 +364,10 @@ __device__ __forceinline__ uint32_t enc_full_lengths(uint32_t sin, uint32_t prev
 #pragma unroll
     for (int j = 0; j < kWTRows; ++j) {
         const uint4 x = enc_row<kDelta, kAny>(sin, j, last);
-        const uint32_t l0 = blen(x.x), l1 = blen(x.y), l2 = blen(x.z), l3 = blen(x.w);
-        lens[j] = l0 | (l1 << 8) | (l2 << 16) | (l3 << 24);
-        P[j / 3] |= (l0 + l1 + l2 + l3) << (10 * (j % 3));
-        sts8(sctrl + 32 * j + lane, (l0 - 1) | ((l1 - 1) << 2) | ((l2 - 1) << 4) | ((l3 - 1) << 6));
+        const uint32_t c = blen_m1(x.x) | (blen_m1(x.y) << 2) | (blen_m1(x.z) << 4) | (blen_m1(x.w) << 6);
+        lens[j] = lens_of_ctrl(c);
+        P[j / 3] |= __dp4a(lens[j], 0x01010101u, 0u) << (10 * (j % 3));
+        sts8(sctrl + 32 * j + lane, c);
     }
     bool ones = true;
 #pragma unroll
@@ -569,10 +574,6 @@ __device__ __forceinline__ void store_realigned(uint32_t src, uint32_t len, uint
 // are live at once and the fully unrolled bodies overflow the instruction cache).
 // Row j's packed lengths are rebuilt from its control byte, row offsets are picked
 // from qw with selects: no per-row arrays, so nothing spills to local memory.
-__device__ __forceinline__ uint32_t lens_of_ctrl(uint32_t c) {  // l_i = field_i + 1, one per byte
-    const uint32_t t = c | (c << 6);  // OR, not a multiply: the shifted copies overlap
-    return ((t | (t << 12)) & 0x03030303u) + 0x01010101u;
-}
 __device__ __forceinline__ uint32_t row_q_sel(const uint32_t (&qw)[4], int j) {
     const uint32_t w = (j >> 1) == 0 ? qw[0] : (j >> 1) == 1 ? qw[1] : (j >> 1) == 2 ? qw[2] : qw[3];
     return (w >> (16 * (j & 1))) & 0xFFFFu;
