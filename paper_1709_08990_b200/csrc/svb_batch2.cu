@@ -242,7 +242,11 @@ __global__ void __launch_bounds__(kBThreads)
                         expand_full<0, false>(wA, sd, ot, 0);
                 }
             } else {
-                // partial tile and/or unaligned output: lean masked expansion, realigned stores
+                // partial tile and/or unaligned output: lean masked expansion, realigned stores.
+                // An all-zero full tile's ctrl_full skipped the row offsets: group g is data byte 4 g.
+                if (zeroA)
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) wA.qw[q] = (256u * q + 4u * lane) | ((256u * q + 128u + 4u * lane) << 16);
                 const uint32_t ng = (uint32_t)(ngroups - g0 < (uint64_t)kWTGroups ? ngroups - g0 : (uint64_t)kWTGroups);
                 const uint32_t tail = (g0 + ng == ngroups && (A.n & 3u)) ? (A.n & 3u) : 4u;
                 after = expand_any<kDelta>(wA, sh_addr(B.data[ds]) + head, ng, tail, o + 4 * g0, carry);

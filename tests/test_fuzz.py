@@ -1,4 +1,5 @@
-"""Randomised parity: hypothesis draws sizes, value shapes, delta/prev and buffer offsets, and
+"""Randomised parity: hypothesis draws sizes, value shapes, delta/prev and buffer offsets (and, for
+batches, segment lengths, layouts and ring sizes), and
 every encode / decode path the library dispatches between (one-pass, slot, two-read, sums +
 pooled decode) must reproduce the pinned oracle byte for byte."""
 import ctypes as C
@@ -153,3 +154,60 @@ def test_fuzz_malformed(env, n, kind, codec, delta, seed, edit, where):
     assert gst == ost, (codec, edit, gst, ost)
     if ost == oracle.OK:
         assert np.array_equal(out[:n2], ovals[:n2])
+
+
+@settings(max_examples=int(os.environ.get("FUZZ_EXAMPLES", "200")) // 2, deadline=None,
+          suppress_health_check=list(HealthCheck))
+@given(nseg=st.integers(1, 3000), long_frac=st.sampled_from([0.0, 0.01, 0.2, 1.0]),
+       kind=st.sampled_from(["classes", "sorted_small", "sorted_wide", "constant", "bytes"]),
+       delta=st.booleans(), seed=st.integers(0, 2**31), gap_in=st.booleans(), gap_out=st.booleans(),
+       ring=st.sampled_from([0, 8, 11, 16]), occ=st.sampled_from([0, 1, 3]), hint=st.booleans())
+def test_fuzz_batches(env, nseg, long_frac, kind, delta, seed, gap_in, gap_out, ring, occ, hint):
+    """Segmented batches (segment-resident and tile-pipeline kernels) against the oracle: random
+    segment lengths (short, the 1920 boundary, long), value shapes, stream / output gaps, ring
+    sizes and CTA caps (many segments per warp, ring wrap-around)."""
+    torch, lib, dev = env
+    from paper_1709_08990_b200.device import DECODE_SEG_DTYPE, ENCODE_SEG_DTYPE, segments_to_tensor
+    rng = np.random.default_rng(seed)
+    if long_frac >= 1.0:
+        nseg = min(nseg, 40)
+    short = (rng.choice(np.array([0, 1, 2, 3, 4, 5, 127, 128, 129, 383, 384, 385, 1919, 1920]), nseg)
+             if seed & 1 else rng.integers(0, 1921, nseg))
+    sizes = np.where(rng.random(nseg) < long_frac, rng.integers(1921, 20_000, nseg), short).astype(np.int64)
+    vals = [_values(kind, int(n), seed + i) for i, n in enumerate(sizes)]
+    prevs = rng.integers(0, 2**32, nseg, dtype=np.uint64).astype(np.uint32) if delta else np.zeros(nseg, np.uint32)
+    encs = [oracle.encode(v, delta=delta, prev=int(p)) for v, p in zip(vals, prevs)]
+    gi = rng.integers(0, 5, nseg) if gap_in else np.zeros(nseg, np.int64)
+    go = rng.integers(0, 17, nseg) if gap_out else np.zeros(nseg, np.int64)
+    src = np.cumsum(gi + np.concatenate([[0], sizes[:-1]]))
+    caps = (sizes + 3) // 4 + 4 * sizes
+    dst = np.cumsum(go + np.concatenate([[0], caps[:-1]]))
+    flat = np.zeros(int(src[-1] + sizes[-1]) + 4, np.uint32)
+    for s_, v in zip(src, vals):
+        flat[int(s_):int(s_) + v.size] = v
+    es = np.zeros(nseg, ENCODE_SEG_DTYPE)
+    es["src_offset"], es["dst_capacity"], es["dst_offset"], es["n"], es["prev"] = src, caps, dst, sizes, prevs
+    d_out = torch.full((int(dst[-1] + caps[-1]) + 32,), 0x3C, dtype=torch.uint8, device="cuda")
+    d_lens = torch.zeros(nseg, dtype=torch.int64, device="cuda")
+    mx = int(sizes.max()) if hint else 0
+    lib.bcgpu_debug_set_flags(dev._ctx, (ring << 24) | (ring << 16) | (occ << 12))
+    try:
+        dev.encode_batch(segments_to_tensor(es, "cuda"), nseg, torch.from_numpy(flat.view(np.int32)).cuda(), d_out,
+                         d_lens, delta=delta, max_seg_n=mx)
+        dev.check()
+        got = d_out.cpu().numpy()
+        assert np.array_equal(d_lens.cpu().numpy(), [len(e) for e in encs])
+        for i, (e, d) in enumerate(zip(encs, dst)):
+            assert got[int(d):int(d) + len(e)].tobytes() == e, f"encode segment {i} n={sizes[i]}"
+        # decode the encoded streams where they lie (gaps between them), outputs at src offsets
+        ds = np.zeros(nseg, DECODE_SEG_DTYPE)
+        ds["src_offset"], ds["src_bytes"], ds["dst_offset"] = dst, [len(e) for e in encs], src
+        ds["n"], ds["prev"] = sizes, prevs
+        d_dec = torch.full((flat.size,), -5, dtype=torch.int32, device="cuda")
+        dev.decode_batch(segments_to_tensor(ds, "cuda"), nseg, d_out, d_dec, delta=delta, max_seg_n=mx)
+        dev.check()
+        dec = d_dec.cpu().numpy().view(np.uint32)
+        for i, (v, s_) in enumerate(zip(vals, src)):
+            assert np.array_equal(dec[int(s_):int(s_) + v.size], v), f"decode segment {i} n={sizes[i]}"
+    finally:
+        lib.bcgpu_debug_set_flags(dev._ctx, 0)
