@@ -135,6 +135,47 @@ __device__ __forceinline__ void store_pass(const uint4 (&v)[4], uint32_t* __rest
     }
 }
 
+// A segment of at most 128 integers (32 groups): one pass with one group per lane, so a short
+// list costs one group's work per lane instead of four (the per-segment floor of the
+// 4-group pass was ~670 warp instructions, ncu at 16 integers per list).
+template <bool kDelta>
+__device__ __forceinline__ uint32_t decode_resident_short(uint32_t S, uint32_t bytes, uint32_t n, uint32_t run,
+                                                          uint32_t* __restrict__ o) {
+    const int lane = threadIdx.x & 31;
+    const uint32_t ng = (n + 3) >> 2;  // <= 32
+    const uint32_t g = (uint32_t)lane;
+    const uint32_t tail = (n & 3u) ? (n & 3u) : 4u;
+    const bool valid = g < ng, lastg = g + 1 == ng;
+    uint32_t c = valid ? lds8(S + g) : 0u;
+    if (lastg && (n & 3u)) c &= (1u << (2 * (n & 3u))) - 1u;  // unused fields of the final control byte
+    const uint32_t len = valid ? fsum(c) + (lastg ? tail : 4u) : 0u;
+    const uint32_t I = warp_inclusive_scan(len);
+    const uint32_t D = S + ng, Dend = S + bytes;
+    const uint32_t a = min(D + I - len, Dend);
+    uint4 v = __all_sync(kFull, c == 0) ? zero_group_s(a) : group_w5(a, c);
+    v = mask_tail(v, valid ? (lastg ? tail : 4u) : 0u);
+    if constexpr (kDelta) {
+        v.y += v.x;
+        v.z += v.y;
+        v.w += v.z;
+        const uint32_t Iv = warp_inclusive_scan(v.w);
+        v = add4(v, run + Iv - v.w);
+    }
+    const int e0 = 4 * lane, cnt = (int)n - e0;
+    if (cnt > 0) {
+        uint32_t* q = o + e0;
+        if (cnt >= 4 && ((uintptr_t)q & 15) == 0) {
+            stg_stream_v4(q, v);
+        } else {
+            q[0] = v.x;
+            if (cnt > 1) q[1] = v.y;
+            if (cnt > 2) q[2] = v.z;
+            if (cnt > 3) q[3] = v.w;
+        }
+    }
+    return __shfl_sync(kFull, I, 31);
+}
+
 template <bool kDelta>
 __device__ __forceinline__ uint32_t decode_resident(uint32_t S, uint32_t bytes, uint32_t n, uint32_t run,
                                                     uint32_t* __restrict__ o) {
@@ -318,7 +359,9 @@ __global__ void __launch_bounds__(kRThreads)
         mbar_wait_parity(&B.bar[slot], (qt / kRSlots) & 1u);
         const RItem it = B.item[slot];
         uint32_t* o = out + it.dst;
-        const uint32_t data = decode_resident<kDelta>(ring + it.spos, it.bytes, it.n, kDelta ? it.prev : 0u, o);
+        const uint32_t data = it.n <= 128
+                                  ? decode_resident_short<kDelta>(ring + it.spos, it.bytes, it.n, kDelta ? it.prev : 0u, o)
+                                  : decode_resident<kDelta>(ring + it.spos, it.bytes, it.n, kDelta ? it.prev : 0u, o);
         if (lane == 0) {
             const uint64_t need = (uint64_t)((it.n + 3) >> 2) + data;
             if (need != it.bytes) report3(status, epoch, need > it.bytes ? BCGPU_ERR_TRUNCATED : BCGPU_ERR_TRAILING_BYTES);
