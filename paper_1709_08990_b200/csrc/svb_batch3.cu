@@ -489,6 +489,11 @@ __device__ __forceinline__ void encode_block(uint32_t Sin, uint32_t blk, uint32_
     uint32_t any = 0;
 #pragma unroll
     for (int j = 0; j < 3; ++j) {
+        if (!kFB && blk + j >= rows) {  // past the piece's last row (warp-uniform)
+            d[j] = make_uint4(0, 0, 0, 0);
+            cnts[j] = 0;
+            continue;
+        }
         const uint32_t g = 32 * (blk + j) + lane;
         const uint32_t cnt = kFB ? 4u : (g + 1 < ng ? 4u : (g + 1 == ng ? tail : 0u));
         const uint32_t a = (kFB || cnt) ? Sin + 16 * g : Sin;
@@ -535,6 +540,10 @@ __device__ __forceinline__ void encode_block(uint32_t Sin, uint32_t blk, uint32_
     uint32_t L4[3], P = 0;
 #pragma unroll
     for (int j = 0; j < 3; ++j) {
+        if (!kFB && blk + j >= rows) {
+            L4[j] = 0;
+            continue;
+        }
         const uint4 x = d[j];
         const uint32_t g = 32 * (blk + j) + lane, cnt = cnts[j];
         const uint32_t m0 = blen_m1(x.x), m1 = blen_m1(x.y), m2 = blen_m1(x.z), m3 = blen_m1(x.w);
