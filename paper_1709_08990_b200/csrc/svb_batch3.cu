@@ -472,8 +472,8 @@ __device__ __forceinline__ void put_bytes(uint8_t* g, const uint8_t* sp, uint32_
         const uint32_t nh = (uint32_t)(a_lo - gb), nt = (uint32_t)(ge - a_hi);
         if ((uint32_t)lane < nh) g[lane] = sp[lane];
         if ((uint32_t)lane < nt) g[(a_hi - gb) + lane] = sp[(a_hi - gb) + lane];
-    } else {
-        for (uint32_t i = lane; i < len; i += 32) g[i] = sp[i];
+    } else if ((uint32_t)lane < len) {  // no aligned interior: < 32 bytes
+        g[lane] = sp[lane];
     }
 }
 
@@ -669,7 +669,7 @@ __global__ void __launch_bounds__(kRThreads)
             uintptr_t a0 = 0;
             if (n == 0) {
                 if (lane == 0) out_lens[s_idx] = 0;
-            } else if (piece == 0 && cap < ((uint64_t)n + 3) / 4 + 4ull * n) {
+            } else if (piece == 0 && cap < (((uint64_t)n + 3) >> 2) + 4ull * n) {
                 if (lane == 0) report3(status, epoch, BCGPU_ERR_INVALID_ARGUMENT);
             } else {
                 m = piece + 1 < npieces ? pn : n - piece * pn;
