@@ -260,20 +260,35 @@ class Batch:
         self.h_v = torch.from_numpy(self.values.view(np.int32)).pin_memory()
         self.h_c = torch.empty(self.d_c.numel(), dtype=torch.uint8).pin_memory()
         self.h_o = torch.empty(self.n, dtype=torch.int32).pin_memory()
+        self.h_tot = torch.zeros(1, dtype=torch.int64).pin_memory()
+        # descriptors as (nseg, 4) u64 rows, so the packed layout can be filled in on the device
+        self.e_rows = self.d_esegs.view(torch.int64).view(self.nseg, 4).clone()
+        self.d_rows = self.d_dsegs.view(torch.int64).view(self.nseg, 4).clone()
+        self.d_sz = torch.zeros(self.nseg, dtype=torch.int64, device="cuda")
         self._torch = torch
 
     def e2e_step(self):
-        # batch API: H2D values, encode_batch, D2H streams; H2D streams, decode_batch, D2H values
+        # what a user of the batch API does with host data: H2D the integers; size pass; pack the
+        # streams back to back (exclusive scan of the sizes -> dst offsets); encode; D2H exactly
+        # the compressed bytes; then H2D those bytes, decode, D2H the integers
         torch = self._torch
         self.d_v.copy_(self.h_v, non_blocking=True)
-        self.encode()
-        self.h_c.copy_(self.d_c, non_blocking=True)
-        self.d_c.copy_(self.h_c, non_blocking=True)
-        self.decode()
+        self.dev.encoded_sizes_batch(self.d_esegs, self.nseg, self.d_v, self.d_sz, delta=True)
+        off = torch.cumsum(self.d_sz, 0) - self.d_sz
+        self.e_rows[:, 2] = off
+        self.h_tot.copy_(self.d_sz.sum().view(1), non_blocking=True)
+        self.dev.encode_batch(self.e_rows.view(torch.uint8), self.nseg, self.d_v, self.d_c, self.d_lens, delta=True,
+                              max_seg_n=self.max_n)
+        torch.cuda.synchronize()
+        cmp = int(self.h_tot[0])
+        self.h_c[:cmp].copy_(self.d_c[:cmp], non_blocking=True)
+        self.d_c[:cmp].copy_(self.h_c[:cmp], non_blocking=True)
+        self.d_rows[:, 0], self.d_rows[:, 1] = off, self.d_sz
+        self.dev.decode_batch(self.d_rows.view(torch.uint8), self.nseg, self.d_c, self.d_o, delta=True,
+                              max_seg_n=self.max_n)
         self.h_o.copy_(self.d_o, non_blocking=True)
         torch.cuda.synchronize()
-        slots = self.d_c.numel()
-        return 4 * self.n + slots, slots + 4 * self.n
+        return 4 * self.n + cmp, cmp + 4 * self.n
 
     def e2e_verify(self):
         assert np.array_equal(self.h_o.numpy().view(np.uint32), self.values)
@@ -471,7 +486,8 @@ def run_gpu(args):
         e2e = {"value": round(n_all / float(e2e_local.item()) / 1e9, 4), "unit": "Gint/s",
                "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
                "path": "bcgpu_svb_encode_host + bcgpu_svb_decode_host (pinned host buffers)"
-               if isinstance(wl, SingleArray) else "H2D + encode_batch + D2H, H2D + decode_batch + D2H"}
+               if isinstance(wl, SingleArray) else "H2D; encoded_sizes_batch + device scan + encode_batch (streams packed back "
+                                                "to back); D2H of the compressed bytes; H2D; decode_batch; D2H"}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu and isinstance(wl, SingleArray):
