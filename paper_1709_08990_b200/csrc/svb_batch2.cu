@@ -275,6 +275,7 @@ cudaError_t launch_decode_batch2(const bcgpu_decode_segment* segs, uint64_t nseg
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o1, svb_decode_batch2_kernel<true>, kBThreads, 0);
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o2, svb_decode_batch2_kernel<false>, kBThreads, 0);
         occ = o1 < o2 ? o1 : o2;
+        if (occ > 4) occ = 4;  // cfg5 sweep: 4 CTAs per SM 2.02 ms, 5 (the occupancy limit) 2.06 ms
         if (occ < 1) occ = 1;
     }
     const uint32_t occ_cap = (ba.flags >> 12) & 7u;  // debug: CTAs per SM
