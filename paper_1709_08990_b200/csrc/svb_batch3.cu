@@ -274,7 +274,7 @@ __global__ void __launch_bounds__(kRThreads)
     __syncwarp();
     const uint64_t gw = (uint64_t)blockIdx.x * kRWarps + warp, GW = (uint64_t)gridDim.x * kRWarps;
     const uint64_t cnt = nseg > gw ? (nseg - gw + GW - 1) / GW : 0;  // segments gw, gw + GW, ...
-    const uint32_t ring = sh_addr(ring_p);
+    const uint32_t ring = sh_addr(ring_p), bar0 = sh_addr(&B.bar[0]);
     const uint64_t pol = l2_policy_drop();
     const unsigned long long* sw = reinterpret_cast<const unsigned long long*>(segs);
 
@@ -339,8 +339,8 @@ __global__ void __launch_bounds__(kRThreads)
                     it.spos = at + (uint32_t)(((uintptr_t)in + src) & 15);
                     it.end = head + waste + cover;
                     fence_async_smem();  // the ring bytes were last read through the generic proxy
-                    mbar_expect(&B.bar[slot], cover);
-                    tma_load_hint(ring_p + at, reinterpret_cast<const void*>(a0), cover, &B.bar[slot], pol);
+                    mbar_expect_s(bar0 + 8 * slot, cover);
+                    tma_load_hint_s(ring + at, reinterpret_cast<const void*>(a0), cover, bar0 + 8 * slot, pol);
                 }
                 head += waste + cover;
                 hpos = at + cover;
@@ -463,17 +463,17 @@ __device__ __forceinline__ uint32_t shr_c(uint32_t x, uint32_t s) { return __fun
 
 // global [g, g + len) <- shared bytes at sp (sp has g's 16-B phase): bulk store of the aligned
 // interior (committed by the caller), lanes store the edge bytes
-__device__ __forceinline__ void put_bytes(uint8_t* g, const uint8_t* sp, uint32_t len) {
+__device__ __forceinline__ void put_bytes(uint8_t* g, uint32_t sp, uint32_t len) {
     const int lane = threadIdx.x & 31;
     const uintptr_t gb = (uintptr_t)g, ge = gb + len;
     const uintptr_t a_lo = (gb + 15) & ~(uintptr_t)15, a_hi = ge & ~(uintptr_t)15;
     if (a_hi > a_lo) {
-        if (lane == 0) tma_store(reinterpret_cast<void*>(a_lo), sp + (a_lo - gb), (uint32_t)(a_hi - a_lo));
+        if (lane == 0) tma_store_s(reinterpret_cast<void*>(a_lo), sp + (uint32_t)(a_lo - gb), (uint32_t)(a_hi - a_lo));
         const uint32_t nh = (uint32_t)(a_lo - gb), nt = (uint32_t)(ge - a_hi);
-        if ((uint32_t)lane < nh) g[lane] = sp[lane];
-        if ((uint32_t)lane < nt) g[(a_hi - gb) + lane] = sp[(a_hi - gb) + lane];
+        if ((uint32_t)lane < nh) g[lane] = (uint8_t)lds8(sp + lane);
+        if ((uint32_t)lane < nt) g[(a_hi - gb) + lane] = (uint8_t)lds8(sp + (uint32_t)(a_hi - gb) + lane);
     } else if ((uint32_t)lane < len) {  // no aligned interior: < 32 bytes
-        g[lane] = sp[lane];
+        g[lane] = (uint8_t)lds8(sp + lane);
     }
 }
 
@@ -633,7 +633,7 @@ __global__ void __launch_bounds__(kRThreads)
     __syncwarp();
     const uint64_t gw = (uint64_t)blockIdx.x * kRWarps + warp, GW = (uint64_t)gridDim.x * kRWarps;
     const uint64_t cnt = nseg > gw ? (nseg - gw + GW - 1) / GW : 0;
-    const uint32_t ring = sh_addr(ring_p);
+    const uint32_t ring = sh_addr(ring_p), bar0 = sh_addr(&B.bar[0]), ctrl0 = sh_addr(&B.ctrl[0][0]);
     const uint64_t pol = l2_policy_drop();
     const unsigned long long* sw = reinterpret_cast<const unsigned long long*>(segs);
     uint64_t dbase = 0;
@@ -663,7 +663,7 @@ __global__ void __launch_bounds__(kRThreads)
             const uint32_t n = (uint32_t)np;
             const uint64_t s_idx = gw + (dbase + di) * GW;
             const uint32_t pn = n <= kBatchSmallN ? n : kEPieceN;  // integers per piece
-            const uint32_t npieces = n <= kBatchSmallN ? (n ? 1u : 0u) : (uint32_t)(((uint64_t)n + kEPieceN - 1) / kEPieceN);
+            const uint32_t npieces = n ? (n - 1) / kEPieceN + 1 : 0u;
             bool take = false, done = true;
             uint32_t at = 0, cover = 0, waste = 0, m = 0;
             uintptr_t a0 = 0;
@@ -703,9 +703,9 @@ __global__ void __launch_bounds__(kRThreads)
                     it.spos = at + kEHead + (uint32_t)((uintptr_t)(in + src + (uint64_t)piece * pn) & 15);
                     it.end = head + waste + cover;
                     fence_async_smem();
-                    mbar_expect(&B.bar[slot], cover - kEHead);
-                    tma_load_hint(ring_p + at + kEHead, reinterpret_cast<const void*>(a0), cover - kEHead, &B.bar[slot],
-                                  pol);
+                    mbar_expect_s(bar0 + 8 * slot, cover - kEHead);
+                    tma_load_hint_s(ring + at + kEHead, reinterpret_cast<const void*>(a0), cover - kEHead, bar0 + 8 * slot,
+                                    pol);
                 }
                 head += waste + cover;
                 hpos = at + cover;
@@ -738,14 +738,14 @@ __global__ void __launch_bounds__(kRThreads)
         const uint32_t hc = (uint32_t)((uintptr_t)gctrl & 15), hd = (uint32_t)((uintptr_t)gdata & 15);
         const uint32_t Sin = ring + it.spos;
         const uint32_t db = ((Sin - 16u) & ~15u) + hd;  // the item's reserved head: 1..31 bytes below Sin
-        uint8_t* cbuf = B.ctrl[qt & 1];
-        const uint32_t data = encode_resident<kDelta>(Sin, it.m, run, sh_addr(cbuf) + hc, db);
+        const uint32_t cbuf = ctrl0 + kECtrlBuf * (qt & 1);
+        const uint32_t data = encode_resident<kDelta>(Sin, it.m, run, cbuf + hc, db);
         if constexpr (kDelta) run = lds32(Sin + 4 * (it.m - 1));  // x_{-1} of the next piece
         off += data;
         fence_async_smem();
         __syncwarp();
         put_bytes(gctrl, cbuf + hc, ng);
-        put_bytes(gdata, ring_p + (db - ring), data);
+        put_bytes(gdata, db, data);
         if (lane == 0) {
             tma_store_commit();
             if ((uint64_t)(it.piece + 1) * pn >= it.n) out_lens[it.seg] = (uint64_t)ngT + off;
