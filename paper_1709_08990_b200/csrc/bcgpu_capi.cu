@@ -61,7 +61,6 @@ struct bcgpu_ctx {
     unsigned long long* trace = nullptr;  // debug phase trace (bcgpu_debug_set_trace)
     uint32_t debug_flags = 0;
     // batch kernels: CTAs for full residency
-    int batch_grid = 0;
     // host-API scratch (device) and stream
     cudaStream_t stream = nullptr;
     cudaStream_t aux = nullptr;        // encode: second stream for the sliced pipeline
@@ -145,7 +144,6 @@ static int make_batch(bcgpu_ctx* c, cudaStream_t s, BatchArgs* ba) {
     if (st) return st;
     ba->status = status_ptr(c);
     ba->epoch = c->epoch;
-    ba->grid = c->batch_grid;
     ba->flags = c->debug_flags;
     return BCGPU_OK;
 }
@@ -284,7 +282,6 @@ int bcgpu_ctx_create(int device, bcgpu_ctx** out) {
     if (!c) return BCGPU_ERR_INVALID_ARGUMENT;
     c->device = device;
     cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, device);
-    c->batch_grid = c->num_sms * occupancy_batch();
     c->pipe_grid = c->num_sms * occupancy_decode_pipe();
     cudaError_t e = cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking);
     if (e != cudaSuccess) {

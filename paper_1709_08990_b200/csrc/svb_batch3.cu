@@ -613,12 +613,39 @@ __device__ __forceinline__ uint32_t encode_resident(uint32_t Sin, uint32_t m, ui
     return off;
 }
 
+// Size pass of one resident piece (bcgpu_svb_encoded_sizes_batch_device): the data bytes of its
+// m integers at shared Sin (run: x_{-1}, delta).
+template <bool kDelta>
+__device__ __forceinline__ uint32_t size_resident(uint32_t Sin, uint32_t m, uint32_t run) {
+    const int lane = threadIdx.x & 31;
+    const uint32_t ng = (m + 3) >> 2, rows = (ng + 31) >> 5, tail = (m & 3u) ? (m & 3u) : 4u;
+    const bool al16 = (Sin & 15u) == 0;
+    uint32_t acc = 0;
+#pragma unroll 4
+    for (uint32_t r = 0; r < rows; ++r) {
+        const uint32_t g = 32 * r + lane;
+        const uint32_t cnt = g + 1 < ng ? 4u : (g + 1 == ng ? tail : 0u);
+        const uint32_t a = cnt ? Sin + 16 * g : Sin;
+        uint4 x = al16 ? lds128(a) : make_uint4(lds32(a), lds32(a + 4), lds32(a + 8), lds32(a + 12));
+        if constexpr (kDelta) {
+            uint32_t pw = __shfl_up_sync(kFull, x.w, 1);
+            if (lane == 0) pw = run;
+            run = __shfl_sync(kFull, x.w, 31);
+            x = make_uint4(x.x - pw, x.y - x.x, x.z - x.y, x.w - x.z);
+        }
+        const uint32_t s4 = blen_m1(x.x) + (cnt > 1 ? blen_m1(x.y) : 0u) + (cnt > 2 ? blen_m1(x.z) : 0u) +
+                            (cnt > 3 ? blen_m1(x.w) : 0u);
+        acc += cnt ? s4 + cnt : 0u;
+    }
+    return __reduce_add_sync(kFull, acc);
+}
+
 }  // namespace
 
 // Items are pieces: a segment of n <= kBatchSmallN integers is one piece; a longer one is cut
 // into kEPieceN-integer pieces that the same warp encodes in order, carrying the data offset
 // and the delta base in registers (control bytes of piece k at k * kEPieceN / 4).
-template <bool kDelta>
+template <bool kDelta, bool kSizes>
 __global__ void __launch_bounds__(kRThreads)
     svb_encode_batch3_kernel(const bcgpu_encode_segment* __restrict__ segs, uint64_t nseg,
                              const uint32_t* __restrict__ in, uint8_t* __restrict__ out,
@@ -669,7 +696,7 @@ __global__ void __launch_bounds__(kRThreads)
             uintptr_t a0 = 0;
             if (n == 0) {
                 if (lane == 0) out_lens[s_idx] = 0;
-            } else if (piece == 0 && cap < (((uint64_t)n + 3) >> 2) + 4ull * n) {
+            } else if (!kSizes && piece == 0 && cap < (((uint64_t)n + 3) >> 2) + 4ull * n) {
                 if (lane == 0) report3(status, epoch, BCGPU_ERR_INVALID_ARGUMENT);
             } else {
                 m = piece + 1 < npieces ? pn : n - piece * pn;
@@ -733,6 +760,16 @@ __global__ void __launch_bounds__(kRThreads)
             run = kDelta ? it.prev : 0u;
             off = 0;
         }
+        if constexpr (kSizes) {  // size pass: no output, the ring frees at once
+            const uint32_t Sin = ring + it.spos;
+            off += size_resident<kDelta>(Sin, it.m, run);
+            if constexpr (kDelta) run = lds32(Sin + 4 * (it.m - 1));
+            if (lane == 0 && (uint64_t)(it.piece + 1) * pn >= it.n) out_lens[it.seg] = (uint64_t)ngT + off;
+            __syncwarp();
+            tail = tail_next = it.end;
+            ++qt;
+            continue;
+        }
         uint8_t* gctrl = out + it.dst + (uint64_t)it.piece * (pn >> 2);
         uint8_t* gdata = out + it.dst + ngT + off;
         const uint32_t hc = (uint32_t)((uintptr_t)gctrl & 15), hd = (uint32_t)((uintptr_t)gdata & 15);
@@ -760,15 +797,17 @@ __global__ void __launch_bounds__(kRThreads)
 }
 
 cudaError_t launch_encode_batch3(const bcgpu_encode_segment* segs, uint64_t nseg, const uint32_t* in, uint8_t* out,
-                                 uint64_t* out_lens, int delta, const BatchArgs& ba, cudaStream_t stream) {
+                                 uint64_t* out_lens, int delta, const BatchArgs& ba, cudaStream_t stream, bool sizes) {
     static int sms = 0;
     static size_t attr_smem = 0;
     const uint32_t ring_kb = (ba.flags >> 24) & 0xFFu;  // debug: ring KiB per warp
     const uint32_t ring = ring_kb ? (ring_kb << 10 < kItemMax ? kItemMax : ring_kb << 10) : kERingDefault;
     const size_t smem = kRWarps * (sizeof(EWarpHdr) + ring + kRingSlack);
     if (smem > attr_smem) {
-        cudaFuncSetAttribute(svb_encode_batch3_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        cudaFuncSetAttribute(svb_encode_batch3_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        cudaFuncSetAttribute(svb_encode_batch3_kernel<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        cudaFuncSetAttribute(svb_encode_batch3_kernel<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        cudaFuncSetAttribute(svb_encode_batch3_kernel<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        cudaFuncSetAttribute(svb_encode_batch3_kernel<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         attr_smem = smem;
     }
     if (!sms) {
@@ -777,8 +816,8 @@ cudaError_t launch_encode_batch3(const bcgpu_encode_segment* segs, uint64_t nseg
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     }
     int o1 = 0, o2 = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o1, svb_encode_batch3_kernel<true>, kRThreads, smem);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o2, svb_encode_batch3_kernel<false>, kRThreads, smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o1, svb_encode_batch3_kernel<true, false>, kRThreads, smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o2, svb_encode_batch3_kernel<false, false>, kRThreads, smem);
     int occ = o1 < o2 ? o1 : o2;
     if (occ < 1) occ = 1;
     const uint32_t occ_cap = (ba.flags >> 12) & 7u;  // debug: CTAs per SM
@@ -786,12 +825,20 @@ cudaError_t launch_encode_batch3(const bcgpu_encode_segment* segs, uint64_t nseg
     const uint64_t want = (nseg + kRWarps - 1) / kRWarps, capg = (uint64_t)sms * occ;
     const int grid = (int)(want < capg ? want : capg);
     if (grid <= 0) return cudaSuccess;
-    if (delta)
-        svb_encode_batch3_kernel<true><<<grid, kRThreads, smem, stream>>>(segs, nseg, in, out, out_lens, ba.status,
-                                                                          ba.epoch, ring);
-    else
-        svb_encode_batch3_kernel<false><<<grid, kRThreads, smem, stream>>>(segs, nseg, in, out, out_lens, ba.status,
-                                                                           ba.epoch, ring);
+    if (sizes) {
+        if (delta)
+            svb_encode_batch3_kernel<true, true><<<grid, kRThreads, smem, stream>>>(segs, nseg, in, out, out_lens,
+                                                                                   ba.status, ba.epoch, ring);
+        else
+            svb_encode_batch3_kernel<false, true><<<grid, kRThreads, smem, stream>>>(segs, nseg, in, out, out_lens,
+                                                                                    ba.status, ba.epoch, ring);
+    } else if (delta) {
+        svb_encode_batch3_kernel<true, false><<<grid, kRThreads, smem, stream>>>(segs, nseg, in, out, out_lens,
+                                                                                ba.status, ba.epoch, ring);
+    } else {
+        svb_encode_batch3_kernel<false, false><<<grid, kRThreads, smem, stream>>>(segs, nseg, in, out, out_lens,
+                                                                                 ba.status, ba.epoch, ring);
+    }
     return cudaGetLastError();
 }
 

@@ -113,48 +113,6 @@ __global__ void __launch_bounds__(kThreads) svb_decode_blocks_kernel(const uint8
     counts[i] = cnt;
 }
 
-struct SegDesc {
-    uint64_t a, b, c;
-    uint32_t n, prev;
-};
-
-__device__ __forceinline__ SegDesc load_desc_warp(const void* segs, uint64_t s) {
-    const int lane = threadIdx.x & 31;
-    const unsigned long long* p = reinterpret_cast<const unsigned long long*>(segs) + 4 * s;
-    const unsigned long long w = lane < 4 ? __ldg(p + lane) : 0ull;
-    SegDesc d;
-    d.a = __shfl_sync(kFull, w, 0);
-    d.b = __shfl_sync(kFull, w, 1);
-    d.c = __shfl_sync(kFull, w, 2);
-    const unsigned long long np = __shfl_sync(kFull, w, 3);
-    d.n = (uint32_t)np;
-    d.prev = (uint32_t)(np >> 32);
-    return d;
-}
-
-// -------- size-only pass, warp per segment
-template <bool kDelta>
-__global__ void __launch_bounds__(kThreads) svb_sizes_batch_kernel(const bcgpu_encode_segment* __restrict__ segs,
-                                                                   uint64_t nseg, const uint32_t* __restrict__ in,
-                                                                   uint64_t* __restrict__ out_lens) {
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const uint64_t gw = (uint64_t)blockIdx.x * kWarps + warp, nw = (uint64_t)gridDim.x * kWarps;
-    for (uint64_t s = gw; s < nseg; s += nw) {
-        const SegDesc e = load_desc_warp(segs, s);
-        const uint32_t* src = in + e.a;
-        uint64_t acc = 0;
-        for (uint64_t i = lane; i < e.n; i += 32) {
-            const uint32_t x = __ldg(src + i);
-            uint32_t v = x;
-            if constexpr (kDelta) v = x - (i ? __ldg(src + i - 1) : e.prev);
-            acc += dev_byte_length(v);
-        }
-#pragma unroll
-        for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(kFull, acc, o);
-        if (lane == 0) out_lens[s] = (((uint64_t)e.n + 3) >> 2) + acc;
-    }
-}
-
 // ===========================================================================
 // launchers
 // ===========================================================================
@@ -172,13 +130,7 @@ cudaError_t launch_decode_blocks(const uint8_t* in, uint64_t in_len, uint64_t n,
     return cudaGetLastError();
 }
 
-static int occ_of(const void* k, int threads) {
-    int occ = 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, threads, 0) != cudaSuccess || occ < 1) occ = 1;
-    return occ;
-}
 
-int occupancy_batch() { return occ_of((const void*)svb_sizes_batch_kernel<true>, kThreads) * kWarps / kWTWarps; }
 
 // decode / encode batches: the warp-pipelined kernels of svb_batch2.cu
 cudaError_t launch_decode_batch(const bcgpu_decode_segment* segs, uint64_t nseg, const uint8_t* in, uint32_t* out,
@@ -197,15 +149,8 @@ cudaError_t launch_encode_batch(const bcgpu_encode_segment* segs, uint64_t nseg,
 
 cudaError_t launch_sizes_batch(const bcgpu_encode_segment* segs, uint64_t nseg, const uint32_t* in,
                                uint64_t* out_lens, int delta, const BatchArgs& ba, cudaStream_t stream) {
-    const uint64_t want = (nseg + kWarps - 1) / kWarps;
-    const uint64_t cap = (uint64_t)ba.grid * kWTWarps / kWarps + 1;
-    const int grid = (int)(want < cap ? want : cap);
-    if (grid <= 0) return cudaSuccess;
-    if (delta)
-        svb_sizes_batch_kernel<true><<<grid, kThreads, 0, stream>>>(segs, nseg, in, out_lens);
-    else
-        svb_sizes_batch_kernel<false><<<grid, kThreads, 0, stream>>>(segs, nseg, in, out_lens);
-    return cudaGetLastError();
+    // the segment-resident encode kernel's size-only variant (svb_batch3.cu)
+    return launch_encode_batch3(segs, nseg, in, nullptr, out_lens, delta, ba, stream, true);
 }
 
 }  // namespace bcgpu

@@ -88,7 +88,6 @@ cudaError_t launch_decode_blocks(const uint8_t* in, uint64_t in_len, uint64_t n,
 struct BatchArgs {
     unsigned long long* status;  // [epoch:32 | bcgpu_status:32]
     uint32_t epoch;
-    int grid;                    // CTAs of the warp-per-segment kernels (full residency)
     uint32_t flags = 0;          // debug flags of the ctx (bits 12..14: batch-decode CTAs per SM)
     uint32_t max_seg_n = 0;      // caller's bound on every segment's n (0 = unknown)
 };
@@ -112,11 +111,11 @@ cudaError_t launch_decode_batch2(const bcgpu_decode_segment* segs, uint64_t nseg
 cudaError_t launch_decode_batch3(const bcgpu_decode_segment* segs, uint64_t nseg, const uint8_t* in, uint32_t* out,
                                  int delta, const BatchArgs& ba, cudaStream_t stream);
 
+// sizes: the size-only pass (no output; out may be null)
 cudaError_t launch_encode_batch3(const bcgpu_encode_segment* segs, uint64_t nseg, const uint32_t* in, uint8_t* out,
-                                 uint64_t* out_lens, int delta, const BatchArgs& ba, cudaStream_t stream);
+                                 uint64_t* out_lens, int delta, const BatchArgs& ba, cudaStream_t stream,
+                                 bool sizes = false);
 
-// CTAs per SM of the batch kernels, for grid sizing.
-int occupancy_batch();
 
 // Control bytes per look-back tile of the block-offsets kernel.
 constexpr uint32_t kOffsetsTileGroups = 2048;
