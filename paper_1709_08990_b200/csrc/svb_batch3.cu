@@ -95,21 +95,26 @@ __device__ __forceinline__ void report3(unsigned long long* st, uint32_t epoch, 
 // 16 B (template: the granule assembly below is static register moves): lane l stores the
 // granules [4q - R, 4q - R + 4) for its groups q; the first takes the previous group's last R
 // integers from lane l - 1 (lane 0: the previous pass's lane 31).
+__device__ __forceinline__ void stg_stream_v8(void* p, const uint4& a, const uint4& b) {
+    asm volatile("st.global.cs.v8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(p), "r"(a.x), "r"(a.y), "r"(a.z),
+                 "r"(a.w), "r"(b.x), "r"(b.y), "r"(b.z), "r"(b.w)
+                 : "memory");
+}
+
+// Store a pass's four granules per lane: granule k = elements [4 (g0 + k) - R, +4) relative to o,
+// at 16-B aligned Bp + 4 (g0 + k).  Lanes are 64 B apart, so each store instruction touches
+// 16 lines; pairs of whole granules on a 32-B boundary leave as one 256-bit store (sm_100),
+// halving the L1 wavefronts of the stores.
 template <uint32_t R>
 __device__ __forceinline__ void store_pass(const uint4 (&v)[4], uint32_t* __restrict__ o, uint32_t g0, int nints,
                                            uint4& carry) {
     const int lane = threadIdx.x & 31;
+    uint4 G[4];
+    uint32_t* Bp = o - R;  // 16-B aligned
     if constexpr (R == 0) {
 #pragma unroll
-        for (int k = 0; k < 4; ++k) {
-            const int e0 = 4 * (int)(g0 + k);
-            if (e0 + 4 <= nints)
-                stg_stream_v4(o + e0, v[k]);
-            else if (e0 < nints)
-                store_group(o + e0, v[k], (uint32_t)(nints - e0), false);
-        }
+        for (int k = 0; k < 4; ++k) G[k] = v[k];
     } else {
-        uint32_t* A = o - R;  // 16-B aligned
         const int src = (lane + 31) & 31;
         uint4 rot = make_uint4(0, 0, 0, 0);
         rot.w = __shfl_sync(kFull, v[3].w, src);
@@ -120,18 +125,44 @@ __device__ __forceinline__ void store_pass(const uint4 (&v)[4], uint32_t* __rest
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
             const uint4 pv = k == 0 ? prv0 : v[k - 1], cv = v[k];
-            const uint4 g = R == 1 ? make_uint4(pv.w, cv.x, cv.y, cv.z)
-                          : R == 2 ? make_uint4(pv.z, pv.w, cv.x, cv.y)
-                                   : make_uint4(pv.y, pv.z, pv.w, cv.x);
-            const int e0 = 4 * (int)(g0 + k) - (int)R;
-            if (e0 >= 0 && e0 + 4 <= nints) {
-                stg_stream_v4(A + 4 * (g0 + k), g);
-            } else {
+            G[k] = R == 1 ? make_uint4(pv.w, cv.x, cv.y, cv.z)
+                 : R == 2 ? make_uint4(pv.z, pv.w, cv.x, cv.y)
+                          : make_uint4(pv.y, pv.z, pv.w, cv.x);
+        }
+    }
+    auto full = [&](int k) {
+        const int e0 = 4 * (int)(g0 + k) - (int)R;
+        return e0 >= 0 && e0 + 4 <= nints;
+    };
+    auto one = [&](int k) {
+        const int e0 = 4 * (int)(g0 + k) - (int)R;
+        if (e0 >= 0 && e0 + 4 <= nints) {
+            stg_stream_v4(Bp + 4 * (g0 + k), G[k]);
+        } else {
 #pragma unroll
-                for (int i = 0; i < 4; ++i)
-                    if (e0 + i >= 0 && e0 + i < nints) A[4 * (g0 + k) + i] = comp(g, i);
+            for (int i = 0; i < 4; ++i)
+                if (e0 + i >= 0 && e0 + i < nints) Bp[4 * (g0 + k) + i] = comp(G[k], i);
+        }
+    };
+    if ((((uintptr_t)Bp) & 31) == 0) {  // warp-uniform: granule pairs (0,1), (2,3) are 32-B aligned
+#pragma unroll
+        for (int k = 0; k < 4; k += 2) {
+            if (full(k) && full(k + 1)) {
+                stg_stream_v8(Bp + 4 * (g0 + k), G[k], G[k + 1]);
+            } else {
+                one(k);
+                one(k + 1);
             }
         }
+    } else {  // pair (1,2) is
+        one(0);
+        if (full(1) && full(2)) {
+            stg_stream_v8(Bp + 4 * (g0 + 1), G[1], G[2]);
+        } else {
+            one(1);
+            one(2);
+        }
+        one(3);
     }
 }
 
