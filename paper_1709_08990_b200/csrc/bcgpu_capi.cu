@@ -213,6 +213,7 @@ int bcgpu_debug_set_trace(bcgpu_ctx* c, void* d_trace) {
 //   512     host API: no piecewise pipelining
 //   1024    decode: sums pass + pooled delta decode instead of the one-pass kernel
 //   0x8000  decode: the control scan only (dev timing; output not written)
+//   0x40000 decode: the control scan also scans the chunk totals before the one-pass decode
 //   bits 12-14 batch kernels: cap CTAs per SM
 //   bits 16-23 segment-resident batch decode: ring KiB per warp (default 8)
 //   bits 24-31 segment-resident batch encode: ring KiB per warp (default 9)

@@ -77,9 +77,9 @@ __global__ void __launch_bounds__(256)
     // the next kernel (programmatic dependent launch) may start its prologue now; it waits
     // for this grid's completion before reading anything written here
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
-    if (zero_sums && tid == 0) meta.chunksums[chunk] = 0;
+    if ((zero_sums & 1) && tid == 0) meta.chunksums[chunk] = 0;
     // delta: clear this chunk's one-pass aggregates, so nothing stale can carry the call's epoch
-    if (zero_sums && tid < kChunkSubs / kCTWarps) {
+    if ((zero_sums & 1) && tid < kChunkSubs / kCTWarps) {
         const uint64_t tile = (uint64_t)chunk * (kChunkSubs / kCTWarps) + tid;
         if (tile * kCTWarps < nsub) meta.agg[tile] = 0;
     }
@@ -102,7 +102,10 @@ __global__ void __launch_bounds__(256)
     const uint64_t sub = (uint64_t)chunk * kChunkSubs + (tid >> 2);
     if ((lane & 3) == 0 && sub < nsub) meta.localpre[sub] = wpre + incl - v;
     if (tid == 0) meta.chunkpre[chunk] = total;
-    // last CTA: scan the chunk totals, validate the stream length
+    // last CTA: scan the chunk totals, validate the stream length -- unless the one-pass
+    // decode follows (zero_sums bit 1): its producers sum the totals themselves and its
+    // last tile checks the length, so this phase is off the critical path
+    if (zero_sums & 2) return;
     __syncthreads();
     if (tid == 0) {
         __threadfence();
@@ -638,7 +641,7 @@ template <bool kTrace>
 __global__ void __launch_bounds__(kSumThreads, 3)
     svb_decode1_kernel(const uint8_t* __restrict__ in, uint64_t in_len, uint64_t n, uint32_t base,
                        uint32_t* __restrict__ out, uint32_t* __restrict__ d_last, DecodeMeta meta, uint32_t pool_bytes,
-                       uint32_t epoch) {
+                       uint32_t epoch, unsigned long long* status, uint32_t totals) {
     extern __shared__ __align__(128) uint8_t dsm[];
     __shared__ D1Shared sh;
     constexpr uint32_t kTileCtrl = kCTWarps * kWTGroups;
@@ -677,20 +680,55 @@ __global__ void __launch_bounds__(kSumThreads, 3)
                 const uint64_t t = (uint64_t)blockIdx.x + (uint64_t)i * G;
                 if (t < ntiles) issue_meta((uint32_t)t, i);
             }
+        // totals: meta.chunkpre holds chunk TOTALS (the control scan skipped its last-CTA
+        // scan); the producer keeps the prefix of its current chunk P and, one tile ahead,
+        // loads the totals between its next two chunks (<= G/8 + 1 <= 64 of them)
+        const uint32_t nchunks = (uint32_t)((nsub + kChunkSubs - 1) / kChunkSubs);
+        constexpr uint32_t kTilesPerChunk = kChunkSubs / kCTWarps;
+        unsigned long long P = 0, r0 = 0, r1 = 0;
+        auto ld_tot = [&](uint32_t j, uint32_t lim) -> unsigned long long {
+            return j < lim ? __ldg(reinterpret_cast<const unsigned long long*>(meta.chunkpre) + j) : 0ull;
+        };
+        if (totals) {
+            const uint32_t c0 = blockIdx.x / kTilesPerChunk;
+            unsigned long long a = ld_tot((uint32_t)lane, c0) + ld_tot((uint32_t)lane + 32, c0);
+#pragma unroll
+            for (int o = 16; o; o >>= 1) a += __shfl_xor_sync(kFull, a, o);
+            P = a;  // c0 <= 63 chunks below the first tile
+            r0 = ld_tot(c0 + lane, nchunks);
+            r1 = ld_tot(c0 + 32 + lane, nchunks);
+        }
         uint32_t k = 0;
         int st = 0;
         uint32_t ph = 0;
         for (uint32_t t = blockIdx.x; t < ntiles; t += G, ++k, st = st + 1 == kD1Stages ? 0 : st + 1, ph ^= st == 0) {
+            unsigned long long Pc = 0, Tc = 0;
+            if (totals) {  // r0 / r1: totals of chunks [c, c + 64) with c = this tile's chunk
+                const uint32_t c = t / kTilesPerChunk;
+                const uint32_t cn = t + G < ntiles ? (t + G) / kTilesPerChunk : c + 1;
+                Pc = P;
+                Tc = __shfl_sync(kFull, r0, 0);
+                unsigned long long a = ((uint32_t)lane < cn - c ? r0 : 0ull) + ((uint32_t)lane + 32 < cn - c ? r1 : 0ull);
+#pragma unroll
+                for (int o = 16; o; o >>= 1) a += __shfl_xor_sync(kFull, a, o);
+                P += a;
+                r0 = ld_tot(cn + lane, nchunks);
+                r1 = ld_tot(cn + 32 + lane, nchunks);
+            }
             uint8_t* sc = dsm + (uint32_t)st * stride;
             uint8_t* pool = sc + kTileCtrl;
             const uint64_t s0 = (uint64_t)t * kCTWarps, chunk = s0 / kChunkSubs;
             const uint32_t ns = (uint32_t)(nsub - s0 < (uint64_t)kCTWarps ? nsub - s0 : (uint64_t)kCTWarps);
             mbar_wait_parity(&sh.mfull[st], ph);
             const SumMeta& M = sh.meta[st];
-            const unsigned long long cpre = M.chk[chunk & 1];
+            const unsigned long long cpre = totals ? Pc : M.chk[chunk & 1];
             const bool end_at_chunk = s0 + ns == nsub || (s0 + ns) % kChunkSubs == 0;
             const unsigned long long A = cpre + M.loc[0];
-            const unsigned long long B = end_at_chunk ? M.chk[(chunk & 1) + 1] : cpre + M.loc[ns];
+            const unsigned long long B = end_at_chunk ? (totals ? Pc + Tc : M.chk[(chunk & 1) + 1]) : cpre + M.loc[ns];
+            if (totals && s0 + ns == nsub && lane == 0) {  // the stream's last tile: its length
+                const uint64_t need = ngroups + B;
+                if (need != in_len) dec_report(status, epoch, need > in_len ? BCGPU_ERR_TRUNCATED : BCGPU_ERR_TRAILING_BYTES);
+            }
             const uint32_t li = (uint32_t)lane < ns ? (uint32_t)lane : ns;
             const unsigned long long my = (li == ns) ? B : cpre + M.loc[li];
             const uintptr_t Ag = data0 + A, Bg = data0 + B, bse = Ag & ~(uintptr_t)15;
@@ -876,7 +914,8 @@ __global__ void __launch_bounds__(kSumThreads, 3)
 
 static cudaError_t launch_decode1(const uint8_t* in, uint64_t in_len, uint64_t n, uint32_t base, uint32_t* out,
                                   uint32_t* d_last, const DecodeMeta& m, double dpb, uint32_t epoch, cudaStream_t stream,
-                                  bool* used) {
+                                  bool* used, unsigned long long* status = nullptr, uint32_t totals = 0,
+                                  uint64_t* grid_only = nullptr) {
     *used = false;
     uint64_t pool = (uint64_t)(1.1 * dpb * kCTWarps) + 64;
     if (pool < 4096) pool = 4096;
@@ -911,10 +950,14 @@ static cudaError_t launch_decode1(const uint8_t* in, uint64_t in_len, uint64_t n
     const uint64_t ntiles = (nsub + kCTWarps - 1) / kCTWarps;
     uint64_t grid = (uint64_t)sms * (uint64_t)occ;
     if (grid > ntiles) grid = ntiles;
+    if (grid_only) {  // query: the grid this stream would get
+        *grid_only = grid;
+        return cudaSuccess;
+    }
     DecodeMeta mm = m;
     uint32_t pb = (uint32_t)pool;
-    void* args[] = {(void*)&in, (void*)&in_len, (void*)&n,  (void*)&base, (void*)&out,
-                    (void*)&d_last, (void*)&mm, (void*)&pb, (void*)&epoch};
+    void* args[] = {(void*)&in, (void*)&in_len, (void*)&n,    (void*)&base,   (void*)&out,   (void*)&d_last,
+                    (void*)&mm, (void*)&pb,     (void*)&epoch, (void*)&status, (void*)&totals};
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((unsigned)grid);
     cfg.blockDim = dim3(kSumThreads);
@@ -1026,7 +1069,8 @@ cudaError_t launch_decode_ctrl(const uint8_t* in, uint64_t in_len, uint64_t n, i
 // order on one stream (each continues the previous range's carry).
 cudaError_t launch_decode_range(const uint8_t* in, uint64_t in_len, uint64_t n, int delta, uint32_t base,
                                 uint32_t* out, uint32_t* d_last, void* meta_ws, uint64_t sub_begin, uint64_t sub_end,
-                                cudaStream_t stream, int* launches, unsigned long long* trace, uint32_t epoch) {
+                                cudaStream_t stream, int* launches, unsigned long long* trace, uint32_t epoch,
+                                unsigned long long* status, uint32_t totals) {
     DecodeMeta m = carve_decode_meta(meta_ws, n);
     m.trace = trace;
     const uint64_t ngroups = (n + 3) >> 2;
@@ -1055,13 +1099,15 @@ cudaError_t launch_decode_range(const uint8_t* in, uint64_t in_len, uint64_t n, 
     } while (0)
     if (delta && sub_begin == 0 && sub_end == nsub && epoch) {
         bool used = false;
-        const cudaError_t e1 = launch_decode1(in, in_len, n, base, out, d_last, m, dpb, epoch, stream, &used);
+        const cudaError_t e1 = launch_decode1(in, in_len, n, base, out, d_last, m, dpb, epoch, stream, &used, status,
+                                              totals);
         if (e1 != cudaSuccess) return e1;
         if (used) {
             *launches = 1;
             return cudaSuccess;
         }
     }
+    if (totals) return cudaErrorInvalidValue;  // the chunk offsets were left unscanned for the one-pass decode
     if (delta) {
         const uint32_t t0 = (uint32_t)(sub_begin / kCTWarps), t1 = (uint32_t)((sub_end + kCTWarps - 1) / kCTWarps);
         const cudaError_t e2 = launch_sums(in, in_len, n, m, dpb, t0, t1, stream);
@@ -1082,17 +1128,30 @@ cudaError_t launch_decode3(const uint8_t* in, uint64_t in_len, uint64_t n, int d
                            uint32_t* d_last, void* meta_ws, unsigned long long* status, uint32_t epoch, int pipe_grid,
                            cudaStream_t stream, int* launches, unsigned long long* trace, uint32_t debug_flags) {
     (void)pipe_grid;
-    cudaError_t e = launch_decode_ctrl(in, in_len, n, delta, meta_ws, status, epoch, stream);
+    const uint64_t ngroups = (n + 3) >> 2;
+    const uint64_t nsub = (ngroups + kWTGroups - 1) / kWTGroups;
+    const uint32_t ep = (debug_flags & 1024) ? 0u : epoch;
+    // the one-pass delta decode sums the chunk totals itself (grid <= 504: a CTA's chunks
+    // advance by <= 64 per tile), so the control scan can skip its last-CTA scan
+    uint32_t totals = 0;
+    if (delta && ep && !(debug_flags & (0x8000 | 0x40000))) {
+        const double dpb = nsub ? (double)(in_len > ngroups ? in_len - ngroups : 0) / (double)nsub : 0.0;
+        uint64_t g1 = 0;
+        bool used = false;
+        const cudaError_t q = launch_decode1(in, in_len, n, base, out, d_last, carve_decode_meta(meta_ws, n), dpb, ep,
+                                             stream, &used, status, 0, &g1);
+        if (q != cudaSuccess) return q;
+        totals = g1 >= 1 && g1 <= 504 ? 1u : 0u;
+    }
+    cudaError_t e = launch_decode_ctrl(in, in_len, n, delta | (totals ? 2 : 0), meta_ws, status, epoch, stream);
     if (e != cudaSuccess) return e;
     if (debug_flags & 0x8000) {  // dev timing: the control scan alone
         *launches = 1;
         return cudaSuccess;
     }
-    const uint64_t ngroups = (n + 3) >> 2;
-    const uint64_t nsub = (ngroups + kWTGroups - 1) / kWTGroups;
     int l = 0;
-    e = launch_decode_range(in, in_len, n, delta, base, out, d_last, meta_ws, 0, nsub, stream, &l, trace,
-                            (debug_flags & 1024) ? 0u : epoch);
+    e = launch_decode_range(in, in_len, n, delta, base, out, d_last, meta_ws, 0, nsub, stream, &l, trace, ep, status,
+                            totals);
     *launches = 1 + l;
     return e;
 }

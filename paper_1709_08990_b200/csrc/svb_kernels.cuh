@@ -30,12 +30,15 @@ cudaError_t launch_decode3(const uint8_t* in, uint64_t in_len, uint64_t n, int d
 uint64_t decode_meta_bytes(uint64_t n);
 // The same split for the pipelined host API: the control scan over the whole stream,
 // then passes 2-3 per range of sub-tiles (chunk multiples, in order for delta).
+// delta bit 1: skip the chunk-total scan (the one-pass decode that follows sums them itself)
 cudaError_t launch_decode_ctrl(const uint8_t* in, uint64_t in_len, uint64_t n, int delta, void* meta_ws,
                                unsigned long long* status, uint32_t epoch, cudaStream_t stream);
 cudaError_t launch_decode_range(const uint8_t* in, uint64_t in_len, uint64_t n, int delta, uint32_t base,
                                 uint32_t* out, uint32_t* d_last, void* meta_ws, uint64_t sub_begin, uint64_t sub_end,
                                 cudaStream_t stream, int* launches, unsigned long long* trace = nullptr,
-                                uint32_t epoch = 0);  // epoch != 0: a whole-stream delta decode may run one-pass
+                                uint32_t epoch = 0,  // epoch != 0: a whole-stream delta decode may run one-pass
+                                unsigned long long* status = nullptr,
+                                uint32_t totals = 0);  // the control scan left chunk totals (one-pass only)
 unsigned long long* decode_chunkpre_ptr(void* meta_ws, uint64_t n);
 unsigned long long* meta_agg_ptr(void* meta_ws, uint64_t n, uint64_t* count);
 cudaError_t launch_decode_sums(const uint8_t* in, uint64_t in_len, uint64_t n, void* meta_ws, cudaStream_t stream);
