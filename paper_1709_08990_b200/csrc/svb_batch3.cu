@@ -613,16 +613,20 @@ __device__ __forceinline__ void encode_block(uint32_t Sin, uint32_t blk, uint32_
         const uint32_t W0 = shl_c(P0, u8), W1 = __funnelshift_lc(P0, P1, u8), W2 = __funnelshift_lc(P1, P2, u8),
                        W3 = __funnelshift_lc(P2, P3, u8), W4 = __funnelshift_lc(P3, 0u, u8);
         const uint32_t nw = ((o & 3u) + tot) >> 2;  // words this group completes (0 past the stream)
-        const uint32_t pend = nw == 0 ? W0 : nw == 1 ? W1 : nw == 2 ? W2 : nw == 3 ? W3 : W4;
+        // a full block's groups hold >= 4 bytes, so nw >= 1
+        const uint32_t pend = nw == 1 ? W1 : nw == 2 ? W2 : nw == 3 ? W3 : (kFB || nw == 4) ? W4 : W0;
         uint32_t pin = __shfl_up_sync(0xffffffffu, pend, 1);
         if (lane == 0) pin = carry;
         carry = __shfl_sync(0xffffffffu, pend, 31);
         const uint32_t wa = o & ~3u;
-        if (nw > 0) sts32(wa, W0 | pin);
+        if (kFB || nw > 0) sts32(wa, W0 | pin);
         if (nw > 1) sts32(wa + 4, W1);
         if (nw > 2) sts32(wa + 8, W2);
         if (nw > 3) sts32(wa + 12, W3);
-        if (g + 1 == ng && ((o + tot) & 3u)) sts32((o + tot) & ~3u, nw ? pend : (pend | pin));
+        // the piece's last group leaves its partial word (in a full block only when the piece
+        // ends on a block: warp-uniform test first)
+        if ((!kFB || (blk + 3) * 32 >= ng) && g + 1 == ng && ((o + tot) & 3u))
+            sts32((o + tot) & ~3u, nw ? pend : (pend | pin));
     }
 }
 
