@@ -165,10 +165,10 @@ __global__ void __launch_bounds__(kBThreads)
     WarpCtrl wA;
     bool zeroA = false;
     // scan item 0 and issue its data
-    auto scan_and_issue = [&](uint32_t i, WarpCtrl& w, bool& zero) {
-        const int cs = (int)(i % 3), ds = (int)(i & 1);
+    auto scan_and_issue = [&](uint32_t i, int cs, uint32_t cph, WarpCtrl& w, bool& zero) {  // cs = i % 3, cph = (i / 3) & 1
+        const int ds = (int)(i & 1);
         BItem& it = B.item[cs];
-        mbar_wait_parity(&B.cbar[cs], (i / 3) & 1u);
+        mbar_wait_parity(&B.cbar[cs], cph);
         const uintptr_t cbeg = (uintptr_t)in + it.src + (uint64_t)it.k * kWTGroups;
         const uint8_t* sc = B.ctrl[cs] + (cbeg & 15);
         const uint64_t ngroups = ((uint64_t)it.n + 3) >> 2, g0 = (uint64_t)it.k * kWTGroups;
@@ -190,10 +190,11 @@ __global__ void __launch_bounds__(kBThreads)
             if (a1 > a0) tma_load(B.data[ds], reinterpret_cast<const void*>(a0), (uint32_t)(a1 - a0), &B.dbar[ds]);
         }
     };
-    if (B.item[0].valid) scan_and_issue(0, wA, zeroA);
+    if (B.item[0].valid) scan_and_issue(0, 0, 0u, wA, zeroA);
 
+    int sa = 0, sb = 1, sc2 = 2;  // i % 3, (i + 1) % 3, (i + 2) % 3
+    uint32_t ph1 = 0;            // ((i + 1) / 3) & 1
     for (uint32_t i = 0;; ++i) {
-        const int sa = (int)(i % 3), sb = (int)((i + 1) % 3), sc2 = (int)((i + 2) % 3);
         if (!B.item[sa].valid) break;
         // 1. item i+2: descriptor walk + control copy
         {
@@ -213,11 +214,13 @@ __global__ void __launch_bounds__(kBThreads)
         bool zeroB = false;
         const BItem A = B.item[sa];
         const bool b_valid = B.item[sb].valid != 0;
-        const bool same = b_valid && B.item[sb].src == A.src && B.item[sb].dst == A.dst && B.item[sb].k == A.k + 1;
+        // items come in order (tile k + 1 of a segment, or tile 0 of the next), so the next
+        // item continues this segment exactly when its tile index is k + 1
+        const bool same = b_valid && B.item[sb].k == A.k + 1;
         if (b_valid) {
             if (lane == 0) B.item[sb].off = same ? A.off + wA.total : 0ull;
             __syncwarp();
-            scan_and_issue(i + 1, wB, zeroB);
+            scan_and_issue(i + 1, sb, ph1, wB, zeroB);
         }
         // 3. item i: expand + store
         {
@@ -261,6 +264,11 @@ __global__ void __launch_bounds__(kBThreads)
         __syncwarp();
         wA = wB;
         zeroA = zeroB;
+        ph1 ^= sc2 == 0 ? 1u : 0u;  // item i + 2 starts a new lap of the 3-slot ring
+        const int t = sa;
+        sa = sb;
+        sb = sc2;
+        sc2 = t;
     }
 }
 
