@@ -7,7 +7,7 @@ LIBDIR := $(PKG)/lib
 ARCH := -gencode arch=compute_100a,code=sm_100a
 NVFLAGS := $(ARCH) -O3 -lineinfo -std=c++20 -Xcompiler -fPIC,-Wall -Iinclude -I$(PKG)/csrc \
            --expt-relaxed-constexpr -Xptxas -v
-SRCS := $(PKG)/csrc/svb_kernels.cu $(PKG)/csrc/svb_batch2.cu $(PKG)/csrc/svb_batch3.cu $(PKG)/csrc/svb_decode.cu $(PKG)/csrc/svb_encode.cu $(PKG)/csrc/svb_query.cu $(PKG)/csrc/svb_gb.cu $(PKG)/csrc/bcgpu_capi.cu $(PKG)/csrc/bytecodec_host.cpp $(PKG)/csrc/svb_format.cpp
+SRCS := $(PKG)/csrc/launch_cache.cu $(PKG)/csrc/svb_batch_host.cu $(PKG)/csrc/svb_kernels.cu $(PKG)/csrc/svb_batch2.cu $(PKG)/csrc/svb_batch3.cu $(PKG)/csrc/svb_decode.cu $(PKG)/csrc/svb_encode.cu $(PKG)/csrc/svb_query.cu $(PKG)/csrc/svb_gb.cu $(PKG)/csrc/bcgpu_capi.cu $(PKG)/csrc/bytecodec_host.cpp $(PKG)/csrc/svb_format.cpp
 HDRS := $(wildcard $(PKG)/csrc/*.cuh) include/bcgpu/bcgpu.h $(wildcard include/bytecodec/*.hpp)
 
 all: $(LIBDIR)/libbytecodec_b200.so $(LIBDIR)/libsvbgen.so oracle

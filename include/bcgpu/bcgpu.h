@@ -162,11 +162,38 @@ int bcgpu_svb_encode_host(bcgpu_ctx *ctx, const uint32_t *values, size_t n, int 
 int bcgpu_svb_decode_host(bcgpu_ctx *ctx, const uint8_t *bytes, size_t len, size_t n, int delta,
                           uint32_t base, uint32_t *out, uint32_t *last);
 /* svb_decode_block for nblocks (block, offset) pairs held in host memory
- * (size_t arrays, as the reference signature takes them). */
+ * (size_t arrays, as the reference signature takes them).  A block index
+ * >= ceil(n/4) returns OUT_OF_RANGE; a block whose control or data bytes lie
+ * past len returns TRUNCATED (the _device variant writes count 0 for both). */
 int bcgpu_svb_decode_blocks_host(bcgpu_ctx *ctx, const uint8_t *bytes, size_t len, size_t n,
                                  const size_t *blocks, const size_t *offsets, size_t nblocks,
                                  uint32_t *out, uint32_t *counts);
 /* svb_block_data_offsets into a host array of ceil(n/4) entries. */
+/* ---- segmented batches through host memory ------------------------------
+ * The chained-chunk contract of the reference (codec.hpp:87-90,
+ * decode_payload_delta(codec, bytes, n, base, out) once per chunk)
+ * for a whole batch in one call.  Segment s has seg_n[s] integers; the values
+ * of all segments are concatenated in `values` / `out`.  Streams are packed
+ * back to back: segment s occupies bytes [offsets[s], offsets[s+1]).  The call
+ * moves the batch in pieces of whole segments so host->device copies, kernels
+ * and device->host copies overlap (pinned host buffers give full overlap).
+ *
+ * encode: seg_prev[s] seeds segment s's delta transform (NULL = all 0; ignored
+ * when delta == 0).  Writes the packed streams to out (out_cap bytes; the sum of
+ * bcgpu_svb_max_compressed_bytes(seg_n[s]) always suffices, INVALID_ARGUMENT
+ * when the packed total exceeds out_cap) and nseg + 1 offsets to out_offsets
+ * (out_offsets[nseg] = total length). */
+int bcgpu_svb_encode_batch_host(bcgpu_ctx *ctx, const uint32_t *values, const uint32_t *seg_n,
+                                const uint32_t *seg_prev, size_t nseg, int delta, uint8_t *out,
+                                size_t out_cap, uint64_t *out_offsets);
+/* decode: in_offsets[nseg + 1] non-decreasing, in_offsets[nseg] <= len
+ * (TRUNCATED otherwise).  Each segment is validated as svb_decode validates a
+ * stream (truncated / trailing_bytes); seg_base[s] is its delta base (NULL = all
+ * 0).  last (nseg entries, may be NULL) receives each segment's last value
+ * (its base when seg_n[s] == 0), decode_payload_delta's return value. */
+int bcgpu_svb_decode_batch_host(bcgpu_ctx *ctx, const uint8_t *bytes, size_t len, const uint64_t *in_offsets,
+                                const uint32_t *seg_n, const uint32_t *seg_base, size_t nseg, int delta,
+                                uint32_t *out, uint32_t *last);
 int bcgpu_svb_block_offsets_host(bcgpu_ctx *ctx, const uint8_t *bytes, size_t len, size_t n,
                                  uint64_t *offsets);
 

@@ -57,4 +57,20 @@ std::vector<size_t> svb_block_data_offsets(std::span<const uint8_t> bytes, size_
 size_t svb_decode_block(std::span<const uint8_t> bytes, size_t n, size_t block, size_t data_offset,
                         uint32_t out[4]);
 
+// Extension: the chained-chunk contract (reference codec.hpp:87-90, one
+// decode_payload_delta call per chunk with base = the previous chunk's last value;
+// SPEC.md:555) for a whole batch in one GPU call.  Segment s holds seg_n[s] of the
+// concatenated values; its stream is bytes[offsets[s], offsets[s+1]).
+struct svb_batch {
+    std::vector<uint8_t> bytes;
+    std::vector<uint64_t> offsets;  // seg_n.size() + 1 entries
+};
+// seg_prev: each segment's delta base (empty = all 0); delta = false encodes plainly.
+svb_batch svb_encode_batch(std::span<const uint32_t> values, std::span<const uint32_t> seg_n,
+                           std::span<const uint32_t> seg_prev, bool delta = true);
+// out holds sum(seg_n) integers; returns every segment's last value (its base when empty).
+std::vector<uint32_t> svb_decode_batch(std::span<const uint8_t> bytes, std::span<const uint64_t> offsets,
+                                       std::span<const uint32_t> seg_n, std::span<const uint32_t> seg_base,
+                                       uint32_t* out, bool delta = true);
+
 }  // namespace bytecodec

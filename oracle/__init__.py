@@ -48,6 +48,8 @@ def _load() -> C.CDLL:
         "svbo_prefix_sum4": (None, [vp, u32, vp]),
         "svbo_block_data_offsets": (None, [vp, sz, vp]),
         "svbo_decode_block": (sz, [vp, sz, sz, sz, sz, vp]),
+        "svbo_paper_decode": (i, [vp, sz, sz, i, u32, vp, vp]),
+        "svbo_paper_decode_batch": (i, [vp, sz, vp, i, vp, vp]),
         "svbo_mt_encode": (sz, [vp, sz, i, u32, vp, i]),
         "svbo_mt_decode": (i, [vp, sz, sz, i, u32, vp, vp, i]),
         "svbo_decode_batch": (i, [vp, sz, vp, vp, i, i]),
@@ -152,6 +154,28 @@ def decode_block(data, n: int, block: int, data_offset: int) -> np.ndarray:
     out = np.zeros(4, np.uint32)
     k = lib.svbo_decode_block(_ptr(b), b.size, n, block, data_offset, out.ctypes.data)
     return out[:k]
+
+
+def paper_decode(data, n: int, delta: bool = False, base: int = 0, buf: np.ndarray | None = None) -> tuple[int, int]:
+    """The paper's timing mode: single-thread O2 decode into a reused
+    4096-integer buffer.  Returns (status, sum of each 4096-block's last integer mod 2^64)."""
+    b = _u8(data)
+    if buf is None:
+        buf = np.empty(4096, np.uint32)
+    chk = C.c_uint64(0)
+    st = lib.svbo_paper_decode(_ptr(b), b.size, n, int(delta), base & 0xFFFFFFFF, buf.ctypes.data, C.byref(chk))
+    return int(st), int(chk.value)
+
+
+def paper_decode_batch(segs: np.ndarray, data, delta: bool, buf: np.ndarray | None = None) -> tuple[int, int]:
+    """paper_decode over every segment (bcgpu_decode_segment layout), one thread, one buffer."""
+    b = _u8(data)
+    s = np.ascontiguousarray(segs)
+    if buf is None:
+        buf = np.empty(4096, np.uint32)
+    chk = C.c_uint64(0)
+    st = lib.svbo_paper_decode_batch(s.ctypes.data, s.size, _ptr(b), int(delta), buf.ctypes.data, C.byref(chk))
+    return int(st), int(chk.value)
 
 
 def mt_encode(values, delta: bool = False, prev: int = 0, threads: int | None = None,

@@ -195,8 +195,8 @@ static const uint8_t *scalar_range(const uint8_t *ctrl, const uint8_t *data, siz
 /* Decode integers [0, n) of a stream whose control bytes start at ctrl and
  * data bytes at data, never reading at or beyond data_end.  Returns the last
  * reconstructed value (delta) or the running base unchanged (plain). */
-static uint32_t o2_decode_range(const uint8_t *ctrl, const uint8_t *data, const uint8_t *data_end, size_t n,
-                                int delta, uint32_t base, uint32_t *out) {
+static uint32_t o2_decode_range_next(const uint8_t *ctrl, const uint8_t *data, const uint8_t *data_end, size_t n,
+                                     int delta, uint32_t base, uint32_t *out, const uint8_t **data_next) {
     ensure_tables();
     size_t i = 0;
     uint32_t acc = base;
@@ -273,8 +273,39 @@ static uint32_t o2_decode_range(const uint8_t *ctrl, const uint8_t *data, const 
         i += 4;
     }
 #endif
-    scalar_range(ctrl, data, i, n - i, delta, &acc, out);
+    const uint8_t *dn = scalar_range(ctrl, data, i, n - i, delta, &acc, out);
+    if (data_next) *data_next = dn;
     return acc;
+}
+
+static uint32_t o2_decode_range(const uint8_t *ctrl, const uint8_t *data, const uint8_t *data_end, size_t n,
+                                int delta, uint32_t base, uint32_t *out) {
+    return o2_decode_range_next(ctrl, data, data_end, n, delta, base, out, NULL);
+}
+
+/* The paper's measurement mode: one thread decodes the stream
+ * sequentially into a reused buffer of 4096 integers (half of a 32 KiB L1), so the
+ * output stays in L1 and the timing is the decoder's, RAM -> L1.  Same O2 kernel as
+ * svbo_ssse3_decode, 4096 integers (1024 control bytes) per call.  *check gets the
+ * sum over blocks of each block's last decoded integer, mod 2^64 (so the work
+ * cannot be elided and callers can compare it with the expected values, without
+ * adding a pass over the buffer to the timed loop). */
+int svbo_paper_decode(const uint8_t *in, size_t in_len, size_t n, int delta, uint32_t base, uint32_t *buf,
+                      uint64_t *check) {
+    int st = validate(in, in_len, n);
+    if (st != SVBO_OK) return st;
+    const size_t nctrl = svbo_control_bytes(n);
+    const uint8_t *data = in + nctrl;
+    uint32_t acc = base;
+    uint64_t sum = 0;
+    for (size_t i = 0; i < n; i += 4096) {
+        const size_t m = n - i < 4096 ? n - i : 4096;
+        const uint32_t r = o2_decode_range_next(in + i / 4, data, in + in_len, m, delta, acc, buf, &data);
+        if (delta) acc = r;
+        sum += buf[m - 1];
+    }
+    if (check) *check = sum;
+    return SVBO_OK;
 }
 
 int svbo_ssse3_decode(const uint8_t *in, size_t in_len, size_t n, int delta, uint32_t base,
@@ -560,6 +591,23 @@ static void enc_batch_fn(void *p, int t, int nt) {
         c->out_lens[s] = svbo_encode((const uint32_t *)c->in + e->src_offset, e->n, c->delta, e->prev,
                                      (uint8_t *)c->out + e->dst_offset);
     }
+}
+
+/* The paper's timing mode over a batch (PAPER.md:415,436 decode posting lists one after
+ * another): every segment, single thread, decoded by svbo_paper_decode into the same
+ * 4096-integer buffer; *check sums the per-segment checks. */
+int svbo_paper_decode_batch(const svbo_decode_segment *segs, size_t nseg, const uint8_t *in, int delta,
+                            uint32_t *buf, uint64_t *check) {
+    uint64_t sum = 0;
+    for (size_t s = 0; s < nseg; ++s) {
+        uint64_t c = 0;
+        int st = svbo_paper_decode(in + segs[s].src_offset, segs[s].src_bytes, segs[s].n, delta, segs[s].prev, buf,
+                                   &c);
+        if (st != SVBO_OK) return st;
+        sum += c;
+    }
+    if (check) *check = sum;
+    return SVBO_OK;
 }
 
 int svbo_encode_batch(const svbo_encode_segment *segs, size_t nseg, const uint32_t *in, uint8_t *out,

@@ -60,6 +60,10 @@ int svbo_decode(const uint8_t *in, size_t in_len, size_t n, int delta, uint32_t 
 /* O2 decoder: paper Fig. 4 + zero fast path + scalar tail. */
 int svbo_ssse3_decode(const uint8_t *in, size_t in_len, size_t n, int delta, uint32_t base,
                       uint32_t *out, uint32_t *last);
+/* The paper's timing mode: O2 decode, single thread, into the
+ * reused 4096-integer buffer buf; *check = sum of every 4096-block's last integer mod 2^64. */
+int svbo_paper_decode(const uint8_t *in, size_t in_len, size_t n, int delta, uint32_t base, uint32_t *buf,
+                      uint64_t *check);
 /* 1 when the O2 decoder was compiled with SSSE3, 0 when it runs its scalar twin. */
 int svbo_ssse3_available(void);
 
@@ -105,6 +109,9 @@ typedef struct {
 
 int svbo_decode_batch(const svbo_decode_segment *segs, size_t nseg, const uint8_t *in,
                       uint32_t *out, int delta, int nthreads);
+/* svbo_paper_decode over every segment of a batch, one thread, one reused buffer. */
+int svbo_paper_decode_batch(const svbo_decode_segment *segs, size_t nseg, const uint8_t *in, int delta,
+                            uint32_t *buf, uint64_t *check);
 int svbo_encode_batch(const svbo_encode_segment *segs, size_t nseg, const uint32_t *in,
                       uint8_t *out, uint64_t *out_lens, int delta, int nthreads);
 

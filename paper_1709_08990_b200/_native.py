@@ -13,7 +13,6 @@ from pathlib import Path
 PKG_DIR = Path(__file__).resolve().parent
 LIB_DIR = PKG_DIR / "lib"
 LIB_PATH = LIB_DIR / "libbytecodec_b200.so"
-GEN_PATH = LIB_DIR / "libsvbgen.so"
 
 
 class NativeLibraryMissing(ImportError):
@@ -66,6 +65,8 @@ SIGNATURES = {
     "bcgpu_svb_decode_host": (_int, [_vp, _vp, _sz, _sz, _int, _u32, _vp, C.POINTER(_u32)]),
     "bcgpu_svb_decode_blocks_host": (_int, [_vp, _vp, _sz, _sz, _vp, _vp, _sz, _vp, _vp]),
     "bcgpu_svb_block_offsets_host": (_int, [_vp, _vp, _sz, _sz, _vp]),
+    "bcgpu_svb_encode_batch_host": (_int, [_vp, _vp, _vp, _vp, _sz, _int, _vp, _sz, _vp]),
+    "bcgpu_svb_decode_batch_host": (_int, [_vp, _vp, _sz, _vp, _vp, _vp, _sz, _int, _vp, _vp]),
     "bcgpu_svb_seek_batch_device": (_int, [_vp, _vp, _sz, _sz, _u32, _vp, _sz, _vp, _vp, _vp]),
     "bcgpu_svb_select_batch_device": (_int, [_vp, _vp, _sz, _sz, _u32, _vp, _sz, _vp, _vp]),
     "bcgpu_svb_seek_host": (_int, [_vp, _vp, _sz, _sz, _u32, _vp, _sz, _vp, _vp]),
@@ -84,20 +85,6 @@ SIGNATURES = {
 lib = _load(LIB_PATH)
 for _name, (_res, _args) in SIGNATURES.items():
     _fn = getattr(lib, _name)
-    _fn.restype = _res
-    _fn.argtypes = _args
-
-_GEN_SIGS = {
-    "svbgen_splitmix64": (_u64, [_u64, _u64]),
-    "svbgen_uniform_classes": (None, [_u64, _u64, _vp, _int]),
-    "svbgen_geometric_sorted": (None, [_u64, _u64, C.c_double, _u32, _vp, _int]),
-    "svbgen_list_lengths": (_u64, [_u64, _u64, _u64, _vp]),
-    "svbgen_posting_lists": (None, [_u64, _u64, _vp, _vp, _u32, _vp, _int]),
-}
-
-gen = _load(GEN_PATH)
-for _name, (_res, _args) in _GEN_SIGS.items():
-    _fn = getattr(gen, _name)
     _fn.restype = _res
     _fn.argtypes = _args
 

@@ -203,6 +203,49 @@ def svb_decode_blocks(data, n: int, blocks, offsets) -> tuple[np.ndarray, np.nda
     return out, cnt
 
 
+# ---- segmented batches through host memory (codec.hpp:87-90 once per segment) ----
+def _np_ptr(a: np.ndarray | None):
+    return a.ctypes.data if a is not None and a.size else None
+
+
+def svb_encode_batch(values, seg_n, seg_prev=None, delta: bool = True, out: np.ndarray | None = None
+                     ) -> tuple[np.ndarray, np.ndarray]:
+    """Encode every segment (seg_n[s] integers of the concatenated ``values``, delta base
+    seg_prev[s]) as its own stream; streams packed back to back.  Returns (bytes, offsets):
+    segment s is bytes[offsets[s]:offsets[s+1]].  One C-ABI call, pipelined over pieces."""
+    v = _u32_array(values)
+    ns = np.ascontiguousarray(seg_n, dtype=np.uint32)
+    if int(ns.sum(dtype=np.uint64)) != v.size:
+        raise ValueError("sum(seg_n) must equal len(values)")
+    pv = None if seg_prev is None else np.ascontiguousarray(seg_prev, dtype=np.uint32)
+    cap = int(((ns.astype(np.uint64) + 3) // 4 + 4 * ns.astype(np.uint64)).sum())
+    o = np.empty(max(1, cap), np.uint8) if out is None else out
+    offs = np.zeros(ns.size + 1, np.uint64)
+    _check(lib.bcgpu_svb_encode_batch_host(_ctx(), _np_ptr(v), _np_ptr(ns), _np_ptr(pv), ns.size, int(delta),
+                                           o.ctypes.data, o.size, offs.ctypes.data), "svb_encode_batch")
+    return o[: int(offs[-1])], offs
+
+
+def svb_decode_batch(data, offsets, seg_n, seg_base=None, delta: bool = True, out: np.ndarray | None = None,
+                     want_last: bool = False):
+    """Decode the packed streams of :func:`svb_encode_batch` (segment s = data[offsets[s]:offsets[s+1]],
+    seg_n[s] integers, delta base seg_base[s]) into one concatenated array; with want_last also
+    every segment's last value (decode_payload_delta's return value)."""
+    b = _byte_array(data)
+    offs = np.ascontiguousarray(offsets, dtype=np.uint64)
+    ns = np.ascontiguousarray(seg_n, dtype=np.uint32)
+    if offs.size != ns.size + 1:
+        raise ValueError("offsets must hold len(seg_n) + 1 entries")
+    bs = None if seg_base is None else np.ascontiguousarray(seg_base, dtype=np.uint32)
+    total = int(ns.sum(dtype=np.uint64))
+    o = np.empty(max(1, total), np.uint32) if out is None else out
+    last = np.zeros(max(1, ns.size), np.uint32) if want_last else None
+    _check(lib.bcgpu_svb_decode_batch_host(_ctx(), _np_ptr(b), b.size, offs.ctypes.data, _np_ptr(ns), _np_ptr(bs),
+                                           ns.size, int(delta), o.ctypes.data, _np_ptr(last)), "svb_decode_batch")
+    res = o[:total]
+    return (res, last[: ns.size]) if want_last else res
+
+
 # ---- varint-GB (varint_gb.hpp:14-31; SPEC.md:164-214) -----------------------
 def _gb_encode(values, delta: bool, prev: int) -> bytes:
     v = _u32_array(values)

@@ -4,6 +4,7 @@
 // status word) and the host-pointer entry points that give the reference's
 // synchronous call semantics (H2D, kernel, D2H, codec_error mapping).
 // No CPU fallback: every compute entry point launches a kernel or fails.
+#include <algorithm>
 #include <atomic>
 #include <cstdio>
 #include <cstring>
@@ -76,6 +77,7 @@ struct bcgpu_ctx {
     unsigned long long* pin = nullptr;       // host pipeline: pinned offsets / status
     size_t pin_cap = 0;                      // entries
     uint64_t agg_n = 0;                      // n whose tile aggregates hold no current-epoch tag
+    cudaEvent_t bev[2 * 128] = {};          // host batches: piece hand-offs (in, done)
     uint32_t* endval = nullptr;              // seek / select: last value of every sub-tile
     size_t endval_cap = 0;                   // entries
     void* gbws = nullptr;                    // varint-GB decode: chunk transfer tables (svb_gb.cu)
@@ -104,7 +106,9 @@ static int ensure_ws(bcgpu_ctx* c, size_t tiles) {
     BC_CUDA(cudaMalloc(&c->ws, bytes));
     BC_CUDA(cudaMemset(c->ws, 0, bytes));
     c->ws_tiles = cap;
-    c->epoch = 0;
+    // the epoch keeps running across reallocations: the one-pass encode's tile aggregates
+    // (in the metadata workspace, not here) keep their old tags, and agg_n trusts that no
+    // aggregate holds a tag >= the next epoch
     c->ticket_base = 0;
     return BCGPU_OK;
 }
@@ -295,6 +299,7 @@ int bcgpu_ctx_create(int device, bcgpu_ctx** out) {
         cudaSuccess)
         c->pin_cap = 4096;
     for (auto& ev : c->events) cudaEventCreateWithFlags(&ev, cudaEventDisableTiming);
+    for (auto& ev : c->bev) cudaEventCreateWithFlags(&ev, cudaEventDisableTiming);
     const int st = ensure_ws(c, 1024);
     if (st) {
         cudaStreamDestroy(c->stream);
@@ -320,6 +325,8 @@ int bcgpu_ctx_destroy(bcgpu_ctx* c) {
     if (c->aux2) cudaStreamDestroy(c->aux2);
     if (c->pin) cudaFreeHost(c->pin);
     for (auto& ev : c->events)
+        if (ev) cudaEventDestroy(ev);
+    for (auto& ev : c->bev)
         if (ev) cudaEventDestroy(ev);
     delete c;
     return BCGPU_OK;
@@ -591,12 +598,16 @@ static uint64_t pipe_piece_ints(uint64_t n) {
 // Encode: pieces stream in on `aux`; piece k's size scan continues from piece k-1's
 // running offset and its tile encode follows on `stream`; once its offset is known on the
 // host (pinned copy) its control and data bytes stream out on `aux2`.
+static int ensure_pin(bcgpu_ctx* c, size_t entries);
+
 static int encode_host_pipelined(bcgpu_ctx* c, const uint32_t* values, size_t n, int delta, uint32_t prev,
                                  uint8_t* out, uint8_t* d, size_t off_out, size_t* out_len) {
     const uint64_t P = pipe_piece_ints(n), K = (n + P - 1) / P;
     const uint64_t ngroups = (n + 3) / 4;
     cudaStream_t sc = c->stream, si = c->aux, so = c->aux2;
-    int st = ensure_meta(c, n, sc);
+    int st = ensure_pin(c, K + 1);
+    if (st) return st;
+    st = ensure_meta(c, n, sc);
     if (st) return st;
     st = next_epoch(c, sc);
     if (st) return st;
@@ -663,7 +674,7 @@ int bcgpu_svb_encode_host(bcgpu_ctx* c, const uint32_t* values, size_t n, int de
 }
 
 static int ensure_pin(bcgpu_ctx* c, size_t entries) {
-    if (entries <= c->pin_cap) return BCGPU_OK;
+    if (c->pin && entries <= c->pin_cap) return BCGPU_OK;
     BC_CUDA(cudaStreamSynchronize(c->stream));
     BC_CUDA(cudaStreamSynchronize(c->aux2));
     if (c->pin) cudaFreeHost(c->pin);
@@ -767,6 +778,18 @@ int bcgpu_svb_decode_blocks_host(bcgpu_ctx* c, const uint8_t* bytes, size_t len,
     if (!c || (nblocks && (!blocks || !offsets || !out || !counts)) || (len && !bytes))
         return BCGPU_ERR_INVALID_ARGUMENT;
     if (nblocks == 0) return BCGPU_OK;
+    // svb_decode_block's contract (stream_vbyte.hpp:51-54) on host data: a block index past
+    // ceil(n/4) is out_of_range; a block whose control byte or data bytes lie past the end
+    // of the stream is truncated (the device entry point reports both as count 0)
+    const size_t ngroups = (n + 3) / 4;
+    for (size_t i = 0; i < nblocks; ++i) {
+        if (blocks[i] >= ngroups) return BCGPU_ERR_OUT_OF_RANGE;
+        if (blocks[i] >= len) return BCGPU_ERR_TRUNCATED;
+        const uint32_t cnt = (blocks[i] == ngroups - 1 && (n & 3)) ? (uint32_t)(n & 3) : 4u;
+        size_t need = 0;
+        for (uint32_t f = 0; f < cnt; ++f) need += ((bytes[blocks[i]] >> (2 * f)) & 3u) + 1u;
+        if (ngroups + offsets[i] + need > len || offsets[i] > len) return BCGPU_ERR_TRUNCATED;
+    }
     DeviceGuard g(c->device);
     const size_t off_q = align_up(len, 256), off_o = off_q + 16 * nblocks, off_c = off_o + 16 * nblocks;
     void* sp = nullptr;
@@ -804,6 +827,194 @@ int bcgpu_svb_block_offsets_host(bcgpu_ctx* c, const uint8_t* bytes, size_t len,
     if (st) return st;
     BC_CUDA(cudaMemcpyAsync(offsets, d + off_o, 8 * nctrl, cudaMemcpyDeviceToHost, c->stream));
     BC_CUDA(cudaStreamSynchronize(c->stream));
+    return BCGPU_OK;
+}
+
+// ---- host-buffer batches: segments of one batch move in pieces of whole segments so the
+// host->device copies, the kernels and the device->host copies of different pieces overlap.
+// A piece closes at >= P integers or >= S segments (P, S chosen so there are <= 121 pieces).
+namespace {
+constexpr int kBatchPieces = 128;
+struct Piece {
+    uint64_t s0, s1;   // segments
+    uint64_t i0, i1;   // integers
+    uint32_t max_n;
+};
+int cut_pieces(const uint32_t* seg_n, size_t nseg, Piece* pieces, int* npieces, uint64_t* total_n,
+               uint64_t* total_cap) {
+    uint64_t N = 0, cap = 0;
+    for (size_t s = 0; s < nseg; ++s) {
+        N += seg_n[s];
+        cap += ((uint64_t)seg_n[s] + 3) / 4 + 4ull * seg_n[s];
+    }
+    const uint64_t P = std::max<uint64_t>(4ull << 20, (N + 59) / 60);
+    const uint64_t S = std::max<uint64_t>(1ull << 20, (nseg + 59) / 60);
+    int k = 0;
+    Piece cur{0, 0, 0, 0, 0};
+    uint64_t at = 0;
+    for (size_t s = 0; s < nseg; ++s) {
+        at += seg_n[s];
+        cur.max_n = std::max(cur.max_n, seg_n[s]);
+        if (at - cur.i0 >= P || s + 1 - cur.s0 >= S || s + 1 == nseg) {
+            if (k >= kBatchPieces) return BCGPU_ERR_INVALID_ARGUMENT;  // cannot happen with the P, S above
+            cur.s1 = s + 1;
+            cur.i1 = at;
+            pieces[k++] = cur;
+            cur = Piece{s + 1, 0, at, 0, 0};
+        }
+    }
+    *npieces = k;
+    *total_n = N;
+    *total_cap = cap;
+    return BCGPU_OK;
+}
+}  // namespace
+
+int bcgpu_svb_encode_batch_host(bcgpu_ctx* c, const uint32_t* values, const uint32_t* seg_n, const uint32_t* seg_prev,
+                                size_t nseg, int delta, uint8_t* out, size_t out_cap, uint64_t* out_offsets) {
+    if (!c || (nseg && (!seg_n || !out_offsets))) return BCGPU_ERR_INVALID_ARGUMENT;
+    if (nseg == 0) {
+        if (out_offsets) out_offsets[0] = 0;
+        return BCGPU_OK;
+    }
+    Piece pieces[kBatchPieces];
+    int K = 0;
+    uint64_t N = 0, cap = 0;
+    int st = cut_pieces(seg_n, nseg, pieces, &K, &N, &cap);
+    if (st) return st;
+    if (N && (!values || !out)) return BCGPU_ERR_INVALID_ARGUMENT;
+    DeviceGuard g(c->device);
+    const size_t o_vals = 0, o_out = align_up(4 * N, 256), o_n = align_up(o_out + cap + 16, 256),
+                 o_prev = align_up(o_n + 4 * nseg, 256), o_es = align_up(o_prev + 4 * nseg, 256),
+                 o_sz = align_up(o_es + sizeof(bcgpu_encode_segment) * nseg, 256),
+                 o_offs = align_up(o_sz + 8 * nseg, 256), o_run = align_up(o_offs + 8 * (nseg + 1), 256);
+    void* sp = nullptr;
+    st = scratch(c, o_run + 256, &sp);
+    if (st) return st;
+    st = ensure_pin(c, (size_t)K + 1);
+    if (st) return st;
+    uint8_t* d = static_cast<uint8_t*>(sp);
+    auto* d_vals = reinterpret_cast<uint32_t*>(d + o_vals);
+    uint8_t* d_out = d + o_out;
+    auto* d_n = reinterpret_cast<uint32_t*>(d + o_n);
+    auto* d_prev = reinterpret_cast<uint32_t*>(d + o_prev);
+    auto* d_es = reinterpret_cast<bcgpu_encode_segment*>(d + o_es);
+    auto* d_sz = reinterpret_cast<uint64_t*>(d + o_sz);
+    auto* d_offs = reinterpret_cast<uint64_t*>(d + o_offs);
+    auto* d_run = reinterpret_cast<unsigned long long*>(d + o_run);
+    cudaStream_t sc = c->stream, si = c->aux, so = c->aux2;
+    BatchArgs ba;
+    st = make_batch(c, sc, &ba);
+    if (st) return st;
+    cudaEvent_t* ev_in = c->bev;
+    cudaEvent_t* ev_done = c->bev + kBatchPieces;
+    BC_CUDA(cudaMemsetAsync(d_run, 0, 8, si));
+    BC_CUDA(cudaMemcpyAsync(d_n, seg_n, 4 * nseg, cudaMemcpyHostToDevice, si));
+    if (seg_prev) BC_CUDA(cudaMemcpyAsync(d_prev, seg_prev, 4 * nseg, cudaMemcpyHostToDevice, si));
+    for (int k = 0; k < K; ++k) {
+        const Piece& p = pieces[k];
+        if (p.i1 > p.i0)
+            BC_CUDA(cudaMemcpyAsync(d_vals + p.i0, values + p.i0, 4 * (p.i1 - p.i0), cudaMemcpyHostToDevice, si));
+        BC_CUDA(cudaEventRecord(ev_in[k], si));
+    }
+    for (int k = 0; k < K; ++k) {
+        const Piece& p = pieces[k];
+        const uint32_t m = (uint32_t)(p.s1 - p.s0);
+        BC_CUDA(cudaStreamWaitEvent(sc, ev_in[k], 0));
+        BC_CUDA(launch_batch_encode_describe(d_n, seg_prev ? d_prev : nullptr, p.s0, m, 0, d_es, sc));
+        BC_CUDA(launch_sizes_batch(d_es + p.s0, m, d_vals, d_sz + p.s0, delta, ba, sc));
+        BC_CUDA(launch_batch_pack(d_sz, p.s0, m, d_es, d_offs, d_run, sc));
+        BC_CUDA(launch_encode_batch(d_es + p.s0, m, d_vals, d_out, d_sz + p.s0, delta, ba, sc));
+        BC_CUDA(cudaMemcpyAsync(c->pin + k, d_run, 8, cudaMemcpyDeviceToHost, sc));
+        BC_CUDA(cudaEventRecord(ev_done[k], sc));
+        g_launches.fetch_add(4);
+    }
+    int result = BCGPU_OK;
+    for (int k = 0; k < K; ++k) {
+        BC_CUDA(cudaEventSynchronize(ev_done[k]));
+        const uint64_t lo = k ? c->pin[k - 1] : 0ull, hi = c->pin[k];
+        if (hi > out_cap) {  // the caller's buffer is too small: stop copying, report after the drain
+            result = BCGPU_ERR_INVALID_ARGUMENT;
+            break;
+        }
+        BC_CUDA(cudaStreamWaitEvent(so, ev_done[k], 0));
+        if (hi > lo) BC_CUDA(cudaMemcpyAsync(out + lo, d_out + lo, hi - lo, cudaMemcpyDeviceToHost, so));
+    }
+    if (result == BCGPU_OK)
+        BC_CUDA(cudaMemcpyAsync(out_offsets, d_offs, 8 * (nseg + 1), cudaMemcpyDeviceToHost, so));
+    BC_CUDA(cudaStreamSynchronize(sc));
+    BC_CUDA(cudaStreamSynchronize(so));
+    if (result) return result;
+    return bcgpu_ctx_sync_status(c, sc);
+}
+
+int bcgpu_svb_decode_batch_host(bcgpu_ctx* c, const uint8_t* bytes, size_t len, const uint64_t* in_offsets,
+                                const uint32_t* seg_n, const uint32_t* seg_base, size_t nseg, int delta, uint32_t* out,
+                                uint32_t* last) {
+    if (!c || (nseg && (!in_offsets || !seg_n))) return BCGPU_ERR_INVALID_ARGUMENT;
+    if (nseg == 0) return BCGPU_OK;
+    for (size_t s = 0; s < nseg; ++s)
+        if (in_offsets[s + 1] < in_offsets[s]) return BCGPU_ERR_INVALID_ARGUMENT;
+    if (in_offsets[nseg] > len) return BCGPU_ERR_TRUNCATED;
+    Piece pieces[kBatchPieces];
+    int K = 0;
+    uint64_t N = 0, cap = 0;
+    int st = cut_pieces(seg_n, nseg, pieces, &K, &N, &cap);
+    if (st) return st;
+    if ((N && !out) || (in_offsets[nseg] > in_offsets[0] && !bytes)) return BCGPU_ERR_INVALID_ARGUMENT;
+    DeviceGuard g(c->device);
+    const size_t o_in = 0, o_out = align_up(len + 16, 256), o_n = align_up(o_out + 4 * N, 256),
+                 o_base = align_up(o_n + 4 * nseg, 256), o_offs = align_up(o_base + 4 * nseg, 256),
+                 o_ds = align_up(o_offs + 8 * (nseg + 1), 256);
+    void* sp = nullptr;
+    st = scratch(c, o_ds + sizeof(bcgpu_decode_segment) * nseg + 256, &sp);
+    if (st) return st;
+    uint8_t* d = static_cast<uint8_t*>(sp);
+    uint8_t* d_in = d + o_in;
+    auto* d_out = reinterpret_cast<uint32_t*>(d + o_out);
+    auto* d_n = reinterpret_cast<uint32_t*>(d + o_n);
+    auto* d_base = reinterpret_cast<uint32_t*>(d + o_base);
+    auto* d_offs = reinterpret_cast<uint64_t*>(d + o_offs);
+    auto* d_ds = reinterpret_cast<bcgpu_decode_segment*>(d + o_ds);
+    cudaStream_t sc = c->stream, si = c->aux, so = c->aux2;
+    BatchArgs ba;
+    st = make_batch(c, sc, &ba);
+    if (st) return st;
+    cudaEvent_t* ev_in = c->bev;
+    cudaEvent_t* ev_done = c->bev + kBatchPieces;
+    BC_CUDA(cudaMemcpyAsync(d_n, seg_n, 4 * nseg, cudaMemcpyHostToDevice, si));
+    if (seg_base) BC_CUDA(cudaMemcpyAsync(d_base, seg_base, 4 * nseg, cudaMemcpyHostToDevice, si));
+    BC_CUDA(cudaMemcpyAsync(d_offs, in_offsets, 8 * (nseg + 1), cudaMemcpyHostToDevice, si));
+    for (int k = 0; k < K; ++k) {
+        const Piece& p = pieces[k];
+        const uint64_t lo = in_offsets[p.s0], hi = in_offsets[p.s1];
+        if (hi > lo) BC_CUDA(cudaMemcpyAsync(d_in + lo, bytes + lo, hi - lo, cudaMemcpyHostToDevice, si));
+        BC_CUDA(cudaEventRecord(ev_in[k], si));
+    }
+    for (int k = 0; k < K; ++k) {
+        const Piece& p = pieces[k];
+        const uint32_t m = (uint32_t)(p.s1 - p.s0);
+        BC_CUDA(cudaStreamWaitEvent(sc, ev_in[k], 0));
+        BC_CUDA(launch_batch_decode_describe(d_n, seg_base ? d_base : nullptr, d_offs, p.s0, m, p.i0, d_ds, sc));
+        BatchArgs bp = ba;
+        bp.max_seg_n = p.max_n ? p.max_n : 1u;
+        BC_CUDA(launch_decode_batch(d_ds + p.s0, m, d_in, d_out, delta, bp, sc));
+        g_launches.fetch_add(p.max_n <= kBatchSmallN ? 2 : 3);
+        BC_CUDA(cudaEventRecord(ev_done[k], sc));
+        BC_CUDA(cudaStreamWaitEvent(so, ev_done[k], 0));
+        if (p.i1 > p.i0)
+            BC_CUDA(cudaMemcpyAsync(out + p.i0, d_out + p.i0, 4 * (p.i1 - p.i0), cudaMemcpyDeviceToHost, so));
+    }
+    BC_CUDA(cudaStreamSynchronize(so));
+    st = bcgpu_ctx_sync_status(c, sc);
+    if (st) return st;
+    if (last) {  // decode_payload_delta's return value per segment (codec.hpp:89-90): the last value, or base
+        uint64_t at = 0;
+        for (size_t s = 0; s < nseg; ++s) {
+            at += seg_n[s];
+            last[s] = seg_n[s] ? out[at - 1] : (seg_base ? seg_base[s] : 0u);
+        }
+    }
     return BCGPU_OK;
 }
 

@@ -9,6 +9,7 @@
 #include <memory>
 #include <mutex>
 #include <cstddef>
+#include <stdexcept>
 #include <string>
 
 #include "bcgpu/bcgpu.h"
@@ -159,6 +160,42 @@ size_t svb_decode_block(std::span<const uint8_t> bytes, size_t n, size_t block, 
                                                 &cnt);
     if (st) throw_status(st, "svb_decode_block");
     return cnt;
+}
+
+svb_batch svb_encode_batch(std::span<const uint32_t> values, std::span<const uint32_t> seg_n,
+                           std::span<const uint32_t> seg_prev, bool delta) {
+    if (!seg_prev.empty() && seg_prev.size() != seg_n.size())
+        throw std::invalid_argument("svb_encode_batch: seg_prev must be empty or hold one base per segment");
+    size_t total = 0, cap = 0;
+    for (uint32_t n : seg_n) {
+        total += n;
+        cap += bcgpu_svb_max_compressed_bytes(n);
+    }
+    if (total != values.size()) throw std::invalid_argument("svb_encode_batch: sum(seg_n) != values.size()");
+    svb_batch b;
+    b.bytes.resize(cap);
+    b.offsets.resize(seg_n.size() + 1);
+    const int st = bcgpu_svb_encode_batch_host(ctx(), values.data(), seg_n.data(),
+                                               seg_prev.empty() ? nullptr : seg_prev.data(), seg_n.size(),
+                                               delta ? 1 : 0, b.bytes.data(), b.bytes.size(), b.offsets.data());
+    if (st) throw_status(st, "svb_encode_batch");
+    b.bytes.resize(b.offsets.back());
+    return b;
+}
+
+std::vector<uint32_t> svb_decode_batch(std::span<const uint8_t> bytes, std::span<const uint64_t> offsets,
+                                       std::span<const uint32_t> seg_n, std::span<const uint32_t> seg_base,
+                                       uint32_t* out, bool delta) {
+    if (offsets.size() != seg_n.size() + 1)
+        throw std::invalid_argument("svb_decode_batch: offsets must hold seg_n.size() + 1 entries");
+    if (!seg_base.empty() && seg_base.size() != seg_n.size())
+        throw std::invalid_argument("svb_decode_batch: seg_base must be empty or hold one base per segment");
+    std::vector<uint32_t> last(seg_n.size());
+    const int st = bcgpu_svb_decode_batch_host(ctx(), bytes.data(), bytes.size(), offsets.data(), seg_n.data(),
+                                               seg_base.empty() ? nullptr : seg_base.data(), seg_n.size(),
+                                               delta ? 1 : 0, out, last.data());
+    if (st) throw_status(st, "svb_decode_batch");
+    return last;
 }
 
 void svb_append(encoded_buffer& buf, uint32_t value) {

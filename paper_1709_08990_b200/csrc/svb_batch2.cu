@@ -20,6 +20,7 @@
 
 #include "svb_device.cuh"
 #include "svb_fast.cuh"
+#include "launch_cache.cuh"
 #include "svb_kernels.cuh"
 #include "svb_tma.cuh"
 #include "svb_warp.cuh"
@@ -274,18 +275,12 @@ __global__ void __launch_bounds__(kBThreads)
 
 cudaError_t launch_decode_batch2(const bcgpu_decode_segment* segs, uint64_t nseg, const uint8_t* in, uint32_t* out,
                                  int delta, const BatchArgs& ba, cudaStream_t stream) {
-    static int sms = 0, occ = 0;
-    if (!sms) {
-        int dev = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        int o1 = 0, o2 = 0;
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o1, svb_decode_batch2_kernel<true>, kBThreads, 0);
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o2, svb_decode_batch2_kernel<false>, kBThreads, 0);
-        occ = o1 < o2 ? o1 : o2;
-        if (occ > 4) occ = 4;  // cfg5 sweep: 4 CTAs per SM 2.02 ms, 5 (the occupancy limit) 2.06 ms
-        if (occ < 1) occ = 1;
-    }
+    const int sms = launch_sms(launch_current_device());
+    const int o1 = launch_occupancy(svb_decode_batch2_kernel<true>, kBThreads, 0);
+    const int o2 = launch_occupancy(svb_decode_batch2_kernel<false>, kBThreads, 0);
+    int occ = o1 < o2 ? o1 : o2;
+    if (occ > 4) occ = 4;  // cfg5 sweep: 4 CTAs per SM 2.02 ms, 5 (the occupancy limit) 2.06 ms
+    if (occ < 1) occ = 1;
     const uint32_t occ_cap = (ba.flags >> 12) & 7u;  // debug: CTAs per SM
     const uint64_t want = (nseg + kBWarps - 1) / kBWarps,
                    cap = (uint64_t)sms * (occ_cap && (int)occ_cap < occ ? (int)occ_cap : occ);

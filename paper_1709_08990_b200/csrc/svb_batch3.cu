@@ -23,6 +23,7 @@
 
 #include "svb_device.cuh"
 #include "svb_fast.cuh"
+#include "launch_cache.cuh"
 #include "svb_kernels.cuh"
 #include "svb_tma.cuh"
 #include "svb_warp.cuh"
@@ -405,35 +406,18 @@ __global__ void __launch_bounds__(kRThreads)
 
 cudaError_t launch_decode_batch3(const bcgpu_decode_segment* segs, uint64_t nseg, const uint8_t* in, uint32_t* out,
                                  int delta, const BatchArgs& ba, cudaStream_t stream) {
-    static int sms = 0, occ_default = 0;
-    static size_t attr_smem = 0;  // dynamic shared memory the kernels are currently allowed
     const uint32_t ring_kb = (ba.flags >> 16) & 0xFFu;  // debug: ring KiB per warp
     const uint32_t ring = ring_kb ? (ring_kb << 10 < kItemMax ? kItemMax : ring_kb << 10) : kRingDefault;
     const size_t smem = kRWarps * (sizeof(RWarpHdr) + ring + kRingSlack);
-    if (smem > attr_smem) {
-        cudaFuncSetAttribute(svb_decode_batch3_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        cudaFuncSetAttribute(svb_decode_batch3_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        attr_smem = smem;
-    }
-    auto occupancy = [&]() {
-        int o1 = 0, o2 = 0;
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o1, svb_decode_batch3_kernel<true>, kRThreads, smem);
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o2, svb_decode_batch3_kernel<false>, kRThreads, smem);
-        const int o = o1 < o2 ? o1 : o2;
-        return o < 1 ? 1 : o;
-    };
-    if (!sms) {
-        int dev = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    }
-    int occ;
-    if (ring == kRingDefault) {
-        if (!occ_default) occ_default = occupancy();
-        occ = occ_default;
-    } else {
-        occ = occupancy();
-    }
+    cudaError_t a = launch_ensure_smem(svb_decode_batch3_kernel<true>, smem);
+    if (a != cudaSuccess) return a;
+    a = launch_ensure_smem(svb_decode_batch3_kernel<false>, smem);
+    if (a != cudaSuccess) return a;
+    const int sms = launch_sms(launch_current_device());
+    const int o1 = launch_occupancy(svb_decode_batch3_kernel<true>, kRThreads, smem);
+    const int o2 = launch_occupancy(svb_decode_batch3_kernel<false>, kRThreads, smem);
+    int occ = o1 < o2 ? o1 : o2;
+    if (occ < 1) occ = 1;
     const uint32_t occ_cap = (ba.flags >> 12) & 7u;  // debug: CTAs per SM
     if (occ_cap && (int)occ_cap < occ) occ = (int)occ_cap;
     const uint64_t want = (nseg + kRWarps - 1) / kRWarps, cap = (uint64_t)sms * occ;
@@ -732,7 +716,10 @@ __global__ void __launch_bounds__(kRThreads)
             if (n == 0) {
                 if (lane == 0) out_lens[s_idx] = 0;
             } else if (!kSizes && piece == 0 && cap < (((uint64_t)n + 3) >> 2) + 4ull * n) {
-                if (lane == 0) report3(status, epoch, BCGPU_ERR_INVALID_ARGUMENT);
+                if (lane == 0) {  // nothing written: a zero length keeps callers that pack by out_lens in bounds
+                    out_lens[s_idx] = 0;
+                    report3(status, epoch, BCGPU_ERR_INVALID_ARGUMENT);
+                }
             } else {
                 m = piece + 1 < npieces ? pn : n - piece * pn;
                 const uintptr_t beg = (uintptr_t)(in + src + (uint64_t)piece * pn);
@@ -833,26 +820,19 @@ __global__ void __launch_bounds__(kRThreads)
 
 cudaError_t launch_encode_batch3(const bcgpu_encode_segment* segs, uint64_t nseg, const uint32_t* in, uint8_t* out,
                                  uint64_t* out_lens, int delta, const BatchArgs& ba, cudaStream_t stream, bool sizes) {
-    static int sms = 0;
-    static size_t attr_smem = 0;
     const uint32_t ring_kb = (ba.flags >> 24) & 0xFFu;  // debug: ring KiB per warp
     const uint32_t ring = ring_kb ? (ring_kb << 10 < kItemMax ? kItemMax : ring_kb << 10) : kERingDefault;
     const size_t smem = kRWarps * (sizeof(EWarpHdr) + ring + kRingSlack);
-    if (smem > attr_smem) {
-        cudaFuncSetAttribute(svb_encode_batch3_kernel<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        cudaFuncSetAttribute(svb_encode_batch3_kernel<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        cudaFuncSetAttribute(svb_encode_batch3_kernel<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        cudaFuncSetAttribute(svb_encode_batch3_kernel<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        attr_smem = smem;
+    const void* fns[4] = {(const void*)svb_encode_batch3_kernel<true, false>,
+                          (const void*)svb_encode_batch3_kernel<false, false>,
+                          (const void*)svb_encode_batch3_kernel<true, true>, (const void*)svb_encode_batch3_kernel<false, true>};
+    for (const void* f : fns) {
+        const cudaError_t a = launch_ensure_smem(f, smem);
+        if (a != cudaSuccess) return a;
     }
-    if (!sms) {
-        int dev = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    }
-    int o1 = 0, o2 = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o1, svb_encode_batch3_kernel<true, false>, kRThreads, smem);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o2, svb_encode_batch3_kernel<false, false>, kRThreads, smem);
+    const int sms = launch_sms(launch_current_device());
+    const int o1 = launch_occupancy(svb_encode_batch3_kernel<true, false>, kRThreads, smem);
+    const int o2 = launch_occupancy(svb_encode_batch3_kernel<false, false>, kRThreads, smem);
     int occ = o1 < o2 ? o1 : o2;
     if (occ < 1) occ = 1;
     const uint32_t occ_cap = (ba.flags >> 12) & 7u;  // debug: CTAs per SM

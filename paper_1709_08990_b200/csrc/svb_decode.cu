@@ -17,6 +17,7 @@
 
 #include "svb_device.cuh"
 #include "svb_fast.cuh"
+#include "launch_cache.cuh"
 #include "svb_kernels.cuh"
 #include "svb_tma.cuh"
 #include "svb_scan.cuh"
@@ -922,28 +923,14 @@ static cudaError_t launch_decode1(const uint8_t* in, uint64_t in_len, uint64_t n
     if (pool > 8ull * kWTDataMax + 64) pool = 8ull * kWTDataMax + 64;
     pool = (pool + 15) & ~15ull;
     const uint32_t smem = (uint32_t)(kD1Stages * (kCTWarps * kWTGroups + pool));
-    static int dev_cached = -1, sms = 0, coop = 0;
-    static uint32_t occ_smem = 0;
-    static int occ = 0;
-    int dev = 0;
-    cudaGetDevice(&dev);
-    if (dev != dev_cached) {
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, dev);
-        const cudaError_t a =
-            cudaFuncSetAttribute(svb_decode1_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
-        if (a != cudaSuccess) return a;
-        const cudaError_t a2 =
-            cudaFuncSetAttribute(svb_decode1_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
-        if (a2 != cudaSuccess) return a2;
-        dev_cached = dev;
-        occ_smem = 0;
-    }
-    if (!coop) return cudaSuccess;
-    if (smem != occ_smem) {
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, svb_decode1_kernel<false>, kSumThreads, smem);
-        occ_smem = smem;
-    }
+    const int dev = launch_current_device();
+    const int sms = launch_sms(dev);
+    if (!launch_coop(dev)) return cudaSuccess;
+    cudaError_t a = launch_ensure_smem(svb_decode1_kernel<false>, 220 * 1024);
+    if (a != cudaSuccess) return a;
+    a = launch_ensure_smem(svb_decode1_kernel<true>, 220 * 1024);
+    if (a != cudaSuccess) return a;
+    const int occ = launch_occupancy(svb_decode1_kernel<false>, kSumThreads, smem);
     if (occ < 1) return cudaSuccess;  // caller falls back to the sums + delta passes
     const uint64_t ngroups = (n + 3) >> 2;
     const uint64_t nsub = (ngroups + kWTGroups - 1) / kWTGroups;
@@ -1027,24 +1014,11 @@ static cudaError_t launch_sums(const uint8_t* in, uint64_t in_len, uint64_t n, c
     if (pool > 8ull * kWTDataMax + 64) pool = 8ull * kWTDataMax + 64;
     pool = (pool + 15) & ~15ull;
     const uint32_t smem = (uint32_t)(kSumStages * (kCTWarps * kWTGroups + pool));
-    static int dev_cached = -1, sms = 0;
-    static uint32_t occ_smem = 0;
-    static int occ = 0;
-    int dev = 0;
-    cudaGetDevice(&dev);
-    if (dev != dev_cached) {
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        const cudaError_t a = cudaFuncSetAttribute(svb_sums_kernel<kSumStages>,
-                                                   cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-        if (a != cudaSuccess) return a;
-        dev_cached = dev;
-        occ_smem = 0;
-    }
-    if (smem != occ_smem) {
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, svb_sums_kernel<kSumStages>, kSumThreads, smem);
-        if (occ < 1) occ = 1;
-        occ_smem = smem;
-    }
+    const int sms = launch_sms(launch_current_device());
+    const cudaError_t a = launch_ensure_smem(svb_sums_kernel<kSumStages>, 200 * 1024);
+    if (a != cudaSuccess) return a;
+    int occ = launch_occupancy(svb_sums_kernel<kSumStages>, kSumThreads, smem);
+    if (occ < 1) occ = 1;
     if (t_end <= t_begin) return cudaSuccess;
     uint64_t grid = (uint64_t)sms * (uint64_t)occ;
     if (grid > t_end - t_begin) grid = t_end - t_begin;
@@ -1091,8 +1065,7 @@ cudaError_t launch_decode_range(const uint8_t* in, uint64_t in_len, uint64_t n, 
     const int pgrid = (int)((sub_end - sub_begin + S - 1) / S);
 #define BC_POOL_LAUNCH(MODE, KK)                                                                                 \
     do {                                                                                                         \
-        static const cudaError_t a_ = cudaFuncSetAttribute(svb_decode_pool_kernel<MODE, KK>,                    \
-                                                           cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024); \
+        const cudaError_t a_ = launch_ensure_smem(svb_decode_pool_kernel<MODE, KK>, 200 * 1024);                \
         if (a_ != cudaSuccess) return a_;                                                                        \
         svb_decode_pool_kernel<MODE, KK><<<pgrid, kCTThreads, smem, stream>>>(in, in_len, n, base, out, d_last, m,  \
                                                                              (uint32_t)pool, sub_begin);        \

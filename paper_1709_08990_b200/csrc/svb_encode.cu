@@ -19,6 +19,7 @@
 
 #include "svb_device.cuh"
 #include "svb_fast.cuh"
+#include "launch_cache.cuh"
 #include "svb_kernels.cuh"
 #include "svb_scan.cuh"
 #include "svb_tma.cuh"
@@ -785,21 +786,17 @@ static cudaError_t launch_encode1(const uint32_t* in, uint64_t n, int delta, uin
     *used = false;
     if (((uintptr_t)in) & 15) return cudaSuccess;
     const uint32_t smem = (uint32_t)(kE1Stages * kE1Stride);
-    static int dev_cached = -1, sms = 0, coop = 0, occ = 0;
-    int dev = 0;
-    cudaGetDevice(&dev);
-    if (dev != dev_cached) {
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, dev);
-        const void* fns[4] = {(const void*)svb_encode1_kernel<true, false>, (const void*)svb_encode1_kernel<false, false>,
-                              (const void*)svb_encode1_kernel<true, true>, (const void*)svb_encode1_kernel<false, true>};
-        for (const void* f : fns) cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        int o1 = 0, o2 = 0;
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o1, svb_encode1_kernel<true, false>, kCTThreads + 32, smem);
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o2, svb_encode1_kernel<false, false>, kCTThreads + 32, smem);
-        occ = o1 < o2 ? o1 : o2;
-        dev_cached = dev;
+    const int dev = launch_current_device();
+    const int sms = launch_sms(dev), coop = launch_coop(dev);
+    const void* fns[4] = {(const void*)svb_encode1_kernel<true, false>, (const void*)svb_encode1_kernel<false, false>,
+                          (const void*)svb_encode1_kernel<true, true>, (const void*)svb_encode1_kernel<false, true>};
+    for (const void* f : fns) {
+        const cudaError_t a = launch_ensure_smem(f, smem);
+        if (a != cudaSuccess) return a;
     }
+    const int o1 = launch_occupancy(svb_encode1_kernel<true, false>, kCTThreads + 32, smem);
+    const int o2 = launch_occupancy(svb_encode1_kernel<false, false>, kCTThreads + 32, smem);
+    const int occ = o1 < o2 ? o1 : o2;
     if (!coop || occ < 1) return cudaSuccess;
     const uint64_t ngroups = (n + 3) >> 2;
     const uint64_t nsub = (ngroups + kWTGroups - 1) / kWTGroups;

@@ -89,6 +89,8 @@ typedef struct {
     uint32_t *out;
     uint32_t *chunk_sums;
     uint64_t n;
+    uint64_t i0;   /* global index of out[0] */
+    uint32_t base; /* x_{i0 - 1} + start: added to every element in pass 1 */
     int nthreads;
     int pass;
 } geo_ctx;
@@ -102,18 +104,17 @@ static inline uint32_t geo_gap(uint64_t seed, double inv_log_q, uint64_t i) {
 
 static void geo_fn(void *p, uint64_t lo, uint64_t hi) {
     geo_ctx *c = (geo_ctx *)p;
-    int t = (int)((lo * (uint64_t)c->nthreads + c->nthreads - 1) / (c->n ? c->n : 1));
-    (void)t;
     if (c->pass == 0) {
         uint32_t s = 0;
         for (uint64_t i = lo; i < hi; ++i) {
-            uint32_t g = (i == 0) ? 0 : geo_gap(c->seed, c->inv_log_q, i);
+            const uint64_t gi = c->i0 + i;
+            uint32_t g = (gi == 0) ? 0 : geo_gap(c->seed, c->inv_log_q, gi);
             s += g;
             c->out[i] = s; /* local inclusive sum */
         }
     } else {
         /* find the chunk index from lo (chunks are the same split as pass 0) */
-        uint32_t carry = 0;
+        uint32_t carry = c->base;
         for (int k = 0; k < c->nthreads; ++k) {
             uint64_t klo = c->n * (uint64_t)k / (uint64_t)c->nthreads;
             if (klo >= lo) break;
@@ -123,24 +124,69 @@ static void geo_fn(void *p, uint64_t lo, uint64_t hi) {
     }
 }
 
-void svbgen_geometric_sorted(uint64_t seed, uint64_t n, double mean_gap, uint32_t start, uint32_t *out,
-                             int nthreads) {
+static void geo_fill(uint64_t seed, uint64_t i0, uint64_t n, double mean_gap, uint32_t base, uint32_t *out,
+                     int nthreads) {
     if (nthreads < 1) nthreads = 1;
     if (n < 65536) nthreads = 1;
     if (nthreads > 256) nthreads = 256;
-    geo_ctx c = {seed, 1.0 / log(1.0 - 1.0 / mean_gap), out, NULL, n, nthreads, 0};
+    geo_ctx c = {seed, 1.0 / log(1.0 - 1.0 / mean_gap), out, NULL, n, i0, base, nthreads, 0};
     uint32_t sums[256];
     c.chunk_sums = sums;
     par_range(n, nthreads, geo_fn, &c);
     for (int k = 0; k < nthreads; ++k) {
         uint64_t hi = n * (uint64_t)(k + 1) / (uint64_t)nthreads;
-        sums[k] = hi ? out[hi - 1] : 0;
+        uint64_t lo = n * (uint64_t)k / (uint64_t)nthreads;
+        sums[k] = hi > lo ? out[hi - 1] : 0;
     }
-    /* pass 1 adds the sum of all earlier chunks' totals, plus start */
+    /* pass 1 adds the sum of all earlier chunks' totals, plus the base */
     c.pass = 1;
     par_range(n, nthreads, geo_fn, &c);
-    if (start)
-        for (uint64_t i = 0; i < n; ++i) out[i] += start;
+}
+
+void svbgen_geometric_sorted(uint64_t seed, uint64_t n, double mean_gap, uint32_t start, uint32_t *out,
+                             int nthreads) {
+    geo_fill(seed, 0, n, mean_gap, start, out, nthreads);
+}
+
+/* sum of gaps g_1 .. g_{i1-1} (mod 2^32), without storing them */
+typedef struct {
+    uint64_t seed;
+    double inv_log_q;
+    uint32_t part[256];
+    int nthreads;
+    uint64_t n;
+} gsum_ctx;
+
+static void gsum_fn(void *p, uint64_t lo, uint64_t hi) {
+    gsum_ctx *c = (gsum_ctx *)p;
+    uint32_t s = 0;
+    for (uint64_t i = lo; i < hi; ++i) s += i ? geo_gap(c->seed, c->inv_log_q, i) : 0u;
+    for (int k = 0; k < c->nthreads; ++k)
+        if (c->n * (uint64_t)k / (uint64_t)c->nthreads == lo) {
+            c->part[k] = s;
+            break;
+        }
+}
+
+/* Elements [i0, i0 + n) of the config-2/5 sequence x_0 = 0, x_i = x_{i-1} + g_i
+ * (identical to the same elements of svbgen_geometric_sorted(seed, N, mean, 0, ...)):
+ * one rank's shard of the sequence without generating the ranks before it. */
+void svbgen_geometric_sorted_range(uint64_t seed, uint64_t i0, uint64_t n, double mean_gap, uint32_t *out,
+                                   int nthreads) {
+    if (nthreads < 1) nthreads = 1;
+    if (nthreads > 256) nthreads = 256;
+    uint32_t carry = 0;
+    if (i0) {
+        gsum_ctx g;
+        g.seed = seed;
+        g.inv_log_q = 1.0 / log(1.0 - 1.0 / mean_gap);
+        g.n = i0;
+        g.nthreads = i0 < 65536 ? 1 : nthreads;
+        for (int k = 0; k < 256; ++k) g.part[k] = 0;
+        par_range(i0, g.nthreads, gsum_fn, &g);
+        for (int k = 0; k < g.nthreads; ++k) carry += g.part[k];
+    }
+    geo_fill(seed, i0, n, mean_gap, carry, out, nthreads);
 }
 
 /* ---- config 4: posting-list-like batch --------------------------------
@@ -181,6 +227,7 @@ typedef struct {
     const uint64_t *offsets;
     uint32_t universe;
     uint32_t *out;
+    uint64_t list_base; /* global index of lens[0] */
 } lists_ctx;
 
 static void lists_fn(void *p, uint64_t lo, uint64_t hi) {
@@ -188,7 +235,7 @@ static void lists_fn(void *p, uint64_t lo, uint64_t hi) {
     for (uint64_t li = lo; li < hi; ++li) {
         uint32_t L = c->lens[li];
         uint32_t *o = c->out + c->offsets[li];
-        uint64_t stream = mix64(c->seed ^ (0xA0761D6478BD642Full * (li + 1)));
+        uint64_t stream = mix64(c->seed ^ (0xA0761D6478BD642Full * (c->list_base + li + 1)));
         /* L+1 exponential spacings; cumulative sums normalised */
         double total = 0.0;
         for (uint32_t j = 0; j <= L; ++j) total += -log(unit_open0(svbgen_splitmix64(stream, j)));
@@ -205,6 +252,14 @@ static void lists_fn(void *p, uint64_t lo, uint64_t hi) {
 
 void svbgen_posting_lists(uint64_t seed, uint64_t nlists, const uint32_t *lens, const uint64_t *offsets,
                           uint32_t universe, uint32_t *out, int nthreads) {
-    lists_ctx c = {seed, lens, offsets, universe, out};
+    lists_ctx c = {seed, lens, offsets, universe, out, 0};
     par_range(nlists, nthreads, lists_fn, &c);
+}
+
+/* Lists [l0, l0 + m) only (one rank's shard): lens / offsets describe those m lists
+ * (offsets relative to out); identical to the same lists of svbgen_posting_lists. */
+void svbgen_posting_lists_range(uint64_t seed, uint64_t l0, uint64_t m, const uint32_t *lens,
+                                const uint64_t *offsets, uint32_t universe, uint32_t *out, int nthreads) {
+    lists_ctx c = {seed, lens, offsets, universe, out, l0};
+    par_range(m, nthreads, lists_fn, &c);
 }

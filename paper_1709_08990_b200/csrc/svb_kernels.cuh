@@ -119,6 +119,14 @@ cudaError_t launch_encode_batch3(const bcgpu_encode_segment* segs, uint64_t nseg
                                  uint64_t* out_lens, int delta, const BatchArgs& ba, cudaStream_t stream,
                                  bool sizes = false);
 
+// host-buffer batches (svb_batch_host.cu): one CTA per piece of segments [s0, s0 + m)
+cudaError_t launch_batch_encode_describe(const uint32_t* seg_n, const uint32_t* seg_prev, uint64_t s0, uint32_t m,
+                                         uint64_t elem_base, bcgpu_encode_segment* es, cudaStream_t stream);
+cudaError_t launch_batch_pack(const uint64_t* sizes, uint64_t s0, uint32_t m, bcgpu_encode_segment* es,
+                              uint64_t* out_offsets, unsigned long long* running, cudaStream_t stream);
+cudaError_t launch_batch_decode_describe(const uint32_t* seg_n, const uint32_t* seg_base, const uint64_t* in_offsets,
+                                         uint64_t s0, uint32_t m, uint64_t elem_base, bcgpu_decode_segment* ds,
+                                         cudaStream_t stream);
 
 // Control bytes per look-back tile of the block-offsets kernel.
 constexpr uint32_t kOffsetsTileGroups = 2048;

@@ -164,6 +164,35 @@ int main() {
             CHECK(e.code() == errc::truncated);
         }
     }
+    {  // batch extension: one call == a loop of svb_encode_delta / svb_decode_delta per segment
+        std::mt19937 rng(11);
+        const std::vector<uint32_t> seg_n = {0, 1, 17, 4000, 3, 70000, 128, 0, 1921};
+        std::vector<uint32_t> vals, prev;
+        uint32_t acc = 0;
+        for (uint32_t n : seg_n) {
+            prev.push_back(acc);
+            for (uint32_t i = 0; i < n; ++i) vals.push_back(acc += rng() % 3000);
+        }
+        const svb_batch b = svb_encode_batch(vals, seg_n, prev);
+        size_t at = 0;
+        for (size_t s = 0; s < seg_n.size(); ++s) {
+            const std::vector<uint32_t> seg(vals.begin() + at, vals.begin() + at + seg_n[s]);
+            const auto one = svb_encode_delta(seg, prev[s]);
+            CHECK(std::vector<uint8_t>(b.bytes.begin() + b.offsets[s], b.bytes.begin() + b.offsets[s + 1]) == one);
+            at += seg_n[s];
+        }
+        std::vector<uint32_t> out(vals.size());
+        const auto last = svb_decode_batch(b.bytes, b.offsets, seg_n, prev, out.data());
+        CHECK(out == vals && last.size() == seg_n.size() && last[0] == prev[0] && last[5] == vals[4000 + 1 + 17 + 3 + 70000 - 1]);
+        auto cut = b.bytes;
+        cut.resize(cut.size() - 1);
+        try {
+            svb_decode_batch(cut, b.offsets, seg_n, prev, out.data());
+            CHECK(false);
+        } catch (const codec_error& e) {
+            CHECK(e.code() == errc::truncated);
+        }
+    }
     if (failures) {
         std::fprintf(stderr, "%d failures\n", failures);
         return 1;

@@ -367,13 +367,26 @@ def test_config3_full_roundtrip(dev):
     assert torch.equal(d_o, d_v)
 
 
+def _slot_bytes(buf, eoff, lens, a, b):
+    """Concatenated stream bytes of segments [a, b) of a worst-case-slot layout
+    (segment s at eoff[s], lens[s] bytes)."""
+    ln = lens[a:b].astype(np.int64)
+    pk = np.zeros(b - a, np.int64)
+    np.cumsum(ln[:-1], out=pk[1:])
+    idx = np.arange(int(ln.sum()), dtype=np.int64) + np.repeat(eoff[a:b].astype(np.int64) - pk, ln)
+    return buf[idx]
+
+
 @pytest.mark.slow
 @pytest.mark.parametrize("cfg", [4, 5])
-def test_batch_full_config(dev, cfg):
+def test_batch_full_config(P, dev, cfg):
     """Full BASELINE.json sizes of the batch configs (cfg4: 1M posting lists, ~2^30 integers;
-    cfg5: 2^31 integers in 64K-integer chunks with chained prev seeds): the batch encode ->
-    decode round trip is exact on the device, every segment's stream length equals the size
-    identity, and 256 sampled segments' streams equal the oracle's bytes."""
+    cfg5: 2^31 integers in 64K-integer chunks with chained prev seeds), EVERY segment:
+    - the device batch kernels (bench's timed path, worst-case slots): each segment's stream
+      length and bytes equal oracle.encode_batch's, the total compressed size too, and the
+      device decode round trip is exact;
+    - the host batch C-ABI (packed streams): the same bytes back to back, offsets = the
+      exclusive scan of the oracle's lengths, and its decode returns the input."""
     import torch
 
     import bench
@@ -382,14 +395,25 @@ def test_batch_full_config(dev, cfg):
     wl.decode()
     torch.cuda.synchronize()
     wl.verify(torch)
-    lens = wl.d_lens.cpu().numpy().astype(np.uint64)
-    caps = (wl.lens.astype(np.uint64) + 3) // 4 + 4 * wl.lens.astype(np.uint64)
-    eoff = np.zeros(wl.nseg + 1, np.uint64)
-    np.cumsum(caps, out=eoff[1:])
-    rng = np.random.default_rng(cfg)
-    for i in sorted(rng.choice(wl.nseg, 256, replace=False)):
-        seg = wl.values[int(wl.offs[i]):int(wl.offs[i + 1])]
-        want = oracle.encode(seg, delta=True, prev=int(wl.prevs[i]))
-        assert int(lens[i]) == len(want) == oracle.compressed_size(seg, delta=True, prev=int(wl.prevs[i])), i
-        got = wl.d_c[int(eoff[i]):int(eoff[i]) + int(lens[i])].cpu().numpy().tobytes()
-        assert got == want, i
+    es, eoff = wl.host_segments()
+    want = np.zeros(int(eoff[-1]) + 16, np.uint8)
+    lens = np.zeros(wl.nseg, np.uint64)
+    assert oracle.encode_batch(es, wl.values, want, lens, True) == oracle.OK
+    assert np.array_equal(wl.enc_lens, lens), "a segment's stream length differs from the oracle's"
+    assert wl.cmp == int(lens.sum())
+    got = wl.d_c.cpu().numpy()
+    wl.release()
+    torch.cuda.empty_cache()
+    step = 4096
+    for a in range(0, wl.nseg, step):
+        b = min(wl.nseg, a + step)
+        assert np.array_equal(_slot_bytes(got, eoff, lens, a, b), _slot_bytes(want, eoff, lens, a, b)), (a, b)
+    del got
+    packed, offs = P.svb_encode_batch(wl.values, wl.lens, wl.prevs)
+    assert offs[0] == 0 and np.array_equal(np.diff(offs), lens)
+    for a in range(0, wl.nseg, step):
+        b = min(wl.nseg, a + step)
+        assert np.array_equal(packed[int(offs[a]):int(offs[b])], _slot_bytes(want, eoff, lens, a, b)), (a, b)
+    del want
+    dec = P.svb_decode_batch(packed, offs, wl.lens, wl.prevs)
+    assert np.array_equal(dec, wl.values)

@@ -1,7 +1,8 @@
 """Multi-GPU sharding host logic on CPU: cost-balanced contiguous
-segment ranges, and a world_size-2 gloo run where every rank handles its shard
-and the root gathers -- the same code path bench.py uses with NCCL on the box.
-The per-segment codec here is the CPU oracle (test infrastructure)."""
+segment ranges, and a world_size-2 gloo run where every rank generates and codes
+its own shard (bench.Batch) and the root gathers -- the same code path bench.py
+uses with NCCL on the box.  The per-segment codec here is the CPU oracle (test
+infrastructure); tests/test_multirank_gpu.py runs the product kernels."""
 import os
 import socket
 
@@ -45,28 +46,27 @@ def _free_port() -> int:
     return port
 
 
-def _worker(rank, world, port, results):
+def _worker(rank, world, port, results, cfg=4, scale=0.0005):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
-    from paper_1709_08990_b200 import gen
-    lb = gen.posting_lists(400, 4, cap_total=400 * 500)
-    lists = [lb.values[int(lb.offsets[i]):int(lb.offsets[i + 1])] for i in range(400)]
-    lo, hi = partition_by_cost(lb.lengths.astype(np.float64) * 6.0, world)[rank]
-    # this rank's shard: encode + decode every segment of its range (no data-path collective)
-    enc = b"".join(oracle.encode(v, delta=True) for v in lists[lo:hi])
-    dec = []
-    pos = 0
-    for v in lists[lo:hi]:
-        m = oracle.compressed_size(v, delta=True)
-        st, out, _ = oracle.decode(enc[pos:pos + m], v.size, delta=True)
-        assert st == oracle.OK
-        dec.append(out)
-        pos += m
-    mine = torch.from_numpy(np.concatenate(dec).view(np.int32) if dec else np.zeros(0, np.int32))
+    import bench
+    # this rank generates and codes only its own shard (bench.Batch), no data-path collective
+    wl = bench.Batch(cfg, rank, world, scale)
+    es, eoff = wl.host_segments()
+    enc = np.zeros(int(eoff[-1]) + 16, np.uint8)
+    lens = np.zeros(wl.nseg, np.uint64)
+    oracle.encode_batch(es, wl.values, enc, lens, True)
+    ds = np.zeros(wl.nseg, bench.DECODE_SEG_DTYPE)
+    ds["src_offset"], ds["src_bytes"], ds["dst_offset"] = eoff[:-1], lens, wl.offs[:-1]
+    ds["n"], ds["prev"] = wl.lens, wl.prevs
+    out = np.zeros(max(1, wl.n), np.uint32)
+    assert oracle.decode_batch(ds, enc, out, True) == oracle.OK
+    mine = torch.from_numpy(out[:wl.n].view(np.int32).copy())
     shards = gather_to_root(mine, world, rank)
     if rank == 0:
+        whole = bench.Batch(cfg, 0, 1, scale)
         full = torch.cat(shards).numpy().view(np.uint32)
-        results.put(bool(np.array_equal(full, lb.values)))
+        results.put(bool(np.array_equal(full, whole.values)))
     dist.barrier()
     dist.destroy_process_group()
 
