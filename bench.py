@@ -770,6 +770,9 @@ def run_gpu(args):
         if dst.rank == 0 and dst.world == 1 and not args.no_cpu:
             r["cpu_baseline"] = cpu_baseline(wl, args)
         results[name] = r
+        if dst.rank == 0:
+            print(f"[bench] {name}: {json.dumps({k: r.get(k) for k in ('value', 'phases', 'e2e')})}", file=sys.stderr,
+                  flush=True)
         wl.release()
         del wl
         torch.cuda.synchronize()

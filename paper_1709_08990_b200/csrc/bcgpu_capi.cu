@@ -921,7 +921,7 @@ int bcgpu_svb_encode_batch_host(bcgpu_ctx* c, const uint32_t* values, const uint
         const Piece& p = pieces[k];
         const uint32_t m = (uint32_t)(p.s1 - p.s0);
         BC_CUDA(cudaStreamWaitEvent(sc, ev_in[k], 0));
-        BC_CUDA(launch_batch_encode_describe(d_n, seg_prev ? d_prev : nullptr, p.s0, m, 0, d_es, sc));
+        BC_CUDA(launch_batch_encode_describe(d_n, seg_prev ? d_prev : nullptr, p.s0, m, p.i0, d_es, sc));
         BC_CUDA(launch_sizes_batch(d_es + p.s0, m, d_vals, d_sz + p.s0, delta, ba, sc));
         BC_CUDA(launch_batch_pack(d_sz, p.s0, m, d_es, d_offs, d_run, sc));
         BC_CUDA(launch_encode_batch(d_es + p.s0, m, d_vals, d_out, d_sz + p.s0, delta, ba, sc));
