@@ -214,6 +214,8 @@ int bcgpu_debug_set_trace(bcgpu_ctx* c, void* d_trace) {
 //   16      encode: two-read path (size scan + tile encode)
 //   32      encode: slot path (bits 6-7: its L2 policies)
 //   2048    encode: never the one-pass kernel;   4096  encode: one-pass for plain streams too
+//   0x80000 encode: plain streams take the two-read path (size scan + tile encode)
+//   0x100000 encode: delta streams take the scanner one-pass kernel (plain streams always do)
 //   512     host API: no piecewise pipelining
 //   1024    decode: sums pass + pooled delta decode instead of the one-pass kernel
 //   0x8000  decode: the control scan only (dev timing; output not written)
@@ -367,8 +369,10 @@ int bcgpu_svb_encode_device(bcgpu_ctx* c, const uint32_t* d_in, size_t n, int de
     // one-pass for delta streams (cfg2: 76 us vs 99 slot / 108 two-read); wide plain data is
     // compute-bound and runs faster through the 4-CTA/SM two-read kernels (cfg3: 646 vs 819 us).
     // Debug flags: 16 two-read, 32 slots, 2048 no one-pass, 4096 one-pass for plain too.
+    // one pass for every 16-B aligned input (cfg3 plain: 472 us one-pass vs 552 us two-read);
+    // debug flag 0x80000 restores the two-read path for plain streams
     const bool one_pass = !(c->debug_flags & (16 | 32 | 2048)) && (((uintptr_t)d_in) & 15) == 0 &&
-                          (delta || (c->debug_flags & 4096));
+                          (delta || !(c->debug_flags & 0x80000) || (c->debug_flags & 4096));
     if (one_pass) {
         // the one-pass encode's tile aggregates must not hold this epoch's tag: true when the
         // workspace was last laid out for this n (older epochs only), else clear them
@@ -378,6 +382,7 @@ int bcgpu_svb_encode_device(bcgpu_ctx* c, const uint32_t* d_in, size_t n, int de
             BC_CUDA(cudaMemsetAsync(agg, 0, cnt * sizeof(unsigned long long), s));
         }
         hints |= 0x100;
+        if (c->debug_flags & 0x100000) hints |= 0x200;  // delta streams through the scanner kernel too
     } else {
         st = ensure_slots(c, n, delta, s, &slots);
         if (st) return st;

@@ -25,6 +25,7 @@
 #include "svb_fast.cuh"
 #include "launch_cache.cuh"
 #include "svb_kernels.cuh"
+#include "svb_pack.cuh"
 #include "svb_tma.cuh"
 #include "svb_warp.cuh"
 
@@ -550,6 +551,29 @@ __device__ __forceinline__ void encode_block(uint32_t Sin, uint32_t blk, uint32_
         off += 384;
         // the piece's last group: its bytes in the word after it (lane 31's W1, now in carry)
         if (blk + 3 == rows && u8 != 0 && lane == 0) sts32((db + off) & ~3u, carry);
+        return;
+    }
+    if constexpr (kFB) {
+        // full block: control bytes, one packed scan, then the branch-free word pack (svb_pack.cuh)
+        uint32_t C3[3], P3 = 0;
+#pragma unroll
+        for (int j = 0; j < 3; ++j) {
+            uint32_t tot;
+            C3[j] = group_ctrl(d[j], tot);
+            sts8(cb + 32 * (blk + j) + lane, C3[j]);
+            P3 |= tot << (10 * j);
+        }
+        const uint32_t I3 = warp_inclusive_scan(P3);
+        const uint32_t T3 = __shfl_sync(0xffffffffu, I3, 31), E3 = I3 - P3;
+        __syncwarp();  // every lane has read the block's integers before any lane packs over them
+#pragma unroll
+        for (int j = 0; j < 3; ++j) {
+            const uint32_t o = db + off + ((E3 >> (10 * j)) & 0x3FFu);
+            off += (T3 >> (10 * j)) & 0x3FFu;
+            pack_group_row(d[j], C3[j], o, carry);
+        }
+        // the piece's last group leaves its partial word (now in carry)
+        if ((blk + 3) * 32 >= ng && lane == 0 && ((db + off) & 3u)) sts32((db + off) & ~3u, carry);
         return;
     }
     uint32_t L4[3], P = 0;

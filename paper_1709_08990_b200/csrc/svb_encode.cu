@@ -21,6 +21,7 @@
 #include "svb_fast.cuh"
 #include "launch_cache.cuh"
 #include "svb_kernels.cuh"
+#include "svb_pack.cuh"
 #include "svb_scan.cuh"
 #include "svb_tma.cuh"
 #include "svb_warp.cuh"
@@ -553,32 +554,36 @@ __global__ void __launch_bounds__(kCTThreads)
 // Replaces slot encode + compaction (or size scan + tile encode): the integers are
 // read once and the compressed bytes written once, straight to their final place.
 // Persistent CTAs (cooperative launch: all co-resident) take tiles t = b, b + G, ...
-// A producer warp TMA-loads each tile's 8192 integers (+ the 4 before them) into a
-// 3-stage ring.  For tile t (round r) the 8 consumer warps
-//   1. size their sub-tiles (all-small shortcut as above), write the control bytes
-//      to their final place (their position does not depend on any data size),
-//      pack the data bytes in place at phase 0, and publish the tile's data size
-//      A(t) as an epoch-tagged aggregate;
-//   2. resolve the data offset of the CTA's previous tile tp = t - G one round
-//      later -- own inclusive offset from two rounds back + the aggregates of the
-//      G - 1 tiles in between (loads issued early) -- and store its packed bytes
-//      from smem, realigned to the destination's 16-B phase (funnel shifts,
-//      128-bit stores), then release its stage.
-// No CTA waits on a tile of its own round (see svb_decode1_kernel).
+// Warps 0-7 (consumers) own one 1024-integer sub-tile of every tile; warp 8 (producer)
+// TMA-loads each tile's 8192 integers (+ the 4 before them) into a 3-stage ring; warp 9
+// (scanner) does the tile-level bookkeeping, so the consumers never wait on each other:
+//   consumers, round r (tile t): size their sub-tile, write its control bytes to their
+//     final place (their position depends on no data size), pack the data at phase 0 in
+//     place, post the sub-tile size (mbarrier `sizes`); then store the PREVIOUS tile
+//     tp = t - G once the scanner has posted its data offset (mbarrier `carried`):
+//     realigned to the destination's 16-B phase, and release its stage;
+//   scanner, round r: resolve tp's offset -- its own inclusive offset from the round
+//     before + the epoch-tagged aggregates of the G - 1 tiles in between, published by
+//     the other CTAs' scanners at least a round earlier -- post it, then wait for tile
+//     t's eight sizes and publish t's aggregate.
+// Round-r aggregates depend only on rounds < r, so once every CTA is resident there
+// is no cycle; a consumer only waits when the scanner's look-back is slower than its
+// own sizing + packing of the next tile.
 constexpr int kE1Stages = 3;
-constexpr uint32_t kE1Ints = kCTWarps * kWTInts;                          // 8192 per tile
-constexpr uint32_t kE1Stride = 16 + kE1Ints * 4 + 16 + kCTWarps * kWTGroups;  // prefix, tile, slack, ctrl
+constexpr uint32_t kE1Ints = kCTWarps * kWTInts;           // 8192 per tile
+constexpr uint32_t kE1Stride = 16 + kE1Ints * 4 + 16;       // prefix, tile, slack
+constexpr int kE1Threads = kCTThreads + 64;                 // consumers, producer, scanner
+constexpr int kE1Producer = kCTWarps, kE1Scanner = kCTWarps + 1;
 
 struct __align__(16) E1Shared {
     uint64_t full[kE1Stages], empty[kE1Stages];
-    uint32_t wsum[3][kCTWarps];
-    uint32_t wpre[kCTWarps];  // exclusive prefix of the resolved tile's sub-tile sizes
-    uint32_t red[kCTWarps];
-    unsigned long long carry, incl;
+    uint64_t sizes[3], carried[3];    // per tile slot (round % 3)
+    uint32_t wsum[3][kCTWarps];       // sub-tile data sizes of the slot's tile
+    unsigned long long carry[3];      // data offset of the slot's tile
 };
 
 template <bool kDelta, bool kTrace>
-__global__ void __launch_bounds__(kCTThreads + 32, 2)
+__global__ void __launch_bounds__(kE1Threads, 2)
     svb_encode1_kernel(const uint32_t* __restrict__ in, uint64_t n, uint32_t prev, uint8_t* __restrict__ out,
                        DecodeMeta meta, uint64_t* __restrict__ d_out_len, unsigned long long* status, uint32_t epoch) {
     extern __shared__ __align__(128) uint8_t dsm[];
@@ -595,6 +600,259 @@ __global__ void __launch_bounds__(kCTThreads + 32, 2)
             mbar_init(&sh.full[k], 1);
             mbar_init(&sh.empty[k], kCTWarps);
         }
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+            mbar_init(&sh.sizes[k], kCTWarps);
+            mbar_init(&sh.carried[k], 1);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    if (warp == kE1Producer) {
+        // ---- producer: the tile's integers (and the 4 before them) -> stage ----
+        const uintptr_t lo = (uintptr_t)in, hi = lo + 4 * n;
+        uint32_t k = 0, ph = 0;
+        int st = 0;
+        for (uint32_t t = blockIdx.x; t < ntiles; t += G, ++k, st = st + 1 == kE1Stages ? 0 : st + 1, ph ^= st == 0) {
+            uint8_t* stage = dsm + (uint32_t)st * kE1Stride;
+            if (k >= (uint32_t)kE1Stages) mbar_wait_parity_lazy(&sh.empty[st], ph ^ 1u, 512);
+            const uint64_t i0 = (uint64_t)t * kE1Ints;
+            const uint64_t cnt = n - i0 < (uint64_t)kE1Ints ? n - i0 : (uint64_t)kE1Ints;
+            const uintptr_t beg = (uintptr_t)(in + i0) - (t ? 16 : 0), end = (uintptr_t)(in + i0 + cnt);
+            uint8_t* dst = stage + (t ? 0 : 16);
+            const uint32_t tx = tma_cover_bytes(beg, end, lo, hi);
+            if (tx != 0xFFFFFFFFu && tx) {
+                if (lane == 0) {
+                    fence_async_smem();
+                    mbar_expect(&sh.full[st], tx);
+                    if (kTrace) meta.trace[8ull * t + 0] = gtimer();
+                    tma_load_hint(dst, reinterpret_cast<const void*>(beg), tx, &sh.full[st], l2_policy_drop());
+                }
+            } else {
+                uint32_t* d32 = reinterpret_cast<uint32_t*>(dst);
+                const uint32_t words = (uint32_t)((end - beg) >> 2);
+                for (uint32_t i = lane; i < words; i += 32) d32[i] = __ldg(reinterpret_cast<const uint32_t*>(beg) + i);
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&sh.full[st]);
+            }
+        }
+        return;
+    }
+    if (warp == kE1Scanner) {
+        // ---- scanner: tile offsets (deferred look-back) and tile aggregates ----
+        unsigned long long incl = 0;  // inclusive data offset of the CTA's last resolved tile
+        uint32_t aprev = 0;           // aggregate of tprev
+        auto entry = [&](uint32_t j, unsigned long long v) -> uint32_t {
+            while ((uint32_t)(v >> 32) != epoch) v = ld_relaxed_u64(meta.agg + j);
+            return (uint32_t)v;
+        };
+        // window of tile tp: tiles wl .. tp - 1 lie between the CTA's own tiles tp - G and tp;
+        // read as 16-B aligned pairs, 8 per lane (512 tiles) issued before the wait for the
+        // current tile's sizes, so the L2 round trip overlaps the consumers' work
+        ulonglong2 v[8];
+        auto issue = [&](uint32_t tp) {
+            const uint32_t wl = tp + 1 > G ? tp + 1 - G : 0u;
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                const uint32_t e = (wl & ~1u) + 64 * u + 2 * lane;
+                v[u] = e < tp ? ld_relaxed_u64x2(meta.agg + e) : make_ulonglong2(0ull, 0ull);
+            }
+        };
+        auto resolve = [&](uint32_t tp, int q) {
+            const uint32_t wl = tp + 1 > G ? tp + 1 - G : 0u;
+            uint32_t part = 0;
+            for (uint32_t e0 = (wl & ~1u); e0 < tp; e0 += 512) {
+                if (e0 != (wl & ~1u)) {  // windows beyond 512 tiles (G > 513)
+#pragma unroll
+                    for (int u = 0; u < 8; ++u) {
+                        const uint32_t e = e0 + 64 * u + 2 * lane;
+                        v[u] = e < tp ? ld_relaxed_u64x2(meta.agg + e) : make_ulonglong2(0ull, 0ull);
+                    }
+                }
+#pragma unroll
+                for (int u = 0; u < 8; ++u) {
+                    const uint32_t e = e0 + 64 * u + 2 * lane;
+                    if (e < tp && e >= wl) part += entry(e, v[u].x);
+                    if (e + 1 < tp && e + 1 >= wl) part += entry(e + 1, v[u].y);
+                }
+            }
+            part = __reduce_add_sync(kFull, part);
+            const unsigned long long c = (tp >= G ? incl : 0ull) + part;  // data offset of tile tp
+            incl = c + aprev;
+            if (lane == 0) {
+                sh.carry[q] = c;
+                mbar_arrive(&sh.carried[q]);
+                if (kTrace) meta.trace[8ull * tp + 4] = gtimer();
+                if (tp == ntiles - 1) {
+                    if (d_out_len) *d_out_len = ngroups + incl;
+                    if (status) *status = ((unsigned long long)epoch << 32);
+                }
+            }
+        };
+        // round k: issue the previous tile's window loads, publish tile t's aggregate as soon
+        // as its eight sizes are posted, then resolve the previous tile while the consumers
+        // pack tile t (its window's aggregates are from rounds <= k - 1)
+        uint32_t k = 0, tprev = 0;
+        int q = 0, qp = 0;
+        for (uint32_t t = blockIdx.x; t < ntiles; t += G, ++k, qp = q, q = q == 2 ? 0 : q + 1) {
+            if (k) issue(tprev);
+            mbar_wait_parity_lazy(&sh.sizes[q], (k / 3) & 1u, 512);  // ~a round of consumer work
+            uint32_t a = lane < kCTWarps ? sh.wsum[q][lane] : 0u;
+            a = __reduce_add_sync(kFull, a);
+            if (lane == 0) {
+                st_relaxed_u64(meta.agg + t, ((unsigned long long)epoch << 32) | a);
+                if (kTrace) meta.trace[8ull * t + 3] = gtimer();
+            }
+            if (k) resolve(tprev, qp);
+            aprev = a;
+            tprev = t;
+        }
+        if (k) {
+            issue(tprev);
+            resolve(tprev, qp);
+        }
+        return;
+    }
+    // ---- consumers ----
+    auto store_prev = [&](uint32_t tp, int st, int q, uint32_t kk) {
+        if (kTrace && threadIdx.x == 0) meta.trace[8ull * tp + 6] = gtimer();
+        if (!mbar_test_parity(&sh.carried[q], (kk / 3) & 1u)) mbar_wait_parity_lazy(&sh.carried[q], (kk / 3) & 1u, 128);
+        if (kTrace && threadIdx.x == 0) meta.trace[8ull * tp + 7] = gtimer();
+        const uint64_t s = (uint64_t)tp * kCTWarps + warp;
+        if (s < nsub) {
+            uint32_t pre = 0;
+#pragma unroll
+            for (int w = 0; w < kCTWarps; ++w) pre += w < warp ? sh.wsum[q][w] : 0u;
+            const uint32_t src = sh_addr(dsm) + (uint32_t)st * kE1Stride + 16 + (uint32_t)warp * (kWTInts * 4);
+            store_realigned2(src, sh.wsum[q][warp], out + ngroups + sh.carry[q] + pre);
+        }
+        __syncwarp();
+        if (lane == 0) {
+            if (kTrace && warp == 0) meta.trace[8ull * tp + 5] = gtimer();
+            mbar_arrive(&sh.empty[st]);
+        }
+    };
+
+    uint32_t k = 0, tprev = 0, ph = 0;
+    int st = 0, q = 0, stp = 0, qp = 0;  // stage / tile slot of this iteration and of the previous one
+    for (uint32_t t = blockIdx.x; t < ntiles;
+         t += G, ++k, stp = st, qp = q, st = st + 1 == kE1Stages ? 0 : st + 1, q = q == 2 ? 0 : q + 1, ph ^= st == 0) {
+        if (kTrace && threadIdx.x == 0) meta.trace[8ull * t + 1] = gtimer();
+        mbar_wait_parity(&sh.full[st], ph);
+        if (kTrace && threadIdx.x == 0) meta.trace[8ull * t + 2] = gtimer();
+        uint8_t* stage = dsm + (uint32_t)st * kE1Stride;
+        const uint64_t s = (uint64_t)t * kCTWarps + warp;
+        const uint64_t g0 = s * kWTGroups;
+        auto post = [&](uint32_t total) {  // the sub-tile's data size -> the scanner
+            if (lane == 0) {
+                sh.wsum[q][warp] = total;
+                mbar_arrive(&sh.sizes[q]);
+            }
+        };
+        if (g0 < ngroups) {
+            const uint32_t sin = sh_addr(stage) + 16 + (uint32_t)warp * (kWTInts * 4);
+            const uint32_t prev_w = warp ? lds32(sin - 4) : (t ? lds32(sh_addr(stage) + 12) : prev);
+            uint8_t* cdst = out + g0;
+            if ((s + 1) * kWTInts <= n) {
+                // delta streams of sorted ids are mostly all-small: check that first
+                const bool small = kDelta && enc_full_small<kDelta>(sin, prev_w);
+                if (small) {
+                    post(kWTInts);
+                    if ((((uintptr_t)cdst) & 15) == 0) {  // 256 zero control bytes
+                        if (lane < (int)(kWTGroups / 16)) reinterpret_cast<uint4*>(cdst)[lane] = make_uint4(0, 0, 0, 0);
+                    } else {
+                        for (uint32_t i = lane; i < kWTGroups; i += 32) cdst[i] = 0;
+                    }
+                    enc_full_small_pack0<kDelta>(sin, prev_w, sin);
+                } else {
+                    // control bytes straight to the stream, the size posted, then the
+                    // branch-free word pack at phase 0 in place (svb_pack.cuh)
+                    uint32_t cw[2], qw[4];
+                    const uint32_t total = enc_lengths2<kDelta>(sin, prev_w, cdst, cw, qw);
+                    post(total);
+                    __syncwarp();
+                    enc_pack2<kDelta>(sin, prev_w, cw, qw, sin, total);
+                }
+            } else {
+                // the stream's last, partial sub-tile
+                EncodeTile tt;
+                uint32_t P[3] = {0, 0, 0};
+                uint32_t last_w = prev_w;
+                const uint8_t* sbytes = stage + 16 + warp * (kWTInts * 4);
+#pragma unroll
+                for (int j = 0; j < kWTRows; ++j) {
+                    const uint32_t cnt = group_count(g0 + 32 * j + lane, ngroups, tail_r);
+                    uint4 x = mask_tail(*reinterpret_cast<const uint4*>(sbytes + 512 * j + 16 * lane), cnt);
+                    if constexpr (kDelta) {
+                        uint32_t p = __shfl_up_sync(kFull, x.w, 1);
+                        if (lane == 0) p = last_w;
+                        last_w = __shfl_sync(kFull, x.w, 31);
+                        x = make_uint4(x.x - p, x.y - x.x, x.z - x.y, x.w - x.z);
+                    }
+                    tt.d[j] = x;
+                    const uint32_t l0 = cnt > 0 ? dev_byte_length(x.x) : 0u;
+                    const uint32_t l1 = cnt > 1 ? dev_byte_length(x.y) : 0u;
+                    const uint32_t l2 = cnt > 2 ? dev_byte_length(x.z) : 0u;
+                    const uint32_t l3 = cnt > 3 ? dev_byte_length(x.w) : 0u;
+                    tt.lens[j] = l0 | (l1 << 8) | (l2 << 16) | (l3 << 24);
+                    P[j / 3] |= (l0 + l1 + l2 + l3) << (10 * (j % 3));
+                    if (cnt)
+                        cdst[32 * j + lane] = (uint8_t)((l0 - 1) | (l1 ? ((l1 - 1) << 2) : 0u) |
+                                                        (l2 ? ((l2 - 1) << 4) : 0u) | (l3 ? ((l3 - 1) << 6) : 0u));
+                }
+                tt.total = packed_row_scan(P, tt.qw);
+                post(tt.total);
+                __syncwarp();
+                encode_pack_at(tt, stage + 16 + warp * (kWTInts * 4), 0);
+            }
+        } else {
+            post(0u);
+        }
+        __syncwarp();
+        if (k) store_prev(tprev, stp, qp, k - 1);
+        tprev = t;
+    }
+    if (k) store_prev(tprev, stp, qp, k - 1);
+}
+
+// ---------------------------------------------------------------------------
+// 4b. one-pass encode for delta streams: the same tiles and deferred look-back, with the
+// tile bookkeeping done by all consumer threads between named barriers (round 1's
+// kernel).  Delta streams of sorted ids are mostly all-small sub-tiles whose packing is
+// short, so nothing would hide a scanner warp's look-back latency behind consumer work;
+// here the look-back loads of the previous tile are issued a whole round before they are
+// needed (cfg2: 65 vs 78 us for the scanner kernel; plain cfg3: 543 vs 472 us).
+// ---------------------------------------------------------------------------
+constexpr int kD1eStages = 3;
+constexpr uint32_t kD1eInts = kCTWarps * kWTInts;                          // 8192 per tile
+constexpr uint32_t kD1eStride = 16 + kD1eInts * 4 + 16 + kCTWarps * kWTGroups;  // prefix, tile, slack, ctrl
+
+struct __align__(16) D1eShared {
+    uint64_t full[kD1eStages], empty[kD1eStages];
+    uint32_t wsum[3][kCTWarps];
+    uint32_t wpre[kCTWarps];  // exclusive prefix of the resolved tile's sub-tile sizes
+    uint32_t red[kCTWarps];
+    unsigned long long carry, incl;
+};
+
+template <bool kDelta, bool kTrace>
+__global__ void __launch_bounds__(kCTThreads + 32, 2)
+    svb_encode1d_kernel(const uint32_t* __restrict__ in, uint64_t n, uint32_t prev, uint8_t* __restrict__ out,
+                       DecodeMeta meta, uint64_t* __restrict__ d_out_len, unsigned long long* status, uint32_t epoch) {
+    extern __shared__ __align__(128) uint8_t dsm[];
+    __shared__ D1eShared sh;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint64_t ngroups = (n + 3) >> 2;
+    const uint32_t tail_r = (uint32_t)(n & 3);
+    const uint64_t nsub = (ngroups + kWTGroups - 1) / kWTGroups;
+    const uint32_t ntiles = (uint32_t)((nsub + kCTWarps - 1) / kCTWarps);
+    const uint32_t G = gridDim.x;
+    if (threadIdx.x == 0) {
+#pragma unroll
+        for (int k = 0; k < kD1eStages; ++k) {
+            mbar_init(&sh.full[k], 1);
+            mbar_init(&sh.empty[k], kCTWarps);
+        }
         sh.incl = 0;
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
@@ -604,11 +862,11 @@ __global__ void __launch_bounds__(kCTThreads + 32, 2)
         const uintptr_t lo = (uintptr_t)in, hi = lo + 4 * n;
         uint32_t k = 0, ph = 0;
         int st = 0;
-        for (uint32_t t = blockIdx.x; t < ntiles; t += G, ++k, st = st + 1 == kE1Stages ? 0 : st + 1, ph ^= st == 0) {
-            uint8_t* stage = dsm + (uint32_t)st * kE1Stride;
-            if (k >= (uint32_t)kE1Stages) mbar_wait_parity_sleep(&sh.empty[st], ph ^ 1u);
-            const uint64_t i0 = (uint64_t)t * kE1Ints;
-            const uint64_t cnt = n - i0 < (uint64_t)kE1Ints ? n - i0 : (uint64_t)kE1Ints;
+        for (uint32_t t = blockIdx.x; t < ntiles; t += G, ++k, st = st + 1 == kD1eStages ? 0 : st + 1, ph ^= st == 0) {
+            uint8_t* stage = dsm + (uint32_t)st * kD1eStride;
+            if (k >= (uint32_t)kD1eStages) mbar_wait_parity_sleep(&sh.empty[st], ph ^ 1u);
+            const uint64_t i0 = (uint64_t)t * kD1eInts;
+            const uint64_t cnt = n - i0 < (uint64_t)kD1eInts ? n - i0 : (uint64_t)kD1eInts;
             const uintptr_t beg = (uintptr_t)(in + i0) - (t ? 16 : 0), end = (uintptr_t)(in + i0 + cnt);
             uint8_t* dst = stage + (t ? 0 : 16);
             const uint32_t tx = tma_cover_bytes(beg, end, lo, hi);
@@ -684,8 +942,8 @@ __global__ void __launch_bounds__(kCTThreads + 32, 2)
         if (kTrace && ct == 0) meta.trace[8ull * tp + 4] = gtimer();
         const uint64_t s = (uint64_t)tp * kCTWarps + warp;
         if (s < nsub) {
-            const uint32_t src = sh_addr(dsm) + (uint32_t)st * kE1Stride + 16 + (uint32_t)warp * (kWTInts * 4);
-            store_realigned(src, sh.wsum[q][warp], out + ngroups + sh.carry + sh.wpre[warp]);
+            const uint32_t src = sh_addr(dsm) + (uint32_t)st * kD1eStride + 16 + (uint32_t)warp * (kWTInts * 4);
+            store_realigned2(src, sh.wsum[q][warp], out + ngroups + sh.carry + sh.wpre[warp]);
         }
         __syncwarp();
         if (kTrace && ct == 0) meta.trace[8ull * tp + 5] = gtimer();
@@ -695,18 +953,18 @@ __global__ void __launch_bounds__(kCTThreads + 32, 2)
     uint32_t k = 0, tprev = 0, ph = 0;
     int st = 0, q = 0, stp = 0, qp = 0;  // stage / wsum slot of this iteration and of the previous one
     for (uint32_t t = blockIdx.x; t < ntiles;
-         t += G, ++k, stp = st, qp = q, st = st + 1 == kE1Stages ? 0 : st + 1, q = q == 2 ? 0 : q + 1, ph ^= st == 0) {
+         t += G, ++k, stp = st, qp = q, st = st + 1 == kD1eStages ? 0 : st + 1, q = q == 2 ? 0 : q + 1, ph ^= st == 0) {
         if (k) prefetch(tprev);
         if (kTrace && ct == 0) meta.trace[8ull * t + 1] = gtimer();
         mbar_wait_parity(&sh.full[st], ph);
         if (kTrace && ct == 0) meta.trace[8ull * t + 2] = gtimer();
-        uint8_t* stage = dsm + (uint32_t)st * kE1Stride;
+        uint8_t* stage = dsm + (uint32_t)st * kD1eStride;
         const uint64_t s = (uint64_t)t * kCTWarps + warp;
         const uint64_t g0 = s * kWTGroups;
         uint32_t total = 0;
         if (g0 < ngroups) {
             const uint32_t sin = sh_addr(stage) + 16 + (uint32_t)warp * (kWTInts * 4);
-            uint8_t* sctrl = stage + 16 + kE1Ints * 4 + 16 + warp * kWTGroups;
+            uint8_t* sctrl = stage + 16 + kD1eInts * 4 + 16 + warp * kWTGroups;
             const uint32_t prev_w = warp ? lds32(sin - 4) : (t ? lds32(sh_addr(stage) + 12) : prev);
             const uint32_t cnt_g = (uint32_t)(ngroups - g0 < (uint64_t)kWTGroups ? ngroups - g0 : (uint64_t)kWTGroups);
             uint8_t* cdst = out + g0;
@@ -720,11 +978,12 @@ __global__ void __launch_bounds__(kCTThreads + 32, 2)
                         for (uint32_t i = lane; i < kWTGroups; i += 32) cdst[i] = 0;
                     }
                 } else {
-                    uint32_t lens[kWTRows], qw[4];
-                    total = enc_full_lengths<kDelta>(sin, prev_w, sh_addr(sctrl), lens, qw);
+                    // control bytes straight to the stream, then the branch-free word pack
+                    // at phase 0 in place (svb_pack.cuh)
+                    uint32_t cw[2], qw[4];
+                    total = enc_lengths2<kDelta>(sin, prev_w, cdst, cw, qw);
                     __syncwarp();
-                    enc_full_pack_w<kDelta>(sin, prev_w, lens, qw, sin, total);
-                    for (uint32_t i = lane; i < cnt_g; i += 32) cdst[i] = sctrl[i];
+                    enc_pack2<kDelta>(sin, prev_w, cw, qw, sin, total);
                 }
             } else {
                 // the stream's last, partial sub-tile
@@ -774,7 +1033,7 @@ __global__ void __launch_bounds__(kCTThreads + 32, 2)
     }
     if (k) {
         prefetch(tprev);
-        resolve(tprev, (int)((k - 1) % kE1Stages), (int)((k - 1) % 3));
+        resolve(tprev, (int)((k - 1) % kD1eStages), (int)((k - 1) % 3));
     }
 }
 
@@ -782,20 +1041,33 @@ __global__ void __launch_bounds__(kCTThreads + 32, 2)
 // *used = false leaves the call to the other paths
 static cudaError_t launch_encode1(const uint32_t* in, uint64_t n, int delta, uint32_t prev, uint8_t* out,
                                   uint64_t* d_out_len, const DecodeMeta& m, unsigned long long* status, uint32_t epoch,
-                                  cudaStream_t stream, bool* used) {
+                                  cudaStream_t stream, bool* used, bool scanner) {
     *used = false;
     if (((uintptr_t)in) & 15) return cudaSuccess;
-    const uint32_t smem = (uint32_t)(kE1Stages * kE1Stride);
+    // plain streams: the scanner kernel; delta streams: the barrier kernel (4b) unless asked
+    const bool sk = !delta || scanner;
+    const uint32_t smem = sk ? (uint32_t)(kE1Stages * kE1Stride) : (uint32_t)(kD1eStages * kD1eStride);
+    const int threads = sk ? kE1Threads : kCTThreads + 32;
+    const void* fns[4];
+    if (sk) {
+        fns[0] = (const void*)svb_encode1_kernel<true, false>;
+        fns[1] = (const void*)svb_encode1_kernel<false, false>;
+        fns[2] = (const void*)svb_encode1_kernel<true, true>;
+        fns[3] = (const void*)svb_encode1_kernel<false, true>;
+    } else {
+        fns[0] = (const void*)svb_encode1d_kernel<true, false>;
+        fns[1] = (const void*)svb_encode1d_kernel<false, false>;
+        fns[2] = (const void*)svb_encode1d_kernel<true, true>;
+        fns[3] = (const void*)svb_encode1d_kernel<false, true>;
+    }
     const int dev = launch_current_device();
     const int sms = launch_sms(dev), coop = launch_coop(dev);
-    const void* fns[4] = {(const void*)svb_encode1_kernel<true, false>, (const void*)svb_encode1_kernel<false, false>,
-                          (const void*)svb_encode1_kernel<true, true>, (const void*)svb_encode1_kernel<false, true>};
     for (const void* f : fns) {
         const cudaError_t a = launch_ensure_smem(f, smem);
         if (a != cudaSuccess) return a;
     }
-    const int o1 = launch_occupancy(svb_encode1_kernel<true, false>, kCTThreads + 32, smem);
-    const int o2 = launch_occupancy(svb_encode1_kernel<false, false>, kCTThreads + 32, smem);
+    const int o1 = launch_occupancy(fns[0], threads, smem);
+    const int o2 = launch_occupancy(fns[1], threads, smem);
     const int occ = o1 < o2 ? o1 : o2;
     if (!coop || occ < 1) return cudaSuccess;
     const uint64_t ngroups = (n + 3) >> 2;
@@ -806,9 +1078,8 @@ static cudaError_t launch_encode1(const uint32_t* in, uint64_t n, int delta, uin
     DecodeMeta mm = m;
     void* args[] = {(void*)&in, (void*)&n, (void*)&prev, (void*)&out, (void*)&mm, (void*)&d_out_len, (void*)&status,
                     (void*)&epoch};
-    const void* fn = m.trace ? (delta ? (const void*)svb_encode1_kernel<true, true> : (const void*)svb_encode1_kernel<false, true>)
-                             : (delta ? (const void*)svb_encode1_kernel<true, false> : (const void*)svb_encode1_kernel<false, false>);
-    const cudaError_t e = cudaLaunchCooperativeKernel(fn, dim3((unsigned)grid), dim3(kCTThreads + 32), args, smem, stream);
+    const void* fn = fns[(m.trace ? 2 : 0) + (delta ? 0 : 1)];
+    const cudaError_t e = cudaLaunchCooperativeKernel(fn, dim3((unsigned)grid), dim3(threads), args, smem, stream);
     if (e == cudaSuccess) *used = true;
     return e;
 }
@@ -833,7 +1104,8 @@ cudaError_t launch_encode3(const uint32_t* in, uint64_t n, int delta, uint32_t p
     const uint32_t nchunks = (uint32_t)((nsub + kChunkSubs - 1) / kChunkSubs);
     if (hints & 0x100) {  // one-pass (the ctrl scan of a decode is not run here: clear the aggregates)
         bool used = false;
-        const cudaError_t e = launch_encode1(in, n, delta, prev, out, d_out_len, m, status, epoch, stream, &used);
+        const cudaError_t e =
+            launch_encode1(in, n, delta, prev, out, d_out_len, m, status, epoch, stream, &used, (hints & 0x200) != 0);
         if (e != cudaSuccess) return e;
         if (used) {
             *launches = 1;

@@ -1,0 +1,190 @@
+// svb_pack.cuh -- branch-free group pack for the Stream VByte encoders (sm_100a).
+//
+// A group is 4 integers x0..x3 and its control byte c (field i = byte_length(x_i) - 1,
+// codec.hpp:70-72).  Its data is x0[0:l0] x1[0:l1] x2[0:l2] x3[0:l3],
+// 4..16 bytes (the low bytes, little-endian).  Every x_i is zero above its length, so
+// concatenation is shift + OR, no masking:
+//   A = x0 | x1 << 8 l0 (<= 8 bytes, two words), B = x2 | x3 << 8 l2, G = A | B << 8 (l0 + l1)
+// G (<= 16 bytes, four words) is then shifted onto the shared-memory word grid at the
+// group's byte address and stored as whole words.  Adjacent groups of a row belong to
+// adjacent lanes, so the one word two groups share is passed up one lane by a shuffle and
+// OR-ed in: every word is written once, by one lane, with predicated stores (no branches).
+//
+// Pipe budget (B200): integer ops run on the ALU pipe (IADD3/LOP3/SHF/PRMT/SEL) and the
+// FMA pipe (IMAD), each 1 warp instruction per 2 cycles per SM sub-partition, so the pack
+// is written for few ALU ops: ~55 per group against ~150 with the earlier branchy pack
+// (ncu, cfg3 one-pass encode: 63 executed instructions per integer).
+#pragma once
+
+#include <cstdint>
+
+#include "svb_device.cuh"
+#include "svb_fast.cuh"
+#include "svb_tma.cuh"
+
+namespace bcgpu {
+
+__device__ __forceinline__ uint32_t shfl_l(uint32_t lo, uint32_t hi, uint32_t s) {  // (hi:lo << s) >> 32, s < 32
+    return __funnelshift_l(lo, hi, s);
+}
+
+// byte_length - 1 of the four integers -> control byte (field i in bits 2i..2i+1);
+// tot = the group's data bytes
+__device__ __forceinline__ uint32_t group_ctrl(const uint4& x, uint32_t& tot) {
+    const uint32_t m0 = blen_m1(x.x), m1 = blen_m1(x.y), m2 = blen_m1(x.z), m3 = blen_m1(x.w);
+    tot = m0 + m1 + m2 + m3 + 4u;
+    return m0 | (m1 << 2) | (m2 << 4) | (m3 << 6);
+}
+
+// data bytes of a control byte: 4 + the sum of its fields (length[c])
+__device__ __forceinline__ uint32_t ctrl_bytes(uint32_t c) {
+    return (c & 3u) + ((c >> 2) & 3u) + ((c >> 4) & 3u) + (c >> 6) + 4u;
+}
+
+// The group's data as four little-endian words G0..G3 (bytes past its length are zero).
+// e8 = 8 * the group's data bytes.
+__device__ __forceinline__ uint4 group_bytes(const uint4& x, uint32_t c, uint32_t& e8) {
+    const uint32_t sA = ((c & 3u) << 3) + 8u;          // 8 l0, 8..32
+    const uint32_t sB = ((c >> 1) & 0x18u) + 8u;       // 8 l2
+    const uint32_t A0 = x.x | __funnelshift_lc(0u, x.y, sA);  // x1 << 8 l0 (0 when l0 = 4)
+    const uint32_t A1 = __funnelshift_lc(x.y, 0u, sA);        // x1 >> (32 - 8 l0)
+    const uint32_t B0 = x.z | __funnelshift_lc(0u, x.w, sB);
+    const uint32_t B1 = __funnelshift_lc(x.w, 0u, sB);
+    const uint32_t la8 = sA + ((c << 1) & 0x18u) + 8u;  // 8 (l0 + l1), 16..64
+    e8 = la8 + sB + ((c >> 3) & 0x18u) + 8u;
+    const uint32_t tb = la8 & 31u;
+    const bool k1 = la8 >= 32u, k2 = la8 == 64u;       // B starts in word 1 / word 2
+    const uint32_t Z0 = B0 << tb, Z1 = shfl_l(B0, B1, tb), Z2 = shfl_l(B1, 0u, tb);
+    uint4 G;
+    G.x = A0 | (k1 ? 0u : Z0);
+    G.y = A1 | (k1 ? (k2 ? 0u : Z0) : Z1);
+    G.z = k1 ? (k2 ? Z0 : Z1) : Z2;
+    G.w = k1 ? (k2 ? Z1 : Z2) : 0u;
+    return G;
+}
+
+// Pack one group of each lane of a row at shared byte address a (groups of consecutive
+// lanes are consecutive in the stream: a_{l+1} = a_l + ctrl_bytes(c_l)).  carry: the
+// pending (partially filled) word after the previous row's last group, in and out; the
+// caller stores it after the last row.  Every lane of the warp must call this.
+__device__ __forceinline__ void pack_group_row(const uint4& x, uint32_t c, uint32_t a, uint32_t& carry) {
+    const int lane = threadIdx.x & 31;
+    uint32_t e8;
+    const uint4 G = group_bytes(x, c, e8);
+    const uint32_t u = (a & 3u) << 3;
+    const uint32_t W0 = G.x << u, W1 = shfl_l(G.x, G.y, u), W2 = shfl_l(G.y, G.z, u), W3 = shfl_l(G.z, G.w, u),
+                   W4 = shfl_l(G.w, 0u, u);
+    e8 += u;  // 8 e, e = 4..19: words [a & ~3, +e) are touched
+    const bool p1 = e8 >= 64u, p2 = e8 >= 96u, p3 = e8 >= 128u;
+    // the word the next group shares (all zero when this group ends on a word boundary)
+    const uint32_t pend = p3 ? W4 : p2 ? W3 : p1 ? W2 : W1;
+    uint32_t pin = __shfl_up_sync(kFull, pend, 1);
+    if (lane == 0) pin = carry;
+    carry = __shfl_sync(kFull, pend, 31);
+    const uint32_t wa = a & ~3u;
+    sts32(wa, W0 | pin);
+    if (p1) sts32(wa + 4, W1);
+    if (p2) sts32(wa + 8, W2);
+    if (p3) sts32(wa + 12, W3);
+}
+
+// Packed bytes [src, src + len) of shared memory (16-B aligned, >= 16 readable bytes after
+// the end) -> global dst at any alignment.  Interior 16-B granules of the destination are
+// funnel-shifted out of five shared words each and stored with 128-bit stores; the < 16
+// bytes before the first and after the last aligned granule are single-byte stores of one
+// lane each.
+__device__ __forceinline__ void store_realigned2(uint32_t src, uint32_t len, uint8_t* dst) {
+    const int lane = threadIdx.x & 31;
+    if (len == 0) return;
+    const uintptr_t D = (uintptr_t)dst, Dend = D + len;
+    const uintptr_t A0 = (D + 15) & ~(uintptr_t)15, A1 = Dend & ~(uintptr_t)15;
+    const uint32_t head = (uint32_t)((A0 < Dend ? A0 : Dend) - D);  // bytes before the first aligned granule
+    // interior granules [A0, A1): destination byte a comes from src + (a - D)
+    if (A1 > A0) {
+        const uint32_t ng = (uint32_t)((A1 - A0) >> 4);
+        const uint32_t s0 = src + head;                 // source of the first interior byte
+        const uint32_t r = (s0 & 3u) << 3;
+        for (uint32_t k = lane; k < ng; k += 32) {
+            const uint32_t wa = (s0 + 16 * k) & ~3u;
+            const uint32_t w0 = lds32v(wa), w1 = lds32v(wa + 4), w2 = lds32v(wa + 8), w3 = lds32v(wa + 12),
+                           w4 = lds32v(wa + 16);
+            const uint4 v = make_uint4(__funnelshift_r(w0, w1, r), __funnelshift_r(w1, w2, r),
+                                       __funnelshift_r(w2, w3, r), __funnelshift_r(w3, w4, r));
+            *reinterpret_cast<uint4*>(A0 + 16 * (uintptr_t)k) = v;
+        }
+    }
+    if ((uint32_t)lane < head) dst[lane] = (uint8_t)lds8(src + lane);
+    const uint32_t tail = A1 >= A0 ? (uint32_t)(Dend - A1) : 0u;  // bytes after the last aligned granule
+    if ((uint32_t)lane < tail) {
+        const uint32_t o = (uint32_t)(A1 - D) + lane;
+        dst[o] = (uint8_t)lds8(src + o);
+    }
+}
+
+// Packed bytes at shared sdst (sdst has dst's 16-B phase), len bytes -> global dst: one bulk
+// copy of the 16-B aligned interior (lane 0 issues and commits it; the caller waits for its
+// smem read before reusing the buffer), lanes store the < 16 edge bytes at each end.  Every
+// lane must have fenced its shared writes for the async proxy and synced the warp first.
+__device__ __forceinline__ void put_packed(uint8_t* dst, uint32_t sdst, uint32_t len) {
+    const int lane = threadIdx.x & 31;
+    const uintptr_t gb = (uintptr_t)dst, ge = gb + len;
+    const uintptr_t a_lo = (gb + 15) & ~(uintptr_t)15, a_hi = ge & ~(uintptr_t)15;
+    if (a_hi > a_lo) {
+        if (lane == 0) {
+            tma_store_s(reinterpret_cast<void*>(a_lo), sdst + (uint32_t)(a_lo - gb), (uint32_t)(a_hi - a_lo));
+            tma_store_commit();
+        }
+        const uint32_t nh = (uint32_t)(a_lo - gb), nt = (uint32_t)(ge - a_hi);
+        if ((uint32_t)lane < nh) dst[lane] = (uint8_t)lds8(sdst + lane);
+        if ((uint32_t)lane < nt) dst[(a_hi - gb) + lane] = (uint8_t)lds8(sdst + (uint32_t)(a_hi - gb) + lane);
+    } else {
+        for (uint32_t i = lane; i < len; i += 32) dst[i] = (uint8_t)lds8(sdst + i);
+    }
+}
+
+// ---- full sub-tiles (1024 integers, row j lane l = group 32 j + l) -----------------
+// Pass 1: control bytes (stored straight to the stream: byte 32 j + l of cdst, any
+// alignment, 32 consecutive bytes per row), the lane's control bytes kept in cw (row j in
+// byte j & 3 of cw[j >> 2]) and the rows' packed exclusive offsets in qw; returns the
+// sub-tile's data size.
+template <bool kDelta, bool kAny = false>
+__device__ __forceinline__ uint32_t enc_lengths2(uint32_t sin, uint32_t prev_w, uint8_t* __restrict__ cdst,
+                                                 uint32_t (&cw)[2], uint32_t (&qw)[4]) {
+    const int lane = threadIdx.x & 31;
+    uint32_t P[3] = {0, 0, 0};
+    uint32_t last = prev_w;
+    cw[0] = cw[1] = 0;
+#pragma unroll
+    for (int j = 0; j < kWTRows; ++j) {
+        const uint4 x = enc_row<kDelta, kAny>(sin, j, last);
+        uint32_t tot;
+        const uint32_t c = group_ctrl(x, tot);
+        cw[j >> 2] |= c << (8 * (j & 3));
+        P[j / 3] += tot << (10 * (j % 3));
+        cdst[32 * j + lane] = (uint8_t)c;
+    }
+    return packed_row_scan(P, qw);
+}
+
+// Pass 2: pack every row in place at shared byte sdst (sdst <= sin, 4-B aligned so that a
+// row's completed words end before the next row's integers), then the final pending word.
+template <bool kDelta, bool kAny = false>
+__device__ __forceinline__ void enc_pack2(uint32_t sin, uint32_t prev_w, const uint32_t (&cw)[2],
+                                          const uint32_t (&qw)[4], uint32_t sdst, uint32_t total) {
+    uint32_t last = prev_w, carry = 0;
+    // rows in pairs: both rows are read before either is written (row j + 1's output ends
+    // before row j + 2's integers), so the two packs' dependency chains interleave
+#pragma unroll
+    for (int j = 0; j < kWTRows; j += 2) {
+        const uint4 x0 = enc_row<kDelta, kAny>(sin, j, last);
+        const uint4 x1 = enc_row<kDelta, kAny>(sin, j + 1, last);
+        const uint32_t c0 = (cw[j >> 2] >> (8 * (j & 3))) & 0xFFu, c1 = (cw[j >> 2] >> (8 * (j & 3) + 8)) & 0xFFu;
+        const uint32_t a0 = sdst + (qw[j >> 1] & 0xFFFFu), a1 = sdst + (qw[j >> 1] >> 16);
+        __syncwarp();  // every lane has read both rows before any lane writes over them
+        pack_group_row(x0, c0, a0, carry);
+        pack_group_row(x1, c1, a1, carry);
+    }
+    if (((sdst + total) & 3u) && (threadIdx.x & 31) == 0) sts32((sdst + total) & ~3u, carry);
+}
+
+}  // namespace bcgpu

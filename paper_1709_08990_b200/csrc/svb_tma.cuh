@@ -61,6 +61,16 @@ __device__ __forceinline__ void mbar_wait_parity_sleep(uint64_t* bar, uint32_t p
     }
 }
 
+// a wait expected to take a while (a service warp waiting for a whole round of consumer
+// work): poll with a longer back-off so the spin takes few issue slots
+__device__ __forceinline__ void mbar_wait_parity_lazy(uint64_t* bar, uint32_t parity, uint32_t max_ns) {
+    uint32_t ns = 64;
+    while (!mbar_test_parity(bar, parity)) {
+        __nanosleep(ns);
+        ns = ns < max_ns ? 2 * ns : max_ns;
+    }
+}
+
 __device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 
 // global -> shared, completion on `bar` (dst, src 16-B aligned; bytes % 16 == 0)
