@@ -216,6 +216,7 @@ int bcgpu_debug_set_trace(bcgpu_ctx* c, void* d_trace) {
 //   2048    encode: never the one-pass kernel;   4096  encode: one-pass for plain streams too
 //   0x80000 encode: plain streams take the two-read path (size scan + tile encode)
 //   0x100000 encode: delta streams take the scanner one-pass kernel (plain streams always do)
+//   0x400000 decode: dense delta streams (1 byte per integer) still run the control scan
 //   512     host API: no piecewise pipelining
 //   1024    decode: sums pass + pooled delta decode instead of the one-pass kernel
 //   0x8000  decode: the control scan only (dev timing; output not written)
@@ -414,8 +415,10 @@ int bcgpu_svb_decode_device(bcgpu_ctx* c, const uint8_t* d_in, size_t in_len, si
     const int st = next_epoch(c, s);
     if (st) return st;
     int launches = 0;
+    // 0x800000: this layout's tile aggregates hold no current-epoch tag (a dense stream's
+    // one-pass decode then skips clearing them)
     BC_CUDA(launch_decode3(d_in, in_len, n, delta, base, d_out, d_last, c->offs, status_ptr(c), c->epoch,
-                           c->pipe_grid, s, &launches, c->trace, c->debug_flags));
+                           c->pipe_grid, s, &launches, c->trace, c->debug_flags | (c->agg_n == n ? 0x800000u : 0u)));
     if (delta) c->agg_n = n;  // its control scan cleared the aggregates of this layout
     g_launches.fetch_add((uint64_t)launches);
     return BCGPU_OK;

@@ -654,6 +654,12 @@ __global__ void __launch_bounds__(kSumThreads, 3)
     const uint32_t G = gridDim.x;
     const uintptr_t lo = (uintptr_t)in, hi = lo + in_len, data0 = lo + ngroups;
     const uint32_t stride = kTileCtrl + pool_bytes;
+    // dense (totals bit 1): the stream is ceil(n/4) + n bytes, so every data length is 1 and
+    // every control field 0 (else the stream is truncated); data offsets are implicit -- no
+    // control scan ran before this kernel, the producer computes them and the consumers
+    // check that the control bytes are zero
+    const bool dense = (totals & 2u) != 0;
+    totals &= 1u;
     if (threadIdx.x == 0) {
 #pragma unroll
         for (int k = 0; k < kD1Stages; ++k) {
@@ -676,7 +682,7 @@ __global__ void __launch_bounds__(kSumThreads, 3)
             tma_load(sh.meta[st].loc, meta.localpre + s0, 48, &sh.mfull[st]);
             tma_load(sh.meta[st].chk, meta.chunkpre + (c & ~1ull), 32, &sh.mfull[st]);
         };
-        if (lane == 0)
+        if (lane == 0 && !dense)
             for (int i = 0; i < kD1Stages; ++i) {
                 const uint64_t t = (uint64_t)blockIdx.x + (uint64_t)i * G;
                 if (t < ntiles) issue_meta((uint32_t)t, i);
@@ -720,18 +726,22 @@ __global__ void __launch_bounds__(kSumThreads, 3)
             uint8_t* pool = sc + kTileCtrl;
             const uint64_t s0 = (uint64_t)t * kCTWarps, chunk = s0 / kChunkSubs;
             const uint32_t ns = (uint32_t)(nsub - s0 < (uint64_t)kCTWarps ? nsub - s0 : (uint64_t)kCTWarps);
-            mbar_wait_parity(&sh.mfull[st], ph);
+            if (!dense) mbar_wait_parity(&sh.mfull[st], ph);
             const SumMeta& M = sh.meta[st];
-            const unsigned long long cpre = totals ? Pc : M.chk[chunk & 1];
+            const unsigned long long cpre = totals ? Pc : (dense ? 0ull : M.chk[chunk & 1]);
             const bool end_at_chunk = s0 + ns == nsub || (s0 + ns) % kChunkSubs == 0;
-            const unsigned long long A = cpre + M.loc[0];
-            const unsigned long long B = end_at_chunk ? (totals ? Pc + Tc : M.chk[(chunk & 1) + 1]) : cpre + M.loc[ns];
+            const unsigned long long A =
+                dense ? (unsigned long long)s0 * kWTInts : cpre + M.loc[0];
+            const unsigned long long B =
+                dense ? min((unsigned long long)n, (unsigned long long)(s0 + ns) * kWTInts)
+                      : (end_at_chunk ? (totals ? Pc + Tc : M.chk[(chunk & 1) + 1]) : cpre + M.loc[ns]);
             if (totals && s0 + ns == nsub && lane == 0) {  // the stream's last tile: its length
                 const uint64_t need = ngroups + B;
                 if (need != in_len) dec_report(status, epoch, need > in_len ? BCGPU_ERR_TRUNCATED : BCGPU_ERR_TRAILING_BYTES);
             }
             const uint32_t li = (uint32_t)lane < ns ? (uint32_t)lane : ns;
-            const unsigned long long my = (li == ns) ? B : cpre + M.loc[li];
+            const unsigned long long my =
+                (li == ns) ? B : (dense ? (unsigned long long)(s0 + li) * kWTInts : cpre + M.loc[li]);
             const uintptr_t Ag = data0 + A, Bg = data0 + B, bse = Ag & ~(uintptr_t)15;
             const uint32_t tx = tma_cover_bytes(Ag, Bg, lo, hi);
             const bool fits = tx != 0xFFFFFFFFu && tx + 16 <= pool_bytes;
@@ -758,7 +768,7 @@ __global__ void __launch_bounds__(kSumThreads, 3)
                 if (c_tma && ctx) tma_load_hint(sc, reinterpret_cast<const void*>(cb), ctx, &sh.full[st], pol);
                 if (fits && tx) tma_load_hint(pool, reinterpret_cast<const void*>(bse), tx, &sh.full[st], pol);
                 const uint64_t tn = (uint64_t)t + (uint64_t)kD1Stages * G;
-                if (tn < ntiles) issue_meta((uint32_t)tn, st);
+                if (tn < ntiles && !dense) issue_meta((uint32_t)tn, st);
             }
         }
         return;
@@ -866,6 +876,7 @@ __global__ void __launch_bounds__(kSumThreads, 3)
         if (kTrace && ct == 0) meta.trace[8ull * t + 2] = gtimer();
         const uint64_t s = (uint64_t)t * kCTWarps + warp;
         uint32_t sum = 0;
+        bool checked = false;  // the control bytes were seen all zero (or reported)
         if (s < nsub) {
             const uint8_t* sc = dsm + (uint32_t)st * stride + warp * kWTGroups;
             const uint8_t* pool = dsm + (uint32_t)st * stride + kTileCtrl;
@@ -875,9 +886,12 @@ __global__ void __launch_bounds__(kSumThreads, 3)
                 if ((s + 1) * kWTInts <= n && head <= pool_bytes - 32) {
                     const uint32_t sd = sh_addr(pool) + head;
                     if (ctrl_all_zero(sh_addr(sc))) {
+                        checked = true;
                         zbits |= 1u;
                         sum = __reduce_add_sync(kFull, zero_tile_sum(sd));
                     } else {
+                        checked = true;
+                        if (dense && lane == 0) dec_report(status, epoch, BCGPU_ERR_TRUNCATED);
                         bool zero;
                         const WarpCtrl wf = ctrl_full(sh_addr(sc), &zero);
                         sum = __reduce_add_sync(kFull, expand_full<2, false>(wf, sd, nullptr, 0));
@@ -892,6 +906,17 @@ __global__ void __launch_bounds__(kSumThreads, 3)
                 sum = sums_generic(sc, g0, ngroups, tail_r, head,
                                    [&](uint32_t i) { return gword_guarded(gb + 4 * (uintptr_t)i, lo, hi); });
             }
+        }
+        if (dense && !checked && s < nsub) {  // every used control field of a dense stream must be 0
+            const uint8_t* sc = dsm + (uint32_t)st * stride + warp * kWTGroups;
+            const uint64_t g0 = s * kWTGroups;
+            uint32_t orr = 0;
+            for (uint64_t g = g0 + lane; g < ngroups && g < g0 + kWTGroups; g += 32) {
+                uint32_t c = sc[g - g0];
+                if (g + 1 == ngroups && tail_r) c &= (1u << (2 * tail_r)) - 1u;
+                orr |= c;
+            }
+            if (__any_sync(kFull, orr != 0) && lane == 0) dec_report(status, epoch, BCGPU_ERR_TRUNCATED);
         }
         if (lane == 0) sh.wsum[q][warp] = sum;
         consumers_sync();
@@ -1104,6 +1129,28 @@ cudaError_t launch_decode3(const uint8_t* in, uint64_t in_len, uint64_t n, int d
     const uint64_t ngroups = (n + 3) >> 2;
     const uint64_t nsub = (ngroups + kWTGroups - 1) / kWTGroups;
     const uint32_t ep = (debug_flags & 1024) ? 0u : epoch;
+    // a dense delta stream (ceil(n/4) + n bytes: every integer one byte) needs no control
+    // scan: the one-pass decode computes the implicit offsets and checks the control bytes
+    // (debug flag 0x400000: always scan); its tile aggregates must hold no current tag
+    if (delta && ep && in_len == ngroups + n && !(debug_flags & (0x400000 | 0x8000 | 0x40000))) {
+        const DecodeMeta m = carve_decode_meta(meta_ws, n);
+        if (!(debug_flags & 0x800000)) {  // 0x800000: the caller knows the aggregates are clean
+            uint64_t cnt = 0;
+            unsigned long long* agg = meta_agg_ptr(meta_ws, n, &cnt);
+            const cudaError_t ce = cudaMemsetAsync(agg, 0, cnt * sizeof(unsigned long long), stream);
+            if (ce != cudaSuccess) return ce;
+        }
+        bool used = false;
+        const double dpb = 1024.0;
+        DecodeMeta mm = m;
+        mm.trace = trace;
+        const cudaError_t e1 = launch_decode1(in, in_len, n, base, out, d_last, mm, dpb, ep, stream, &used, status, 2u);
+        if (e1 != cudaSuccess) return e1;
+        if (used) {
+            *launches = 1;
+            return cudaSuccess;
+        }
+    }
     // the one-pass delta decode sums the chunk totals itself (grid <= 504: a CTA's chunks
     // advance by <= 64 per tile), so the control scan can skip its last-CTA scan
     uint32_t totals = 0;

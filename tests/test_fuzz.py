@@ -17,7 +17,7 @@ pytestmark = pytest.mark.gpu
 # debug flags of the ctx (bcgpu_capi.cu): which path runs
 ENCODE_PATHS = {"default": 0, "two_read": 16, "slots": 32, "one_pass_plain": 4096, "two_read_plain": 0x80000,
                 "scanner_delta": 0x100000}
-DECODE_PATHS = {"default": 0, "sums_pooled": 0x400}
+DECODE_PATHS = {"default": 0, "sums_pooled": 0x400, "scan_dense": 0x400000}
 
 
 @pytest.fixture(scope="module")

@@ -163,6 +163,48 @@ def test_device_misaligned_pointers(P, dev):
                 assert (int(last.item()) & 0xFFFFFFFF) == int(v[-1])
 
 
+@pytest.mark.parametrize("flags", [0, 0x400000])
+def test_dense_delta_streams(dev, flags):
+    """Dense delta streams (every delta < 256: ceil(n/4) + n bytes) decode without a control
+    scan, with implicit offsets (flag 0x400000 forces the scan): exact against the oracle at
+    every tile/sub-tile boundary and tail, through the device API, and a stream of dense
+    length whose control bytes are not all zero is reported as truncated."""
+    import ctypes as C
+    import torch
+    from paper_1709_08990_b200._native import lib
+    lib.bcgpu_debug_set_flags.argtypes = [C.c_void_p, C.c_uint32]
+    rng = np.random.default_rng(11)
+    lib.bcgpu_debug_set_flags(dev._ctx, flags)
+    try:
+        for n in (1, 3, 4, 5, 1023, 1024, 1025, 8191, 8192, 8193, 65536 * 3 + 5, 2_500_001):
+            prev = int(rng.integers(0, 2**32))
+            v = (prev + np.cumsum(rng.integers(0, 256, n, dtype=np.uint64))).astype(np.uint32)
+            enc = oracle.encode(v, delta=True, prev=prev)
+            assert len(enc) == (n + 3) // 4 + n
+            d_in = torch.from_numpy(np.frombuffer(enc, np.uint8).copy()).cuda()
+            d_o = torch.zeros(n, dtype=torch.int32, device="cuda")
+            d_last = torch.zeros(1, dtype=torch.int32, device="cuda")
+            dev.decode(d_in, n, d_o, delta=True, base=prev, last=d_last)
+            dev.check()
+            assert np.array_equal(d_o.cpu().numpy().view(np.uint32), v), (n, flags)
+            assert int(d_last.item()) & 0xFFFFFFFF == int(v[-1])
+        # dense length, one control field non-zero (one delta >= 256, its stream cut by a byte)
+        for n, at in ((100_000, 77_777), (9000, 8999), (8192 * 5, 3)):
+            g = rng.integers(0, 256, n, dtype=np.uint64)
+            g[at] = 300
+            v = np.cumsum(g).astype(np.uint32)
+            enc = oracle.encode(v, delta=True, prev=0)
+            bad = np.frombuffer(enc[:-1], np.uint8).copy()
+            assert bad.size == (n + 3) // 4 + n
+            d_o = torch.zeros(n, dtype=torch.int32, device="cuda")
+            dev.decode(torch.from_numpy(bad).cuda(), n, d_o, delta=True, base=0)
+            with pytest.raises(Exception) as e:
+                dev.check()
+            assert "truncated" in str(e.value), (n, at, str(e.value))
+    finally:
+        lib.bcgpu_debug_set_flags(dev._ctx, 0)
+
+
 @pytest.mark.parametrize("flags", [16, 32, 4096])
 def test_encode_both_paths(dev, flags):
     """Every single-array encode path, whichever the dispatch picks for the stream kind:
