@@ -193,3 +193,29 @@ def test_mt_reference_matches_o1():
         out = np.empty((v.size + 3) // 4 + 4 * v.size + 1, np.uint8)
         m = oracle.mt_encode(v, delta=True, threads=th, out=out)
         assert out[:m].tobytes() == ref
+
+
+def test_paper_mode_decode():
+    """The paper's timing mode: O2 decode into a reused 4096-integer buffer,
+    single segments and batches; the check value is the sum of each block's last integer."""
+    rng = np.random.default_rng(21)
+    buf = np.empty(4096, np.uint32)
+    for n, delta in ((1, False), (4095, True), (4096, False), (4097, True), (100_003, True), (50_000, False)):
+        v = np.cumsum(rng.integers(0, 1000, n)).astype(np.uint32) if delta else \
+            rng.integers(0, 2**32, n, dtype=np.uint64).astype(np.uint32) >> rng.integers(0, 32, n).astype(np.uint32)
+        enc = oracle.encode(v, delta=delta, prev=3)
+        st, chk = oracle.paper_decode(enc, n, delta, 3, buf)
+        idx = np.minimum(np.arange(0, n, 4096) + 4095, n - 1)
+        assert st == oracle.OK and chk == int(v[idx].astype(np.uint64).sum()) % (1 << 64)
+        assert oracle.paper_decode(enc[:-1], n, delta, 3, buf)[0] == oracle.TRUNCATED
+    # batch form over the bcgpu_decode_segment layout
+    segs_v = [np.cumsum(rng.integers(1, 300, k)).astype(np.uint32) for k in (5, 4096, 9000, 1)]
+    encs = [oracle.encode(x, delta=True, prev=0) for x in segs_v]
+    dt = np.dtype([("src_offset", "<u8"), ("src_bytes", "<u8"), ("dst_offset", "<u8"), ("n", "<u4"), ("prev", "<u4")])
+    ds = np.zeros(len(encs), dt)
+    ds["src_offset"] = np.concatenate([[0], np.cumsum([len(e) for e in encs])[:-1]])
+    ds["src_bytes"] = [len(e) for e in encs]
+    ds["n"] = [x.size for x in segs_v]
+    st, chk = oracle.paper_decode_batch(ds, b"".join(encs), True, buf)
+    want = sum(int(x[np.minimum(np.arange(0, x.size, 4096) + 4095, x.size - 1)].astype(np.uint64).sum()) for x in segs_v)
+    assert st == oracle.OK and chk == want % (1 << 64)
