@@ -88,8 +88,8 @@ __device__ __forceinline__ void pack_group_row(const uint4& x, uint32_t c, uint3
     if (p3) sts32(wa + 12, W3);
 }
 
-// Packed bytes [src, src + len) of shared memory (16-B aligned, >= 16 readable bytes after
-// the end) -> global dst at any alignment.  Interior 16-B granules of the destination are
+// Packed bytes [src, src + len) of shared memory (>= 32 readable bytes after the end) -> global
+// dst at any alignment.  Interior 16-B granules of the destination are
 // funnel-shifted out of five shared words each and stored with 128-bit stores; the < 16
 // bytes before the first and after the last aligned granule are single-byte stores of one
 // lane each.
@@ -101,15 +101,35 @@ __device__ __forceinline__ void store_realigned2(uint32_t src, uint32_t len, uin
     const uint32_t head = (uint32_t)((A0 < Dend ? A0 : Dend) - D);  // bytes before the first aligned granule
     // interior granules [A0, A1): destination byte a comes from src + (a - D)
     if (A1 > A0) {
+        // source granule k = bytes [s0 + 16 k, +16): two 128-bit loads of the aligned 32 bytes
+        // around it (consecutive lanes read consecutive chunks: no bank conflicts, where five
+        // word loads 16 B apart were 4-way conflicted), then a funnel shift by the source's
+        // 16-B phase, which is the same for every lane (a uniform switch, no selects)
         const uint32_t ng = (uint32_t)((A1 - A0) >> 4);
         const uint32_t s0 = src + head;                 // source of the first interior byte
-        const uint32_t r = (s0 & 3u) << 3;
+        const uint32_t r = (s0 & 3u) << 3, q = (s0 >> 2) & 3u;
+        const uint32_t c0 = s0 & ~15u;
         for (uint32_t k = lane; k < ng; k += 32) {
-            const uint32_t wa = (s0 + 16 * k) & ~3u;
-            const uint32_t w0 = lds32v(wa), w1 = lds32v(wa + 4), w2 = lds32v(wa + 8), w3 = lds32v(wa + 12),
-                           w4 = lds32v(wa + 16);
-            const uint4 v = make_uint4(__funnelshift_r(w0, w1, r), __funnelshift_r(w1, w2, r),
-                                       __funnelshift_r(w2, w3, r), __funnelshift_r(w3, w4, r));
+            const uint4 lo = lds128v(c0 + 16 * k), hi = lds128v(c0 + 16 * k + 16);
+            uint4 v;
+            switch (q) {
+                case 0:
+                    v = make_uint4(__funnelshift_r(lo.x, lo.y, r), __funnelshift_r(lo.y, lo.z, r),
+                                   __funnelshift_r(lo.z, lo.w, r), __funnelshift_r(lo.w, hi.x, r));
+                    break;
+                case 1:
+                    v = make_uint4(__funnelshift_r(lo.y, lo.z, r), __funnelshift_r(lo.z, lo.w, r),
+                                   __funnelshift_r(lo.w, hi.x, r), __funnelshift_r(hi.x, hi.y, r));
+                    break;
+                case 2:
+                    v = make_uint4(__funnelshift_r(lo.z, lo.w, r), __funnelshift_r(lo.w, hi.x, r),
+                                   __funnelshift_r(hi.x, hi.y, r), __funnelshift_r(hi.y, hi.z, r));
+                    break;
+                default:
+                    v = make_uint4(__funnelshift_r(lo.w, hi.x, r), __funnelshift_r(hi.x, hi.y, r),
+                                   __funnelshift_r(hi.y, hi.z, r), __funnelshift_r(hi.z, hi.w, r));
+                    break;
+            }
             *reinterpret_cast<uint4*>(A0 + 16 * (uintptr_t)k) = v;
         }
     }
