@@ -63,12 +63,16 @@ __device__ __forceinline__ void mbar_wait_parity_sleep(uint64_t* bar, uint32_t p
 
 // a wait expected to take a while (a service warp waiting for a whole round of consumer
 // work): poll with a longer back-off so the spin takes few issue slots
+// (mbarrier.try_wait with a suspend-time hint: the warp is descheduled until the phase
+// completes or the hint expires, instead of polling; __nanosleep may return at once)
 __device__ __forceinline__ void mbar_wait_parity_lazy(uint64_t* bar, uint32_t parity, uint32_t max_ns) {
-    uint32_t ns = 64;
-    while (!mbar_test_parity(bar, parity)) {
-        __nanosleep(ns);
-        ns = ns < max_ns ? 2 * ns : max_ns;
-    }
+    asm volatile(
+        "{\n\t.reg .pred p;\n"
+        "LAZY_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n\t"
+        "@!p bra LAZY_%=;\n}" ::"r"(smem_addr(bar)),
+        "r"(parity), "r"(max_ns * 8u)
+        : "memory");
 }
 
 __device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
