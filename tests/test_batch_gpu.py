@@ -248,9 +248,13 @@ def test_encode_small_values_and_wide_values(dev):
 def test_encode_capacity_too_small(dev):
     from paper_1709_08990_b200.codec import GpuError
     rng = np.random.default_rng(9)
-    _run_encode(dev, [10, 500, 20], True, rng, cap_short=1, hint=0)
+    want, dst, d_out, d_lens = _run_encode(dev, [10, 500, 20], True, rng, cap_short=1, hint=0)
     with pytest.raises(GpuError, match="(?i)invalid"):
         dev.check()
+    # the short segment writes nothing and reports length 0 (callers packing by the lengths
+    # stay in bounds); the others are encoded as usual
+    lens = d_lens.cpu().numpy()
+    assert lens[1] == 0 and lens[0] == len(want[0]) and lens[2] == len(want[2])
 
 
 @pytest.mark.parametrize("ring_kb", [0, 8, 9, 13, 23])

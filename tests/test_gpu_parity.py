@@ -246,6 +246,15 @@ def test_block_offsets_and_random_access(P):
             ref = oracle.decode_block(enc, n, int(k), int(want[k]))
             assert cnts[j] == len(ref) and list(vals[j, :cnts[j]]) == list(ref)
     assert list(P.svb_decode_block(oracle.encode(np.array([1, 2, 300], np.uint32)), 3, 0, 0)) == [1, 2, 300]
+    # svb_decode_block's contract on host data: a block past ceil(n/4) is out_of_range, a block
+    # whose bytes lie past the end of the stream is truncated
+    enc3 = oracle.encode(np.array([1, 2, 300, 70000, 5], np.uint32))
+    with pytest.raises(P.CodecError) as e:
+        P.svb_decode_block(enc3, 5, 2, 0)
+    assert e.value.code == P.errc.out_of_range
+    with pytest.raises(P.CodecError) as e:
+        P.svb_decode_block(enc3[:-2], 5, 1, 7)
+    assert e.value.code == P.errc.truncated
 
 
 # ---- BASELINE.json configs (scaled where the oracle needs it) ---------------
