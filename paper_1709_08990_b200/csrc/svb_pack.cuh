@@ -28,6 +28,13 @@ __device__ __forceinline__ uint32_t shfl_l(uint32_t lo, uint32_t hi, uint32_t s)
     return __funnelshift_l(lo, hi, s);
 }
 
+// predicated shared store (no branch around it)
+__device__ __forceinline__ void sts32_if(uint32_t a, uint32_t v, bool pred) {
+    asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %2, 0;\n\t@p st.shared.u32 [%0], %1;\n\t}" ::"r"(a), "r"(v),
+                 "r"((uint32_t)pred)
+                 : "memory");
+}
+
 // byte_length - 1 of the four integers -> control byte (field i in bits 2i..2i+1);
 // tot = the group's data bytes
 __device__ __forceinline__ uint32_t group_ctrl(const uint4& x, uint32_t& tot) {
@@ -83,9 +90,9 @@ __device__ __forceinline__ void pack_group_row(const uint4& x, uint32_t c, uint3
     carry = __shfl_sync(kFull, pend, 31);
     const uint32_t wa = a & ~3u;
     sts32(wa, W0 | pin);
-    if (p1) sts32(wa + 4, W1);
-    if (p2) sts32(wa + 8, W2);
-    if (p3) sts32(wa + 12, W3);
+    sts32_if(wa + 4, W1, p1);
+    sts32_if(wa + 8, W2, p2);
+    sts32_if(wa + 12, W3, p3);
 }
 
 // Packed bytes [src, src + len) of shared memory (>= 32 readable bytes after the end) -> global
