@@ -627,10 +627,10 @@ __device__ __forceinline__ void encode_block(uint32_t Sin, uint32_t blk, uint32_
         if (lane == 0) pin = carry;
         carry = __shfl_sync(0xffffffffu, pend, 31);
         const uint32_t wa = o & ~3u;
-        if (kFB || nw > 0) sts32(wa, W0 | pin);
-        if (nw > 1) sts32(wa + 4, W1);
-        if (nw > 2) sts32(wa + 8, W2);
-        if (nw > 3) sts32(wa + 12, W3);
+        sts32_if(wa, W0 | pin, kFB || nw > 0);
+        sts32_if(wa + 4, W1, nw > 1);
+        sts32_if(wa + 8, W2, nw > 2);
+        sts32_if(wa + 12, W3, nw > 3);
         // the piece's last group leaves its partial word (in a full block only when the piece
         // ends on a block: warp-uniform test first)
         if ((!kFB || (blk + 3) * 32 >= ng) && g + 1 == ng && ((o + tot) & 3u))

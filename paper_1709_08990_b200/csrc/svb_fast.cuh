@@ -42,6 +42,12 @@ __device__ __forceinline__ void sts8(uint32_t a, uint32_t v) {
 __device__ __forceinline__ void sts32(uint32_t a, uint32_t v) {
     asm volatile("st.shared.u32 [%0], %1;" ::"r"(a), "r"(v) : "memory");
 }
+// predicated shared store (no branch around it)
+__device__ __forceinline__ void sts32_if(uint32_t a, uint32_t v, bool pred) {
+    asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %2, 0;\n\t@p st.shared.u32 [%0], %1;\n\t}" ::"r"(a), "r"(v),
+                 "r"((uint32_t)pred)
+                 : "memory");
+}
 
 // Control bytes of a full sub-tile at shared address sc (row j, lane l <-> byte 32j + l).
 // Sets *all_zero (warp-uniform) and skips the offset scan when every control byte is 0:
@@ -519,9 +525,9 @@ __device__ __forceinline__ uint32_t pack_group_words(const uint4& x, uint32_t L,
     carry = __shfl_sync(kFull, pend, 31);
     const uint32_t wa = o & ~3u;
     sts32(wa, W0 | pin);
-    if (nw > 1) sts32(wa + 4, W1);
-    if (nw > 2) sts32(wa + 8, W2);
-    if (nw > 3) sts32(wa + 12, W3);
+    sts32_if(wa + 4, W1, nw > 1);
+    sts32_if(wa + 8, W2, nw > 2);
+    sts32_if(wa + 12, W3, nw > 3);
     return pend;
 }
 

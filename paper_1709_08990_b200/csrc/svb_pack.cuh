@@ -28,13 +28,6 @@ __device__ __forceinline__ uint32_t shfl_l(uint32_t lo, uint32_t hi, uint32_t s)
     return __funnelshift_l(lo, hi, s);
 }
 
-// predicated shared store (no branch around it)
-__device__ __forceinline__ void sts32_if(uint32_t a, uint32_t v, bool pred) {
-    asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %2, 0;\n\t@p st.shared.u32 [%0], %1;\n\t}" ::"r"(a), "r"(v),
-                 "r"((uint32_t)pred)
-                 : "memory");
-}
-
 // byte_length - 1 of the four integers -> control byte (field i in bits 2i..2i+1);
 // tot = the group's data bytes
 __device__ __forceinline__ uint32_t group_ctrl(const uint4& x, uint32_t& tot) {
