@@ -52,14 +52,16 @@ __device__ __forceinline__ uint4 group_bytes(const uint4& x, uint32_t c, uint32_
     const uint32_t B1 = __funnelshift_lc(x.w, 0u, sB);
     const uint32_t la8 = sA + ((c << 1) & 0x18u) + 8u;  // 8 (l0 + l1), 16..64
     e8 = la8 + sB + ((c >> 3) & 0x18u) + 8u;
-    const uint32_t tb = la8 & 31u;
-    const bool k1 = la8 >= 32u, k2 = la8 == 64u;       // B starts in word 1 / word 2
-    const uint32_t Z0 = B0 << tb, Z1 = shfl_l(B0, B1, tb), Z2 = shfl_l(B1, 0u, tb);
+    // B << 8 (l0 + l1) over four words: shift B by t = la8 (la8 < 32) or la8 - 32 (la8 >= 32,
+    // then one word up); clamped funnel shifts make t = 32 (la8 = 64) land B in words 2-3
+    const bool k1 = la8 >= 32u;                         // B starts in word 1 (or 2 when la8 = 64)
+    const uint32_t t = k1 ? la8 - 32u : la8;             // 0..32
+    const uint32_t Z0 = __funnelshift_lc(0u, B0, t), Z1 = __funnelshift_lc(B0, B1, t), Z2 = __funnelshift_lc(B1, 0u, t);
     uint4 G;
     G.x = A0 | (k1 ? 0u : Z0);
-    G.y = A1 | (k1 ? (k2 ? 0u : Z0) : Z1);
-    G.z = k1 ? (k2 ? Z0 : Z1) : Z2;
-    G.w = k1 ? (k2 ? Z1 : Z2) : 0u;
+    G.y = A1 | (k1 ? Z0 : Z1);
+    G.z = k1 ? Z1 : Z2;
+    G.w = k1 ? Z2 : 0u;
     return G;
 }
 
