@@ -474,8 +474,6 @@ struct __align__(16) EWarpHdr {
     uint8_t ctrl[2][kECtrlBuf];
 };
 
-__device__ __forceinline__ uint32_t shl_c(uint32_t x, uint32_t s) { return __funnelshift_lc(0u, x, s); }  // s <= 32
-__device__ __forceinline__ uint32_t shr_c(uint32_t x, uint32_t s) { return __funnelshift_rc(x, 0u, s); }  // s <= 32
 
 // global [g, g + len) <- shared bytes at sp (sp has g's 16-B phase): bulk store of the aligned
 // interior (committed by the caller), lanes store the edge bytes
@@ -575,66 +573,33 @@ __device__ __forceinline__ void encode_block(uint32_t Sin, uint32_t blk, uint32_
         // the piece's last group leaves its partial word (now in carry)
         if ((blk + 3) * 32 >= ng && lane == 0 && ((db + off) & 3u)) sts32((db + off) & ~3u, carry);
         return;
-    }
-    uint32_t L4[3], P = 0;
+    } else {
+        // the piece's last block: rows past its end skipped, groups past its end write nothing
+        // (except the lane right after the last group, which stores that group's pending word)
+        uint32_t C3[3], T3r[3], P3 = 0;
 #pragma unroll
-    for (int j = 0; j < 3; ++j) {
-        if (!kFB && blk + j >= rows) {
-            L4[j] = 0;
-            continue;
+        for (int j = 0; j < 3; ++j) {
+            uint32_t tot;
+            C3[j] = group_ctrl(d[j], tot);
+            const uint32_t cnt = cnts[j];
+            T3r[j] = cnt ? tot - (4u - cnt) : 0u;  // unused places count 1 byte in tot
+            if (cnt) sts8(cb + 32 * (blk + j) + lane, C3[j]);
+            P3 |= T3r[j] << (10 * j);
         }
-        const uint4 x = d[j];
-        const uint32_t g = 32 * (blk + j) + lane, cnt = cnts[j];
-        const uint32_t m0 = blen_m1(x.x), m1 = blen_m1(x.y), m2 = blen_m1(x.z), m3 = blen_m1(x.w);
-        // lengths (0 past the stream) one per byte; unused fields of a final partial control
-        // byte stay 0 (their integers are 0: length 1, field 0)
-        uint32_t L = (m0 + 1u) | ((m1 + 1u) << 8) | ((m2 + 1u) << 16) | ((m3 + 1u) << 24);
-        if (!kFB) L &= cnt >= 4 ? 0xFFFFFFFFu : ((1u << (8 * cnt)) - 1u);
-        if (kFB || cnt) sts8(cb + g, m0 | (m1 << 2) | (m2 << 4) | (m3 << 6));
-        L4[j] = L;
-        P |= __dp4a(L, 0x01010101u, 0u) << (10 * j);
-    }
-    const uint32_t I = warp_inclusive_scan(P);
-    const uint32_t T = __shfl_sync(0xffffffffu, I, 31), E = I - P;
-    __syncwarp();  // every lane has read the block's integers before any lane packs over them
+        const uint32_t I3 = warp_inclusive_scan(P3);
+        const uint32_t T3 = __shfl_sync(0xffffffffu, I3, 31), E3 = I3 - P3;
+        __syncwarp();  // every lane has read the block's integers before any lane packs over them
 #pragma unroll
-    for (int j = 0; j < 3; ++j) {
-        const uint32_t row = blk + j;
-        if (!kFB && row >= rows) break;
-        const uint32_t g = 32 * row + lane;
-        const uint32_t L = L4[j];
-        const uint32_t tot = __dp4a(L, 0x01010101u, 0u);
-        const uint32_t o = db + off + ((E >> (10 * j)) & 0x3FFu);  // shared byte of the group's data
-        off += (T >> (10 * j)) & 0x3FFu;
-        const uint4 x = d[j];
-        // pack the group: A = d0 ++ d1, B = d2 ++ d3 (64-bit), P = A ++ B (128-bit)
-        const uint32_t l0 = L & 0xFFu, l1 = (L >> 8) & 0xFFu, l2 = (L >> 16) & 0xFFu;
-        const uint32_t Alo = x.x | shl_c(x.y, 8 * l0), Ahi = shr_c(x.y, 32 - 8 * l0);
-        const uint32_t Blo = x.z | shl_c(x.w, 8 * l2), Bhi = shr_c(x.w, 32 - 8 * l2);
-        const uint32_t t = 8 * (l0 + l1);  // 0..64
-        const bool hi = t >= 32;
-        const uint32_t tt = hi ? t - 32 : t;
-        const uint32_t q0 = shl_c(Blo, tt), q1 = __funnelshift_lc(Blo, Bhi, tt), q2 = shr_c(Bhi, 32 - tt);
-        const uint32_t P0 = Alo | (hi ? 0u : q0), P1 = Ahi | (hi ? q0 : q1), P2 = hi ? q1 : q2, P3 = hi ? q2 : 0u;
-        // onto the word grid: word k of the group = bytes [4k - u, 4k - u + 4) of P
-        const uint32_t u8 = (o & 3u) << 3;
-        const uint32_t W0 = shl_c(P0, u8), W1 = __funnelshift_lc(P0, P1, u8), W2 = __funnelshift_lc(P1, P2, u8),
-                       W3 = __funnelshift_lc(P2, P3, u8), W4 = __funnelshift_lc(P3, 0u, u8);
-        const uint32_t nw = ((o & 3u) + tot) >> 2;  // words this group completes (0 past the stream)
-        // a full block's groups hold >= 4 bytes, so nw >= 1
-        const uint32_t pend = nw == 1 ? W1 : nw == 2 ? W2 : nw == 3 ? W3 : (kFB || nw == 4) ? W4 : W0;
-        uint32_t pin = __shfl_up_sync(0xffffffffu, pend, 1);
-        if (lane == 0) pin = carry;
-        carry = __shfl_sync(0xffffffffu, pend, 31);
-        const uint32_t wa = o & ~3u;
-        sts32_if(wa, W0 | pin, kFB || nw > 0);
-        sts32_if(wa + 4, W1, nw > 1);
-        sts32_if(wa + 8, W2, nw > 2);
-        sts32_if(wa + 12, W3, nw > 3);
-        // the piece's last group leaves its partial word (in a full block only when the piece
-        // ends on a block: warp-uniform test first)
-        if ((!kFB || (blk + 3) * 32 >= ng) && g + 1 == ng && ((o + tot) & 3u))
-            sts32((o + tot) & ~3u, nw ? pend : (pend | pin));
+        for (int j = 0; j < 3; ++j) {
+            if (blk + j >= rows) break;  // warp-uniform
+            const uint32_t g = 32 * (blk + j) + lane;
+            const uint32_t o = db + off + ((E3 >> (10 * j)) & 0x3FFu);
+            off += (T3 >> (10 * j)) & 0x3FFu;
+            pack_group_row_masked(d[j], C3[j], o, carry, T3r[j], g <= ng);
+        }
+        // a last row that ends with lane 31 left the last group's pending word in carry
+        if ((ng & 31u) == 0 && lane == 0 && ((db + off) & 3u)) sts32((db + off) & ~3u, carry);
+        return;
     }
 }
 

@@ -143,6 +143,38 @@ __device__ __forceinline__ void store_realigned2(uint32_t src, uint32_t len, uin
     }
 }
 
+// pack_group_row for a row that may end early: tot = the group's real data bytes (0 for a lane
+// past the last group; a last group of cnt < 4 integers has zero integers -- control fields 0
+// -- in its unused places, whose bytes are left out), w0 = whether this lane stores its first
+// word: every group lane, and the one lane right after the last group, which stores the last
+// group's pending word (its own W0 is 0).  Lanes further on store nothing.
+__device__ __forceinline__ void pack_group_row_masked(const uint4& x, uint32_t c, uint32_t a, uint32_t& carry,
+                                                      uint32_t tot, bool w0) {
+    const int lane = threadIdx.x & 31;
+    uint32_t e8;
+    const uint4 G = group_bytes(x, c, e8);
+    const uint32_t u = (a & 3u) << 3;
+    const uint32_t W0 = G.x << u, W1 = shfl_l(G.x, G.y, u), W2 = shfl_l(G.y, G.z, u), W3 = shfl_l(G.z, G.w, u),
+                   W4 = shfl_l(G.w, 0u, u);
+    e8 = 8u * tot + u;
+    // a group of < 4 bytes (the last, partial group; tot = 0 past it) may end inside its first
+    // word: that word is then its pending one, merged with the word it received, and the next
+    // lane needs the merged value -- a second shuffle (such groups are never adjacent)
+    const bool p0 = e8 >= 32u, p1 = e8 >= 64u, p2 = e8 >= 96u, p3 = e8 >= 128u;
+    const uint32_t pend0 = p3 ? W4 : p2 ? W3 : p1 ? W2 : W1;
+    uint32_t pin = __shfl_up_sync(kFull, pend0, 1);
+    if (lane == 0) pin = carry;
+    const uint32_t pend = p0 ? pend0 : (W0 | pin);
+    uint32_t pin2 = __shfl_up_sync(kFull, pend, 1);
+    if (lane == 0) pin2 = carry;
+    carry = __shfl_sync(kFull, pend, 31);
+    const uint32_t wa = a & ~3u;
+    sts32_if(wa, W0 | pin2, w0 && (p0 || tot == 0u));
+    sts32_if(wa + 4, W1, p1);
+    sts32_if(wa + 8, W2, p2);
+    sts32_if(wa + 12, W3, p3);
+}
+
 // Packed bytes at shared sdst (sdst has dst's 16-B phase), len bytes -> global dst: one bulk
 // copy of the 16-B aligned interior (lane 0 issues and commits it; the caller waits for its
 // smem read before reusing the buffer), lanes store the < 16 edge bytes at each end.  Every
