@@ -33,6 +33,12 @@ namespace bcgpu {
 
 namespace {
 
+#ifndef BC_DEC3_MODE
+#define BC_DEC3_MODE 1  // 1: four groups per lane in every pass (measured best); 0: a k-groups-per-lane last pass; 2: runtime k in every pass
+#endif
+#ifndef BC_DEC3_MINB
+#define BC_DEC3_MINB 5  // decode CTAs per SM the register budget must allow (6 spills)
+#endif
 constexpr int kRWarps = 4;
 constexpr int kRThreads = 32 * kRWarps;
 constexpr uint32_t kRingDefault = 8192;   // ring bytes per warp (launch-time; >= kItemMax)
@@ -291,10 +297,271 @@ __device__ __forceinline__ uint32_t decode_resident(uint32_t S, uint32_t bytes, 
     return off;
 }
 
+// ---- decode v2: fewer instructions per group -------------------------------------------
+// x zero-extended from its low b bits (b clamped to 32): one SGXT instead of a mask shift + AND
+__device__ __forceinline__ uint32_t szext(uint32_t x, uint32_t b) {
+    uint32_t r;
+    asm("szext.clamp.u32 %0, %1, %2;" : "=r"(r) : "r"(x), "r"(b));
+    return r;
+}
+
+// Inclusive warp scan whose steps add under the shuffle's own in-range predicate (two
+// instructions per step instead of shuffle + lane compare + select + add).
+__device__ __forceinline__ uint32_t warp_scan_p(uint32_t v) {
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1)
+        asm("{\n\t.reg .pred p;\n\t.reg .u32 t;\n\t"
+            "shfl.sync.up.b32 t|p, %0, %1, 0, 0xffffffff;\n\t"
+            "@p add.u32 %0, %0, t;\n\t}"
+            : "+r"(v)
+            : "r"(o));
+    return v;
+}
+
+// One control byte c whose data starts at shared byte address a -> 4 integers.  The group's
+// 16 bytes X0..X3 act as a queue: integer i is the queue's low l_i bytes (SGXT by 8 l_i), then
+// the queue drops them (clamped funnel shifts: 8 l_i = 32 moves a whole word).  Each step
+// needs one word less, so the four integers cost 4 SGXT + 6 funnel shifts, with no selects
+// (group_w5 picks each integer's word pair with compare + select chains).
+// Shared word at a when pred, else 0 (a predicated load: no branch).
+__device__ __forceinline__ uint32_t lds32_if(uint32_t a, bool pred) {
+    uint32_t v = 0;
+    asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %2, 0;\n\t@p ld.shared.u32 %0, [%1];\n\t}"
+                 : "+r"(v)
+                 : "r"(a), "r"((uint32_t)pred));
+    return v;
+}
+
+// len = the group's data bytes: only the words they touch are loaded (cfg4 groups average ~10
+// bytes, ~3.4 of the five words; every window load is ~4-way bank-conflicted, and shared-memory
+// wavefronts bound this kernel once the ALU work is down)
+__device__ __forceinline__ uint4 group_q(uint32_t a, uint32_t c, uint32_t len) {
+    const uint32_t wa = a & ~3u, sh = (a & 3u) << 3;
+    const uint32_t e = (a & 3u) + len;  // window bytes in use
+    const uint32_t w0 = lds32(wa), w1 = lds32_if(wa + 4, e > 4), w2 = lds32_if(wa + 8, e > 8),
+                   w3 = lds32_if(wa + 12, e > 12), w4 = lds32_if(wa + 16, e > 16);
+    const uint32_t X0 = __funnelshift_r(w0, w1, sh), X1 = __funnelshift_r(w1, w2, sh),
+                   X2 = __funnelshift_r(w2, w3, sh), X3 = __funnelshift_r(w3, w4, sh);
+    const uint32_t b0 = ((c << 3) & 0x18u) + 8u, b1 = ((c << 1) & 0x18u) + 8u, b2 = ((c >> 1) & 0x18u) + 8u,
+                   b3 = ((c >> 3) & 0x18u) + 8u;  // 8 l_i
+    uint4 v;
+    v.x = szext(X0, b0);
+    const uint32_t Y0 = __funnelshift_rc(X0, X1, b0), Y1 = __funnelshift_rc(X1, X2, b0),
+                   Y2 = __funnelshift_rc(X2, X3, b0);
+    v.y = szext(Y0, b1);
+    const uint32_t Z0 = __funnelshift_rc(Y0, Y1, b1), Z1 = __funnelshift_rc(Y1, Y2, b1);
+    v.z = szext(Z0, b2);
+    v.w = szext(__funnelshift_rc(Z0, Z1, b2), b3);
+    return v;
+}
+
+// Vector stores of the whole granules among a lane's groups g0 .. g0 + k - 1 (k = K, or the
+// runtime k when K = 0; see store_pass for the granule layout).  K = 4: pairs on a 32-B
+// boundary leave as one 256-bit store.  Granules that straddle the segment's ends are left
+// to edge_stores, so each phase's block is a few predicated stores.
+template <uint32_t R, int K>
+__device__ __forceinline__ void store_whole(const uint4 (&v)[4], uint32_t* __restrict__ o, uint32_t g0, uint32_t k,
+                                            int nints, uint4& carry) {
+    const int lane = threadIdx.x & 31;
+    const uint32_t kk = K ? (uint32_t)K : k;
+    uint4 G[4];
+    uint32_t* Bp = o - R;  // 16-B aligned
+    if constexpr (R == 0) {
+#pragma unroll
+        for (int j = 0; j < 4; ++j) G[j] = v[j];
+    } else {
+        uint4 vl;  // the lane's last group
+        if constexpr (K == 4)
+            vl = v[3];
+        else
+            vl = kk == 1 ? v[0] : kk == 2 ? v[1] : kk == 3 ? v[2] : v[3];
+        const int src = (lane + 31) & 31;
+        uint4 rot = make_uint4(0, 0, 0, 0);
+        rot.w = __shfl_sync(kFull, vl.w, src);
+        if (R >= 2) rot.z = __shfl_sync(kFull, vl.z, src);
+        if (R >= 3) rot.y = __shfl_sync(kFull, vl.y, src);
+        const uint4 prv0 = lane == 0 ? carry : rot;
+        carry = rot;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const uint4 pv = j == 0 ? prv0 : v[j - 1], cv = v[j];
+            G[j] = R == 1 ? make_uint4(pv.w, cv.x, cv.y, cv.z)
+                 : R == 2 ? make_uint4(pv.z, pv.w, cv.x, cv.y)
+                          : make_uint4(pv.y, pv.z, pv.w, cv.x);
+        }
+    }
+    bool f[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+        const int e0 = 4 * (int)(g0 + j) - (int)R;
+        f[j] = (K || (uint32_t)j < kk) && e0 >= 0 && e0 + 4 <= nints;
+    }
+    if constexpr (K == 4) {
+        if ((((uintptr_t)(Bp + 4 * g0)) & 31) == 0) {  // warp-uniform (g0 even): pairs (0,1), (2,3)
+#pragma unroll
+            for (int j = 0; j < 4; j += 2) {
+                if (f[j] && f[j + 1]) {
+                    stg_stream_v8(Bp + 4 * (g0 + j), G[j], G[j + 1]);
+                } else {
+                    if (f[j]) stg_stream_v4(Bp + 4 * (g0 + j), G[j]);
+                    if (f[j + 1]) stg_stream_v4(Bp + 4 * (g0 + j + 1), G[j + 1]);
+                }
+            }
+        } else {  // pair (1,2)
+            if (f[0]) stg_stream_v4(Bp + 4 * g0, G[0]);
+            if (f[1] && f[2]) {
+                stg_stream_v8(Bp + 4 * (g0 + 1), G[1], G[2]);
+            } else {
+                if (f[1]) stg_stream_v4(Bp + 4 * (g0 + 1), G[1]);
+                if (f[2]) stg_stream_v4(Bp + 4 * (g0 + 2), G[2]);
+            }
+            if (f[3]) stg_stream_v4(Bp + 4 * (g0 + 3), G[3]);
+        }
+    } else {
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+            if (f[j]) stg_stream_v4(Bp + 4 * (g0 + j), G[j]);
+    }
+}
+
+// The integers no whole granule holds: the head granule's [0, 4 - R) (R != 0) and the tail
+// [T, n), T = the start of the last, partial granule.  Phase-independent (one copy), element
+// stores from the lane that decoded them; at most two lanes of a segment take the branch.
+template <int K>
+__device__ __forceinline__ void edge_stores(const uint4 (&v)[4], uint32_t* __restrict__ o, uint32_t g0, uint32_t k,
+                                            int n, uint32_t R, int T) {
+    const uint32_t kk = K ? (uint32_t)K : k;
+    const int lo = 4 * (int)g0, hi = lo + 4 * (int)kk;
+    const int head = R ? (4 - (int)R < n ? 4 - (int)R : n) : 0;
+    if ((lo < head) || (hi > T && lo < n)) {
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            if (K || (uint32_t)j < kk) {
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                    const int e = lo + 4 * j + i;
+                    if (e < n && (e < head || e >= T)) o[e] = comp(v[j], i);
+                }
+            }
+        }
+    }
+}
+
+// One pass of decode_resident2: lane l owns groups g0 .. g0 + k - 1 (g0 = gp + k l) of the
+// pass starting at group gp.  Full passes (and a last pass of 128 groups) are K = 4; a
+// shorter last pass uses K = 0 with k = ceil(groups left / 32), so it costs k groups per
+// lane, not four.  Groups past the segment's end decode garbage that is never stored: it
+// only follows the valid integers in lane order, so no position, delta prefix or store of a
+// valid integer sees it.
+template <bool kDelta, int K>
+__device__ __forceinline__ void decode_pass(uint32_t S, uint32_t D, uint32_t Dend, uint32_t ng, uint32_t n,
+                                            uint32_t tail, uint32_t tmask, uint32_t gp, uint32_t k, bool lastp,
+                                            uint32_t R, int T, uint32_t& off, uint32_t& run, uint4& carry,
+                                            uint32_t* __restrict__ o) {
+    const int lane = threadIdx.x & 31;
+    const uint32_t kk = K ? (uint32_t)K : k;
+    const uint32_t g0 = gp + kk * lane;
+    const uint32_t ca = S + g0;
+    uint32_t cw = __funnelshift_r(lds32(ca & ~3u), lds32((ca & ~3u) + 4), (ca & 3u) << 3);
+    uint32_t lens;
+    if (!lastp) {
+        lens = swar_lengths(cw);
+    } else {
+        // the lane's valid groups; the final group's unused fields and anything past it count 0
+        const uint32_t nv = ng > g0 ? (ng - g0 < kk ? ng - g0 : kk) : 0u;
+        const uint32_t bm = nv >= 4 ? 0xFFFFFFFFu : ((1u << (8 * nv)) - 1u);
+        const bool hl = nv && g0 + nv == ng;
+        if (hl) cw &= ~(0xFFu << (8 * (nv - 1))) | (tmask << (8 * (nv - 1)));
+        cw &= bm;
+        lens = swar_lengths(cw) & bm;
+        if (hl) lens -= (4u - tail) << (8 * (nv - 1));
+    }
+    const uint32_t lt = __dp4a(lens, 0x01010101u, 0u);  // <= 64
+    const uint32_t I = warp_scan_p(lt);
+    uint32_t p = D + off + I - lt;
+    off += __shfl_sync(kFull, I, 31);
+    uint4 v[4];
+    if (__all_sync(kFull, cw == 0)) {
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+            if (K || (uint32_t)j < kk) v[j] = zero_group_s(min(p + 4 * j, Dend));
+    } else {
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            if (K || (uint32_t)j < kk) {
+                const uint32_t lj = (lens >> (8 * j)) & 0xFFu;
+                v[j] = group_q(min(p, Dend), (cw >> (8 * j)) & 0xFFu, lj);
+                p += lj;
+            }
+        }
+    }
+    if constexpr (kDelta) {
+        uint32_t s = 0;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            if (K || (uint32_t)j < kk) {
+                v[j].x += s;
+                v[j].y += v[j].x;
+                v[j].z += v[j].y;
+                v[j].w += v[j].z;
+                s = v[j].w;
+            }
+        }
+        const uint32_t Iv = warp_scan_p(s);
+        const uint32_t add = run + Iv - s;
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+            if (K || (uint32_t)j < kk) v[j] = add4(v[j], add);
+        run += __shfl_sync(kFull, Iv, 31);
+    }
+    switch (R) {  // warp-uniform; only these small store blocks are per phase
+        case 0: store_whole<0, K>(v, o, g0, kk, (int)n, carry); break;
+        case 1: store_whole<1, K>(v, o, g0, kk, (int)n, carry); break;
+        case 2: store_whole<2, K>(v, o, g0, kk, (int)n, carry); break;
+        default: store_whole<3, K>(v, o, g0, kk, (int)n, carry); break;
+    }
+    // the pass holds the head or part of the tail (the tail can start in the pass before the last)
+    if (gp == 0 || 4 * (int)(gp + 32 * kk) > T) edge_stores<K>(v, o, g0, kk, (int)n, R, T);
+}
+
+// decode_resident with group_q, predicated scans, the k-groups-per-lane last pass (cfg4: 85% ->
+// 94% of the group slots hold integers) and the segment-edge stores out of the per-phase
+// store blocks.  Segments of <= 128 integers are one pass with k = 1.
+template <bool kDelta>
+__device__ __forceinline__ uint32_t decode_resident2(uint32_t S, uint32_t bytes, uint32_t n, uint32_t run,
+                                                     uint32_t* __restrict__ o) {
+    const uint32_t R = (uint32_t)(((uintptr_t)o >> 2) & 3u);
+    const uint32_t ng = (n + 3) >> 2;
+    const uint32_t tail = (n & 3u) ? (n & 3u) : 4u;
+    const uint32_t tmask = (n & 3u) ? ((1u << (2 * (n & 3u))) - 1u) : 0xFFu;
+    const uint32_t D = S + ng, Dend = S + bytes;
+    const int T = 4 * (int)((n + R) >> 2) - (int)R;  // the tail no whole granule holds: [T, n)
+    const uint32_t full_passes = (ng - 1) >> 7;       // every pass but the last holds 128 groups
+    const uint32_t gl = 128 * full_passes, kl = (ng - gl + 31) >> 5;
+    uint32_t off = 0;
+    uint4 carry = make_uint4(0, 0, 0, 0);
+#pragma unroll 1
+    for (uint32_t ps = 0;; ++ps) {
+        const bool lastp = ps == full_passes;
+#if BC_DEC3_MODE == 1
+        decode_pass<kDelta, 4>(S, D, Dend, ng, n, tail, tmask, 128 * ps, 4, lastp, R, T, off, run, carry, o);
+#elif BC_DEC3_MODE == 2
+        decode_pass<kDelta, 0>(S, D, Dend, ng, n, tail, tmask, 128 * ps, lastp ? kl : 4u, lastp, R, T, off, run, carry, o);
+#else
+        if (!lastp || kl == 4)
+            decode_pass<kDelta, 4>(S, D, Dend, ng, n, tail, tmask, 128 * ps, 4, lastp, R, T, off, run, carry, o);
+        else
+            decode_pass<kDelta, 0>(S, D, Dend, ng, n, tail, tmask, gl, kl, true, R, T, off, run, carry, o);
+#endif
+        if (lastp) break;
+    }
+    return off;
+}
+
 }  // namespace
 
-template <bool kDelta>
-__global__ void __launch_bounds__(kRThreads)
+template <bool kDelta, bool kV1>
+__global__ void __launch_bounds__(kRThreads, BC_DEC3_MINB)
     svb_decode_batch3_kernel(const bcgpu_decode_segment* __restrict__ segs, uint64_t nseg,
                              const uint8_t* __restrict__ in, uint32_t* __restrict__ out, unsigned long long* status,
                              uint32_t epoch, uint32_t long_hint, uint32_t ring_bytes) {
@@ -325,64 +592,71 @@ __global__ void __launch_bounds__(kRThreads)
         }
     };
     refill();
+    // Each lane also checks its own descriptor once per refill: info = its ring cover (decodes
+    // here) | the status it reports << 16 | 1 << 31 when the segment is not decoded here.
+    uint32_t info = 0;
+    auto check = [&]() {
+        const uint32_t n = (uint32_t)d3;
+        const uint64_t ngroups = ((uint64_t)n + 3) >> 2;
+        uint32_t code = 0;
+        if (n > kBatchSmallN)  // svb_batch2.cu decodes it -- unless the caller's max_seg_n said no segment is long
+            code = long_hint && n > long_hint ? (uint32_t)BCGPU_ERR_INVALID_ARGUMENT : 0u;
+        else if (n == 0)
+            code = d1 != 0 ? (uint32_t)BCGPU_ERR_TRAILING_BYTES : 0u;
+        else if (d1 < ngroups)
+            code = BCGPU_ERR_TRUNCATED;
+        else if (d1 > ngroups + 4ull * n)
+            code = BCGPU_ERR_TRAILING_BYTES;
+        const uintptr_t beg = (uintptr_t)in + d0;
+        const uint32_t cover = (uint32_t)(((beg + d1 + 15) & ~(uintptr_t)15) - (beg & ~(uintptr_t)15));
+        const bool here = n != 0 && n <= kBatchSmallN && code == 0;
+        info = here ? cover : (0x80000000u | (code << 16));
+    };
+    check();
     uint32_t di = 0;                // next descriptor of the batch (lane index)
     uint32_t head = 0, tail = 0;    // ring byte counters (allocated incl. wrap waste, freed)
     uint32_t hpos = 0;              // ring offset of the next allocation
     uint32_t qh = 0, qt = 0;        // items issued, consumed
     for (;;) {
-        // issue every segment that fits
+        // issue every segment that fits (a full ring leaves descriptor di pending: its check is
+        // per lane above, so a retry costs one shuffle)
         while (qh - qt < kRSlots && dbase + di < cnt) {
-            const unsigned long long src = __shfl_sync(kFull, d0, di), bytes = __shfl_sync(kFull, d1, di);
-            const unsigned long long dst = __shfl_sync(kFull, d2, di), np = __shfl_sync(kFull, d3, di);
-            const uint32_t n = (uint32_t)np;
-            bool take = false;
-            uint32_t at = 0, cover = 0, waste = 0;
-            uintptr_t a0 = 0;
-            if (n > kBatchSmallN) {
-                // svb_batch2.cu decodes it -- unless the caller's max_seg_n said no segment is long
-                if (long_hint && n > long_hint && lane == 0) report3(status, epoch, BCGPU_ERR_INVALID_ARGUMENT);
-            } else {
-                const uint64_t ngroups = ((uint64_t)n + 3) >> 2;
-                if (n == 0) {
-                    if (bytes != 0 && lane == 0) report3(status, epoch, BCGPU_ERR_TRAILING_BYTES);
-                } else if (bytes < ngroups) {
-                    if (lane == 0) report3(status, epoch, BCGPU_ERR_TRUNCATED);
-                } else if (bytes > ngroups + 4ull * n) {
-                    if (lane == 0) report3(status, epoch, BCGPU_ERR_TRAILING_BYTES);
-                } else {
-                    const uintptr_t beg = (uintptr_t)in + src;
-                    a0 = beg & ~(uintptr_t)15;
-                    cover = (uint32_t)(((beg + bytes + 15) & ~(uintptr_t)15) - a0);
-                    if (qh == qt) head = tail = hpos = 0;  // empty ring: restart at 0 (any item fits)
-                    const bool wrap = hpos + cover > ring_bytes;  // skip the ring's end (possibly 0 bytes)
-                    waste = wrap ? ring_bytes - hpos : 0u;
-                    at = wrap ? 0u : hpos;
-                    if (head + waste + cover - tail > ring_bytes) break;  // wait for space
-                    take = true;
-                }
-            }
-            if (take) {
+            const uint32_t inf = __shfl_sync(kFull, info, di);
+            if (!(inf & 0x80000000u)) {
+                const uint32_t cover = inf;
+                if (qh == qt) head = tail = hpos = 0;  // empty ring: restart at 0 (any item fits)
+                const bool wrap = hpos + cover > ring_bytes;  // skip the ring's end (possibly 0 bytes)
+                const uint32_t waste = wrap ? ring_bytes - hpos : 0u;
+                const uint32_t at = wrap ? 0u : hpos;
+                if (head + waste + cover - tail > ring_bytes) break;  // wait for space
+                const unsigned long long src = __shfl_sync(kFull, d0, di), bytes = __shfl_sync(kFull, d1, di);
+                const unsigned long long dst = __shfl_sync(kFull, d2, di), np = __shfl_sync(kFull, d3, di);
                 const uint32_t slot = qh % kRSlots;
                 if (lane == 0) {
+                    const uintptr_t beg = (uintptr_t)in + src;
                     RItem& it = B.item[slot];
                     it.dst = dst;
-                    it.n = n;
+                    it.n = (uint32_t)np;
                     it.prev = (uint32_t)(np >> 32);
                     it.bytes = (uint32_t)bytes;
-                    it.spos = at + (uint32_t)(((uintptr_t)in + src) & 15);
+                    it.spos = at + (uint32_t)(beg & 15);
                     it.end = head + waste + cover;
                     fence_async_smem();  // the ring bytes were last read through the generic proxy
                     mbar_expect_s(bar0 + 8 * slot, cover);
-                    tma_load_hint_s(ring + at, reinterpret_cast<const void*>(a0), cover, bar0 + 8 * slot, pol);
+                    tma_load_hint_s(ring + at, reinterpret_cast<const void*>(beg & ~(uintptr_t)15), cover,
+                                    bar0 + 8 * slot, pol);
                 }
                 head += waste + cover;
                 hpos = at + cover;
                 ++qh;
+            } else if (lane == 0 && (inf >> 16) != 0x8000u) {  // not decoded here: report its status
+                report3(status, epoch, (inf >> 16) & 0x7FFFu);
             }
             if (++di == 32) {
                 dbase += 32;
                 di = 0;
                 refill();
+                check();
             }
         }
         __syncwarp();  // lane 0's item records before every lane reads them
@@ -392,7 +666,8 @@ __global__ void __launch_bounds__(kRThreads)
         mbar_wait_parity(&B.bar[slot], (qt / kRSlots) & 1u);
         const RItem it = B.item[slot];
         uint32_t* o = out + it.dst;
-        const uint32_t data = it.n <= 128
+        const uint32_t data = !kV1 ? decode_resident2<kDelta>(ring + it.spos, it.bytes, it.n, kDelta ? it.prev : 0u, o)
+                              : it.n <= 128
                                   ? decode_resident_short<kDelta>(ring + it.spos, it.bytes, it.n, kDelta ? it.prev : 0u, o)
                                   : decode_resident<kDelta>(ring + it.spos, it.bytes, it.n, kDelta ? it.prev : 0u, o);
         if (lane == 0) {
@@ -410,13 +685,16 @@ cudaError_t launch_decode_batch3(const bcgpu_decode_segment* segs, uint64_t nseg
     const uint32_t ring_kb = (ba.flags >> 16) & 0xFFu;  // debug: ring KiB per warp
     const uint32_t ring = ring_kb ? (ring_kb << 10 < kItemMax ? kItemMax : ring_kb << 10) : kRingDefault;
     const size_t smem = kRWarps * (sizeof(RWarpHdr) + ring + kRingSlack);
-    cudaError_t a = launch_ensure_smem(svb_decode_batch3_kernel<true>, smem);
+    const bool v1 = (ba.flags & 1u) != 0;  // debug: the round-1 pass (group_w5, 4 groups per lane)
+    auto kd = v1 ? svb_decode_batch3_kernel<true, true> : svb_decode_batch3_kernel<true, false>;
+    auto kp = v1 ? svb_decode_batch3_kernel<false, true> : svb_decode_batch3_kernel<false, false>;
+    cudaError_t a = launch_ensure_smem(kd, smem);
     if (a != cudaSuccess) return a;
-    a = launch_ensure_smem(svb_decode_batch3_kernel<false>, smem);
+    a = launch_ensure_smem(kp, smem);
     if (a != cudaSuccess) return a;
     const int sms = launch_sms(launch_current_device());
-    const int o1 = launch_occupancy(svb_decode_batch3_kernel<true>, kRThreads, smem);
-    const int o2 = launch_occupancy(svb_decode_batch3_kernel<false>, kRThreads, smem);
+    const int o1 = launch_occupancy(kd, kRThreads, smem);
+    const int o2 = launch_occupancy(kp, kRThreads, smem);
     int occ = o1 < o2 ? o1 : o2;
     if (occ < 1) occ = 1;
     const uint32_t occ_cap = (ba.flags >> 12) & 7u;  // debug: CTAs per SM
@@ -427,12 +705,7 @@ cudaError_t launch_decode_batch3(const bcgpu_decode_segment* segs, uint64_t nseg
     // a non-zero max_seg_n <= kBatchSmallN means no long-segment launch follows: a longer
     // segment contradicts the hint and is reported instead of silently skipped
     const uint32_t hint = ba.max_seg_n != 0 && ba.max_seg_n <= kBatchSmallN ? ba.max_seg_n : 0u;
-    if (delta)
-        svb_decode_batch3_kernel<true><<<grid, kRThreads, smem, stream>>>(segs, nseg, in, out, ba.status, ba.epoch, hint,
-                                                                          ring);
-    else
-        svb_decode_batch3_kernel<false><<<grid, kRThreads, smem, stream>>>(segs, nseg, in, out, ba.status, ba.epoch, hint,
-                                                                           ring);
+    (delta ? kd : kp)<<<grid, kRThreads, smem, stream>>>(segs, nseg, in, out, ba.status, ba.epoch, hint, ring);
     return cudaGetLastError();
 }
 
