@@ -323,27 +323,27 @@ __device__ __forceinline__ uint32_t warp_scan_p(uint32_t v) {
 // the queue drops them (clamped funnel shifts: 8 l_i = 32 moves a whole word).  Each step
 // needs one word less, so the four integers cost 4 SGXT + 6 funnel shifts, with no selects
 // (group_w5 picks each integer's word pair with compare + select chains).
-// Shared word at a when pred, else 0 (a predicated load: no branch).
+// Shared word at a when pred, else whatever the register held (a predicated load: no branch,
+// no zeroing move).  Callers only use bytes of words they loaded.
 __device__ __forceinline__ uint32_t lds32_if(uint32_t a, bool pred) {
-    uint32_t v = 0;
+    uint32_t v;
     asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %2, 0;\n\t@p ld.shared.u32 %0, [%1];\n\t}"
-                 : "+r"(v)
+                 : "=r"(v)
                  : "r"(a), "r"((uint32_t)pred));
     return v;
 }
 
 // len = the group's data bytes: only the words they touch are loaded (cfg4 groups average ~10
 // bytes, ~3.4 of the five words; every window load is ~4-way bank-conflicted, and shared-memory
-// wavefronts bound this kernel once the ALU work is down)
-__device__ __forceinline__ uint4 group_q(uint32_t a, uint32_t c, uint32_t len) {
+// wavefronts bound this kernel once the ALU work is down).  b0..b3 = 8 l_i of its integers.
+__device__ __forceinline__ uint4 group_q(uint32_t a, uint32_t len, uint32_t b0, uint32_t b1, uint32_t b2,
+                                         uint32_t b3) {
     const uint32_t wa = a & ~3u, sh = (a & 3u) << 3;
     const uint32_t e = (a & 3u) + len;  // window bytes in use
     const uint32_t w0 = lds32(wa), w1 = lds32_if(wa + 4, e > 4), w2 = lds32_if(wa + 8, e > 8),
                    w3 = lds32_if(wa + 12, e > 12), w4 = lds32_if(wa + 16, e > 16);
     const uint32_t X0 = __funnelshift_r(w0, w1, sh), X1 = __funnelshift_r(w1, w2, sh),
                    X2 = __funnelshift_r(w2, w3, sh), X3 = __funnelshift_r(w3, w4, sh);
-    const uint32_t b0 = ((c << 3) & 0x18u) + 8u, b1 = ((c << 1) & 0x18u) + 8u, b2 = ((c >> 1) & 0x18u) + 8u,
-                   b3 = ((c >> 3) & 0x18u) + 8u;  // 8 l_i
     uint4 v;
     v.x = szext(X0, b0);
     const uint32_t Y0 = __funnelshift_rc(X0, X1, b0), Y1 = __funnelshift_rc(X1, X2, b0),
@@ -424,24 +424,31 @@ __device__ __forceinline__ void store_whole(const uint4 (&v)[4], uint32_t* __res
     }
 }
 
-// The integers no whole granule holds: the head granule's [0, 4 - R) (R != 0) and the tail
-// [T, n), T = the start of the last, partial granule.  Phase-independent (one copy), element
-// stores from the lane that decoded them; at most two lanes of a segment take the branch.
+// The integers no whole granule holds: the head granule's [0, 4 - R) (R != 0: lane 0's first
+// group in the first pass) and the tail [T, n) (<= 3 integers, T = the start of the last,
+// partial granule).  Phase-independent (one copy); at most two lanes take the tail branch.
 template <int K>
 __device__ __forceinline__ void edge_stores(const uint4 (&v)[4], uint32_t* __restrict__ o, uint32_t g0, uint32_t k,
-                                            int n, uint32_t R, int T) {
+                                            int n, uint32_t R, int T, bool first) {
+    const int lane = threadIdx.x & 31;
     const uint32_t kk = K ? (uint32_t)K : k;
+    if (first && R != 0 && lane == 0) {
+        const int h = 4 - (int)R < n ? 4 - (int)R : n;
+        o[0] = v[0].x;
+        if (h > 1) o[1] = v[0].y;
+        if (h > 2) o[2] = v[0].z;
+    }
     const int lo = 4 * (int)g0, hi = lo + 4 * (int)kk;
-    const int head = R ? (4 - (int)R < n ? 4 - (int)R : n) : 0;
-    if ((lo < head) || (hi > T && lo < n)) {
+    if (hi > T && lo < n) {
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
-            if (K || (uint32_t)j < kk) {
-#pragma unroll
-                for (int i = 0; i < 4; ++i) {
-                    const int e = lo + 4 * j + i;
-                    if (e < n && (e < head || e >= T)) o[e] = comp(v[j], i);
-                }
+            const int a = T - (lo + 4 * j), b = n - (lo + 4 * j);  // group j holds integers i, a <= i < b
+            if ((K || (uint32_t)j < kk) && a < 4 && b > 0) {
+                uint32_t* q = o + lo + 4 * j;
+                if (a <= 0) q[0] = v[j].x;
+                if (a <= 1 && b > 1) q[1] = v[j].y;
+                if (a <= 2 && b > 2) q[2] = v[j].z;
+                if (b > 3) q[3] = v[j].w;
             }
         }
     }
@@ -486,11 +493,17 @@ __device__ __forceinline__ void decode_pass(uint32_t S, uint32_t D, uint32_t Den
         for (int j = 0; j < 4; ++j)
             if (K || (uint32_t)j < kk) v[j] = zero_group_s(min(p + 4 * j, Dend));
     } else {
+        // 8 l of every integer of the lane's groups, four per word: byte j of Bi = 8 (field i of
+        // control byte j) + 8; one PRMT isolates each (three ops apiece from the control byte)
+        const uint32_t Bx = (cw & 0x03030303u) * 8u + 0x08080808u, By = ((cw >> 2) & 0x03030303u) * 8u + 0x08080808u,
+                       Bz = ((cw >> 4) & 0x03030303u) * 8u + 0x08080808u, Bw = ((cw >> 6) & 0x03030303u) * 8u + 0x08080808u;
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
             if (K || (uint32_t)j < kk) {
-                const uint32_t lj = (lens >> (8 * j)) & 0xFFu;
-                v[j] = group_q(min(p, Dend), (cw >> (8 * j)) & 0xFFu, lj);
+                const uint32_t sel = 0x4440u | (uint32_t)j;
+                const uint32_t lj = __byte_perm(lens, 0u, sel);
+                v[j] = group_q(min(p, Dend), lj, __byte_perm(Bx, 0u, sel), __byte_perm(By, 0u, sel),
+                               __byte_perm(Bz, 0u, sel), __byte_perm(Bw, 0u, sel));
                 p += lj;
             }
         }
@@ -521,7 +534,7 @@ __device__ __forceinline__ void decode_pass(uint32_t S, uint32_t D, uint32_t Den
         default: store_whole<3, K>(v, o, g0, kk, (int)n, carry); break;
     }
     // the pass holds the head or part of the tail (the tail can start in the pass before the last)
-    if (gp == 0 || 4 * (int)(gp + 32 * kk) > T) edge_stores<K>(v, o, g0, kk, (int)n, R, T);
+    if ((gp == 0 && R != 0) || 4 * (int)(gp + 32 * kk) > T) edge_stores<K>(v, o, g0, kk, (int)n, R, T, gp == 0);
 }
 
 // decode_resident with group_q, predicated scans, the k-groups-per-lane last pass (cfg4: 85% ->
@@ -572,45 +585,41 @@ __global__ void __launch_bounds__(kRThreads, BC_DEC3_MINB)
     if (lane == 0)
         for (uint32_t q = 0; q < kRSlots; ++q) mbar_init1(&B.bar[q]);
     __syncwarp();
-    const uint64_t gw = (uint64_t)blockIdx.x * kRWarps + warp, GW = (uint64_t)gridDim.x * kRWarps;
-    const uint64_t cnt = nseg > gw ? (nseg - gw + GW - 1) / GW : 0;  // segments gw, gw + GW, ...
+    // nseg < 2^32 (the launcher splits larger batches)
+    const uint32_t gw = blockIdx.x * kRWarps + warp, GW = gridDim.x * kRWarps;
+    const uint32_t cnt = nseg > gw ? (uint32_t)((nseg - gw + GW - 1) / GW) : 0u;  // segments gw, gw + GW, ...
     const uint32_t ring = sh_addr(ring_p), bar0 = sh_addr(&B.bar[0]);
     const uint64_t pol = l2_policy_drop();
-    const unsigned long long* sw = reinterpret_cast<const unsigned long long*>(segs);
-
-    // lane l holds the descriptor of the warp's segment dbase + l
-    uint64_t dbase = 0;
-    unsigned long long d0 = 0, d1 = 0, d2 = 0, d3 = 0;
-    auto refill = [&]() {
-        const uint64_t k = dbase + lane;
-        if (k < cnt) {
-            const unsigned long long* p = sw + 4 * (gw + k * GW);
-            d0 = __ldg(p);
-            d1 = __ldg(p + 1);
-            d2 = __ldg(p + 2);
-            d3 = __ldg(p + 3);
-        }
+    auto seg_ptr = [&](uint32_t k) {  // the warp's k-th segment
+        return reinterpret_cast<const ulonglong2*>(segs + gw + (uint64_t)k * GW);
     };
-    refill();
-    // Each lane also checks its own descriptor once per refill: info = its ring cover (decodes
-    // here) | the status it reports << 16 | 1 << 31 when the segment is not decoded here.
-    uint32_t info = 0;
+
+    // Lane l checks the descriptor of the warp's segment dbase + l once: info = its ring cover
+    // (decoded here) | the status it reports << 16 | 1 << 31 when it is not decoded here.  The
+    // descriptors themselves stay in memory (lane 0 re-reads one from L1 when it issues it), so
+    // they hold no registers through the decode.
+    uint32_t dbase = 0, info = 0;
     auto check = [&]() {
-        const uint32_t n = (uint32_t)d3;
-        const uint64_t ngroups = ((uint64_t)n + 3) >> 2;
-        uint32_t code = 0;
-        if (n > kBatchSmallN)  // svb_batch2.cu decodes it -- unless the caller's max_seg_n said no segment is long
-            code = long_hint && n > long_hint ? (uint32_t)BCGPU_ERR_INVALID_ARGUMENT : 0u;
-        else if (n == 0)
-            code = d1 != 0 ? (uint32_t)BCGPU_ERR_TRAILING_BYTES : 0u;
-        else if (d1 < ngroups)
-            code = BCGPU_ERR_TRUNCATED;
-        else if (d1 > ngroups + 4ull * n)
-            code = BCGPU_ERR_TRAILING_BYTES;
-        const uintptr_t beg = (uintptr_t)in + d0;
-        const uint32_t cover = (uint32_t)(((beg + d1 + 15) & ~(uintptr_t)15) - (beg & ~(uintptr_t)15));
-        const bool here = n != 0 && n <= kBatchSmallN && code == 0;
-        info = here ? cover : (0x80000000u | (code << 16));
+        const uint32_t k = dbase + lane;
+        info = 0x80000000u;
+        if (k < cnt) {
+            const ulonglong2 sb = __ldg(seg_ptr(k));  // src_offset, src_bytes
+            const uint32_t n = (uint32_t)__ldg(seg_ptr(k) + 1).y;
+            const uint64_t ngroups = ((uint64_t)n + 3) >> 2;
+            uint32_t code = 0;
+            if (n > kBatchSmallN)  // svb_batch2.cu decodes it -- unless the caller's max_seg_n said no segment is long
+                code = long_hint && n > long_hint ? (uint32_t)BCGPU_ERR_INVALID_ARGUMENT : 0u;
+            else if (n == 0)
+                code = sb.y != 0 ? (uint32_t)BCGPU_ERR_TRAILING_BYTES : 0u;
+            else if (sb.y < ngroups)
+                code = BCGPU_ERR_TRUNCATED;
+            else if (sb.y > ngroups + 4ull * n)
+                code = BCGPU_ERR_TRAILING_BYTES;
+            const uintptr_t beg = (uintptr_t)in + sb.x;
+            const uint32_t cover = (uint32_t)(((beg + sb.y + 15) & ~(uintptr_t)15) - (beg & ~(uintptr_t)15));
+            const bool here = n != 0 && n <= kBatchSmallN && code == 0;
+            info = here ? cover : (0x80000000u | (code << 16));
+        }
     };
     check();
     uint32_t di = 0;                // next descriptor of the batch (lane index)
@@ -629,16 +638,15 @@ __global__ void __launch_bounds__(kRThreads, BC_DEC3_MINB)
                 const uint32_t waste = wrap ? ring_bytes - hpos : 0u;
                 const uint32_t at = wrap ? 0u : hpos;
                 if (head + waste + cover - tail > ring_bytes) break;  // wait for space
-                const unsigned long long src = __shfl_sync(kFull, d0, di), bytes = __shfl_sync(kFull, d1, di);
-                const unsigned long long dst = __shfl_sync(kFull, d2, di), np = __shfl_sync(kFull, d3, di);
                 const uint32_t slot = qh % kRSlots;
                 if (lane == 0) {
-                    const uintptr_t beg = (uintptr_t)in + src;
+                    const ulonglong2 sb = __ldg(seg_ptr(dbase + di)), dn = __ldg(seg_ptr(dbase + di) + 1);
+                    const uintptr_t beg = (uintptr_t)in + sb.x;
                     RItem& it = B.item[slot];
-                    it.dst = dst;
-                    it.n = (uint32_t)np;
-                    it.prev = (uint32_t)(np >> 32);
-                    it.bytes = (uint32_t)bytes;
+                    it.dst = dn.x;
+                    it.n = (uint32_t)dn.y;
+                    it.prev = (uint32_t)(dn.y >> 32);
+                    it.bytes = (uint32_t)sb.y;
                     it.spos = at + (uint32_t)(beg & 15);
                     it.end = head + waste + cover;
                     fence_async_smem();  // the ring bytes were last read through the generic proxy
@@ -655,7 +663,6 @@ __global__ void __launch_bounds__(kRThreads, BC_DEC3_MINB)
             if (++di == 32) {
                 dbase += 32;
                 di = 0;
-                refill();
                 check();
             }
         }
@@ -705,7 +712,11 @@ cudaError_t launch_decode_batch3(const bcgpu_decode_segment* segs, uint64_t nseg
     // a non-zero max_seg_n <= kBatchSmallN means no long-segment launch follows: a longer
     // segment contradicts the hint and is reported instead of silently skipped
     const uint32_t hint = ba.max_seg_n != 0 && ba.max_seg_n <= kBatchSmallN ? ba.max_seg_n : 0u;
-    (delta ? kd : kp)<<<grid, kRThreads, smem, stream>>>(segs, nseg, in, out, ba.status, ba.epoch, hint, ring);
+    constexpr uint64_t kMaxSeg = 1ull << 31;  // the kernel counts segments in 32 bits
+    for (uint64_t s0 = 0; s0 < nseg; s0 += kMaxSeg) {
+        const uint64_t ns = nseg - s0 < kMaxSeg ? nseg - s0 : kMaxSeg;
+        (delta ? kd : kp)<<<grid, kRThreads, smem, stream>>>(segs + s0, ns, in, out, ba.status, ba.epoch, hint, ring);
+    }
     return cudaGetLastError();
 }
 
