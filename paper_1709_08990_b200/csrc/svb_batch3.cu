@@ -33,9 +33,6 @@ namespace bcgpu {
 
 namespace {
 
-#ifndef BC_DEC3_MODE
-#define BC_DEC3_MODE 1  // 1: four groups per lane in every pass (measured best); 0: a k-groups-per-lane last pass; 2: runtime k in every pass
-#endif
 #ifndef BC_DEC3_MINB
 #define BC_DEC3_MINB 5  // decode CTAs per SM the register budget must allow (6 spills)
 #endif
@@ -355,31 +352,25 @@ __device__ __forceinline__ uint4 group_q(uint32_t a, uint32_t len, uint32_t b0, 
     return v;
 }
 
-// Vector stores of the whole granules among a lane's groups g0 .. g0 + k - 1 (k = K, or the
-// runtime k when K = 0; see store_pass for the granule layout).  K = 4: pairs on a 32-B
-// boundary leave as one 256-bit store.  Granules that straddle the segment's ends are left
-// to edge_stores, so each phase's block is a few predicated stores.
-template <uint32_t R, int K>
-__device__ __forceinline__ void store_whole(const uint4 (&v)[4], uint32_t* __restrict__ o, uint32_t g0, uint32_t k,
-                                            int nints, uint4& carry) {
+// Vector stores of the whole granules among a lane's groups g0 .. g0 + 3 (see store_pass for
+// the granule layout); pairs on a 32-B boundary leave as one 256-bit store.  Granules that
+// straddle the segment's ends are left to edge_stores, so each phase's block is a few
+// predicated stores.
+template <uint32_t R>
+__device__ __forceinline__ void store_whole(const uint4 (&v)[4], uint32_t* __restrict__ o, uint32_t g0, int nints,
+                                            uint4& carry) {
     const int lane = threadIdx.x & 31;
-    const uint32_t kk = K ? (uint32_t)K : k;
     uint4 G[4];
     uint32_t* Bp = o - R;  // 16-B aligned
     if constexpr (R == 0) {
 #pragma unroll
         for (int j = 0; j < 4; ++j) G[j] = v[j];
     } else {
-        uint4 vl;  // the lane's last group
-        if constexpr (K == 4)
-            vl = v[3];
-        else
-            vl = kk == 1 ? v[0] : kk == 2 ? v[1] : kk == 3 ? v[2] : v[3];
         const int src = (lane + 31) & 31;
         uint4 rot = make_uint4(0, 0, 0, 0);
-        rot.w = __shfl_sync(kFull, vl.w, src);
-        if (R >= 2) rot.z = __shfl_sync(kFull, vl.z, src);
-        if (R >= 3) rot.y = __shfl_sync(kFull, vl.y, src);
+        rot.w = __shfl_sync(kFull, v[3].w, src);
+        if (R >= 2) rot.z = __shfl_sync(kFull, v[3].z, src);
+        if (R >= 3) rot.y = __shfl_sync(kFull, v[3].y, src);
         const uint4 prv0 = lane == 0 ? carry : rot;
         carry = rot;
 #pragma unroll
@@ -394,104 +385,69 @@ __device__ __forceinline__ void store_whole(const uint4 (&v)[4], uint32_t* __res
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
         const int e0 = 4 * (int)(g0 + j) - (int)R;
-        f[j] = (K || (uint32_t)j < kk) && e0 >= 0 && e0 + 4 <= nints;
+        f[j] = e0 >= 0 && e0 + 4 <= nints;
     }
-    if constexpr (K == 4) {
-        if ((((uintptr_t)(Bp + 4 * g0)) & 31) == 0) {  // warp-uniform (g0 even): pairs (0,1), (2,3)
+    if ((((uintptr_t)Bp) & 31) == 0) {  // warp-uniform (g0 even): pairs (0,1), (2,3)
 #pragma unroll
-            for (int j = 0; j < 4; j += 2) {
-                if (f[j] && f[j + 1]) {
-                    stg_stream_v8(Bp + 4 * (g0 + j), G[j], G[j + 1]);
-                } else {
-                    if (f[j]) stg_stream_v4(Bp + 4 * (g0 + j), G[j]);
-                    if (f[j + 1]) stg_stream_v4(Bp + 4 * (g0 + j + 1), G[j + 1]);
-                }
-            }
-        } else {  // pair (1,2)
-            if (f[0]) stg_stream_v4(Bp + 4 * g0, G[0]);
-            if (f[1] && f[2]) {
-                stg_stream_v8(Bp + 4 * (g0 + 1), G[1], G[2]);
+        for (int j = 0; j < 4; j += 2) {
+            if (f[j] && f[j + 1]) {
+                stg_stream_v8(Bp + 4 * (g0 + j), G[j], G[j + 1]);
             } else {
-                if (f[1]) stg_stream_v4(Bp + 4 * (g0 + 1), G[1]);
-                if (f[2]) stg_stream_v4(Bp + 4 * (g0 + 2), G[2]);
+                if (f[j]) stg_stream_v4(Bp + 4 * (g0 + j), G[j]);
+                if (f[j + 1]) stg_stream_v4(Bp + 4 * (g0 + j + 1), G[j + 1]);
             }
-            if (f[3]) stg_stream_v4(Bp + 4 * (g0 + 3), G[3]);
         }
-    } else {
-#pragma unroll
-        for (int j = 0; j < 4; ++j)
-            if (f[j]) stg_stream_v4(Bp + 4 * (g0 + j), G[j]);
+    } else {  // pair (1,2)
+        if (f[0]) stg_stream_v4(Bp + 4 * g0, G[0]);
+        if (f[1] && f[2]) {
+            stg_stream_v8(Bp + 4 * (g0 + 1), G[1], G[2]);
+        } else {
+            if (f[1]) stg_stream_v4(Bp + 4 * (g0 + 1), G[1]);
+            if (f[2]) stg_stream_v4(Bp + 4 * (g0 + 2), G[2]);
+        }
+        if (f[3]) stg_stream_v4(Bp + 4 * (g0 + 3), G[3]);
     }
 }
 
-// The integers no whole granule holds: the head granule's [0, 4 - R) (R != 0: lane 0's first
-// group in the first pass) and the tail [T, n) (<= 3 integers, T = the start of the last,
-// partial granule).  Phase-independent (one copy); at most two lanes take the tail branch.
-template <int K>
-__device__ __forceinline__ void edge_stores(const uint4 (&v)[4], uint32_t* __restrict__ o, uint32_t g0, uint32_t k,
-                                            int n, uint32_t R, int T, bool first) {
-    const int lane = threadIdx.x & 31;
-    const uint32_t kk = K ? (uint32_t)K : k;
-    if (first && R != 0 && lane == 0) {
-        const int h = 4 - (int)R < n ? 4 - (int)R : n;
-        o[0] = v[0].x;
-        if (h > 1) o[1] = v[0].y;
-        if (h > 2) o[2] = v[0].z;
-    }
-    const int lo = 4 * (int)g0, hi = lo + 4 * (int)kk;
-    if (hi > T && lo < n) {
-#pragma unroll
-        for (int j = 0; j < 4; ++j) {
-            const int a = T - (lo + 4 * j), b = n - (lo + 4 * j);  // group j holds integers i, a <= i < b
-            if ((K || (uint32_t)j < kk) && a < 4 && b > 0) {
-                uint32_t* q = o + lo + 4 * j;
-                if (a <= 0) q[0] = v[j].x;
-                if (a <= 1 && b > 1) q[1] = v[j].y;
-                if (a <= 2 && b > 2) q[2] = v[j].z;
-                if (b > 3) q[3] = v[j].w;
-            }
-        }
-    }
-}
-
-// One pass of decode_resident2: lane l owns groups g0 .. g0 + k - 1 (g0 = gp + k l) of the
-// pass starting at group gp.  Full passes (and a last pass of 128 groups) are K = 4; a
-// shorter last pass uses K = 0 with k = ceil(groups left / 32), so it costs k groups per
-// lane, not four.  Groups past the segment's end decode garbage that is never stored: it
-// only follows the valid integers in lane order, so no position, delta prefix or store of a
-// valid integer sees it.
-template <bool kDelta, int K>
+// One pass of decode_resident2: 128 groups from group gp, lane l owning groups g0 = gp + 4 l
+// .. g0 + 3.  In the segment's last pass the groups past its end decode garbage that is never
+// stored: it only follows the valid integers in lane order, so no position, delta prefix or
+// store of a valid integer sees it, and the declared data length comes from the lane holding
+// the last group.  (A last pass of k = ceil(groups left / 32) groups per lane was built and
+// measured: the runtime k cost more in every pass than it saved in the last.)
+template <bool kDelta>
 __device__ __forceinline__ void decode_pass(uint32_t S, uint32_t D, uint32_t Dend, uint32_t ng, uint32_t n,
-                                            uint32_t tail, uint32_t tmask, uint32_t gp, uint32_t k, bool lastp,
-                                            uint32_t R, int T, uint32_t& off, uint32_t& run, uint4& carry,
-                                            uint32_t* __restrict__ o) {
+                                            uint32_t gp, bool lastp, uint32_t R, int T, uint32_t& off, uint32_t& run,
+                                            uint4& carry, uint32_t* __restrict__ o) {
     const int lane = threadIdx.x & 31;
-    const uint32_t kk = K ? (uint32_t)K : k;
-    const uint32_t g0 = gp + kk * lane;
+    const uint32_t g0 = gp + 4 * lane;
     const uint32_t ca = S + g0;
     uint32_t cw = __funnelshift_r(lds32(ca & ~3u), lds32((ca & ~3u) + 4), (ca & 3u) << 3);
-    uint32_t lens;
-    if (!lastp) {
-        lens = swar_lengths(cw);
-    } else {
-        // the lane's valid groups; the final group's unused fields and anything past it count 0
-        const uint32_t nv = ng > g0 ? (ng - g0 < kk ? ng - g0 : kk) : 0u;
+    uint32_t lens = swar_lengths(cw);
+    if (lastp) {  // groups past the end (their "control bytes" are data) load and decode nothing
+        const uint32_t nv = ng > g0 ? ng - g0 : 0u;
         const uint32_t bm = nv >= 4 ? 0xFFFFFFFFu : ((1u << (8 * nv)) - 1u);
-        const bool hl = nv && g0 + nv == ng;
-        if (hl) cw &= ~(0xFFu << (8 * (nv - 1))) | (tmask << (8 * (nv - 1)));
         cw &= bm;
-        lens = swar_lengths(cw) & bm;
-        if (hl) lens -= (4u - tail) << (8 * (nv - 1));
+        lens &= bm;
     }
     const uint32_t lt = __dp4a(lens, 0x01010101u, 0u);  // <= 64
     const uint32_t I = warp_scan_p(lt);
     uint32_t p = D + off + I - lt;
-    off += __shfl_sync(kFull, I, 31);
+    if (!lastp) {
+        off += __shfl_sync(kFull, I, 31);
+    } else {
+        // data bytes up to the end of the last group (ng - 1), its unused fields left out: from
+        // the lane holding it, j = its place in the lane
+        const uint32_t q = ng - 1 - gp, j = q & 3u, r = n & 3u;
+        const uint32_t before = __byte_perm(lens * 0x01010100u, 0u, 0x4440u | j);  // lens of groups < j
+        const uint32_t cl = __byte_perm(cw, 0u, 0x4440u | j) & (r ? (1u << (2 * r)) - 1u : 0xFFu);
+        const uint32_t mine = (I - lt) + before + field_sum(cl) + (r ? r : 4u);
+        off += __shfl_sync(kFull, mine, (int)(q >> 2));
+    }
     uint4 v[4];
     if (__all_sync(kFull, cw == 0)) {
 #pragma unroll
-        for (int j = 0; j < 4; ++j)
-            if (K || (uint32_t)j < kk) v[j] = zero_group_s(min(p + 4 * j, Dend));
+        for (int j = 0; j < 4; ++j) v[j] = zero_group_s(min(p + 4 * j, Dend));
     } else {
         // 8 l of every integer of the lane's groups, four per word: byte j of Bi = 8 (field i of
         // control byte j) + 8; one PRMT isolates each (three ops apiece from the control byte)
@@ -499,73 +455,78 @@ __device__ __forceinline__ void decode_pass(uint32_t S, uint32_t D, uint32_t Den
                        Bz = ((cw >> 4) & 0x03030303u) * 8u + 0x08080808u, Bw = ((cw >> 6) & 0x03030303u) * 8u + 0x08080808u;
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
-            if (K || (uint32_t)j < kk) {
-                const uint32_t sel = 0x4440u | (uint32_t)j;
-                const uint32_t lj = __byte_perm(lens, 0u, sel);
-                v[j] = group_q(min(p, Dend), lj, __byte_perm(Bx, 0u, sel), __byte_perm(By, 0u, sel),
-                               __byte_perm(Bz, 0u, sel), __byte_perm(Bw, 0u, sel));
-                p += lj;
-            }
+            const uint32_t sel = 0x4440u | (uint32_t)j;
+            const uint32_t lj = __byte_perm(lens, 0u, sel);
+            v[j] = group_q(min(p, Dend), lj, __byte_perm(Bx, 0u, sel), __byte_perm(By, 0u, sel),
+                           __byte_perm(Bz, 0u, sel), __byte_perm(Bw, 0u, sel));
+            p += lj;
         }
     }
     if constexpr (kDelta) {
         uint32_t s = 0;
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
-            if (K || (uint32_t)j < kk) {
-                v[j].x += s;
-                v[j].y += v[j].x;
-                v[j].z += v[j].y;
-                v[j].w += v[j].z;
-                s = v[j].w;
-            }
+            v[j].x += s;
+            v[j].y += v[j].x;
+            v[j].z += v[j].y;
+            v[j].w += v[j].z;
+            s = v[j].w;
         }
         const uint32_t Iv = warp_scan_p(s);
         const uint32_t add = run + Iv - s;
 #pragma unroll
-        for (int j = 0; j < 4; ++j)
-            if (K || (uint32_t)j < kk) v[j] = add4(v[j], add);
+        for (int j = 0; j < 4; ++j) v[j] = add4(v[j], add);
         run += __shfl_sync(kFull, Iv, 31);
     }
     switch (R) {  // warp-uniform; only these small store blocks are per phase
-        case 0: store_whole<0, K>(v, o, g0, kk, (int)n, carry); break;
-        case 1: store_whole<1, K>(v, o, g0, kk, (int)n, carry); break;
-        case 2: store_whole<2, K>(v, o, g0, kk, (int)n, carry); break;
-        default: store_whole<3, K>(v, o, g0, kk, (int)n, carry); break;
+        case 0: store_whole<0>(v, o, g0, (int)n, carry); break;
+        case 1: store_whole<1>(v, o, g0, (int)n, carry); break;
+        case 2: store_whole<2>(v, o, g0, (int)n, carry); break;
+        default: store_whole<3>(v, o, g0, (int)n, carry); break;
     }
-    // the pass holds the head or part of the tail (the tail can start in the pass before the last)
-    if ((gp == 0 && R != 0) || 4 * (int)(gp + 32 * kk) > T) edge_stores<K>(v, o, g0, kk, (int)n, R, T, gp == 0);
+    // The integers no whole granule holds: the head granule's [0, 4 - R) (R != 0: lane 0's first
+    // group in the first pass) and the tail [T, n), <= 3 integers held by at most two lanes
+    // (T = the start of the last, partial granule; it can start in the pass before the last).
+    if (gp == 0 && R != 0 && lane == 0) {
+        const int h = 4 - (int)R < (int)n ? 4 - (int)R : (int)n;
+        o[0] = v[0].x;
+        if (h > 1) o[1] = v[0].y;
+        if (h > 2) o[2] = v[0].z;
+    }
+    const int rel = T - 4 * (int)gp;
+    if (rel < 512 && (lane == (rel >> 4) || lane == (((int)n - 1 - 4 * (int)gp) >> 4))) {
+        const int lo = 4 * (int)g0;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const int a = T - (lo + 4 * j), b = (int)n - (lo + 4 * j);  // group j holds integers i, a <= i < b
+            if (a < 4 && b > 0) {
+                uint32_t* qo = o + lo + 4 * j;
+                if (a <= 0) qo[0] = v[j].x;
+                if (a <= 1 && b > 1) qo[1] = v[j].y;
+                if (a <= 2 && b > 2) qo[2] = v[j].z;
+                if (b > 3) qo[3] = v[j].w;
+            }
+        }
+    }
 }
 
-// decode_resident with group_q, predicated scans, the k-groups-per-lane last pass (cfg4: 85% ->
-// 94% of the group slots hold integers) and the segment-edge stores out of the per-phase
-// store blocks.  Segments of <= 128 integers are one pass with k = 1.
+// Decode one resident segment (any n <= kBatchSmallN) in passes of 512 integers; returns the
+// data bytes its control stream declares.  group_q extraction, predicated scans, whole-granule
+// stores per phase and the segment-edge integers outside the per-phase blocks.
 template <bool kDelta>
 __device__ __forceinline__ uint32_t decode_resident2(uint32_t S, uint32_t bytes, uint32_t n, uint32_t run,
                                                      uint32_t* __restrict__ o) {
     const uint32_t R = (uint32_t)(((uintptr_t)o >> 2) & 3u);
     const uint32_t ng = (n + 3) >> 2;
-    const uint32_t tail = (n & 3u) ? (n & 3u) : 4u;
-    const uint32_t tmask = (n & 3u) ? ((1u << (2 * (n & 3u))) - 1u) : 0xFFu;
     const uint32_t D = S + ng, Dend = S + bytes;
     const int T = 4 * (int)((n + R) >> 2) - (int)R;  // the tail no whole granule holds: [T, n)
     const uint32_t full_passes = (ng - 1) >> 7;       // every pass but the last holds 128 groups
-    const uint32_t gl = 128 * full_passes, kl = (ng - gl + 31) >> 5;
     uint32_t off = 0;
     uint4 carry = make_uint4(0, 0, 0, 0);
 #pragma unroll 1
     for (uint32_t ps = 0;; ++ps) {
         const bool lastp = ps == full_passes;
-#if BC_DEC3_MODE == 1
-        decode_pass<kDelta, 4>(S, D, Dend, ng, n, tail, tmask, 128 * ps, 4, lastp, R, T, off, run, carry, o);
-#elif BC_DEC3_MODE == 2
-        decode_pass<kDelta, 0>(S, D, Dend, ng, n, tail, tmask, 128 * ps, lastp ? kl : 4u, lastp, R, T, off, run, carry, o);
-#else
-        if (!lastp || kl == 4)
-            decode_pass<kDelta, 4>(S, D, Dend, ng, n, tail, tmask, 128 * ps, 4, lastp, R, T, off, run, carry, o);
-        else
-            decode_pass<kDelta, 0>(S, D, Dend, ng, n, tail, tmask, gl, kl, true, R, T, off, run, carry, o);
-#endif
+        decode_pass<kDelta>(S, D, Dend, ng, n, 128 * ps, lastp, R, T, off, run, carry, o);
         if (lastp) break;
     }
     return off;
