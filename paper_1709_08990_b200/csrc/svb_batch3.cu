@@ -302,19 +302,6 @@ __device__ __forceinline__ uint32_t szext(uint32_t x, uint32_t b) {
     return r;
 }
 
-// Inclusive warp scan whose steps add under the shuffle's own in-range predicate (two
-// instructions per step instead of shuffle + lane compare + select + add).
-__device__ __forceinline__ uint32_t warp_scan_p(uint32_t v) {
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1)
-        asm("{\n\t.reg .pred p;\n\t.reg .u32 t;\n\t"
-            "shfl.sync.up.b32 t|p, %0, %1, 0, 0xffffffff;\n\t"
-            "@p add.u32 %0, %0, t;\n\t}"
-            : "+r"(v)
-            : "r"(o));
-    return v;
-}
-
 // One control byte c whose data starts at shared byte address a -> 4 integers.  The group's
 // 16 bytes X0..X3 act as a queue: integer i is the queue's low l_i bytes (SGXT by 8 l_i), then
 // the queue drops them (clamped funnel shifts: 8 l_i = 32 moves a whole word).  Each step
@@ -431,7 +418,7 @@ __device__ __forceinline__ void decode_pass(uint32_t S, uint32_t D, uint32_t Den
         lens &= bm;
     }
     const uint32_t lt = __dp4a(lens, 0x01010101u, 0u);  // <= 64
-    const uint32_t I = warp_scan_p(lt);
+    const uint32_t I = warp_inclusive_scan(lt);
     uint32_t p = D + off + I - lt;
     if (!lastp) {
         off += __shfl_sync(kFull, I, 31);
@@ -472,7 +459,7 @@ __device__ __forceinline__ void decode_pass(uint32_t S, uint32_t D, uint32_t Den
             v[j].w += v[j].z;
             s = v[j].w;
         }
-        const uint32_t Iv = warp_scan_p(s);
+        const uint32_t Iv = warp_inclusive_scan(s);
         const uint32_t add = run + Iv - s;
 #pragma unroll
         for (int j = 0; j < 4; ++j) v[j] = add4(v[j], add);
@@ -840,7 +827,11 @@ __device__ __forceinline__ void encode_block(uint32_t Sin, uint32_t blk, uint32_
             const uint32_t g = 32 * (blk + j) + lane;
             const uint32_t o = db + off + ((E3 >> (10 * j)) & 0x3FFu);
             off += (T3 >> (10 * j)) & 0x3FFu;
-            pack_group_row_masked(d[j], C3[j], o, carry, T3r[j], g <= ng);
+            const uint32_t re = 32 * (blk + j + 1);  // groups up to the row's end
+            if (re < ng || (re == ng && tail == 4))  // a whole row (warp-uniform): the unmasked pack
+                pack_group_row(d[j], C3[j], o, carry);
+            else
+                pack_group_row_masked(d[j], C3[j], o, carry, T3r[j], g <= ng);
         }
         // a last row that ends with lane 31 left the last group's pending word in carry
         if ((ng & 31u) == 0 && lane == 0 && ((db + off) & 3u)) sts32((db + off) & ~3u, carry);
@@ -911,24 +902,29 @@ __global__ void __launch_bounds__(kRThreads)
     if (lane == 0)
         for (uint32_t q = 0; q < kRSlots; ++q) mbar_init1(&B.bar[q]);
     __syncwarp();
-    const uint64_t gw = (uint64_t)blockIdx.x * kRWarps + warp, GW = (uint64_t)gridDim.x * kRWarps;
-    const uint64_t cnt = nseg > gw ? (nseg - gw + GW - 1) / GW : 0;
+    // nseg < 2^32 (the launcher splits larger batches)
+    const uint32_t gw = blockIdx.x * kRWarps + warp, GW = gridDim.x * kRWarps;
+    const uint32_t cnt = nseg > gw ? (uint32_t)((nseg - gw + GW - 1) / GW) : 0u;
     const uint32_t ring = sh_addr(ring_p), bar0 = sh_addr(&B.bar[0]), ctrl0 = sh_addr(&B.ctrl[0][0]);
     const uint64_t pol = l2_policy_drop();
-    const unsigned long long* sw = reinterpret_cast<const unsigned long long*>(segs);
-    uint64_t dbase = 0;
-    unsigned long long d0 = 0, d1 = 0, d2 = 0, d3 = 0;
-    auto refill = [&]() {
-        const uint64_t k = dbase + lane;
+    auto seg_ptr = [&](uint32_t k) {  // the warp's k-th segment
+        return reinterpret_cast<const ulonglong2*>(segs + gw + (uint64_t)k * GW);
+    };
+    // Lane l checks the descriptor of the warp's segment dbase + l once: its n, and the 16-B
+    // phase of its integers | 0x100 when it is empty | 0x200 when its capacity is short.  The
+    // descriptors stay in memory (lane 0 re-reads one from L1 when it issues a piece).
+    uint32_t dbase = 0, info_n = 0, info_f = 0;
+    auto check = [&]() {
+        const uint32_t k = dbase + lane;
         if (k < cnt) {
-            const unsigned long long* p = sw + 4 * (gw + k * GW);
-            d0 = __ldg(p);
-            d1 = __ldg(p + 1);
-            d2 = __ldg(p + 2);
-            d3 = __ldg(p + 3);
+            const ulonglong2 sc = __ldg(seg_ptr(k));  // src_offset, dst_capacity
+            const uint32_t n = (uint32_t)__ldg(seg_ptr(k) + 1).y;
+            info_n = n;
+            info_f = (uint32_t)((uintptr_t)(in + sc.x) & 15) | (n == 0 ? 0x100u : 0u) |
+                     (!kSizes && n && sc.y < (((uint64_t)n + 3) >> 2) + 4ull * n ? 0x200u : 0u);
         }
     };
-    refill();
+    check();
     uint32_t di = 0;
     uint32_t piece = 0;      // next piece of descriptor di
     uint32_t head = 0, tail = 0, hpos = 0;
@@ -938,27 +934,20 @@ __global__ void __launch_bounds__(kRThreads)
     unsigned long long off = 0;  // data bytes of the segment's earlier pieces
     for (;;) {
         while (qh - qt < kRSlots && dbase + di < cnt) {
-            const unsigned long long src = __shfl_sync(kFull, d0, di), cap = __shfl_sync(kFull, d1, di);
-            const unsigned long long dst = __shfl_sync(kFull, d2, di), np = __shfl_sync(kFull, d3, di);
-            const uint32_t n = (uint32_t)np;
-            const uint64_t s_idx = gw + (dbase + di) * GW;
-            const uint32_t pn = n <= kBatchSmallN ? n : kEPieceN;  // integers per piece
-            const uint32_t npieces = n ? (n - 1) / kEPieceN + 1 : 0u;
-            bool take = false, done = true;
-            uint32_t at = 0, cover = 0, waste = 0, m = 0;
-            uintptr_t a0 = 0;
-            if (n == 0) {
-                if (lane == 0) out_lens[s_idx] = 0;
-            } else if (!kSizes && piece == 0 && cap < (((uint64_t)n + 3) >> 2) + 4ull * n) {
-                if (lane == 0) {  // nothing written: a zero length keeps callers that pack by out_lens in bounds
+            const uint32_t n = __shfl_sync(kFull, info_n, di), f = __shfl_sync(kFull, info_f, di);
+            const uint64_t s_idx = gw + (uint64_t)(dbase + di) * GW;
+            bool done = true;
+            if (f & 0x300u) {  // empty, or capacity short: nothing written; a zero length keeps
+                if (lane == 0) {  // callers that pack by out_lens in bounds
                     out_lens[s_idx] = 0;
-                    report3(status, epoch, BCGPU_ERR_INVALID_ARGUMENT);
+                    if (f & 0x200u) report3(status, epoch, BCGPU_ERR_INVALID_ARGUMENT);
                 }
             } else {
-                m = piece + 1 < npieces ? pn : n - piece * pn;
-                const uintptr_t beg = (uintptr_t)(in + src + (uint64_t)piece * pn);
-                a0 = beg & ~(uintptr_t)15;
-                cover = (uint32_t)(((beg + 4ull * m + 15) & ~(uintptr_t)15) - a0) + kEHead;
+                const uint32_t pn = n <= kBatchSmallN ? n : kEPieceN;  // integers per piece
+                const uint32_t npieces = (n - 1) / kEPieceN + 1;
+                const uint32_t m = piece + 1 < npieces ? pn : n - piece * pn;
+                const uint32_t ph = f & 15u;  // pieces start 7680 B apart: every piece has the segment's phase
+                const uint32_t cover = ((ph + 4 * m + 15) & ~15u) + kEHead;
                 if (qh == qt) {  // nothing unconsumed: once the last item's stores have read it, restart at 0
                     if (tail_next != tail) {
                         if (lane == 0) tma_store_wait_read();
@@ -967,28 +956,27 @@ __global__ void __launch_bounds__(kRThreads)
                     head = tail = tail_next = hpos = 0;
                 }
                 const bool wrap = hpos + cover > ring_bytes;
-                waste = wrap ? ring_bytes - hpos : 0u;
-                at = wrap ? 0u : hpos;
+                const uint32_t waste = wrap ? ring_bytes - hpos : 0u;
+                const uint32_t at = wrap ? 0u : hpos;
                 if (head + waste + cover - tail > ring_bytes) break;  // wait for space
-                take = true;
                 done = piece + 1 == npieces;
-            }
-            if (take) {
                 const uint32_t slot = qh % kRSlots;
                 if (lane == 0) {
+                    const ulonglong2 sc = __ldg(seg_ptr(dbase + di)), dn = __ldg(seg_ptr(dbase + di) + 1);
+                    const uintptr_t beg = (uintptr_t)(in + sc.x + (uint64_t)piece * pn);
                     EItem3& it = B.item[slot];
-                    it.dst = dst;
+                    it.dst = dn.x;
                     it.seg = s_idx;
                     it.n = n;
-                    it.prev = (uint32_t)(np >> 32);
+                    it.prev = (uint32_t)(dn.y >> 32);
                     it.m = m;
                     it.piece = piece;
-                    it.spos = at + kEHead + (uint32_t)((uintptr_t)(in + src + (uint64_t)piece * pn) & 15);
+                    it.spos = at + kEHead + ph;
                     it.end = head + waste + cover;
                     fence_async_smem();
                     mbar_expect_s(bar0 + 8 * slot, cover - kEHead);
-                    tma_load_hint_s(ring + at + kEHead, reinterpret_cast<const void*>(a0), cover - kEHead, bar0 + 8 * slot,
-                                    pol);
+                    tma_load_hint_s(ring + at + kEHead, reinterpret_cast<const void*>(beg & ~(uintptr_t)15),
+                                    cover - kEHead, bar0 + 8 * slot, pol);
                 }
                 head += waste + cover;
                 hpos = at + cover;
@@ -999,7 +987,7 @@ __global__ void __launch_bounds__(kRThreads)
                 if (++di == 32) {
                     dbase += 32;
                     di = 0;
-                    refill();
+                    check();
                 }
             } else {
                 ++piece;
@@ -1074,19 +1062,12 @@ cudaError_t launch_encode_batch3(const bcgpu_encode_segment* segs, uint64_t nseg
     const uint64_t want = (nseg + kRWarps - 1) / kRWarps, capg = (uint64_t)sms * occ;
     const int grid = (int)(want < capg ? want : capg);
     if (grid <= 0) return cudaSuccess;
-    if (sizes) {
-        if (delta)
-            svb_encode_batch3_kernel<true, true><<<grid, kRThreads, smem, stream>>>(segs, nseg, in, out, out_lens,
-                                                                                   ba.status, ba.epoch, ring);
-        else
-            svb_encode_batch3_kernel<false, true><<<grid, kRThreads, smem, stream>>>(segs, nseg, in, out, out_lens,
-                                                                                    ba.status, ba.epoch, ring);
-    } else if (delta) {
-        svb_encode_batch3_kernel<true, false><<<grid, kRThreads, smem, stream>>>(segs, nseg, in, out, out_lens,
-                                                                                ba.status, ba.epoch, ring);
-    } else {
-        svb_encode_batch3_kernel<false, false><<<grid, kRThreads, smem, stream>>>(segs, nseg, in, out, out_lens,
-                                                                                 ba.status, ba.epoch, ring);
+    auto kern = sizes ? (delta ? svb_encode_batch3_kernel<true, true> : svb_encode_batch3_kernel<false, true>)
+                      : (delta ? svb_encode_batch3_kernel<true, false> : svb_encode_batch3_kernel<false, false>);
+    constexpr uint64_t kMaxSeg = 1ull << 31;  // the kernel counts segments in 32 bits
+    for (uint64_t s0 = 0; s0 < nseg; s0 += kMaxSeg) {
+        const uint64_t ns = nseg - s0 < kMaxSeg ? nseg - s0 : kMaxSeg;
+        kern<<<grid, kRThreads, smem, stream>>>(segs + s0, ns, in, out, out_lens + s0, ba.status, ba.epoch, ring);
     }
     return cudaGetLastError();
 }

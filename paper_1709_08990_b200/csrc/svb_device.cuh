@@ -139,13 +139,16 @@ __device__ __forceinline__ uint64_t lookback_exclusive_wide(const uint64_t* stat
 }
 
 // ---- scans -------------------------------------------------------------
+// Each step adds under the shuffle's own in-range predicate: shuffle + predicated add, where
+// shuffle + lane compare + select + add is what the compiler makes of `if (lane >= o) v += t`.
 __device__ __forceinline__ uint32_t warp_inclusive_scan(uint32_t v) {
-    const int lane = threadIdx.x & 31;
 #pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-        const uint32_t t = __shfl_up_sync(kFull, v, o);
-        if (lane >= o) v += t;
-    }
+    for (int o = 1; o < 32; o <<= 1)
+        asm("{\n\t.reg .pred p;\n\t.reg .u32 t;\n\t"
+            "shfl.sync.up.b32 t|p, %0, %1, 0, 0xffffffff;\n\t"
+            "@p add.u32 %0, %0, t;\n\t}"
+            : "+r"(v)
+            : "r"(o));
     return v;
 }
 
