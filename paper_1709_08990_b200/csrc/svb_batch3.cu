@@ -55,6 +55,7 @@ struct RItem {
 struct __align__(16) RWarpHdr {  // per warp, ahead of the rings in dynamic shared memory
     uint64_t bar[kRSlots];
     RItem item[kRSlots];
+    ulonglong2 desc[32][2];  // the descriptors of the warp's current 32 segments
 };
 
 // One control byte c whose data starts at shared byte address a -> 4 integers, from ONE read
@@ -544,15 +545,19 @@ __global__ void __launch_bounds__(kRThreads, BC_DEC3_MINB)
 
     // Lane l checks the descriptor of the warp's segment dbase + l once: info = its ring cover
     // (decoded here) | the status it reports << 16 | 1 << 31 when it is not decoded here.  The
-    // descriptors themselves stay in memory (lane 0 re-reads one from L1 when it issues it), so
-    // they hold no registers through the decode.
+    // descriptors go to a per-warp table in shared memory (lane 0 reads one when it issues it),
+    // so they hold no registers through the decode (re-reading them from global memory stalled
+    // lane 0 on L2 misses: the warp's descriptors are a grid-stride apart).
     uint32_t dbase = 0, info = 0;
     auto check = [&]() {
         const uint32_t k = dbase + lane;
         info = 0x80000000u;
         if (k < cnt) {
             const ulonglong2 sb = __ldg(seg_ptr(k));  // src_offset, src_bytes
-            const uint32_t n = (uint32_t)__ldg(seg_ptr(k) + 1).y;
+            const ulonglong2 dn = __ldg(seg_ptr(k) + 1);  // dst_offset, n | prev << 32
+            B.desc[lane][0] = sb;
+            B.desc[lane][1] = dn;
+            const uint32_t n = (uint32_t)dn.y;
             const uint64_t ngroups = ((uint64_t)n + 3) >> 2;
             uint32_t code = 0;
             if (n > kBatchSmallN)  // svb_batch2.cu decodes it -- unless the caller's max_seg_n said no segment is long
@@ -570,6 +575,7 @@ __global__ void __launch_bounds__(kRThreads, BC_DEC3_MINB)
         }
     };
     check();
+    __syncwarp();
     uint32_t di = 0;                // next descriptor of the batch (lane index)
     uint32_t head = 0, tail = 0;    // ring byte counters (allocated incl. wrap waste, freed)
     uint32_t hpos = 0;              // ring offset of the next allocation
@@ -588,7 +594,7 @@ __global__ void __launch_bounds__(kRThreads, BC_DEC3_MINB)
                 if (head + waste + cover - tail > ring_bytes) break;  // wait for space
                 const uint32_t slot = qh % kRSlots;
                 if (lane == 0) {
-                    const ulonglong2 sb = __ldg(seg_ptr(dbase + di)), dn = __ldg(seg_ptr(dbase + di) + 1);
+                    const ulonglong2 sb = B.desc[di][0], dn = B.desc[di][1];
                     const uintptr_t beg = (uintptr_t)in + sb.x;
                     RItem& it = B.item[slot];
                     it.dst = dn.x;
@@ -611,7 +617,9 @@ __global__ void __launch_bounds__(kRThreads, BC_DEC3_MINB)
             if (++di == 32) {
                 dbase += 32;
                 di = 0;
+                __syncwarp();  // lane 0 has read the table
                 check();
+                __syncwarp();
             }
         }
         __syncwarp();  // lane 0's item records before every lane reads them
@@ -911,15 +919,20 @@ __global__ void __launch_bounds__(kRThreads)
         return reinterpret_cast<const ulonglong2*>(segs + gw + (uint64_t)k * GW);
     };
     // Lane l checks the descriptor of the warp's segment dbase + l once: its n, and the 16-B
-    // phase of its integers | 0x100 when it is empty | 0x200 when its capacity is short.  The
-    // descriptors stay in memory (lane 0 re-reads one from L1 when it issues a piece).
-    uint32_t dbase = 0, info_n = 0, info_f = 0;
+    // phase of its integers | 0x100 when it is empty | 0x200 when its capacity is short; it
+    // keeps src, dst and prev for the shuffles that issue its pieces.
+    uint32_t dbase = 0, info_n = 0, info_f = 0, info_p = 0;
+    unsigned long long info_s = 0, info_d = 0;
     auto check = [&]() {
         const uint32_t k = dbase + lane;
         if (k < cnt) {
             const ulonglong2 sc = __ldg(seg_ptr(k));  // src_offset, dst_capacity
-            const uint32_t n = (uint32_t)__ldg(seg_ptr(k) + 1).y;
+            const ulonglong2 dn = __ldg(seg_ptr(k) + 1);  // dst_offset, n | prev << 32
+            const uint32_t n = (uint32_t)dn.y;
             info_n = n;
+            info_p = (uint32_t)(dn.y >> 32);
+            info_s = sc.x;
+            info_d = dn.x;
             info_f = (uint32_t)((uintptr_t)(in + sc.x) & 15) | (n == 0 ? 0x100u : 0u) |
                      (!kSizes && n && sc.y < (((uint64_t)n + 3) >> 2) + 4ull * n ? 0x200u : 0u);
         }
@@ -961,14 +974,15 @@ __global__ void __launch_bounds__(kRThreads)
                 if (head + waste + cover - tail > ring_bytes) break;  // wait for space
                 done = piece + 1 == npieces;
                 const uint32_t slot = qh % kRSlots;
+                const unsigned long long src = __shfl_sync(kFull, info_s, di), dst = __shfl_sync(kFull, info_d, di);
+                const uint32_t prv = __shfl_sync(kFull, info_p, di);
                 if (lane == 0) {
-                    const ulonglong2 sc = __ldg(seg_ptr(dbase + di)), dn = __ldg(seg_ptr(dbase + di) + 1);
-                    const uintptr_t beg = (uintptr_t)(in + sc.x + (uint64_t)piece * pn);
+                    const uintptr_t beg = (uintptr_t)(in + src + (uint64_t)piece * pn);
                     EItem3& it = B.item[slot];
-                    it.dst = dn.x;
+                    it.dst = dst;
                     it.seg = s_idx;
                     it.n = n;
-                    it.prev = (uint32_t)(dn.y >> 32);
+                    it.prev = prv;
                     it.m = m;
                     it.piece = piece;
                     it.spos = at + kEHead + ph;
