@@ -17,7 +17,7 @@
 // many segments in flight as fit (up to kRSlots), then decodes the oldest one
 // straight from the ring, 512 integers per warp pass with each lane owning
 // four consecutive groups (one length scan and one delta scan per pass);
-// outputs at any 4-B phase leave as 128-bit stores of 16-B granules.
+// outputs at any 4-B phase leave as 128/256-bit stores of 16-B granules.
 // Longer segments stay on svb_batch2.cu (they are skipped here).
 #include <cstdint>
 
@@ -58,244 +58,17 @@ struct __align__(16) RWarpHdr {  // per warp, ahead of the rings in dynamic shar
     ulonglong2 desc[32][2];  // the descriptors of the warp's current 32 segments
 };
 
-// One control byte c whose data starts at shared byte address a -> 4 integers, from ONE read
-// of the 20-byte window (five 32-bit loads instead of two per integer: the scattered lane
-// addresses make every load ~3.5-way bank-conflicted, and shared-memory wavefronts bound
-// this kernel).  X = the 16 data bytes from a; integer i starts at byte s_i of X.
-__device__ __forceinline__ uint32_t low_bytes(uint32_t x, uint32_t l) {  // l in 1..4
-    return x & (0xFFFFFFFFu >> (32u - 8u * l));
-}
-__device__ __forceinline__ uint4 group_w5(uint32_t a, uint32_t c) {
-    const uint32_t wa = a & ~3u, sh = (a & 3u) << 3;
-    const uint32_t w0 = lds32(wa), w1 = lds32(wa + 4), w2 = lds32(wa + 8), w3 = lds32(wa + 12), w4 = lds32(wa + 16);
-    const uint32_t X0 = __funnelshift_r(w0, w1, sh), X1 = __funnelshift_r(w1, w2, sh),
-                   X2 = __funnelshift_r(w2, w3, sh), X3 = __funnelshift_r(w3, w4, sh);
-    const uint32_t l0 = (c & 3u) + 1u, l1 = ((c >> 2) & 3u) + 1u, l2 = ((c >> 4) & 3u) + 1u, l3 = (c >> 6) + 1u;
-    const uint32_t s1 = l0, s2 = s1 + l1, s3 = s2 + l2;  // s1 in 1..4, s2 in 2..8, s3 in 3..12
-    uint4 v;
-    v.x = low_bytes(X0, l0);
-    v.y = low_bytes(__funnelshift_rc(X0, X1, 8 * s1), l1);
-    {
-        const bool q = s2 > 4;
-        v.z = low_bytes(__funnelshift_rc(q ? X1 : X0, q ? X2 : X1, 8 * (q ? s2 - 4 : s2)), l2);
-    }
-    {
-        const bool q2 = s3 > 8, q1 = s3 > 4;
-        const uint32_t lo = q2 ? X2 : (q1 ? X1 : X0), hi = q2 ? X3 : (q1 ? X2 : X1);
-        v.w = low_bytes(__funnelshift_rc(lo, hi, 8 * (s3 - (q2 ? 8u : (q1 ? 4u : 0u)))), l3);
-    }
-    return v;
-}
-
 __device__ __forceinline__ void report3(unsigned long long* st, uint32_t epoch, uint32_t code) {
     if (st) *st = ((unsigned long long)epoch << 32) | code;
 }
 
-// Decode one resident segment.  S = shared address of its byte 0; returns the data bytes the
-// control stream declares (the caller checks it against the stream length).
-//
-// Lane-contiguous layout: a pass covers 128 control bytes (512 integers); lane l owns groups
-// 4l..4l+3 of it, so one 32-bit read gives its four control bytes, SWAR gives their lengths,
-// and ONE warp scan of the lane totals places every group.  The delta prefix is a lane-serial
-// sum over the lane's 16 integers plus one warp scan.  R = the output's 4-B phase inside
-// 16 B (template: the granule assembly below is static register moves): lane l stores the
-// granules [4q - R, 4q - R + 4) for its groups q; the first takes the previous group's last R
-// integers from lane l - 1 (lane 0: the previous pass's lane 31).
 __device__ __forceinline__ void stg_stream_v8(void* p, const uint4& a, const uint4& b) {
     asm volatile("st.global.cs.v8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(p), "r"(a.x), "r"(a.y), "r"(a.z),
                  "r"(a.w), "r"(b.x), "r"(b.y), "r"(b.z), "r"(b.w)
                  : "memory");
 }
 
-// Store a pass's four granules per lane: granule k = elements [4 (g0 + k) - R, +4) relative to o,
-// at 16-B aligned Bp + 4 (g0 + k).  Lanes are 64 B apart, so each store instruction touches
-// 16 lines; pairs of whole granules on a 32-B boundary leave as one 256-bit store (sm_100),
-// halving the L1 wavefronts of the stores.
-template <uint32_t R>
-__device__ __forceinline__ void store_pass(const uint4 (&v)[4], uint32_t* __restrict__ o, uint32_t g0, int nints,
-                                           uint4& carry) {
-    const int lane = threadIdx.x & 31;
-    uint4 G[4];
-    uint32_t* Bp = o - R;  // 16-B aligned
-    if constexpr (R == 0) {
-#pragma unroll
-        for (int k = 0; k < 4; ++k) G[k] = v[k];
-    } else {
-        const int src = (lane + 31) & 31;
-        uint4 rot = make_uint4(0, 0, 0, 0);
-        rot.w = __shfl_sync(kFull, v[3].w, src);
-        if (R >= 2) rot.z = __shfl_sync(kFull, v[3].z, src);
-        if (R >= 3) rot.y = __shfl_sync(kFull, v[3].y, src);
-        const uint4 prv0 = lane == 0 ? carry : rot;
-        carry = rot;
-#pragma unroll
-        for (int k = 0; k < 4; ++k) {
-            const uint4 pv = k == 0 ? prv0 : v[k - 1], cv = v[k];
-            G[k] = R == 1 ? make_uint4(pv.w, cv.x, cv.y, cv.z)
-                 : R == 2 ? make_uint4(pv.z, pv.w, cv.x, cv.y)
-                          : make_uint4(pv.y, pv.z, pv.w, cv.x);
-        }
-    }
-    auto full = [&](int k) {
-        const int e0 = 4 * (int)(g0 + k) - (int)R;
-        return e0 >= 0 && e0 + 4 <= nints;
-    };
-    auto one = [&](int k) {
-        const int e0 = 4 * (int)(g0 + k) - (int)R;
-        if (e0 >= 0 && e0 + 4 <= nints) {
-            stg_stream_v4(Bp + 4 * (g0 + k), G[k]);
-        } else {
-#pragma unroll
-            for (int i = 0; i < 4; ++i)
-                if (e0 + i >= 0 && e0 + i < nints) Bp[4 * (g0 + k) + i] = comp(G[k], i);
-        }
-    };
-    if ((((uintptr_t)Bp) & 31) == 0) {  // warp-uniform: granule pairs (0,1), (2,3) are 32-B aligned
-#pragma unroll
-        for (int k = 0; k < 4; k += 2) {
-            if (full(k) && full(k + 1)) {
-                stg_stream_v8(Bp + 4 * (g0 + k), G[k], G[k + 1]);
-            } else {
-                one(k);
-                one(k + 1);
-            }
-        }
-    } else {  // pair (1,2) is
-        one(0);
-        if (full(1) && full(2)) {
-            stg_stream_v8(Bp + 4 * (g0 + 1), G[1], G[2]);
-        } else {
-            one(1);
-            one(2);
-        }
-        one(3);
-    }
-}
-
-// A segment of at most 128 integers (32 groups): one pass with one group per lane, so a short
-// list costs one group's work per lane instead of four (the per-segment floor of the
-// 4-group pass was ~670 warp instructions, ncu at 16 integers per list).
-template <bool kDelta>
-__device__ __forceinline__ uint32_t decode_resident_short(uint32_t S, uint32_t bytes, uint32_t n, uint32_t run,
-                                                          uint32_t* __restrict__ o) {
-    const int lane = threadIdx.x & 31;
-    const uint32_t ng = (n + 3) >> 2;  // <= 32
-    const uint32_t g = (uint32_t)lane;
-    const uint32_t tail = (n & 3u) ? (n & 3u) : 4u;
-    const bool valid = g < ng, lastg = g + 1 == ng;
-    uint32_t c = valid ? lds8(S + g) : 0u;
-    if (lastg && (n & 3u)) c &= (1u << (2 * (n & 3u))) - 1u;  // unused fields of the final control byte
-    const uint32_t len = valid ? fsum(c) + (lastg ? tail : 4u) : 0u;
-    const uint32_t I = warp_inclusive_scan(len);
-    const uint32_t D = S + ng, Dend = S + bytes;
-    const uint32_t a = min(D + I - len, Dend);
-    uint4 v = __all_sync(kFull, c == 0) ? zero_group_s(a) : group_w5(a, c);
-    v = mask_tail(v, valid ? (lastg ? tail : 4u) : 0u);
-    if constexpr (kDelta) {
-        v.y += v.x;
-        v.z += v.y;
-        v.w += v.z;
-        const uint32_t Iv = warp_inclusive_scan(v.w);
-        v = add4(v, run + Iv - v.w);
-    }
-    const int e0 = 4 * lane, cnt = (int)n - e0;
-    if (cnt > 0) {
-        uint32_t* q = o + e0;
-        if (cnt >= 4 && ((uintptr_t)q & 15) == 0) {
-            stg_stream_v4(q, v);
-        } else {
-            q[0] = v.x;
-            if (cnt > 1) q[1] = v.y;
-            if (cnt > 2) q[2] = v.z;
-            if (cnt > 3) q[3] = v.w;
-        }
-    }
-    return __shfl_sync(kFull, I, 31);
-}
-
-template <bool kDelta>
-__device__ __forceinline__ uint32_t decode_resident(uint32_t S, uint32_t bytes, uint32_t n, uint32_t run,
-                                                    uint32_t* __restrict__ o) {
-    const int lane = threadIdx.x & 31;
-    const uint32_t R = (uint32_t)(((uintptr_t)o >> 2) & 3u);  // output phase inside 16 B
-    const uint32_t ng = (n + 3) >> 2;
-    const uint32_t tail = (n & 3u) ? (n & 3u) : 4u;                          // integers in the last group
-    const uint32_t tmask = (n & 3u) ? ((1u << (2 * (n & 3u))) - 1u) : 0xFFu;  // its used fields
-    const uint32_t D = S + ng, Dend = S + bytes;                            // data region [D, Dend)
-    const uint32_t passes = (ng + 127) >> 7;
-    uint32_t off = 0;
-    uint4 carry = make_uint4(0, 0, 0, 0);
-#pragma unroll 1
-    for (uint32_t ps = 0; ps < passes; ++ps) {
-        const uint32_t g0 = 128 * ps + 4 * lane;  // the lane's first group
-        const uint32_t ca = S + g0;
-        uint32_t cw = __funnelshift_r(lds32(ca & ~3u), lds32((ca & ~3u) + 4), (ca & 3u) << 3);
-        uint32_t lens;
-        const bool lastp = ps + 1 == passes;
-        uint32_t nv = 4;  // valid groups of the lane
-        if (!lastp) {
-            lens = swar_lengths(cw);
-        } else {
-            nv = ng > g0 ? (ng - g0 < 4 ? ng - g0 : 4u) : 0u;
-            const uint32_t bm = nv >= 4 ? 0xFFFFFFFFu : ((1u << (8 * nv)) - 1u);
-            if (nv && g0 + nv == ng) cw &= ~(0xFFu << (8 * (nv - 1))) | (tmask << (8 * (nv - 1)));
-            cw &= bm;
-            lens = swar_lengths(cw) & bm;
-            if (nv && g0 + nv == ng) lens -= (4u - tail) << (8 * (nv - 1));
-        }
-        const uint32_t lt = __dp4a(lens, 0x01010101u, 0u);  // <= 64
-        const uint32_t I = warp_inclusive_scan(lt);
-        uint32_t p = D + off + I - lt;
-        off += __shfl_sync(kFull, I, 31);
-        uint4 v[4];
-        if (__all_sync(kFull, cw == 0)) {
-#pragma unroll
-            for (int k = 0; k < 4; ++k) v[k] = zero_group_s(min(p + 4 * k, Dend));
-        } else {
-#pragma unroll
-            for (int k = 0; k < 4; ++k) {
-                v[k] = group_w5(min(p, Dend), (cw >> (8 * k)) & 0xFFu);
-                p += (lens >> (8 * k)) & 0xFFu;
-            }
-        }
-        if (lastp) {
-#pragma unroll
-            for (int k = 0; k < 4; ++k)
-                v[k] = mask_tail(v[k], (uint32_t)k + 1 < nv ? 4u : ((uint32_t)k + 1 == nv ? (g0 + nv == ng ? tail : 4u) : 0u));
-        }
-        if constexpr (kDelta) {
-            uint32_t s = 0;
-#pragma unroll
-            for (int k = 0; k < 4; ++k) {
-                v[k].x += s;
-                v[k].y += v[k].x;
-                v[k].z += v[k].y;
-                v[k].w += v[k].z;
-                s = v[k].w;
-            }
-            const uint32_t Iv = warp_inclusive_scan(s);
-            const uint32_t add = run + Iv - s;
-#pragma unroll
-            for (int k = 0; k < 4; ++k) v[k] = add4(v[k], add);
-            run += __shfl_sync(kFull, Iv, 31);
-        }
-        switch (R) {  // warp-uniform; only these small store blocks are per phase
-            case 0: store_pass<0>(v, o, g0, (int)n, carry); break;
-            case 1: store_pass<1>(v, o, g0, (int)n, carry); break;
-            case 2: store_pass<2>(v, o, g0, (int)n, carry); break;
-            default: store_pass<3>(v, o, g0, (int)n, carry); break;
-        }
-    }
-    if (R != 0 && lane == 0) {  // the granule after the last pass: lane 31's last R integers (in carry)
-        const int e0 = 512 * (int)passes - (int)R;
-#pragma unroll
-        for (int i = 0; i < 3; ++i)
-            if (i < (int)R && e0 + i < (int)n) o[e0 + i] = comp(carry, 4 - (int)R + i);
-    }
-    return off;
-}
-
-// ---- decode v2: fewer instructions per group -------------------------------------------
+// ---- segment-resident decode -------------------------------------------------------------
 // x zero-extended from its low b bits (b clamped to 32): one SGXT instead of a mask shift + AND
 __device__ __forceinline__ uint32_t szext(uint32_t x, uint32_t b) {
     uint32_t r;
@@ -307,7 +80,8 @@ __device__ __forceinline__ uint32_t szext(uint32_t x, uint32_t b) {
 // 16 bytes X0..X3 act as a queue: integer i is the queue's low l_i bytes (SGXT by 8 l_i), then
 // the queue drops them (clamped funnel shifts: 8 l_i = 32 moves a whole word).  Each step
 // needs one word less, so the four integers cost 4 SGXT + 6 funnel shifts, with no selects
-// (group_w5 picks each integer's word pair with compare + select chains).
+// (round 1 picked each integer's word pair from the window with compare + select chains and
+// masked it with a shift + AND: ~40 instructions per group against ~30 here).
 // Shared word at a when pred, else whatever the register held (a predicated load: no branch,
 // no zeroing move).  Callers only use bytes of words they loaded.
 __device__ __forceinline__ uint32_t lds32_if(uint32_t a, bool pred) {
@@ -340,10 +114,13 @@ __device__ __forceinline__ uint4 group_q(uint32_t a, uint32_t len, uint32_t b0, 
     return v;
 }
 
-// Vector stores of the whole granules among a lane's groups g0 .. g0 + 3 (see store_pass for
-// the granule layout); pairs on a 32-B boundary leave as one 256-bit store.  Granules that
-// straddle the segment's ends are left to edge_stores, so each phase's block is a few
-// predicated stores.
+// Vector stores of the whole granules among a lane's groups g0 .. g0 + 3.  R = the output's
+// 4-B phase inside 16 B (a template: the granule assembly is static register moves): lane l
+// stores the granules [4q - R, 4q - R + 4) for its groups q at 16-B aligned Bp + 4q; the first
+// takes the previous group's last R integers from lane l - 1 (lane 0: the previous pass's lane
+// 31, in carry).  Lanes are 64 B apart, so pairs of granules on a 32-B boundary leave as one
+// 256-bit store (half the L1 wavefronts).  Granules that straddle the segment's ends are left
+// to the edge stores of decode_pass, so each phase's block is a few predicated stores.
 template <uint32_t R>
 __device__ __forceinline__ void store_whole(const uint4 (&v)[4], uint32_t* __restrict__ o, uint32_t g0, int nints,
                                             uint4& carry) {
@@ -397,7 +174,7 @@ __device__ __forceinline__ void store_whole(const uint4 (&v)[4], uint32_t* __res
     }
 }
 
-// One pass of decode_resident2: 128 groups from group gp, lane l owning groups g0 = gp + 4 l
+// One pass of decode_resident: 128 groups from group gp, lane l owning groups g0 = gp + 4 l
 // .. g0 + 3.  In the segment's last pass the groups past its end decode garbage that is never
 // stored: it only follows the valid integers in lane order, so no position, delta prefix or
 // store of a valid integer sees it, and the declared data length comes from the lane holding
@@ -502,7 +279,7 @@ __device__ __forceinline__ void decode_pass(uint32_t S, uint32_t D, uint32_t Den
 // data bytes its control stream declares.  group_q extraction, predicated scans, whole-granule
 // stores per phase and the segment-edge integers outside the per-phase blocks.
 template <bool kDelta>
-__device__ __forceinline__ uint32_t decode_resident2(uint32_t S, uint32_t bytes, uint32_t n, uint32_t run,
+__device__ __forceinline__ uint32_t decode_resident(uint32_t S, uint32_t bytes, uint32_t n, uint32_t run,
                                                      uint32_t* __restrict__ o) {
     const uint32_t R = (uint32_t)(((uintptr_t)o >> 2) & 3u);
     const uint32_t ng = (n + 3) >> 2;
@@ -522,7 +299,7 @@ __device__ __forceinline__ uint32_t decode_resident2(uint32_t S, uint32_t bytes,
 
 }  // namespace
 
-template <bool kDelta, bool kV1>
+template <bool kDelta>
 __global__ void __launch_bounds__(kRThreads, BC_DEC3_MINB)
     svb_decode_batch3_kernel(const bcgpu_decode_segment* __restrict__ segs, uint64_t nseg,
                              const uint8_t* __restrict__ in, uint32_t* __restrict__ out, unsigned long long* status,
@@ -629,10 +406,7 @@ __global__ void __launch_bounds__(kRThreads, BC_DEC3_MINB)
         mbar_wait_parity(&B.bar[slot], (qt / kRSlots) & 1u);
         const RItem it = B.item[slot];
         uint32_t* o = out + it.dst;
-        const uint32_t data = !kV1 ? decode_resident2<kDelta>(ring + it.spos, it.bytes, it.n, kDelta ? it.prev : 0u, o)
-                              : it.n <= 128
-                                  ? decode_resident_short<kDelta>(ring + it.spos, it.bytes, it.n, kDelta ? it.prev : 0u, o)
-                                  : decode_resident<kDelta>(ring + it.spos, it.bytes, it.n, kDelta ? it.prev : 0u, o);
+        const uint32_t data = decode_resident<kDelta>(ring + it.spos, it.bytes, it.n, kDelta ? it.prev : 0u, o);
         if (lane == 0) {
             const uint64_t need = (uint64_t)((it.n + 3) >> 2) + data;
             if (need != it.bytes) report3(status, epoch, need > it.bytes ? BCGPU_ERR_TRUNCATED : BCGPU_ERR_TRAILING_BYTES);
@@ -648,9 +422,8 @@ cudaError_t launch_decode_batch3(const bcgpu_decode_segment* segs, uint64_t nseg
     const uint32_t ring_kb = (ba.flags >> 16) & 0xFFu;  // debug: ring KiB per warp
     const uint32_t ring = ring_kb ? (ring_kb << 10 < kItemMax ? kItemMax : ring_kb << 10) : kRingDefault;
     const size_t smem = kRWarps * (sizeof(RWarpHdr) + ring + kRingSlack);
-    const bool v1 = (ba.flags & 1u) != 0;  // debug: the round-1 pass (group_w5, 4 groups per lane)
-    auto kd = v1 ? svb_decode_batch3_kernel<true, true> : svb_decode_batch3_kernel<true, false>;
-    auto kp = v1 ? svb_decode_batch3_kernel<false, true> : svb_decode_batch3_kernel<false, false>;
+    auto kd = svb_decode_batch3_kernel<true>;
+    auto kp = svb_decode_batch3_kernel<false>;
     cudaError_t a = launch_ensure_smem(kd, smem);
     if (a != cudaSuccess) return a;
     a = launch_ensure_smem(kp, smem);
