@@ -56,6 +56,7 @@ struct __align__(16) RWarpHdr {  // per warp, ahead of the rings in dynamic shar
     uint64_t bar[kRSlots];
     RItem item[kRSlots];
     ulonglong2 desc[32][2];  // the descriptors of the warp's current 32 segments
+    uint4 carry;             // decode: the last R integers of the previous pass's lane 31
 };
 
 __device__ __forceinline__ void report3(unsigned long long* st, uint32_t epoch, uint32_t code) {
@@ -123,7 +124,7 @@ __device__ __forceinline__ uint4 group_q(uint32_t a, uint32_t len, uint32_t b0, 
 // to the edge stores of decode_pass, so each phase's block is a few predicated stores.
 template <uint32_t R>
 __device__ __forceinline__ void store_whole(const uint4 (&v)[4], uint32_t* __restrict__ o, uint32_t g0, int nints,
-                                            uint4& carry) {
+                                            uint32_t cs) {
     const int lane = threadIdx.x & 31;
     uint4 G[4];
     uint32_t* Bp = o - R;  // 16-B aligned
@@ -136,8 +137,10 @@ __device__ __forceinline__ void store_whole(const uint4 (&v)[4], uint32_t* __res
         rot.w = __shfl_sync(kFull, v[3].w, src);
         if (R >= 2) rot.z = __shfl_sync(kFull, v[3].z, src);
         if (R >= 3) rot.y = __shfl_sync(kFull, v[3].y, src);
-        const uint4 prv0 = lane == 0 ? carry : rot;
-        carry = rot;
+        // lane 0 takes the previous pass's lane 31 values from the warp's carry slot in shared
+        // memory (a register uint4 live through every pass cost the sixth CTA per SM)
+        const uint4 prv0 = lane == 0 ? lds128v(cs) : rot;
+        if (lane == 0) sts128(cs, rot);
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
             const uint4 pv = j == 0 ? prv0 : v[j - 1], cv = v[j];
@@ -183,7 +186,7 @@ __device__ __forceinline__ void store_whole(const uint4 (&v)[4], uint32_t* __res
 template <bool kDelta>
 __device__ __forceinline__ void decode_pass(uint32_t S, uint32_t D, uint32_t Dend, uint32_t ng, uint32_t n,
                                             uint32_t gp, bool lastp, uint32_t R, int T, uint32_t& off, uint32_t& run,
-                                            uint4& carry, uint32_t* __restrict__ o) {
+                                            uint32_t cs, uint32_t* __restrict__ o) {
     const int lane = threadIdx.x & 31;
     const uint32_t g0 = gp + 4 * lane;
     const uint32_t ca = S + g0;
@@ -244,10 +247,10 @@ __device__ __forceinline__ void decode_pass(uint32_t S, uint32_t D, uint32_t Den
         run += __shfl_sync(kFull, Iv, 31);
     }
     switch (R) {  // warp-uniform; only these small store blocks are per phase
-        case 0: store_whole<0>(v, o, g0, (int)n, carry); break;
-        case 1: store_whole<1>(v, o, g0, (int)n, carry); break;
-        case 2: store_whole<2>(v, o, g0, (int)n, carry); break;
-        default: store_whole<3>(v, o, g0, (int)n, carry); break;
+        case 0: store_whole<0>(v, o, g0, (int)n, cs); break;
+        case 1: store_whole<1>(v, o, g0, (int)n, cs); break;
+        case 2: store_whole<2>(v, o, g0, (int)n, cs); break;
+        default: store_whole<3>(v, o, g0, (int)n, cs); break;
     }
     // The integers no whole granule holds: the head granule's [0, 4 - R) (R != 0: lane 0's first
     // group in the first pass) and the tail [T, n), <= 3 integers held by at most two lanes
@@ -280,18 +283,17 @@ __device__ __forceinline__ void decode_pass(uint32_t S, uint32_t D, uint32_t Den
 // stores per phase and the segment-edge integers outside the per-phase blocks.
 template <bool kDelta>
 __device__ __forceinline__ uint32_t decode_resident(uint32_t S, uint32_t bytes, uint32_t n, uint32_t run,
-                                                     uint32_t* __restrict__ o) {
+                                                    uint32_t cs, uint32_t* __restrict__ o) {
     const uint32_t R = (uint32_t)(((uintptr_t)o >> 2) & 3u);
     const uint32_t ng = (n + 3) >> 2;
     const uint32_t D = S + ng, Dend = S + bytes;
     const int T = 4 * (int)((n + R) >> 2) - (int)R;  // the tail no whole granule holds: [T, n)
     const uint32_t full_passes = (ng - 1) >> 7;       // every pass but the last holds 128 groups
     uint32_t off = 0;
-    uint4 carry = make_uint4(0, 0, 0, 0);
 #pragma unroll 1
     for (uint32_t ps = 0;; ++ps) {
         const bool lastp = ps == full_passes;
-        decode_pass<kDelta>(S, D, Dend, ng, n, 128 * ps, lastp, R, T, off, run, carry, o);
+        decode_pass<kDelta>(S, D, Dend, ng, n, 128 * ps, lastp, R, T, off, run, cs, o);
         if (lastp) break;
     }
     return off;
@@ -314,7 +316,7 @@ __global__ void __launch_bounds__(kRThreads, BC_DEC3_MINB)
     // nseg < 2^32 (the launcher splits larger batches)
     const uint32_t gw = blockIdx.x * kRWarps + warp, GW = gridDim.x * kRWarps;
     const uint32_t cnt = nseg > gw ? (uint32_t)((nseg - gw + GW - 1) / GW) : 0u;  // segments gw, gw + GW, ...
-    const uint32_t ring = sh_addr(ring_p), bar0 = sh_addr(&B.bar[0]);
+    const uint32_t ring = sh_addr(ring_p), bar0 = sh_addr(&B.bar[0]), carry_s = sh_addr(&B.carry);
     const uint64_t pol = l2_policy_drop();
     auto seg_ptr = [&](uint32_t k) {  // the warp's k-th segment
         return reinterpret_cast<const ulonglong2*>(segs + gw + (uint64_t)k * GW);
@@ -406,7 +408,7 @@ __global__ void __launch_bounds__(kRThreads, BC_DEC3_MINB)
         mbar_wait_parity(&B.bar[slot], (qt / kRSlots) & 1u);
         const RItem it = B.item[slot];
         uint32_t* o = out + it.dst;
-        const uint32_t data = decode_resident<kDelta>(ring + it.spos, it.bytes, it.n, kDelta ? it.prev : 0u, o);
+        const uint32_t data = decode_resident<kDelta>(ring + it.spos, it.bytes, it.n, kDelta ? it.prev : 0u, carry_s, o);
         if (lane == 0) {
             const uint64_t need = (uint64_t)((it.n + 3) >> 2) + data;
             if (need != it.bytes) report3(status, epoch, need > it.bytes ? BCGPU_ERR_TRUNCATED : BCGPU_ERR_TRAILING_BYTES);

@@ -602,9 +602,6 @@ struct __align__(16) D1Shared {
     uint32_t carry, incl;
 };
 
-__device__ __forceinline__ void sts128(uint32_t a, const uint4& v) {
-    asm volatile("st.shared.v4.u32 [%0], {%1,%2,%3,%4};" ::"r"(a), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w) : "memory");
-}
 
 // any sub-tile (partial, or data read from global memory) with carry `run`: word i of its
 // data window is fw(i), data at byte `head`; stores its integers, returns the last value
