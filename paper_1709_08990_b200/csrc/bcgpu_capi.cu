@@ -476,7 +476,9 @@ int bcgpu_svb_encode_batch_device(bcgpu_ctx* c, const bcgpu_encode_segment* d_se
     BatchArgs ba;
     int st = make_batch(c, s, &ba);
     if (st) return st;
-    (void)max_seg_n;  // one kernel serves every segment length
+    // one kernel serves every segment length; a bound <= kBatchSmallN (every segment one piece)
+    // lets it size its rings for a sixth CTA per SM
+    ba.max_seg_n = max_seg_n;
     BC_CUDA(launch_encode_batch(d_segs, nseg, d_in, d_out, d_out_lens, delta, ba, s));
     g_launches.fetch_add(1);
     return BCGPU_OK;
@@ -932,7 +934,9 @@ int bcgpu_svb_encode_batch_host(bcgpu_ctx* c, const uint32_t* values, const uint
         BC_CUDA(launch_batch_encode_describe(d_n, seg_prev ? d_prev : nullptr, p.s0, m, p.i0, d_es, sc));
         BC_CUDA(launch_sizes_batch(d_es + p.s0, m, d_vals, d_sz + p.s0, delta, ba, sc));
         BC_CUDA(launch_batch_pack(d_sz, p.s0, m, d_es, d_offs, d_run, sc));
-        BC_CUDA(launch_encode_batch(d_es + p.s0, m, d_vals, d_out, d_sz + p.s0, delta, ba, sc));
+        BatchArgs be = ba;
+        be.max_seg_n = p.max_n ? p.max_n : 1u;  // the piece's longest segment: ring sizing
+        BC_CUDA(launch_encode_batch(d_es + p.s0, m, d_vals, d_out, d_sz + p.s0, delta, be, sc));
         BC_CUDA(cudaMemcpyAsync(c->pin + k, d_run, 8, cudaMemcpyDeviceToHost, sc));
         BC_CUDA(cudaEventRecord(ev_done[k], sc));
         g_launches.fetch_add(4);

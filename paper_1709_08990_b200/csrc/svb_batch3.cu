@@ -470,6 +470,8 @@ namespace {
 
 constexpr uint32_t kEHead = 16;            // ring bytes reserved below an item's integers
 constexpr uint32_t kERingDefault = 9216;   // ring bytes per warp (sweep: 8-9 KiB best, 5 CTAs per SM)
+constexpr uint32_t kEItemMax = ((15 + 4 * kBatchSmallN + 15) & ~15u) + 16;  // largest encode item (phase, head)
+static_assert(kERingDefault >= kEItemMax, "an encode item must fit the ring");
 constexpr uint32_t kECtrlBuf = 512;        // >= 16 + ceil(kBatchSmallN / 4)
 constexpr uint32_t kEPieceN = kBatchSmallN;  // piece of a long segment: five full 384-integer blocks (cfg5: 1024 -> 1152 -> 1536 -> 1920 ints = 2.97 -> 2.25 -> 2.03 -> 1.91 ms)
 static_assert(16 + (kBatchSmallN + 3) / 4 <= kECtrlBuf, "control buffer");
@@ -832,7 +834,11 @@ __global__ void __launch_bounds__(kRThreads)
 cudaError_t launch_encode_batch3(const bcgpu_encode_segment* segs, uint64_t nseg, const uint32_t* in, uint8_t* out,
                                  uint64_t* out_lens, int delta, const BatchArgs& ba, cudaStream_t stream, bool sizes) {
     const uint32_t ring_kb = (ba.flags >> 24) & 0xFFu;  // debug: ring KiB per warp
-    const uint32_t ring = ring_kb ? (ring_kb << 10 < kItemMax ? kItemMax : ring_kb << 10) : kERingDefault;
+    // rings: 9 KiB by default (5 CTAs per SM; a long segment's 7.5 KiB pieces still overlap with
+    // short items); when the caller bounds every segment to one piece, rings of exactly one
+    // largest item let a sixth CTA fit (cfg4: 2.01 -> 1.98 ms; cfg5's pieces lose the overlap)
+    const uint32_t ring = ring_kb ? (ring_kb << 10 < kEItemMax ? kEItemMax : ring_kb << 10)
+                                  : (ba.max_seg_n != 0 && ba.max_seg_n <= kBatchSmallN ? kEItemMax : kERingDefault);
     const size_t smem = kRWarps * (sizeof(EWarpHdr) + ring + kRingSlack);
     const void* fns[4] = {(const void*)svb_encode_batch3_kernel<true, false>,
                           (const void*)svb_encode_batch3_kernel<false, false>,
