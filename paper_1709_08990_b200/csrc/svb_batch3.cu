@@ -36,6 +36,9 @@ namespace {
 #ifndef BC_DEC3_MINB
 #define BC_DEC3_MINB 5  // decode CTAs per SM the register budget must allow (6 spills)
 #endif
+#ifndef BC_ENC3_MINB
+#define BC_ENC3_MINB 5  // encode CTAs per SM the register budget must allow (6: <= 80 registers spills, cfg4 1.96 vs 1.88 ms)
+#endif
 constexpr int kRWarps = 4;
 constexpr int kRThreads = 32 * kRWarps;
 constexpr uint32_t kRingDefault = 8192;   // ring bytes per warp (launch-time; >= kItemMax)
@@ -675,7 +678,7 @@ __device__ __forceinline__ uint32_t size_resident(uint32_t Sin, uint32_t m, uint
 // into kEPieceN-integer pieces that the same warp encodes in order, carrying the data offset
 // and the delta base in registers (control bytes of piece k at k * kEPieceN / 4).
 template <bool kDelta, bool kSizes>
-__global__ void __launch_bounds__(kRThreads)
+__global__ void __launch_bounds__(kRThreads, BC_ENC3_MINB)
     svb_encode_batch3_kernel(const bcgpu_encode_segment* __restrict__ segs, uint64_t nseg,
                              const uint32_t* __restrict__ in, uint8_t* __restrict__ out,
                              uint64_t* __restrict__ out_lens, unsigned long long* status, uint32_t epoch,

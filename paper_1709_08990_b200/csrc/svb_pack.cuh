@@ -17,6 +17,7 @@
 #pragma once
 
 #include <cstdint>
+#include <type_traits>
 
 #include "svb_device.cuh"
 #include "svb_fast.cuh"
@@ -33,7 +34,7 @@ __device__ __forceinline__ uint32_t shfl_l(uint32_t lo, uint32_t hi, uint32_t s)
 __device__ __forceinline__ uint32_t group_ctrl(const uint4& x, uint32_t& tot) {
     const uint32_t m0 = blen_m1(x.x), m1 = blen_m1(x.y), m2 = blen_m1(x.z), m3 = blen_m1(x.w);
     tot = m0 + m1 + m2 + m3 + 4u;
-    return m0 | (m1 << 2) | (m2 << 4) | (m3 << 6);
+    return m0 + (m1 << 2) + (m2 << 4) + (m3 << 6);  // disjoint fields: + lets ptxas use either integer pipe
 }
 
 // data bytes of a control byte: 4 + the sum of its fields (length[c])
@@ -46,29 +47,33 @@ __device__ __forceinline__ uint32_t ctrl_bytes(uint32_t c) {
 __device__ __forceinline__ uint4 group_bytes(const uint4& x, uint32_t c, uint32_t& e8) {
     const uint32_t sA = ((c & 3u) << 3) + 8u;          // 8 l0, 8..32
     const uint32_t sB = ((c >> 1) & 0x18u) + 8u;       // 8 l2
-    const uint32_t A0 = x.x | __funnelshift_lc(0u, x.y, sA);  // x1 << 8 l0 (0 when l0 = 4)
+    const uint32_t A0 = x.x + __funnelshift_lc(0u, x.y, sA);  // x1 << 8 l0 (0 when l0 = 4)
     const uint32_t A1 = __funnelshift_lc(x.y, 0u, sA);        // x1 >> (32 - 8 l0)
-    const uint32_t B0 = x.z | __funnelshift_lc(0u, x.w, sB);
+    const uint32_t B0 = x.z + __funnelshift_lc(0u, x.w, sB);
     const uint32_t B1 = __funnelshift_lc(x.w, 0u, sB);
     const uint32_t la8 = sA + ((c << 1) & 0x18u) + 8u;  // 8 (l0 + l1), 16..64
     e8 = la8 + sB + ((c >> 3) & 0x18u) + 8u;
-    // B << 8 (l0 + l1) over four words: shift B by t = la8 (la8 < 32) or la8 - 32 (la8 >= 32,
-    // then one word up); clamped funnel shifts make t = 32 (la8 = 64) land B in words 2-3
-    const bool k1 = la8 >= 32u;                         // B starts in word 1 (or 2 when la8 = 64)
-    const uint32_t t = k1 ? la8 - 32u : la8;             // 0..32
-    const uint32_t Z0 = __funnelshift_lc(0u, B0, t), Z1 = __funnelshift_lc(B0, B1, t), Z2 = __funnelshift_lc(B1, 0u, t);
+    // B << 8 (l0 + l1) over four words, la8 = 16..64: one 64-bit shift left for words 0-1 and
+    // one right (by 64 - la8) for words 2-3.  PTX shifts clamp at 64, and each 64-bit shift is
+    // two SHF (no word selects: the 32-bit form needed a compare, a subtract and five selects)
+    uint64_t Bq, L, H;
+    asm("mov.b64 %0, {%1, %2};" : "=l"(Bq) : "r"(B0), "r"(B1));
+    asm("shl.b64 %0, %1, %2;" : "=l"(L) : "l"(Bq), "r"(la8));
+    asm("shr.b64 %0, %1, %2;" : "=l"(H) : "l"(Bq), "r"(64u - la8));
+    uint32_t L0, L1;
     uint4 G;
-    G.x = A0 | (k1 ? 0u : Z0);
-    G.y = A1 | (k1 ? Z0 : Z1);
-    G.z = k1 ? Z1 : Z2;
-    G.w = k1 ? Z2 : 0u;
+    asm("mov.b64 {%0, %1}, %2;" : "=r"(L0), "=r"(L1) : "l"(L));
+    asm("mov.b64 {%0, %1}, %2;" : "=r"(G.z), "=r"(G.w) : "l"(H));
+    G.x = A0 + L0;
+    G.y = A1 + L1;
     return G;
 }
 
 // Pack one group of each lane of a row at shared byte address a (groups of consecutive
 // lanes are consecutive in the stream: a_{l+1} = a_l + ctrl_bytes(c_l)).  carry: the
 // pending (partially filled) word after the previous row's last group, in and out; the
-// caller stores it after the last row.  Every lane of the warp must call this.
+// caller stores it after the last row (lane 0 holds it; other lanes' values are not meaningful).
+// Every lane of the warp must call this.
 __device__ __forceinline__ void pack_group_row(const uint4& x, uint32_t c, uint32_t a, uint32_t& carry) {
     const int lane = threadIdx.x & 31;
     uint32_t e8;
@@ -80,14 +85,24 @@ __device__ __forceinline__ void pack_group_row(const uint4& x, uint32_t c, uint3
     const bool p1 = e8 >= 64u, p2 = e8 >= 96u, p3 = e8 >= 128u;
     // the word the next group shares (all zero when this group ends on a word boundary)
     const uint32_t pend = p3 ? W4 : p2 ? W3 : p1 ? W2 : W1;
-    uint32_t pin = __shfl_up_sync(kFull, pend, 1);
-    if (lane == 0) pin = carry;
-    carry = __shfl_sync(kFull, pend, 31);
+    // one rotation: lanes 1..31 take their left neighbour's pending word, lane 0 takes lane
+    // 31's, which is what it needs for the NEXT row (carry is only meaningful in lane 0)
+    const uint32_t rot = __shfl_sync(kFull, pend, (lane + 31) & 31);
+    const uint32_t pin = lane == 0 ? carry : rot;
+    carry = rot;
     const uint32_t wa = a & ~3u;
-    sts32(wa, W0 | pin);
+    sts32(wa, W0 + pin);
     sts32_if(wa + 4, W1, p1);
     sts32_if(wa + 8, W2, p2);
     sts32_if(wa + 12, W3, p3);
+}
+
+// 16 bytes at word phase Q (0..3) and bit phase r of the 32 aligned bytes lo:hi
+template <int Q>
+__device__ __forceinline__ uint4 realign_pick(const uint4& lo, const uint4& hi, uint32_t r) {
+    const uint32_t w[8] = {lo.x, lo.y, lo.z, lo.w, hi.x, hi.y, hi.z, hi.w};
+    return make_uint4(__funnelshift_r(w[Q], w[Q + 1], r), __funnelshift_r(w[Q + 1], w[Q + 2], r),
+                      __funnelshift_r(w[Q + 2], w[Q + 3], r), __funnelshift_r(w[Q + 3], w[Q + 4], r));
 }
 
 // Packed bytes [src, src + len) of shared memory (>= 32 readable bytes after the end) -> global
@@ -111,28 +126,28 @@ __device__ __forceinline__ void store_realigned2(uint32_t src, uint32_t len, uin
         const uint32_t s0 = src + head;                 // source of the first interior byte
         const uint32_t r = (s0 & 3u) << 3, q = (s0 >> 2) & 3u;
         const uint32_t c0 = s0 & ~15u;
-        for (uint32_t k = lane; k < ng; k += 32) {
-            const uint4 lo = lds128v(c0 + 16 * k), hi = lds128v(c0 + 16 * k + 16);
-            uint4 v;
-            switch (q) {
-                case 0:
-                    v = make_uint4(__funnelshift_r(lo.x, lo.y, r), __funnelshift_r(lo.y, lo.z, r),
-                                   __funnelshift_r(lo.z, lo.w, r), __funnelshift_r(lo.w, hi.x, r));
-                    break;
-                case 1:
-                    v = make_uint4(__funnelshift_r(lo.y, lo.z, r), __funnelshift_r(lo.z, lo.w, r),
-                                   __funnelshift_r(lo.w, hi.x, r), __funnelshift_r(hi.x, hi.y, r));
-                    break;
-                case 2:
-                    v = make_uint4(__funnelshift_r(lo.z, lo.w, r), __funnelshift_r(lo.w, hi.x, r),
-                                   __funnelshift_r(hi.x, hi.y, r), __funnelshift_r(hi.y, hi.z, r));
-                    break;
-                default:
-                    v = make_uint4(__funnelshift_r(lo.w, hi.x, r), __funnelshift_r(hi.x, hi.y, r),
-                                   __funnelshift_r(hi.y, hi.z, r), __funnelshift_r(hi.z, hi.w, r));
-                    break;
+        // the phase switch sits outside the loop and the loop handles two granules per lane
+        // and trip, all four loads first (one granule per trip left every lane waiting out a
+        // shared-memory round trip ~6 times per sub-tile)
+        auto run = [&](auto qc) {
+            constexpr int Q = decltype(qc)::value;
+            uint32_t k = lane;
+            for (; k + 32 < ng; k += 64) {
+                const uint4 lo0 = lds128v(c0 + 16 * k), hi0 = lds128v(c0 + 16 * k + 16);
+                const uint4 lo1 = lds128v(c0 + 16 * k + 512), hi1 = lds128v(c0 + 16 * k + 528);
+                *reinterpret_cast<uint4*>(A0 + 16 * (uintptr_t)k) = realign_pick<Q>(lo0, hi0, r);
+                *reinterpret_cast<uint4*>(A0 + 16 * (uintptr_t)k + 512) = realign_pick<Q>(lo1, hi1, r);
             }
-            *reinterpret_cast<uint4*>(A0 + 16 * (uintptr_t)k) = v;
+            if (k < ng) {
+                const uint4 lo = lds128v(c0 + 16 * k), hi = lds128v(c0 + 16 * k + 16);
+                *reinterpret_cast<uint4*>(A0 + 16 * (uintptr_t)k) = realign_pick<Q>(lo, hi, r);
+            }
+        };
+        switch (q) {
+            case 0: run(std::integral_constant<int, 0>{}); break;
+            case 1: run(std::integral_constant<int, 1>{}); break;
+            case 2: run(std::integral_constant<int, 2>{}); break;
+            default: run(std::integral_constant<int, 3>{}); break;
         }
     }
     if ((uint32_t)lane < head) dst[lane] = (uint8_t)lds8(src + lane);
@@ -213,7 +228,7 @@ __device__ __forceinline__ uint32_t enc_lengths2(uint32_t sin, uint32_t prev_w, 
         const uint4 x = enc_row<kDelta, kAny>(sin, j, last);
         uint32_t tot;
         const uint32_t c = group_ctrl(x, tot);
-        cw[j >> 2] |= c << (8 * (j & 3));
+        cw[j >> 2] += c << (8 * (j & 3));
         P[j / 3] += tot << (10 * (j % 3));
         cdst[32 * j + lane] = (uint8_t)c;
     }

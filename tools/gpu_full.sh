@@ -14,5 +14,5 @@ for W in cfg3 cfg2 cfg4 cfg5; do
 done
 python tools/sweep_encode.py 3 0x0 > gpurun_out/sweep_$T.log 2>&1 && \
 ncu --set full --clock-control none --import-source on -k regex:"svb_encode1" -s 2 -c 1 -o gpurun_out/ncu_${T}_cfg3enc python tools/sweep_encode.py 3 0x0 > /dev/null 2>&1
-tail -2 gpurun_out/pytest_$T.log gpurun_out/smoke_$T.log; grep "\[bench\]" gpurun_out/bench_$T.log | cut -c 1-400; tail -c 300 gpurun_out/ref_$T.log
+for f in gpurun_out/pytest_$T.log gpurun_out/smoke_$T.log; do tail -n 2 $f; done; grep "\[bench\]" gpurun_out/bench_$T.log | cut -c 1-400; tail -c 300 gpurun_out/ref_$T.log
 bash tools/gpu_ncu_batch.sh ${T}b 0x0 > /dev/null 2>&1
