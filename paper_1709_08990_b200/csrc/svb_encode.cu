@@ -642,10 +642,6 @@ __global__ void __launch_bounds__(kE1Threads, 2)
         // ---- scanner: tile offsets (deferred look-back) and tile aggregates ----
         unsigned long long incl = 0;  // inclusive data offset of the CTA's last resolved tile
         uint32_t aprev = 0;           // aggregate of tprev
-        auto entry = [&](uint32_t j, unsigned long long v) -> uint32_t {
-            while ((uint32_t)(v >> 32) != epoch) v = ld_relaxed_u64(meta.agg + j);
-            return (uint32_t)v;
-        };
         // window of tile tp: tiles wl .. tp - 1 lie between the CTA's own tiles tp - G and tp;
         // read as 16-B aligned pairs, 8 per lane (512 tiles) issued before the wait for the
         // current tile's sizes, so the L2 round trip overlaps the consumers' work
@@ -658,6 +654,23 @@ __global__ void __launch_bounds__(kE1Threads, 2)
                 v[u] = e < tp ? ld_relaxed_u64x2(meta.agg + e) : make_ulonglong2(0ull, 0ull);
             }
         };
+        // pairs of tile tp's window (from e0) that still hold an older tag are re-read, all of a
+        // lane's re-reads in flight together; true when this lane re-read any
+        auto refresh = [&](uint32_t tp, uint32_t e0) -> bool {
+            const uint32_t wl = tp + 1 > G ? tp + 1 - G : 0u;
+            bool stale = false;
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                const uint32_t e = e0 + 64 * u + 2 * lane;
+                const bool nx = e < tp && e >= wl && (uint32_t)(v[u].x >> 32) != epoch;
+                const bool ny = e + 1 < tp && e + 1 >= wl && (uint32_t)(v[u].y >> 32) != epoch;
+                if (nx || ny) {
+                    v[u] = ld_relaxed_u64x2(meta.agg + e);
+                    stale = true;
+                }
+            }
+            return stale;
+        };
         auto resolve = [&](uint32_t tp, int q) {
             const uint32_t wl = tp + 1 > G ? tp + 1 - G : 0u;
             uint32_t part = 0;
@@ -669,11 +682,12 @@ __global__ void __launch_bounds__(kE1Threads, 2)
                         v[u] = e < tp ? ld_relaxed_u64x2(meta.agg + e) : make_ulonglong2(0ull, 0ull);
                     }
                 }
+                while (refresh(tp, e0)) {}
 #pragma unroll
                 for (int u = 0; u < 8; ++u) {
                     const uint32_t e = e0 + 64 * u + 2 * lane;
-                    if (e < tp && e >= wl) part += entry(e, v[u].x);
-                    if (e + 1 < tp && e + 1 >= wl) part += entry(e + 1, v[u].y);
+                    if (e < tp && e >= wl) part += (uint32_t)v[u].x;
+                    if (e + 1 < tp && e + 1 >= wl) part += (uint32_t)v[u].y;
                 }
             }
             part = __reduce_add_sync(kFull, part);
@@ -695,8 +709,15 @@ __global__ void __launch_bounds__(kE1Threads, 2)
         uint32_t k = 0, tprev = 0;
         int q = 0, qp = 0;
         for (uint32_t t = blockIdx.x; t < ntiles; t += G, ++k, qp = q, q = q == 2 ? 0 : q + 1) {
+            // The window loads go out when the consumers start this round (they have stored tile
+            // k - 2 and freed its stage), about one L2 round trip before the sizes arrive.  Issued
+            // right after the previous resolve they sampled the other CTAs' aggregates ~2 us
+            // earlier, many not yet published, and the re-read after the sizes was a second
+            // round trip on the consumers' critical path (cfg3 387 -> 379 us; issuing early AND
+            // re-reading the missing entries at the round start: 401 us).
+            if (k >= 2) mbar_wait_parity_lazy(&sh.empty[(k - 2) % kE1Stages], ((k - 2) / kE1Stages) & 1u, 128);
             if (k) issue(tprev);
-            mbar_wait_parity_lazy(&sh.sizes[q], (k / 3) & 1u, 512);  // ~a round of consumer work
+            mbar_wait_parity_lazy(&sh.sizes[q], (k / 3) & 1u, 256);
             uint32_t a = lane < kCTWarps ? sh.wsum[q][lane] : 0u;
             a = __reduce_add_sync(kFull, a);
             if (lane == 0) {

@@ -32,9 +32,16 @@ __device__ __forceinline__ uint32_t shfl_l(uint32_t lo, uint32_t hi, uint32_t s)
 // byte_length - 1 of the four integers -> control byte (field i in bits 2i..2i+1);
 // tot = the group's data bytes
 __device__ __forceinline__ uint32_t group_ctrl(const uint4& x, uint32_t& tot) {
-    const uint32_t m0 = blen_m1(x.x), m1 = blen_m1(x.y), m2 = blen_m1(x.z), m3 = blen_m1(x.w);
-    tot = m0 + m1 + m2 + m3 + 4u;
-    return m0 + (m1 << 2) + (m2 << 4) + (m3 << 6);  // disjoint fields: + lets ptxas use either integer pipe
+    // top-bit indices (7..31) packed one per byte, then one shift + mask gives the four
+    // byte_length - 1 fields M (instead of a shift per integer); one multiply gathers them into
+    // the control byte: field i sits at bit 8 i of M and lands at bit 24 + 2 i of M * K,
+    // K = 2^24 + 2^18 + 2^12 + 2^6 (the other partial products fall below bit 24 or leave the
+    // word, and none overlap)
+    const uint32_t f0 = bfind_u32(x.x | 0x80u), f1 = bfind_u32(x.y | 0x80u), f2 = bfind_u32(x.z | 0x80u),
+                   f3 = bfind_u32(x.w | 0x80u);
+    const uint32_t M = ((f0 + (f1 << 8) + (f2 << 16) + (f3 << 24)) >> 3) & 0x03030303u;
+    tot = __dp4a(M, 0x01010101u, 4u);
+    return (M * 0x01041040u) >> 24;
 }
 
 // data bytes of a control byte: 4 + the sum of its fields (length[c])
@@ -45,14 +52,19 @@ __device__ __forceinline__ uint32_t ctrl_bytes(uint32_t c) {
 // The group's data as four little-endian words G0..G3 (bytes past its length are zero).
 // e8 = 8 * the group's data bytes.
 __device__ __forceinline__ uint4 group_bytes(const uint4& x, uint32_t c, uint32_t& e8) {
-    const uint32_t sA = ((c & 3u) << 3) + 8u;          // 8 l0, 8..32
-    const uint32_t sB = ((c >> 1) & 0x18u) + 8u;       // 8 l2
+    // byte_length - 1 of the four integers one per byte (the even and the odd fields spread by
+    // one multiply each: no partial products overlap inside a field's byte), then one multiply
+    // gives the running bit offsets: bytes of P8 = 8 l0, 8 (l0 + l1), 8 (l0 + l1 + l2), 8 total
+    const uint32_t Lm = ((c & 0x33u) * 0x1001u + (c & 0xCCu) * 0x40040u) & 0x03030303u;
+    const uint32_t P8 = Lm * 0x08080808u + 0x20181008u;
+    const uint32_t sA = P8 & 0xFFu;                              // 8 l0, 8..32
+    const uint32_t sB = __byte_perm(Lm, 0u, 0x4442u) * 8u + 8u;   // 8 l2
+    const uint32_t la8 = __byte_perm(P8, 0u, 0x4441u);           // 8 (l0 + l1), 16..64
+    e8 = P8 >> 24;
     const uint32_t A0 = x.x + __funnelshift_lc(0u, x.y, sA);  // x1 << 8 l0 (0 when l0 = 4)
     const uint32_t A1 = __funnelshift_lc(x.y, 0u, sA);        // x1 >> (32 - 8 l0)
     const uint32_t B0 = x.z + __funnelshift_lc(0u, x.w, sB);
     const uint32_t B1 = __funnelshift_lc(x.w, 0u, sB);
-    const uint32_t la8 = sA + ((c << 1) & 0x18u) + 8u;  // 8 (l0 + l1), 16..64
-    e8 = la8 + sB + ((c >> 3) & 0x18u) + 8u;
     // B << 8 (l0 + l1) over four words, la8 = 16..64: one 64-bit shift left for words 0-1 and
     // one right (by 64 - la8) for words 2-3.  PTX shifts clamp at 64, and each 64-bit shift is
     // two SHF (no word selects: the 32-bit form needed a compare, a subtract and five selects)
