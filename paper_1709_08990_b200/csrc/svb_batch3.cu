@@ -39,7 +39,10 @@ namespace {
 #ifndef BC_ENC3_MINB
 #define BC_ENC3_MINB 5  // encode CTAs per SM the register budget must allow (6: <= 80 registers spills, cfg4 1.96 vs 1.88 ms)
 #endif
-constexpr int kRWarps = 4;
+#ifndef BC_R_WARPS
+#define BC_R_WARPS 4
+#endif
+constexpr int kRWarps = BC_R_WARPS;
 constexpr int kRThreads = 32 * kRWarps;
 constexpr uint32_t kRingDefault = 8192;   // ring bytes per warp (launch-time; >= kItemMax)
 constexpr uint32_t kRingSlack = 192;      // over-reads past an item land here (control bytes of idle lanes: < 140 B)

@@ -1023,7 +1023,7 @@ uint64_t decode_meta_bytes(uint64_t n) {
     const uint64_t nchunks = (nsub + kChunkSubs - 1) / kChunkSubs;
     const uint64_t ntiles = (nsub + kCTWarps - 1) / kCTWarps;
     return 32 + align16(4 * (nsub + 64)) + align16(8 * (nchunks + 4)) + align16(4 * nsub) +
-           2 * align16(4 * (nchunks + 1)) + align16(4 * (ntiles + 8)) + align16(8 * (ntiles + 8)) + 64;
+           2 * align16(4 * (nchunks + 1)) + align16(4 * (ntiles + 8)) + align16(8 * ((nsub + 3) / 4 + 8)) + 64;
 }
 
 int occupancy_decode_pipe() { return 1; }  // the tile kernel is not persistent
@@ -1177,7 +1177,7 @@ cudaError_t launch_decode3(const uint8_t* in, uint64_t in_len, uint64_t n, int d
 unsigned long long* meta_agg_ptr(void* meta_ws, uint64_t n, uint64_t* count) {
     const uint64_t ngroups = (n + 3) >> 2;
     const uint64_t nsub = (ngroups + kWTGroups - 1) / kWTGroups;
-    *count = (nsub + kCTWarps - 1) / kCTWarps;
+    *count = (nsub + 3) / 4;  // tiles of >= 4 sub-tiles (the one-pass encode's tile is a build constant)
     return carve_decode_meta(meta_ws, n).agg;
 }
 

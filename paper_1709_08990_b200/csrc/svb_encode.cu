@@ -569,17 +569,26 @@ __global__ void __launch_bounds__(kCTThreads)
 // Round-r aggregates depend only on rounds < r, so once every CTA is resident there
 // is no cycle; a consumer only waits when the scanner's look-back is slower than its
 // own sizing + packing of the next tile.
-constexpr int kE1Stages = 3;
-constexpr uint32_t kE1Ints = kCTWarps * kWTInts;           // 8192 per tile
+#ifndef BC_E1_W
+#define BC_E1_W 8       // consumer warps = sub-tiles per tile
+#endif
+#ifndef BC_E1_STAGES
+#define BC_E1_STAGES 3  // stages per CTA: one loading, one being packed, kE1Defer waiting for their offset
+#endif
+constexpr int kE1W = BC_E1_W;
+constexpr int kE1Stages = BC_E1_STAGES;
+constexpr int kE1Defer = kE1Stages - 2;                     // a tile is stored this many rounds after it was packed
+constexpr uint32_t kE1Ints = kE1W * kWTInts;                // integers per tile
 constexpr uint32_t kE1Stride = 16 + kE1Ints * 4 + 16;       // prefix, tile, slack
-constexpr int kE1Threads = kCTThreads + 64;                 // consumers, producer, scanner
-constexpr int kE1Producer = kCTWarps, kE1Scanner = kCTWarps + 1;
+constexpr int kE1Threads = 32 * kE1W + 64;                  // consumers, producer, scanner
+constexpr int kE1Producer = kE1W, kE1Scanner = kE1W + 1;
+static_assert(kE1W >= 4 && kE1W <= 8 && kE1Defer >= 1, "tile geometry (the aggregate array holds nsub / 4 tiles)");
 
 struct __align__(16) E1Shared {
     uint64_t full[kE1Stages], empty[kE1Stages];
-    uint64_t sizes[3], carried[3];    // per tile slot (round % 3)
-    uint32_t wsum[3][kCTWarps];       // sub-tile data sizes of the slot's tile
-    unsigned long long carry[3];      // data offset of the slot's tile
+    uint64_t sizes[kE1Stages], carried[kE1Stages];  // per tile slot (round % kE1Stages, as the stage)
+    uint32_t wsum[kE1Stages][kE1W];                 // sub-tile data sizes of the slot's tile
+    unsigned long long carry[kE1Stages];            // data offset of the slot's tile
 };
 
 template <bool kDelta, bool kTrace>
@@ -592,17 +601,17 @@ __global__ void __launch_bounds__(kE1Threads, 2)
     const uint64_t ngroups = (n + 3) >> 2;
     const uint32_t tail_r = (uint32_t)(n & 3);
     const uint64_t nsub = (ngroups + kWTGroups - 1) / kWTGroups;
-    const uint32_t ntiles = (uint32_t)((nsub + kCTWarps - 1) / kCTWarps);
+    const uint32_t ntiles = (uint32_t)((nsub + kE1W - 1) / kE1W);
     const uint32_t G = gridDim.x;
     if (threadIdx.x == 0) {
 #pragma unroll
         for (int k = 0; k < kE1Stages; ++k) {
             mbar_init(&sh.full[k], 1);
-            mbar_init(&sh.empty[k], kCTWarps);
+            mbar_init(&sh.empty[k], kE1W);
         }
 #pragma unroll
-        for (int k = 0; k < 3; ++k) {
-            mbar_init(&sh.sizes[k], kCTWarps);
+        for (int k = 0; k < kE1Stages; ++k) {
+            mbar_init(&sh.sizes[k], kE1W);
             mbar_init(&sh.carried[k], 1);
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -708,17 +717,20 @@ __global__ void __launch_bounds__(kE1Threads, 2)
         // pack tile t (its window's aggregates are from rounds <= k - 1)
         uint32_t k = 0, tprev = 0;
         int q = 0, qp = 0;
-        for (uint32_t t = blockIdx.x; t < ntiles; t += G, ++k, qp = q, q = q == 2 ? 0 : q + 1) {
-            // The window loads go out when the consumers start this round (they have stored tile
-            // k - 2 and freed its stage), about one L2 round trip before the sizes arrive.  Issued
-            // right after the previous resolve they sampled the other CTAs' aggregates ~2 us
-            // earlier, many not yet published, and the re-read after the sizes was a second
-            // round trip on the consumers' critical path (cfg3 387 -> 379 us; issuing early AND
-            // re-reading the missing entries at the round start: 401 us).
-            if (k >= 2) mbar_wait_parity_lazy(&sh.empty[(k - 2) % kE1Stages], ((k - 2) / kE1Stages) & 1u, 128);
+        for (uint32_t t = blockIdx.x; t < ntiles; t += G, ++k, qp = q, q = q + 1 == kE1Stages ? 0 : q + 1) {
+            // The window loads go out when the consumers start this round (they have stored a
+            // tile and freed its stage), about one L2 round trip (~2 us under load) before the
+            // offset is needed.  Issued right after the previous resolve they sampled the other
+            // CTAs' aggregates too early, many not yet published, and the re-read after the sizes
+            // was a second round trip on the consumers' critical path (cfg3 387 -> 379 us).
+            // Sampling early as well was slower: with a blocking re-read at the round start 401 us,
+            // with a second register set used when complete 385 us (twice the polling loads, and
+            // CTAs whose offset comes early run ahead of the ones they later wait for).
+            if (k >= 1 + kE1Defer)
+                mbar_wait_parity_lazy(&sh.empty[(k - 1 - kE1Defer) % kE1Stages], ((k - 1 - kE1Defer) / kE1Stages) & 1u, 128);
             if (k) issue(tprev);
-            mbar_wait_parity_lazy(&sh.sizes[q], (k / 3) & 1u, 256);
-            uint32_t a = lane < kCTWarps ? sh.wsum[q][lane] : 0u;
+            mbar_wait_parity_lazy(&sh.sizes[q], (k / kE1Stages) & 1u, 256);
+            uint32_t a = lane < kE1W ? sh.wsum[q][lane] : 0u;
             a = __reduce_add_sync(kFull, a);
             if (lane == 0) {
                 st_relaxed_u64(meta.agg + t, ((unsigned long long)epoch << 32) | a);
@@ -737,13 +749,14 @@ __global__ void __launch_bounds__(kE1Threads, 2)
     // ---- consumers ----
     auto store_prev = [&](uint32_t tp, int st, int q, uint32_t kk) {
         if (kTrace && threadIdx.x == 0) meta.trace[8ull * tp + 6] = gtimer();
-        if (!mbar_test_parity(&sh.carried[q], (kk / 3) & 1u)) mbar_wait_parity_lazy(&sh.carried[q], (kk / 3) & 1u, 128);
+        if (!mbar_test_parity(&sh.carried[q], (kk / kE1Stages) & 1u))
+            mbar_wait_parity_lazy(&sh.carried[q], (kk / kE1Stages) & 1u, 128);
         if (kTrace && threadIdx.x == 0) meta.trace[8ull * tp + 7] = gtimer();
-        const uint64_t s = (uint64_t)tp * kCTWarps + warp;
+        const uint64_t s = (uint64_t)tp * kE1W + warp;
         if (s < nsub) {
             uint32_t pre = 0;
 #pragma unroll
-            for (int w = 0; w < kCTWarps; ++w) pre += w < warp ? sh.wsum[q][w] : 0u;
+            for (int w = 0; w < kE1W; ++w) pre += w < warp ? sh.wsum[q][w] : 0u;
             const uint32_t src = sh_addr(dsm) + (uint32_t)st * kE1Stride + 16 + (uint32_t)warp * (kWTInts * 4);
             store_realigned2(src, sh.wsum[q][warp], out + ngroups + sh.carry[q] + pre);
         }
@@ -754,15 +767,20 @@ __global__ void __launch_bounds__(kE1Threads, 2)
         }
     };
 
-    uint32_t k = 0, tprev = 0, ph = 0;
-    int st = 0, q = 0, stp = 0, qp = 0;  // stage / tile slot of this iteration and of the previous one
-    for (uint32_t t = blockIdx.x; t < ntiles;
-         t += G, ++k, stp = st, qp = q, st = st + 1 == kE1Stages ? 0 : st + 1, q = q == 2 ? 0 : q + 1, ph ^= st == 0) {
+    // stage = tile slot = k % kE1Stages; tile k is stored in round k + kE1Defer
+    uint32_t k = 0, ph = 0;
+    int st = 0;
+    auto store_kth = [&](uint32_t kk) {  // the CTA's kk-th tile
+        const int sk = (int)(kk % kE1Stages);
+        store_prev(blockIdx.x + kk * G, sk, sk, kk);
+    };
+    for (uint32_t t = blockIdx.x; t < ntiles; t += G, ++k, st = st + 1 == kE1Stages ? 0 : st + 1, ph ^= st == 0) {
+        const int q = st;
         if (kTrace && threadIdx.x == 0) meta.trace[8ull * t + 1] = gtimer();
         mbar_wait_parity(&sh.full[st], ph);
         if (kTrace && threadIdx.x == 0) meta.trace[8ull * t + 2] = gtimer();
         uint8_t* stage = dsm + (uint32_t)st * kE1Stride;
-        const uint64_t s = (uint64_t)t * kCTWarps + warp;
+        const uint64_t s = (uint64_t)t * kE1W + warp;
         const uint64_t g0 = s * kWTGroups;
         auto post = [&](uint32_t total) {  // the sub-tile's data size -> the scanner
             if (lane == 0) {
@@ -789,8 +807,7 @@ __global__ void __launch_bounds__(kE1Threads, 2)
                     // control bytes straight to the stream, the size posted, then the
                     // branch-free word pack at phase 0 in place (svb_pack.cuh)
                     uint32_t cw[2], qw[4];
-                    const uint32_t total = enc_lengths2<kDelta>(sin, prev_w, cdst, cw, qw);
-                    post(total);
+                    const uint32_t total = enc_lengths2<kDelta>(sin, prev_w, cdst, cw, qw, post);
                     __syncwarp();
                     enc_pack2<kDelta>(sin, prev_w, cw, qw, sin, total);
                 }
@@ -830,10 +847,9 @@ __global__ void __launch_bounds__(kE1Threads, 2)
             post(0u);
         }
         __syncwarp();
-        if (k) store_prev(tprev, stp, qp, k - 1);
-        tprev = t;
+        if (k >= (uint32_t)kE1Defer) store_kth(k - kE1Defer);
     }
-    if (k) store_prev(tprev, stp, qp, k - 1);
+    for (uint32_t kk = k > (uint32_t)kE1Defer ? k - kE1Defer : 0u; kk < k; ++kk) store_kth(kk);
 }
 
 // ---------------------------------------------------------------------------
@@ -1002,7 +1018,7 @@ __global__ void __launch_bounds__(kCTThreads + 32, 2)
                     // control bytes straight to the stream, then the branch-free word pack
                     // at phase 0 in place (svb_pack.cuh)
                     uint32_t cw[2], qw[4];
-                    total = enc_lengths2<kDelta>(sin, prev_w, cdst, cw, qw);
+                    total = enc_lengths2<kDelta>(sin, prev_w, cdst, cw, qw, [](uint32_t) {});
                     __syncwarp();
                     enc_pack2<kDelta>(sin, prev_w, cw, qw, sin, total);
                 }
@@ -1093,7 +1109,8 @@ static cudaError_t launch_encode1(const uint32_t* in, uint64_t n, int delta, uin
     if (!coop || occ < 1) return cudaSuccess;
     const uint64_t ngroups = (n + 3) >> 2;
     const uint64_t nsub = (ngroups + kWTGroups - 1) / kWTGroups;
-    const uint64_t ntiles = (nsub + kCTWarps - 1) / kCTWarps;
+    const uint64_t tw = sk ? (uint64_t)kE1W : (uint64_t)kCTWarps;  // sub-tiles per tile
+    const uint64_t ntiles = (nsub + tw - 1) / tw;
     uint64_t grid = (uint64_t)sms * (uint64_t)occ;
     if (grid > ntiles) grid = ntiles;
     DecodeMeta mm = m;

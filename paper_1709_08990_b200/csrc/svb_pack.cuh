@@ -228,12 +228,15 @@ __device__ __forceinline__ void put_packed(uint8_t* dst, uint32_t sdst, uint32_t
 // alignment, 32 consecutive bytes per row), the lane's control bytes kept in cw (row j in
 // byte j & 3 of cw[j >> 2]) and the rows' packed exclusive offsets in qw; returns the
 // sub-tile's data size.
-template <bool kDelta, bool kAny = false>
+// early(total) is called with the sub-tile's data size as soon as it is known (one warp
+// reduction), before the row scan: the one-pass encode posts it there, which takes the scan's
+// five dependent shuffle steps off the path every other CTA's look-back waits on.
+template <bool kDelta, bool kAny = false, class Early>
 __device__ __forceinline__ uint32_t enc_lengths2(uint32_t sin, uint32_t prev_w, uint8_t* __restrict__ cdst,
-                                                 uint32_t (&cw)[2], uint32_t (&qw)[4]) {
+                                                 uint32_t (&cw)[2], uint32_t (&qw)[4], Early early) {
     const int lane = threadIdx.x & 31;
     uint32_t P[3] = {0, 0, 0};
-    uint32_t last = prev_w;
+    uint32_t last = prev_w, lt = 0;
     cw[0] = cw[1] = 0;
 #pragma unroll
     for (int j = 0; j < kWTRows; ++j) {
@@ -242,8 +245,10 @@ __device__ __forceinline__ uint32_t enc_lengths2(uint32_t sin, uint32_t prev_w, 
         const uint32_t c = group_ctrl(x, tot);
         cw[j >> 2] += c << (8 * (j & 3));
         P[j / 3] += tot << (10 * (j % 3));
+        lt += tot;
         cdst[32 * j + lane] = (uint8_t)c;
     }
+    early(__reduce_add_sync(kFull, lt));
     return packed_row_scan(P, qw);
 }
 
