@@ -577,12 +577,20 @@ __global__ void __launch_bounds__(kCTThreads)
 #endif
 constexpr int kE1W = BC_E1_W;
 constexpr int kE1Stages = BC_E1_STAGES;
-constexpr int kE1Defer = kE1Stages - 2;                     // a tile is stored this many rounds after it was packed
-constexpr uint32_t kE1Ints = kE1W * kWTInts;                // integers per tile
-constexpr uint32_t kE1Stride = 16 + kE1Ints * 4 + 16;       // prefix, tile, slack
+#ifndef BC_E1_DEFER
+#define BC_E1_DEFER 1   // a tile is stored this many rounds after it was packed (stages - 1 - this = tiles loading)
+#endif
+constexpr int kE1Defer = BC_E1_DEFER;
+#ifndef BC_E1_ROWS
+#define BC_E1_ROWS 8    // rows of 128 integers per sub-tile (plain streams; delta streams keep 8)
+#endif
+constexpr int e1_rows(bool delta) { return delta ? kWTRows : BC_E1_ROWS; }
+constexpr uint32_t e1_ints(bool delta) { return (uint32_t)kE1W * 128u * e1_rows(delta); }  // integers per tile
+constexpr uint32_t e1_stride(bool delta) { return 16 + e1_ints(delta) * 4 + 16; }         // prefix, tile, slack
 constexpr int kE1Threads = 32 * kE1W + 64;                  // consumers, producer, scanner
 constexpr int kE1Producer = kE1W, kE1Scanner = kE1W + 1;
-static_assert(kE1W >= 4 && kE1W <= 8 && kE1Defer >= 1, "tile geometry (the aggregate array holds nsub / 4 tiles)");
+static_assert(kE1W * BC_E1_ROWS >= 32 && kE1W <= 8 && kE1Defer >= 1 && kE1Defer <= kE1Stages - 2 && BC_E1_ROWS <= kWTRows,
+              "tile geometry (the aggregate array holds a tile per 1024 groups)");
 
 struct __align__(16) E1Shared {
     uint64_t full[kE1Stages], empty[kE1Stages];
@@ -600,7 +608,10 @@ __global__ void __launch_bounds__(kE1Threads, 2)
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint64_t ngroups = (n + 3) >> 2;
     const uint32_t tail_r = (uint32_t)(n & 3);
-    const uint64_t nsub = (ngroups + kWTGroups - 1) / kWTGroups;
+    constexpr int kR = e1_rows(kDelta);                       // rows per sub-tile
+    constexpr uint32_t kSubInts = 128u * kR, kSubGroups = 32u * kR;
+    constexpr uint32_t kE1Ints = e1_ints(kDelta), kE1Stride = e1_stride(kDelta);
+    const uint64_t nsub = (ngroups + kSubGroups - 1) / kSubGroups;
     const uint32_t ntiles = (uint32_t)((nsub + kE1W - 1) / kE1W);
     const uint32_t G = gridDim.x;
     if (threadIdx.x == 0) {
@@ -725,7 +736,9 @@ __global__ void __launch_bounds__(kE1Threads, 2)
             // was a second round trip on the consumers' critical path (cfg3 387 -> 379 us).
             // Sampling early as well was slower: with a blocking re-read at the round start 401 us,
             // with a second register set used when complete 385 us (twice the polling loads, and
-            // CTAs whose offset comes early run ahead of the ones they later wait for).
+            // CTAs whose offset comes early run ahead of the ones they later wait for).  A fixed
+            // delay after the previous resolve instead of the round start: 0.4 / 0.7 / 1.0 / 1.3 /
+            // 1.7 us -> 379 / 377 / 365 / 369 / 389 us (the round start is ~1.1 us after it).
             if (k >= 1 + kE1Defer)
                 mbar_wait_parity_lazy(&sh.empty[(k - 1 - kE1Defer) % kE1Stages], ((k - 1 - kE1Defer) / kE1Stages) & 1u, 128);
             if (k) issue(tprev);
@@ -757,7 +770,7 @@ __global__ void __launch_bounds__(kE1Threads, 2)
             uint32_t pre = 0;
 #pragma unroll
             for (int w = 0; w < kE1W; ++w) pre += w < warp ? sh.wsum[q][w] : 0u;
-            const uint32_t src = sh_addr(dsm) + (uint32_t)st * kE1Stride + 16 + (uint32_t)warp * (kWTInts * 4);
+            const uint32_t src = sh_addr(dsm) + (uint32_t)st * kE1Stride + 16 + (uint32_t)warp * (kSubInts * 4);
             store_realigned2(src, sh.wsum[q][warp], out + ngroups + sh.carry[q] + pre);
         }
         __syncwarp();
@@ -781,7 +794,7 @@ __global__ void __launch_bounds__(kE1Threads, 2)
         if (kTrace && threadIdx.x == 0) meta.trace[8ull * t + 2] = gtimer();
         uint8_t* stage = dsm + (uint32_t)st * kE1Stride;
         const uint64_t s = (uint64_t)t * kE1W + warp;
-        const uint64_t g0 = s * kWTGroups;
+        const uint64_t g0 = s * kSubGroups;
         auto post = [&](uint32_t total) {  // the sub-tile's data size -> the scanner
             if (lane == 0) {
                 sh.wsum[q][warp] = total;
@@ -789,36 +802,41 @@ __global__ void __launch_bounds__(kE1Threads, 2)
             }
         };
         if (g0 < ngroups) {
-            const uint32_t sin = sh_addr(stage) + 16 + (uint32_t)warp * (kWTInts * 4);
+            const uint32_t sin = sh_addr(stage) + 16 + (uint32_t)warp * (kSubInts * 4);
             const uint32_t prev_w = warp ? lds32(sin - 4) : (t ? lds32(sh_addr(stage) + 12) : prev);
             uint8_t* cdst = out + g0;
-            if ((s + 1) * kWTInts <= n) {
+            if ((s + 1) * kSubInts <= n) {
                 // delta streams of sorted ids are mostly all-small: check that first
                 const bool small = kDelta && enc_full_small<kDelta>(sin, prev_w);
                 if (small) {
-                    post(kWTInts);
+                    post(kSubInts);
                     if ((((uintptr_t)cdst) & 15) == 0) {  // 256 zero control bytes
-                        if (lane < (int)(kWTGroups / 16)) reinterpret_cast<uint4*>(cdst)[lane] = make_uint4(0, 0, 0, 0);
+                        if (lane < (int)(kSubGroups / 16)) reinterpret_cast<uint4*>(cdst)[lane] = make_uint4(0, 0, 0, 0);
                     } else {
-                        for (uint32_t i = lane; i < kWTGroups; i += 32) cdst[i] = 0;
+                        for (uint32_t i = lane; i < kSubGroups; i += 32) cdst[i] = 0;
                     }
                     enc_full_small_pack0<kDelta>(sin, prev_w, sin);
                 } else {
                     // control bytes straight to the stream, the size posted, then the
                     // branch-free word pack at phase 0 in place (svb_pack.cuh)
                     uint32_t cw[2], qw[4];
-                    const uint32_t total = enc_lengths2<kDelta>(sin, prev_w, cdst, cw, qw, post);
+                    const uint32_t total = enc_lengths2<kDelta, false, kR>(sin, prev_w, cdst, cw, qw, post);
                     __syncwarp();
-                    enc_pack2<kDelta>(sin, prev_w, cw, qw, sin, total);
+                    enc_pack2<kDelta, false, kR>(sin, prev_w, cw, qw, sin, total);
                 }
             } else {
                 // the stream's last, partial sub-tile
                 EncodeTile tt;
                 uint32_t P[3] = {0, 0, 0};
                 uint32_t last_w = prev_w;
-                const uint8_t* sbytes = stage + 16 + warp * (kWTInts * 4);
+                const uint8_t* sbytes = stage + 16 + warp * (kSubInts * 4);
 #pragma unroll
                 for (int j = 0; j < kWTRows; ++j) {
+                    if (j >= kR) {  // the sub-tile has kR rows: none beyond
+                        tt.d[j] = make_uint4(0, 0, 0, 0);
+                        tt.lens[j] = 0;
+                        continue;
+                    }
                     const uint32_t cnt = group_count(g0 + 32 * j + lane, ngroups, tail_r);
                     uint4 x = mask_tail(*reinterpret_cast<const uint4*>(sbytes + 512 * j + 16 * lane), cnt);
                     if constexpr (kDelta) {
@@ -841,7 +859,7 @@ __global__ void __launch_bounds__(kE1Threads, 2)
                 tt.total = packed_row_scan(P, tt.qw);
                 post(tt.total);
                 __syncwarp();
-                encode_pack_at(tt, stage + 16 + warp * (kWTInts * 4), 0);
+                encode_pack_at(tt, stage + 16 + warp * (kSubInts * 4), 0);
             }
         } else {
             post(0u);
@@ -1083,7 +1101,8 @@ static cudaError_t launch_encode1(const uint32_t* in, uint64_t n, int delta, uin
     if (((uintptr_t)in) & 15) return cudaSuccess;
     // plain streams: the scanner kernel; delta streams: the barrier kernel (4b) unless asked
     const bool sk = !delta || scanner;
-    const uint32_t smem = sk ? (uint32_t)(kE1Stages * kE1Stride) : (uint32_t)(kD1eStages * kD1eStride);
+    const uint32_t smem = sk ? (uint32_t)kE1Stages * (delta ? e1_stride(true) : e1_stride(false))
+                             : (uint32_t)(kD1eStages * kD1eStride);
     const int threads = sk ? kE1Threads : kCTThreads + 32;
     const void* fns[4];
     if (sk) {
@@ -1109,8 +1128,10 @@ static cudaError_t launch_encode1(const uint32_t* in, uint64_t n, int delta, uin
     if (!coop || occ < 1) return cudaSuccess;
     const uint64_t ngroups = (n + 3) >> 2;
     const uint64_t nsub = (ngroups + kWTGroups - 1) / kWTGroups;
-    const uint64_t tw = sk ? (uint64_t)kE1W : (uint64_t)kCTWarps;  // sub-tiles per tile
-    const uint64_t ntiles = (nsub + tw - 1) / tw;
+    // groups per tile (the scanner kernel's tile geometry is a build constant)
+    const uint64_t tg = sk ? (uint64_t)kE1W * 32u * (uint64_t)(delta ? e1_rows(true) : e1_rows(false))
+                           : (uint64_t)kCTWarps * kWTGroups;
+    const uint64_t ntiles = (ngroups + tg - 1) / tg;
     uint64_t grid = (uint64_t)sms * (uint64_t)occ;
     if (grid > ntiles) grid = ntiles;
     DecodeMeta mm = m;

@@ -231,7 +231,7 @@ __device__ __forceinline__ void put_packed(uint8_t* dst, uint32_t sdst, uint32_t
 // early(total) is called with the sub-tile's data size as soon as it is known (one warp
 // reduction), before the row scan: the one-pass encode posts it there, which takes the scan's
 // five dependent shuffle steps off the path every other CTA's look-back waits on.
-template <bool kDelta, bool kAny = false, class Early>
+template <bool kDelta, bool kAny = false, int kRows = kWTRows, class Early>
 __device__ __forceinline__ uint32_t enc_lengths2(uint32_t sin, uint32_t prev_w, uint8_t* __restrict__ cdst,
                                                  uint32_t (&cw)[2], uint32_t (&qw)[4], Early early) {
     const int lane = threadIdx.x & 31;
@@ -239,7 +239,7 @@ __device__ __forceinline__ uint32_t enc_lengths2(uint32_t sin, uint32_t prev_w, 
     uint32_t last = prev_w, lt = 0;
     cw[0] = cw[1] = 0;
 #pragma unroll
-    for (int j = 0; j < kWTRows; ++j) {
+    for (int j = 0; j < kRows; ++j) {
         const uint4 x = enc_row<kDelta, kAny>(sin, j, last);
         uint32_t tot;
         const uint32_t c = group_ctrl(x, tot);
@@ -249,19 +249,19 @@ __device__ __forceinline__ uint32_t enc_lengths2(uint32_t sin, uint32_t prev_w, 
         cdst[32 * j + lane] = (uint8_t)c;
     }
     early(__reduce_add_sync(kFull, lt));
-    return packed_row_scan(P, qw);
+    return packed_row_scan<kRows>(P, qw);
 }
 
 // Pass 2: pack every row in place at shared byte sdst (sdst <= sin, 4-B aligned so that a
 // row's completed words end before the next row's integers), then the final pending word.
-template <bool kDelta, bool kAny = false>
+template <bool kDelta, bool kAny = false, int kRows = kWTRows>
 __device__ __forceinline__ void enc_pack2(uint32_t sin, uint32_t prev_w, const uint32_t (&cw)[2],
                                           const uint32_t (&qw)[4], uint32_t sdst, uint32_t total) {
     uint32_t last = prev_w, carry = 0;
     // rows in pairs: both rows are read before either is written (row j + 1's output ends
     // before row j + 2's integers), so the two packs' dependency chains interleave
 #pragma unroll
-    for (int j = 0; j < kWTRows; j += 2) {
+    for (int j = 0; j + 1 < kRows; j += 2) {
         const uint4 x0 = enc_row<kDelta, kAny>(sin, j, last);
         const uint4 x1 = enc_row<kDelta, kAny>(sin, j + 1, last);
         const uint32_t c0 = (cw[j >> 2] >> (8 * (j & 3))) & 0xFFu, c1 = (cw[j >> 2] >> (8 * (j & 3) + 8)) & 0xFFu;
@@ -269,6 +269,14 @@ __device__ __forceinline__ void enc_pack2(uint32_t sin, uint32_t prev_w, const u
         __syncwarp();  // every lane has read both rows before any lane writes over them
         pack_group_row(x0, c0, a0, carry);
         pack_group_row(x1, c1, a1, carry);
+    }
+    if constexpr (kRows & 1) {  // an odd last row
+        constexpr int j = kRows - 1;
+        const uint4 x0 = enc_row<kDelta, kAny>(sin, j, last);
+        const uint32_t c0 = (cw[j >> 2] >> (8 * (j & 3))) & 0xFFu;
+        const uint32_t a0 = sdst + (qw[j >> 1] & 0xFFFFu);
+        __syncwarp();
+        pack_group_row(x0, c0, a0, carry);
     }
     if (((sdst + total) & 3u) && (threadIdx.x & 31) == 0) sts32((sdst + total) & ~3u, carry);
 }

@@ -52,6 +52,7 @@ __device__ __forceinline__ uint32_t fsum(uint32_t c) { return __popc(c & 0x55u) 
 
 // Packed exclusive scan of 8 per-lane row values (each <= 16, row totals <= 512):
 // three 3x10-bit warp scans.  q[j] = exclusive offset of (row j, lane) in row-major order.
+template <int kRows = kWTRows>
 __device__ __forceinline__ uint32_t packed_row_scan(const uint32_t (&P)[3], uint32_t (&qw)[4]) {
     uint32_t base = 0;
     qw[0] = qw[1] = qw[2] = qw[3] = 0;
@@ -63,7 +64,7 @@ __device__ __forceinline__ uint32_t packed_row_scan(const uint32_t (&P)[3], uint
 #pragma unroll
         for (int f = 0; f < 3; ++f) {
             const int j = 3 * k + f;
-            if (j < kWTRows) {
+            if (j < kRows) {
                 qw[j >> 1] |= (base + ((E >> (10 * f)) & 0x3FFu)) << (16 * (j & 1));
                 base += (T >> (10 * f)) & 0x3FFu;
             }
