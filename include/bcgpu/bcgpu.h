@@ -136,8 +136,8 @@ int bcgpu_svb_decode_blocks_device(bcgpu_ctx *ctx, const uint8_t *d_in, size_t i
  * max_seg_n bounds every segment's n (0 = unknown).  Decode: segments with
  * n <= 1920 are decoded segment-resident, longer ones by the tile pipeline,
  * which is not launched when 0 < max_seg_n <= 1920 (a longer segment then
- * fails with BCGPU_ERR_INVALID_ARGUMENT).  Encode codes every length; a bound
- * <= 1920 only sizes its shared-memory rings for one more CTA per SM. */
+ * fails with BCGPU_ERR_INVALID_ARGUMENT).  Encode codes every length and does
+ * not use the bound. */
 int bcgpu_svb_decode_batch_device(bcgpu_ctx *ctx, const bcgpu_decode_segment *d_segs, size_t nseg,
                                   const uint8_t *d_in, uint32_t *d_out, int delta, uint32_t max_seg_n,
                                   void *stream);

@@ -840,11 +840,11 @@ __global__ void __launch_bounds__(kRThreads, BC_ENC3_MINB)
 cudaError_t launch_encode_batch3(const bcgpu_encode_segment* segs, uint64_t nseg, const uint32_t* in, uint8_t* out,
                                  uint64_t* out_lens, int delta, const BatchArgs& ba, cudaStream_t stream, bool sizes) {
     const uint32_t ring_kb = (ba.flags >> 24) & 0xFFu;  // debug: ring KiB per warp
-    // rings: 9 KiB by default (5 CTAs per SM; a long segment's 7.5 KiB pieces still overlap with
-    // short items); when the caller bounds every segment to one piece, rings of exactly one
-    // largest item let a sixth CTA fit (cfg4: 2.01 -> 1.98 ms; cfg5's pieces lose the overlap)
-    const uint32_t ring = ring_kb ? (ring_kb << 10 < kEItemMax ? kEItemMax : ring_kb << 10)
-                                  : (ba.max_seg_n != 0 && ba.max_seg_n <= kBatchSmallN ? kEItemMax : kERingDefault);
+    // rings: 9 KiB (5 CTAs per SM at 94 registers; a long segment's 7.5 KiB pieces still overlap
+    // with short items).  Rings of exactly one largest item let a sixth CTA fit while the kernel
+    // took 80 registers; the 64-bit-shift pack needs 94 (80 spills: cfg4 1.96 vs 1.86 ms), and at
+    // five CTAs the larger ring is the faster one (cfg4 1.848 vs 1.862 ms)
+    const uint32_t ring = ring_kb ? (ring_kb << 10 < kEItemMax ? kEItemMax : ring_kb << 10) : kERingDefault;
     const size_t smem = kRWarps * (sizeof(EWarpHdr) + ring + kRingSlack);
     const void* fns[4] = {(const void*)svb_encode_batch3_kernel<true, false>,
                           (const void*)svb_encode_batch3_kernel<false, false>,
