@@ -149,6 +149,7 @@ static int make_batch(bcgpu_ctx* c, cudaStream_t s, BatchArgs* ba) {
     ba->status = status_ptr(c);
     ba->epoch = c->epoch;
     ba->flags = c->debug_flags;
+    ba->tickets = c->ws + 2;  // two spare words of the workspace head (zeroed with it; the kernels reset them)
     return BCGPU_OK;
 }
 

@@ -311,7 +311,8 @@ template <bool kDelta>
 __global__ void __launch_bounds__(kRThreads, BC_DEC3_MINB)
     svb_decode_batch3_kernel(const bcgpu_decode_segment* __restrict__ segs, uint64_t nseg,
                              const uint8_t* __restrict__ in, uint32_t* __restrict__ out, unsigned long long* status,
-                             uint32_t epoch, uint32_t long_hint, uint32_t ring_bytes) {
+                             uint32_t epoch, uint32_t long_hint, uint32_t ring_bytes, unsigned long long* tickets,
+                             uint32_t chunk) {
     extern __shared__ __align__(128) uint8_t rdsm[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     RWarpHdr& B = reinterpret_cast<RWarpHdr*>(rdsm)[warp];
@@ -319,13 +320,35 @@ __global__ void __launch_bounds__(kRThreads, BC_DEC3_MINB)
     if (lane == 0)
         for (uint32_t q = 0; q < kRSlots; ++q) mbar_init1(&B.bar[q]);
     __syncwarp();
-    // nseg < 2^32 (the launcher splits larger batches)
-    const uint32_t gw = blockIdx.x * kRWarps + warp, GW = gridDim.x * kRWarps;
-    const uint32_t cnt = nseg > gw ? (uint32_t)((nseg - gw + GW - 1) / GW) : 0u;  // segments gw, gw + GW, ...
+    // nseg < 2^31 (the launcher splits larger batches).  Warps draw chunks of `chunk` (<= 32)
+    // consecutive segments from a global ticket: list lengths vary, and with a fixed stride the
+    // warp with the most integers finished ~14% after the average one (cfg4), the SMs draining
+    // unevenly; a chunk's descriptors are also one coalesced read.  The next chunk is drawn a
+    // whole chunk ahead, so the atomic's round trip is never waited for.
+    const uint32_t GW = gridDim.x * kRWarps;
+    const uint32_t nsg = (uint32_t)nseg;
     const uint32_t ring = sh_addr(ring_p), bar0 = sh_addr(&B.bar[0]), carry_s = sh_addr(&B.carry);
     const uint64_t pol = l2_policy_drop();
-    auto seg_ptr = [&](uint32_t k) {  // the warp's k-th segment
-        return reinterpret_cast<const ulonglong2*>(segs + gw + (uint64_t)k * GW);
+    // chunk = 0: few segments per warp (large ones, as a rule): the fixed stride gw, gw + GW, ...
+    // instead, 32 of them checked per refill (a chunk of one or two segments per draw exposed
+    // the descriptor read's latency at every draw: cfg5 +1.5%)
+    const bool stat = chunk == 0;
+    const uint32_t gw = blockIdx.x * kRWarps + warp;
+    const uint32_t cnt = nsg > gw ? (nsg - gw + GW - 1) / GW : 0u;  // fixed stride: this warp's segments
+    uint32_t tnext = 0;  // lane 0: the chunk after the current one
+    auto draw = [&]() {  // -> the current chunk's first segment; draws the one after it
+        const uint32_t cur = __shfl_sync(kFull, tnext, 0);
+        if (lane == 0) tnext = stat ? tnext + 32u : (uint32_t)atomicAdd(tickets, (unsigned long long)chunk);
+        return cur;
+    };
+    auto left = [&](uint32_t c) {  // segments of the chunk that starts at c
+        return stat ? (c < cnt ? min(32u, cnt - c) : 0u) : (c < nsg ? min(chunk, nsg - c) : 0u);
+    };
+    if (lane == 0) tnext = stat ? 0u : (uint32_t)atomicAdd(tickets, (unsigned long long)chunk);
+    uint32_t cb = draw();      // the current chunk: its first segment (fixed stride: its first index k)
+    uint32_t ncur = left(cb);  // its segments
+    auto seg_ptr = [&](uint32_t k) {  // the chunk's k-th segment
+        return reinterpret_cast<const ulonglong2*>(segs + (stat ? gw + (uint64_t)(cb + k) * GW : (uint64_t)cb + k));
     };
 
     // Lane l checks the descriptor of the warp's segment dbase + l once: info = its ring cover
@@ -333,11 +356,11 @@ __global__ void __launch_bounds__(kRThreads, BC_DEC3_MINB)
     // descriptors go to a per-warp table in shared memory (lane 0 reads one when it issues it),
     // so they hold no registers through the decode (re-reading them from global memory stalled
     // lane 0 on L2 misses: the warp's descriptors are a grid-stride apart).
-    uint32_t dbase = 0, info = 0;
+    uint32_t info = 0;
     auto check = [&]() {
-        const uint32_t k = dbase + lane;
+        const uint32_t k = lane;
         info = 0x80000000u;
-        if (k < cnt) {
+        if (k < ncur) {
             const ulonglong2 sb = __ldg(seg_ptr(k));  // src_offset, src_bytes
             const ulonglong2 dn = __ldg(seg_ptr(k) + 1);  // dst_offset, n | prev << 32
             B.desc[lane][0] = sb;
@@ -368,7 +391,7 @@ __global__ void __launch_bounds__(kRThreads, BC_DEC3_MINB)
     for (;;) {
         // issue every segment that fits (a full ring leaves descriptor di pending: its check is
         // per lane above, so a retry costs one shuffle)
-        while (qh - qt < kRSlots && dbase + di < cnt) {
+        while (qh - qt < kRSlots && di < ncur) {
             const uint32_t inf = __shfl_sync(kFull, info, di);
             if (!(inf & 0x80000000u)) {
                 const uint32_t cover = inf;
@@ -399,8 +422,9 @@ __global__ void __launch_bounds__(kRThreads, BC_DEC3_MINB)
             } else if (lane == 0 && (inf >> 16) != 0x8000u) {  // not decoded here: report its status
                 report3(status, epoch, (inf >> 16) & 0x7FFFu);
             }
-            if (++di == 32) {
-                dbase += 32;
+            if (++di == ncur) {  // the chunk is issued: on to the next one
+                cb = draw();
+                ncur = left(cb);
                 di = 0;
                 __syncwarp();  // lane 0 has read the table
                 check();
@@ -422,6 +446,11 @@ __global__ void __launch_bounds__(kRThreads, BC_DEC3_MINB)
         tail = it.end;
         ++qt;
         __syncwarp();
+    }
+    // the last warp of the grid to finish leaves the ticket words zero for the next launch
+    if (lane == 0 && atomicAdd(tickets + 1, 1ull) == (unsigned long long)GW - 1) {
+        tickets[0] = 0;
+        tickets[1] = 0;
     }
 }
 
@@ -452,7 +481,12 @@ cudaError_t launch_decode_batch3(const bcgpu_decode_segment* segs, uint64_t nseg
     constexpr uint64_t kMaxSeg = 1ull << 31;  // the kernel counts segments in 32 bits
     for (uint64_t s0 = 0; s0 < nseg; s0 += kMaxSeg) {
         const uint64_t ns = nseg - s0 < kMaxSeg ? nseg - s0 : kMaxSeg;
-        (delta ? kd : kp)<<<grid, kRThreads, smem, stream>>>(segs + s0, ns, in, out, ba.status, ba.epoch, hint, ring);
+        // chunks of up to 32 segments (a quarter of a warp's share at most); 0 = the fixed stride,
+        // when a warp's share is under 32 segments
+        const uint64_t per = ns / (4ull * (uint64_t)grid * kRWarps);
+        const uint32_t chunk = per >= 32 ? 32u : (per < 8 ? 0u : (uint32_t)per);
+        (delta ? kd : kp)<<<grid, kRThreads, smem, stream>>>(segs + s0, ns, in, out, ba.status, ba.epoch, hint, ring,
+                                                             ba.tickets, chunk);
     }
     return cudaGetLastError();
 }
@@ -685,7 +719,7 @@ __global__ void __launch_bounds__(kRThreads, BC_ENC3_MINB)
     svb_encode_batch3_kernel(const bcgpu_encode_segment* __restrict__ segs, uint64_t nseg,
                              const uint32_t* __restrict__ in, uint8_t* __restrict__ out,
                              uint64_t* __restrict__ out_lens, unsigned long long* status, uint32_t epoch,
-                             uint32_t ring_bytes) {
+                             uint32_t ring_bytes, unsigned long long* tickets, uint32_t chunk) {
     extern __shared__ __align__(128) uint8_t edsm[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     EWarpHdr& B = reinterpret_cast<EWarpHdr*>(edsm)[warp];
@@ -693,22 +727,39 @@ __global__ void __launch_bounds__(kRThreads, BC_ENC3_MINB)
     if (lane == 0)
         for (uint32_t q = 0; q < kRSlots; ++q) mbar_init1(&B.bar[q]);
     __syncwarp();
-    // nseg < 2^32 (the launcher splits larger batches)
-    const uint32_t gw = blockIdx.x * kRWarps + warp, GW = gridDim.x * kRWarps;
-    const uint32_t cnt = nseg > gw ? (uint32_t)((nseg - gw + GW - 1) / GW) : 0u;
+    // nseg < 2^31 (the launcher splits larger batches); warps draw chunks of `chunk` consecutive
+    // segments from the global ticket, one chunk ahead (see svb_decode_batch3_kernel)
+    const uint32_t GW = gridDim.x * kRWarps;
+    const uint32_t nsg = (uint32_t)nseg;
     const uint32_t ring = sh_addr(ring_p), bar0 = sh_addr(&B.bar[0]), ctrl0 = sh_addr(&B.ctrl[0][0]);
     const uint64_t pol = l2_policy_drop();
-    auto seg_ptr = [&](uint32_t k) {  // the warp's k-th segment
-        return reinterpret_cast<const ulonglong2*>(segs + gw + (uint64_t)k * GW);
+    const bool stat = chunk == 0;  // fixed stride gw, gw + GW, ... (few segments per warp)
+    const uint32_t gw = blockIdx.x * kRWarps + warp;
+    const uint32_t cnt = nsg > gw ? (nsg - gw + GW - 1) / GW : 0u;
+    uint32_t tnext = 0;
+    auto draw = [&]() {
+        const uint32_t cur = __shfl_sync(kFull, tnext, 0);
+        if (lane == 0) tnext = stat ? tnext + 32u : (uint32_t)atomicAdd(tickets, (unsigned long long)chunk);
+        return cur;
     };
+    auto left = [&](uint32_t c) {
+        return stat ? (c < cnt ? min(32u, cnt - c) : 0u) : (c < nsg ? min(chunk, nsg - c) : 0u);
+    };
+    if (lane == 0) tnext = stat ? 0u : (uint32_t)atomicAdd(tickets, (unsigned long long)chunk);
+    uint32_t cb = draw();
+    uint32_t ncur = left(cb);
+    auto seg_index = [&](uint32_t k) -> uint64_t {  // the chunk's k-th segment
+        return stat ? gw + (uint64_t)(cb + k) * GW : (uint64_t)cb + k;
+    };
+    auto seg_ptr = [&](uint32_t k) { return reinterpret_cast<const ulonglong2*>(segs + seg_index(k)); };
     // Lane l checks the descriptor of the warp's segment dbase + l once: its n, and the 16-B
     // phase of its integers | 0x100 when it is empty | 0x200 when its capacity is short; it
     // keeps src, dst and prev for the shuffles that issue its pieces.
-    uint32_t dbase = 0, info_n = 0, info_f = 0, info_p = 0;
+    uint32_t info_n = 0, info_f = 0, info_p = 0;
     unsigned long long info_s = 0, info_d = 0;
     auto check = [&]() {
-        const uint32_t k = dbase + lane;
-        if (k < cnt) {
+        const uint32_t k = lane;
+        if (k < ncur) {
             const ulonglong2 sc = __ldg(seg_ptr(k));  // src_offset, dst_capacity
             const ulonglong2 dn = __ldg(seg_ptr(k) + 1);  // dst_offset, n | prev << 32
             const uint32_t n = (uint32_t)dn.y;
@@ -729,9 +780,9 @@ __global__ void __launch_bounds__(kRThreads, BC_ENC3_MINB)
     uint32_t run = 0;        // delta base of the next piece of the segment being encoded
     unsigned long long off = 0;  // data bytes of the segment's earlier pieces
     for (;;) {
-        while (qh - qt < kRSlots && dbase + di < cnt) {
+        while (qh - qt < kRSlots && di < ncur) {
             const uint32_t n = __shfl_sync(kFull, info_n, di), f = __shfl_sync(kFull, info_f, di);
-            const uint64_t s_idx = gw + (uint64_t)(dbase + di) * GW;
+            const uint64_t s_idx = seg_index(di);
             bool done = true;
             if (f & 0x300u) {  // empty, or capacity short: nothing written; a zero length keeps
                 if (lane == 0) {  // callers that pack by out_lens in bounds
@@ -781,8 +832,9 @@ __global__ void __launch_bounds__(kRThreads, BC_ENC3_MINB)
             }
             if (done) {
                 piece = 0;
-                if (++di == 32) {
-                    dbase += 32;
+                if (++di == ncur) {  // the chunk is issued: on to the next one
+                    cb = draw();
+                    ncur = left(cb);
                     di = 0;
                     check();
                 }
@@ -834,7 +886,14 @@ __global__ void __launch_bounds__(kRThreads, BC_ENC3_MINB)
         tail_next = it.end;
         ++qt;
     }
-    if (lane == 0) tma_store_wait_read();
+    if (lane == 0) {
+        tma_store_wait_read();
+        // the last warp of the grid to finish leaves the ticket words zero for the next launch
+        if (atomicAdd(tickets + 1, 1ull) == (unsigned long long)GW - 1) {
+            tickets[0] = 0;
+            tickets[1] = 0;
+        }
+    }
 }
 
 cudaError_t launch_encode_batch3(const bcgpu_encode_segment* segs, uint64_t nseg, const uint32_t* in, uint8_t* out,
@@ -868,7 +927,10 @@ cudaError_t launch_encode_batch3(const bcgpu_encode_segment* segs, uint64_t nseg
     constexpr uint64_t kMaxSeg = 1ull << 31;  // the kernel counts segments in 32 bits
     for (uint64_t s0 = 0; s0 < nseg; s0 += kMaxSeg) {
         const uint64_t ns = nseg - s0 < kMaxSeg ? nseg - s0 : kMaxSeg;
-        kern<<<grid, kRThreads, smem, stream>>>(segs + s0, ns, in, out, out_lens + s0, ba.status, ba.epoch, ring);
+        const uint64_t per = ns / (4ull * (uint64_t)grid * kRWarps);
+        const uint32_t chunk = per >= 32 ? 32u : (per < 8 ? 0u : (uint32_t)per);
+        kern<<<grid, kRThreads, smem, stream>>>(segs + s0, ns, in, out, out_lens + s0, ba.status, ba.epoch, ring,
+                                                ba.tickets, chunk);
     }
     return cudaGetLastError();
 }

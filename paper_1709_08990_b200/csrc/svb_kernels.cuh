@@ -93,6 +93,7 @@ struct BatchArgs {
     uint32_t epoch;
     uint32_t flags = 0;          // debug flags of the ctx (bits 12..14: batch-decode CTAs per SM)
     uint32_t max_seg_n = 0;      // caller's bound on every segment's n (0 = unknown)
+    unsigned long long* tickets = nullptr;  // [2] zero between launches: next segment chunk, warps done
 };
 
 // Segments with n <= kBatchSmallN decode segment-resident (svb_batch3.cu): their worst-case
