@@ -47,6 +47,7 @@ constexpr int kRThreads = 32 * kRWarps;
 constexpr uint32_t kRingDefault = 8192;   // ring bytes per warp (launch-time; >= kItemMax)
 constexpr uint32_t kRingSlack = 192;      // over-reads past an item land here (control bytes of idle lanes: < 140 B)
 constexpr uint32_t kRSlots = 8;           // items in flight per warp
+constexpr uint32_t kChunkMax = 8;         // segments a warp draws at a time (<= 32: one descriptor per lane); cfg4: 4 / 8 / 16 / 24 / 32 -> encode 1.70 / 1.69 / 1.70 / 1.72 / 1.74 ms, decode 1.58 / 1.56 / 1.57 / 1.58 / 1.59 ms
 constexpr uint32_t kItemMax = 8192;       // largest 16-B cover of an item
 static_assert(kBatchSmallN / 4 + 1 + 4ull * kBatchSmallN + 30 <= kItemMax, "short-segment stream must fit an item");
 
@@ -481,10 +482,10 @@ cudaError_t launch_decode_batch3(const bcgpu_decode_segment* segs, uint64_t nseg
     constexpr uint64_t kMaxSeg = 1ull << 31;  // the kernel counts segments in 32 bits
     for (uint64_t s0 = 0; s0 < nseg; s0 += kMaxSeg) {
         const uint64_t ns = nseg - s0 < kMaxSeg ? nseg - s0 : kMaxSeg;
-        // chunks of up to 32 segments (a quarter of a warp's share at most); 0 = the fixed stride,
-        // when a warp's share is under 32 segments
+        // chunks of kChunkMax segments when a warp's share is at least four of them; else 0 = the
+        // fixed stride
         const uint64_t per = ns / (4ull * (uint64_t)grid * kRWarps);
-        const uint32_t chunk = per >= 32 ? 32u : (per < 8 ? 0u : (uint32_t)per);
+        const uint32_t chunk = per >= kChunkMax ? kChunkMax : 0u;
         (delta ? kd : kp)<<<grid, kRThreads, smem, stream>>>(segs + s0, ns, in, out, ba.status, ba.epoch, hint, ring,
                                                              ba.tickets, chunk);
     }
@@ -928,7 +929,7 @@ cudaError_t launch_encode_batch3(const bcgpu_encode_segment* segs, uint64_t nseg
     for (uint64_t s0 = 0; s0 < nseg; s0 += kMaxSeg) {
         const uint64_t ns = nseg - s0 < kMaxSeg ? nseg - s0 : kMaxSeg;
         const uint64_t per = ns / (4ull * (uint64_t)grid * kRWarps);
-        const uint32_t chunk = per >= 32 ? 32u : (per < 8 ? 0u : (uint32_t)per);
+        const uint32_t chunk = per >= kChunkMax ? kChunkMax : 0u;
         kern<<<grid, kRThreads, smem, stream>>>(segs + s0, ns, in, out, out_lens + s0, ba.status, ba.epoch, ring,
                                                 ba.tickets, chunk);
     }
