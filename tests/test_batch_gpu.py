@@ -279,3 +279,48 @@ def test_encode_one_byte_blocks(dev, delta):
     sizes = [384, 768, 1152, 1536, 1920, 383, 385, 1024, 3 * 1024, 5000, 65536, 130_000, 7] * 4
     rng.shuffle(sizes)
     _check_encode(dev, *_run_encode(dev, sizes, delta, rng, small=0.8))
+
+
+@pytest.mark.parametrize("delta", [True, False])
+def test_many_segments_dynamic_chunks(dev, delta):
+    """Batches with at least 32 segments per resident warp take the ticket path: warps draw
+    chunks of 8 consecutive segments instead of a fixed stride (svb_batch3.cu).  160K segments
+    of 0..300 integers (some empty, one long), every byte and every integer against the oracle,
+    run twice on one context: the ticket words must be zero again after a launch."""
+    import torch
+    from paper_1709_08990_b200.device import DECODE_SEG_DTYPE, ENCODE_SEG_DTYPE, segments_to_tensor
+    rng = np.random.default_rng(77 + delta)
+    nseg = 160_000
+    lens = rng.integers(0, 301, nseg).astype(np.uint32)
+    lens[12345] = 5000  # one segment in pieces (encode) / on the tile pipeline (decode)
+    offs = np.zeros(nseg + 1, np.uint64)
+    np.cumsum(lens, out=offs[1:])
+    n = int(offs[-1])
+    vals = _values(rng, n, delta)
+    prevs = rng.integers(0, 2**32, nseg, dtype=np.uint64).astype(np.uint32)
+    caps = (lens.astype(np.uint64) + 3) // 4 + 4 * lens.astype(np.uint64)
+    eoff = np.zeros(nseg + 1, np.uint64)
+    np.cumsum(caps + rng.integers(0, 5, nseg).astype(np.uint64), out=eoff[1:])
+    es = np.zeros(nseg, ENCODE_SEG_DTYPE)
+    es["src_offset"], es["dst_capacity"], es["dst_offset"], es["n"], es["prev"] = offs[:-1], caps, eoff[:-1], lens, prevs
+    want = np.full(int(eoff[-1]) + 16, 0xA5, np.uint8)
+    want_lens = np.zeros(nseg, np.uint64)
+    oracle.encode_batch(es, vals, want, want_lens, delta)
+    d_es = segments_to_tensor(es, "cuda")
+    d_v = torch.from_numpy(vals.view(np.int32)).cuda()
+    for _ in range(2):
+        d_c = torch.full((int(eoff[-1]) + 16,), 0xA5, dtype=torch.uint8, device="cuda")
+        d_lens = torch.zeros(nseg, dtype=torch.int64, device="cuda")
+        dev.encode_batch(d_es, nseg, d_v, d_c, d_lens, delta=delta)
+        dev.check()
+        assert np.array_equal(d_lens.cpu().numpy().astype(np.uint64), want_lens)
+        assert np.array_equal(d_c.cpu().numpy(), want)
+        ds = np.zeros(nseg, DECODE_SEG_DTYPE)
+        ds["src_offset"], ds["src_bytes"], ds["dst_offset"], ds["n"], ds["prev"] = eoff[:-1], want_lens, offs[:-1], lens, prevs
+        d_ds = segments_to_tensor(ds, "cuda")
+        d_o = torch.full((n + 4,), -1, dtype=torch.int32, device="cuda")
+        dev.decode_batch(d_ds, nseg, d_c, d_o, delta=delta)
+        dev.check()
+        got = d_o.cpu().numpy().view(np.uint32)
+        assert np.array_equal(got[:n], vals)
+        assert (got[n:] == 0xFFFFFFFF).all()
