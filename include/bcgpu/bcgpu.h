@@ -83,7 +83,9 @@ typedef struct bcgpu_encode_segment {
 
 /* ---- library / context ------------------------------------------------ */
 int bcgpu_abi_version(void);
-/* Device index a ctx is bound to; the ctx allocates its workspace lazily. */
+/* Device index a ctx is bound to; the ctx allocates its workspace lazily.  A ctx
+ * carries per-call device state (status word, look-back tags, batch tickets): use
+ * it from one host thread and one stream at a time; separate ctxs run concurrently. */
 int bcgpu_ctx_create(int device, bcgpu_ctx **out);
 int bcgpu_ctx_destroy(bcgpu_ctx *ctx);
 /* Synchronise `stream` and return the status of the last *_device call made
